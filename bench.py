@@ -1,0 +1,340 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the B200 MR/FV Euler hot path (and the reference arm).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg1]
+    python bench.py --impl reference ...      # the reference's own CPU path
+
+Default workload (BASELINE.json configs[3], "cfg4"): 3D Euler, 512^3 uniform
+mesh, fp64, unit cube, outflow, seeded ellipsoid blast, AUSM+/minmod/RK2,
+CFL 0.4 (sum-over-axes rule). A "step" is one RK2 step (two
+stages) over the whole mesh. Metric: cell-updates/s = cells x 2 stages x K /
+time (BASELINE.json metric). Multi-GPU (torchrun): z-slabs, NCCL halo
+exchange, strong scaling (the mesh is fixed).
+
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec (fp64, leaf cells x RK stages)"
+UNIT = "cell-updates/s"
+
+WORKLOADS = {
+    # name: (BASELINE config index, case kind, dim, level, cfl, seed, steps in the config)
+    "cfg4": (3, 2, 3, 9, 0.4, 1, 100),
+    "cfg1": (0, 0, 2, 8, 0.5, 1, 200),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        finally:
+            os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------- CPU legs -----
+def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, threads: int,
+                       level_override: int | None = None):
+    """Times the CPU implementation (`kind` "reference" = oracle/_ref, the
+    reference library compiled from its own sources; "port" = the C
+    restatement) on a bounded sample of the workload: the same generator and
+    scheme at a smaller level (per-cell work of a uniform mesh is
+    size-independent), `threads` independent copies run concurrently (the
+    reference is single-threaded). Returns (rate, sample description)."""
+    from oracle import oracle as O
+    _, case, dim, level, cfl, seed, _ = WORKLOADS[workload]
+    lvl = level_override if level_override is not None else (7 if dim == 3 else level)
+    init = O.case_fill(case, seed, lvl)
+    cells = init.shape[0]
+    lib_kind = "ref" if kind == "reference" else "port"
+    results = [None] * threads
+
+    def one(i):
+        if warmup:
+            O.uniform_run(lib_kind, O.make_params(dim, lvl, warmup, cfl=cfl), init)
+        _, _, res = O.uniform_run(lib_kind, O.make_params(dim, lvl, steps, cfl=cfl), init)
+        results[i] = res
+
+    ts = [threading.Thread(target=one, args=(i,)) for i in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    wall = max(r["wall_seconds"] for r in results)
+    rate = threads * cells * 2 * steps / wall
+    sample = (f"{threads} independent single-threaded copies of the {workload} generator at "
+              f"level {lvl} ({cells} cells), {steps} RK2 steps each after {warmup} warm-up "
+              f"steps; steady_clock around the step loop (unigrid.cpp:31-48)")
+    return rate, sample, wall
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU implementation (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    kind = "reference" if O.available("ref") else "port"
+    if kind == "port" and not O.available("port"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle libraries not built"}))
+        return
+    threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+    rate, sample, wall = reference_cpu_rate(kind, args.workload, max(1, args.steps),
+                                            max(0, args.warmup), threads,
+                                            level_override=args.ref_level)
+    idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.workload, 1),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(workload, n_gpus):
+    idx, case, dim, level, cfl, seed, steps = WORKLOADS[workload]
+    n = 1 << level
+    return {"workload": f"{workload}: BASELINE.json configs[{idx}]",
+            "mesh": "x".join([str(n)] * dim), "dim": dim, "scheme": "AUSM+/minmod/RK2",
+            "cfl": cfl, "cfl_rule": "dt = cfl*dx / max_cells sum_a(|v_a|+c)", "seed": seed,
+            "bc": "outflow", "decomposition": f"{n_gpus} slab(s) along the last axis",
+            "l2": "inputs larger than L2 (no flush)" if (n ** dim) * 40 > 126e6
+                  else "working set fits in L2 (latency-bound config)",
+            "parity_mode": "bit-exact (--fmad=false)"}
+
+
+# ----------------------------------------------------------------- GPU arm --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-threads", type=int, default=8)
+    ap.add_argument("--ref-level", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import ctypes as C
+    from paper_1603_05211_b200 import _abi
+    from paper_1603_05211_b200 import uniform as U
+
+    lib = _abi.load()
+    idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
+    comm = None
+    if world > 1:
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            assert lib.af_comm_unique_id(C.cast(uid, C.c_char_p)) == 0
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        st = lib.af_comm_create(C.cast(uid, C.c_char_p), world, rank, local, C.byref(h))
+        assert st == 0, "af_comm_create failed"
+        comm = h
+
+    solver = U.UniformSolver(dim, level, scheme=U.SchemeConfig(limiter=U.MINMOD),
+                             device=local, comm=comm)
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream)
+    n = 1 << level
+    init_host = U.case_fill(case, seed, level, z0=solver.z0, nz=solver.nz)
+    init_pinned = torch.from_numpy(init_host).pin_memory()
+    init_dev = init_pinned.to(f"cuda:{local}")
+    out_pinned = torch.empty_like(init_pinned).pin_memory()
+    cells_local = solver.cells
+    cells_total = n ** dim
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident throughput ("value") -------------------------------
+    solver.upload(init_dev)
+    solver.run(args.warmup, cfl=cfl, collect=False)   # W untimed warm-up steps
+    solver.sync()
+    l0 = solver.kernel_launches()
+    sampler = ClockSampler(local)
+    barrier()
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    solver.run(args.steps, cfl=cfl, collect=False)
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    launches = solver.kernel_launches() - l0
+    solver.sync()
+    ms = max_over_ranks(ms)
+    value = cells_total * 2 * args.steps / (ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        solver.upload(init_pinned.numpy())   # pinned host -> device
+        solver.run(args.steps, cfl=cfl, collect=False)
+        solver.download(out_pinned.numpy())  # device -> pinned host (synchronises)
+        t1.record(stream)
+        barrier()
+        ems = max_over_ranks(t0.elapsed_time(t1))
+        e2e = {"value": cells_total * 2 * args.steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(cells_local * 40 * world / args.steps),
+               "d2h_bytes_per_step": int(cells_local * 40 * world / args.steps),
+               "what": "one run_uniform-equivalent call: upload of the initial state from "
+                       "pinned host memory, K steps, download of the final state"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (the fused RK2 stage) ---------------
+    hbm, src = peaks()
+    S = (dim + 2) * 8
+    alg_bytes_per_launch = 2.5 * S * cells_local       # 2.5 S per cell-stage
+    avg_launch_s = (ms / 1e3) / (2 * args.steps)        # timed region = 2 stage launches/step
+    achieved = alg_bytes_per_launch / avg_launch_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
+            "kernel": "fv3d_stage" if dim == 3 else "fv2d_stage",
+            "note": "fp64-ALU bound in parity mode (no FMA contraction); see DESIGN.md"}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import oracle as O
+            kind = "reference" if O.available("ref") else "port"
+            threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+            rate, sample, _ = reference_cpu_rate(kind, args.workload, 2, 1, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+                   "sample": sample}
+        except Exception as e:  # the CPU leg must not sink the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args.workload, world),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

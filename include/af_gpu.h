@@ -1,0 +1,164 @@
+/*
+ * af_gpu.h — C ABI of libafgpu, the B200-native (sm_100a) implementation of
+ * the adaptflow MR/FV compressible-Euler hot path.
+ *
+ * This is the drop-in boundary: the reference's C++ entry points stay, and
+ * their bodies call these functions (INTEGRATION.md shows the shim). Every
+ * function returns af_status; no exception crosses the boundary. On error,
+ * af_last_error() returns a record from which the host shim rethrows the
+ * reference's exception type with the reference's message.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/core):
+ *   af_uniform_*          BlockData + fill_ghosts + step_block / rk2_stage
+ *                         (grid.hpp:15-68,128; step.hpp:62-64,77-79) as driven
+ *                         by run_uniform (unigrid.hpp:24-26, unigrid.cpp:33-47)
+ *   af_step_diag          StepDiag (step.hpp:52-55)
+ *   af_error              NonPhysicalState / RegisterMismatch (errors.hpp:18-21,69-72)
+ *   af_case_fill          init_case (cases.cpp:125-135) for the seeded BASELINE
+ *                         configs (the reference has no seeded cases)
+ *
+ * Data layout at the boundary: AoS, 5 doubles per cell (rho, mom0, mom1,
+ * mom2, rhoE) = adaptflow::ConservedState (euler.hpp:24-28), interior cells
+ * only, x fastest. In 2D mom2 is written as +0 (the reference keeps it
+ * identically zero).
+ *
+ * Streams: calls are ordered on the context's stream (af_*_set_stream, default
+ * a private non-blocking stream). Functions that return host-visible results
+ * synchronise that stream; the rest are asynchronous and graph-capturable.
+ */
+#ifndef AF_GPU_H
+#define AF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AF_ABI_VERSION 1
+
+typedef enum af_status {
+  AF_OK = 0,
+  AF_E_NONPHYSICAL = 1,       /* adaptflow::NonPhysicalState */
+  AF_E_REGISTER_MISMATCH = 2, /* adaptflow::RegisterMismatch */
+  AF_E_CONFIG = 3,            /* adaptflow::ConfigError */
+  AF_E_LEVEL_MISMATCH = 4,    /* adaptflow::LevelMismatch */
+  AF_E_CUDA = 5,              /* CUDA runtime failure (no reference equivalent) */
+  AF_E_NCCL = 6,              /* NCCL failure */
+  AF_E_ARGUMENT = 7,          /* invalid argument / null pointer */
+  AF_E_UNSUPPORTED = 8        /* option outside the hot path (e.g. AUSMDV) */
+} af_status;
+
+enum { AF_BC_OUTFLOW = 0, AF_BC_PERIODIC = 1, AF_BC_REFLECTIVE = 2 }; /* BcKind grid.hpp:70 */
+enum { AF_FLUX_AUSM_PLUS = 0, AF_FLUX_AUSMDV = 1 };                    /* FluxKind scheme.hpp:16 */
+enum { AF_LIMITER_VAN_ALBADA = 0, AF_LIMITER_MINMOD = 1 };            /* LimiterKind scheme.hpp:17 */
+enum { AF_INTEGRATOR_RK2 = 0, AF_INTEGRATOR_MUSCL_HANCOCK = 1 };      /* IntegratorKind scheme.hpp:18 */
+
+/* Geometry, gas and scheme of one solver instance (UniformGrid grid.hpp:90-123,
+ * GasModel euler.hpp:17-19, SchemeConfig scheme.hpp:23-40, BoundaryCondition
+ * grid.hpp:74-86). */
+typedef struct af_config {
+  int dim;         /* 2 or 3 */
+  int level;       /* cells per axis n = 2^level */
+  double origin;   /* domain [origin, origin+extent]^dim */
+  double extent;
+  double gamma;    /* 1.4 */
+  int bc[6];       /* face 2*axis+side, AF_BC_* */
+  int flux;        /* AF_FLUX_AUSM_PLUS */
+  int limiter;     /* AF_LIMITER_* */
+  int integrator;  /* AF_INTEGRATOR_RK2 */
+  int device;      /* CUDA device ordinal */
+} af_config;
+
+/* StepDiag (step.hpp:52-55) */
+typedef struct af_step_diag {
+  double max_wave_speed; /* max over cells, axes and both stages of |v_a| + c */
+  long fallbacks;        /* first-order reconstruction fallbacks */
+} af_step_diag;
+
+/* Aggregate of a multi-step run (RunReport fields, metrics.hpp:66-79). */
+typedef struct af_run_diag {
+  double max_wave_speed; /* max over steps of StepDiag::max_wave_speed */
+  double max_cfl;        /* max over steps of max_wave_speed * dt / dx (unigrid.cpp:43) */
+  long fallbacks;
+  long steps_done;
+  double t;              /* simulated time advanced */
+} af_run_diag;
+
+/* First-offender record of a failed call. */
+typedef struct af_error {
+  int status;            /* af_status */
+  long step;             /* step index, -1 if none */
+  int stage;             /* RK stage 1/2, 0 if none */
+  int i, j, k;           /* cell index (reference convention, may be a ghost) */
+  int level;             /* MR level, -1 for uniform */
+  int is_ghost;
+  double rho, p;
+  char message[512];     /* the reference's exception text, e.g.
+                            "step 7: cell (15,16): rho=0.164652 p=-4.999935" */
+} af_error;
+
+const char* af_version(void);
+int af_abi_version(void);
+
+/* Seeded synthetic initial data (include/af_cases.h): writes n^(dim-1)*nz
+ * cells (slab [z0, z0+nz) of the slab axis) as AoS to host memory `out`. */
+af_status af_case_fill(int kind, uint64_t seed, int level, double gamma, int z0, int nz,
+                       double* out);
+
+/* ------------------------------------------------------------------ comm -- */
+/* Multi-GPU: one process per GPU, NCCL over NVLink/NVSwitch. Rank 0 calls
+ * af_comm_unique_id, the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed), every rank calls af_comm_create. */
+typedef struct af_comm af_comm;
+af_status af_comm_unique_id(unsigned char id[128]);
+af_status af_comm_create(const unsigned char id[128], int n_ranks, int rank, int device,
+                         af_comm** out);
+af_status af_comm_destroy(af_comm* comm);
+
+/* --------------------------------------------------------------- uniform -- */
+typedef struct af_uniform af_uniform;
+
+/* Creates a uniform-mesh solver. comm == NULL: single GPU, whole domain.
+ * Otherwise the slab axis (z in 3D, y in 2D) is split into contiguous slabs,
+ * rank r owning [z0, z0+nz) (af_uniform_local_extent); results are bitwise
+ * independent of the number of ranks. */
+af_status af_uniform_create(const af_config* cfg, af_comm* comm, af_uniform** out);
+af_status af_uniform_destroy(af_uniform* u);
+af_status af_uniform_set_stream(af_uniform* u, void* cuda_stream);
+af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz);
+
+/* AoS state transfer of the rank's slab (host or device pointer). */
+af_status af_uniform_upload(af_uniform* u, const double* aos);
+af_status af_uniform_download(af_uniform* u, double* aos);
+
+/* step_block (step.hpp:77-79) for RK2: one step of size dt. diag may be
+ * NULL (then the call is asynchronous). */
+af_status af_uniform_step(af_uniform* u, double dt, af_step_diag* diag);
+
+/* n_steps steps entirely on the device. cfl > 0: dt_s = cfl*dx / max over
+ * cells of sum_a(|v_a|+c) of the state at the start of step s (computed on
+ * the device, no host round trip); else dt = fixed_dt (unigrid.cpp:20).
+ * dt_hist (host, n_steps doubles) and diag may be NULL. Both non-NULL
+ * outputs synchronise. With both NULL the call is asynchronous (errors are
+ * then reported by the next synchronising call). */
+af_status af_uniform_run(af_uniform* u, long n_steps, double cfl, double fixed_dt,
+                         double* dt_hist, af_run_diag* diag);
+
+/* Max over cells of sum_a(|v_a|+c) of the current state (synchronises). */
+af_status af_uniform_speed_sum(af_uniform* u, double* smax);
+
+/* Synchronises and reports any pending asynchronous error. */
+af_status af_uniform_sync(af_uniform* u);
+
+af_status af_uniform_last_error(const af_uniform* u, af_error* err);
+
+/* Number of libafgpu kernels launched by this solver since creation. */
+af_status af_uniform_kernel_launches(const af_uniform* u, long* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AF_GPU_H */

@@ -1,0 +1,157 @@
+"""oracle.py — TEST INFRASTRUCTURE ONLY: ctypes access to the two CPU oracles.
+
+  * ``ref``  — oracle/_ref/libafref.so: the reference library compiled from
+    /root/reference sources (oracle/Makefile) + ref_harness.cpp.
+  * ``port`` — oracle/_build/libaforacle.so: the plain-C restatement.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libafref.so")
+PORT_SO = os.path.join(HERE, "_build", "libaforacle.so")
+REFERENCE_SRC = "/root/reference/proj/core"
+
+CASE_QUADRANTS, CASE_QUADRANTS_NOISE, CASE_ELLIPSOID, CASE_ELLIPSOID_PRATIO = 0, 1, 2, 3
+OUTFLOW, PERIODIC, REFLECTIVE = 0, 1, 2
+VAN_ALBADA, MINMOD = 0, 1
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("level", C.c_int), ("bc", C.c_int * 6), ("limiter", C.c_int),
+        ("flux", C.c_int), ("gamma", C.c_double), ("n_steps", C.c_long), ("cfl", C.c_double),
+        ("fixed_dt", C.c_double), ("eps", C.c_double), ("eps_level", C.POINTER(C.c_double)),
+        ("min_leaf_level", C.c_int), ("local_time", C.c_int), ("lt_gap", C.c_int),
+    ]
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("max_wave_speed", C.c_double), ("max_cfl", C.c_double), ("fallbacks", C.c_long),
+        ("wall_seconds", C.c_double), ("n_cycles", C.c_long), ("steps_done", C.c_long),
+        ("err_kind", C.c_int), ("err", C.c_char * 512),
+    ]
+
+    def as_dict(self):
+        return {k: (getattr(self, k).decode() if k == "err" else getattr(self, k))
+                for k, _ in self._fields_}
+
+
+def build(force: bool = False, ref: bool = True) -> None:
+    """Builds the restatement (always) and the reference (when its sources exist)."""
+    targets = ["oracle"]
+    if ref and os.path.isdir(REFERENCE_SRC):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE] + (["-B"] if force else []) + targets,
+                   check=True)
+
+
+_libs: dict = {}
+
+
+def _load(kind: str):
+    if kind in _libs:
+        return _libs[kind]
+    path = REF_SO if kind == "ref" else PORT_SO
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"oracle library {path} missing (run `make -C oracle`)")
+    lib = C.CDLL(path)
+    pre = "afref_" if kind == "ref" else "afo_"
+    dp = C.POINTER(C.c_double)
+    for name, args in [
+        ("uniform_run", [C.POINTER(Params), dp, dp, dp, C.POINTER(Result)]),
+        ("mr_run", [C.POINTER(Params), dp, dp, C.POINTER(C.c_uint64), C.POINTER(C.c_long),
+                    C.POINTER(C.c_long), C.c_long, dp, C.POINTER(Result)]),
+        ("mr_last_dump", [C.c_char_p]),
+    ]:
+        f = getattr(lib, pre + name)
+        f.argtypes = args
+        f.restype = C.c_int
+    if kind == "port":
+        lib.afo_case_fill.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int,
+                                      C.c_int, dp]
+        lib.afo_case_fill.restype = C.c_int
+    _libs[kind] = lib
+    return lib
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(REF_SO if kind == "ref" else PORT_SO)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def case_fill(kind: int, seed: int, level: int, gamma: float = 1.4, z0: int = 0,
+              nz: int | None = None) -> np.ndarray:
+    """Seeded initial data (include/af_cases.h), shape (cells, 5) AoS."""
+    lib = _load("port")
+    dim = 3 if kind in (CASE_ELLIPSOID, CASE_ELLIPSOID_PRATIO) else 2
+    n = 1 << level
+    nz = n if nz is None else nz
+    out = np.zeros((nz * n ** (dim - 1), 5), dtype=np.float64)
+    rc = lib.afo_case_fill(kind, seed, level, gamma, z0, nz, _dp(out))
+    if rc:
+        raise ValueError("af_case_fill rejected its arguments")
+    return out
+
+
+def make_params(dim, level, n_steps, cfl=0.5, fixed_dt=0.0, limiter=MINMOD, bc=None,
+                gamma=1.4, eps=0.0, eps_level=None, min_leaf_level=0, local_time=False,
+                lt_gap=3):
+    p = Params()
+    p.dim, p.level, p.n_steps = dim, level, n_steps
+    for f in range(6):
+        p.bc[f] = OUTFLOW if bc is None else bc[f]
+    p.limiter, p.flux, p.gamma = limiter, 0, gamma
+    p.cfl, p.fixed_dt = cfl, fixed_dt
+    p.eps = eps
+    keep = None
+    if eps_level is not None:
+        keep = np.ascontiguousarray(eps_level, dtype=np.float64)
+        p.eps_level = _dp(keep)
+    p.min_leaf_level, p.local_time, p.lt_gap = min_leaf_level, int(local_time), lt_gap
+    p._keep = keep  # keep the table alive with the struct
+    return p
+
+
+def uniform_run(kind: str, params: Params, init: np.ndarray):
+    lib = _load(kind)
+    out = np.zeros_like(init)
+    dts = np.zeros(max(params.n_steps, 1), dtype=np.float64)
+    res = Result()
+    fn = lib.afref_uniform_run if kind == "ref" else lib.afo_uniform_run
+    fn(C.byref(params), _dp(np.ascontiguousarray(init)), _dp(out), _dp(dts), C.byref(res))
+    return out, dts[: params.n_steps], res.as_dict()
+
+
+def mr_run(kind: str, params: Params, init: np.ndarray, max_cycles: int | None = None,
+           dump_path: str | None = None):
+    lib = _load(kind)
+    out = np.zeros_like(init)
+    max_cycles = params.n_steps if max_cycles is None else max_cycles
+    per_cycle = np.zeros((max_cycles, 4), dtype=np.int64)
+    dts = np.zeros(max_cycles, dtype=np.float64)
+    cap = init.shape[0] + 1
+    keys = np.zeros(cap, dtype=np.uint64)
+    nl = C.c_long(cap)
+    res = Result()
+    fn = lib.afref_mr_run if kind == "ref" else lib.afo_mr_run
+    fn(C.byref(params), _dp(np.ascontiguousarray(init)), _dp(out),
+       keys.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(nl),
+       per_cycle.ctypes.data_as(C.POINTER(C.c_long)), max_cycles, _dp(dts), C.byref(res))
+    r = res.as_dict()
+    nc = min(r["n_cycles"], max_cycles)
+    if dump_path is not None:
+        (lib.afref_mr_last_dump if kind == "ref" else lib.afo_mr_last_dump)(
+            dump_path.encode())
+    return out, keys[: nl.value].copy(), per_cycle[:nc].copy(), dts[:nc].copy(), r

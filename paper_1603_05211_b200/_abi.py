@@ -1,0 +1,93 @@
+"""ctypes binding of include/af_gpu.h (libafgpu.so).
+
+There is no fallback: if the library is missing or fails to load, importing
+the solver API raises. The product path is the CUDA library and nothing else.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+AF_OK = 0
+AF_E_NONPHYSICAL = 1
+AF_E_REGISTER_MISMATCH = 2
+AF_E_CONFIG = 3
+AF_E_LEVEL_MISMATCH = 4
+AF_E_CUDA = 5
+AF_E_NCCL = 6
+AF_E_ARGUMENT = 7
+AF_E_UNSUPPORTED = 8
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("level", C.c_int), ("origin", C.c_double), ("extent", C.c_double),
+        ("gamma", C.c_double), ("bc", C.c_int * 6), ("flux", C.c_int), ("limiter", C.c_int),
+        ("integrator", C.c_int), ("device", C.c_int),
+    ]
+
+
+class StepDiag(C.Structure):
+    _fields_ = [("max_wave_speed", C.c_double), ("fallbacks", C.c_long)]
+
+
+class RunDiag(C.Structure):
+    _fields_ = [("max_wave_speed", C.c_double), ("max_cfl", C.c_double),
+                ("fallbacks", C.c_long), ("steps_done", C.c_long), ("t", C.c_double)]
+
+
+class ErrorRec(C.Structure):
+    _fields_ = [("status", C.c_int), ("step", C.c_long), ("stage", C.c_int), ("i", C.c_int),
+                ("j", C.c_int), ("k", C.c_int), ("level", C.c_int), ("is_ghost", C.c_int),
+                ("rho", C.c_double), ("p", C.c_double), ("message", C.c_char * 512)]
+
+
+# name -> (restype, argtypes); the complete exported surface of af_gpu.h
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+SIGNATURES = {
+    "af_version": (C.c_char_p, []),
+    "af_abi_version": (C.c_int, []),
+    "af_case_fill": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int, C.c_int, _dp]),
+    "af_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "af_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "af_comm_destroy": (C.c_int, [_vp]),
+    "af_uniform_create": (C.c_int, [C.POINTER(Config), _vp, C.POINTER(_vp)]),
+    "af_uniform_destroy": (C.c_int, [_vp]),
+    "af_uniform_set_stream": (C.c_int, [_vp, _vp]),
+    "af_uniform_local_extent": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "af_uniform_upload": (C.c_int, [_vp, _vp]),
+    "af_uniform_download": (C.c_int, [_vp, _vp]),
+    "af_uniform_step": (C.c_int, [_vp, C.c_double, C.POINTER(StepDiag)]),
+    "af_uniform_run": (C.c_int, [_vp, C.c_long, C.c_double, C.c_double, _dp,
+                                 C.POINTER(RunDiag)]),
+    "af_uniform_speed_sum": (C.c_int, [_vp, _dp]),
+    "af_uniform_sync": (C.c_int, [_vp]),
+    "af_uniform_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
+    "af_uniform_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+}
+
+_lib = None
+
+
+def load(build_if_missing: bool = True):
+    """Loads libafgpu.so (building it in-tree first if it is absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH) and build_if_missing:
+        _build.build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libafgpu.so not found at {LIB_PATH}; run "
+                          "`python -m paper_1603_05211_b200.build`")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,78 @@
+"""In-tree build of libafgpu.so (sm_100a) with nvcc.
+
+The parity build uses --fmad=false: the reference CPU build (x86-64, -O3, no
+-mfma) never contracts a*b+c into an FMA, so disabling contraction on the GPU
+is what makes the results bit-identical. Division and sqrt are IEEE
+correctly rounded in both.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIBDIR = os.path.join(PKG, "_lib")
+LIB = os.path.join(LIBDIR, "libafgpu.so")
+
+SOURCES = ["af_abi.cu", "af_uniform.cu", "af_mr.cu"]
+HEADERS = ["af_physics.cuh", "af_uniform_kernels.cuh", "af_internal.h", "af_uniform.h",
+           "af_comm.h", "af_mr.h", "af_mr_kernels.cuh"]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xcompiler", "-fno-fast-math",
+    "-shared",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+            return cand
+    return "nvcc"
+
+
+def _nccl_dirs() -> tuple[str, str]:
+    """torch's bundled NCCL (the one libtorch_cuda needs; one libnccl.so.2 per
+    process, so libafgpu must use the same build)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []) or []:
+        inc, lib = os.path.join(base, "nccl", "include"), os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps += [os.path.join(ROOT, "include", f) for f in ("af_gpu.h", "af_cases.h")]
+    return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
+    nccl_inc, nccl_lib = _nccl_dirs()
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", CSRC, "-I", os.path.join(ROOT, "include"),
+           "-I", nccl_inc, "-o", LIB + ".tmp", *srcs, "-L", nccl_lib, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath", "-Xlinker", nccl_lib]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

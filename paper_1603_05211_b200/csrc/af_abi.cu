@@ -1,0 +1,175 @@
+// af_abi.cu — the extern "C" boundary of libafgpu (include/af_gpu.h).
+// Every entry point catches af::Error / std::exception and returns an
+// af_status; the last error is kept per object (or thread-local for calls
+// without one) for af_*_last_error.
+#include <nccl.h>
+
+#include <cstring>
+#include <new>
+
+#include "af_cases.h"
+#include "af_comm.h"
+#include "af_gpu.h"
+#include "af_uniform.h"
+
+struct af_uniform {
+  af::Uniform* impl;
+};
+
+namespace {
+
+thread_local af_error g_last{};
+
+af_status record(af_error* slot, af_status st, const char* msg) {
+  af_error& e = slot ? *slot : g_last;
+  if (st != AF_E_NONPHYSICAL || e.status != AF_E_NONPHYSICAL) {
+    std::memset(&e, 0, sizeof(e));
+    e.step = -1;
+    e.level = -1;
+  }
+  e.status = st;
+  if (msg) std::snprintf(e.message, sizeof e.message, "%s", msg);
+  return st;
+}
+
+template <class F>
+af_status guard(af_error* slot, F&& f) {
+  try {
+    f();
+    return AF_OK;
+  } catch (const af::Error& e) {
+    return record(slot, e.status, e.what());
+  } catch (const std::bad_alloc&) {
+    return record(slot, AF_E_CUDA, "host allocation failed");
+  } catch (const std::exception& e) {
+    return record(slot, AF_E_ARGUMENT, e.what());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* af_version(void) { return "afgpu 0.1 (sm_100a)"; }
+int af_abi_version(void) { return AF_ABI_VERSION; }
+
+af_status af_case_fill(int kind, uint64_t seed, int level, double gamma, int z0, int nz,
+                       double* out) {
+  if (!out || kind < 0 || kind > 3) return record(nullptr, AF_E_ARGUMENT, "af_case_fill: bad argument");
+  return ::af_cases_fill(kind, seed, level, gamma, z0, nz, out) == 0
+             ? AF_OK
+             : record(nullptr, AF_E_ARGUMENT, "af_case_fill: bad argument");
+}
+
+af_status af_comm_unique_id(unsigned char id[128]) {
+  return guard(nullptr, [&] {
+    if (!id) throw af::Error(AF_E_ARGUMENT, "null id");
+    ncclUniqueId u;
+    const ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) throw af::Error(AF_E_NCCL, ncclGetErrorString(r));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+af_status af_comm_create(const unsigned char id[128], int n_ranks, int rank, int device,
+                         af_comm** out) {
+  return guard(nullptr, [&] {
+    if (!id || !out || n_ranks < 1 || rank < 0 || rank >= n_ranks)
+      throw af::Error(AF_E_ARGUMENT, "af_comm_create: bad argument");
+    AF_CUDA(cudaSetDevice(device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    auto* c = new af_comm;
+    c->c.n = n_ranks;
+    c->c.rank = rank;
+    c->c.device = device;
+    const ncclResult_t r = ncclCommInitRank(&c->c.nccl, n_ranks, u, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw af::Error(AF_E_NCCL, ncclGetErrorString(r));
+    }
+    *out = c;
+  });
+}
+
+af_status af_comm_destroy(af_comm* comm) {
+  if (!comm) return AF_OK;
+  if (comm->c.nccl) ncclCommDestroy(comm->c.nccl);
+  delete comm;
+  return AF_OK;
+}
+
+af_status af_uniform_create(const af_config* cfg, af_comm* comm, af_uniform** out) {
+  return guard(nullptr, [&] {
+    if (!cfg || !out) throw af::Error(AF_E_ARGUMENT, "af_uniform_create: null argument");
+    auto* h = new af_uniform;
+    try {
+      h->impl = new af::Uniform(*cfg, comm ? &comm->c : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+af_status af_uniform_destroy(af_uniform* u) {
+  if (!u) return AF_OK;
+  delete u->impl;
+  delete u;
+  return AF_OK;
+}
+
+#define AF_U_GUARD(body)                                                     \
+  do {                                                                       \
+    if (!u || !u->impl) return record(nullptr, AF_E_ARGUMENT, "null solver"); \
+    return guard(&u->impl->last_error(), [&] { body; });                     \
+  } while (0)
+
+af_status af_uniform_set_stream(af_uniform* u, void* s) {
+  AF_U_GUARD(u->impl->set_stream(static_cast<cudaStream_t>(s)));
+}
+
+af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz) {
+  if (!u || !u->impl || !z0 || !nz) return record(nullptr, AF_E_ARGUMENT, "null argument");
+  *z0 = u->impl->grid().zlo;
+  *nz = u->impl->grid().nzl;
+  return AF_OK;
+}
+
+af_status af_uniform_upload(af_uniform* u, const double* aos) { AF_U_GUARD(u->impl->upload(aos)); }
+
+af_status af_uniform_download(af_uniform* u, double* aos) { AF_U_GUARD(u->impl->download(aos)); }
+
+af_status af_uniform_step(af_uniform* u, double dt, af_step_diag* diag) {
+  AF_U_GUARD(u->impl->step(dt, diag));
+}
+
+af_status af_uniform_run(af_uniform* u, long n_steps, double cfl, double fixed_dt,
+                         double* dt_hist, af_run_diag* diag) {
+  AF_U_GUARD(u->impl->run(n_steps, cfl, fixed_dt, dt_hist, diag));
+}
+
+af_status af_uniform_speed_sum(af_uniform* u, double* smax) {
+  AF_U_GUARD({
+    if (!smax) throw af::Error(AF_E_ARGUMENT, "null output");
+    *smax = u->impl->speed_sum();
+  });
+}
+
+af_status af_uniform_sync(af_uniform* u) { AF_U_GUARD(u->impl->sync()); }
+
+af_status af_uniform_last_error(const af_uniform* u, af_error* err) {
+  if (!err) return AF_E_ARGUMENT;
+  *err = (u && u->impl) ? u->impl->last_error() : g_last;
+  return AF_OK;
+}
+
+af_status af_uniform_kernel_launches(const af_uniform* u, long* count) {
+  if (!u || !u->impl || !count) return AF_E_ARGUMENT;
+  *count = u->impl->launches();
+  return AF_OK;
+}
+
+}  // extern "C"

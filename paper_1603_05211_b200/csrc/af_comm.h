@@ -1,0 +1,19 @@
+// af_comm.h — NCCL communicator of libafgpu (one process per GPU).
+#pragma once
+
+#include <nccl.h>
+
+namespace af {
+
+struct Comm {
+  ncclComm_t nccl = nullptr;
+  int n = 1;
+  int rank = 0;
+  int device = 0;
+};
+
+}  // namespace af
+
+struct af_comm {
+  af::Comm c;
+};

@@ -1,0 +1,486 @@
+// af_uniform.cu — host side of the uniform FV solver (af_uniform_* of af_gpu.h).
+//
+// Mirrors run_uniform's step loop (unigrid.cpp:33-47) and step_block's RK2
+// (step.cpp:237-251): per step, stage(u,u,mid,dt/2) then stage(u,mid,u,dt).
+// The ghost fill (grid.cpp:9-62) is folded into the kernels' index mapping;
+// only inter-rank halo planes are exchanged (NCCL send/recv over NVLink).
+// Δt (CFL rule) is reduced on the device by the previous step's stage-2
+// epilogue, so a multi-step run issues no host synchronisation and can be
+// captured in a CUDA graph.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "af_comm.h"
+#include "af_uniform.h"
+#include "af_uniform_kernels.cuh"
+
+namespace af {
+
+namespace {
+
+constexpr int kTY = 8;
+
+__global__ void aos_to_soa(const double* __restrict__ aos, double* __restrict__ soa, UGrid g) {
+  const long cells = g.plane * g.nzl;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    const long off = (c / g.plane + 2) * g.zs + c % g.plane;
+    const double* q = aos + 5 * c;
+    if (g.ncomp == 5) {
+#pragma unroll
+      for (int m = 0; m < 5; ++m) soa[m * g.cs + off] = q[m];
+    } else {  // 2D: drop mom2 (identically zero in the reference)
+      soa[off] = q[0];
+      soa[g.cs + off] = q[1];
+      soa[2 * g.cs + off] = q[2];
+      soa[3 * g.cs + off] = q[4];
+    }
+  }
+}
+
+__global__ void soa_to_aos(const double* __restrict__ soa, double* __restrict__ aos, UGrid g) {
+  const long cells = g.plane * g.nzl;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    const long off = (c / g.plane + 2) * g.zs + c % g.plane;
+    double* q = aos + 5 * c;
+    if (g.ncomp == 5) {
+#pragma unroll
+      for (int m = 0; m < 5; ++m) q[m] = soa[m * g.cs + off];
+    } else {
+      q[0] = soa[off];
+      q[1] = soa[g.cs + off];
+      q[2] = soa[2 * g.cs + off];
+      q[3] = 0.0;
+      q[4] = soa[3 * g.cs + off];
+    }
+  }
+}
+
+std::string fmt_f(double v) {  // std::to_string(double) == "%f"
+  char b[64];
+  std::snprintf(b, sizeof b, "%f", v);
+  return b;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
+  if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
+  if (c.level < 3 || c.level > 15)
+    throw Error(AF_E_CONFIG, "level must be in [3, 15] (>= 8 cells per axis)");
+  if (c.flux != AF_FLUX_AUSM_PLUS)
+    throw Error(AF_E_UNSUPPORTED, "only the AUSM+ flux is on the device hot path");
+  if (c.integrator != AF_INTEGRATOR_RK2)
+    throw Error(AF_E_UNSUPPORTED, "only the RK2 integrator is on the device hot path");
+  if (c.limiter != AF_LIMITER_MINMOD && c.limiter != AF_LIMITER_VAN_ALBADA)
+    throw Error(AF_E_CONFIG, "unknown limiter");
+  for (int f = 0; f < 6; ++f)
+    if (c.bc[f] < 0 || c.bc[f] > 2) throw Error(AF_E_CONFIG, "unknown boundary condition");
+  if (!(c.gamma > 1.0)) throw Error(AF_E_CONFIG, "gamma must exceed 1");
+  AF_CUDA(cudaSetDevice(c.device));
+  const int n = 1 << c.level;
+  g_.dim = c.dim;
+  g_.n = n;
+  g_.nranks = comm ? comm->n : 1;
+  const int rank = comm ? comm->rank : 0;
+  // Contiguous slabs; 2D slabs stay multiples of the tile height.
+  const int quantum = c.dim == 2 ? kTY : 2;
+  const int units = n / quantum;
+  if (units < g_.nranks) throw Error(AF_E_CONFIG, "too many ranks for this mesh");
+  const int lo_u = (int)((long)units * rank / g_.nranks);
+  const int hi_u = (int)((long)units * (rank + 1) / g_.nranks);
+  g_.zlo = lo_u * quantum;
+  g_.nzl = (hi_u - lo_u) * quantum;
+  for (int f = 0; f < 6; ++f) g_.bc[f] = c.bc[f];
+  g_.ncomp = c.dim == 3 ? 5 : 4;
+  g_.plane = c.dim == 3 ? (long)n * n : (long)n;
+  g_.cs = g_.plane;
+  g_.zs = g_.ncomp * g_.plane;
+  g_.total = g_.zs * (g_.nzl + 4);
+  dx_ = c.extent / static_cast<double>(n);  // grid.hpp:98
+  inv_dx_ = 1.0 / dx_;                      // step.cpp:62
+  AF_CUDA(cudaMalloc(&d_u_, sizeof(double) * g_.total));
+  AF_CUDA(cudaMalloc(&d_mid_, sizeof(double) * g_.total));
+  AF_CUDA(cudaMemset(d_u_, 0, sizeof(double) * g_.total));
+  AF_CUDA(cudaMemset(d_mid_, 0, sizeof(double) * g_.total));
+  AF_CUDA(cudaMalloc(&d_err_, 2 * sizeof(int)));
+  AF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  stream_ = own_stream_;
+  reset_error_();
+  std::memset(&last_, 0, sizeof(last_));
+  last_.step = -1;
+  const size_t sm3 = Fv3d<1, 32, kTY>::smem_bytes;
+  for (auto fn : {(const void*)fv3d_stage<0, 32, kTY>, (const void*)fv3d_stage<1, 32, kTY>,
+                  (const void*)fv3d_stage<0, 16, kTY>, (const void*)fv3d_stage<1, 16, kTY>,
+                  (const void*)fv3d_stage<0, 8, kTY>, (const void*)fv3d_stage<1, 8, kTY>})
+    AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+}
+
+Uniform::~Uniform() {
+  cudaSetDevice(cfg_.device);
+  if (own_stream_) cudaStreamSynchronize(own_stream_);
+  cudaFree(d_u_);
+  cudaFree(d_mid_);
+  cudaFree(d_err_);
+  cudaFree(d_stage_);
+  free_records_();
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+}
+
+void Uniform::set_stream(cudaStream_t s) { stream_ = s ? s : own_stream_; }
+
+void Uniform::reset_error_() {
+  // flag = 0, first failing stage = 0x7f7f7f7f (larger than any step*2+1)
+  AF_CUDA(cudaMemsetAsync(d_err_, 0, sizeof(int), stream_));
+  AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
+}
+
+void Uniform::free_records_() {
+  cudaFree(rec_.smax);
+  cudaFree(rec_.wave_u);
+  cudaFree(rec_.wave_mid);
+  cudaFree(rec_.fb);
+  cudaFree(rec_.dt);
+  rec_ = RunRecords{};
+  rec_cap_ = 0;
+}
+
+void Uniform::ensure_records_(long n) {
+  if (n <= rec_cap_) return;
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  free_records_();
+  const long cap = std::max<long>(n, 64);
+  AF_CUDA(cudaMalloc(&rec_.smax, sizeof(unsigned long long) * (cap + 1)));
+  AF_CUDA(cudaMalloc(&rec_.wave_u, sizeof(unsigned long long) * cap));
+  AF_CUDA(cudaMalloc(&rec_.wave_mid, sizeof(unsigned long long) * cap));
+  AF_CUDA(cudaMalloc(&rec_.fb, sizeof(unsigned long long) * cap));
+  AF_CUDA(cudaMalloc(&rec_.dt, sizeof(double) * cap));
+  rec_cap_ = cap;
+}
+
+void Uniform::ensure_staging_() {
+  const size_t need = sizeof(double) * 5 * g_.plane * g_.nzl;
+  if (stage_bytes_ >= need) return;
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(d_stage_);
+  d_stage_ = nullptr;
+  AF_CUDA(cudaMalloc(&d_stage_, need));
+  stage_bytes_ = need;
+}
+
+void Uniform::upload(const double* aos) {
+  if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
+  const size_t bytes = sizeof(double) * 5 * g_.plane * g_.nzl;
+  const double* src = aos;
+  if (!is_device_ptr(aos)) {
+    ensure_staging_();
+    AF_CUDA(cudaMemcpyAsync(d_stage_, aos, bytes, cudaMemcpyHostToDevice, stream_));
+    src = d_stage_;
+  }
+  aos_to_soa<<<4 * 148, 256, 0, stream_>>>(src, d_u_, g_);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+  reset_error_();
+}
+
+void Uniform::download(double* aos) {
+  if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
+  const size_t bytes = sizeof(double) * 5 * g_.plane * g_.nzl;
+  if (is_device_ptr(aos)) {
+    soa_to_aos<<<4 * 148, 256, 0, stream_>>>(d_u_, aos, g_);
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    return;
+  }
+  ensure_staging_();
+  soa_to_aos<<<4 * 148, 256, 0, stream_>>>(d_u_, d_stage_, g_);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+  AF_CUDA(cudaMemcpyAsync(aos, d_stage_, bytes, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// Halo planes of `q` along the slab axis: 2 planes to each neighbour, one
+// NCCL message per direction (per-plane SoA keeps them contiguous).
+void Uniform::exchange_halos_(double* q) {
+  if (!comm_ || comm_->n == 1) return;
+  const int r = comm_->rank, P = comm_->n;
+  const bool periodic = g_.bc[2 * (g_.dim - 1)] == AF_BC_PERIODIC &&
+                        g_.bc[2 * (g_.dim - 1) + 1] == AF_BC_PERIODIC;
+  const int lo = r > 0 ? r - 1 : (periodic ? P - 1 : -1);
+  const int hi = r < P - 1 ? r + 1 : (periodic ? 0 : -1);
+  const size_t cnt = (size_t)2 * g_.zs;
+  ncclComm_t nc = comm_->nccl;
+  auto ck = [](ncclResult_t e) {
+    if (e != ncclSuccess) throw Error(AF_E_NCCL, ncclGetErrorString(e));
+  };
+  // Posting order (top->hi, low halo<-lo, bottom->lo, high halo<-hi) keeps the
+  // pairwise send/recv matching right when lo == hi (two periodic ranks).
+  ck(ncclGroupStart());
+  if (hi >= 0) ck(ncclSend(q + (long)g_.nzl * g_.zs, cnt, ncclDouble, hi, nc, stream_));
+  if (lo >= 0) ck(ncclRecv(q, cnt, ncclDouble, lo, nc, stream_));
+  if (lo >= 0) ck(ncclSend(q + 2 * g_.zs, cnt, ncclDouble, lo, nc, stream_));
+  if (hi >= 0) ck(ncclRecv(q + (long)(g_.nzl + 2) * g_.zs, cnt, ncclDouble, hi, nc, stream_));
+  ck(ncclGroupEnd());
+}
+
+void Uniform::launch_stage_(const StageArgs& a) {
+  const int n = g_.n;
+  const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
+  const int lim = cfg_.limiter;
+  if (g_.dim == 3) {
+    const long tiles = (long)(n / tx) * (n / kTY);
+    const long target = 148L * 2 * 8;
+    int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, g_.nzl / 8));
+    StageArgs b = a;
+    b.zchunk = (g_.nzl + chunks - 1) / chunks;
+    chunks = (g_.nzl + b.zchunk - 1) / b.zchunk;
+    dim3 grid((unsigned)tiles, (unsigned)chunks);
+#define AF_L3(L, TX)                                                                     \
+  fv3d_stage<L, TX, kTY><<<grid, TX * kTY, Fv3d<L, TX, kTY>::smem_bytes, stream_>>>(b, g_)
+    if (tx == 32) {
+      if (lim) AF_L3(1, 32); else AF_L3(0, 32);
+    } else if (tx == 16) {
+      if (lim) AF_L3(1, 16); else AF_L3(0, 16);
+    } else {
+      if (lim) AF_L3(1, 8); else AF_L3(0, 8);
+    }
+#undef AF_L3
+  } else {
+    const unsigned tiles = (unsigned)((n / tx) * (g_.nzl / kTY));
+#define AF_L2(L, TX) \
+  fv2d_stage<L, TX, kTY><<<tiles, TX * kTY, Fv2d<L, TX, kTY>::smem_bytes, stream_>>>(a, g_)
+    if (tx == 32) {
+      if (lim) AF_L2(1, 32); else AF_L2(0, 32);
+    } else if (tx == 16) {
+      if (lim) AF_L2(1, 16); else AF_L2(0, 16);
+    } else {
+      if (lim) AF_L2(1, 8); else AF_L2(0, 8);
+    }
+#undef AF_L2
+  }
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+}
+
+void Uniform::launch_speed_sum_(const double* q, unsigned long long* target) {
+  if (g_.dim == 3)
+    speed_sum_kernel<3><<<2 * 148, 256, 0, stream_>>>(q, g_, cfg_.gamma, target, d_err_);
+  else
+    speed_sum_kernel<2><<<2 * 148, 256, 0, stream_>>>(q, g_, cfg_.gamma, target, d_err_);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+}
+
+// Enqueues n_steps RK2 steps (no host synchronisation).
+void Uniform::enqueue_steps_(long n_steps, double cfl, double fixed_dt) {
+  ensure_records_(n_steps);
+  AF_CUDA(cudaMemsetAsync(rec_.smax, 0, sizeof(unsigned long long) * (n_steps + 1), stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.wave_u, 0, sizeof(unsigned long long) * n_steps, stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.wave_mid, 0, sizeof(unsigned long long) * n_steps, stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.fb, 0, sizeof(unsigned long long) * n_steps, stream_));
+  RunRecords r = rec_;
+  r.err = d_err_;
+  StageArgs a{};
+  a.dx = dx_;
+  a.inv_dx = inv_dx_;
+  a.gamma = cfg_.gamma;
+  a.gm1 = cfg_.gamma - 1.0;
+  a.cfl = cfl;
+  a.fixed_dt = fixed_dt;
+  a.use_cfl = cfl > 0.0 ? 1 : 0;
+  a.r = r;
+  if (a.use_cfl) {
+    launch_speed_sum_(d_u_, rec_.smax);
+    if (comm_ && comm_->n > 1) allreduce_max_(rec_.smax);
+  }
+  for (long s = 0; s < n_steps; ++s) {
+    a.step = (int)s;
+    exchange_halos_(d_u_);
+    a.stage = 1;
+    a.dt_scale = 0.5;
+    a.eval = d_u_;
+    a.base = d_u_;
+    a.out = d_mid_;
+    launch_stage_(a);
+    exchange_halos_(d_mid_);
+    a.stage = 2;
+    a.dt_scale = 1.0;
+    a.eval = d_mid_;
+    a.base = d_u_;
+    a.out = d_u_;
+    launch_stage_(a);
+    if (a.use_cfl && comm_ && comm_->n > 1) allreduce_max_(rec_.smax + s + 1);
+  }
+}
+
+void Uniform::allreduce_max_(unsigned long long* bits) {
+  // max of non-negative doubles == max of their bit patterns
+  const ncclResult_t e = ncclAllReduce(bits, bits, 1, ncclUint64, ncclMax, comm_->nccl, stream_);
+  if (e != ncclSuccess) throw Error(AF_E_NCCL, ncclGetErrorString(e));
+}
+
+// Reads the device error record; on failure rebuilds the reference's
+// message (first offender in build_primitives' scan order, step.cpp:22-38).
+void Uniform::check_error_() {
+  int h[2];
+  AF_CUDA(cudaMemcpyAsync(h, d_err_, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  if (!h[0]) return;
+  const long step = h[1] / 2;
+  const int stage = h[1] % 2 + 1;
+  const double* eval = stage == 1 ? d_u_ : d_mid_;
+  std::vector<double> hs(g_.total);
+  AF_CUDA(cudaMemcpy(hs.data(), eval, sizeof(double) * g_.total, cudaMemcpyDeviceToHost));
+  std::memset(&last_, 0, sizeof(last_));
+  last_.status = AF_E_NONPHYSICAL;
+  last_.step = step;
+  last_.stage = stage;
+  last_.level = -1;
+  const int n = g_.n, dim = g_.dim;
+  const double gm1 = cfg_.gamma - 1.0;
+  auto map = [&](int c, int axis, bool& flip) {
+    flip = false;
+    if (c >= 0 && c < n) return c;
+    const int kind = c < 0 ? g_.bc[2 * axis] : g_.bc[2 * axis + 1];
+    if (kind == AF_BC_OUTFLOW) return c < 0 ? 0 : n - 1;
+    if (kind == AF_BC_PERIODIC) return ((c % n) + n) % n;
+    while (c < 0 || c >= n) {
+      if (c < 0) c = -1 - c;
+      if (c >= n) c = 2 * n - 1 - c;
+      flip = !flip;
+    }
+    return c;
+  };
+  const int gz = dim == 3 ? 2 : 0;
+  const int nk = dim == 3 ? n : 1;
+  bool found = false;
+  // The slab owns global slab-axis range [zlo, zlo+nzl); ghosts beyond the
+  // global domain are scanned by the owning edge rank.
+  for (int k = -gz; k < nk + gz && !found; ++k)
+    for (int j = -2; j < n + 2 && !found; ++j)
+      for (int i = -2; i < n + 2 && !found; ++i) {
+        const int sl = dim == 3 ? k : j;  // slab-axis coordinate
+        bool f;
+        const int msl = map(sl, dim - 1, f);
+        if (msl < g_.zlo || msl >= g_.zlo + g_.nzl) continue;
+        const int mi = map(i, 0, f);
+        const int mj = dim == 3 ? map(j, 1, f) : msl;
+        const long off = (long)(msl - g_.zlo + 2) * g_.zs + (dim == 3 ? (long)mj * n : 0) + mi;
+        const double rho = hs[off];
+        double msq = hs[g_.cs + off] * hs[g_.cs + off] + hs[2 * g_.cs + off] * hs[2 * g_.cs + off];
+        if (dim == 3) msq = msq + hs[3 * g_.cs + off] * hs[3 * g_.cs + off];
+        const double E = hs[(g_.ncomp - 1) * g_.cs + off];
+        const double inv_rho = 1.0 / rho;
+        const double kin = 0.5 * msq * inv_rho;
+        const double p = gm1 * (E - kin);
+        if (!(rho > 1e-12) || !(rho > 1e-12 && p > 1e-12)) {
+          found = true;
+          const bool ghost = i < 0 || i >= n || j < 0 || j >= n || (dim == 3 && (k < 0 || k >= n));
+          last_.i = i;
+          last_.j = j;
+          last_.k = dim == 3 ? k : 0;
+          last_.is_ghost = ghost;
+          last_.rho = rho;
+          last_.p = p;
+          std::string cs = "(" + std::to_string(i) + "," + std::to_string(j);
+          if (dim == 3) cs += "," + std::to_string(k);
+          cs += ")";
+          const std::string msg = "step " + std::to_string(step) + ": cell " + cs +
+                                  (ghost ? " (ghost)" : "") + ": rho=" + fmt_f(rho) +
+                                  " p=" + fmt_f(p);
+          std::snprintf(last_.message, sizeof last_.message, "%s", msg.c_str());
+        }
+      }
+  if (!found)
+    std::snprintf(last_.message, sizeof last_.message,
+                  "step %ld: non-physical state on another rank", step);
+  throw Error(AF_E_NONPHYSICAL, last_.message);
+}
+
+void Uniform::collect_(long n_steps, double* dt_hist, af_run_diag* rd, af_step_diag* sd) {
+  check_error_();
+  std::vector<unsigned long long> wu(n_steps), wm(n_steps), fb(n_steps);
+  std::vector<double> dts(n_steps);
+  AF_CUDA(cudaMemcpyAsync(wu.data(), rec_.wave_u, 8 * n_steps, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaMemcpyAsync(wm.data(), rec_.wave_mid, 8 * n_steps, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaMemcpyAsync(fb.data(), rec_.fb, 8 * n_steps, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaMemcpyAsync(dts.data(), rec_.dt, 8 * n_steps, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  auto asd = [](unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+  };
+  double max_ws = 0.0, max_cfl = 0.0, t = 0.0;
+  long fbs = 0;
+  for (long s = 0; s < n_steps; ++s) {
+    const double ms = std::max(asd(wu[s]), asd(wm[s]));  // step.cpp:243
+    max_ws = std::max(max_ws, ms);
+    max_cfl = std::max(max_cfl, ms * dts[s] / dx_);  // unigrid.cpp:43
+    fbs += (long)fb[s];
+    t += dts[s];
+  }
+  if (dt_hist) std::memcpy(dt_hist, dts.data(), sizeof(double) * n_steps);
+  if (rd) {
+    rd->max_wave_speed = max_ws;
+    rd->max_cfl = max_cfl;
+    rd->fallbacks = fbs;
+    rd->steps_done = n_steps;
+    rd->t = t;
+  }
+  if (sd) {
+    sd->max_wave_speed = max_ws;
+    sd->fallbacks = fbs;
+  }
+}
+
+void Uniform::step(double dt, af_step_diag* diag) {
+  if (!(dt > 0.0)) throw Error(AF_E_ARGUMENT, "dt must be positive");
+  enqueue_steps_(1, 0.0, dt);
+  if (diag) collect_(1, nullptr, nullptr, diag);
+}
+
+void Uniform::run(long n_steps, double cfl, double fixed_dt, double* dt_hist, af_run_diag* rd) {
+  if (n_steps < 0) throw Error(AF_E_ARGUMENT, "n_steps must be >= 0");
+  if (n_steps == 0) {
+    if (rd) *rd = af_run_diag{};
+    return;
+  }
+  if (!(cfl > 0.0) && !(fixed_dt > 0.0))
+    throw Error(AF_E_ARGUMENT, "either cfl or fixed_dt must be positive");
+  enqueue_steps_(n_steps, cfl, fixed_dt);
+  if (dt_hist || rd) collect_(n_steps, dt_hist, rd, nullptr);
+}
+
+double Uniform::speed_sum() {
+  ensure_records_(1);
+  AF_CUDA(cudaMemsetAsync(rec_.smax, 0, sizeof(unsigned long long), stream_));
+  launch_speed_sum_(d_u_, rec_.smax);
+  if (comm_ && comm_->n > 1) allreduce_max_(rec_.smax);
+  unsigned long long b = 0;
+  AF_CUDA(cudaMemcpyAsync(&b, rec_.smax, 8, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+void Uniform::sync() { check_error_(); }
+
+}  // namespace af

@@ -1,0 +1,61 @@
+// af_uniform.h — host class behind af_uniform_* (see af_uniform.cu).
+#pragma once
+
+#include "af_comm.h"
+#include "af_internal.h"
+
+namespace af {
+
+struct StageArgs;
+
+class Uniform {
+ public:
+  Uniform(const af_config& cfg, Comm* comm);
+  ~Uniform();
+  Uniform(const Uniform&) = delete;
+  Uniform& operator=(const Uniform&) = delete;
+
+  void set_stream(cudaStream_t s);
+  void upload(const double* aos);
+  void download(double* aos);
+  void step(double dt, af_step_diag* diag);
+  void run(long n_steps, double cfl, double fixed_dt, double* dt_hist, af_run_diag* diag);
+  double speed_sum();
+  void sync();
+
+  const UGrid& grid() const { return g_; }
+  long launches() const { return launches_; }
+  const af_error& last_error() const { return last_; }
+  af_error& last_error() { return last_; }
+
+ private:
+  void reset_error_();
+  void free_records_();
+  void ensure_records_(long n);
+  void ensure_staging_();
+  void exchange_halos_(double* q);
+  void allreduce_max_(unsigned long long* bits);
+  void launch_stage_(const StageArgs& a);
+  void launch_speed_sum_(const double* q, unsigned long long* target);
+  void enqueue_steps_(long n_steps, double cfl, double fixed_dt);
+  void check_error_();
+  void collect_(long n_steps, double* dt_hist, af_run_diag* rd, af_step_diag* sd);
+
+  af_config cfg_;
+  Comm* comm_;
+  UGrid g_{};
+  double dx_ = 0.0, inv_dx_ = 0.0;
+  double* d_u_ = nullptr;
+  double* d_mid_ = nullptr;
+  double* d_stage_ = nullptr;
+  size_t stage_bytes_ = 0;
+  int* d_err_ = nullptr;
+  RunRecords rec_{};
+  long rec_cap_ = 0;
+  cudaStream_t stream_ = nullptr;
+  cudaStream_t own_stream_ = nullptr;
+  long launches_ = 0;
+  af_error last_{};
+};
+
+}  // namespace af

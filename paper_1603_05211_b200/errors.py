@@ -1,0 +1,40 @@
+"""Exception hierarchy of the reference (errors.hpp:10-77), raised from af_status."""
+from __future__ import annotations
+
+
+class Error(RuntimeError):
+    """adaptflow::Error"""
+
+
+class NonPhysicalState(Error):
+    """adaptflow::NonPhysicalState (errors.hpp:18-21)"""
+
+
+class RegisterMismatch(Error):
+    """adaptflow::RegisterMismatch (errors.hpp:69-72)"""
+
+
+class ConfigError(Error):
+    """adaptflow::ConfigError (errors.hpp:33-36)"""
+
+
+class LevelMismatch(Error):
+    """adaptflow::LevelMismatch (errors.hpp:23-26)"""
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure (no reference equivalent)."""
+
+
+class UnsupportedOption(ConfigError):
+    """Scheme option outside the device hot path (e.g. AUSMDV, MUSCL-Hancock)."""
+
+
+_BY_STATUS = {1: NonPhysicalState, 2: RegisterMismatch, 3: ConfigError, 4: LevelMismatch,
+              5: DeviceError, 6: DeviceError, 7: ValueError, 8: UnsupportedOption}
+
+
+def raise_status(status: int, message: str) -> None:
+    if status == 0:
+        return
+    raise _BY_STATUS.get(status, Error)(message)
