@@ -225,7 +225,9 @@ def main():
 
     solver = U.UniformSolver(dim, level, scheme=U.SchemeConfig(limiter=U.MINMOD),
                              device=local, comm=comm)
-    stream = torch.cuda.current_stream()
+    # A dedicated (non-default) stream: the solver's kernels and the timing
+    # events must be on the same stream.
+    stream = torch.cuda.Stream(device=local)
     solver.set_stream(stream)
     n = 1 << level
     init_host = U.case_fill(case, seed, level, z0=solver.z0, nz=solver.nz)

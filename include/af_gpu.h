@@ -157,6 +157,62 @@ af_status af_uniform_last_error(const af_uniform* u, af_error* err);
 /* Number of libafgpu kernels launched by this solver since creation. */
 af_status af_uniform_kernel_launches(const af_uniform* u, long* count);
 
+/* -------------------------------------------------------------------- MR -- */
+/* Adaptive multiresolution solver: MRTree (mr_tree.hpp:57-196) + MRSolver
+ * (mr_solver.hpp:15-58) + the run_mr loop (mr_solver.hpp:78-79), on per-level
+ * dense grids in HBM. Global (MR) and local (MRLT) time stepping. */
+typedef struct af_mr af_mr;
+
+/* MROptions (mr_solver.hpp:65-74) plus the level-dependent threshold and the
+ * coarsest-leaf-level knob BASELINE.json asks for. */
+typedef struct af_mr_options {
+  double eps;              /* MROptions::epsilon (refine >= eps, coarsen < eps) */
+  const double* eps_level; /* nullable; eps_level[l] = threshold for details whose
+                              children are at level l (size level+1); copied */
+  int min_leaf_level;      /* MRTree::set_min_leaf_level (mr_tree.hpp:78) */
+  int local_time;          /* MROptions::local_time */
+  int lt_gap;              /* MROptions::local_time_level_gap (default 3) */
+} af_mr_options;
+
+/* Per macro cycle record (RunReport cells/leaves_per_step, mr_solver.cpp:369-374). */
+typedef struct af_mr_cycle {
+  long leaves;   /* leaf_count() after refine */
+  long nodes;    /* node_count() incl. virtual leaves */
+  long sub;      /* finest steps in this cycle (LT), 1 for MR */
+  int top;       /* LT top level (L for MR) */
+  double dt;     /* finest-level step size dt_L */
+} af_mr_cycle;
+
+af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** out);
+af_status af_mr_destroy(af_mr* m);
+af_status af_mr_set_stream(af_mr* m, void* cuda_stream);
+/* from_uniform(level-L AoS data, 0, bc), norms, min leaf level, coarsen(eps)
+ * (mr_tree.cpp:29-71, mr_solver.cpp:406-410). */
+af_status af_mr_build(af_mr* m, const double* aos);
+/* MRTree::refine (mr_tree.cpp:361-402); top >= 0 applies the LT buffer
+ * radii of mr_solver.cpp:358-362 for that top level. */
+af_status af_mr_refine(af_mr* m, int top);
+af_status af_mr_add_virtual_leaves(af_mr* m);
+af_status af_mr_remove_virtual_leaves(af_mr* m);
+af_status af_mr_coarsen(af_mr* m);
+af_status af_mr_evolve_global(af_mr* m, double dt, af_step_diag* diag);
+af_status af_mr_advance_local(af_mr* m, int top, double t, double dt, af_step_diag* diag);
+/* The run_mr cycle loop (mr_solver.cpp:318-400) for n_steps finest steps;
+ * cfl > 0 selects dt_L = cfl*dx_L / max_leaves sum_a(|v_a|+c) per cycle.
+ * cycles (capacity max_cycles) and diag may be NULL. */
+af_status af_mr_run(af_mr* m, long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles,
+                    long max_cycles, af_run_diag* diag);
+af_status af_mr_counts(af_mr* m, long* leaves, long* nodes, long* internals);
+af_status af_mr_coarsest_leaf_level(af_mr* m, int* level);
+/* Sorted pack_key (mr_tree.hpp:26-30) of every leaf; *n: capacity in, count out. */
+af_status af_mr_leaf_keys(af_mr* m, uint64_t* keys, size_t* n);
+/* MRTree::to_uniform(level) (mr_tree.cpp:608-621) as AoS. */
+af_status af_mr_to_uniform(af_mr* m, int level, double* aos);
+/* detail() of every node at `level` (NaN where the node is not internal). */
+af_status af_mr_details(af_mr* m, int level, double* out);
+af_status af_mr_last_error(const af_mr* m, af_error* err);
+af_status af_mr_kernel_launches(const af_mr* m, long* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,16 @@ class ErrorRec(C.Structure):
                 ("rho", C.c_double), ("p", C.c_double), ("message", C.c_char * 512)]
 
 
+class MROptions(C.Structure):
+    _fields_ = [("eps", C.c_double), ("eps_level", C.POINTER(C.c_double)),
+                ("min_leaf_level", C.c_int), ("local_time", C.c_int), ("lt_gap", C.c_int)]
+
+
+class MRCycle(C.Structure):
+    _fields_ = [("leaves", C.c_long), ("nodes", C.c_long), ("sub", C.c_long), ("top", C.c_int),
+                ("dt", C.c_double)]
+
+
 # name -> (restype, argtypes); the complete exported surface of af_gpu.h
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
@@ -69,6 +79,27 @@ SIGNATURES = {
     "af_uniform_sync": (C.c_int, [_vp]),
     "af_uniform_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
     "af_uniform_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+    "af_mr_create": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), C.POINTER(_vp)]),
+    "af_mr_destroy": (C.c_int, [_vp]),
+    "af_mr_set_stream": (C.c_int, [_vp, _vp]),
+    "af_mr_build": (C.c_int, [_vp, _vp]),
+    "af_mr_refine": (C.c_int, [_vp, C.c_int]),
+    "af_mr_add_virtual_leaves": (C.c_int, [_vp]),
+    "af_mr_remove_virtual_leaves": (C.c_int, [_vp]),
+    "af_mr_coarsen": (C.c_int, [_vp]),
+    "af_mr_evolve_global": (C.c_int, [_vp, C.c_double, C.POINTER(StepDiag)]),
+    "af_mr_advance_local": (C.c_int, [_vp, C.c_int, C.c_double, C.c_double,
+                                      C.POINTER(StepDiag)]),
+    "af_mr_run": (C.c_int, [_vp, C.c_long, C.c_double, C.c_double, C.POINTER(MRCycle), C.c_long,
+                            C.POINTER(RunDiag)]),
+    "af_mr_counts": (C.c_int, [_vp, C.POINTER(C.c_long), C.POINTER(C.c_long),
+                               C.POINTER(C.c_long)]),
+    "af_mr_coarsest_leaf_level": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "af_mr_leaf_keys": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_size_t)]),
+    "af_mr_to_uniform": (C.c_int, [_vp, C.c_int, _vp]),
+    "af_mr_details": (C.c_int, [_vp, C.c_int, _vp]),
+    "af_mr_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
+    "af_mr_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
 }
 
 _lib = None

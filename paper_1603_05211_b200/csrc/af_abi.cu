@@ -10,10 +10,15 @@
 #include "af_cases.h"
 #include "af_comm.h"
 #include "af_gpu.h"
+#include "af_mr.h"
 #include "af_uniform.h"
 
 struct af_uniform {
   af::Uniform* impl;
+};
+
+struct af_mr {
+  af::MR* impl;
 };
 
 namespace {
@@ -169,6 +174,91 @@ af_status af_uniform_last_error(const af_uniform* u, af_error* err) {
 af_status af_uniform_kernel_launches(const af_uniform* u, long* count) {
   if (!u || !u->impl || !count) return AF_E_ARGUMENT;
   *count = u->impl->launches();
+  return AF_OK;
+}
+
+af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** out) {
+  return guard(nullptr, [&] {
+    if (!cfg || !opt || !out) throw af::Error(AF_E_ARGUMENT, "af_mr_create: null argument");
+    auto* h = new af_mr;
+    try {
+      h->impl = new af::MR(*cfg, *opt);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+af_status af_mr_destroy(af_mr* m) {
+  if (!m) return AF_OK;
+  delete m->impl;
+  delete m;
+  return AF_OK;
+}
+
+#define AF_M_GUARD(body)                                                     \
+  do {                                                                       \
+    if (!m || !m->impl) return record(nullptr, AF_E_ARGUMENT, "null solver"); \
+    return guard(&m->impl->last_error(), [&] { body; });                     \
+  } while (0)
+
+af_status af_mr_set_stream(af_mr* m, void* s) {
+  AF_M_GUARD(m->impl->set_stream(static_cast<cudaStream_t>(s)));
+}
+af_status af_mr_build(af_mr* m, const double* aos) { AF_M_GUARD(m->impl->build(aos)); }
+af_status af_mr_refine(af_mr* m, int top) { AF_M_GUARD(m->impl->refine(top)); }
+af_status af_mr_add_virtual_leaves(af_mr* m) { AF_M_GUARD(m->impl->add_virtual_leaves()); }
+af_status af_mr_remove_virtual_leaves(af_mr* m) {
+  AF_M_GUARD(m->impl->remove_virtual_leaves());
+}
+af_status af_mr_coarsen(af_mr* m) { AF_M_GUARD(m->impl->coarsen()); }
+af_status af_mr_evolve_global(af_mr* m, double dt, af_step_diag* diag) {
+  AF_M_GUARD(m->impl->evolve_global(dt, diag));
+}
+af_status af_mr_advance_local(af_mr* m, int top, double t, double dt, af_step_diag* diag) {
+  AF_M_GUARD(m->impl->advance_local(top, t, dt, diag));
+}
+af_status af_mr_run(af_mr* m, long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles,
+                    long max_cycles, af_run_diag* diag) {
+  AF_M_GUARD(m->impl->run(n_steps, cfl, fixed_dt, cycles, max_cycles, diag));
+}
+af_status af_mr_counts(af_mr* m, long* leaves, long* nodes, long* internals) {
+  AF_M_GUARD(m->impl->counts(leaves, nodes, internals));
+}
+af_status af_mr_coarsest_leaf_level(af_mr* m, int* level) {
+  AF_M_GUARD({
+    if (!level) throw af::Error(AF_E_ARGUMENT, "null output");
+    *level = m->impl->coarsest_leaf_level();
+  });
+}
+af_status af_mr_leaf_keys(af_mr* m, uint64_t* keys, size_t* n) {
+  AF_M_GUARD({
+    if (!n) throw af::Error(AF_E_ARGUMENT, "null count");
+    *n = (size_t)m->impl->leaf_keys(keys, (long)*n);
+  });
+}
+af_status af_mr_to_uniform(af_mr* m, int level, double* aos) {
+  AF_M_GUARD({
+    if (!aos) throw af::Error(AF_E_ARGUMENT, "null output");
+    m->impl->to_uniform(level, aos);
+  });
+}
+af_status af_mr_details(af_mr* m, int level, double* out) {
+  AF_M_GUARD({
+    if (!out) throw af::Error(AF_E_ARGUMENT, "null output");
+    m->impl->details(level, out);
+  });
+}
+af_status af_mr_last_error(const af_mr* m, af_error* err) {
+  if (!err) return AF_E_ARGUMENT;
+  *err = (m && m->impl) ? m->impl->last_error() : g_last;
+  return AF_OK;
+}
+af_status af_mr_kernel_launches(const af_mr* m, long* count) {
+  if (!m || !m->impl || !count) return AF_E_ARGUMENT;
+  *count = m->impl->launches();
   return AF_OK;
 }
 

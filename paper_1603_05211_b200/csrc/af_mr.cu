@@ -1,0 +1,723 @@
+// af_mr.cu — host side of the adaptive MR solver (af_mr_* of af_gpu.h).
+//
+// Mirrors MRTree (mr_tree.cpp), MRSolver::step_levels (mr_solver.cpp:232-316)
+// and the run_mr cycle (mr_solver.cpp:318-400) on per-level dense grids:
+//   refine  = details -> split flags [-> LT buffer dilation] -> apply ->
+//             gradedness fixpoint (decide-all / apply passes)
+//   evolve  = per stage: stage kernels for every stepping level (all reads
+//             before any write, as the reference's two-pass stage), commit,
+//             project_range (finest first), prediction refresh (top-down)
+//   coarsen = finest-first level sweeps repeated until nothing merges
+// Host synchronisation happens only where the reference makes a decision
+// that depends on data (fixpoint loops, per-cycle counts and errors).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "af_mr.h"
+#include "af_mr_stage.cuh"
+
+namespace af {
+
+namespace {
+
+constexpr int kGrid = 148 * 8;
+
+inline unsigned grid_for(long n, int block = 256) {
+  long b = (n + block - 1) / block;
+  return (unsigned)std::max<long>(1, std::min<long>(b, kGrid));
+}
+
+template <int D>
+__global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLevels g) {
+  const long cells = mr_cells(D, g.L), off = g.cell_off[g.L], comp = g.total_cells;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    const double* q = aos + 5 * c;
+    V[off + c] = q[0];
+    V[comp + off + c] = q[1];
+    V[2 * comp + off + c] = q[2];
+    if (D == 3) V[3 * comp + off + c] = q[3];
+    V[(D + 1) * comp + off + c] = q[4];
+  }
+}
+
+template <int D>
+__global__ void mr_download_level(const double* V, double* __restrict__ aos, MRLevels g, int l) {
+  const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    double* q = aos + 5 * c;
+    q[0] = V[off + c];
+    q[1] = V[comp + off + c];
+    q[2] = V[2 * comp + off + c];
+    q[3] = D == 3 ? V[3 * comp + off + c] : 0.0;
+    q[4] = V[(D + 1) * comp + off + c];
+  }
+}
+
+// Copies the leaf values of level l from src to dst (q_old snapshot / commit).
+// `guard`: skip when a pass-1 or post-step failure is pending (the failing
+// stage never commits, as the reference throws before pass 2 completes).
+__global__ void mr_copy_leaves(const double* src, double* dst, const uint8_t* st, long off,
+                               long cells, long comp, int nc, const int* guard, int promote) {
+  if (guard) {
+    __shared__ int s;
+    if (threadIdx.x == 0) s = guard[0] | guard[2];
+    __syncthreads();
+    if (s) {
+      if (promote && blockIdx.x == 0 && threadIdx.x == 0) atomicExch((int*)guard, 1);
+      return;
+    }
+  }
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_LEAF) continue;
+    for (int m = 0; m < nc; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
+  }
+}
+
+// Virtual q_old snapshot (mr_solver.cpp:251-266): VQold = V at the virtual
+// children of the stepping leaves of level l-1.
+template <int D>
+__global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* st,
+                                    const uint8_t* mark, MRLevels g, int l) {
+  const int n = 1 << l, pn = n >> 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
+  const long comp = g.total_cells;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_ABSENT) continue;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    if (!mark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
+    for (int m = 0; m < D + 2; ++m) VQ[m * comp + off + c] = V[m * comp + off + c];
+  }
+}
+
+// Leaf cells of level l (count) -> out[l].
+__global__ void mr_level_leaf_count(const uint8_t* st, long off, long cells,
+                                    unsigned long long* out) {
+  unsigned long long lv = 0;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x)
+    lv += st[off + c] == ST_LEAF;
+  for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
+  if ((threadIdx.x & 31) == 0 && lv) atomicAdd(out, lv);
+}
+
+std::string fmt_f(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%f", v);
+  return b;
+}
+
+double as_d(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+constexpr int kTX2 = 32, kTY2 = 8;
+constexpr int kMaxStageRecords = 2048;
+constexpr int kTX3 = 8, kTY3 = 8, kTZ3 = 4;
+
+}  // namespace
+
+MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
+  if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
+  if (c.level < 2 || c.level > 15) throw Error(AF_E_CONFIG, "level must be in [2, 15]");
+  if (c.flux != AF_FLUX_AUSM_PLUS || c.integrator != AF_INTEGRATOR_RK2)
+    throw Error(AF_E_UNSUPPORTED, "the MR device path implements AUSM+ with RK2");
+  if (c.limiter != AF_LIMITER_MINMOD && c.limiter != AF_LIMITER_VAN_ALBADA)
+    throw Error(AF_E_CONFIG, "unknown limiter");
+  for (int f = 0; f < 6; ++f)
+    if (c.bc[f] < 0 || c.bc[f] > 2) throw Error(AF_E_CONFIG, "unknown boundary condition");
+  D_ = c.dim;
+  L_ = c.level;
+  NC_ = D_ + 2;
+  if (o.eps_level) eps_level_.assign(o.eps_level, o.eps_level + L_ + 1);
+  opt_.eps_level = nullptr;
+  AF_CUDA(cudaSetDevice(c.device));
+  g_.dim = D_;
+  g_.L = L_;
+  g_.nc = NC_;
+  for (int f = 0; f < 6; ++f) g_.bc[f] = c.bc[f];
+  long tot = 0;
+  for (int l = 0; l <= L_; ++l) {
+    g_.cell_off[l] = tot;
+    tot += mr_cells(D_, l);
+    const double dx = c.extent / static_cast<double>(1 << l);  // mr_tree.hpp:73
+    g_.inv_dx[l] = 1.0 / dx;
+  }
+  g_.cell_off[L_ + 1] = tot;
+  g_.total_cells = tot;
+  const size_t vbytes = sizeof(double) * NC_ * tot;
+  AF_CUDA(cudaMalloc(&d_st_, tot));
+  AF_CUDA(cudaMalloc(&d_mark_, tot));
+  AF_CUDA(cudaMalloc(&d_flag_, tot));
+  AF_CUDA(cudaMalloc(&d_flag2_, tot));
+  AF_CUDA(cudaMalloc(&d_V_, vbytes));
+  AF_CUDA(cudaMalloc(&d_Vs_, vbytes));
+  AF_CUDA(cudaMalloc(&d_Qold_, vbytes));
+  if (o.local_time) AF_CUDA(cudaMalloc(&d_VQold_, vbytes));
+  AF_CUDA(cudaMalloc(&d_det_, sizeof(double) * tot));
+  AF_CUDA(cudaMalloc(&d_norms_, sizeof(double) * 5));
+  AF_CUDA(cudaMalloc(&d_err_, 4 * sizeof(int)));
+  AF_CUDA(cudaMalloc(&d_flagi_, sizeof(int)));
+  AF_CUDA(cudaMalloc(&d_red_, sizeof(unsigned long long) * (64 + 17 * kMaxStageRecords)));
+  tile_off_.assign(L_ + 2, 0);
+  tile_count_.assign(L_ + 1, 0);
+  long toff = 0;
+  for (int l = 0; l <= L_; ++l) {
+    tile_off_[l] = toff;
+    const int n = 1 << l;
+    const long t = D_ == 2 ? (long)((n + kTX2 - 1) / kTX2) * ((n + kTY2 - 1) / kTY2)
+                           : (long)((n + kTX3 - 1) / kTX3) * ((n + kTY3 - 1) / kTY3) *
+                                 ((n + kTZ3 - 1) / kTZ3);
+    toff += t;
+  }
+  tile_off_[L_ + 1] = toff;
+  AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
+  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * (L_ + 1)));
+  AF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  stream_ = own_stream_;
+  AF_CUDA(cudaMemsetAsync(d_st_, ST_ABSENT, tot, stream_));
+  AF_CUDA(cudaMemsetAsync(d_mark_, 0, tot, stream_));
+  AF_CUDA(cudaMemsetAsync(d_V_, 0, vbytes, stream_));
+  AF_CUDA(cudaMemsetAsync(d_Vs_, 0, vbytes, stream_));
+  AF_CUDA(cudaMemsetAsync(d_Qold_, 0, vbytes, stream_));
+  AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
+  AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
+  t_old_.assign(L_ + 1, 0.0);
+  t_new_.assign(L_ + 1, 0.0);
+  leaves_per_level_.assign(L_ + 1, 0);
+  std::memset(&last_, 0, sizeof(last_));
+  last_.step = -1;
+  if (D_ == 3) {
+    for (auto fn : {(const void*)mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>,
+                    (const void*)mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>})
+      AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes));
+  }
+}
+
+MR::~MR() {
+  cudaSetDevice(cfg_.device);
+  if (own_stream_) cudaStreamSynchronize(own_stream_);
+  for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
+                  (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
+                  (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
+                  (void*)d_flagi_, (void*)d_red_})
+    cudaFree(p);
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+}
+
+void MR::set_stream(cudaStream_t s) { stream_ = s ? s : own_stream_; }
+
+double MR::eps_at_(int child_level) const {
+  return eps_level_.empty() ? opt_.eps : eps_level_[child_level];
+}
+
+#define AF_MR_LAUNCH(kern, grid, ...)                                   \
+  do {                                                                  \
+    if (D_ == 3)                                                        \
+      kern<3><<<(grid), 256, 0, stream_>>>(__VA_ARGS__);                \
+    else                                                                \
+      kern<2><<<(grid), 256, 0, stream_>>>(__VA_ARGS__);                \
+    ++launches_;                                                        \
+    AF_CUDA(cudaGetLastError());                                        \
+  } while (0)
+
+void MR::predict_fill_(int lo, int hi) {
+  for (int l = 1; l <= L_; ++l)
+    AF_MR_LAUNCH(mr_predict_level, grid_for(mr_cells(D_, l)), d_V_, d_st_,
+                 virtuals_ ? d_mark_ : nullptr, g_, l, lo, hi);
+}
+
+// project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
+void MR::project_range_(int lo, int top) {
+  for (int l = std::min(top - 1, L_ - 1); l >= lo; --l)
+    AF_MR_LAUNCH(mr_project_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, g_, l);
+}
+
+void MR::level_counts_() {
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * (L_ + 1), stream_));
+  for (int l = 0; l <= L_; ++l) {
+    mr_level_leaf_count<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
+        d_st_, g_.cell_off[l], mr_cells(D_, l), d_red_ + l);
+    ++launches_;
+  }
+  std::vector<unsigned long long> h(L_ + 1);
+  AF_CUDA(cudaMemcpyAsync(h.data(), d_red_, 8 * (L_ + 1), cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  for (int l = 0; l <= L_; ++l) leaves_per_level_[l] = (long)h[l];
+}
+
+void MR::build_tiles_() {
+  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * (L_ + 1), stream_));
+  for (int l = 0; l <= L_; ++l) {
+    if (!leaves_per_level_[l]) continue;
+    const long nt = tile_off_[l + 1] - tile_off_[l];
+    const unsigned grid = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
+    if (D_ == 2)
+      mr_tile_list_kernel<2, kTX2, kTY2, 1><<<grid, 256, 0, stream_>>>(
+          d_st_, g_, l, d_tiles_ + tile_off_[l], d_tile_count_ + l);
+    else
+      mr_tile_list_kernel<3, kTX3, kTY3, kTZ3><<<grid, 256, 0, stream_>>>(
+          d_st_, g_, l, d_tiles_ + tile_off_[l], d_tile_count_ + l);
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+  }
+  AF_CUDA(cudaMemcpyAsync(tile_count_.data(), d_tile_count_, sizeof(int) * (L_ + 1),
+                          cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void MR::build(const double* aos) {
+  if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
+  const long cells = mr_cells(D_, L_);
+  double* stage = nullptr;
+  AF_CUDA(cudaMalloc(&stage, sizeof(double) * 5 * cells));
+  AF_CUDA(cudaMemcpyAsync(stage, aos, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
+  AF_MR_LAUNCH(mr_upload_finest, grid_for(cells), stage, d_V_, g_);
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(stage);
+  // from_uniform (mr_tree.cpp:29-71): leaves at L, internals above.
+  AF_CUDA(cudaMemsetAsync(d_st_, ST_INTERNAL, g_.cell_off[L_], stream_));
+  AF_CUDA(cudaMemsetAsync(d_st_ + g_.cell_off[L_], ST_LEAF, cells, stream_));
+  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
+  AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
+  virtuals_ = false;
+  project_range_(0, L_);
+  // set_norms_from (mr_tree.cpp:73-87)
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 8, stream_));
+  AF_MR_LAUNCH(mr_norm_kernel, grid_for(cells), d_V_, g_, d_red_);
+  unsigned long long nb[5] = {0, 0, 0, 0, 0};
+  AF_CUDA(cudaMemcpyAsync(nb, d_red_, 8 * NC_, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  double n[5] = {0, 0, 0, 0, 0};
+  n[0] = as_d(nb[0]);
+  for (int a = 0; a < D_; ++a) n[1 + a] = as_d(nb[1 + a]);
+  n[4] = as_d(nb[D_ + 1]);
+  const double global = std::max({n[0], n[1], n[2], n[3], n[4], 1e-300});
+  for (double& v : n)
+    if (v < 1e-12 * global) v = global;
+  std::memcpy(norms_host_, n, sizeof n);
+  AF_CUDA(cudaMemcpyAsync(d_norms_, norms_host_, sizeof n, cudaMemcpyHostToDevice, stream_));
+  min_leaf_ = opt_.min_leaf_level;
+  if (opt_.local_time) min_leaf_ = std::max(min_leaf_, std::max(0, L_ - opt_.lt_gap));
+  max_cfl_ = 0.0;
+  fallbacks_ = 0;
+  max_wave_ = 0.0;
+  coarsen();
+  level_counts_();
+}
+
+void MR::refine(int top) {
+  AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
+  AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
+  for (int l = 0; l <= L_ - 2; ++l)
+    AF_MR_LAUNCH(mr_detail_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, d_det_, g_, l,
+                 d_norms_);
+  for (int l = 1; l <= L_ - 1; ++l)
+    AF_MR_LAUNCH(mr_refine_flag_level, grid_for(mr_cells(D_, l)), d_st_, d_det_, d_flag_, g_,
+                 l, eps_at_(l));
+  uint8_t* split = d_flag_;
+  if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
+    for (int l = 1; l <= L_ - 1; ++l) {
+      const int r = l > top + 1 ? 1 << (l - top - 1) : 1;
+      AF_MR_LAUNCH(mr_dilate_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, d_flag2_, g_, l,
+                   r);
+    }
+    split = d_flag2_;
+  }
+  AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
+  for (int l = 1; l <= L_ - 1; ++l)
+    AF_MR_LAUNCH(mr_apply_split_level, grid_for(mr_cells(D_, l)), d_st_, split, g_, l, d_flagi_);
+  // enforce_gradedness (mr_tree.cpp:404-444)
+  for (;;) {
+    for (int l = 0; l <= L_ - 1; ++l)
+      AF_MR_LAUNCH(mr_grade_flag_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, g_, l);
+    AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
+    for (int l = 0; l <= L_ - 1; ++l)
+      AF_MR_LAUNCH(mr_apply_split_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, g_, l,
+                   d_flagi_);
+    int changed = 0;
+    AF_CUDA(cudaMemcpyAsync(&changed, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    if (!changed) break;
+  }
+  level_counts_();
+}
+
+void MR::add_virtual_leaves() {
+  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  for (int l = 1; l <= L_; ++l)
+    AF_MR_LAUNCH(mr_virtual_mark_level, grid_for(mr_cells(D_, l)), d_st_, d_mark_, g_, l);
+  virtuals_ = true;
+}
+
+void MR::remove_virtual_leaves() {
+  virtuals_ = false;
+  predict_fill_(1, 0);  // former virtual positions read as fresh predictions again
+}
+
+void MR::counts(long* leaves, long* nodes, long* internals) {
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 3, stream_));
+  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(
+      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
+  ++launches_;
+  unsigned long long h[3];
+  AF_CUDA(cudaMemcpyAsync(h, d_red_, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  if (leaves) *leaves = (long)h[0];
+  if (internals) *internals = (long)h[1];
+  if (nodes) *nodes = (long)(h[0] + h[1] + (h[2] << D_));
+}
+
+int MR::coarsest_leaf_level() {
+  for (int l = 0; l <= L_; ++l)
+    if (leaves_per_level_[l]) return l;
+  return L_;
+}
+
+double MR::leaf_speed_sum() {
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long), stream_));
+  for (int l = 0; l <= L_; ++l) {
+    if (!leaves_per_level_[l]) continue;
+    if (D_ == 3)
+      mr_leaf_speed_kernel<3><<<grid_for(mr_cells(3, l)), 256, 0, stream_>>>(
+          d_V_, d_st_, g_, l, cfg_.gamma, d_red_);
+    else
+      mr_leaf_speed_kernel<2><<<grid_for(mr_cells(2, l)), 256, 0, stream_>>>(
+          d_V_, d_st_, g_, l, cfg_.gamma, d_red_);
+    ++launches_;
+  }
+  unsigned long long b = 0;
+  AF_CUDA(cudaMemcpyAsync(&b, d_red_, 8, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  return as_d(b);
+}
+
+void MR::snapshot_(int lo, int hi) {
+  for (int l = lo; l <= std::min(hi, L_); ++l) {
+    if (!leaves_per_level_[l]) continue;
+    mr_copy_leaves<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
+        d_V_, d_Qold_, d_st_, g_.cell_off[l], mr_cells(D_, l), g_.total_cells, NC_, nullptr, 0);
+    ++launches_;
+  }
+}
+
+// One RK stage for the leaves of levels [lo, hi] (MRSolver::stage,
+// mr_solver.cpp:163-193): all levels read the same state, then commit.
+void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
+  MRStageArgs a{};
+  a.eval = d_V_;
+  a.base = d_Qold_;
+  a.out = d_Vs_;
+  a.st = d_st_;
+  a.gamma = cfg_.gamma;
+  a.gm1 = cfg_.gamma - 1.0;
+  a.sdt = sdt;
+  a.step3 = (int)(3 * step);
+  a.stage = stage;
+  a.post_check = stage == 2;
+  a.err = d_err_;
+  a.lo = lo;
+  a.vmark = d_mark_;
+  a.vq_old = d_VQold_;
+  for (int lv = 0; lv <= L_ && lv < 16; ++lv) {
+    const double denom = t_new_[lv] - t_old_[lv];
+    a.theta[lv] = denom > 0.0 ? std::clamp((tau - t_old_[lv]) / denom, 0.0, 1.0) : 1.0;
+  }
+  const int slot = (int)(stage_records_.size());
+  if (slot >= kMaxStageRecords) throw Error(AF_E_CONFIG, "too many stages per cycle");
+  stage_records_.push_back({slot, 0.0, lo, hi});
+  unsigned long long* wave = d_red_ + 64 + slot * 17;
+  unsigned long long* fb = d_red_ + 64 + slot * 17 + 16;
+  AF_CUDA(cudaMemsetAsync(wave, 0, sizeof(unsigned long long) * 17, stream_));
+  a.wave = wave;
+  a.fb = fb;
+  for (int l = lo; l <= std::min(hi, L_); ++l) {
+    if (!tile_count_[l]) continue;
+    a.tiles = d_tiles_ + tile_off_[l];
+    const int lim = cfg_.limiter;
+    if (D_ == 2) {
+      const size_t sm = MRTile<2, kTX2, kTY2, 1>::smem_bytes;
+      if (lim)
+        mr_stage_kernel<2, 1, kTX2, kTY2, 1><<<tile_count_[l], kTX2 * kTY2, sm, stream_>>>(a, g_, l);
+      else
+        mr_stage_kernel<2, 0, kTX2, kTY2, 1><<<tile_count_[l], kTX2 * kTY2, sm, stream_>>>(a, g_, l);
+    } else {
+      const size_t sm = MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes;
+      if (lim)
+        mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>
+            <<<tile_count_[l], kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, l);
+      else
+        mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>
+            <<<tile_count_[l], kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, l);
+    }
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+  }
+  for (int l = lo; l <= std::min(hi, L_); ++l) {
+    if (!leaves_per_level_[l]) continue;
+    mr_copy_leaves<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
+        d_Vs_, d_V_, d_st_, g_.cell_off[l], mr_cells(D_, l), g_.total_cells, NC_, d_err_,
+        stage == 2);
+    ++launches_;
+  }
+}
+
+// MRSolver::step_levels (mr_solver.cpp:232-316).
+void MR::step_levels_(int lo, int hi, double t, double dt) {
+  const int top = std::min(hi, L_);
+  snapshot_(lo, top);
+  for (int l = lo; l <= top; ++l) {
+    t_old_[l] = t;
+    t_new_[l] = t + dt;
+  }
+  // refresh_virtuals + the virtual q_old snapshot (mr_solver.cpp:251-266)
+  predict_fill_(lo, top);
+  if (d_VQold_)
+    for (int l = lo + 1; l <= std::min(top + 1, L_); ++l)
+      AF_MR_LAUNCH(mr_virtual_snapshot, grid_for(mr_cells(D_, l)), d_V_, d_VQold_, d_st_,
+                   d_mark_, g_, l);
+  const size_t r0 = stage_records_.size();
+  stage_(lo, top, t, 0.5 * dt, 1, cur_step_);
+  project_range_(lo, top);
+  predict_fill_(lo, top);
+  stage_(lo, top, t + 0.5 * dt, dt, 2, cur_step_);
+  project_range_(lo, top);
+  predict_fill_(lo, top);
+  for (size_t r = r0; r < stage_records_.size(); ++r) stage_records_[r].step_dt = dt;
+  bool deeper = false;
+  for (int l = top + 1; l <= L_; ++l) deeper = deeper || leaves_per_level_[l] > 0;
+  if (deeper) {
+    if (!opt_.local_time) throw Error(AF_E_CONFIG, "finer leaves outside the stepping set");
+    step_levels_(top + 1, top + 1, t, 0.5 * dt);
+    step_levels_(top + 1, top + 1, t + 0.5 * dt, 0.5 * dt);
+    apply_registers_(top);
+    project_range_(lo, top + 1);
+    predict_fill_(1, 0);
+  }
+}
+
+void MR::evolve_global(double dt, af_step_diag* d) {
+  stage_records_.clear();
+  build_tiles_();
+  step_levels_(0, L_, 0.0, dt);
+  collect_stage_records_(d);
+}
+
+void MR::advance_local(int top, double t, double dt, af_step_diag* d) {
+  stage_records_.clear();
+  build_tiles_();
+  step_levels_(0, top, t, dt);
+  collect_stage_records_(d);
+}
+
+// Reads the per-stage wave/fallback records of the last evolve and folds
+// them into the MRSolver accumulators (mr_solver.cpp:176-178); checks errors.
+void MR::collect_stage_records_(af_step_diag* d) {
+  check_error_(cur_step_);
+  const size_t ns = stage_records_.size();
+  if (!ns) return;
+  std::vector<unsigned long long> h(ns * 17);
+  AF_CUDA(cudaMemcpyAsync(h.data(), d_red_ + 64, 8 * ns * 17, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  double ws = 0.0;
+  long fbs = 0;
+  for (size_t r = 0; r < ns; ++r) {
+    const StageRec& sr = stage_records_[r];
+    for (int l = sr.lo; l <= std::min(sr.hi, L_); ++l) {
+      if (!leaves_per_level_[l]) continue;
+      const double w = as_d(h[r * 17 + l]);
+      const double dx = cfg_.extent / static_cast<double>(1 << l);
+      max_cfl_ = std::max(max_cfl_, w * sr.step_dt / dx);
+      ws = std::max(ws, w);
+    }
+    fbs += (long)h[r * 17 + 16];
+  }
+  fallbacks_ += fbs;
+  max_wave_ = std::max(max_wave_, ws);
+  if (d) {
+    d->max_wave_speed = ws;
+    d->fallbacks = fbs;
+  }
+}
+
+// apply_registers (mr_solver.cpp:210-230) — local time stepping only.
+void MR::apply_registers_(int coarse_level) {
+  (void)coarse_level;
+  throw Error(AF_E_UNSUPPORTED, "local time stepping registers are not implemented yet");
+}
+
+void MR::coarsen() {
+  for (;;) {
+    AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
+    for (int l = L_ - 1; l >= min_leaf_; --l)
+      AF_MR_LAUNCH(mr_coarsen_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, g_, l,
+                   eps_at_(l + 1), d_norms_, d_flagi_);
+    int merged = 0;
+    AF_CUDA(cudaMemcpyAsync(&merged, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    if (!merged) break;
+    predict_fill_(1, 0);
+  }
+}
+
+void MR::check_error_(long step) {
+  int h[4];
+  AF_CUDA(cudaMemcpyAsync(h, d_err_, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  if (!h[0] && !h[2]) return;
+  const int kind = h[1] % 3;  // 0/1 pass-1 of stage 1/2, 2 post-step
+  const double* src = d_V_;
+  std::vector<double> hv((size_t)NC_ * g_.total_cells);
+  std::vector<uint8_t> hs(g_.total_cells);
+  AF_CUDA(cudaMemcpy(hv.data(), kind == 2 ? d_Vs_ : src, hv.size() * 8, cudaMemcpyDeviceToHost));
+  AF_CUDA(cudaMemcpy(hs.data(), d_st_, hs.size(), cudaMemcpyDeviceToHost));
+  const double gm1 = cfg_.gamma - 1.0;
+  const long comp = g_.total_cells;
+  std::memset(&last_, 0, sizeof(last_));
+  last_.status = AF_E_NONPHYSICAL;
+  last_.step = step;
+  last_.stage = kind == 2 ? 2 : kind + 1;
+  const std::string pre = step >= 0 ? "step " + std::to_string(step) + ": " : "";
+  std::string msg = pre + "non-physical state";
+  // leaves in ascending pack_key order: level, then i, then j, then k
+  bool found = false;
+  for (int l = 0; l <= L_ && !found; ++l) {
+    const int n = 1 << l;
+    const int nk = D_ == 3 ? n : 1;
+    for (int i = 0; i < n && !found; ++i)
+      for (int j = 0; j < n && !found; ++j)
+        for (int k = 0; k < nk && !found; ++k) {
+          const long c = g_.cell_off[l] + (D_ == 3 ? ((long)k * n + j) * n + i : (long)j * n + i);
+          if (hs[c] != ST_LEAF) continue;
+          const double rho = hv[c];
+          double msq = hv[comp + c] * hv[comp + c] + hv[2 * comp + c] * hv[2 * comp + c];
+          if (D_ == 3) msq = msq + hv[3 * comp + c] * hv[3 * comp + c];
+          const double inv = 1.0 / rho;
+          const double p = gm1 * (hv[(NC_ - 1) * comp + c] - 0.5 * msq * inv);
+          if (!(rho > 1e-12) || !(rho > 1e-12 && p > 1e-12)) {
+            found = true;
+            last_.level = l;
+            last_.i = i;
+            last_.j = j;
+            last_.k = k;
+            last_.rho = rho;
+            last_.p = p;
+            const std::string node = "level " + std::to_string(l) + " (" + std::to_string(i) +
+                                     "," + std::to_string(j) + "," + std::to_string(k) + ")";
+            msg = kind == 2 ? pre + "post-step " + node
+                            : pre + node + ": rho=" + fmt_f(rho) + " p=" + fmt_f(p);
+          }
+        }
+  }
+  std::snprintf(last_.message, sizeof last_.message, "%s", msg.c_str());
+  throw Error(AF_E_NONPHYSICAL, last_.message);
+}
+
+void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, long max_cycles,
+             af_run_diag* rd) {
+  if (n_steps < 0) throw Error(AF_E_ARGUMENT, "n_steps must be >= 0");
+  if (!(cfl > 0.0) && !(fixed_dt > 0.0))
+    throw Error(AF_E_ARGUMENT, "either cfl or fixed_dt must be positive");
+  const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
+  long done = 0, cycle = 0;
+  double t = 0.0;
+  while (done < n_steps) {
+    long sub = 1;
+    int top = L_;
+    if (opt_.local_time) {  // mr_solver.cpp:345-354
+      top = std::max(coarsest_leaf_level(), min_leaf_);
+      long span = 1L << (L_ - top);
+      while (span > n_steps - done) {
+        span >>= 1;
+        ++top;
+      }
+      sub = span;
+    }
+    refine(opt_.local_time ? top : -1);
+    add_virtual_leaves();
+    long leaves = 0, nodes = 0;
+    counts(&leaves, &nodes, nullptr);
+    double dt = fixed_dt;
+    if (cfl > 0.0) dt = cfl * dx_L / leaf_speed_sum();
+    if (cycles && cycle < max_cycles) {
+      cycles[cycle].leaves = leaves;
+      cycles[cycle].nodes = nodes;
+      cycles[cycle].sub = sub;
+      cycles[cycle].top = top;
+      cycles[cycle].dt = dt;
+    }
+    const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
+    cur_step_ = done;
+    if (opt_.local_time)
+      advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
+    else
+      evolve_global(dt, nullptr);
+    cur_step_ = -1;
+    remove_virtual_leaves();
+    coarsen();
+    level_counts_();
+    done += sub;
+    t = t_cycle + static_cast<double>(sub) * dt;
+    ++cycle;
+  }
+  if (rd) {
+    rd->max_wave_speed = max_wave_;
+    rd->max_cfl = max_cfl_;
+    rd->fallbacks = fallbacks_;
+    rd->steps_done = done;
+    rd->t = t;
+  }
+}
+
+long MR::leaf_keys(uint64_t* keys, long cap) {
+  std::vector<uint8_t> hs(g_.total_cells);
+  AF_CUDA(cudaMemcpyAsync(hs.data(), d_st_, hs.size(), cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  std::vector<uint64_t> out;
+  for (int l = 0; l <= L_; ++l) {
+    const int n = 1 << l;
+    const long cells = mr_cells(D_, l);
+    for (long c = 0; c < cells; ++c) {
+      if (hs[g_.cell_off[l] + c] != ST_LEAF) continue;
+      const uint64_t i = c % n, j = (c / n) % n, k = D_ == 3 ? c / ((long)n * n) : 0;
+      out.push_back(((uint64_t)l << 45) | (i << 30) | (j << 15) | k);  // pack_key
+    }
+  }
+  std::sort(out.begin(), out.end());
+  if (keys)
+    for (long q = 0; q < (long)out.size() && q < cap; ++q) keys[q] = out[q];
+  return (long)out.size();
+}
+
+void MR::to_uniform(int level, double* aos) {
+  if (level < 0 || level > L_) throw Error(AF_E_LEVEL_MISMATCH, "to_uniform: bad level");
+  const long cells = mr_cells(D_, level);
+  double* tmp = nullptr;
+  AF_CUDA(cudaMalloc(&tmp, sizeof(double) * 5 * cells));
+  AF_MR_LAUNCH(mr_download_level, grid_for(cells), d_V_, tmp, g_, level);
+  AF_CUDA(cudaMemcpyAsync(aos, tmp, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(tmp);
+}
+
+void MR::details(int level, double* out) {
+  if (level < 0 || level >= L_) throw Error(AF_E_LEVEL_MISMATCH, "details: bad level");
+  const long cells = mr_cells(D_, level);
+  AF_CUDA(cudaMemsetAsync(d_det_ + g_.cell_off[level], 0xff, sizeof(double) * cells, stream_));
+  AF_MR_LAUNCH(mr_detail_level, grid_for(cells), d_V_, d_st_, d_det_, g_, level, d_norms_);
+  AF_CUDA(cudaMemcpyAsync(out, d_det_ + g_.cell_off[level], sizeof(double) * cells,
+                          cudaMemcpyDefault, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace af

@@ -1,0 +1,98 @@
+// af_mr.h — host class behind af_mr_* (see af_mr.cu).
+#pragma once
+
+#include <vector>
+
+#include "af_comm.h"
+#include "af_internal.h"
+#include "af_mr_types.h"
+
+namespace af {
+
+struct MRStageArgs;
+
+class MR {
+ public:
+  MR(const af_config& cfg, const af_mr_options& opt);
+  ~MR();
+  MR(const MR&) = delete;
+  MR& operator=(const MR&) = delete;
+
+  void set_stream(cudaStream_t s);
+  // MRTree::from_uniform + set_min_leaf_level + coarsen(eps) (mr_solver.cpp:406-410)
+  void build(const double* aos);
+  void refine(int top);              // MRTree::refine (+ LT buffer when top >= 0)
+  void add_virtual_leaves();         // marks the virtual set (and counts it)
+  void evolve_global(double dt, af_step_diag* d);
+  void advance_local(int top, double t, double dt, af_step_diag* d);
+  void coarsen();                    // MRTree::coarsen
+  void remove_virtual_leaves();
+  void run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, long max_cycles,
+           af_run_diag* rd);
+  void counts(long* leaves, long* nodes, long* internals);
+  int coarsest_leaf_level();
+  long leaf_keys(uint64_t* keys, long cap);
+  void to_uniform(int level, double* aos);
+  void details(int level, double* out);
+  double leaf_speed_sum();
+
+  long launches() const { return launches_; }
+  af_error& last_error() { return last_; }
+
+ private:
+  void predict_fill_(int lo, int hi);
+  void project_range_(int lo, int top);
+  void build_tiles_();
+  void level_counts_();
+  void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
+  void step_levels_(int lo, int hi, double t, double dt);
+  void snapshot_(int lo, int hi);
+  void check_error_(long step);
+  void collect_stage_records_(af_step_diag* d);
+  void apply_registers_(int coarse_level);
+  struct StageRec {
+    int slot;
+    double step_dt;
+    int lo, hi;
+  };
+  std::vector<StageRec> stage_records_;
+  double norms_host_[5] = {1, 1, 1, 1, 1};
+  double eps_at_(int child_level) const;
+
+  af_config cfg_;
+  af_mr_options opt_;
+  std::vector<double> eps_level_;
+  int D_, L_, NC_;
+  MRLevels g_{};
+  uint8_t* d_st_ = nullptr;
+  uint8_t* d_mark_ = nullptr;    // virtual parents
+  uint8_t* d_flag_ = nullptr;
+  uint8_t* d_flag2_ = nullptr;
+  double* d_V_ = nullptr;        // value_at field
+  double* d_Vs_ = nullptr;       // stage output
+  double* d_Qold_ = nullptr;     // step-start leaf values
+  double* d_VQold_ = nullptr;    // virtual q_old snapshots (LT)
+  double* d_det_ = nullptr;
+  double* d_norms_ = nullptr;
+  int* d_tiles_ = nullptr;
+  int* d_tile_count_ = nullptr;
+  int* d_err_ = nullptr;
+  int* d_flagi_ = nullptr;
+  unsigned long long* d_red_ = nullptr;  // scratch reductions
+  std::vector<long> tile_off_;           // per-level offset into d_tiles_
+  std::vector<int> tile_count_;
+  std::vector<long> leaves_per_level_;
+  std::vector<double> t_old_, t_new_;
+  int min_leaf_ = 0;
+  cudaStream_t stream_ = nullptr, own_stream_ = nullptr;
+  long launches_ = 0;
+  bool virtuals_ = false;
+  // per-run accumulators (MRSolver::max_cfl_, fallbacks_)
+  double max_cfl_ = 0.0;
+  long fallbacks_ = 0;
+  double max_wave_ = 0.0;
+  long cur_step_ = 0;
+  af_error last_{};
+};
+
+}  // namespace af

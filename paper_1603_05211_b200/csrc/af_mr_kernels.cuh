@@ -1,0 +1,485 @@
+// af_mr_kernels.cuh — Harten cell-average multiresolution on per-level dense
+// grids (sm_100a).
+//
+// Storage: every level l in [0, L] is a dense 2^l-per-axis grid of
+//   status  uint8  ABSENT / LEAF / INTERNAL  (the MRTree node map, mr_tree.hpp:195)
+//   value   NC doubles SoA — the reference's `value_at` field: the node's q
+//           where a node exists, and the recursive prediction where it does
+//           not (mr_tree.cpp:171-180). Keeping predictions materialised makes
+//           every stencil read a plain load; they are refreshed top-down after
+//           each projection, which is exactly when the reference's virtual
+//           leaves are re-predicted (refresh_virtuals, mr_solver.cpp:195-208).
+// Tree operations become level-synchronous passes whose results are
+// bit-identical to the reference's sequential loops (SURVEY.md §8(a) rows
+// 20-21 give the argument; tests/test_mr_gpu.py checks full trees).
+#pragma once
+
+#include "af_internal.h"
+#include "af_mr_types.h"
+#include "af_physics.cuh"
+#include "af_uniform_kernels.cuh"
+
+namespace af {
+
+// map_position (mr_tree.cpp:146-169): periodic when the LOW face is periodic
+// (BoundaryCondition::periodic), outflow clamps, reflective folds and flips.
+__device__ __forceinline__ int mr_map(int c, int n, int lo, int hi, bool& flip) {
+  flip = false;
+  if (c >= 0 && c < n) return c;
+  if (lo == AF_BC_PERIODIC) {
+    c %= n;
+    return c < 0 ? c + n : c;
+  }
+  const int kind = c < 0 ? lo : hi;
+  if (kind == AF_BC_OUTFLOW) return c < 0 ? 0 : n - 1;
+  while (c < 0 || c >= n) {
+    if (c < 0) c = -1 - c;
+    if (c >= n) c = 2 * n - 1 - c;
+    flip = !flip;
+  }
+  return c;
+}
+
+__device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
+  return D == 3 ? ((long)k * n + j) * n + i : (long)j * n + i;
+}
+
+// ------------------------------------------------------------ projection --
+// project_internals / project_range (mr_tree.cpp:319-338, mr_solver.cpp:268-282):
+// internal q = (sum over children, x-fastest child order) * (1/2^d).
+template <int D>
+__global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l) {
+  constexpr int NC = D + 2;
+  const int n = 1 << l, nf = n << 1;
+  const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
+  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+  const long comp = g.total_cells;
+  const double w = 1.0 / (double)(1 << D);
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_INTERNAL) continue;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    double s[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) s[m] = 0.0;
+#pragma unroll
+    for (int ch = 0; ch < (1 << D); ++ch) {
+      const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                                    D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+#pragma unroll
+      for (int m = 0; m < NC; ++m) s[m] = s[m] + V[m * comp + fc];
+    }
+#pragma unroll
+    for (int m = 0; m < NC; ++m) V[m * comp + off + c] = s[m] * w;
+  }
+  (void)fcells;
+}
+
+// ------------------------------------------------------------ prediction --
+// axis_stencil (mr_tree.cpp:199-236): positions and low/high-child weights.
+struct AxisSt {
+  int pos[3];
+  double wl[3], wh[3];
+};
+
+__device__ __forceinline__ AxisSt axis_stencil(int n, int coord, bool periodic) {
+  AxisSt s;
+  if (periodic || (coord > 0 && coord < n - 1)) {
+    s.pos[0] = coord - 1; s.pos[1] = coord; s.pos[2] = coord + 1;
+    s.wl[0] = 1.0 / 8.0; s.wl[1] = 1.0; s.wl[2] = -1.0 / 8.0;
+    s.wh[0] = -1.0 / 8.0; s.wh[1] = 1.0; s.wh[2] = 1.0 / 8.0;
+    if (periodic) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t) s.pos[t] = ((s.pos[t] % n) + n) % n;  // value_at wraps
+    }
+    return s;
+  }
+  if (n == 1) {
+    s.pos[0] = s.pos[1] = s.pos[2] = 0;
+    s.wl[0] = 1.0; s.wl[1] = 0.0; s.wl[2] = 0.0;
+    s.wh[0] = 1.0; s.wh[1] = 0.0; s.wh[2] = 0.0;
+    return s;
+  }
+  if (n == 2) {
+    s.pos[0] = 0; s.pos[1] = 1; s.pos[2] = 1;
+    if (coord == 0) {
+      s.wl[0] = 5.0 / 4.0; s.wl[1] = -1.0 / 4.0; s.wl[2] = 0.0;
+      s.wh[0] = 3.0 / 4.0; s.wh[1] = 1.0 / 4.0; s.wh[2] = 0.0;
+    } else {
+      s.wl[0] = 1.0 / 4.0; s.wl[1] = 3.0 / 4.0; s.wl[2] = 0.0;
+      s.wh[0] = -1.0 / 4.0; s.wh[1] = 5.0 / 4.0; s.wh[2] = 0.0;
+    }
+    return s;
+  }
+  if (coord == 0) {
+    s.pos[0] = 0; s.pos[1] = 1; s.pos[2] = 2;
+    s.wl[0] = 11.0 / 8.0; s.wl[1] = -4.0 / 8.0; s.wl[2] = 1.0 / 8.0;
+    s.wh[0] = 5.0 / 8.0; s.wh[1] = 4.0 / 8.0; s.wh[2] = -1.0 / 8.0;
+  } else {
+    s.pos[0] = n - 3; s.pos[1] = n - 2; s.pos[2] = n - 1;
+    s.wl[0] = -1.0 / 8.0; s.wl[1] = 4.0 / 8.0; s.wl[2] = 5.0 / 8.0;
+    s.wh[0] = 1.0 / 8.0; s.wh[1] = -4.0 / 8.0; s.wh[2] = 11.0 / 8.0;
+  }
+  return s;
+}
+
+// Prediction of child `ch` (x-fastest child bits) of the level-(l-1) parent
+// (pi,pj,pk) from the dense values of level l-1 (predict_children,
+// mr_tree.cpp:238-279: weights w = wx * (wy * wz), zero weights skipped,
+// accumulation ck -> cj -> ci).
+template <int D>
+__device__ __forceinline__ void predict_child(const double* V, long comp, long poff, int pn,
+                                              const int* bc, int pi, int pj, int pk, int ch,
+                                              double* out) {
+  constexpr int NC = D + 2;
+  const AxisSt sx = axis_stencil(pn, pi, bc[0] == AF_BC_PERIODIC);
+  const AxisSt sy = axis_stencil(pn, pj, bc[2] == AF_BC_PERIODIC);
+  AxisSt sz;
+  if (D == 3) sz = axis_stencil(pn, pk, bc[4] == AF_BC_PERIODIC);
+  const double* wx = (ch & 1) ? sx.wh : sx.wl;
+  const double* wy = ((ch >> 1) & 1) ? sy.wh : sy.wl;
+  const double* wz = D == 3 ? (((ch >> 2) & 1) ? sz.wh : sz.wl) : nullptr;
+#pragma unroll
+  for (int m = 0; m < NC; ++m) out[m] = 0.0;
+  const int nz = D == 3 ? 3 : 1;
+  for (int ck = 0; ck < nz; ++ck) {
+    const double wk = D == 3 ? wz[ck] : 1.0;
+    if (wk == 0.0) continue;
+#pragma unroll
+    for (int cj = 0; cj < 3; ++cj) {
+      const double wjk = wy[cj] * wk;
+      if (wjk == 0.0) continue;
+#pragma unroll
+      for (int ci = 0; ci < 3; ++ci) {
+        const double w = wx[ci] * wjk;
+        if (w == 0.0) continue;
+        const long c = poff + mr_idx(D, pn, sx.pos[ci], sy.pos[cj], D == 3 ? sz.pos[ck] : 0);
+#pragma unroll
+        for (int m = 0; m < NC; ++m) out[m] = out[m] + V[m * comp + c] * w;
+      }
+    }
+  }
+}
+
+// Fills ABSENT cells of level l (l >= 1) with their prediction from level
+// l-1: value_at / predict_single for absent nodes (mr_tree.cpp:171-180,
+// 281-289). Virtual leaves (children of a leaf marked in `vmark`, materialised
+// by add_virtual_leaves, mr_tree.cpp:513-551) keep their stored value unless
+// their parent level is in [lo, hi] — refresh_virtuals (mr_solver.cpp:195-208)
+// re-predicts only the virtual children of the stepping leaves.
+template <int D>
+__global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
+                                 MRLevels g, int l, int lo, int hi) {
+  constexpr int NC = D + 2;
+  const int n = 1 << l, pn = n >> 1;
+  const long cells = mr_cells(D, l);
+  const long off = g.cell_off[l], poff = g.cell_off[l - 1];
+  const long comp = g.total_cells;
+  const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_ABSENT) continue;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
+    const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
+    double q[NC];
+    predict_child<D>(V, comp, poff, pn, g.bc, i >> 1, j >> 1, k >> 1, ch, q);
+#pragma unroll
+    for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
+  }
+}
+
+// ---------------------------------------------------------------- detail --
+// detail / detail_between (mr_tree.cpp:291-317): max over children and
+// components of |q_child - pred_child| / norm_k. Zero numerators are returned
+// directly (0/x == 0 exactly) to stay off the division slow path.
+template <int D>
+__device__ __forceinline__ double node_detail(const double* V, long comp, const MRLevels& g,
+                                              int l, int i, int j, int k, const double* norms) {
+  constexpr int NC = D + 2;
+  const int n = 1 << l, nf = n << 1;
+  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+  double mag = 0.0;
+  for (int ch = 0; ch < (1 << D); ++ch) {
+    double pred[NC];
+    predict_child<D>(V, comp, off, n, g.bc, i, j, k, ch, pred);
+    const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                                  D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+#pragma unroll
+    for (int m = 0; m < NC; ++m) {
+      const double d = fabs(V[m * comp + fc] - pred[m]);
+      // norms index: rho 0, mom 1..D, rhoE 4 (the 2D mom2 term is 0/global == 0)
+      const int ni = m == NC - 1 ? 4 : m;
+      const double r = d == 0.0 ? 0.0 : d / norms[ni];
+      mag = mag > r ? mag : r;  // std::max(mag, r)
+    }
+  }
+  return mag;
+}
+
+// Detail of every INTERNAL node at level l.
+template <int D>
+__global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
+                                int l, const double* norms) {
+  const int n = 1 << l;
+  const long cells = mr_cells(D, l), off = g.cell_off[l];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_INTERNAL) continue;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    det[off + c] = node_detail<D>(V, g.total_cells, g, l, i, j, k, norms);
+  }
+}
+
+// Buffer dilation of the LT refine (mr_tree.cpp:374-396): every leaf within
+// Chebyshev radius r of a flagged leaf (same level, bc-mapped) is flagged too.
+// flag[] holds 1 for detail-flagged leaves; this pass writes 2 for dilated.
+template <int D>
+__global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
+                                     MRLevels g, int l, double eps) {
+  const int n = 1 << l, pn = n >> 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    uint8_t f = 0;
+    if (st[off + c] == ST_LEAF && l >= 1 && l < g.L) {
+      const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+      f = det[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)] >= eps ? 1 : 0;
+    }
+    flag[off + c] = f;
+  }
+}
+
+template <int D>
+__global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
+                                MRLevels g, int l, int r) {
+  // Target t is inserted iff some detail-flagged source s has map(s + o) == t
+  // for an offset o != 0 with |o|_inf <= r. Clamping and folding never move a
+  // position farther from s, so scanning the in-domain (or periodically
+  // wrapped) sources s = t - o is exhaustive.
+  const int n = 1 << l;
+  const long cells = mr_cells(D, l), off = g.cell_off[l];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    uint8_t f = flag[off + c];
+    if (!f && st[off + c] == ST_LEAF) {
+      const int t[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+      const int rz = D == 3 ? r : 0;
+      for (int dk = -rz; dk <= rz && !f; ++dk)
+        for (int dj = -r; dj <= r && !f; ++dj)
+          for (int di = -r; di <= r && !f; ++di) {
+            if (di == 0 && dj == 0 && dk == 0) continue;
+            int s[3] = {t[0] - di, t[1] - dj, t[2] - dk};
+            bool ok = true;
+            for (int a = 0; a < D; ++a) {
+              if (s[a] >= 0 && s[a] < n) continue;
+              if (g.bc[2 * a] == AF_BC_PERIODIC)
+                s[a] = ((s[a] % n) + n) % n;
+              else
+                ok = false;
+            }
+            if (ok && flag[off + mr_idx(D, n, s[0], s[1], s[2])] == 1) f = 2;
+          }
+    }
+    flag2[off + c] = f;
+  }
+}
+
+template <int D>
+__global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels g, int l,
+                                     int* changed) {
+  const int n = 1 << l, nf = n << 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (!flag[off + c] || st[off + c] != ST_LEAF) continue;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    st[off + c] = ST_INTERNAL;
+    for (int ch = 0; ch < (1 << D); ++ch)
+      st[foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                       D == 3 ? 2 * k + ((ch >> 2) & 1) : 0)] = ST_LEAF;
+    *changed = 1;
+  }
+}
+
+// enforce_gradedness (mr_tree.cpp:404-444), decision half of one pass: a
+// leaf below L must split when a same-level face neighbour is INTERNAL with
+// an INTERNAL child on the shared face. (Unique least fixpoint; decide all,
+// then apply, repeat.)
+template <int D>
+__global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l) {
+  const int n = 1 << l, nf = n << 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    uint8_t need = 0;
+    if (st[off + c] == ST_LEAF && l < g.L) {
+      const int idx[3] = {(int)(c % n), (int)((c / n) % n),
+                          D == 3 ? (int)(c / ((long)n * n)) : 0};
+      for (int a = 0; a < D && !need; ++a)
+        for (int dir = -1; dir <= 1 && !need; dir += 2) {
+          int p[3] = {idx[0], idx[1], idx[2]};
+          p[a] += dir;
+          const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+          if (!per && (p[a] < 0 || p[a] >= n)) continue;
+          bool fl;
+          p[a] = mr_map(p[a], n, g.bc[2 * a], g.bc[2 * a + 1], fl);
+          if (st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_INTERNAL) continue;
+          const int face_bit = dir > 0 ? 0 : 1;
+          const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
+          const int tzn = D == 3 ? 2 : 1;
+          for (int t2 = 0; t2 < tzn && !need; ++t2)
+            for (int t1 = 0; t1 < 2 && !need; ++t1) {
+              int ci[3];
+              ci[a] = 2 * p[a] + face_bit;
+              ci[b1] = 2 * p[b1] + t1;
+              ci[b2] = D == 3 ? 2 * p[b2] + t2 : 0;
+              if (st[foff + mr_idx(D, nf, ci[0], ci[1], ci[2])] == ST_INTERNAL) need = 1;
+            }
+        }
+    }
+    flag[off + c] = need;
+  }
+}
+
+// coarsen (mr_tree.cpp:446-511), one level of one finest-first sweep:
+// an INTERNAL node at level l >= min_leaf merges iff all children are leaves,
+// detail < eps_{l+1}, and no face-ring cell at level l+1 is INTERNAL.
+template <int D>
+__global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
+                                 const double* norms, int* merged) {
+  const int n = 1 << l, nf = n << 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_INTERNAL) continue;
+    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    bool all_leaves = true;
+    for (int ch = 0; ch < (1 << D) && all_leaves; ++ch)
+      if (st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
+                           D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] != ST_LEAF)
+        all_leaves = false;
+    if (!all_leaves) continue;
+    const double d = node_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], norms);
+    if (!(d < eps)) continue;
+    bool allowed = true;  // merge_allowed (mr_tree.cpp:446-471)
+    for (int a = 0; a < D && allowed; ++a)
+      for (int dir = -1; dir <= 1 && allowed; dir += 2) {
+        const int tzn = D == 3 ? 2 : 1;
+        const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
+        for (int t2 = 0; t2 < tzn && allowed; ++t2)
+          for (int t1 = 0; t1 < 2 && allowed; ++t1) {
+            int r[3];
+            r[a] = dir > 0 ? 2 * idx[a] + 2 : 2 * idx[a] - 1;
+            r[b1] = 2 * idx[b1] + t1;
+            r[b2] = D == 3 ? 2 * idx[b2] + t2 : 0;
+            const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+            if (!per && (r[a] < 0 || r[a] >= nf)) continue;
+            bool fl;
+            r[a] = mr_map(r[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
+            if (st[foff + mr_idx(D, nf, r[0], r[1], r[2])] == ST_INTERNAL) allowed = false;
+          }
+      }
+    if (!allowed) continue;
+    // merged q = mean of the children == the projection already stored
+    st[off + c] = ST_LEAF;
+    for (int ch = 0; ch < (1 << D); ++ch)
+      st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
+                       D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] = ST_ABSENT;
+    *merged = 1;
+  }
+}
+
+// Virtual-leaf count (add_virtual_leaves, mr_tree.cpp:513-551): a level-(l-1)
+// leaf P gets 2^d virtual children when some axis-stencil position (+-1, +-2)
+// of a level-l leaf maps into an absent child of P. Marks P in `mark`.
+template <int D>
+__global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l) {
+  const int n = 1 << l, pn = n >> 1;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_LEAF) continue;
+    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    for (int a = 0; a < D; ++a)
+      for (int o = -2; o <= 2; ++o) {
+        if (o == 0) continue;
+        int p[3] = {idx[0], idx[1], idx[2]};
+        p[a] += o;
+        const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+        if (!per && (p[a] < 0 || p[a] >= n)) continue;
+        bool fl;
+        p[a] = mr_map(p[a], n, g.bc[2 * a], g.bc[2 * a + 1], fl);
+        if (st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_ABSENT) continue;
+        const long pc = poff + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+        if (st[pc] == ST_LEAF) mark[pc] = 1;
+      }
+  }
+}
+
+// Counts per level: [0] leaves, [1] internals, [2] virtual-marked parents.
+static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, long n,
+                                unsigned long long* out) {
+  unsigned long long lv = 0, in = 0, vm = 0;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n;
+       c += (long)gridDim.x * blockDim.x) {
+    const uint8_t s = st[c];
+    lv += s == ST_LEAF;
+    in += s == ST_INTERNAL;
+    if (mark) vm += mark[c];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    in += __shfl_xor_sync(0xffffffffu, in, o);
+    vm += __shfl_xor_sync(0xffffffffu, vm, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lv) atomicAdd(out, lv);
+    if (in) atomicAdd(out + 1, in);
+    if (vm) atomicAdd(out + 2, vm);
+  }
+}
+
+// Max over leaves of sum_a(|v_a|+c) (CFL rule) for the leaves of level l.
+template <int D>
+__global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
+                                     double gamma, unsigned long long* target) {
+  __shared__ double red[8];
+  const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
+  double best = 0.0;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    if (st[off + c] != ST_LEAF) continue;
+    Cons<D> q;
+    q.rho = V[off + c];
+#pragma unroll
+    for (int a = 0; a < D; ++a) q.m[a] = V[(1 + a) * comp + off + c];
+    q.E = V[(D + 1) * comp + off + c];
+    double s, m;
+    wave_speeds(primitives(q, gamma - 1.0), gamma, s, m);
+    best = fmax(best, s);
+  }
+  block_max_atomic<256>(best, red, target);
+}
+
+// Per-component max |q| of the finest level (set_norms_from, mr_tree.cpp:73-87).
+template <int D>
+__global__ void mr_norm_kernel(const double* V, MRLevels g, unsigned long long* out) {
+  constexpr int NC = D + 2;
+  const long cells = mr_cells(D, g.L), off = g.cell_off[g.L], comp = g.total_cells;
+  double mx[NC];
+#pragma unroll
+  for (int m = 0; m < NC; ++m) mx[m] = 0.0;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int m = 0; m < NC; ++m) mx[m] = fmax(mx[m], fabs(V[m * comp + off + c]));
+  }
+#pragma unroll
+  for (int m = 0; m < NC; ++m) {
+    double v = warp_max(mx[m]);
+    if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(out + m, dbits(v));
+  }
+}
+
+}  // namespace af

@@ -1,0 +1,404 @@
+// af_mr_stage.cuh — one RK stage for the leaves of one MR level (sm_100a).
+//
+// MRSolver::stage (mr_solver.cpp:163-193) for the leaves of level l, as a
+// tile kernel over the level's dense grid: the tile's primitives (2-cell
+// halo, bc-mapped as map_position, mr_tree.cpp:146-169) are staged in shared
+// memory, every face touching a leaf is evaluated once, and each leaf sums
+// its 2d faces in the reference order (rhs += F(a,-)/dx; rhs -= F(a,+)/dx,
+// mr_solver.cpp:182-185). Faces whose same-level neighbour is INTERNAL take
+// the coarse side of the interface rule instead: the mean of the 2^(d-1)
+// fine sub-face fluxes (fine_face_average, mr_solver.cpp:59-95), including
+// its asymmetric low-face stencil (p-2, p-1 | p, p+2) (mr_solver.cpp:80).
+#pragma once
+
+#include "af_mr_kernels.cuh"
+
+namespace af {
+
+struct MRStageArgs {
+  const double* eval;  // concatenated level values the fluxes read
+  const double* base;  // step-start values (q_old)
+  double* out;         // stage output (leaves of this level)
+  const uint8_t* st;
+  double gamma, gm1;
+  double sdt;          // stage_dt
+  int step3;           // error code base: 3*step; + stage-1 for pass 1, + 2 for post-step
+  int stage;
+  int post_check;      // stage 2: positivity of the completed step
+  unsigned long long* wave;  // per-level max (|v_a|+c) of the evaluated leaves
+  unsigned long long* fb;    // fallbacks
+  int* err;                  // [0] flag, [1] min code
+  const int* tiles;
+  // local time stepping: virtual leaves whose parent level is below `lo`
+  // read as q_old*(1-theta) + q*theta (resolve, mr_solver.cpp:43-50)
+  int lo;
+  const uint8_t* vmark;
+  const double* vq_old;
+  double theta[16];  // by parent level
+};
+
+// resolve() for level l (mr_solver.cpp:36-57, global mode): bc-mapped read of
+// the dense level value with the reflective momentum flip.
+template <int D>
+__device__ __forceinline__ Cons<D> resolve_at(const double* V, long comp, const MRLevels& g,
+                                              int l, int i, int j, int k,
+                                              const MRStageArgs* lt = nullptr) {
+  const int n = 1 << l;
+  bool fi, fj, fk = false;
+  const int mi = mr_map(i, n, g.bc[0], g.bc[1], fi);
+  const int mj = mr_map(j, n, g.bc[2], g.bc[3], fj);
+  const int mk = D == 3 ? mr_map(k, n, g.bc[4], g.bc[5], fk) : 0;
+  const long c = g.cell_off[l] + mr_idx(D, n, mi, mj, mk);
+  Cons<D> q;
+  q.rho = V[c];
+#pragma unroll
+  for (int a = 0; a < D; ++a) q.m[a] = V[(1 + a) * comp + c];
+  q.E = V[(D + 1) * comp + c];
+  if (lt && l - 1 < lt->lo && l >= 1) {
+    const long pc = g.cell_off[l - 1] + mr_idx(D, n >> 1, mi >> 1, mj >> 1, mk >> 1);
+    // a virtual leaf over an already-advanced coarser leaf: interpolate in time
+    if (lt->vmark[pc] && lt->st[c] == ST_ABSENT) {
+      const double th = lt->theta[l - 1], om = 1.0 - th;
+      q.rho = lt->vq_old[c] * om + q.rho * th;
+#pragma unroll
+      for (int a = 0; a < D; ++a) q.m[a] = lt->vq_old[(1 + a) * comp + c] * om + q.m[a] * th;
+      q.E = lt->vq_old[(D + 1) * comp + c] * om + q.E * th;
+    }
+  }
+  if (fi) q.m[0] = -q.m[0];
+  if (fj) q.m[1] = -q.m[1];
+  if (D == 3 && fk) q.m[D - 1] = -q.m[D - 1];
+  return q;
+}
+
+template <int D, int AX, int LIM>
+__device__ __forceinline__ Cons<D> flux4(const Cons<D>& qa, const Cons<D>& qb, const Cons<D>& qc,
+                                         const Cons<D>& qd, double gamma, double gm1, int* fb) {
+  const Prim<D> wa = primitives(qa, gm1), wb = primitives(qb, gm1);
+  const Prim<D> wc = primitives(qc, gm1), wd = primitives(qd, gm1);
+  return face_flux<D, AX, LIM>(qb.E, qc.E, wa, wb, wc, wd, gamma, gm1, fb);
+}
+
+// fine_face_average (mr_solver.cpp:59-95) of leaf (c0,c1,c2) at level l.
+template <int D, int AX, int LIM>
+__device__ Cons<D> fine_face_average(const double* V, long comp, const MRLevels& g, int l,
+                                     const int* c, int dir, double gamma, double gm1, int* fb) {
+  constexpr int b1 = AX == 0 ? 1 : 0;
+  constexpr int b2 = AX == 2 ? 1 : 2;
+  const int fl = l + 1;
+  const int tzn = D == 3 ? 2 : 1;
+  Cons<D> sum;
+  sum.rho = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) sum.m[a] = 0.0;
+  sum.E = 0.0;
+  for (int t2 = 0; t2 < tzn; ++t2)
+    for (int t1 = 0; t1 < 2; ++t1) {
+      int p[3];
+      p[AX] = 2 * c[AX] + (dir > 0 ? 1 : 0);
+      p[b1] = 2 * c[b1] + t1;
+      p[b2] = D == 3 ? 2 * c[b2] + t2 : 0;
+      int s0[3] = {p[0], p[1], p[2]}, s2[3] = {p[0], p[1], p[2]}, s3[3] = {p[0], p[1], p[2]};
+      s0[AX] += dir > 0 ? -1 : 2;  // the reference's (p-2, p-1 | p, p+2) on the low face
+      s2[AX] += dir;
+      s3[AX] += 2 * dir;
+      const int* A = dir > 0 ? s0 : s3;
+      const int* B = dir > 0 ? p : s2;
+      const int* Cc = dir > 0 ? s2 : p;
+      const int* Dd = dir > 0 ? s3 : s0;
+      const Cons<D> qa = resolve_at<D>(V, comp, g, fl, A[0], A[1], A[2]);
+      const Cons<D> qb = resolve_at<D>(V, comp, g, fl, B[0], B[1], B[2]);
+      const Cons<D> qc = resolve_at<D>(V, comp, g, fl, Cc[0], Cc[1], Cc[2]);
+      const Cons<D> qd = resolve_at<D>(V, comp, g, fl, Dd[0], Dd[1], Dd[2]);
+      const Cons<D> f = flux4<D, AX, LIM>(qa, qb, qc, qd, gamma, gm1, fb);
+      sum.rho = sum.rho + f.rho;
+#pragma unroll
+      for (int a = 0; a < D; ++a) sum.m[a] = sum.m[a] + f.m[a];
+      sum.E = sum.E + f.E;
+    }
+  const double s = 1.0 / (double)(tzn * 2);
+  sum.rho = sum.rho * s;
+#pragma unroll
+  for (int a = 0; a < D; ++a) sum.m[a] = sum.m[a] * s;
+  sum.E = sum.E * s;
+  return sum;
+}
+
+template <int D, int TX, int TY, int TZ>
+struct MRTile {
+  static constexpr int NT = TX * TY * TZ;
+  static constexpr int HX = TX + 4, HY = TY + 4, HZ = D == 3 ? TZ + 4 : 1;
+  static constexpr int HP = HX * HY * HZ;
+  static constexpr int NXF = (TX + 1) * TY * TZ;
+  static constexpr int NYF = TX * (TY + 1) * TZ;
+  static constexpr int NZF = D == 3 ? TX * TY * (TZ + 1) : 0;
+  static constexpr int NF = NXF + NYF + NZF;
+  static constexpr int NC = D + 2;
+  static constexpr size_t smem_bytes =
+      sizeof(double) * ((size_t)NC * HP + (size_t)NC * NF + NT / 32) + NF + NT + 16;
+};
+
+template <int D, int LIM, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(TX* TY* TZ, 2)
+    mr_stage_kernel(MRStageArgs a, MRLevels g, int l) {
+  using K = MRTile<D, TX, TY, TZ>;
+  constexpr int NC = K::NC;
+  if (failed_before(a.err)) return;
+  extern __shared__ double sm[];
+  double* pr = sm;                        // [NC][HP] primitives
+  double* fl = pr + NC * K::HP;           // [NC][NF] face fluxes
+  double* red = fl + NC * K::NF;          // [NT/32]
+  uint8_t* ffb = reinterpret_cast<uint8_t*>(red + K::NT / 32);  // [NF] fallback flags
+  uint8_t* leaf = ffb + K::NF;            // [NT] leaf mask
+  __shared__ int s_fb, s_bad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = 1 << l;
+  const long comp = g.total_cells, off = g.cell_off[l];
+  const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
+  const int t = a.tiles[blockIdx.x];
+  const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
+  const int z0 = D == 3 ? (t / (ntx * nty)) * TZ : 0;
+  const double gamma = a.gamma, gm1 = a.gm1;
+  const double inv_dx = g.inv_dx[l];
+  if (tid == 0) {
+    s_fb = 0;
+    s_bad = 0;
+  }
+  // leaf mask of the tile cells
+  const int tx = tid % TX, ty = (tid / TX) % TY, tz = D == 3 ? tid / (TX * TY) : 0;
+  const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
+  const bool inside = cx < n && cy < n && (D == 2 || cz < n);
+  const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
+  const bool is_leaf = inside && a.st[own] == ST_LEAF;
+  leaf[tid] = is_leaf;
+  double wave = 0.0;
+  int bad = 0;
+  for (int idx = tid; idx < K::HP; idx += K::NT) {
+    const int ix = idx % K::HX, iy = (idx / K::HX) % K::HY, iz = D == 3 ? idx / (K::HX * K::HY) : 0;
+    const bool ccx = ix >= 2 && ix < TX + 2, ccy = iy >= 2 && iy < TY + 2;
+    const bool ccz = D == 2 || (iz >= 2 && iz < TZ + 2);
+    if ((int)!ccx + (int)!ccy + (int)!ccz > 1) continue;  // never on an axis stencil
+    const Cons<D> q = resolve_at<D>(a.eval, comp, g, l, x0 - 2 + ix, y0 - 2 + iy,
+                                    D == 3 ? z0 - 2 + iz : 0, &a);
+    const Prim<D> w = primitives(q, gm1);
+#pragma unroll
+    for (int m = 0; m < NC; ++m)
+      pr[m * K::HP + idx] = m == 0 ? w.rho : (m == NC - 1 ? w.p : w.v[m - 1]);
+  }
+  // Pass-1 checks of this thread's leaf (mr_solver.cpp:171-178).
+  if (is_leaf) {
+    Cons<D> q;
+    q.rho = a.eval[own];
+#pragma unroll
+    for (int d = 0; d < D; ++d) q.m[d] = a.eval[(1 + d) * comp + own];
+    q.E = a.eval[(D + 1) * comp + own];
+    const Prim<D> w = primitives(q, gm1);
+    if (!cell_ok(q, w)) bad = 1;
+    double s, m;
+    wave_speeds(w, gamma, s, m);
+    wave = m;
+  }
+  __syncthreads();
+  auto P = [&](int ix, int iy, int iz) {
+    const int idx = (iz * K::HY + iy) * K::HX + ix;
+    Prim<D> w;
+    w.rho = pr[idx];
+#pragma unroll
+    for (int d = 0; d < D; ++d) w.v[d] = pr[(1 + d) * K::HP + idx];
+    w.p = pr[(NC - 1) * K::HP + idx];
+    return w;
+  };
+  auto leaf_at = [&](int x, int y, int z) {  // tile-local coords, -1/T allowed
+    if (x < 0 || x >= TX || y < 0 || y >= TY || z < 0 || z >= TZ) return false;
+    return leaf[(z * TY + y) * TX + x] != 0;
+  };
+  auto energy_at = [&](int x, int y, int z) {
+    return resolve_at<D>(a.eval, comp, g, l, x, y, z, &a).E;
+  };
+  // Face fluxes needed by a leaf of the tile.
+  constexpr int UX = (K::NXF + 31) / 32, UY = (K::NYF + 31) / 32, UZ = (K::NZF + 31) / 32;
+  for (int u = warp; u < UX + UY + UZ; u += K::NT / 32) {
+    int fb = 0;
+    if (u < UX) {
+      const int f = u * 32 + lane;
+      if (f < K::NXF) {
+        const int fx = f % (TX + 1), fy = (f / (TX + 1)) % TY, fz = D == 3 ? f / ((TX + 1) * TY) : 0;
+        if (leaf_at(fx - 1, fy, fz) || leaf_at(fx, fy, fz)) {
+          const int iy = fy + 2, iz = D == 3 ? fz + 2 : 0;
+          const Prim<D> wm1 = P(fx, iy, iz), w0 = P(fx + 1, iy, iz), wp1 = P(fx + 2, iy, iz),
+                        wp2 = P(fx + 3, iy, iz);
+          Prim<D> lft, rgt;
+          Cons<D> F;
+          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
+            fb = 1;
+            F = ausm_plus<D, 0>(energy_at(x0 + fx - 1, y0 + fy, z0 + fz), w0,
+                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+          } else {
+            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
+            F = ausm_plus<D, 0>(ql.E, lft, qr.E, rgt, gamma);
+          }
+          fl[f] = F.rho;
+#pragma unroll
+          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + f] = F.m[d];
+          fl[(NC - 1) * K::NF + f] = F.E;
+          ffb[f] = fb;
+        }
+      }
+    } else if (u < UX + UY) {
+      const int f = (u - UX) * 32 + lane;
+      if (f < K::NYF) {
+        const int fx = f % TX, fy = (f / TX) % (TY + 1), fz = D == 3 ? f / (TX * (TY + 1)) : 0;
+        if (leaf_at(fx, fy - 1, fz) || leaf_at(fx, fy, fz)) {
+          const int ix = fx + 2, iz = D == 3 ? fz + 2 : 0;
+          const Prim<D> wm1 = P(ix, fy, iz), w0 = P(ix, fy + 1, iz), wp1 = P(ix, fy + 2, iz),
+                        wp2 = P(ix, fy + 3, iz);
+          Prim<D> lft, rgt;
+          Cons<D> F;
+          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
+            fb = 1;
+            F = ausm_plus<D, 1>(energy_at(x0 + fx, y0 + fy - 1, z0 + fz), w0,
+                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+          } else {
+            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
+            F = ausm_plus<D, 1>(ql.E, lft, qr.E, rgt, gamma);
+          }
+          const int g2 = K::NXF + f;
+          fl[g2] = F.rho;
+#pragma unroll
+          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + g2] = F.m[d];
+          fl[(NC - 1) * K::NF + g2] = F.E;
+          ffb[g2] = fb;
+        }
+      }
+    } else if constexpr (D == 3) {
+      const int f = (u - UX - UY) * 32 + lane;
+      if (f < K::NZF) {
+        const int fx = f % TX, fy = (f / TX) % TY, fz = f / (TX * TY);
+        if (leaf_at(fx, fy, fz - 1) || leaf_at(fx, fy, fz)) {
+          const int ix = fx + 2, iy = fy + 2;
+          const Prim<D> wm1 = P(ix, iy, fz), w0 = P(ix, iy, fz + 1), wp1 = P(ix, iy, fz + 2),
+                        wp2 = P(ix, iy, fz + 3);
+          Prim<D> lft, rgt;
+          Cons<D> F;
+          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
+            fb = 1;
+            F = ausm_plus<D, 2>(energy_at(x0 + fx, y0 + fy, z0 + fz - 1), w0,
+                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+          } else {
+            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
+            F = ausm_plus<D, 2>(ql.E, lft, qr.E, rgt, gamma);
+          }
+          const int g3 = K::NXF + K::NYF + f;
+          fl[g3] = F.rho;
+#pragma unroll
+          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + g3] = F.m[d];
+          fl[(NC - 1) * K::NF + g3] = F.E;
+          ffb[g3] = fb;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int nfb = 0;
+  double ssum = 0.0;
+  if (is_leaf) {
+    const int c[3] = {cx, cy, cz};
+    double rhs[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) rhs[m] = 0.0;
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+#pragma unroll
+      for (int dir = -1; dir <= 1; dir += 2) {
+        // neighbour across the face, same level, bc-mapped (face_flux_at, mr_solver.cpp:99-103)
+        int p[3] = {c[0], c[1], c[2]};
+        p[ax] += dir;
+        bool flp;
+        p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
+        const bool internal = a.st[off + mr_idx(D, n, p[0], p[1], p[2])] == ST_INTERNAL;
+        double F[NC];
+        if (internal) {
+          Cons<D> f;
+          if (ax == 0) f = fine_face_average<D, 0, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
+          else if (ax == 1) f = fine_face_average<D, 1, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
+          else f = fine_face_average<D, (D == 3 ? 2 : 1), LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
+          F[0] = f.rho;
+#pragma unroll
+          for (int d = 0; d < D; ++d) F[1 + d] = f.m[d];
+          F[NC - 1] = f.E;
+        } else {
+          int fi;
+          if (ax == 0) fi = (tz * TY + ty) * (TX + 1) + tx + (dir > 0);
+          else if (ax == 1) fi = K::NXF + (tz * (TY + 1) + ty + (dir > 0)) * TX + tx;
+          else fi = K::NXF + K::NYF + ((tz + (dir > 0)) * TY + ty) * TX + tx;
+#pragma unroll
+          for (int m = 0; m < NC; ++m) F[m] = fl[m * K::NF + fi];
+          nfb += ffb[fi];
+        }
+        if (dir < 0) {
+#pragma unroll
+          for (int m = 0; m < NC; ++m) rhs[m] = rhs[m] + F[m] * inv_dx;
+        } else {
+#pragma unroll
+          for (int m = 0; m < NC; ++m) rhs[m] = rhs[m] - F[m] * inv_dx;
+        }
+      }
+    }
+    Cons<D> q;
+    double o[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) {
+      o[m] = a.base[m * comp + own] + rhs[m] * a.sdt;
+      a.out[m * comp + own] = o[m];
+    }
+    if (a.post_check) {  // positivity of the completed step (mr_solver.cpp:290-297)
+      q.rho = o[0];
+#pragma unroll
+      for (int d = 0; d < D; ++d) q.m[d] = o[1 + d];
+      q.E = o[NC - 1];
+      if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
+    }
+  }
+  (void)ssum;
+  if (bad) atomicOr(&s_bad, bad);
+  if (nfb) atomicAdd(&s_fb, nfb);
+  block_max_atomic<K::NT>(wave, red, a.wave + l);
+  if (tid == 0) {
+    if (s_bad) {
+      // pass-1 failures stop every later launch; a post-step failure only
+      // stops the commit, so a pass-1 failure of a later level of the same
+      // stage (which the reference reports first) is still detected
+      atomicExch(a.err + ((s_bad & 1) ? 0 : 2), 1);
+      atomicMin(a.err + 1, a.step3 + ((s_bad & 1) ? a.stage - 1 : 2));
+    }
+    if (s_fb) atomicAdd(a.fb, (unsigned long long)s_fb);
+  }
+}
+
+// Tiles of level l holding at least one leaf (order irrelevant: every tile
+// writes only its own leaves).
+template <int D, int TX, int TY, int TZ>
+__global__ void mr_tile_list_kernel(const uint8_t* st, MRLevels g, int l, int* tiles,
+                                    int* count) {
+  const int n = 1 << l;
+  const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
+  const int ntz = D == 3 ? (n + TZ - 1) / TZ : 1;
+  const long ntiles = (long)ntx * nty * ntz;
+  const long off = g.cell_off[l];
+  for (long t = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32; t < ntiles;
+       t += (long)gridDim.x * (blockDim.x / 32)) {
+    const int x0 = (int)(t % ntx) * TX, y0 = (int)((t / ntx) % nty) * TY;
+    const int z0 = D == 3 ? (int)(t / ((long)ntx * nty)) * TZ : 0;
+    bool any = false;
+    for (int c = threadIdx.x & 31; c < TX * TY * TZ; c += 32) {
+      const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
+      if (x < n && y < n && (D == 2 || z < n) && st[off + mr_idx(D, n, x, y, z)] == ST_LEAF)
+        any = true;
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (any && (threadIdx.x & 31) == 0) tiles[atomicAdd(count, 1)] = (int)t;
+  }
+}
+
+}  // namespace af

@@ -1,0 +1,25 @@
+// af_mr_types.h — MR level geometry shared by host and device code.
+#pragma once
+
+#include <cstdint>
+
+namespace af {
+
+enum : uint8_t { ST_ABSENT = 0, ST_LEAF = 1, ST_INTERNAL = 2 };
+
+// Per-level geometry shared by all MR kernels.
+struct MRLevels {
+  int dim;
+  int L;
+  int nc;                  // stored components (4 in 2D, 5 in 3D)
+  int bc[6];
+  long cell_off[17];       // first cell of level l in the concatenated level arrays
+  long total_cells;
+  double inv_dx[17];       // 1 / dx_l, dx_l = extent / 2^l (mr_tree.hpp:73, mr_solver.cpp:181)
+};
+
+__host__ __device__ __forceinline__ long mr_cells(int dim, int l) {
+  return dim == 3 ? (1L << (3 * l)) : (1L << (2 * l));
+}
+
+}  // namespace af

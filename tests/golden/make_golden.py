@@ -30,8 +30,37 @@ UNIFORM = {
 }
 
 
+def eps_levels(eps, L, d):
+    return [eps * 2.0 ** (d * (l - L)) for l in range(L + 1)]
+
+
+# name: (kind, seed, level, steps, cfl, fixed_dt, eps, eps_level, min_leaf, local_time, gap,
+#        limiter, bc)
+MR = {
+    "mr_quad_L6_global": (0, 31, 6, 12, 0.5, 0.0, 1e-3, None, 0, 0, 3, O.MINMOD, None),
+    "mr_quad_L7_epsl_min3": (0, 32, 7, 12, 0.5, 0.0, 1e-3, eps_levels(1e-3, 7, 2), 3, 0, 3,
+                             O.MINMOD, None),
+    "mr_ell_L4_global": (2, 33, 4, 4, 0.4, 0.0, 1e-3, None, 0, 0, 3, O.MINMOD, None),
+}
+
+
 def main():
     O.build()
+    for name, (kind, seed, level, steps, cfl, fdt, eps, epsl, mleaf, lt, gap, lim,
+               bc) in MR.items():
+        dim = 3 if kind >= 2 else 2
+        init = O.case_fill(kind, seed, level)
+        p = O.make_params(dim, level, steps, cfl=cfl, fixed_dt=fdt, limiter=lim, bc=bc, eps=eps,
+                          eps_level=epsl, min_leaf_level=mleaf, local_time=lt, lt_gap=gap)
+        out, keys, cyc, dts, res = O.mr_run("ref", p, init)
+        assert res["err_kind"] == 0, res["err"]
+        np.savez_compressed(
+            os.path.join(HERE, name + ".npz"), kind=kind, seed=seed, level=level, steps=steps,
+            cfl=cfl, fixed_dt=fdt, eps=eps, has_eps_level=int(epsl is not None),
+            eps_level=np.array(epsl if epsl else [0.0]), min_leaf=mleaf, local_time=lt,
+            gap=gap, limiter=lim, bc=np.array(bc if bc else [0] * 6), out=out, keys=keys,
+            cycles=cyc, dt=dts, max_cfl=res["max_cfl"], fallbacks=res["fallbacks"])
+        print(name, len(keys), "leaves", res["max_cfl"])
     for name, (kind, seed, level, steps, cfl, fdt, lim, bc) in UNIFORM.items():
         dim = 3 if kind >= 2 else 2
         init = O.case_fill(kind, seed, level)
