@@ -33,7 +33,7 @@ enum af_case_kind {
   AF_CASE_QUADRANTS = 0,       /* cfg1/cfg2: seeded four-quadrant Riemann problem (2D) */
   AF_CASE_QUADRANTS_NOISE = 1, /* cfg3: quadrants + rho*(1 + 0.01*U[-1,1]) per cell (2D) */
   AF_CASE_ELLIPSOID = 2,       /* cfg4: axis-aligned ellipsoid blast, p 10 | 0.1 (3D) */
-  AF_CASE_ELLIPSOID_PRATIO = 3 /* cfg5: ellipsoid with p_in ~ U[10,100], p_out 0.1 (3D) */
+  AF_CASE_ELLIPSOID_PRATIO = 3 /* cfg5: ellipsoid, p_in/p_out ~ U[10,100], p_out 0.1 (3D) */
 };
 
 typedef struct af_rng {
@@ -96,7 +96,8 @@ static inline void af_case_draw(int kind, uint64_t seed, af_case_params* cp, af_
     }
   } else {
     for (int a = 0; a < 3; ++a) cp->semi[a] = af_rng_uniform(r, 0.1, 0.3);
-    if (kind == AF_CASE_ELLIPSOID_PRATIO) cp->p_in = af_rng_uniform(r, 10.0, 100.0);
+    /* cfg5: pressure RATIO p_in/p_out ~ U[10,100] with p_out = 0.1 */
+    if (kind == AF_CASE_ELLIPSOID_PRATIO) cp->p_in = cp->p_out * af_rng_uniform(r, 10.0, 100.0);
   }
 }
 

@@ -108,14 +108,18 @@ def test_mr_matches_golden(gpu_lib, path):
     compare(init, out, keys, rep, ref)
 
 
-def test_mr_nonphysical_message(gpu_lib, oracle):
+@pytest.mark.parametrize("kind,seed,level,steps,kw", [
+    (0, 7, 6, 30, dict(cfl=3.0, eps=1e-3)),
+    (2, 8, 5, 4, dict(cfl=2.0, eps=1e-3, min_leaf=2)),
+])
+def test_mr_nonphysical_message(gpu_lib, oracle, kind, seed, level, steps, kw):
     from paper_1603_05211_b200.errors import NonPhysicalState
     if not oracle.available("ref"):
         pytest.skip("reference build not present")
     from paper_1603_05211_b200 import uniform as U
-    init = U.case_fill(0, 7, 6)
-    ref = ref_mr(oracle, init, 0, 6, 30, cfl=3.0, eps=1e-3)
+    init = U.case_fill(kind, seed, level)
+    ref = ref_mr(oracle, init, kind, level, steps, **kw)
     assert ref[4]["err_kind"] == 1
     with pytest.raises(NonPhysicalState) as ei:
-        gpu_mr(0, 7, 6, 30, cfl=3.0, eps=1e-3)
+        gpu_mr(kind, seed, level, steps, **kw)
     assert str(ei.value) == ref[4]["err"]
