@@ -161,7 +161,14 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   AF_CUDA(cudaMalloc(&d_V_, vbytes));
   AF_CUDA(cudaMalloc(&d_Vs_, vbytes));
   AF_CUDA(cudaMalloc(&d_Qold_, vbytes));
-  if (o.local_time) AF_CUDA(cudaMalloc(&d_VQold_, vbytes));
+  if (o.local_time) {
+    AF_CUDA(cudaMalloc(&d_VQold_, vbytes));
+    AF_CUDA(cudaMalloc(&d_regbase_, sizeof(int) * tot));
+    AF_CUDA(cudaMalloc(&d_regmask_, tot));
+    AF_CUDA(cudaMalloc(&d_regcount_, sizeof(int)));
+    AF_CUDA(cudaMalloc(&d_regerr_, sizeof(int)));
+    AF_CUDA(cudaMalloc(&d_badkey_, sizeof(unsigned long long)));
+  }
   AF_CUDA(cudaMalloc(&d_det_, sizeof(double) * tot));
   AF_CUDA(cudaMalloc(&d_norms_, sizeof(double) * 5));
   AF_CUDA(cudaMalloc(&d_err_, 4 * sizeof(int)));
@@ -209,7 +216,9 @@ MR::~MR() {
   for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
                   (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
                   (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
-                  (void*)d_flagi_, (void*)d_red_})
+                  (void*)d_flagi_, (void*)d_red_, (void*)d_regbase_, (void*)d_regmask_,
+                  (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_,
+                  (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
     cudaFree(p);
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
@@ -317,6 +326,7 @@ void MR::build(const double* aos) {
 }
 
 void MR::refine(int top) {
+  registers_built_ = false;
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
   AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
   for (int l = 0; l <= L_ - 2; ++l)
@@ -427,9 +437,21 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   a.post_check = stage == 2;
   a.err = d_err_;
   a.lo = lo;
+  a.hi = hi;
   a.vmark = d_mark_;
   a.vq_old = d_VQold_;
-  for (int lv = 0; lv <= L_ && lv < 16; ++lv) {
+  a.reg_stage = stage == 2 && registers_built_;
+  a.step_dt = step_dt_;
+  a.share = D_ == 3 ? 0.25 : 0.5;  // mr_solver.cpp:239
+  a.sub = sub_;
+  a.regbase = d_regbase_;
+  a.regmask = d_regmask_;
+  a.regc = d_regc_;
+  a.regf = d_regf_;
+  a.regfc = d_regfc_;
+  a.regff = d_regff_;
+  a.regerr = d_regerr_;
+  for (int lv = 0; lv <= L_ && lv < 17; ++lv) {
     const double denom = t_new_[lv] - t_old_[lv];
     a.theta[lv] = denom > 0.0 ? std::clamp((tau - t_old_[lv]) / denom, 0.0, 1.0) : 1.0;
   }
@@ -472,8 +494,9 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   }
 }
 
-// MRSolver::step_levels (mr_solver.cpp:232-316).
-void MR::step_levels_(int lo, int hi, double t, double dt) {
+// MRSolver::step_levels (mr_solver.cpp:232-316). `sub` is which of the
+// parent's two substeps this call is (the fine register slot).
+void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
   const int top = std::min(hi, L_);
   snapshot_(lo, top);
   for (int l = lo; l <= top; ++l) {
@@ -487,9 +510,13 @@ void MR::step_levels_(int lo, int hi, double t, double dt) {
       AF_MR_LAUNCH(mr_virtual_snapshot, grid_for(mr_cells(D_, l)), d_V_, d_VQold_, d_st_,
                    d_mark_, g_, l);
   const size_t r0 = stage_records_.size();
+  step_dt_ = dt;
+  sub_ = sub;
   stage_(lo, top, t, 0.5 * dt, 1, cur_step_);
   project_range_(lo, top);
   predict_fill_(lo, top);
+  step_dt_ = dt;
+  sub_ = sub;
   stage_(lo, top, t + 0.5 * dt, dt, 2, cur_step_);
   project_range_(lo, top);
   predict_fill_(lo, top);
@@ -498,8 +525,8 @@ void MR::step_levels_(int lo, int hi, double t, double dt) {
   for (int l = top + 1; l <= L_; ++l) deeper = deeper || leaves_per_level_[l] > 0;
   if (deeper) {
     if (!opt_.local_time) throw Error(AF_E_CONFIG, "finer leaves outside the stepping set");
-    step_levels_(top + 1, top + 1, t, 0.5 * dt);
-    step_levels_(top + 1, top + 1, t + 0.5 * dt, 0.5 * dt);
+    step_levels_(top + 1, top + 1, t, 0.5 * dt, 0);
+    step_levels_(top + 1, top + 1, t + 0.5 * dt, 0.5 * dt, 1);
     apply_registers_(top);
     project_range_(lo, top + 1);
     predict_fill_(1, 0);
@@ -509,14 +536,15 @@ void MR::step_levels_(int lo, int hi, double t, double dt) {
 void MR::evolve_global(double dt, af_step_diag* d) {
   stage_records_.clear();
   build_tiles_();
-  step_levels_(0, L_, 0.0, dt);
+  step_levels_(0, L_, 0.0, dt, 0);
   collect_stage_records_(d);
 }
 
 void MR::advance_local(int top, double t, double dt, af_step_diag* d) {
   stage_records_.clear();
   build_tiles_();
-  step_levels_(0, top, t, dt);
+  if (opt_.local_time && !registers_built_) build_registers_(top);
+  step_levels_(0, top, t, dt, 0);
   collect_stage_records_(d);
 }
 
@@ -550,13 +578,47 @@ void MR::collect_stage_records_(af_step_diag* d) {
   }
 }
 
-// apply_registers (mr_solver.cpp:210-230) — local time stepping only.
+// Register slots for the leaves of levels [top, L-1] with an INTERNAL
+// neighbour (valid until the tree changes at the end of the cycle).
+void MR::build_registers_(int top) {
+  if (!d_regbase_) throw Error(AF_E_CONFIG, "registers need local_time");
+  AF_CUDA(cudaMemsetAsync(d_regmask_, 0, g_.total_cells, stream_));
+  AF_CUDA(cudaMemsetAsync(d_regcount_, 0, sizeof(int), stream_));
+  for (int l = std::max(top, 0); l <= L_ - 1; ++l)
+    AF_MR_LAUNCH(mr_reg_build_level, grid_for(mr_cells(D_, l)), d_st_, g_, l, d_regbase_,
+                 d_regmask_, d_regcount_);
+  int count = 0;
+  AF_CUDA(cudaMemcpyAsync(&count, d_regcount_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  if (count > reg_cap_) {
+    for (void* p : {(void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_}) cudaFree(p);
+    reg_cap_ = std::max<long>(count, 1024);
+    AF_CUDA(cudaMalloc(&d_regc_, sizeof(double) * NC_ * reg_cap_));
+    AF_CUDA(cudaMalloc(&d_regf_, sizeof(double) * NC_ * 8 * reg_cap_));
+    AF_CUDA(cudaMalloc(&d_regfc_, reg_cap_));
+    AF_CUDA(cudaMalloc(&d_regff_, reg_cap_));
+  }
+  if (reg_cap_) {
+    AF_CUDA(cudaMemsetAsync(d_regfc_, 0, reg_cap_, stream_));
+    AF_CUDA(cudaMemsetAsync(d_regff_, 0, reg_cap_, stream_));
+    AF_CUDA(cudaMemsetAsync(d_regf_, 0, sizeof(double) * NC_ * 8 * reg_cap_, stream_));
+  }
+  AF_CUDA(cudaMemsetAsync(d_regerr_, 0, sizeof(int), stream_));
+  AF_CUDA(cudaMemsetAsync(d_badkey_, 0xff, sizeof(unsigned long long), stream_));
+  registers_built_ = true;
+}
+
+// apply_registers (mr_solver.cpp:210-230) for the cells of `coarse_level`.
 void MR::apply_registers_(int coarse_level) {
-  (void)coarse_level;
-  throw Error(AF_E_UNSUPPORTED, "local time stepping registers are not implemented yet");
+  if (!registers_built_) return;
+  const double dx = cfg_.extent / static_cast<double>(1 << coarse_level);
+  AF_MR_LAUNCH(mr_reg_apply_level, grid_for(mr_cells(D_, coarse_level)), d_V_, d_st_, g_,
+               coarse_level, d_regbase_, d_regmask_, d_regc_, d_regf_, d_regfc_, d_regff_,
+               1.0 / dx, d_badkey_, d_err_);
 }
 
 void MR::coarsen() {
+  registers_built_ = false;
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
     for (int l = L_ - 1; l >= min_leaf_; --l)
@@ -575,6 +637,30 @@ void MR::check_error_(long step) {
   AF_CUDA(cudaMemcpyAsync(h, d_err_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
   if (!h[0] && !h[2]) return;
+  if (d_badkey_) {
+    unsigned long long bk = ~0ull;
+    int regerr = 0;
+    AF_CUDA(cudaMemcpy(&bk, d_badkey_, sizeof bk, cudaMemcpyDeviceToHost));
+    AF_CUDA(cudaMemcpy(&regerr, d_regerr_, sizeof regerr, cudaMemcpyDeviceToHost));
+    if (bk != ~0ull) {
+      const unsigned long long ck = bk >> 3;
+      const unsigned long long mask = (1ull << 15) - 1;
+      const std::string node = "level " + std::to_string(ck >> 45) + " (" +
+                               std::to_string((ck >> 30) & mask) + "," +
+                               std::to_string((ck >> 15) & mask) + "," +
+                               std::to_string(ck & mask) + ")";
+      std::memset(&last_, 0, sizeof(last_));
+      last_.status = AF_E_REGISTER_MISMATCH;
+      last_.step = step;
+      last_.level = (int)(ck >> 45);
+      std::snprintf(last_.message, sizeof last_.message,
+                    "interface flux register at %s is missing a side", node.c_str());
+      throw Error(AF_E_REGISTER_MISMATCH, last_.message);
+    }
+    if (regerr) throw Error(AF_E_REGISTER_MISMATCH, "flux register slot missing");
+  }
+  const int lvl_lo = h[3] ? ((h[3] - 1) >> 8) : 0;
+  const int lvl_hi = h[3] ? ((h[3] - 1) & 255) : L_;
   const int kind = h[1] % 3;  // 0/1 pass-1 of stage 1/2, 2 post-step
   const double* src = d_V_;
   std::vector<double> hv((size_t)NC_ * g_.total_cells);
@@ -591,7 +677,7 @@ void MR::check_error_(long step) {
   std::string msg = pre + "non-physical state";
   // leaves in ascending pack_key order: level, then i, then j, then k
   bool found = false;
-  for (int l = 0; l <= L_ && !found; ++l) {
+  for (int l = lvl_lo; l <= std::min(lvl_hi, L_) && !found; ++l) {
     const int n = 1 << l;
     const int nk = D_ == 3 ? n : 1;
     for (int i = 0; i < n && !found; ++i)
@@ -658,11 +744,13 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
     }
     const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
     cur_step_ = done;
+    if (opt_.local_time) build_registers_(top);
     if (opt_.local_time)
       advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
     else
       evolve_global(dt, nullptr);
     cur_step_ = -1;
+    registers_built_ = false;
     remove_virtual_leaves();
     coarsen();
     level_counts_();

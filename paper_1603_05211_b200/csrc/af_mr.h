@@ -45,7 +45,8 @@ class MR {
   void build_tiles_();
   void level_counts_();
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
-  void step_levels_(int lo, int hi, double t, double dt);
+  void step_levels_(int lo, int hi, double t, double dt, int sub);
+  void build_registers_(int top);
   void snapshot_(int lo, int hi);
   void check_error_(long step);
   void collect_stage_records_(af_step_diag* d);
@@ -78,6 +79,18 @@ class MR {
   int* d_tile_count_ = nullptr;
   int* d_err_ = nullptr;
   int* d_flagi_ = nullptr;
+  // flux registers (local time stepping)
+  int* d_regbase_ = nullptr;
+  uint8_t* d_regmask_ = nullptr;
+  double* d_regc_ = nullptr;
+  double* d_regf_ = nullptr;
+  uint8_t* d_regfc_ = nullptr;
+  uint8_t* d_regff_ = nullptr;
+  int* d_regcount_ = nullptr;
+  int* d_regerr_ = nullptr;
+  unsigned long long* d_badkey_ = nullptr;
+  long reg_cap_ = 0;
+  bool registers_built_ = false;
   unsigned long long* d_red_ = nullptr;  // scratch reductions
   std::vector<long> tile_off_;           // per-level offset into d_tiles_
   std::vector<int> tile_count_;
@@ -92,6 +105,8 @@ class MR {
   long fallbacks_ = 0;
   double max_wave_ = 0.0;
   long cur_step_ = 0;
+  double step_dt_ = 0.0;
+  int sub_ = 0;
   af_error last_{};
 };
 

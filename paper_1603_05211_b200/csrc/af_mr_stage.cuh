@@ -31,11 +31,29 @@ struct MRStageArgs {
   const int* tiles;
   // local time stepping: virtual leaves whose parent level is below `lo`
   // read as q_old*(1-theta) + q*theta (resolve, mr_solver.cpp:43-50)
-  int lo;
+  int lo, hi;
   const uint8_t* vmark;
   const double* vq_old;
-  double theta[16];  // by parent level
+  double theta[17];  // by parent level
+  // flux registers (face_flux_at, mr_solver.cpp:111-159; stage 2 only)
+  int reg_stage;
+  double step_dt, share;
+  int sub;                   // which of the two fine substeps (0/1)
+  const int* regbase;        // per cell: first register of the cell
+  const uint8_t* regmask;    // per cell: faces (axis*2+side) holding a register
+  double* regc;              // [R][NC] coarse provisional flux * step_dt
+  double* regf;              // [R][2 substeps][4 sub-faces][NC]
+  uint8_t* regfc;            // [R] has_coarse
+  uint8_t* regff;            // [R] has_fine
+  int* regerr;               // fine contribution without a register slot
 };
+
+__device__ __forceinline__ int reg_index(const int* base, const uint8_t* mask, long cell,
+                                         int bit) {
+  const unsigned m = mask[cell];
+  if (!((m >> bit) & 1u)) return -1;
+  return base[cell] + __popc(m & ((1u << bit) - 1u));
+}
 
 // resolve() for level l (mr_solver.cpp:36-57, global mode): bc-mapped read of
 // the dense level value with the reflective momentum flip.
@@ -316,9 +334,11 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         p[ax] += dir;
         bool flp;
         p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
-        const bool internal = a.st[off + mr_idx(D, n, p[0], p[1], p[2])] == ST_INTERNAL;
+        const long pcell = off + mr_idx(D, n, p[0], p[1], p[2]);
+        const uint8_t nst = a.st[pcell];
+        const bool internal = nst == ST_INTERNAL;
         double F[NC];
-        if (internal) {
+        if (internal && l + 1 <= a.hi) {
           Cons<D> f;
           if (ax == 0) f = fine_face_average<D, 0, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
           else if (ax == 1) f = fine_face_average<D, 1, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
@@ -335,6 +355,40 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
 #pragma unroll
           for (int m = 0; m < NC; ++m) F[m] = fl[m * K::NF + fi];
           nfb += ffb[fi];
+          if (a.reg_stage) {
+            if (internal) {
+              // finer neighbour advancing later: provisional flux, coarse register
+              const int R = reg_index(a.regbase, a.regmask, own, ax * 2 + (dir > 0));
+              if (R >= 0) {
+#pragma unroll
+                for (int m = 0; m < NC; ++m) a.regc[(long)R * NC + m] = F[m] * a.step_dt;
+                a.regfc[R] = 1;
+              } else {
+                atomicExch(a.regerr, 1);
+              }
+            } else if (nst == ST_ABSENT && l >= 1 && l - 1 < a.lo) {
+              const int pn = n >> 1;
+              const long pc = g.cell_off[l - 1] + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+              if (a.vmark[pc]) {
+                // face into an already-advanced coarser cell: fine register share
+                const int R = reg_index(a.regbase, a.regmask, pc, ax * 2 + (dir > 0 ? 0 : 1));
+                if (R >= 0) {
+                  // sub-face slot in ascending pack_key order of the fine cells
+                  int t = 0;
+#pragma unroll
+                  for (int b = 0; b < D; ++b)
+                    if (b != ax) t = 2 * t + (c[b] & 1);
+                  const double w = a.step_dt * a.share;
+                  double* dst = a.regf + (((long)R * 2 + a.sub) * 4 + t) * NC;
+#pragma unroll
+                  for (int m = 0; m < NC; ++m) dst[m] = F[m] * w;
+                  a.regff[R] = 1;
+                } else {
+                  atomicExch(a.regerr, 1);
+                }
+              }
+            }
+          }
         }
         if (dir < 0) {
 #pragma unroll
@@ -371,8 +425,96 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       // stage (which the reference reports first) is still detected
       atomicExch(a.err + ((s_bad & 1) ? 0 : 2), 1);
       atomicMin(a.err + 1, a.step3 + ((s_bad & 1) ? a.stage - 1 : 2));
+      atomicCAS(a.err + 3, 0, ((a.lo << 8) | a.hi) + 1);
     }
     if (s_fb) atomicAdd(a.fb, (unsigned long long)s_fb);
+  }
+}
+
+// Register faces of the leaves of level l: faces whose same-level (bc-mapped)
+// neighbour is INTERNAL. Each gets a slot for the coarse provisional flux and
+// the 2 x 2^(d-1) fine contributions (registers_, mr_solver.cpp:17-20).
+template <int D>
+__global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* regbase,
+                                   uint8_t* regmask, int* count) {
+  const int n = 1 << l;
+  const long cells = mr_cells(D, l), off = g.cell_off[l];
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    unsigned mask = 0;
+    if (st[off + c] == ST_LEAF) {
+      const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+      for (int ax = 0; ax < D; ++ax)
+        for (int side = 0; side < 2; ++side) {
+          int p[3] = {idx[0], idx[1], idx[2]};
+          p[ax] += side ? 1 : -1;
+          bool fl;
+          p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], fl);
+          if (st[off + mr_idx(D, n, p[0], p[1], p[2])] == ST_INTERNAL) mask |= 1u << (ax * 2 + side);
+        }
+    }
+    regmask[off + c] = (uint8_t)mask;
+    if (mask) regbase[off + c] = atomicAdd(count, __popc(mask));
+  }
+}
+
+// apply_registers (mr_solver.cpp:210-230) for the leaves of level l: each
+// cell applies its faces in ascending (axis, side) order; the fine sum runs
+// substep 1 then 2, sub-faces in ascending key order (the reference's visit
+// order). Missing sides raise RegisterMismatch (min face key recorded).
+template <int D>
+__global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int l,
+                                   const int* regbase, const uint8_t* regmask, const double* regc,
+                                   const double* regf, uint8_t* regfc, uint8_t* regff,
+                                   double inv_sign_dx, unsigned long long* bad_key, int* err) {
+  constexpr int NC = D + 2;
+  if (failed_before(err)) return;
+  const int n = 1 << l;
+  const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
+  const int nsub = D == 3 ? 4 : 2;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+       c += (long)gridDim.x * blockDim.x) {
+    const unsigned mask = regmask[off + c];
+    if (!mask) continue;
+    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    const unsigned long long key = ((unsigned long long)l << 45) |
+                                   ((unsigned long long)idx[0] << 30) |
+                                   ((unsigned long long)idx[1] << 15) | (unsigned long long)idx[2];
+    double q[NC];
+#pragma unroll
+    for (int m = 0; m < NC; ++m) q[m] = V[m * comp + off + c];
+    int R = regbase[off + c];
+    bool ok = true;
+    for (int bit = 0; bit < 2 * D; ++bit) {
+      if (!((mask >> bit) & 1u)) continue;
+      const bool hc = regfc[R], hf = regff[R];
+      if (!hc && !hf) {  // never touched this cycle step: no register entry
+        ++R;
+        continue;
+      }
+      if (!hc || !hf) {
+        atomicMin(bad_key, (key << 3) | bit);
+        atomicExch(err, 1);  // RegisterMismatch: stop every later launch
+        ok = false;
+        break;
+      }
+      const double sgn = (bit & 1) ? 1.0 : -1.0;
+      const double s = sgn * inv_sign_dx;  // == sign / dx (dx a power of two)
+#pragma unroll
+      for (int m = 0; m < NC; ++m) {
+        double f = 0.0;
+        for (int sub = 0; sub < 2; ++sub)
+          for (int t = 0; t < nsub; ++t) f = f + regf[(((long)R * 2 + sub) * 4 + t) * NC + m];
+        q[m] = q[m] + (regc[(long)R * NC + m] - f) * s;
+      }
+      regfc[R] = 0;
+      regff[R] = 0;
+      ++R;
+    }
+    if (ok) {
+#pragma unroll
+      for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
+    }
   }
 }
 

@@ -41,6 +41,8 @@ MR = {
     "mr_quad_L7_epsl_min3": (0, 32, 7, 12, 0.5, 0.0, 1e-3, eps_levels(1e-3, 7, 2), 3, 0, 3,
                              O.MINMOD, None),
     "mr_ell_L4_global": (2, 33, 4, 4, 0.4, 0.0, 1e-3, None, 0, 0, 3, O.MINMOD, None),
+    "mr_quad_L6_lt": (0, 34, 6, 16, 0.5, 0.0, 1e-3, None, 0, 1, 3, O.MINMOD, None),
+    "mr_noise_L7_lt": (1, 35, 7, 8, 0.5, 0.0, 1e-3, None, 0, 1, 3, O.MINMOD, None),
 }
 
 

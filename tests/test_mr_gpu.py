@@ -83,6 +83,26 @@ def test_mr_global_matches_reference(gpu_lib, oracle, kind, seed, level, steps, 
     compare(init, out, keys, rep, ref_mr(oracle, init, kind, level, steps, **kw))
 
 
+CASES_LT = [
+    (0, 41, 6, 16, dict(eps=1e-3, local_time=True)),
+    (1, 42, 7, 16, dict(eps=1e-3, local_time=True)),                       # cfg3 generator
+    (0, 44, 7, 16, dict(eps=1e-3, local_time=True, gap=2, bc=[1] * 6)),
+    (0, 45, 7, 12, dict(eps=2e-3, local_time=True, gap=4, limiter=0)),
+    (2, 43, 5, 8, dict(eps=1e-3, cfl=0.4, local_time=True)),
+    (3, 46, 5, 8, dict(eps=1e-3, cfl=0.4, local_time=True, gap=3,
+                       eps_level=eps_levels(1e-3, 5, 3), min_leaf=1)),        # cfg5 rule
+]
+
+
+@pytest.mark.parametrize("kind,seed,level,steps,kw", CASES_LT,
+                         ids=[f"k{c[0]}_L{c[2]}_{i}" for i, c in enumerate(CASES_LT)])
+def test_mr_local_time_matches_reference(gpu_lib, oracle, kind, seed, level, steps, kw):
+    if not oracle.available("ref"):
+        pytest.skip("reference build not present; golden fixtures cover MRLT")
+    init, out, keys, rep = gpu_mr(kind, seed, level, steps, **kw)
+    compare(init, out, keys, rep, ref_mr(oracle, init, kind, level, steps, **kw))
+
+
 def test_mr_eps0_equals_uniform(gpu_lib):
     """with eps = 0 the MR solver is the uniform FV solver (bitwise)."""
     from paper_1603_05211_b200 import uniform as U
