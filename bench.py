@@ -35,9 +35,24 @@ UNIT = "cell-updates/s"
 
 WORKLOADS = {
     # name: (BASELINE config index, case kind, dim, level, cfl, seed, steps in the config)
-    "cfg4": (3, 2, 3, 9, 0.4, 1, 100),
     "cfg1": (0, 0, 2, 8, 0.5, 1, 200),
+    "cfg2": (1, 0, 2, 10, 0.5, 1, 500),
+    "cfg3": (2, 1, 2, 13, 0.5, 1, 64),
+    "cfg4": (3, 2, 3, 9, 0.4, 1, 100),
 }
+# MR options per MR workload (BASELINE.json configs[1], configs[2])
+MR_OPTS = {
+    "cfg2": dict(eps=1e-3, eps_scaled=True, min_leaf=3, local_time=False, gap=3),
+    "cfg3": dict(eps=1e-3, eps_scaled=False, min_leaf=0, local_time=True, gap=3),
+}
+
+
+def mr_options(workload):
+    o = MR_OPTS[workload]
+    _, _, dim, level, _, _, _ = WORKLOADS[workload]
+    epsl = ([o["eps"] * 2.0 ** (dim * (l - level)) for l in range(level + 1)]
+            if o["eps_scaled"] else None)
+    return o, epsl
 
 
 def peaks():
@@ -113,16 +128,45 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
     reference is single-threaded). Returns (rate, sample description)."""
     from oracle import oracle as O
     _, case, dim, level, cfl, seed, _ = WORKLOADS[workload]
-    lvl = level_override if level_override is not None else (7 if dim == 3 else level)
+    is_mr = workload in MR_OPTS
+    if level_override is not None:
+        lvl = level_override
+    elif is_mr:
+        # The reference's from_uniform + coarsen (its recursive predictions)
+        # takes minutes at L >= 8 for cfg2's level thresholds, so the bounded
+        # sample uses L=7 (cfg2) / L=8 (cfg3); the timed loop excludes the build.
+        lvl = {"cfg2": 7, "cfg3": 8}[workload]
+    else:
+        lvl = 7 if dim == 3 else level
     init = O.case_fill(case, seed, lvl)
     cells = init.shape[0]
     lib_kind = "ref" if kind == "reference" else "port"
     results = [None] * threads
+    work = [0] * threads
+
+    def params(n):
+        if not is_mr:
+            return O.make_params(dim, lvl, n, cfl=cfl)
+        o = MR_OPTS[workload]
+        epsl = ([o["eps"] * 2.0 ** (dim * (l - lvl)) for l in range(lvl + 1)]
+                if o["eps_scaled"] else None)
+        return O.make_params(dim, lvl, n, cfl=cfl, eps=o["eps"], eps_level=epsl,
+                             min_leaf_level=o["min_leaf"], local_time=o["local_time"],
+                             lt_gap=o["gap"])
 
     def one(i):
-        if warmup:
-            O.uniform_run(lib_kind, O.make_params(dim, lvl, warmup, cfl=cfl), init)
-        _, _, res = O.uniform_run(lib_kind, O.make_params(dim, lvl, steps, cfl=cfl), init)
+        if is_mr:
+            # warm-up cycles then the timed cycles, continuing is not exposed by
+            # the harness: time `steps` cycles from the start after a warm-up run
+            if warmup:
+                O.mr_run(lib_kind, params(warmup), init)
+            _, _, cyc, _, res = O.mr_run(lib_kind, params(steps), init)
+            work[i] = int(cyc[:, 4].sum())
+        else:
+            if warmup:
+                O.uniform_run(lib_kind, params(warmup), init)
+            _, _, res = O.uniform_run(lib_kind, params(steps), init)
+            work[i] = cells * 2 * steps
         results[i] = res
 
     ts = [threading.Thread(target=one, args=(i,)) for i in range(threads)]
@@ -131,10 +175,12 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
     for t in ts:
         t.join()
     wall = max(r["wall_seconds"] for r in results)
-    rate = threads * cells * 2 * steps / wall
+    rate = sum(work) / wall
+    what = "MR cycles (refine/evolve/coarsen)" if is_mr else "RK2 steps"
     sample = (f"{threads} independent single-threaded copies of the {workload} generator at "
-              f"level {lvl} ({cells} cells), {steps} RK2 steps each after {warmup} warm-up "
-              f"steps; steady_clock around the step loop (unigrid.cpp:31-48)")
+              f"level {lvl} ({cells} finest cells), {steps} {what} each after {warmup} "
+              f"warm-up; steady_clock around the step loop only (unigrid.cpp:31-48, "
+              f"mr_solver.cpp:339-395); value = leaf-cell RK-stage updates / s")
     return rate, sample, wall
 
 
@@ -168,13 +214,24 @@ def run_reference_arm(args, rank, world):
 def workload_config(workload, n_gpus):
     idx, case, dim, level, cfl, seed, steps = WORKLOADS[workload]
     n = 1 << level
-    return {"workload": f"{workload}: BASELINE.json configs[{idx}]",
-            "mesh": "x".join([str(n)] * dim), "dim": dim, "scheme": "AUSM+/minmod/RK2",
-            "cfl": cfl, "cfl_rule": "dt = cfl*dx / max_cells sum_a(|v_a|+c)", "seed": seed,
-            "bc": "outflow", "decomposition": f"{n_gpus} slab(s) along the last axis",
-            "l2": "inputs larger than L2 (no flush)" if (n ** dim) * 40 > 126e6
-                  else "working set fits in L2 (latency-bound config)",
-            "parity_mode": "bit-exact (--fmad=false)"}
+    c = {"workload": f"{workload}: BASELINE.json configs[{idx}]",
+         "mesh": "x".join([str(n)] * dim), "dim": dim, "scheme": "AUSM+/minmod/RK2",
+         "cfl": cfl, "cfl_rule": "dt_L = cfl*dx_L / max_leaves sum_a(|v_a|+c)", "seed": seed,
+         "bc": "outflow",
+         "l2": "inputs larger than L2 (no flush)" if (n ** dim) * 40 > 126e6
+               else "working set fits in L2 (latency-bound config)",
+         "parity_mode": "bit-exact (--fmad=false)"}
+    if workload in MR_OPTS:
+        o = MR_OPTS[workload]
+        c.update({"method": "MRLT" if o["local_time"] else "MR (global dt)",
+                  "finest_level": level, "min_leaf_level": o["min_leaf"],
+                  "eps": ("1e-3*2^(d(l-L))" if o["eps_scaled"] else o["eps"]),
+                  "lt_gap": o["gap"] if o["local_time"] else None,
+                  "step": "one MR cycle (refine, virtual leaves, evolve, coarsen)",
+                  "decomposition": "single GPU (per-level dense grids)"})
+    else:
+        c["decomposition"] = f"{n_gpus} slab(s) along the last axis"
+    return c
 
 
 # ----------------------------------------------------------------- GPU arm --
@@ -184,7 +241,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-threads", type=int, default=8)
     ap.add_argument("--ref-level", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -223,6 +280,20 @@ def main():
         assert st == 0, "af_comm_create failed"
         comm = h
 
+    if args.workload in MR_OPTS:
+        line = mr_bench(args, rank, world, local, torch, dist)
+    else:
+        line = uniform_bench(args, rank, world, local, comm, torch, dist)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def uniform_bench(args, rank, world, local, comm, torch, dist):
+    from paper_1603_05211_b200 import uniform as U
+    idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
     solver = U.UniformSolver(dim, level, scheme=U.SchemeConfig(limiter=U.MINMOD),
                              device=local, comm=comm)
     # A dedicated (non-default) stream: the solver's kernels and the timing
@@ -288,10 +359,7 @@ def main():
                        "pinned host memory, K steps, download of the final state"}
 
     if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+        return None
 
     # ---- roofline of the dominant kernel (the fused RK2 stage) ---------------
     hbm, src = peaks()
@@ -332,10 +400,121 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return line
+
+
+
+
+def mr_bench(args, rank, world, local, torch, dist):
+    """MR / MRLT workloads (cfg2, cfg3). A step = one macro cycle of run_mr
+    (refine, virtual leaves, evolve, coarsen); value = leaf-cell RK-stage
+    updates actually performed / s. Multi-GPU: independent replicas (the MR
+    domain decomposition of SURVEY §8(e) is not built yet) -> weak scaling."""
+    from paper_1603_05211_b200 import mr as M
+    from paper_1603_05211_b200 import uniform as U
+    idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
+    o, epsl = mr_options(args.workload)
+    opts = M.MROptions(epsilon=o["eps"], eps_level=epsl, min_leaf_level=o["min_leaf"],
+                       local_time=o["local_time"], local_time_level_gap=o["gap"])
+    solver = M.MRSolver(dim, level, opts, scheme=U.SchemeConfig(limiter=U.MINMOD), device=local)
+    stream = torch.cuda.Stream(device=local)
+    solver.set_stream(stream)
+    init_host = U.case_fill(case, seed, level)
+    init_pinned = torch.from_numpy(init_host).pin_memory()
+    init_dev = init_pinned.to(f"cuda:{local}")
+    out_pinned = torch.empty_like(init_pinned).pin_memory()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def reduce(x, op):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    # ---- device-resident throughput ------------------------------------------
+    solver.build(init_dev)
+    if args.warmup:
+        solver.run(args.warmup, cfl=cfl)        # W untimed warm-up cycles
+    l0 = solver.kernel_launches()
+    solver.profile(True)
+    sampler = ClockSampler(local)
+    barrier()
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = solver.run(args.steps, cfl=cfl)
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = reduce(e0.elapsed_time(e1), dist.ReduceOp.MAX if world > 1 else None)
+    launches = solver.kernel_launches() - l0
+    stage_ms, stage_launches, stage_updates = solver.stage_stats()
+    solver.profile(False)
+    updates = reduce(float(rep.updates), dist.ReduceOp.SUM if world > 1 else None)
+    value = updates / (ms / 1e3)
+
+    # ---- end to end: pinned host input -> build -> K cycles -> to_uniform ----
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        solver.build(init_pinned.numpy())
+        rep2 = solver.run(args.steps, cfl=cfl)
+        solver._check(solver._lib.af_mr_to_uniform(
+            solver._h, level, __import__("ctypes").c_void_p(out_pinned.data_ptr())))
+        t1.record(stream)
+        barrier()
+        ems = reduce(t0.elapsed_time(t1), dist.ReduceOp.MAX if world > 1 else None)
+        upd2 = reduce(float(rep2.updates), dist.ReduceOp.SUM if world > 1 else None)
+        nbytes = init_host.nbytes
+        e2e = {"value": upd2 / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(nbytes * world / args.steps),
+               "d2h_bytes_per_step": int(nbytes * world / args.steps),
+               "what": "one run_mr-equivalent call: build from the pinned host initial state, "
+                       "K cycles, to_uniform(L) download to pinned host"}
+    if rank != 0:
+        return None
+
+    hbm, src = peaks()
+    S = (dim + 2) * 8
+    # stage kernels: 2.5 S per leaf-cell stage (SURVEY §8(d)), timed live by
+    # CUDA events around each stage's launches on the solver stream
+    achieved = 2.5 * S * stage_updates / (stage_ms / 1e3) / 1e9 if stage_ms > 0 else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "peak_source": src, "kernel": "mr_stage_kernel",
+            "kernel_share_of_step": stage_ms / ms if ms > 0 else None,
+            "stage_launches": stage_launches,
+            "note": "per-launch average over the timed region; the MR cycle also runs "
+                    "refine/coarsen/projection/prediction kernels and host decisions"}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import oracle as O
+            kind = "reference" if O.available("ref") else "port"
+            threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+            rate, sample, _ = reference_cpu_rate(kind, args.workload, 8, 2, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {e}"}
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(args.workload, world),
+                       leaves_last_cycle=int(rep.cycles[-1, 0]) if len(rep.cycles) else None,
+                       replicas=world),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks,
+    }
 
 
 if __name__ == "__main__":

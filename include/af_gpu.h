@@ -181,6 +181,8 @@ typedef struct af_mr_cycle {
   long sub;      /* finest steps in this cycle (LT), 1 for MR */
   int top;       /* LT top level (L for MR) */
   double dt;     /* finest-level step size dt_L */
+  long updates;  /* leaf-cell RK-stage updates actually performed in the cycle:
+                    2 * sum_l leaves_l * max(1, 2^(l - top)) */
 } af_mr_cycle;
 
 af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** out);
@@ -210,6 +212,11 @@ af_status af_mr_leaf_keys(af_mr* m, uint64_t* keys, size_t* n);
 af_status af_mr_to_uniform(af_mr* m, int level, double* aos);
 /* detail() of every node at `level` (NaN where the node is not internal). */
 af_status af_mr_details(af_mr* m, int level, double* out);
+/* Stage-kernel timing (CUDA events around every stage's kernel launches on
+ * the solver stream): enable, then read the accumulated device time, the
+ * number of stage-kernel launches and of leaf-cell stage updates. */
+af_status af_mr_profile(af_mr* m, int enable);
+af_status af_mr_stage_stats(af_mr* m, double* ms, long* launches, long* updates);
 af_status af_mr_last_error(const af_mr* m, af_error* err);
 af_status af_mr_kernel_launches(const af_mr* m, long* count);
 

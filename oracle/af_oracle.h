@@ -67,7 +67,7 @@ int afo_uniform_run(const af_oracle_params* p, const double* init, double* out,
  * MR / MRLT run (mr_solver.cpp:318-400 loop). out: to_uniform(L) of the final
  * tree (n^dim*5). leaf_keys: sorted pack_key leaves of the final tree
  * (capacity *n_leaves on entry, count on exit; nullable). per_cycle: for each
- * macro cycle {leaves, nodes incl. virtual, sub, top} as 4 longs (capacity
+ * macro cycle {leaves, nodes incl. virtual, sub, top, leaf-stage updates} as 5 longs (capacity
  * max_cycles; nullable). dt_hist: dt_L per cycle (nullable).
  */
 int afref_mr_run(const af_oracle_params* p, const double* init, double* out,

@@ -139,7 +139,7 @@ def mr_run(kind: str, params: Params, init: np.ndarray, max_cycles: int | None =
     lib = _load(kind)
     out = np.zeros_like(init)
     max_cycles = params.n_steps if max_cycles is None else max_cycles
-    per_cycle = np.zeros((max_cycles, 4), dtype=np.int64)
+    per_cycle = np.zeros((max_cycles, 5), dtype=np.int64)
     dts = np.zeros(max_cycles, dtype=np.float64)
     cap = init.shape[0] + 1
     keys = np.zeros(cap, dtype=np.uint64)

@@ -53,7 +53,7 @@ class MROptions(C.Structure):
 
 class MRCycle(C.Structure):
     _fields_ = [("leaves", C.c_long), ("nodes", C.c_long), ("sub", C.c_long), ("top", C.c_int),
-                ("dt", C.c_double)]
+                ("dt", C.c_double), ("updates", C.c_long)]
 
 
 # name -> (restype, argtypes); the complete exported surface of af_gpu.h
@@ -98,6 +98,9 @@ SIGNATURES = {
     "af_mr_leaf_keys": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_size_t)]),
     "af_mr_to_uniform": (C.c_int, [_vp, C.c_int, _vp]),
     "af_mr_details": (C.c_int, [_vp, C.c_int, _vp]),
+    "af_mr_profile": (C.c_int, [_vp, C.c_int]),
+    "af_mr_stage_stats": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_long),
+                                    C.POINTER(C.c_long)]),
     "af_mr_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
     "af_mr_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
 }

@@ -251,6 +251,10 @@ af_status af_mr_details(af_mr* m, int level, double* out) {
     m->impl->details(level, out);
   });
 }
+af_status af_mr_profile(af_mr* m, int enable) { AF_M_GUARD(m->impl->profile(enable != 0)); }
+af_status af_mr_stage_stats(af_mr* m, double* ms, long* launches, long* updates) {
+  AF_M_GUARD(m->impl->stage_stats(ms, launches, updates));
+}
 af_status af_mr_last_error(const af_mr* m, af_error* err) {
   if (!err) return AF_E_ARGUMENT;
   *err = (m && m->impl) ? m->impl->last_error() : g_last;

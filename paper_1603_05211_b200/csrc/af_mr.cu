@@ -213,6 +213,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
 MR::~MR() {
   cudaSetDevice(cfg_.device);
   if (own_stream_) cudaStreamSynchronize(own_stream_);
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
                   (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
                   (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
@@ -463,8 +464,21 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   AF_CUDA(cudaMemsetAsync(wave, 0, sizeof(unsigned long long) * 17, stream_));
   a.wave = wave;
   a.fb = fb;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (profile_) {
+    while (ev_pool_.size() < ev_used_ + 2) {
+      cudaEvent_t e;
+      AF_CUDA(cudaEventCreate(&e));
+      ev_pool_.push_back(e);
+    }
+    e0 = ev_pool_[ev_used_++];
+    e1 = ev_pool_[ev_used_++];
+    AF_CUDA(cudaEventRecord(e0, stream_));
+  }
   for (int l = lo; l <= std::min(hi, L_); ++l) {
     if (!tile_count_[l]) continue;
+    stage_launches_ += profile_ ? 1 : 0;
+    stage_updates_ += profile_ ? leaves_per_level_[l] : 0;
     a.tiles = d_tiles_ + tile_off_[l];
     const int lim = cfg_.limiter;
     if (D_ == 2) {
@@ -485,6 +499,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     ++launches_;
     AF_CUDA(cudaGetLastError());
   }
+  if (profile_) AF_CUDA(cudaEventRecord(e1, stream_));
   for (int l = lo; l <= std::min(hi, L_); ++l) {
     if (!leaves_per_level_[l]) continue;
     mr_copy_leaves<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
@@ -550,8 +565,34 @@ void MR::advance_local(int top, double t, double dt, af_step_diag* d) {
 
 // Reads the per-stage wave/fallback records of the last evolve and folds
 // them into the MRSolver accumulators (mr_solver.cpp:176-178); checks errors.
+void MR::profile(bool on) {
+  profile_ = on;
+  stage_ms_ = 0.0;
+  stage_launches_ = 0;
+  stage_updates_ = 0;
+}
+
+void MR::harvest_events_() {
+  if (!ev_used_) return;
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  for (size_t e = 0; e + 1 < ev_used_; e += 2) {
+    float ms = 0.f;
+    AF_CUDA(cudaEventElapsedTime(&ms, ev_pool_[e], ev_pool_[e + 1]));
+    stage_ms_ += ms;
+  }
+  ev_used_ = 0;
+}
+
+void MR::stage_stats(double* ms, long* launches, long* updates) {
+  harvest_events_();
+  if (ms) *ms = stage_ms_;
+  if (launches) *launches = stage_launches_;
+  if (updates) *updates = stage_updates_;
+}
+
 void MR::collect_stage_records_(af_step_diag* d) {
   check_error_(cur_step_);
+  harvest_events_();
   const size_t ns = stage_records_.size();
   if (!ns) return;
   std::vector<unsigned long long> h(ns * 17);
@@ -741,6 +782,10 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
       cycles[cycle].sub = sub;
       cycles[cycle].top = top;
       cycles[cycle].dt = dt;
+      long upd = 0;
+      for (int l = 0; l <= L_; ++l)
+        upd += 2 * leaves_per_level_[l] * (l > top ? (1L << (l - top)) : 1L);
+      cycles[cycle].updates = upd;
     }
     const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
     cur_step_ = done;

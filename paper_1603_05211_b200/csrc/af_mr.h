@@ -37,6 +37,8 @@ class MR {
   double leaf_speed_sum();
 
   long launches() const { return launches_; }
+  void profile(bool on);
+  void stage_stats(double* ms, long* launches, long* updates);
   af_error& last_error() { return last_; }
 
  private:
@@ -105,6 +107,13 @@ class MR {
   long fallbacks_ = 0;
   double max_wave_ = 0.0;
   long cur_step_ = 0;
+  // stage-kernel timing
+  bool profile_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_used_ = 0;
+  double stage_ms_ = 0.0;
+  long stage_launches_ = 0, stage_updates_ = 0;
+  void harvest_events_();
   double step_dt_ = 0.0;
   int sub_ = 0;
   af_error last_{};

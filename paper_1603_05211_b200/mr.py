@@ -39,7 +39,12 @@ class MRReport:
     max_cfl: float = 0.0
     fallbacks: int = 0
     t: float = 0.0
-    cycles: np.ndarray = field(default_factory=lambda: np.zeros((0, 5)))
+    cycles: np.ndarray = field(default_factory=lambda: np.zeros((0, 6)))
+
+    @property
+    def updates(self) -> int:
+        """leaf-cell RK-stage updates performed (the bench metric's numerator)"""
+        return int(self.cycles[:, 5].sum())
 
     @property
     def leaves_per_step(self):
@@ -117,6 +122,16 @@ class MRSolver:
         self._lib.af_mr_kernel_launches(self._h, C.byref(c))
         return c.value
 
+    def profile(self, enable: bool = True) -> None:
+        """Times every stage's kernels with CUDA events on the solver stream."""
+        self._check(self._lib.af_mr_profile(self._h, int(enable)))
+
+    def stage_stats(self):
+        """(stage-kernel device ms, stage launches, leaf-cell stage updates)."""
+        ms, la, up = C.c_double(), C.c_long(), C.c_long()
+        self._check(self._lib.af_mr_stage_stats(self._h, C.byref(ms), C.byref(la), C.byref(up)))
+        return ms.value, la.value, up.value
+
     # MRTree
     def build(self, aos) -> None:
         self._check(self._lib.af_mr_build(self._h, C.c_void_p(_ptr(aos))))
@@ -188,7 +203,7 @@ class MRSolver:
         for c in cyc:
             if c.sub == 0:
                 break
-            rows.append((c.leaves, c.nodes, c.sub, c.top, c.dt))
+            rows.append((c.leaves, c.nodes, c.sub, c.top, c.dt, c.updates))
             nc += 1
         return MRReport(n_steps=d.steps_done, max_cfl=d.max_cfl, fallbacks=d.fallbacks, t=d.t,
-                        cycles=np.array(rows, dtype=np.float64).reshape(-1, 5))
+                        cycles=np.array(rows, dtype=np.float64).reshape(-1, 6))

@@ -55,6 +55,7 @@ def compare(init, out, keys, rep, ref):
     assert np.array_equal(rcyc[:, 1], rep.cycles[:, 1].astype(np.int64)), "nodes per cycle"
     assert np.array_equal(rcyc[:, 2], rep.cycles[:, 2].astype(np.int64)), "sub per cycle"
     assert np.array_equal(bits(rdt), bits(rep.cycles[:, 4])), "dt per cycle"
+    assert np.array_equal(rcyc[:, 4], rep.cycles[:, 5].astype(np.int64)), "updates per cycle"
     assert np.array_equal(rkeys, keys), "final leaf set"
     assert np.array_equal(bits(rout), bits(out)), "to_uniform(L) state"
     assert rep.max_cfl == rres["max_cfl"]
