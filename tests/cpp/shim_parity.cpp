@@ -1,0 +1,107 @@
+// shim_parity.cpp — drop-in check: the reference's own entry points
+// (run_uniform, run_mr on its built-in cases lax_liu_6 / ellipsoid3d, fixed
+// dt = t_end / n_steps) against the same calls through the C++ shim
+// (paper_1603_05211_b200/host/adaptflow_gpu.hpp -> libafgpu.so). Built by
+// `make -C oracle shim` (needs the reference headers; the binary travels to
+// the GPU box) and run by tests/test_shim_gpu.py. Exit 0 iff every check is
+// bit-identical.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "adaptflow_gpu.hpp"
+
+using namespace adaptflow;
+
+static int failures = 0;
+
+static bool same_grid(const UniformGrid& a, const UniformGrid& b) {
+  bool ok = true;
+  a.block().for_interior([&](int i, int j, int k) {
+    const ConservedState& x = a.block().at(i, j, k);
+    const ConservedState& y = b.block().at(i, j, k);
+    const double xa[5] = {x.rho, x.mom[0], x.mom[1], x.mom[2], x.rhoE};
+    const double ya[5] = {y.rho, y.mom[0], y.mom[1], y.mom[2], y.rhoE};
+    for (int m = 0; m < 5; ++m)
+      if (!(xa[m] == ya[m])) ok = false;  // +0 == -0
+  });
+  return ok;
+}
+
+static void report(const std::string& what, bool ok) {
+  std::printf("%s %s\n", ok ? "OK  " : "FAIL", what.c_str());
+  if (!ok) ++failures;
+}
+
+int main() {
+  std::setvbuf(stdout, nullptr, _IONBF, 0);
+  // Uniform FV: lax_liu_6 (MR preset AUSM+/van Albada/RK2), ellipsoid3d.
+  {
+    const CaseSpec& s = find_case("lax_liu_6");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 7;
+    const long n = s.steps_for_level(L);
+    UniformRunResult r = run_uniform(s, L, n, sc);
+    UniformRunResult g = gpu::run_uniform(s, L, n, sc);
+    report("run_uniform lax_liu_6 L=7 state", same_grid(r.grid, g.grid));
+    report("run_uniform lax_liu_6 L=7 max_cfl", r.report.max_cfl == g.report.max_cfl);
+  }
+  {
+    const CaseSpec& s = find_case("ellipsoid3d");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 4;
+    const long n = s.steps_for_level(L);
+    UniformRunResult r = run_uniform(s, L, n, sc);
+    UniformRunResult g = gpu::run_uniform(s, L, n, sc);
+    report("run_uniform ellipsoid3d L=4 state", same_grid(r.grid, g.grid));
+    report("run_uniform ellipsoid3d L=4 max_cfl", r.report.max_cfl == g.report.max_cfl);
+  }
+  // step_block with the reference's refill = fill_ghosts(bc)
+  {
+    const CaseSpec& s = find_case("lax_liu_6");
+    UniformGrid a(2, 6, s.origin, s.extent);
+    init_case(s, a);
+    UniformGrid b = a;
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    fill_ghosts(a.block(), s.bc);
+    const StepDiag d1 = step_block(a.block(), a.dx(), 1e-3, sc, s.gas,
+                                   [&](BlockData& blk) { fill_ghosts(blk, s.bc); });
+    const StepDiag d2 = gpu::step_block(b.block(), b, 1e-3, sc, s.gas, s.bc);
+    report("step_block lax_liu_6 L=6 state", same_grid(a, b));
+    report("step_block StepDiag", d1.max_wave_speed == d2.max_wave_speed &&
+                                      d1.fallbacks == d2.fallbacks);
+  }
+  // MR and MRLT on lax_liu_6 with its own epsilon and step schedule
+  for (int lt = 0; lt <= 1; ++lt) {
+    const CaseSpec& s = find_case("lax_liu_6");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 6;
+    const long n = s.steps_for_level(L);
+    MROptions o;
+    o.epsilon = s.mr_epsilon;
+    o.local_time = lt == 1;
+    MRRunResult r = run_mr(s, L, n, sc, o);
+    gpu::MRDeviceResult g = gpu::run_mr(s, L, n, sc, o);
+    const std::string tag = lt ? "run_mr (MRLT) lax_liu_6 L=6" : "run_mr lax_liu_6 L=6";
+    report(tag + " leaves", r.tree.leaves() == g.leaves);
+    report(tag + " to_uniform state", same_grid(r.tree.to_uniform(L), g.grid));
+    report(tag + " leaves_per_step", r.report.leaves_per_step == g.report.leaves_per_step);
+    report(tag + " cells_per_step", r.report.cells_per_step == g.report.cells_per_step);
+    report(tag + " max_cfl", r.report.max_cfl == g.report.max_cfl);
+  }
+  {
+    const CaseSpec& s = find_case("ellipsoid3d");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 4;
+    const long n = s.steps_for_level(L);
+    MROptions o;
+    o.epsilon = s.mr_epsilon;
+    MRRunResult r = run_mr(s, L, n, sc, o);
+    gpu::MRDeviceResult g = gpu::run_mr(s, L, n, sc, o);
+    report("run_mr ellipsoid3d L=4 leaves", r.tree.leaves() == g.leaves);
+    report("run_mr ellipsoid3d L=4 state", same_grid(r.tree.to_uniform(L), g.grid));
+  }
+  std::printf("%s (%d failures)\n", failures ? "SHIM PARITY FAILED" : "SHIM PARITY OK", failures);
+  return failures ? 1 : 0;
+}
