@@ -176,18 +176,25 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   AF_CUDA(cudaMalloc(&d_red_, sizeof(unsigned long long) * (64 + 17 * kMaxStageRecords)));
   tile_off_.assign(L_ + 2, 0);
   tile_count_.assign(L_ + 1, 0);
+  band_count_.assign(L_ + 1, 0);
   long toff = 0;
   for (int l = 0; l <= L_; ++l) {
     tile_off_[l] = toff;
+    g_.tile_off[l] = toff;
     const int n = 1 << l;
-    const long t = D_ == 2 ? (long)((n + kTX2 - 1) / kTX2) * ((n + kTY2 - 1) / kTY2)
-                           : (long)((n + kTX3 - 1) / kTX3) * ((n + kTY3 - 1) / kTY3) *
-                                 ((n + kTZ3 - 1) / kTZ3);
-    toff += t;
+    const int tx = D_ == 2 ? kTX2 : kTX3, ty = D_ == 2 ? kTY2 : kTY3, tz = D_ == 2 ? 1 : kTZ3;
+    g_.ntx[l] = (n + tx - 1) / tx;
+    g_.nty[l] = (n + ty - 1) / ty;
+    g_.ntz[l] = D_ == 3 ? (n + tz - 1) / tz : 1;
+    toff += (long)g_.ntx[l] * g_.nty[l] * g_.ntz[l];
   }
   tile_off_[L_ + 1] = toff;
+  g_.tile_off[L_ + 1] = toff;
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
-  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * (L_ + 1)));
+  AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
+  AF_CUDA(cudaMalloc(&d_tflag_, toff));
+  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 34));
+  AF_CUDA(cudaMalloc(&d_lpl_, sizeof(unsigned long long) * 17));
   AF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
   AF_CUDA(cudaMemsetAsync(d_st_, ST_ABSENT, tot, stream_));
@@ -217,6 +224,7 @@ MR::~MR() {
   for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
                   (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
                   (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
+                  (void*)d_band_, (void*)d_tflag_, (void*)d_lpl_,
                   (void*)d_flagi_, (void*)d_red_, (void*)d_regbase_, (void*)d_regmask_,
                   (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_,
                   (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
@@ -240,49 +248,54 @@ double MR::eps_at_(int child_level) const {
     AF_CUDA(cudaGetLastError());                                        \
   } while (0)
 
+// band / leaf tile list of level l and a grid for it
+#define AF_BAND(l) d_band_ + tile_off_[l], band_count_[l]
+#define AF_LEAFT(l) d_tiles_ + tile_off_[l], tile_count_[l]
+#define AF_TGRID(cnt) ((unsigned)std::max(1, std::min((cnt), kGrid)))
+
 void MR::predict_fill_(int lo, int hi) {
   for (int l = 1; l <= L_; ++l)
-    AF_MR_LAUNCH(mr_predict_level, grid_for(mr_cells(D_, l)), d_V_, d_st_,
-                 virtuals_ ? d_mark_ : nullptr, g_, l, lo, hi);
+    if (band_count_[l])
+      AF_MR_LAUNCH(mr_predict_level, AF_TGRID(band_count_[l]), d_V_, d_st_,
+                   virtuals_ ? d_mark_ : nullptr, g_, l, lo, hi, AF_BAND(l));
+  fresh_ = !virtuals_ || (lo == 0 && hi >= L_);
 }
 
 // project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
 void MR::project_range_(int lo, int top) {
   for (int l = std::min(top - 1, L_ - 1); l >= lo; --l)
-    AF_MR_LAUNCH(mr_project_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, g_, l);
+    if (band_count_[l])
+      AF_MR_LAUNCH(mr_project_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+  fresh_ = false;
 }
 
-void MR::level_counts_() {
-  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * (L_ + 1), stream_));
-  for (int l = 0; l <= L_; ++l) {
-    mr_level_leaf_count<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
-        d_st_, g_.cell_off[l], mr_cells(D_, l), d_red_ + l);
-    ++launches_;
+// Per-level band / leaf tile lists and leaf counts (one host synchronisation).
+void MR::build_lists_() {
+  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * 34, stream_));
+  AF_CUDA(cudaMemsetAsync(d_lpl_, 0, sizeof(unsigned long long) * 17, stream_));
+  const long nt = tile_off_[L_ + 1];
+  const unsigned gw = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
+  const unsigned gt = grid_for(nt);
+  if (D_ == 3) {
+    mr_tile_flags_all<3><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
+    mr_tile_lists_all<3><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
+  } else {
+    mr_tile_flags_all<2><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
+    mr_tile_lists_all<2><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
   }
-  std::vector<unsigned long long> h(L_ + 1);
-  AF_CUDA(cudaMemcpyAsync(h.data(), d_red_, 8 * (L_ + 1), cudaMemcpyDeviceToHost, stream_));
+  launches_ += 2;
+  AF_CUDA(cudaGetLastError());
+  int h[34];
+  unsigned long long lp[17];
+  AF_CUDA(cudaMemcpyAsync(h, d_tile_count_, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaMemcpyAsync(lp, d_lpl_, sizeof lp, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
-  for (int l = 0; l <= L_; ++l) leaves_per_level_[l] = (long)h[l];
-}
-
-void MR::build_tiles_() {
-  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * (L_ + 1), stream_));
   for (int l = 0; l <= L_; ++l) {
-    if (!leaves_per_level_[l]) continue;
-    const long nt = tile_off_[l + 1] - tile_off_[l];
-    const unsigned grid = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
-    if (D_ == 2)
-      mr_tile_list_kernel<2, kTX2, kTY2, 1><<<grid, 256, 0, stream_>>>(
-          d_st_, g_, l, d_tiles_ + tile_off_[l], d_tile_count_ + l);
-    else
-      mr_tile_list_kernel<3, kTX3, kTY3, kTZ3><<<grid, 256, 0, stream_>>>(
-          d_st_, g_, l, d_tiles_ + tile_off_[l], d_tile_count_ + l);
-    ++launches_;
-    AF_CUDA(cudaGetLastError());
+    band_count_[l] = h[l];
+    tile_count_[l] = h[17 + l];
+    leaves_per_level_[l] = (long)lp[l];
   }
-  AF_CUDA(cudaMemcpyAsync(tile_count_.data(), d_tile_count_, sizeof(int) * (L_ + 1),
-                          cudaMemcpyDeviceToHost, stream_));
-  AF_CUDA(cudaStreamSynchronize(stream_));
+  lists_valid_ = true;
 }
 
 void MR::build(const double* aos) {
@@ -301,6 +314,7 @@ void MR::build(const double* aos) {
   AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
   virtuals_ = false;
+  build_lists_();
   project_range_(0, L_);
   // set_norms_from (mr_tree.cpp:73-87)
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 8, stream_));
@@ -323,57 +337,75 @@ void MR::build(const double* aos) {
   fallbacks_ = 0;
   max_wave_ = 0.0;
   coarsen();
-  level_counts_();
+  build_lists_();
 }
 
 void MR::refine(int top) {
   registers_built_ = false;
+  if (!lists_valid_) build_lists_();
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
   AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
   for (int l = 0; l <= L_ - 2; ++l)
-    AF_MR_LAUNCH(mr_detail_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, d_det_, g_, l,
-                 d_norms_);
+    if (band_count_[l])
+      AF_MR_LAUNCH(mr_detail_level, AF_TGRID(band_count_[l]), d_V_, d_st_, d_det_, g_, l,
+                   d_norms_, AF_BAND(l));
   for (int l = 1; l <= L_ - 1; ++l)
-    AF_MR_LAUNCH(mr_refine_flag_level, grid_for(mr_cells(D_, l)), d_st_, d_det_, d_flag_, g_,
-                 l, eps_at_(l));
+    if (band_count_[l])
+      AF_MR_LAUNCH(mr_refine_flag_level, AF_TGRID(band_count_[l]), d_st_, d_det_, d_flag_, g_,
+                   l, eps_at_(l), AF_BAND(l));
   uint8_t* split = d_flag_;
   if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
     for (int l = 1; l <= L_ - 1; ++l) {
       const int r = l > top + 1 ? 1 << (l - top - 1) : 1;
-      AF_MR_LAUNCH(mr_dilate_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, d_flag2_, g_, l,
-                   r);
+      if (band_count_[l])
+        AF_MR_LAUNCH(mr_dilate_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, d_flag2_, g_, l,
+                     r, AF_BAND(l));
     }
     split = d_flag2_;
   }
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
   for (int l = 1; l <= L_ - 1; ++l)
-    AF_MR_LAUNCH(mr_apply_split_level, grid_for(mr_cells(D_, l)), d_st_, split, g_, l, d_flagi_);
+    if (band_count_[l])
+      AF_MR_LAUNCH(mr_apply_split_level, AF_TGRID(band_count_[l]), d_st_, split, g_, l,
+                   d_flagi_, AF_BAND(l));
   // enforce_gradedness (mr_tree.cpp:404-444)
   for (;;) {
     for (int l = 0; l <= L_ - 1; ++l)
-      AF_MR_LAUNCH(mr_grade_flag_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, g_, l);
+      if (band_count_[l])
+        AF_MR_LAUNCH(mr_grade_flag_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, g_, l,
+                     AF_BAND(l));
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
     for (int l = 0; l <= L_ - 1; ++l)
-      AF_MR_LAUNCH(mr_apply_split_level, grid_for(mr_cells(D_, l)), d_st_, d_flag_, g_, l,
-                   d_flagi_);
+      if (band_count_[l])
+        AF_MR_LAUNCH(mr_apply_split_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, g_, l,
+                     d_flagi_, AF_BAND(l));
     int changed = 0;
     AF_CUDA(cudaMemcpyAsync(&changed, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
     if (!changed) break;
   }
-  level_counts_();
+  build_lists_();
+  lists_valid_ = true;
+  predict_fill_(1, 0);  // predictions for band cells the splits brought in
 }
 
 void MR::add_virtual_leaves() {
   AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  if (!lists_valid_) build_lists_();
   for (int l = 1; l <= L_; ++l)
-    AF_MR_LAUNCH(mr_virtual_mark_level, grid_for(mr_cells(D_, l)), d_st_, d_mark_, g_, l);
+    if (tile_count_[l])
+      AF_MR_LAUNCH(mr_virtual_mark_level, AF_TGRID(tile_count_[l]), d_st_, d_mark_, g_, l,
+                   AF_LEAFT(l));
   virtuals_ = true;
 }
 
 void MR::remove_virtual_leaves() {
+  const bool was_fresh = fresh_;
   virtuals_ = false;
-  predict_fill_(1, 0);  // former virtual positions read as fresh predictions again
+  // former virtual positions read as fresh predictions again (a no-op when
+  // every virtual was just refreshed, as after a global step)
+  if (!was_fresh) predict_fill_(1, 0);
+  fresh_ = true;
 }
 
 void MR::counts(long* leaves, long* nodes, long* internals) {
@@ -400,11 +432,11 @@ double MR::leaf_speed_sum() {
   for (int l = 0; l <= L_; ++l) {
     if (!leaves_per_level_[l]) continue;
     if (D_ == 3)
-      mr_leaf_speed_kernel<3><<<grid_for(mr_cells(3, l)), 256, 0, stream_>>>(
-          d_V_, d_st_, g_, l, cfg_.gamma, d_red_);
+      mr_leaf_speed_kernel<3><<<AF_TGRID(tile_count_[l]), 256, 0, stream_>>>(
+          d_V_, d_st_, g_, l, cfg_.gamma, d_red_, AF_LEAFT(l));
     else
-      mr_leaf_speed_kernel<2><<<grid_for(mr_cells(2, l)), 256, 0, stream_>>>(
-          d_V_, d_st_, g_, l, cfg_.gamma, d_red_);
+      mr_leaf_speed_kernel<2><<<AF_TGRID(tile_count_[l]), 256, 0, stream_>>>(
+          d_V_, d_st_, g_, l, cfg_.gamma, d_red_, AF_LEAFT(l));
     ++launches_;
   }
   unsigned long long b = 0;
@@ -416,9 +448,8 @@ double MR::leaf_speed_sum() {
 void MR::snapshot_(int lo, int hi) {
   for (int l = lo; l <= std::min(hi, L_); ++l) {
     if (!leaves_per_level_[l]) continue;
-    mr_copy_leaves<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
-        d_V_, d_Qold_, d_st_, g_.cell_off[l], mr_cells(D_, l), g_.total_cells, NC_, nullptr, 0);
-    ++launches_;
+    AF_MR_LAUNCH(mr_copy_leaves_tiles, AF_TGRID(tile_count_[l]), d_V_, d_Qold_, d_st_, g_, l,
+                 AF_LEAFT(l), nullptr, 0);
   }
 }
 
@@ -502,10 +533,8 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   if (profile_) AF_CUDA(cudaEventRecord(e1, stream_));
   for (int l = lo; l <= std::min(hi, L_); ++l) {
     if (!leaves_per_level_[l]) continue;
-    mr_copy_leaves<<<grid_for(mr_cells(D_, l)), 256, 0, stream_>>>(
-        d_Vs_, d_V_, d_st_, g_.cell_off[l], mr_cells(D_, l), g_.total_cells, NC_, d_err_,
-        stage == 2);
-    ++launches_;
+    AF_MR_LAUNCH(mr_copy_leaves_tiles, AF_TGRID(tile_count_[l]), d_Vs_, d_V_, d_st_, g_, l,
+                 AF_LEAFT(l), d_err_, stage == 2);
   }
 }
 
@@ -518,8 +547,9 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
     t_old_[l] = t;
     t_new_[l] = t + dt;
   }
-  // refresh_virtuals + the virtual q_old snapshot (mr_solver.cpp:251-266)
-  predict_fill_(lo, top);
+  // refresh_virtuals + the virtual q_old snapshot (mr_solver.cpp:251-266);
+  // nothing to refresh when every prediction is current and all levels step
+  if (!(fresh_ && lo == 0 && top >= L_)) predict_fill_(lo, top);
   if (d_VQold_)
     for (int l = lo + 1; l <= std::min(top + 1, L_); ++l)
       AF_MR_LAUNCH(mr_virtual_snapshot, grid_for(mr_cells(D_, l)), d_V_, d_VQold_, d_st_,
@@ -550,14 +580,16 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
 
 void MR::evolve_global(double dt, af_step_diag* d) {
   stage_records_.clear();
-  build_tiles_();
+  if (!lists_valid_) build_lists_();
+  lists_valid_ = true;
   step_levels_(0, L_, 0.0, dt, 0);
   collect_stage_records_(d);
 }
 
 void MR::advance_local(int top, double t, double dt, af_step_diag* d) {
   stage_records_.clear();
-  build_tiles_();
+  if (!lists_valid_) build_lists_();
+  lists_valid_ = true;
   if (opt_.local_time && !registers_built_) build_registers_(top);
   step_levels_(0, top, t, dt, 0);
   collect_stage_records_(d);
@@ -660,15 +692,21 @@ void MR::apply_registers_(int coarse_level) {
 
 void MR::coarsen() {
   registers_built_ = false;
+  if (!lists_valid_) {
+    build_lists_();
+    lists_valid_ = true;
+  }
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
     for (int l = L_ - 1; l >= min_leaf_; --l)
-      AF_MR_LAUNCH(mr_coarsen_level, grid_for(mr_cells(D_, l)), d_V_, d_st_, g_, l,
-                   eps_at_(l + 1), d_norms_, d_flagi_);
+      if (band_count_[l])
+        AF_MR_LAUNCH(mr_coarsen_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l,
+                     eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
     int merged = 0;
     AF_CUDA(cudaMemcpyAsync(&merged, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
     if (!merged) break;
+    lists_valid_ = false;
     predict_fill_(1, 0);
   }
 }
@@ -798,7 +836,8 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
     registers_built_ = false;
     remove_virtual_leaves();
     coarsen();
-    level_counts_();
+    build_lists_();
+    lists_valid_ = true;
     done += sub;
     t = t_cycle + static_cast<double>(sub) * dt;
     ++cycle;

@@ -44,8 +44,7 @@ class MR {
  private:
   void predict_fill_(int lo, int hi);
   void project_range_(int lo, int top);
-  void build_tiles_();
-  void level_counts_();
+  void build_lists_();
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);
   void build_registers_(int top);
@@ -77,8 +76,11 @@ class MR {
   double* d_VQold_ = nullptr;    // virtual q_old snapshots (LT)
   double* d_det_ = nullptr;
   double* d_norms_ = nullptr;
-  int* d_tiles_ = nullptr;
-  int* d_tile_count_ = nullptr;
+  int* d_tiles_ = nullptr;       // per-level leaf-tile lists (tile_off_ regions)
+  int* d_band_ = nullptr;        // per-level band-tile lists
+  uint8_t* d_tflag_ = nullptr;
+  int* d_tile_count_ = nullptr;  // [0..16] band counts, [17..33] leaf-tile counts
+  unsigned long long* d_lpl_ = nullptr;  // leaves per level
   int* d_err_ = nullptr;
   int* d_flagi_ = nullptr;
   // flux registers (local time stepping)
@@ -95,7 +97,10 @@ class MR {
   bool registers_built_ = false;
   unsigned long long* d_red_ = nullptr;  // scratch reductions
   std::vector<long> tile_off_;           // per-level offset into d_tiles_
-  std::vector<int> tile_count_;
+  std::vector<int> tile_count_;  // leaf tiles per level
+  std::vector<int> band_count_;  // band tiles per level
+  bool fresh_ = false;
+  bool lists_valid_ = false;           // every absent band cell holds its current prediction
   std::vector<long> leaves_per_level_;
   std::vector<double> t_old_, t_new_;
   int min_leaf_ = 0;

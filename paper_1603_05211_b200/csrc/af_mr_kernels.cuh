@@ -44,20 +44,47 @@ __device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
   return D == 3 ? ((long)k * n + j) * n + i : (long)j * n + i;
 }
 
+// Cell iteration of a level: over the cells of the listed work tiles (one
+// thread per cell, 256-thread blocks, grid-stride over the list), or over
+// every cell of the level when `tiles` is null. Work then scales with the
+// tree's band of tiles instead of the dense level.
+template <int D, class F>
+__device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int* tiles,
+                                            int ntiles, F&& f) {
+  const int n = 1 << l;
+  if (tiles) {
+    constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
+    const int ntx = g.ntx[l], nty = g.nty[l];
+    const int tx = threadIdx.x % TX, ty = (threadIdx.x / TX) % TY;
+    const int tz = D == 3 ? threadIdx.x / (TX * TY) : 0;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+      const int t = tiles[ti];
+      const int x = (t % ntx) * TX + tx, y = ((t / ntx) % nty) * TY + ty;
+      const int z = D == 3 ? (t / (ntx * nty)) * kTileZ3 + tz : 0;
+      if (x < n && y < n && (D == 2 || z < n)) f(mr_idx(D, n, x, y, z));
+    }
+  } else {
+    const long cells = mr_cells(D, l);
+    for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
+         c += (long)gridDim.x * blockDim.x)
+      f(c);
+  }
+}
+
 // ------------------------------------------------------------ projection --
 // project_internals / project_range (mr_tree.cpp:319-338, mr_solver.cpp:268-282):
 // internal q = (sum over children, x-fastest child order) * (1/2^d).
 template <int D>
-__global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l) {
+__global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l,
+    const int* tiles = nullptr, int ntiles = 0) {
   constexpr int NC = D + 2;
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
   const long off = g.cell_off[l], foff = g.cell_off[l + 1];
   const long comp = g.total_cells;
   const double w = 1.0 / (double)(1 << D);
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_INTERNAL) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_INTERNAL) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     double s[NC];
 #pragma unroll
@@ -71,7 +98,7 @@ __global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l
     }
 #pragma unroll
     for (int m = 0; m < NC; ++m) V[m * comp + off + c] = s[m] * w;
-  }
+  });
   (void)fcells;
 }
 
@@ -169,24 +196,24 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
 // re-predicts only the virtual children of the stepping leaves.
 template <int D>
 __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
-                                 MRLevels g, int l, int lo, int hi) {
+                                 MRLevels g, int l, int lo, int hi,
+    const int* tiles = nullptr, int ntiles = 0) {
   constexpr int NC = D + 2;
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l);
   const long off = g.cell_off[l], poff = g.cell_off[l - 1];
   const long comp = g.total_cells;
   const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_ABSENT) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_ABSENT) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-    if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
+    if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
     const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
     double q[NC];
     predict_child<D>(V, comp, poff, pn, g.bc, i >> 1, j >> 1, k >> 1, ch, q);
 #pragma unroll
     for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
-  }
+  });
 }
 
 // ---------------------------------------------------------------- detail --
@@ -220,15 +247,15 @@ __device__ __forceinline__ double node_detail(const double* V, long comp, const 
 // Detail of every INTERNAL node at level l.
 template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
-                                int l, const double* norms) {
+                                int l, const double* norms,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l;
   const long cells = mr_cells(D, l), off = g.cell_off[l];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_INTERNAL) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_INTERNAL) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     det[off + c] = node_detail<D>(V, g.total_cells, g, l, i, j, k, norms);
-  }
+  });
 }
 
 // Buffer dilation of the LT refine (mr_tree.cpp:374-396): every leaf within
@@ -236,31 +263,31 @@ __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det,
 // flag[] holds 1 for detail-flagged leaves; this pass writes 2 for dilated.
 template <int D>
 __global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
-                                     MRLevels g, int l, double eps) {
+                                     MRLevels g, int l, double eps,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
     uint8_t f = 0;
     if (st[off + c] == ST_LEAF && l >= 1 && l < g.L) {
       const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
       f = det[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)] >= eps ? 1 : 0;
     }
     flag[off + c] = f;
-  }
+  });
 }
 
 template <int D>
 __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
-                                MRLevels g, int l, int r) {
+                                MRLevels g, int l, int r,
+    const int* tiles = nullptr, int ntiles = 0) {
   // Target t is inserted iff some detail-flagged source s has map(s + o) == t
   // for an offset o != 0 with |o|_inf <= r. Clamping and folding never move a
   // position farther from s, so scanning the in-domain (or periodically
   // wrapped) sources s = t - o is exhaustive.
   const int n = 1 << l;
   const long cells = mr_cells(D, l), off = g.cell_off[l];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
     uint8_t f = flag[off + c];
     if (!f && st[off + c] == ST_LEAF) {
       const int t[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
@@ -282,24 +309,24 @@ __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t*
           }
     }
     flag2[off + c] = f;
-  }
+  });
 }
 
 template <int D>
 __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels g, int l,
-                                     int* changed) {
+                                     int* changed,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (!flag[off + c] || st[off + c] != ST_LEAF) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (!flag[off + c] || st[off + c] != ST_LEAF) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     st[off + c] = ST_INTERNAL;
     for (int ch = 0; ch < (1 << D); ++ch)
       st[foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                        D == 3 ? 2 * k + ((ch >> 2) & 1) : 0)] = ST_LEAF;
     *changed = 1;
-  }
+  });
 }
 
 // enforce_gradedness (mr_tree.cpp:404-444), decision half of one pass: a
@@ -307,11 +334,11 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
 // an INTERNAL child on the shared face. (Unique least fixpoint; decide all,
 // then apply, repeat.)
 template <int D>
-__global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l) {
+__global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
     uint8_t need = 0;
     if (st[off + c] == ST_LEAF && l < g.L) {
       const int idx[3] = {(int)(c % n), (int)((c / n) % n),
@@ -339,7 +366,7 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
         }
     }
     flag[off + c] = need;
-  }
+  });
 }
 
 // coarsen (mr_tree.cpp:446-511), one level of one finest-first sweep:
@@ -347,21 +374,21 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
 // detail < eps_{l+1}, and no face-ring cell at level l+1 is INTERNAL.
 template <int D>
 __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
-                                 const double* norms, int* merged) {
+                                 const double* norms, int* merged,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_INTERNAL) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_INTERNAL) return;
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
     bool all_leaves = true;
     for (int ch = 0; ch < (1 << D) && all_leaves; ++ch)
       if (st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
                            D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] != ST_LEAF)
         all_leaves = false;
-    if (!all_leaves) continue;
+    if (!all_leaves) return;
     const double d = node_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], norms);
-    if (!(d < eps)) continue;
+    if (!(d < eps)) return;
     bool allowed = true;  // merge_allowed (mr_tree.cpp:446-471)
     for (int a = 0; a < D && allowed; ++a)
       for (int dir = -1; dir <= 1 && allowed; dir += 2) {
@@ -380,26 +407,26 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
             if (st[foff + mr_idx(D, nf, r[0], r[1], r[2])] == ST_INTERNAL) allowed = false;
           }
       }
-    if (!allowed) continue;
+    if (!allowed) return;
     // merged q = mean of the children == the projection already stored
     st[off + c] = ST_LEAF;
     for (int ch = 0; ch < (1 << D); ++ch)
       st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
                        D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] = ST_ABSENT;
     *merged = 1;
-  }
+  });
 }
 
 // Virtual-leaf count (add_virtual_leaves, mr_tree.cpp:513-551): a level-(l-1)
 // leaf P gets 2^d virtual children when some axis-stencil position (+-1, +-2)
 // of a level-l leaf maps into an absent child of P. Marks P in `mark`.
 template <int D>
-__global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l) {
+__global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l,
+    const int* tiles = nullptr, int ntiles = 0) {
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_LEAF) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_LEAF) return;
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
     for (int a = 0; a < D; ++a)
       for (int o = -2; o <= 2; ++o) {
@@ -414,7 +441,7 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
         const long pc = poff + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
         if (st[pc] == ST_LEAF) mark[pc] = 1;
       }
-  }
+  });
 }
 
 // Counts per level: [0] leaves, [1] internals, [2] virtual-marked parents.
@@ -443,13 +470,13 @@ static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, l
 // Max over leaves of sum_a(|v_a|+c) (CFL rule) for the leaves of level l.
 template <int D>
 __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
-                                     double gamma, unsigned long long* target) {
+                                     double gamma, unsigned long long* target,
+                                     const int* tiles = nullptr, int ntiles = 0) {
   __shared__ double red[8];
-  const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
+  const long off = g.cell_off[l], comp = g.total_cells;
   double best = 0.0;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_LEAF) continue;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_LEAF) return;
     Cons<D> q;
     q.rho = V[off + c];
 #pragma unroll
@@ -458,7 +485,7 @@ __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevel
     double s, m;
     wave_speeds(primitives(q, gamma - 1.0), gamma, s, m);
     best = fmax(best, s);
-  }
+  });
   block_max_atomic<256>(best, red, target);
 }
 

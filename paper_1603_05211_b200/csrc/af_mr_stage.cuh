@@ -518,6 +518,107 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
   }
 }
 
+// Work-tile flags over every level at once (one warp per tile): bit 0 the
+// tile holds a leaf, bit 1 it holds a cell whose parent exists (every node's
+// parent exists, so these tiles cover the tree and everything a split can
+// create). Leaves per level are counted on the way.
+template <int D>
+__global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
+                                  unsigned long long* leaves_per_level) {
+  constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
+  constexpr int TZ = D == 3 ? kTileZ3 : 1;
+  const long total = g.tile_off[g.L + 1];
+  const int lane = threadIdx.x & 31;
+  for (long tg = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32; tg < total;
+       tg += (long)gridDim.x * (blockDim.x / 32)) {
+    int l = 0;
+    while (tg >= g.tile_off[l + 1]) ++l;
+    const long t = tg - g.tile_off[l];
+    const int n = 1 << l;
+    const int x0 = (int)(t % g.ntx[l]) * TX, y0 = (int)((t / g.ntx[l]) % g.nty[l]) * TY;
+    const int z0 = D == 3 ? (int)(t / ((long)g.ntx[l] * g.nty[l])) * TZ : 0;
+    unsigned nleaf = 0;
+    bool pex = false;
+    for (int c = lane; c < TX * TY * TZ; c += 32) {
+      const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
+      if (x >= n || y >= n || (D == 3 && z >= n)) continue;
+      nleaf += st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF;
+      pex = pex || l == 0 ||
+            st[g.cell_off[l - 1] + mr_idx(D, n >> 1, x >> 1, y >> 1, z >> 1)] != ST_ABSENT;
+    }
+    for (int o = 16; o > 0; o >>= 1) nleaf += __shfl_xor_sync(0xffffffffu, nleaf, o);
+    pex = __any_sync(0xffffffffu, pex);
+    if (lane == 0) {
+      tflag[tg] = (nleaf ? 1 : 0) | (pex ? 2 : 0);
+      if (nleaf) atomicAdd(leaves_per_level + l, (unsigned long long)nleaf);
+    }
+  }
+}
+
+// Per-level tile lists: `leaf` = tiles holding a leaf (the stage kernels'
+// work), `band` = tiles within one tile of a flag-2 tile (periodic axes wrap):
+// every cell the reference could read as a node value or a prediction lies
+// within the stencil reach (<= 3 cells) of a node, so this band is where
+// projections, predictions, details and merges are evaluated.
+template <int D>
+__global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, int* leaf,
+                                  int* counts) {
+  const long total = g.tile_off[g.L + 1];
+  for (long tg = blockIdx.x * (long)blockDim.x + threadIdx.x; tg < total;
+       tg += (long)gridDim.x * blockDim.x) {
+    int l = 0;
+    while (tg >= g.tile_off[l + 1]) ++l;
+    const long t = tg - g.tile_off[l];
+    const int nt[3] = {g.ntx[l], g.nty[l], D == 3 ? g.ntz[l] : 1};
+    const int tc[3] = {(int)(t % nt[0]), (int)((t / nt[0]) % nt[1]),
+                       D == 3 ? (int)(t / ((long)nt[0] * nt[1])) : 0};
+    bool in_band = false;
+    const int rz = D == 3 ? 1 : 0;
+    for (int dz = -rz; dz <= rz && !in_band; ++dz)
+      for (int dy = -1; dy <= 1 && !in_band; ++dy)
+        for (int dx = -1; dx <= 1 && !in_band; ++dx) {
+          int q[3] = {tc[0] + dx, tc[1] + dy, tc[2] + dz};
+          bool ok = true;
+          for (int a = 0; a < D; ++a) {
+            if (q[a] >= 0 && q[a] < nt[a]) continue;
+            if (g.bc[2 * a] == AF_BC_PERIODIC)
+              q[a] = (q[a] + nt[a]) % nt[a];
+            else
+              ok = false;
+          }
+          if (ok && (tflag[g.tile_off[l] + ((long)q[2] * nt[1] + q[1]) * nt[0] + q[0]] & 2))
+            in_band = true;
+        }
+    if (in_band) band[g.tile_off[l] + atomicAdd(counts + l, 1)] = (int)t;
+    if (tflag[tg] & 1) leaf[g.tile_off[l] + atomicAdd(counts + 17 + l, 1)] = (int)t;
+  }
+}
+
+// Copies the leaf values of the listed tiles of level l from src to dst
+// (q_old snapshot, stage commit). `guard`: skip when a pass-1 or post-step
+// failure is pending (the failing stage never commits: the reference throws
+// before pass 2 completes); `promote` turns a post-step failure into a stop.
+template <int D>
+__global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8_t* st,
+                                     MRLevels g, int l, const int* tiles, int ntiles,
+                                     const int* guard, int promote) {
+  if (guard) {
+    __shared__ int s;
+    if (threadIdx.x == 0) s = guard[0] | guard[2];
+    __syncthreads();
+    if (s) {
+      if (promote && blockIdx.x == 0 && threadIdx.x == 0) atomicExch((int*)guard, 1);
+      return;
+    }
+  }
+  const long off = g.cell_off[l], comp = g.total_cells;
+  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+    if (st[off + c] != ST_LEAF) return;
+#pragma unroll
+    for (int m = 0; m < D + 2; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
+  });
+}
+
 // Tiles of level l holding at least one leaf (order irrelevant: every tile
 // writes only its own leaves).
 template <int D, int TX, int TY, int TZ>

@@ -16,7 +16,13 @@ struct MRLevels {
   long cell_off[17];       // first cell of level l in the concatenated level arrays
   long total_cells;
   double inv_dx[17];       // 1 / dx_l, dx_l = extent / 2^l (mr_tree.hpp:73, mr_solver.cpp:181)
+  // work tiles (2D 32x8, 3D 8x8x4 cells = 256 threads): per-level tile grid
+  int ntx[17], nty[17], ntz[17];
+  long tile_off[17];       // first tile of level l in the concatenated tile space
 };
+
+constexpr int kTileX2 = 32, kTileY2 = 8;
+constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
 
 __host__ __device__ __forceinline__ long mr_cells(int dim, int l) {
   return dim == 3 ? (1L << (3 * l)) : (1L << (2 * l));
