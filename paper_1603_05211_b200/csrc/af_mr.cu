@@ -16,6 +16,9 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "af_mr.h"
 #include "af_mr_stage.cuh"
 
@@ -24,6 +27,7 @@ namespace af {
 namespace {
 
 constexpr int kGrid = 148 * 8;
+constexpr int kGridFixed = 148 * 2;  // graph replay: grid-stride over device-side counts
 
 inline unsigned grid_for(long n, int block = 256) {
   long b = (n + block - 1) / block;
@@ -194,6 +198,11 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
   AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 34));
+  AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 34));
+  g_.dcnt = d_tile_count_;
+  AF_CUDA(cudaMalloc(&d_dt_, sizeof(double)));
+  AF_CUDA(cudaMalloc(&d_step3_, sizeof(int)));
+  AF_CUDA(cudaMallocHost(&h_dt_step_, 64));
   AF_CUDA(cudaMalloc(&d_lpl_, sizeof(unsigned long long) * 17));
   AF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
@@ -218,13 +227,20 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
 }
 
 MR::~MR() {
+  if (std::getenv("AF_MR_TIMING"))
+    std::fprintf(stderr, "AF_MR_TIMING refine %.3f ms, virtual+counts+dt %.3f ms, evolve %.3f ms, "
+                 "coarsen+lists %.3f ms (totals); evolve GPU span %.3f ms\n", 1e3 * phase_s_[0],
+                 1e3 * phase_s_[1], 1e3 * phase_s_[2], 1e3 * phase_s_[3], evolve_gpu_ms_);
   cudaSetDevice(cfg_.device);
   if (own_stream_) cudaStreamSynchronize(own_stream_);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  for (GraphCache& gc : graphs_)
+    if (gc.exec) cudaGraphExecDestroy(gc.exec);
+  if (h_dt_step_) cudaFreeHost(h_dt_step_);
   for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
                   (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
                   (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
-                  (void*)d_band_, (void*)d_tflag_, (void*)d_lpl_,
+                  (void*)d_band_, (void*)d_tflag_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
                   (void*)d_flagi_, (void*)d_red_, (void*)d_regbase_, (void*)d_regmask_,
                   (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_,
                   (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
@@ -248,28 +264,75 @@ double MR::eps_at_(int child_level) const {
     AF_CUDA(cudaGetLastError());                                        \
   } while (0)
 
-// band / leaf tile list of level l and a grid for it
-#define AF_BAND(l) d_band_ + tile_off_[l], band_count_[l]
-#define AF_LEAFT(l) d_tiles_ + tile_off_[l], tile_count_[l]
-#define AF_TGRID(cnt) ((unsigned)std::max(1, std::min((cnt), kGrid)))
+// multi-level launch of a per-level kernel over levels [lo, hi] (band or leaf lists)
+#define AF_ML_LAUNCH(kern, lo, hi, leaf, ...)                                      \
+  do {                                                                             \
+    dim3 grid_;                                                                    \
+    if (ml_grid_((lo), (hi), (leaf), &grid_)) {                                    \
+      const int AF_L = -(std::max((lo), 0) + 1);                                   \
+      const int* AF_T = (leaf) ? d_tiles_ : d_band_;                               \
+      const int AF_S = (leaf) ? 1 : 0;                                             \
+      if (D_ == 3)                                                                 \
+        kern<3><<<grid_, 256, 0, stream_>>>(__VA_ARGS__, AF_T, AF_S);              \
+      else                                                                         \
+        kern<2><<<grid_, 256, 0, stream_>>>(__VA_ARGS__, AF_T, AF_S);              \
+      ++launches_;                                                                 \
+      AF_CUDA(cudaGetLastError());                                                 \
+    }                                                                              \
+  } while (0)
 
-void MR::predict_fill_(int lo, int hi) {
-  for (int l = 1; l <= L_; ++l)
-    if (band_count_[l])
+// band / leaf tile list of level l and a grid for it
+#define AF_BAND(l) d_band_ + tile_off_[l], (fixed_grids_ ? -1 : band_count_[l])
+#define AF_LEAFT(l) d_tiles_ + tile_off_[l], (fixed_grids_ ? -2 : tile_count_[l])
+#define AF_TGRID(cnt) ((unsigned)(fixed_grids_ ? kGridFixed : std::max(1, std::min((cnt), kGrid))))
+#define AF_HAS(cnt) (fixed_grids_ || (cnt) > 0)
+
+// Cooperative launch of an all-levels kernel (grid-wide barrier per level).
+template <class K, class... A>
+static void coop_launch(K kern, int blocks, cudaStream_t s, A... args) {
+  void* argv[] = {static_cast<void*>(&args)...};
+  AF_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks),
+                                      dim3(256), argv, 0, s));
+}
+
+int MR::coop_blocks_() {
+  if (coop_blocks_cache_ > 0) return coop_blocks_cache_;
+  int dev = 0, sms = 0, nb1 = 0, nb2 = 0;
+  AF_CUDA(cudaGetDevice(&dev));
+  AF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (D_ == 3) {
+    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, mr_predict_all<3>, 256, 0));
+    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, mr_project_all<3>, 256, 0));
+  } else {
+    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, mr_predict_all<2>, 256, 0));
+    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, mr_project_all<2>, 256, 0));
+  }
+  coop_blocks_cache_ = sms * std::max(1, std::min({nb1, nb2, 4}));
+  return coop_blocks_cache_;
+}
+
+// Prediction refresh over the band tiles, coarsest level first (one launch
+// per level: the all-levels cooperative variant with grid-wide barriers,
+// mr_predict_all, measured slower on B200 for both cfg2 and cfg3).
+// Only levels above `from` can hold stale predictions: a prediction at level
+// l reads level l-1 only, so after values of levels [lo, hi] change (stage
+// commit + projection) the refresh starts at lo+1.
+void MR::predict_fill_(int lo, int hi, int from) {
+  for (int l = std::max(1, from); l <= L_; ++l)
+    if (AF_HAS(band_count_[l]))
       AF_MR_LAUNCH(mr_predict_level, AF_TGRID(band_count_[l]), d_V_, d_st_,
                    virtuals_ ? d_mark_ : nullptr, g_, l, lo, hi, AF_BAND(l));
-  fresh_ = !virtuals_ || (lo == 0 && hi >= L_);
+  fresh_ = (!virtuals_ || (lo == 0 && hi >= L_)) && from <= 1;
 }
 
 // project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
 void MR::project_range_(int lo, int top) {
   for (int l = std::min(top - 1, L_ - 1); l >= lo; --l)
-    if (band_count_[l])
+    if (AF_HAS(band_count_[l]))
       AF_MR_LAUNCH(mr_project_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
   fresh_ = false;
 }
 
-// Per-level band / leaf tile lists and leaf counts (one host synchronisation).
 void MR::build_lists_() {
   AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * 34, stream_));
   AF_CUDA(cudaMemsetAsync(d_lpl_, 0, sizeof(unsigned long long) * 17, stream_));
@@ -294,8 +357,26 @@ void MR::build_lists_() {
     band_count_[l] = h[l];
     tile_count_[l] = h[17 + l];
     leaves_per_level_[l] = (long)lp[l];
+    g_.band_cnt[l] = h[l];
+    g_.leaf_cnt[l] = h[17 + l];
   }
   lists_valid_ = true;
+}
+
+// Grid of a multi-level launch over levels [lo, hi] (AF_ML_RESOLVE): x spans
+// the largest list, y the levels. Returns false when every list is empty.
+bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid) const {
+  if (fixed_grids_) {  // graph capture: parameters independent of this cycle's counts
+    if (hi < lo) return false;
+    *grid = dim3((unsigned)kGridFixed, (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
+    return true;
+  }
+  int mx = 0;
+  for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l)
+    mx = std::max(mx, leaf ? tile_count_[l] : band_count_[l]);
+  if (!mx || hi < lo) return false;
+  *grid = dim3((unsigned)std::min(mx, kGrid), (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
+  return true;
 }
 
 void MR::build(const double* aos) {
@@ -345,14 +426,9 @@ void MR::refine(int top) {
   if (!lists_valid_) build_lists_();
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
   AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
-  for (int l = 0; l <= L_ - 2; ++l)
-    if (band_count_[l])
-      AF_MR_LAUNCH(mr_detail_level, AF_TGRID(band_count_[l]), d_V_, d_st_, d_det_, g_, l,
-                   d_norms_, AF_BAND(l));
-  for (int l = 1; l <= L_ - 1; ++l)
-    if (band_count_[l])
-      AF_MR_LAUNCH(mr_refine_flag_level, AF_TGRID(band_count_[l]), d_st_, d_det_, d_flag_, g_,
-                   l, eps_at_(l), AF_BAND(l));
+  AF_ML_LAUNCH(mr_detail_level, 0, L_ - 2, false, d_V_, d_st_, d_det_, g_, AF_L, d_norms_);
+  for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
+  AF_ML_LAUNCH(mr_refine_flag_level, 1, L_ - 1, false, d_st_, d_det_, d_flag_, g_, AF_L, -1.0);
   uint8_t* split = d_flag_;
   if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
     for (int l = 1; l <= L_ - 1; ++l) {
@@ -364,21 +440,16 @@ void MR::refine(int top) {
     split = d_flag2_;
   }
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
-  for (int l = 1; l <= L_ - 1; ++l)
-    if (band_count_[l])
-      AF_MR_LAUNCH(mr_apply_split_level, AF_TGRID(band_count_[l]), d_st_, split, g_, l,
-                   d_flagi_, AF_BAND(l));
+  AF_ML_LAUNCH(mr_apply_split_level, 1, L_ - 1, false, d_st_, split, g_, AF_L, d_flagi_);
   // enforce_gradedness (mr_tree.cpp:404-444)
   for (;;) {
-    for (int l = 0; l <= L_ - 1; ++l)
-      if (band_count_[l])
-        AF_MR_LAUNCH(mr_grade_flag_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, g_, l,
-                     AF_BAND(l));
+    // two decide/apply passes per host check: the fixpoint usually needs one
+    // pass plus the verifying one, so this saves a synchronisation
+    AF_ML_LAUNCH(mr_grade_flag_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L);
+    AF_ML_LAUNCH(mr_apply_split_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
+    AF_ML_LAUNCH(mr_grade_flag_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L);
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
-    for (int l = 0; l <= L_ - 1; ++l)
-      if (band_count_[l])
-        AF_MR_LAUNCH(mr_apply_split_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, g_, l,
-                     d_flagi_, AF_BAND(l));
+    AF_ML_LAUNCH(mr_apply_split_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
     int changed = 0;
     AF_CUDA(cudaMemcpyAsync(&changed, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
@@ -392,10 +463,7 @@ void MR::refine(int top) {
 void MR::add_virtual_leaves() {
   AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
   if (!lists_valid_) build_lists_();
-  for (int l = 1; l <= L_; ++l)
-    if (tile_count_[l])
-      AF_MR_LAUNCH(mr_virtual_mark_level, AF_TGRID(tile_count_[l]), d_st_, d_mark_, g_, l,
-                   AF_LEAFT(l));
+  AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
   virtuals_ = true;
 }
 
@@ -421,6 +489,22 @@ void MR::counts(long* leaves, long* nodes, long* internals) {
   if (nodes) *nodes = (long)(h[0] + h[1] + (h[2] << D_));
 }
 
+// counts (leaves, nodes incl. virtual) and the CFL speed in one synchronisation
+void MR::cycle_stats_(long* leaves, long* nodes, double* smax) {
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
+  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(
+      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
+  ++launches_;
+  if (smax)
+    AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
+  unsigned long long h[4];
+  AF_CUDA(cudaMemcpyAsync(h, d_red_, sizeof h, cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  *leaves = (long)h[0];
+  *nodes = (long)(h[0] + h[1] + (h[2] << D_));
+  if (smax) *smax = as_d(h[3]);
+}
+
 int MR::coarsest_leaf_level() {
   for (int l = 0; l <= L_; ++l)
     if (leaves_per_level_[l]) return l;
@@ -429,16 +513,7 @@ int MR::coarsest_leaf_level() {
 
 double MR::leaf_speed_sum() {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long), stream_));
-  for (int l = 0; l <= L_; ++l) {
-    if (!leaves_per_level_[l]) continue;
-    if (D_ == 3)
-      mr_leaf_speed_kernel<3><<<AF_TGRID(tile_count_[l]), 256, 0, stream_>>>(
-          d_V_, d_st_, g_, l, cfg_.gamma, d_red_, AF_LEAFT(l));
-    else
-      mr_leaf_speed_kernel<2><<<AF_TGRID(tile_count_[l]), 256, 0, stream_>>>(
-          d_V_, d_st_, g_, l, cfg_.gamma, d_red_, AF_LEAFT(l));
-    ++launches_;
-  }
+  AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_);
   unsigned long long b = 0;
   AF_CUDA(cudaMemcpyAsync(&b, d_red_, 8, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
@@ -446,11 +521,7 @@ double MR::leaf_speed_sum() {
 }
 
 void MR::snapshot_(int lo, int hi) {
-  for (int l = lo; l <= std::min(hi, L_); ++l) {
-    if (!leaves_per_level_[l]) continue;
-    AF_MR_LAUNCH(mr_copy_leaves_tiles, AF_TGRID(tile_count_[l]), d_V_, d_Qold_, d_st_, g_, l,
-                 AF_LEAFT(l), nullptr, 0);
-  }
+  AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_V_, d_Qold_, d_st_, g_, AF_L, nullptr, 0);
 }
 
 // One RK stage for the leaves of levels [lo, hi] (MRSolver::stage,
@@ -464,7 +535,12 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   a.gamma = cfg_.gamma;
   a.gm1 = cfg_.gamma - 1.0;
   a.sdt = sdt;
-  a.step3 = (int)(3 * step);
+  a.step3 = (int)(3 * std::max(step, 0L));
+  if (fixed_grids_) {
+    a.dt_dev = d_dt_;
+    a.dt_scale = stage == 1 ? 0.5 : 1.0;  // step_levels: stage(dt/2), stage(dt)
+    a.step3_dev = d_step3_;
+  }
   a.stage = stage;
   a.post_check = stage == 2;
   a.err = d_err_;
@@ -504,38 +580,43 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     }
     e0 = ev_pool_[ev_used_++];
     e1 = ev_pool_[ev_used_++];
-    AF_CUDA(cudaEventRecord(e0, stream_));
+    AF_CUDA(cudaEventRecordWithFlags(e0, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
   }
-  for (int l = lo; l <= std::min(hi, L_); ++l) {
-    if (!tile_count_[l]) continue;
-    stage_launches_ += profile_ ? 1 : 0;
-    stage_updates_ += profile_ ? leaves_per_level_[l] : 0;
-    a.tiles = d_tiles_ + tile_off_[l];
+  // one launch for every stepping level: blockIdx.y = level (AF_ML_RESOLVE);
+  // all levels read the same state and write only their own leaves
+  for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l)
+    if (tile_count_[l] && profile_) {
+      ++stage_launches_;
+      stage_updates_ += leaves_per_level_[l];
+    }
+  dim3 grid;
+  if (ml_grid_(lo, hi, true, &grid)) {
+    a.tiles = d_tiles_;
+    a.ntiles = 1;
+    const int lcode = -(std::max(lo, 0) + 1);
     const int lim = cfg_.limiter;
     if (D_ == 2) {
       const size_t sm = MRTile<2, kTX2, kTY2, 1>::smem_bytes;
       if (lim)
-        mr_stage_kernel<2, 1, kTX2, kTY2, 1><<<tile_count_[l], kTX2 * kTY2, sm, stream_>>>(a, g_, l);
+        mr_stage_kernel<2, 1, kTX2, kTY2, 1><<<grid, kTX2 * kTY2, sm, stream_>>>(a, g_, lcode);
       else
-        mr_stage_kernel<2, 0, kTX2, kTY2, 1><<<tile_count_[l], kTX2 * kTY2, sm, stream_>>>(a, g_, l);
+        mr_stage_kernel<2, 0, kTX2, kTY2, 1><<<grid, kTX2 * kTY2, sm, stream_>>>(a, g_, lcode);
     } else {
       const size_t sm = MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes;
       if (lim)
         mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>
-            <<<tile_count_[l], kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, l);
+            <<<grid, kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, lcode);
       else
         mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>
-            <<<tile_count_[l], kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, l);
+            <<<grid, kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, lcode);
     }
     ++launches_;
     AF_CUDA(cudaGetLastError());
   }
-  if (profile_) AF_CUDA(cudaEventRecord(e1, stream_));
-  for (int l = lo; l <= std::min(hi, L_); ++l) {
-    if (!leaves_per_level_[l]) continue;
-    AF_MR_LAUNCH(mr_copy_leaves_tiles, AF_TGRID(tile_count_[l]), d_Vs_, d_V_, d_st_, g_, l,
-                 AF_LEAFT(l), d_err_, stage == 2);
-  }
+  if (profile_)
+    AF_CUDA(cudaEventRecordWithFlags(e1, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
+  AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
+               stage == 2);
 }
 
 // MRSolver::step_levels (mr_solver.cpp:232-316). `sub` is which of the
@@ -549,7 +630,7 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
   }
   // refresh_virtuals + the virtual q_old snapshot (mr_solver.cpp:251-266);
   // nothing to refresh when every prediction is current and all levels step
-  if (!(fresh_ && lo == 0 && top >= L_)) predict_fill_(lo, top);
+  if (!(fresh_ && lo == 0 && top >= L_)) predict_fill_(lo, top, lo + 1);
   if (d_VQold_)
     for (int l = lo + 1; l <= std::min(top + 1, L_); ++l)
       AF_MR_LAUNCH(mr_virtual_snapshot, grid_for(mr_cells(D_, l)), d_V_, d_VQold_, d_st_,
@@ -559,12 +640,12 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
   sub_ = sub;
   stage_(lo, top, t, 0.5 * dt, 1, cur_step_);
   project_range_(lo, top);
-  predict_fill_(lo, top);
+  predict_fill_(lo, top, lo + 1);
   step_dt_ = dt;
   sub_ = sub;
   stage_(lo, top, t + 0.5 * dt, dt, 2, cur_step_);
   project_range_(lo, top);
-  predict_fill_(lo, top);
+  predict_fill_(lo, top, lo + 1);
   for (size_t r = r0; r < stage_records_.size(); ++r) stage_records_[r].step_dt = dt;
   bool deeper = false;
   for (int l = top + 1; l <= L_; ++l) deeper = deeper || leaves_per_level_[l] > 0;
@@ -574,7 +655,7 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
     step_levels_(top + 1, top + 1, t + 0.5 * dt, 0.5 * dt, 1);
     apply_registers_(top);
     project_range_(lo, top + 1);
-    predict_fill_(1, 0);
+    predict_fill_(1, 0, lo + 1);
   }
 }
 
@@ -582,8 +663,69 @@ void MR::evolve_global(double dt, af_step_diag* d) {
   stage_records_.clear();
   if (!lists_valid_) build_lists_();
   lists_valid_ = true;
-  step_levels_(0, L_, 0.0, dt, 0);
+  if (fresh_ && !std::getenv("AF_MR_NO_GRAPH"))
+    evolve_global_graph_(dt);
+  else
+    step_levels_(0, L_, 0.0, dt, 0);
   collect_stage_records_(d);
+}
+
+// The global step's launch sequence is identical every cycle once the counts,
+// dt and the step index are read from device memory, so it is captured once
+// into a CUDA graph and replayed (one launch instead of ~45 per cycle).
+void MR::evolve_global_graph_(double dt) {
+  h_dt_step_[0] = dt;
+  reinterpret_cast<int*>(h_dt_step_ + 1)[0] = (int)(3 * std::max(cur_step_, 0L));
+  AF_CUDA(cudaMemcpyAsync(d_dt_, h_dt_step_, sizeof(double), cudaMemcpyHostToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(d_step3_, h_dt_step_ + 1, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  // one cached graph per profiling mode (events are part of the graph)
+  GraphCache& gc = graphs_[profile_ ? 1 : 0];
+  graph_exec_ = gc.exec;
+  graph_recs_ = gc.recs;
+  graph_launches_ = gc.launches;
+  graph_events_ = gc.events;
+  if (!graph_exec_) {
+    harvest_events_();
+    const long l0 = launches_, s0 = stage_launches_, u0 = stage_updates_;
+    fixed_grids_ = true;
+    cudaGraph_t graph = nullptr;
+    AF_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    try {
+      step_levels_(0, L_, 0.0, dt, 0);
+    } catch (...) {
+      fixed_grids_ = false;
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    AF_CUDA(cudaStreamEndCapture(stream_, &graph));
+    fixed_grids_ = false;
+    AF_CUDA(cudaGraphInstantiate(&graph_exec_, graph, 0));
+    AF_CUDA(cudaGraphDestroy(graph));
+    graph_recs_ = stage_records_;
+    graph_launches_ = launches_ - l0;
+    graph_stage_launches_ = stage_launches_ - s0;
+    graph_stage_updates_ = stage_updates_ - u0;
+    graph_events_ = ev_used_;
+    gc = GraphCache{graph_exec_, graph_recs_, graph_launches_, graph_events_};
+    launches_ = l0;
+    stage_launches_ = s0;
+    stage_updates_ = u0;
+  }
+  AF_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  launches_ += graph_launches_;
+  if (profile_) {
+    // the stage updates of this cycle (leaf counts differ from the capture's)
+    for (int l = 0; l <= L_; ++l)
+      if (tile_count_[l]) {
+        stage_launches_ += 2;
+        stage_updates_ += 2 * leaves_per_level_[l];
+      }
+    ev_used_ = graph_events_;
+  }
+  stage_records_ = graph_recs_;
+  for (StageRec& r : stage_records_) r.step_dt = dt;
+  fresh_ = true;
 }
 
 void MR::advance_local(int top, double t, double dt, af_step_diag* d) {
@@ -707,7 +849,7 @@ void MR::coarsen() {
     AF_CUDA(cudaStreamSynchronize(stream_));
     if (!merged) break;
     lists_valid_ = false;
-    predict_fill_(1, 0);
+    predict_fill_(1, 0, min_leaf_ + 1);  // merges only create absent cells above min_leaf
   }
 }
 
@@ -808,12 +950,31 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
       }
       sub = span;
     }
+    const bool timing = std::getenv("AF_MR_TIMING") != nullptr;
+    auto tick = [&](int slot) {
+      if (!timing) return;
+      AF_CUDA(cudaStreamSynchronize(stream_));
+      const double now = std::chrono::duration<double>(
+          std::chrono::steady_clock::now().time_since_epoch()).count();
+      if (slot > 0) phase_s_[slot - 1] += now - phase_t0_;
+      phase_t0_ = now;
+    };
+    tick(0);
     refine(opt_.local_time ? top : -1);
+    tick(1);
     add_virtual_leaves();
     long leaves = 0, nodes = 0;
-    counts(&leaves, &nodes, nullptr);
+    double smax = 0.0;
+    cycle_stats_(&leaves, &nodes, cfl > 0.0 ? &smax : nullptr);
     double dt = fixed_dt;
-    if (cfl > 0.0) dt = cfl * dx_L / leaf_speed_sum();
+    if (cfl > 0.0) dt = cfl * dx_L / smax;
+    tick(2);
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    if (timing) {
+      cudaEventCreate(&te0);
+      cudaEventCreate(&te1);
+      cudaEventRecord(te0, stream_);
+    }
     if (cycles && cycle < max_cycles) {
       cycles[cycle].leaves = leaves;
       cycles[cycle].nodes = nodes;
@@ -832,11 +993,22 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
       advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
     else
       evolve_global(dt, nullptr);
+    if (timing) {
+      cudaEventRecord(te1, stream_);
+      cudaEventSynchronize(te1);
+      float ems = 0.f;
+      cudaEventElapsedTime(&ems, te0, te1);
+      evolve_gpu_ms_ += ems;
+      cudaEventDestroy(te0);
+      cudaEventDestroy(te1);
+    }
+    tick(3);
     cur_step_ = -1;
     registers_built_ = false;
     remove_virtual_leaves();
     coarsen();
     build_lists_();
+    tick(4);
     lists_valid_ = true;
     done += sub;
     t = t_cycle + static_cast<double>(sub) * dt;

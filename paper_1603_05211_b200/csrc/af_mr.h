@@ -42,9 +42,13 @@ class MR {
   af_error& last_error() { return last_; }
 
  private:
-  void predict_fill_(int lo, int hi);
+  void predict_fill_(int lo, int hi, int from = 1);
   void project_range_(int lo, int top);
   void build_lists_();
+  bool ml_grid_(int lo, int hi, bool leaf, dim3* grid) const;
+  int coop_blocks_();
+  void cycle_stats_(long* leaves, long* nodes, double* smax);
+  int coop_blocks_cache_ = 0;
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);
   void build_registers_(int top);
@@ -58,6 +62,25 @@ class MR {
     int lo, hi;
   };
   std::vector<StageRec> stage_records_;
+  // CUDA graph of the global-time-step evolve (parameters are cycle-invariant:
+  // counts, dt and the step index live in device memory)
+  bool fixed_grids_ = false;
+  double* d_dt_ = nullptr;
+  int* d_step3_ = nullptr;
+  double* h_dt_step_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  size_t graph_records_ = 0;
+  long graph_launches_ = 0, graph_stage_launches_ = 0, graph_stage_updates_ = 0;
+  std::vector<StageRec> graph_recs_;
+  size_t graph_events_ = 0;
+  void evolve_global_graph_(double dt);
+  struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<StageRec> recs;
+    long launches = 0;
+    size_t events = 0;
+  };
+  GraphCache graphs_[2];
   double norms_host_[5] = {1, 1, 1, 1, 1};
   double eps_at_(int child_level) const;
 
@@ -100,7 +123,10 @@ class MR {
   std::vector<int> tile_count_;  // leaf tiles per level
   std::vector<int> band_count_;  // band tiles per level
   bool fresh_ = false;
-  bool lists_valid_ = false;           // every absent band cell holds its current prediction
+  bool lists_valid_ = false;
+  double phase_s_[4] = {0, 0, 0, 0};
+  double phase_t0_ = 0.0;
+  double evolve_gpu_ms_ = 0.0;           // every absent band cell holds its current prediction
   std::vector<long> leaves_per_level_;
   std::vector<double> t_old_, t_new_;
   int min_leaf_ = 0;

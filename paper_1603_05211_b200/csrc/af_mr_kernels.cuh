@@ -19,6 +19,9 @@
 #include "af_physics.cuh"
 #include "af_uniform_kernels.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace af {
 
 // map_position (mr_tree.cpp:146-169): periodic when the LOW face is periodic
@@ -75,8 +78,9 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
 // project_internals / project_range (mr_tree.cpp:319-338, mr_solver.cpp:268-282):
 // internal q = (sum over children, x-fastest child order) * (1/2^d).
 template <int D>
-__global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l,
-    const int* tiles = nullptr, int ntiles = 0) {
+__device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, MRLevels g, int l,
+    const int* tiles, int ntiles) {
+  AF_ML_RESOLVE();
   constexpr int NC = D + 2;
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
@@ -102,53 +106,68 @@ __global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l
   (void)fcells;
 }
 
+template <int D>
+__global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l,
+    const int* tiles = nullptr, int ntiles = 0) {
+  project_level_dev<D>(V, st, g, l, tiles, ntiles);
+}
+
 // ------------------------------------------------------------ prediction --
-// axis_stencil (mr_tree.cpp:199-236): positions and low/high-child weights.
-struct AxisSt {
-  int pos[3];
-  double wl[3], wh[3];
+// axis_stencil (mr_tree.cpp:199-236): positions and the weights of the low
+// (hi == 0) or high (hi == 1) child along one axis. Returned by value with
+// constant-indexed members so everything stays in registers.
+struct AxisW {
+  int p0, p1, p2;
+  double w0, w1, w2;
 };
 
-__device__ __forceinline__ AxisSt axis_stencil(int n, int coord, bool periodic) {
-  AxisSt s;
+__device__ __forceinline__ AxisW axis_weights(int n, int coord, bool periodic, int hi) {
+  AxisW s;
   if (periodic || (coord > 0 && coord < n - 1)) {
-    s.pos[0] = coord - 1; s.pos[1] = coord; s.pos[2] = coord + 1;
-    s.wl[0] = 1.0 / 8.0; s.wl[1] = 1.0; s.wl[2] = -1.0 / 8.0;
-    s.wh[0] = -1.0 / 8.0; s.wh[1] = 1.0; s.wh[2] = 1.0 / 8.0;
-    if (periodic) {
-#pragma unroll
-      for (int t = 0; t < 3; ++t) s.pos[t] = ((s.pos[t] % n) + n) % n;  // value_at wraps
+    s.p0 = coord - 1; s.p1 = coord; s.p2 = coord + 1;
+    if (periodic) {  // value_at wraps periodic axes
+      s.p0 = ((s.p0 % n) + n) % n;
+      s.p1 = ((s.p1 % n) + n) % n;
+      s.p2 = ((s.p2 % n) + n) % n;
     }
+    s.w0 = hi ? -1.0 / 8.0 : 1.0 / 8.0;
+    s.w1 = 1.0;
+    s.w2 = hi ? 1.0 / 8.0 : -1.0 / 8.0;
     return s;
   }
   if (n == 1) {
-    s.pos[0] = s.pos[1] = s.pos[2] = 0;
-    s.wl[0] = 1.0; s.wl[1] = 0.0; s.wl[2] = 0.0;
-    s.wh[0] = 1.0; s.wh[1] = 0.0; s.wh[2] = 0.0;
+    s.p0 = s.p1 = s.p2 = 0;
+    s.w0 = 1.0; s.w1 = 0.0; s.w2 = 0.0;
     return s;
   }
   if (n == 2) {
-    s.pos[0] = 0; s.pos[1] = 1; s.pos[2] = 1;
+    s.p0 = 0; s.p1 = 1; s.p2 = 1;
     if (coord == 0) {
-      s.wl[0] = 5.0 / 4.0; s.wl[1] = -1.0 / 4.0; s.wl[2] = 0.0;
-      s.wh[0] = 3.0 / 4.0; s.wh[1] = 1.0 / 4.0; s.wh[2] = 0.0;
+      s.w0 = hi ? 3.0 / 4.0 : 5.0 / 4.0;
+      s.w1 = hi ? 1.0 / 4.0 : -1.0 / 4.0;
     } else {
-      s.wl[0] = 1.0 / 4.0; s.wl[1] = 3.0 / 4.0; s.wl[2] = 0.0;
-      s.wh[0] = -1.0 / 4.0; s.wh[1] = 5.0 / 4.0; s.wh[2] = 0.0;
+      s.w0 = hi ? -1.0 / 4.0 : 1.0 / 4.0;
+      s.w1 = hi ? 5.0 / 4.0 : 3.0 / 4.0;
     }
+    s.w2 = 0.0;
     return s;
   }
   if (coord == 0) {
-    s.pos[0] = 0; s.pos[1] = 1; s.pos[2] = 2;
-    s.wl[0] = 11.0 / 8.0; s.wl[1] = -4.0 / 8.0; s.wl[2] = 1.0 / 8.0;
-    s.wh[0] = 5.0 / 8.0; s.wh[1] = 4.0 / 8.0; s.wh[2] = -1.0 / 8.0;
+    s.p0 = 0; s.p1 = 1; s.p2 = 2;
+    s.w0 = hi ? 5.0 / 8.0 : 11.0 / 8.0;
+    s.w1 = hi ? 4.0 / 8.0 : -4.0 / 8.0;
+    s.w2 = hi ? -1.0 / 8.0 : 1.0 / 8.0;
   } else {
-    s.pos[0] = n - 3; s.pos[1] = n - 2; s.pos[2] = n - 1;
-    s.wl[0] = -1.0 / 8.0; s.wl[1] = 4.0 / 8.0; s.wl[2] = 5.0 / 8.0;
-    s.wh[0] = 1.0 / 8.0; s.wh[1] = -4.0 / 8.0; s.wh[2] = 11.0 / 8.0;
+    s.p0 = n - 3; s.p1 = n - 2; s.p2 = n - 1;
+    s.w0 = hi ? 1.0 / 8.0 : -1.0 / 8.0;
+    s.w1 = hi ? -4.0 / 8.0 : 4.0 / 8.0;
+    s.w2 = hi ? 11.0 / 8.0 : 5.0 / 8.0;
   }
   return s;
 }
+
+__device__ __forceinline__ int axw_p(const AxisW& s, int t) { return t == 0 ? s.p0 : t == 1 ? s.p1 : s.p2; }
+__device__ __forceinline__ double axw_w(const AxisW& s, int t) { return t == 0 ? s.w0 : t == 1 ? s.w1 : s.w2; }
 
 // Prediction of child `ch` (x-fastest child bits) of the level-(l-1) parent
 // (pi,pj,pk) from the dense values of level l-1 (predict_children,
@@ -156,31 +175,29 @@ __device__ __forceinline__ AxisSt axis_stencil(int n, int coord, bool periodic) 
 // accumulation ck -> cj -> ci).
 template <int D>
 __device__ __forceinline__ void predict_child(const double* V, long comp, long poff, int pn,
-                                              const int* bc, int pi, int pj, int pk, int ch,
-                                              double* out) {
+                                              int bcx, int bcy, int bcz, int pi, int pj, int pk,
+                                              int ch, double* out) {
   constexpr int NC = D + 2;
-  const AxisSt sx = axis_stencil(pn, pi, bc[0] == AF_BC_PERIODIC);
-  const AxisSt sy = axis_stencil(pn, pj, bc[2] == AF_BC_PERIODIC);
-  AxisSt sz;
-  if (D == 3) sz = axis_stencil(pn, pk, bc[4] == AF_BC_PERIODIC);
-  const double* wx = (ch & 1) ? sx.wh : sx.wl;
-  const double* wy = ((ch >> 1) & 1) ? sy.wh : sy.wl;
-  const double* wz = D == 3 ? (((ch >> 2) & 1) ? sz.wh : sz.wl) : nullptr;
+  constexpr int NZ = D == 3 ? 3 : 1;
+  const AxisW sx = axis_weights(pn, pi, bcx == AF_BC_PERIODIC, ch & 1);
+  const AxisW sy = axis_weights(pn, pj, bcy == AF_BC_PERIODIC, (ch >> 1) & 1);
+  AxisW sz;
+  if constexpr (D == 3) sz = axis_weights(pn, pk, bcz == AF_BC_PERIODIC, (ch >> 2) & 1);
 #pragma unroll
   for (int m = 0; m < NC; ++m) out[m] = 0.0;
-  const int nz = D == 3 ? 3 : 1;
-  for (int ck = 0; ck < nz; ++ck) {
-    const double wk = D == 3 ? wz[ck] : 1.0;
+#pragma unroll
+  for (int ck = 0; ck < NZ; ++ck) {
+    const double wk = D == 3 ? axw_w(sz, ck) : 1.0;
     if (wk == 0.0) continue;
 #pragma unroll
     for (int cj = 0; cj < 3; ++cj) {
-      const double wjk = wy[cj] * wk;
+      const double wjk = axw_w(sy, cj) * wk;
       if (wjk == 0.0) continue;
 #pragma unroll
       for (int ci = 0; ci < 3; ++ci) {
-        const double w = wx[ci] * wjk;
+        const double w = axw_w(sx, ci) * wjk;
         if (w == 0.0) continue;
-        const long c = poff + mr_idx(D, pn, sx.pos[ci], sy.pos[cj], D == 3 ? sz.pos[ck] : 0);
+        const long c = poff + mr_idx(D, pn, axw_p(sx, ci), axw_p(sy, cj), D == 3 ? axw_p(sz, ck) : 0);
 #pragma unroll
         for (int m = 0; m < NC; ++m) out[m] = out[m] + V[m * comp + c] * w;
       }
@@ -195,25 +212,57 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
 // their parent level is in [lo, hi] — refresh_virtuals (mr_solver.cpp:195-208)
 // re-predicts only the virtual children of the stepping leaves.
 template <int D>
-__global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
+__device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, const uint8_t* vmark,
                                  MRLevels g, int l, int lo, int hi,
-    const int* tiles = nullptr, int ntiles = 0) {
+    const int* tiles, int ntiles) {
+  AF_ML_RESOLVE();
   constexpr int NC = D + 2;
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l);
   const long off = g.cell_off[l], poff = g.cell_off[l - 1];
   const long comp = g.total_cells;
   const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
+  const int bcx = g.bc[0], bcy = g.bc[2], bcz = g.bc[4];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
     if (st[off + c] != ST_ABSENT) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
     const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
     double q[NC];
-    predict_child<D>(V, comp, poff, pn, g.bc, i >> 1, j >> 1, k >> 1, ch, q);
+    predict_child<D>(V, comp, poff, pn, bcx, bcy, bcz, i >> 1, j >> 1, k >> 1, ch, q);
 #pragma unroll
     for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
   });
+}
+
+template <int D>
+__global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
+                                 MRLevels g, int l, int lo, int hi,
+    const int* tiles = nullptr, int ntiles = 0) {
+  predict_level_dev<D>(V, st, vmark, g, l, lo, hi, tiles, ntiles);
+}
+
+// All levels in one cooperative launch (grid-wide barrier between levels):
+// projection finest-first over [lo, top-1], prediction refresh coarsest-first.
+template <int D>
+__global__ void mr_project_all(double* V, const uint8_t* st, MRLevels g, int lo, int top,
+                               const int* band) {
+  cg::grid_group grid = cg::this_grid();
+  for (int l = top - 1; l >= lo; --l) {
+    if (g.band_cnt[l]) project_level_dev<D>(V, st, g, l, band + g.tile_off[l], g.band_cnt[l]);
+    grid.sync();
+  }
+}
+
+template <int D>
+__global__ void mr_predict_all(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
+                               int lo, int hi, const int* band) {
+  cg::grid_group grid = cg::this_grid();
+  for (int l = 1; l <= g.L; ++l) {
+    if (g.band_cnt[l])
+      predict_level_dev<D>(V, st, vmark, g, l, lo, hi, band + g.tile_off[l], g.band_cnt[l]);
+    grid.sync();
+  }
 }
 
 // ---------------------------------------------------------------- detail --
@@ -229,7 +278,7 @@ __device__ __forceinline__ double node_detail(const double* V, long comp, const 
   double mag = 0.0;
   for (int ch = 0; ch < (1 << D); ++ch) {
     double pred[NC];
-    predict_child<D>(V, comp, off, n, g.bc, i, j, k, ch, pred);
+    predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
     const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                                   D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
 #pragma unroll
@@ -249,6 +298,7 @@ template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
                                 int l, const double* norms,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l;
   const long cells = mr_cells(D, l), off = g.cell_off[l];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
@@ -265,13 +315,14 @@ template <int D>
 __global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
                                      MRLevels g, int l, double eps,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
     uint8_t f = 0;
     if (st[off + c] == ST_LEAF && l >= 1 && l < g.L) {
       const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-      f = det[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)] >= eps ? 1 : 0;
+      f = det[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)] >= (eps < 0.0 ? g.eps_l[l] : eps) ? 1 : 0;
     }
     flag[off + c] = f;
   });
@@ -281,6 +332,7 @@ template <int D>
 __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
                                 MRLevels g, int l, int r,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   // Target t is inserted iff some detail-flagged source s has map(s + o) == t
   // for an offset o != 0 with |o|_inf <= r. Clamping and folding never move a
   // position farther from s, so scanning the in-domain (or periodically
@@ -316,6 +368,7 @@ template <int D>
 __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels g, int l,
                                      int* changed,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
@@ -336,6 +389,7 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
 template <int D>
 __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
@@ -376,6 +430,7 @@ template <int D>
 __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
                                  const double* norms, int* merged,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
@@ -423,6 +478,7 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
 template <int D>
 __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
   level_cells<D>(g, l, tiles, ntiles, [&](long c) {
@@ -472,6 +528,7 @@ template <int D>
 __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
                                      double gamma, unsigned long long* target,
                                      const int* tiles = nullptr, int ntiles = 0) {
+  AF_ML_RESOLVE();
   __shared__ double red[8];
   const long off = g.cell_off[l], comp = g.total_cells;
   double best = 0.0;

@@ -21,7 +21,10 @@ struct MRStageArgs {
   double* out;         // stage output (leaves of this level)
   const uint8_t* st;
   double gamma, gm1;
-  double sdt;          // stage_dt
+  double sdt;          // stage_dt (or dt_scale * *dt_dev when dt_dev is set)
+  const double* dt_dev;
+  double dt_scale;
+  const int* step3_dev; // device copy of step3 (graph replay)
   int step3;           // error code base: 3*step; + stage-1 for pass 1, + 2 for post-step
   int stage;
   int post_check;      // stage 2: positivity of the completed step
@@ -29,6 +32,7 @@ struct MRStageArgs {
   unsigned long long* fb;    // fallbacks
   int* err;                  // [0] flag, [1] min code
   const int* tiles;
+  int ntiles;          // tiles in the list (or the leaf-list selector 1 in multi-level mode)
   // local time stepping: virtual leaves whose parent level is below `lo`
   // read as q_old*(1-theta) + q*theta (resolve, mr_solver.cpp:43-50)
   int lo, hi;
@@ -170,28 +174,34 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   uint8_t* leaf = ffb + K::NF;            // [NT] leaf mask
   __shared__ int s_fb, s_bad;
 
+  const int* tiles = a.tiles;
+  int ntiles = a.ntiles;
+  AF_ML_RESOLVE();
+  const double sdt = a.dt_dev ? a.dt_scale * *a.dt_dev : a.sdt;  // 0.5 * dt, 1.0 * dt == dt
+  const int step3 = a.step3_dev ? *a.step3_dev : a.step3;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = 1 << l;
   const long comp = g.total_cells, off = g.cell_off[l];
   const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
-  const int t = a.tiles[blockIdx.x];
-  const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
-  const int z0 = D == 3 ? (t / (ntx * nty)) * TZ : 0;
   const double gamma = a.gamma, gm1 = a.gm1;
   const double inv_dx = g.inv_dx[l];
   if (tid == 0) {
     s_fb = 0;
     s_bad = 0;
   }
-  // leaf mask of the tile cells
+  double wave = 0.0;  // accumulated over this block's tiles
+  int bad = 0, nfb = 0;
   const int tx = tid % TX, ty = (tid / TX) % TY, tz = D == 3 ? tid / (TX * TY) : 0;
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+  const int t = tiles[ti];
+  const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
+  const int z0 = D == 3 ? (t / (ntx * nty)) * TZ : 0;
+  // leaf mask of the tile cells
   const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
   const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
   const bool is_leaf = inside && a.st[own] == ST_LEAF;
   leaf[tid] = is_leaf;
-  double wave = 0.0;
-  int bad = 0;
   for (int idx = tid; idx < K::HP; idx += K::NT) {
     const int ix = idx % K::HX, iy = (idx / K::HX) % K::HY, iz = D == 3 ? idx / (K::HX * K::HY) : 0;
     const bool ccx = ix >= 2 && ix < TX + 2, ccy = iy >= 2 && iy < TY + 2;
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     if (!cell_ok(q, w)) bad = 1;
     double s, m;
     wave_speeds(w, gamma, s, m);
-    wave = m;
+    wave = fmax(wave, m);
   }
   __syncthreads();
   auto P = [&](int ix, int iy, int iz) {
@@ -318,8 +328,6 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     }
   }
   __syncthreads();
-  int nfb = 0;
-  double ssum = 0.0;
   if (is_leaf) {
     const int c[3] = {cx, cy, cz};
     double rhs[NC];
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     double o[NC];
 #pragma unroll
     for (int m = 0; m < NC; ++m) {
-      o[m] = a.base[m * comp + own] + rhs[m] * a.sdt;
+      o[m] = a.base[m * comp + own] + rhs[m] * sdt;
       a.out[m * comp + own] = o[m];
     }
     if (a.post_check) {  // positivity of the completed step (mr_solver.cpp:290-297)
@@ -414,7 +422,8 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
     }
   }
-  (void)ssum;
+  __syncthreads();  // the next tile reuses the shared-memory staging
+  }
   if (bad) atomicOr(&s_bad, bad);
   if (nfb) atomicAdd(&s_fb, nfb);
   block_max_atomic<K::NT>(wave, red, a.wave + l);
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       // stops the commit, so a pass-1 failure of a later level of the same
       // stage (which the reference reports first) is still detected
       atomicExch(a.err + ((s_bad & 1) ? 0 : 2), 1);
-      atomicMin(a.err + 1, a.step3 + ((s_bad & 1) ? a.stage - 1 : 2));
+      atomicMin(a.err + 1, step3 + ((s_bad & 1) ? a.stage - 1 : 2));
       atomicCAS(a.err + 3, 0, ((a.lo << 8) | a.hi) + 1);
     }
     if (s_fb) atomicAdd(a.fb, (unsigned long long)s_fb);
@@ -600,8 +609,9 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, i
 // before pass 2 completes); `promote` turns a post-step failure into a stop.
 template <int D>
 __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8_t* st,
-                                     MRLevels g, int l, const int* tiles, int ntiles,
-                                     const int* guard, int promote) {
+                                     MRLevels g, int l, const int* guard, int promote,
+                                     const int* tiles, int ntiles) {
+  AF_ML_RESOLVE();
   if (guard) {
     __shared__ int s;
     if (threadIdx.x == 0) s = guard[0] | guard[2];

@@ -19,7 +19,26 @@ struct MRLevels {
   // work tiles (2D 32x8, 3D 8x8x4 cells = 256 threads): per-level tile grid
   int ntx[17], nty[17], ntz[17];
   long tile_off[17];       // first tile of level l in the concatenated tile space
+  int band_cnt[17];        // tiles in the level's band list (host-filled)
+  int leaf_cnt[17];        // tiles in the level's leaf-tile list
+  double eps_l[17];        // refine threshold for leaves of level l (host-filled)
+  const int* dcnt;         // device copy of the counts: [l] band, [17 + l] leaf tiles
 };
+
+// Multi-level launch convention: a kernel called with l = -(l0 + 1) runs
+// level l0 + blockIdx.y, with `tiles` the base of the concatenated per-level
+// lists and `ntiles` selecting the band (0) or leaf (1) list counts.
+// The counts are read from device memory (g.dcnt) so a launch's parameters
+// do not change from cycle to cycle (CUDA-graph replay). A single-level launch
+// may pass ntiles = -1 (band) / -2 (leaf tiles) to read its count likewise.
+#define AF_ML_RESOLVE()                                      \
+  if (l < 0) {                                               \
+    l = -l - 1 + (int)blockIdx.y;                            \
+    tiles += g.tile_off[l];                                  \
+    ntiles = ntiles ? g.dcnt[17 + l] : g.dcnt[l];            \
+  } else if (ntiles < 0) {                                   \
+    ntiles = ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l];      \
+  }
 
 constexpr int kTileX2 = 32, kTileY2 = 8;
 constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
