@@ -120,8 +120,20 @@ struct Fv3d {
   static constexpr int UX = (NXF + 31) / 32, UY = (NYF + 31) / 32;
   static constexpr int NC = 5;  // primitives per cell in the ring: rho, v0, v1, v2, p
   static constexpr size_t smem_bytes =
-      sizeof(double) * (size_t)(4 * NC * HP + 5 * NXF + 5 * NYF + NW);
+      sizeof(double) * (size_t)(4 * NC * HP + 5 * NXF + 5 * NYF + NW + 5 * HP);
 };
+
+// cp.async (LDGSTS) of one double: global -> shared, completion tracked per thread.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
 
 template <int LIM, int TX, int TY>
 __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
@@ -133,6 +145,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   double* fxs = ring + 4 * K::NC * K::HP;      // [5][NXF]
   double* fys = fxs + 5 * K::NXF;              // [5][NYF]
   double* red = fys + 5 * K::NYF;              // [NW]
+  double* raw = red + K::NW;                   // [5][HP] conserved plane in flight (cp.async)
   __shared__ int s_fb, s_bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -155,11 +168,13 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   double ssum = 0.0;  // stage 2: max of sum_a(|v_a|+c) over the updated cells
   int bad = 0;
 
-  auto load_plane = [&](int gz) {
+  // Plane gz of eval -> primitives of ring slot gz&3, in two halves so the
+  // global loads of plane k+3 overlap the flux work of plane k: issue_plane
+  // starts cp.async copies of the conserved values of this thread's cells,
+  // convert_plane (same thread, same cells) turns them into primitives.
+  auto issue_plane = [&](int gz) {
     bool fz;
     const int zl = slab_map(gz, g, 2, fz);
-    double* dst = ring + ((gz + 4) & 3) * (K::NC * K::HP);
-    const bool own = gz >= zc0 && gz < zc1;
     for (int idx = tid; idx < K::HP; idx += K::NT) {
       const int ix = idx % K::HX, iy = idx / K::HX;
       const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
@@ -168,12 +183,30 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
       const int mx = bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
       const int my = bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
       const long off = (long)zl * zs + (long)my * n + mx;
+#pragma unroll
+      for (int m = 0; m < 5; ++m) cp_async8(raw + m * K::HP + idx, ev + m * cs + off);
+    }
+    cp_async_commit();
+  };
+  auto convert_plane = [&](int gz) {
+    cp_async_wait_all();
+    bool fz;
+    (void)slab_map(gz, g, 2, fz);
+    double* dst = ring + ((gz + 4) & 3) * (K::NC * K::HP);
+    const bool own = gz >= zc0 && gz < zc1;
+    for (int idx = tid; idx < K::HP; idx += K::NT) {
+      const int ix = idx % K::HX, iy = idx / K::HX;
+      const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
+      if (!cx && !cy) continue;
+      bool fx, fy;
+      (void)bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
+      (void)bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
       Cons<D> q;
-      q.rho = __ldg(ev + off);
-      q.m[0] = __ldg(ev + cs + off);
-      q.m[1] = __ldg(ev + 2 * cs + off);
-      q.m[2] = __ldg(ev + 3 * cs + off);
-      q.E = __ldg(ev + 4 * cs + off);
+      q.rho = raw[idx];
+      q.m[0] = raw[K::HP + idx];
+      q.m[1] = raw[2 * K::HP + idx];
+      q.m[2] = raw[3 * K::HP + idx];
+      q.E = raw[4 * K::HP + idx];
       Prim<D> w = primitives(q, gm1);
       if (own && cx && cy) {
         if (!cell_ok(q, w)) bad = 1;
@@ -226,8 +259,13 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     return ausm_plus<D, 2>(ql.E, l, qr.E, r, gamma);
   };
 
-  // Prologue: planes zc0-2 .. zc0+1 and the chunk's first low z face.
-  for (int z = zc0 - 2; z < zc0 + 2; ++z) load_plane(z);
+  // Prologue: planes zc0-2 .. zc0+1 and the chunk's first low z face; the
+  // copies of plane zc0+2 are put in flight.
+  for (int z = zc0 - 2; z < zc0 + 2; ++z) {
+    issue_plane(z);
+    convert_plane(z);
+  }
+  issue_plane(zc0 + 2);
   __syncthreads();
   Cons<D> fz_lo = zface(zc0);
 
@@ -237,7 +275,8 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     double b[5];
 #pragma unroll
     for (int m = 0; m < 5; ++m) b[m] = a.base[m * cs + own];
-    load_plane(k + 2);
+    convert_plane(k + 2);                  // landed during the previous plane's work
+    if (k + 3 < zc1 + 2) issue_plane(k + 3);  // in flight during this plane's work
     __syncthreads();
     const Cons<D> fz_hi = zface(k + 1);
     for (int u = warp; u < K::UX + K::UY; u += K::NW) {
