@@ -157,6 +157,16 @@ af_status af_uniform_last_error(const af_uniform* u, af_error* err);
 /* Number of libafgpu kernels launched by this solver since creation. */
 af_status af_uniform_kernel_launches(const af_uniform* u, long* count);
 
+/* Local emulation of an n-rank slab decomposition on ONE GPU: creates the n
+ * rank solvers (rank r owns the slab af_uniform_local_extent reports), and
+ * runs them in lockstep on rank 0's stream. Halos move by device-to-device
+ * copies and the CFL maximum is reduced over the ranks' records, so
+ * everything per rank is the multi-GPU code path except the NCCL transport.
+ * Used to check that results are bitwise independent of the rank count. */
+af_status af_uniform_create_group(const af_config* cfg, int n_ranks, af_uniform** ranks);
+af_status af_uniform_run_group(af_uniform** ranks, int n_ranks, long n_steps, double cfl,
+                               double fixed_dt, double* dt_hist, af_run_diag* diag);
+
 /* -------------------------------------------------------------------- MR -- */
 /* Adaptive multiresolution solver: MRTree (mr_tree.hpp:57-196) + MRSolver
  * (mr_solver.hpp:15-58) + the run_mr loop (mr_solver.hpp:78-79), on per-level

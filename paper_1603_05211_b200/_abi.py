@@ -79,6 +79,9 @@ SIGNATURES = {
     "af_uniform_sync": (C.c_int, [_vp]),
     "af_uniform_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
     "af_uniform_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+    "af_uniform_create_group": (C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(_vp)]),
+    "af_uniform_run_group": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_long, C.c_double, C.c_double,
+                                       _dp, C.POINTER(RunDiag)]),
     "af_mr_create": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), C.POINTER(_vp)]),
     "af_mr_destroy": (C.c_int, [_vp]),
     "af_mr_set_stream": (C.c_int, [_vp, _vp]),

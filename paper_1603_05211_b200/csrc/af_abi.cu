@@ -6,6 +6,7 @@
 
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "af_cases.h"
 #include "af_comm.h"
@@ -15,6 +16,7 @@
 
 struct af_uniform {
   af::Uniform* impl;
+  af::Comm* owned_comm = nullptr;  // local-group rank descriptor
 };
 
 struct af_mr {
@@ -122,8 +124,46 @@ af_status af_uniform_create(const af_config* cfg, af_comm* comm, af_uniform** ou
 af_status af_uniform_destroy(af_uniform* u) {
   if (!u) return AF_OK;
   delete u->impl;
+  delete u->owned_comm;
   delete u;
   return AF_OK;
+}
+
+af_status af_uniform_create_group(const af_config* cfg, int n_ranks, af_uniform** ranks) {
+  return guard(nullptr, [&] {
+    if (!cfg || !ranks || n_ranks < 1 || n_ranks > 16)
+      throw af::Error(AF_E_ARGUMENT, "af_uniform_create_group: bad argument");
+    for (int r = 0; r < n_ranks; ++r) ranks[r] = nullptr;
+    try {
+      for (int r = 0; r < n_ranks; ++r) {
+        auto* h = new af_uniform;
+        h->impl = nullptr;
+        h->owned_comm = new af::Comm;
+        h->owned_comm->n = n_ranks;
+        h->owned_comm->rank = r;
+        h->owned_comm->device = cfg->device;
+        h->owned_comm->local = true;
+        ranks[r] = h;
+        h->impl = new af::Uniform(*cfg, h->owned_comm);
+      }
+    } catch (...) {
+      for (int r = 0; r < n_ranks; ++r)
+        if (ranks[r]) af_uniform_destroy(ranks[r]);
+      throw;
+    }
+  });
+}
+
+af_status af_uniform_run_group(af_uniform** ranks, int n_ranks, long n_steps, double cfl,
+                               double fixed_dt, double* dt_hist, af_run_diag* diag) {
+  if (!ranks || n_ranks < 1) return record(nullptr, AF_E_ARGUMENT, "null group");
+  std::vector<af::Uniform*> R(n_ranks);
+  for (int r = 0; r < n_ranks; ++r) {
+    if (!ranks[r] || !ranks[r]->impl) return record(nullptr, AF_E_ARGUMENT, "null rank");
+    R[r] = ranks[r]->impl;
+  }
+  return guard(&R[0]->last_error(),
+               [&] { af::Uniform::run_group(R, n_steps, cfl, fixed_dt, dt_hist, diag); });
 }
 
 #define AF_U_GUARD(body)                                                     \

@@ -10,6 +10,7 @@ struct Comm {
   int n = 1;
   int rank = 0;
   int device = 0;
+  bool local = false;  // ranks emulated in one process on one GPU (af_uniform_create_group)
 };
 
 }  // namespace af

@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kGrid = 148 * 8;
 constexpr int kGridFixed = 148 * 2;  // graph replay: grid-stride over device-side counts
+constexpr int kSmallTiles = 64;      // levels with at most this many tiles: cooperative launch
 
 inline unsigned grid_for(long n, int block = 256) {
   long b = (n + block - 1) / block;
@@ -157,6 +158,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   }
   g_.cell_off[L_ + 1] = tot;
   g_.total_cells = tot;
+  for (int l = 0; l <= L_; ++l) g_.eps_l[l] = eps_at_(l);
   const size_t vbytes = sizeof(double) * NC_ * tot;
   AF_CUDA(cudaMalloc(&d_st_, tot));
   AF_CUDA(cudaMalloc(&d_mark_, tot));
@@ -194,6 +196,12 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   }
   tile_off_[L_ + 1] = toff;
   g_.tile_off[L_ + 1] = toff;
+  // coarse levels with few tiles go through the single cooperative launches
+  small_hi_ = -1;
+  if (!std::getenv("AF_MR_NO_SMALL"))
+    for (int l = 0; l <= L_; ++l)
+      if ((long)g_.ntx[l] * g_.nty[l] * g_.ntz[l] <= kSmallTiles) small_hi_ = l;
+  small_coarsen_ = std::getenv("AF_MR_SMALL_COARSEN") != nullptr;
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
@@ -318,18 +326,41 @@ int MR::coop_blocks_() {
 // l reads level l-1 only, so after values of levels [lo, hi] change (stage
 // commit + projection) the refresh starts at lo+1.
 void MR::predict_fill_(int lo, int hi, int from) {
-  for (int l = std::max(1, from); l <= L_; ++l)
+  const int f = std::max(1, from);
+  const uint8_t* vm = virtuals_ ? d_mark_ : nullptr;
+  if (f <= small_hi_) {
+    const int to = std::min(small_hi_, L_);
+    if (D_ == 3)
+      coop_launch(mr_predict_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm, g_,
+                  f, to, lo, hi, (const int*)d_band_);
+    else
+      coop_launch(mr_predict_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm, g_,
+                  f, to, lo, hi, (const int*)d_band_);
+    ++launches_;
+  }
+  for (int l = std::max(f, small_hi_ + 1); l <= L_; ++l)
     if (AF_HAS(band_count_[l]))
-      AF_MR_LAUNCH(mr_predict_level, AF_TGRID(band_count_[l]), d_V_, d_st_,
-                   virtuals_ ? d_mark_ : nullptr, g_, l, lo, hi, AF_BAND(l));
+      AF_MR_LAUNCH(mr_predict_level, AF_TGRID(band_count_[l]), d_V_, d_st_, vm, g_, l, lo, hi,
+                   AF_BAND(l));
   fresh_ = (!virtuals_ || (lo == 0 && hi >= L_)) && from <= 1;
 }
 
 // project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
 void MR::project_range_(int lo, int top) {
-  for (int l = std::min(top - 1, L_ - 1); l >= lo; --l)
+  const int hi = std::min(top - 1, L_ - 1);
+  for (int l = hi; l >= std::max(lo, small_hi_ + 1); --l)
     if (AF_HAS(band_count_[l]))
       AF_MR_LAUNCH(mr_project_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+  const int shi = std::min(hi, small_hi_);
+  if (shi >= lo) {
+    if (D_ == 3)
+      coop_launch(mr_project_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_, shi,
+                  lo, (const int*)d_band_);
+    else
+      coop_launch(mr_project_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_, shi,
+                  lo, (const int*)d_band_);
+    ++launches_;
+  }
   fresh_ = false;
 }
 
@@ -840,10 +871,21 @@ void MR::coarsen() {
   }
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
-    for (int l = L_ - 1; l >= min_leaf_; --l)
+    const int csm = small_coarsen_ ? small_hi_ : -1;
+    for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l)
       if (band_count_[l])
         AF_MR_LAUNCH(mr_coarsen_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l,
                      eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
+    const int shi = std::min(L_ - 1, csm);
+    if (shi >= min_leaf_) {
+      if (D_ == 3)
+        coop_launch(mr_coarsen_small<3>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
+                    min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
+      else
+        coop_launch(mr_coarsen_small<2>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
+                    min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
+      ++launches_;
+    }
     int merged = 0;
     AF_CUDA(cudaMemcpyAsync(&merged, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));

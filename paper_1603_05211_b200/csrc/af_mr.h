@@ -49,6 +49,8 @@ class MR {
   int coop_blocks_();
   void cycle_stats_(long* leaves, long* nodes, double* smax);
   int coop_blocks_cache_ = 0;
+  int small_hi_ = 0;
+  bool small_coarsen_ = false;  // coarsest levels [0, small_hi_] use the cooperative small-level kernels
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);
   void build_registers_(int top);

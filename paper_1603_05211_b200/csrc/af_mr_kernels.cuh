@@ -427,9 +427,9 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
 // an INTERNAL node at level l >= min_leaf merges iff all children are leaves,
 // detail < eps_{l+1}, and no face-ring cell at level l+1 is INTERNAL.
 template <int D>
-__global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
+__device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, MRLevels g, int l, double eps,
                                  const double* norms, int* merged,
-    const int* tiles = nullptr, int ntiles = 0) {
+    const int* tiles, int ntiles) {
   AF_ML_RESOLVE();
   const int n = 1 << l, nf = n << 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
@@ -470,6 +470,47 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
                        D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] = ST_ABSENT;
     *merged = 1;
   });
+}
+
+template <int D>
+__global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
+                                 const double* norms, int* merged,
+    const int* tiles = nullptr, int ntiles = 0) {
+  coarsen_level_dev<D>(V, st, g, l, eps, norms, merged, tiles, ntiles);
+}
+
+// The coarse levels (a few tiles each) in one cooperative launch with a
+// grid-wide barrier between levels: their per-level work is shorter than a
+// kernel launch, and the level order (prediction coarsest-first, projection
+// and coarsening finest-first) is kept by the barrier.
+template <int D>
+__global__ void mr_predict_small(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
+                                 int lfrom, int lto, int lo, int hi, const int* band) {
+  cg::grid_group grid = cg::this_grid();
+  for (int l = lfrom; l <= lto; ++l) {
+    predict_level_dev<D>(V, st, vmark, g, l, lo, hi, band + g.tile_off[l], -1);
+    grid.sync();
+  }
+}
+
+template <int D>
+__global__ void mr_project_small(double* V, const uint8_t* st, MRLevels g, int lhigh, int llow,
+                                 const int* band) {
+  cg::grid_group grid = cg::this_grid();
+  for (int l = lhigh; l >= llow; --l) {
+    project_level_dev<D>(V, st, g, l, band + g.tile_off[l], -1);
+    grid.sync();
+  }
+}
+
+template <int D>
+__global__ void mr_coarsen_small(const double* V, uint8_t* st, MRLevels g, int lhigh, int llow,
+                                 const double* norms, int* merged, const int* band) {
+  cg::grid_group grid = cg::this_grid();
+  for (int l = lhigh; l >= llow; --l) {
+    coarsen_level_dev<D>(V, st, g, l, g.eps_l[l + 1], norms, merged, band + g.tile_off[l], -1);
+    grid.sync();
+  }
 }
 
 // Virtual-leaf count (add_virtual_leaves, mr_tree.cpp:513-551): a level-(l-1)

@@ -219,6 +219,7 @@ void Uniform::download(double* aos) {
 // NCCL message per direction (per-plane SoA keeps them contiguous).
 void Uniform::exchange_halos_(double* q) {
   if (!comm_ || comm_->n == 1) return;
+  if (comm_->local) throw Error(AF_E_ARGUMENT, "ranks of a local group run via af_uniform_run_group");
   const int r = comm_->rank, P = comm_->n;
   const bool periodic = g_.bc[2 * (g_.dim - 1)] == AF_BC_PERIODIC &&
                         g_.bc[2 * (g_.dim - 1) + 1] == AF_BC_PERIODIC;
@@ -329,7 +330,134 @@ void Uniform::enqueue_steps_(long n_steps, double cfl, double fixed_dt) {
   }
 }
 
+namespace {
+struct GroupPtrs {
+  unsigned long long* p[16];
+};
+__global__ void group_max_kernel(GroupPtrs g, int n) {
+  unsigned long long m = 0;
+  for (int r = 0; r < n; ++r) m = m > *g.p[r] ? m : *g.p[r];
+  for (int r = 0; r < n; ++r) *g.p[r] = m;
+}
+}  // namespace
+
+void Uniform::run_group(const std::vector<Uniform*>& R, long n_steps, double cfl,
+                        double fixed_dt, double* dt_hist, af_run_diag* rd) {
+  const int P = (int)R.size();
+  if (P < 1 || P > 16) throw Error(AF_E_ARGUMENT, "group size must be in [1, 16]");
+  if (!(cfl > 0.0) && !(fixed_dt > 0.0))
+    throw Error(AF_E_ARGUMENT, "either cfl or fixed_dt must be positive");
+  cudaStream_t st = R[0]->stream_;
+  std::vector<StageArgs> A(P);
+  for (int r = 0; r < P; ++r) {
+    Uniform& u = *R[r];
+    u.stream_ = st;
+    u.ensure_records_(n_steps);
+    AF_CUDA(cudaMemsetAsync(u.rec_.smax, 0, 8 * (n_steps + 1), st));
+    AF_CUDA(cudaMemsetAsync(u.rec_.wave_u, 0, 8 * n_steps, st));
+    AF_CUDA(cudaMemsetAsync(u.rec_.wave_mid, 0, 8 * n_steps, st));
+    AF_CUDA(cudaMemsetAsync(u.rec_.fb, 0, 8 * n_steps, st));
+    StageArgs& a = A[r];
+    a = StageArgs{};
+    a.dx = u.dx_;
+    a.inv_dx = u.inv_dx_;
+    a.gamma = u.cfg_.gamma;
+    a.gm1 = u.cfg_.gamma - 1.0;
+    a.cfl = cfl;
+    a.fixed_dt = fixed_dt;
+    a.use_cfl = cfl > 0.0 ? 1 : 0;
+    a.r = u.rec_;
+    a.r.err = u.d_err_;
+  }
+  const UGrid& g0 = R[0]->g_;
+  const int axis = g0.dim - 1;
+  const bool periodic = g0.bc[2 * axis] == AF_BC_PERIODIC && g0.bc[2 * axis + 1] == AF_BC_PERIODIC;
+  // halo planes of buffer `which` (0 = u, 1 = mid) between neighbouring slabs
+  auto exchange = [&](int which) {
+    for (int r = 0; r < P; ++r) {
+      const int hi = r < P - 1 ? r + 1 : (periodic ? 0 : -1);
+      if (hi < 0 || P == 1) continue;
+      Uniform& a = *R[r];
+      Uniform& b = *R[hi];
+      double* qa = which ? a.d_mid_ : a.d_u_;
+      double* qb = which ? b.d_mid_ : b.d_u_;
+      const size_t bytes = sizeof(double) * 2 * a.g_.zs;
+      // a's top two planes -> b's low halo; b's bottom two planes -> a's high halo
+      AF_CUDA(cudaMemcpyAsync(qb, qa + (long)a.g_.nzl * a.g_.zs, bytes, cudaMemcpyDeviceToDevice, st));
+      AF_CUDA(cudaMemcpyAsync(qa + (long)(a.g_.nzl + 2) * a.g_.zs, qb + 2 * b.g_.zs, bytes,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+  };
+  auto group_max = [&](long slot) {
+    GroupPtrs gp{};
+    for (int r = 0; r < P; ++r) gp.p[r] = R[r]->rec_.smax + slot;
+    group_max_kernel<<<1, 1, 0, st>>>(gp, P);
+    AF_CUDA(cudaGetLastError());
+  };
+  if (cfl > 0.0) {
+    for (int r = 0; r < P; ++r) R[r]->launch_speed_sum_(R[r]->d_u_, R[r]->rec_.smax);
+    group_max(0);
+  }
+  for (long s = 0; s < n_steps; ++s) {
+    exchange(0);
+    for (int r = 0; r < P; ++r) {
+      StageArgs& a = A[r];
+      a.step = (int)s;
+      a.stage = 1;
+      a.dt_scale = 0.5;
+      a.eval = R[r]->d_u_;
+      a.base = R[r]->d_u_;
+      a.out = R[r]->d_mid_;
+      R[r]->launch_stage_(a);
+    }
+    exchange(1);
+    for (int r = 0; r < P; ++r) {
+      StageArgs& a = A[r];
+      a.stage = 2;
+      a.dt_scale = 1.0;
+      a.eval = R[r]->d_mid_;
+      a.base = R[r]->d_u_;
+      a.out = R[r]->d_u_;
+      R[r]->launch_stage_(a);
+    }
+    if (cfl > 0.0) group_max(s + 1);
+  }
+  // per-rank records -> the run's diagnostics (max/sum over ranks)
+  af_run_diag total{};
+  for (int r = 0; r < P; ++r) {
+    af_run_diag d{};
+    std::vector<double> dts(n_steps);
+    R[r]->collect_(n_steps, dts.data(), &d, nullptr);
+    if (r == 0 && dt_hist) std::memcpy(dt_hist, dts.data(), sizeof(double) * n_steps);
+    total.max_wave_speed = std::max(total.max_wave_speed, d.max_wave_speed);
+    total.fallbacks += d.fallbacks;
+    total.steps_done = d.steps_done;
+    total.t = d.t;
+  }
+  // max_cfl from the combined per-step wave maxima (unigrid.cpp:43)
+  if (rd) {
+    std::vector<double> ms(n_steps, 0.0), dts(n_steps);
+    for (int r = 0; r < P; ++r) {
+      std::vector<unsigned long long> wu(n_steps), wm(n_steps);
+      AF_CUDA(cudaMemcpy(wu.data(), R[r]->rec_.wave_u, 8 * n_steps, cudaMemcpyDeviceToHost));
+      AF_CUDA(cudaMemcpy(wm.data(), R[r]->rec_.wave_mid, 8 * n_steps, cudaMemcpyDeviceToHost));
+      if (r == 0) AF_CUDA(cudaMemcpy(dts.data(), R[0]->rec_.dt, 8 * n_steps, cudaMemcpyDeviceToHost));
+      for (long s = 0; s < n_steps; ++s) {
+        double a, b;
+        std::memcpy(&a, &wu[s], 8);
+        std::memcpy(&b, &wm[s], 8);
+        ms[s] = std::max(ms[s], std::max(a, b));
+      }
+    }
+    double mc = 0.0;
+    for (long s = 0; s < n_steps; ++s) mc = std::max(mc, ms[s] * dts[s] / R[0]->dx_);
+    total.max_cfl = mc;
+    *rd = total;
+  }
+}
+
 void Uniform::allreduce_max_(unsigned long long* bits) {
+  if (comm_->local) throw Error(AF_E_ARGUMENT, "ranks of a local group run via af_uniform_run_group");
   // max of non-negative doubles == max of their bit patterns
   const ncclResult_t e = ncclAllReduce(bits, bits, 1, ncclUint64, ncclMax, comm_->nccl, stream_);
   if (e != ncclSuccess) throw Error(AF_E_NCCL, ncclGetErrorString(e));

@@ -2,6 +2,8 @@
 #pragma once
 
 #include "af_comm.h"
+#include <vector>
+
 #include "af_internal.h"
 
 namespace af {
@@ -22,6 +24,12 @@ class Uniform {
   void run(long n_steps, double cfl, double fixed_dt, double* dt_hist, af_run_diag* diag);
   double speed_sum();
   void sync();
+  // Lockstep run of a locally emulated slab decomposition (all ranks on one
+  // GPU and one stream; halos move by device-to-device copies, the CFL
+  // reduction by a max over the ranks' records). Exercises exactly the
+  // per-rank code of the NCCL path except the transport itself.
+  static void run_group(const std::vector<Uniform*>& ranks, long n_steps, double cfl,
+                        double fixed_dt, double* dt_hist, af_run_diag* diag);
 
   const UGrid& grid() const { return g_; }
   long launches() const { return launches_; }

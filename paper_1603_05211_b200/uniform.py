@@ -203,3 +203,75 @@ def run_uniform(init: np.ndarray, dim: int, level: int, n_steps: int, cfl: float
         return s.download(), rep
     finally:
         s.close()
+
+
+class UniformGroup:
+    """n_ranks slabs of one mesh emulated on ONE GPU (af_uniform_create_group):
+    the per-rank multi-GPU code path (slab extents, halo planes, boundary
+    handling at slab edges, the CFL max over ranks) with device-to-device
+    copies in place of NCCL. Used to check rank-count independence."""
+
+    def __init__(self, dim: int, level: int, n_ranks: int, scheme: SchemeConfig | None = None,
+                 bc=None, gamma: float = 1.4, device: int = 0):
+        self._lib = _abi.load()
+        scheme = scheme or SchemeConfig()
+        cfg = _abi.Config()
+        cfg.dim, cfg.level, cfg.origin, cfg.extent, cfg.gamma = dim, level, 0.0, 1.0, gamma
+        for f in range(6):
+            cfg.bc[f] = OUTFLOW if bc is None else int(bc[f])
+        cfg.flux, cfg.limiter, cfg.integrator = scheme.flux, scheme.limiter, scheme.integrator
+        cfg.device = device
+        self.n_ranks, self.dim, self.level, self.n = n_ranks, dim, level, 1 << level
+        self._h = (C.c_void_p * n_ranks)()
+        st = self._lib.af_uniform_create_group(C.byref(cfg), n_ranks, self._h)
+        if st:
+            e = _abi.ErrorRec()
+            self._lib.af_uniform_last_error(None, C.byref(e))
+            raise_status(st, e.message.decode())
+        self.extents = []
+        for r in range(n_ranks):
+            z0, nz = C.c_int(), C.c_int()
+            self._lib.af_uniform_local_extent(self._h[r], C.byref(z0), C.byref(nz))
+            self.extents.append((z0.value, nz.value))
+        self.row = self.n ** (dim - 1)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            for r in range(self.n_ranks):
+                self._lib.af_uniform_destroy(self._h[r])
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, r=0):
+        if st:
+            e = _abi.ErrorRec()
+            self._lib.af_uniform_last_error(self._h[r], C.byref(e))
+            raise_status(st, e.message.decode())
+
+    def upload(self, aos: np.ndarray) -> None:
+        for r, (z0, nz) in enumerate(self.extents):
+            part = np.ascontiguousarray(aos[z0 * self.row:(z0 + nz) * self.row])
+            self._check(self._lib.af_uniform_upload(self._h[r], C.c_void_p(part.ctypes.data)), r)
+
+    def download(self) -> np.ndarray:
+        out = np.empty((self.n ** self.dim, 5), dtype=np.float64)
+        for r, (z0, nz) in enumerate(self.extents):
+            part = np.empty((nz * self.row, 5), dtype=np.float64)
+            self._check(self._lib.af_uniform_download(self._h[r], C.c_void_p(part.ctypes.data)), r)
+            out[z0 * self.row:(z0 + nz) * self.row] = part
+        return out
+
+    def run(self, n_steps: int, cfl: float = 0.0, fixed_dt: float = 0.0) -> RunReport:
+        dts = np.zeros(max(n_steps, 1), dtype=np.float64)
+        d = _abi.RunDiag()
+        self._check(self._lib.af_uniform_run_group(
+            self._h, self.n_ranks, n_steps, cfl, fixed_dt,
+            dts.ctypes.data_as(C.POINTER(C.c_double)), C.byref(d)))
+        return RunReport(level=self.level, n_steps=n_steps, max_cfl=d.max_cfl,
+                         max_wave_speed=d.max_wave_speed, fallbacks=d.fallbacks, t=d.t,
+                         dt=dts[:n_steps])
