@@ -184,6 +184,15 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
     return rate, sample, wall
 
 
+def host_threads(req: int) -> int:
+    """Cores this process may run on (cgroup/affinity aware), capped by `req` if > 0."""
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count() or 1
+    return max(1, min(avail, req) if req > 0 else avail)
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's own CPU implementation (rank 0 only)."""
     if rank != 0:
@@ -193,7 +202,7 @@ def run_reference_arm(args, rank, world):
     if kind == "port" and not O.available("port"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle libraries not built"}))
         return
-    threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+    threads = host_threads(args.cpu_threads)
     rate, sample, wall = reference_cpu_rate(kind, args.workload, max(1, args.steps),
                                             max(0, args.warmup), threads,
                                             level_override=args.ref_level)
@@ -242,7 +251,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-threads", type=int, default=8)
+    ap.add_argument("--cpu-threads", type=int, default=0,
+                    help="host threads for the CPU legs (0 = every core this process may use)")
     ap.add_argument("--ref-level", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -384,7 +394,7 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
         try:
             from oracle import oracle as O
             kind = "reference" if O.available("ref") else "port"
-            threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+            threads = host_threads(args.cpu_threads)
             rate, sample, _ = reference_cpu_rate(kind, args.workload, 2, 1, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
                    "sample": sample}
@@ -498,7 +508,7 @@ def mr_bench(args, rank, world, local, torch, dist):
         try:
             from oracle import oracle as O
             kind = "reference" if O.available("ref") else "port"
-            threads = max(1, min(os.cpu_count() or 1, args.cpu_threads))
+            threads = host_threads(args.cpu_threads)
             rate, sample, _ = reference_cpu_rate(kind, args.workload, 8, 2, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
         except Exception as e:
