@@ -47,7 +47,8 @@ typedef enum af_status {
   AF_E_CUDA = 5,              /* CUDA runtime failure (no reference equivalent) */
   AF_E_NCCL = 6,              /* NCCL failure */
   AF_E_ARGUMENT = 7,          /* invalid argument / null pointer */
-  AF_E_UNSUPPORTED = 8        /* option outside the hot path (e.g. AUSMDV) */
+  AF_E_UNSUPPORTED = 8,       /* option outside the hot path (e.g. AUSMDV) */
+  AF_E_INTERNAL = 9           /* internal invariant check failed (debug switches) */
 } af_status;
 
 enum { AF_BC_OUTFLOW = 0, AF_BC_PERIODIC = 1, AF_BC_REFLECTIVE = 2 }; /* BcKind grid.hpp:70 */

@@ -21,6 +21,7 @@ AF_E_CUDA = 5
 AF_E_NCCL = 6
 AF_E_ARGUMENT = 7
 AF_E_UNSUPPORTED = 8
+AF_E_INTERNAL = 9
 
 
 class Config(C.Structure):

@@ -178,7 +178,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   AF_CUDA(cudaMalloc(&d_det_, sizeof(double) * tot));
   AF_CUDA(cudaMalloc(&d_norms_, sizeof(double) * 5));
   AF_CUDA(cudaMalloc(&d_err_, 4 * sizeof(int)));
-  AF_CUDA(cudaMalloc(&d_flagi_, sizeof(int)));
+  AF_CUDA(cudaMalloc(&d_flagi_, 2 * sizeof(int)));
   AF_CUDA(cudaMalloc(&d_red_, sizeof(unsigned long long) * (64 + 17 * kMaxStageRecords)));
   tile_off_.assign(L_ + 2, 0);
   tile_count_.assign(L_ + 1, 0);
@@ -202,6 +202,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
     for (int l = 0; l <= L_; ++l)
       if ((long)g_.ntx[l] * g_.nty[l] * g_.ntz[l] <= kSmallTiles) small_hi_ = l;
   small_coarsen_ = std::getenv("AF_MR_SMALL_COARSEN") != nullptr;
+  full_sweeps_ = std::getenv("AF_MR_FULL_SWEEPS") != nullptr;
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
@@ -273,10 +274,10 @@ double MR::eps_at_(int child_level) const {
   } while (0)
 
 // multi-level launch of a per-level kernel over levels [lo, hi] (band or leaf lists)
-#define AF_ML_LAUNCH(kern, lo, hi, leaf, ...)                                      \
+#define AF_ML_LAUNCH_M(kern, lo, hi, leaf, mult, ...)                                    \
   do {                                                                             \
     dim3 grid_;                                                                    \
-    if (ml_grid_((lo), (hi), (leaf), &grid_)) {                                    \
+    if (ml_grid_((lo), (hi), (leaf), &grid_, (mult))) {                           \
       const int AF_L = -(std::max((lo), 0) + 1);                                   \
       const int* AF_T = (leaf) ? d_tiles_ : d_band_;                               \
       const int AF_S = (leaf) ? 1 : 0;                                             \
@@ -288,6 +289,8 @@ double MR::eps_at_(int child_level) const {
       AF_CUDA(cudaGetLastError());                                                 \
     }                                                                              \
   } while (0)
+
+#define AF_ML_LAUNCH(kern, lo, hi, leaf, ...) AF_ML_LAUNCH_M(kern, lo, hi, leaf, 1, __VA_ARGS__)
 
 // band / leaf tile list of level l and a grid for it
 #define AF_BAND(l) d_band_ + tile_off_[l], (fixed_grids_ ? -1 : band_count_[l])
@@ -396,7 +399,7 @@ void MR::build_lists_() {
 
 // Grid of a multi-level launch over levels [lo, hi] (AF_ML_RESOLVE): x spans
 // the largest list, y the levels. Returns false when every list is empty.
-bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid) const {
+bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult) const {
   if (fixed_grids_) {  // graph capture: parameters independent of this cycle's counts
     if (hi < lo) return false;
     *grid = dim3((unsigned)kGridFixed, (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
@@ -406,7 +409,7 @@ bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid) const {
   for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l)
     mx = std::max(mx, leaf ? tile_count_[l] : band_count_[l]);
   if (!mx || hi < lo) return false;
-  *grid = dim3((unsigned)std::min(mx, kGrid), (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
+  *grid = dim3((unsigned)std::min(mx * mult, kGrid), (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
   return true;
 }
 
@@ -457,7 +460,7 @@ void MR::refine(int top) {
   if (!lists_valid_) build_lists_();
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
   AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
-  AF_ML_LAUNCH(mr_detail_level, 0, L_ - 2, false, d_V_, d_st_, d_det_, g_, AF_L, d_norms_);
+  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L, d_norms_);
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
   AF_ML_LAUNCH(mr_refine_flag_level, 1, L_ - 1, false, d_st_, d_det_, d_flag_, g_, AF_L, -1.0);
   uint8_t* split = d_flag_;
@@ -869,12 +872,13 @@ void MR::coarsen() {
     build_lists_();
     lists_valid_ = true;
   }
+  bool clean = false;  // the previous sweep raised no re-sweep flag
   for (;;) {
-    AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
+    AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
     const int csm = small_coarsen_ ? small_hi_ : -1;
     for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l)
       if (band_count_[l])
-        AF_MR_LAUNCH(mr_coarsen_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l,
+        AF_MR_LAUNCH(mr_coarsen_level, AF_TGRID(band_count_[l] << D_), d_V_, d_st_, g_, l,
                      eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
     const int shi = std::min(L_ - 1, csm);
     if (shi >= min_leaf_) {
@@ -886,12 +890,19 @@ void MR::coarsen() {
                     min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
       ++launches_;
     }
-    int merged = 0;
-    AF_CUDA(cudaMemcpyAsync(&merged, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    int merged[2] = {0, 0};
+    AF_CUDA(cudaMemcpyAsync(merged, d_flagi_, sizeof merged, cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
-    if (!merged) break;
+    if (full_sweeps_ && clean && merged[0])
+      throw Error(AF_E_INTERNAL, "coarsen: a sweep after a clean sweep merged (skip test unsound)");
+    if (!merged[0]) break;
+    clean = !merged[1];
     lists_valid_ = false;
     predict_fill_(1, 0, min_leaf_ + 1);  // merges only create absent cells above min_leaf
+    // coarsen's while(merged) loop (mr_tree.cpp:474-510): the next sweep is
+    // skipped when no merge can have changed a candidate's detail (merged[1],
+    // see coarsen_level_dev); it would find nothing to merge.
+    if (!merged[1] && !full_sweeps_) break;
   }
 }
 

@@ -45,11 +45,12 @@ class MR {
   void predict_fill_(int lo, int hi, int from = 1);
   void project_range_(int lo, int top);
   void build_lists_();
-  bool ml_grid_(int lo, int hi, bool leaf, dim3* grid) const;
+  bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1) const;
   int coop_blocks_();
   void cycle_stats_(long* leaves, long* nodes, double* smax);
   int coop_blocks_cache_ = 0;
   int small_hi_ = 0;
+  bool full_sweeps_ = false;    // AF_MR_FULL_SWEEPS: never skip a coarsen sweep; check the skip test
   bool small_coarsen_ = false;  // coarsest levels [0, small_hi_] use the cooperative small-level kernels
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);

@@ -78,7 +78,7 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
 // project_internals / project_range (mr_tree.cpp:319-338, mr_solver.cpp:268-282):
 // internal q = (sum over children, x-fastest child order) * (1/2^d).
 template <int D>
-__device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, MRLevels g, int l,
+__device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, const MRLevels& g, int l,
     const int* tiles, int ntiles) {
   AF_ML_RESOLVE();
   constexpr int NC = D + 2;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
 // re-predicts only the virtual children of the stepping leaves.
 template <int D>
 __device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, const uint8_t* vmark,
-                                 MRLevels g, int l, int lo, int hi,
+                                 const MRLevels& g, int l, int lo, int hi,
     const int* tiles, int ntiles) {
   AF_ML_RESOLVE();
   constexpr int NC = D + 2;
@@ -269,42 +269,101 @@ __global__ void mr_predict_all(double* V, const uint8_t* st, const uint8_t* vmar
 // detail / detail_between (mr_tree.cpp:291-317): max over children and
 // components of |q_child - pred_child| / norm_k. Zero numerators are returned
 // directly (0/x == 0 exactly) to stay off the division slow path.
+// Child-parallel iteration over the nodes of level l: 2^D consecutive lanes
+// share one node (lane & (2^D-1) = child index, x-fastest), so each child's
+// prediction runs on its own lane and the per-node reductions are 2^D-lane
+// shuffles. Every lane of a warp runs the same trip count (valid=false on
+// the padding), which keeps the shuffles convergent. Blocks are 256 threads.
+template <int D, class F>
+__device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, const int* tiles,
+                                                     int ntiles, F&& f) {
+  constexpr int NCH = 1 << D;
+  const int n = 1 << l;
+  if (tiles) {
+    // block b takes round (b & (2^D-1)) of tile (b >> D): a tile's 2^D*256
+    // (node, child) items are spread over 2^D blocks, one item per thread
+    constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
+    const int ntx = g.ntx[l], nty = g.nty[l];
+    for (int tb = blockIdx.x; tb < (ntiles << D); tb += gridDim.x) {
+      const int t = tiles[tb >> D];
+      const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
+      const int z0 = D == 3 ? (t / (ntx * nty)) * kTileZ3 : 0;
+      const int item = (tb & (NCH - 1)) * 256 + (int)threadIdx.x, tn = item >> D;
+      const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
+      const bool valid = x < n && y < n && (D == 2 || z < n);
+      f(valid ? mr_idx(D, n, x, y, z) : 0L, valid, item & (NCH - 1));
+    }
+  } else {
+    const long total = mr_cells(D, l) << D;
+    for (long base = (long)blockIdx.x * blockDim.x; base < total; base += (long)gridDim.x * blockDim.x) {
+      const long item = base + threadIdx.x;
+      const bool valid = item < total;
+      f(valid ? item >> D : 0L, valid, (int)(item & (NCH - 1)));
+    }
+  }
+}
+
+// max / all over the 2^D lanes of one node (all 32 lanes must call)
 template <int D>
-__device__ __forceinline__ double node_detail(const double* V, long comp, const MRLevels& g,
-                                              int l, int i, int j, int k, const double* norms) {
+__device__ __forceinline__ double node_group_max(double v) {
+#pragma unroll
+  for (int o = 1; o < (1 << D); o <<= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = v > w ? v : w;
+  }
+  return v;
+}
+template <int D>
+__device__ __forceinline__ bool node_group_all(bool b) {
+  const unsigned m = __ballot_sync(0xffffffffu, b);
+  const unsigned gm = ((1u << (1 << D)) - 1u) << ((threadIdx.x & 31) & ~((1 << D) - 1));
+  return (m & gm) == gm;
+}
+
+// MRTree::detail / detail_between (mr_tree.cpp:291-317) restricted to ONE child:
+// max over components of |q_child - prediction| / norm. The node's detail is
+// the max of this over its 2^d children (node_group_max); every term is >= 0,
+// so the reduction order does not change the result.
+template <int D>
+__device__ __forceinline__ double child_detail(const double* V, long comp, const MRLevels& g,
+                                               int l, int i, int j, int k, int ch,
+                                               const double* norms) {
   constexpr int NC = D + 2;
   const int n = 1 << l, nf = n << 1;
   const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+  double pred[NC];
+  predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
+  const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                                D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
   double mag = 0.0;
-  for (int ch = 0; ch < (1 << D); ++ch) {
-    double pred[NC];
-    predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
-    const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
-                                  D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
 #pragma unroll
-    for (int m = 0; m < NC; ++m) {
-      const double d = fabs(V[m * comp + fc] - pred[m]);
-      // norms index: rho 0, mom 1..D, rhoE 4 (the 2D mom2 term is 0/global == 0)
-      const int ni = m == NC - 1 ? 4 : m;
-      const double r = d == 0.0 ? 0.0 : d / norms[ni];
-      mag = mag > r ? mag : r;  // std::max(mag, r)
-    }
+  for (int m = 0; m < NC; ++m) {
+    const double d = fabs(V[m * comp + fc] - pred[m]);
+    // norms index: rho 0, mom 1..D, rhoE 4 (the 2D mom2 term is 0/global == 0)
+    const int ni = m == NC - 1 ? 4 : m;
+    const double r = d == 0.0 ? 0.0 : d / norms[ni];
+    mag = mag > r ? mag : r;  // std::max(mag, r)
   }
   return mag;
 }
 
-// Detail of every INTERNAL node at level l.
+// Detail of every INTERNAL node at level l (child-parallel).
 template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
                                 int l, const double* norms,
     const int* tiles = nullptr, int ntiles = 0) {
   AF_ML_RESOLVE();
   const int n = 1 << l;
-  const long cells = mr_cells(D, l), off = g.cell_off[l];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
-    if (st[off + c] != ST_INTERNAL) return;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-    det[off + c] = node_detail<D>(V, g.total_cells, g, l, i, j, k, norms);
+  const long off = g.cell_off[l];
+  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](long c, bool valid, int ch) {
+    const bool internal = valid && st[off + c] == ST_INTERNAL;
+    double r = 0.0;
+    if (internal) {
+      const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+      r = child_detail<D>(V, g.total_cells, g, l, i, j, k, ch, norms);
+    }
+    r = node_group_max<D>(r);
+    if (internal && ch == 0) det[off + c] = r;
   });
 }
 
@@ -427,48 +486,106 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
 // an INTERNAL node at level l >= min_leaf merges iff all children are leaves,
 // detail < eps_{l+1}, and no face-ring cell at level l+1 is INTERNAL.
 template <int D>
-__device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, MRLevels g, int l, double eps,
+__device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, const MRLevels& g, int l, double eps,
                                  const double* norms, int* merged,
     const int* tiles, int ntiles) {
   AF_ML_RESOLVE();
   const int n = 1 << l, nf = n << 1;
-  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
-    if (st[off + c] != ST_INTERNAL) return;
+  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+  // One lane per (node, child). Nodes at one level never interact: a merge
+  // turns level-(l+1) LEAFs into ABSENT, and merge_allowed only looks for
+  // level-(l+1) INTERNAL cells.
+  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](long c, bool valid, int ch) {
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
-    bool all_leaves = true;
-    for (int ch = 0; ch < (1 << D) && all_leaves; ++ch)
-      if (st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
-                           D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] != ST_LEAF)
-        all_leaves = false;
-    if (!all_leaves) return;
-    const double d = node_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], norms);
-    if (!(d < eps)) return;
-    bool allowed = true;  // merge_allowed (mr_tree.cpp:446-471)
-    for (int a = 0; a < D && allowed; ++a)
-      for (int dir = -1; dir <= 1 && allowed; dir += 2) {
-        const int tzn = D == 3 ? 2 : 1;
-        const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
-        for (int t2 = 0; t2 < tzn && allowed; ++t2)
-          for (int t1 = 0; t1 < 2 && allowed; ++t1) {
-            int r[3];
-            r[a] = dir > 0 ? 2 * idx[a] + 2 : 2 * idx[a] - 1;
-            r[b1] = 2 * idx[b1] + t1;
-            r[b2] = D == 3 ? 2 * idx[b2] + t2 : 0;
-            const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
-            if (!per && (r[a] < 0 || r[a] >= nf)) continue;
-            bool fl;
-            r[a] = mr_map(r[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
-            if (st[foff + mr_idx(D, nf, r[0], r[1], r[2])] == ST_INTERNAL) allowed = false;
-          }
+    int cc[3];
+    cc[0] = 2 * idx[0] + (ch & 1);
+    cc[1] = 2 * idx[1] + ((ch >> 1) & 1);
+    cc[2] = D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0;
+    const long fc = foff + mr_idx(D, nf, cc[0], cc[1], cc[2]);
+    // candidate: INTERNAL node whose children are all leaves (mr_tree.cpp:486-497)
+    const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF);
+    double r = 0.0;
+    if (cand) r = child_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], ch, norms);
+    r = node_group_max<D>(r);
+    bool allowed = true;
+    if (cand && r < eps) {
+      // merge_allowed (mr_tree.cpp:446-471): no INTERNAL level-(l+1) cell
+      // face-adjacent to the children. This lane checks its child's D outward
+      // neighbours; the 2^d lanes together cover every position.
+#pragma unroll
+      for (int a = 0; a < D; ++a) {  // unrolled: g.bc[] stays in the param space
+        int q[3] = {cc[0], cc[1], cc[2]};
+        q[a] = ((ch >> a) & 1) ? 2 * idx[a] + 2 : 2 * idx[a] - 1;
+        const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+        if (!per && (q[a] < 0 || q[a] >= nf)) continue;
+        bool fl;
+        q[a] = mr_map(q[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
+        if (st[foff + mr_idx(D, nf, q[0], q[1], q[2])] == ST_INTERNAL) allowed = false;
       }
-    if (!allowed) return;
-    // merged q = mean of the children == the projection already stored
-    st[off + c] = ST_LEAF;
-    for (int ch = 0; ch < (1 << D); ++ch)
-      st[foff + mr_idx(D, nf, 2 * idx[0] + (ch & 1), 2 * idx[1] + ((ch >> 1) & 1),
-                       D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0)] = ST_ABSENT;
-    *merged = 1;
+    }
+    const bool merge = node_group_all<D>(cand && r < eps && allowed);
+    if (merge) {
+      // merged q = mean of the children == the projection already stored
+      st[fc] = ST_ABSENT;
+      if (ch == 0) {
+        st[off + c] = ST_LEAF;
+        merged[0] = 1;
+      }
+      // Another sweep can only merge more if an erased child lies in the
+      // prediction stencil (predict_children / axis_stencil, mr_tree.cpp:199-253)
+      // of a level-(l+1) merge candidate that this sweep already evaluated:
+      // that candidate's detail now sees a predicted value. Per axis the
+      // stencil is {p-1, p, p+1}, or one-sided {0,1,2} / {n-3,n-2,n-1} at a
+      // non-periodic wall, so the candidates within reach of child position p
+      // are p-1..p+1 plus 0 (p == 2) or n-1 (p == n-3). Flag merged[1] when
+      // any of them is a candidate (INTERNAL with all-leaf children).
+      if (l + 2 <= g.L) {
+        const long ffoff = g.cell_off[l + 2];
+        const int nff = nf << 1;
+        int pos[3][4];
+        bool okp[3][4];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a >= D) {
+            pos[a][0] = 0, okp[a][0] = true;
+            pos[a][1] = pos[a][2] = pos[a][3] = 0;
+            okp[a][1] = okp[a][2] = okp[a][3] = false;
+            continue;
+          }
+          const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+          const int p = cc[a];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            int q = p - 1 + t;
+            bool ok = true;
+            if (q < 0 || q >= nf) {
+              if (per) q = (q + nf) % nf;
+              else ok = false;
+            }
+            pos[a][t] = q, okp[a][t] = ok;
+          }
+          pos[a][3] = p == 2 ? 0 : nf - 1;
+          okp[a][3] = !per && nf > 2 && (p == 2 || p == nf - 3);
+        }
+        bool hit = false;
+#pragma unroll
+        for (int tz = 0; tz < (D == 3 ? 4 : 1); ++tz)
+#pragma unroll
+          for (int ty = 0; ty < 4; ++ty)
+#pragma unroll
+            for (int tx = 0; tx < 4; ++tx) {
+              if (!(okp[0][tx] && okp[1][ty] && okp[2][tz])) continue;
+              const int q0 = pos[0][tx], q1 = pos[1][ty], q2 = pos[2][tz];
+              if (st[foff + mr_idx(D, nf, q0, q1, q2)] != ST_INTERNAL) continue;
+              bool all = true;
+              for (int c2 = 0; c2 < (1 << D) && all; ++c2)
+                all = st[ffoff + mr_idx(D, nff, 2 * q0 + (c2 & 1), 2 * q1 + ((c2 >> 1) & 1),
+                                        D == 3 ? 2 * q2 + ((c2 >> 2) & 1) : 0)] == ST_LEAF;
+              hit = hit || all;
+            }
+        if (hit) merged[1] = 1;
+      }
+    }
   });
 }
 

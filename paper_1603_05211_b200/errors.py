@@ -31,7 +31,8 @@ class UnsupportedOption(ConfigError):
 
 
 _BY_STATUS = {1: NonPhysicalState, 2: RegisterMismatch, 3: ConfigError, 4: LevelMismatch,
-              5: DeviceError, 6: DeviceError, 7: ValueError, 8: UnsupportedOption}
+              5: DeviceError, 6: DeviceError, 7: ValueError, 8: UnsupportedOption,
+              9: DeviceError}
 
 
 def raise_status(status: int, message: str) -> None:

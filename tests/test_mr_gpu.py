@@ -144,3 +144,16 @@ def test_mr_nonphysical_message(gpu_lib, oracle, kind, seed, level, steps, kw):
     with pytest.raises(NonPhysicalState) as ei:
         gpu_mr(kind, seed, level, steps, **kw)
     assert str(ei.value) == ref[4]["err"]
+
+
+@pytest.mark.parametrize("kind,seed,level,steps,kw", CASES_GLOBAL[:4] + CASES_LT[:3],
+                         ids=[f"c{i}" for i in range(7)])
+def test_mr_sweep_skip_is_sound(gpu_lib, monkeypatch, kind, seed, level, steps, kw):
+    """coarsen skips the re-sweep of mr_tree.cpp:474-510 when no merge touched a
+    candidate's prediction stencil. AF_MR_FULL_SWEEPS runs every sweep and
+    raises if a sweep after a 'clean' one merges; the results must not change."""
+    base = gpu_mr(kind, seed, level, steps, **kw)
+    monkeypatch.setenv("AF_MR_FULL_SWEEPS", "1")
+    full = gpu_mr(kind, seed, level, steps, **kw)
+    assert np.array_equal(base[2], full[2])
+    assert np.array_equal(bits(base[1]), bits(full[1]))
