@@ -27,7 +27,6 @@ namespace af {
 namespace {
 
 constexpr int kGrid = 148 * 8;
-constexpr int kGridFixed = 148 * 2;  // graph replay: grid-stride over device-side counts
 constexpr int kSmallTiles = 64;      // levels with at most this many tiles: cooperative launch
 
 inline unsigned grid_for(long n, int block = 256) {
@@ -63,27 +62,6 @@ __global__ void mr_download_level(const double* V, double* __restrict__ aos, MRL
   }
 }
 
-// Copies the leaf values of level l from src to dst (q_old snapshot / commit).
-// `guard`: skip when a pass-1 or post-step failure is pending (the failing
-// stage never commits, as the reference throws before pass 2 completes).
-__global__ void mr_copy_leaves(const double* src, double* dst, const uint8_t* st, long off,
-                               long cells, long comp, int nc, const int* guard, int promote) {
-  if (guard) {
-    __shared__ int s;
-    if (threadIdx.x == 0) s = guard[0] | guard[2];
-    __syncthreads();
-    if (s) {
-      if (promote && blockIdx.x == 0 && threadIdx.x == 0) atomicExch((int*)guard, 1);
-      return;
-    }
-  }
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (st[off + c] != ST_LEAF) continue;
-    for (int m = 0; m < nc; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
-  }
-}
-
 // Virtual q_old snapshot (mr_solver.cpp:251-266): VQold = V at the virtual
 // children of the stepping leaves of level l-1.
 template <int D>
@@ -101,15 +79,71 @@ __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* 
   }
 }
 
-// Leaf cells of level l (count) -> out[l].
-__global__ void mr_level_leaf_count(const uint8_t* st, long off, long cells,
-                                    unsigned long long* out) {
-  unsigned long long lv = 0;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x)
-    lv += st[off + c] == ST_LEAF;
-  for (int o = 16; o > 0; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
-  if ((threadIdx.x & 31) == 0 && lv) atomicAdd(out, lv);
+// ---- whole-cycle graph helpers (MR::run_batch_graph_) ---------------------
+// Re-arms a WHILE conditional node: continue while flags[0] (both == 0) or
+// flags[0] && flags[1] (both == 1); clears the flags for the next iteration
+// and counts the iteration in iters[0].
+__global__ void mr_while_cond(cudaGraphConditionalHandle h, int* flags, int both,
+                              unsigned long long* iters) {
+  const bool go = both ? (flags[0] != 0 && flags[1] != 0) : flags[0] != 0;
+  flags[0] = 0;
+  flags[1] = 0;
+  ++iters[0];
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+// Device part of the run_mr cycle head (mr_solver.cpp:339-374) for a global
+// step: dt from the CFL rule (cfl * dx_L / smax, the host's operation order)
+// or the fixed dt; the step index for error records; the cycle record.
+// ctl[0] = global step index, ctl[1] = record slot in the batch.
+__global__ void mr_cycle_begin(const unsigned long long* red, const unsigned long long* lpl,
+                               int L, int D, double cfl, double fixed_dt, double dx_L,
+                               double* dt_out, int* step3, long long* ctl, af_mr_cycle* rec) {
+  const double smax = __longlong_as_double((long long)red[3]);
+  double dt = fixed_dt;
+  if (cfl > 0.0) dt = cfl * dx_L / smax;
+  *dt_out = dt;
+  *step3 = (int)(3 * ctl[0]);
+  af_mr_cycle r;
+  r.leaves = (long)red[0];
+  r.nodes = (long)(red[0] + red[1] + (red[2] << D));
+  r.sub = 1;
+  r.top = L;
+  r.dt = dt;
+  long upd = 0;
+  for (int l = 0; l <= L; ++l) upd += 2 * (long)lpl[l];
+  r.updates = upd;
+  rec[ctl[1]] = r;
+}
+
+// collect_stage_records_ for the two stages of a global step, accumulated on
+// the device: acc[0] = max_cfl bits, acc[1] = max wave speed bits,
+// acc[2] = fallbacks (std::max order and expressions as on the host).
+__global__ void mr_cycle_end(const unsigned long long* srec, const unsigned long long* lpl, int L,
+                             double extent, const double* dt_p, unsigned long long* acc,
+                             long long* ctl) {
+  const double dt = *dt_p;
+  double mc = __longlong_as_double((long long)acc[0]);
+  double mw = __longlong_as_double((long long)acc[1]);
+  double ws = 0.0;
+  unsigned long long fbs = 0;
+  for (int r = 0; r < 2; ++r) {
+    for (int l = 0; l <= L; ++l) {
+      if (!lpl[l]) continue;
+      const double w = __longlong_as_double((long long)srec[r * 17 + l]);
+      const double dx = extent / static_cast<double>(1 << l);
+      const double c = w * dt / dx;
+      mc = mc < c ? c : mc;
+      ws = ws < w ? w : ws;
+    }
+    fbs += srec[r * 17 + 16];
+  }
+  mw = mw < ws ? ws : mw;
+  acc[0] = (unsigned long long)__double_as_longlong(mc);
+  acc[1] = (unsigned long long)__double_as_longlong(mw);
+  acc[2] += fbs;
+  ++ctl[0];
+  ++ctl[1];
 }
 
 std::string fmt_f(double v) {
@@ -126,6 +160,7 @@ double as_d(unsigned long long b) {
 
 constexpr int kTX2 = 32, kTY2 = 8;
 constexpr int kMaxStageRecords = 2048;
+constexpr long kCycBatch = 64;  // cycles per graph batch (one host synchronisation)
 constexpr int kTX3 = 8, kTY3 = 8, kTZ3 = 4;
 
 }  // namespace
@@ -245,6 +280,15 @@ MR::~MR() {
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   for (GraphCache& gc : graphs_)
     if (gc.exec) cudaGraphExecDestroy(gc.exec);
+  for (CycleGraph& cg : cyc_) {
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    if (cg.graph) cudaGraphDestroy(cg.graph);
+  }
+  if (side_stream_) cudaStreamDestroy(side_stream_);
+  if (h_cycrec_) cudaFreeHost(h_cycrec_);
+  if (h_small_) cudaFreeHost(h_small_);
+  for (void* p : {(void*)d_ckV_, (void*)d_ckSt_, (void*)d_cycrec_, (void*)d_cycctl_, (void*)d_acc_})
+    cudaFree(p);
   if (h_dt_step_) cudaFreeHost(h_dt_step_);
   for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
                   (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
@@ -295,7 +339,11 @@ double MR::eps_at_(int child_level) const {
 // band / leaf tile list of level l and a grid for it
 #define AF_BAND(l) d_band_ + tile_off_[l], (fixed_grids_ ? -1 : band_count_[l])
 #define AF_LEAFT(l) d_tiles_ + tile_off_[l], (fixed_grids_ ? -2 : tile_count_[l])
-#define AF_TGRID(cnt) ((unsigned)(fixed_grids_ ? kGridFixed : std::max(1, std::min((cnt), kGrid))))
+// per-level tile-list grid: the live count, or in graph capture (device-side
+// counts) the level's tile total as the cycle-invariant bound
+#define AF_TGRIDL(l, cnt, mult)                                                        \
+  ((unsigned)std::max(1, std::min((fixed_grids_ ? level_tiles_(l) : (cnt)) * (mult), kGrid)))
+#define AF_TGRID(l, cnt) AF_TGRIDL(l, cnt, 1)
 #define AF_HAS(cnt) (fixed_grids_ || (cnt) > 0)
 
 // Cooperative launch of an all-levels kernel (grid-wide barrier per level).
@@ -331,7 +379,8 @@ int MR::coop_blocks_() {
 void MR::predict_fill_(int lo, int hi, int from) {
   const int f = std::max(1, from);
   const uint8_t* vm = virtuals_ ? d_mark_ : nullptr;
-  if (f <= small_hi_) {
+  const int small = in_body_ ? -1 : small_hi_;
+  if (f <= small) {
     const int to = std::min(small_hi_, L_);
     if (D_ == 3)
       coop_launch(mr_predict_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm, g_,
@@ -341,9 +390,9 @@ void MR::predict_fill_(int lo, int hi, int from) {
                   f, to, lo, hi, (const int*)d_band_);
     ++launches_;
   }
-  for (int l = std::max(f, small_hi_ + 1); l <= L_; ++l)
+  for (int l = std::max(f, small + 1); l <= L_; ++l)
     if (AF_HAS(band_count_[l]))
-      AF_MR_LAUNCH(mr_predict_level, AF_TGRID(band_count_[l]), d_V_, d_st_, vm, g_, l, lo, hi,
+      AF_MR_LAUNCH(mr_predict_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, vm, g_, l, lo, hi,
                    AF_BAND(l));
   fresh_ = (!virtuals_ || (lo == 0 && hi >= L_)) && from <= 1;
 }
@@ -353,7 +402,7 @@ void MR::project_range_(int lo, int top) {
   const int hi = std::min(top - 1, L_ - 1);
   for (int l = hi; l >= std::max(lo, small_hi_ + 1); --l)
     if (AF_HAS(band_count_[l]))
-      AF_MR_LAUNCH(mr_project_level, AF_TGRID(band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
   const int shi = std::min(hi, small_hi_);
   if (shi >= lo) {
     if (D_ == 3)
@@ -368,20 +417,7 @@ void MR::project_range_(int lo, int top) {
 }
 
 void MR::build_lists_() {
-  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * 34, stream_));
-  AF_CUDA(cudaMemsetAsync(d_lpl_, 0, sizeof(unsigned long long) * 17, stream_));
-  const long nt = tile_off_[L_ + 1];
-  const unsigned gw = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
-  const unsigned gt = grid_for(nt);
-  if (D_ == 3) {
-    mr_tile_flags_all<3><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
-    mr_tile_lists_all<3><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
-  } else {
-    mr_tile_flags_all<2><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
-    mr_tile_lists_all<2><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
-  }
-  launches_ += 2;
-  AF_CUDA(cudaGetLastError());
+  build_lists_enqueue_();
   int h[34];
   unsigned long long lp[17];
   AF_CUDA(cudaMemcpyAsync(h, d_tile_count_, sizeof h, cudaMemcpyDeviceToHost, stream_));
@@ -397,12 +433,34 @@ void MR::build_lists_() {
   lists_valid_ = true;
 }
 
+// Band / leaf tile lists and leaves per level, device side only (counts in
+// d_tile_count_ == g_.dcnt and d_lpl_).
+void MR::build_lists_enqueue_() {
+  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * 34, stream_));
+  AF_CUDA(cudaMemsetAsync(d_lpl_, 0, sizeof(unsigned long long) * 17, stream_));
+  const long nt = tile_off_[L_ + 1];
+  const unsigned gw = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
+  const unsigned gt = grid_for(nt);
+  if (D_ == 3) {
+    mr_tile_flags_all<3><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
+    mr_tile_lists_all<3><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
+  } else {
+    mr_tile_flags_all<2><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
+    mr_tile_lists_all<2><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
+  }
+  launches_ += 2;
+  AF_CUDA(cudaGetLastError());
+}
+
 // Grid of a multi-level launch over levels [lo, hi] (AF_ML_RESOLVE): x spans
 // the largest list, y the levels. Returns false when every list is empty.
 bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult) const {
   if (fixed_grids_) {  // graph capture: parameters independent of this cycle's counts
     if (hi < lo) return false;
-    *grid = dim3((unsigned)kGridFixed, (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
+    int mt = 0;
+    for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l) mt = std::max(mt, level_tiles_(l));
+    *grid = dim3((unsigned)std::max(1, std::min(mt * mult, kGrid)),
+                 (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
     return true;
   }
   int mx = 0;
@@ -468,7 +526,7 @@ void MR::refine(int top) {
     for (int l = 1; l <= L_ - 1; ++l) {
       const int r = l > top + 1 ? 1 << (l - top - 1) : 1;
       if (band_count_[l])
-        AF_MR_LAUNCH(mr_dilate_level, AF_TGRID(band_count_[l]), d_st_, d_flag_, d_flag2_, g_, l,
+        AF_MR_LAUNCH(mr_dilate_level, AF_TGRID(l, band_count_[l]), d_st_, d_flag_, d_flag2_, g_, l,
                      r, AF_BAND(l));
     }
     split = d_flag2_;
@@ -615,6 +673,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     e0 = ev_pool_[ev_used_++];
     e1 = ev_pool_[ev_used_++];
     AF_CUDA(cudaEventRecordWithFlags(e0, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
+    note_event_node_();
   }
   // one launch for every stepping level: blockIdx.y = level (AF_ML_RESOLVE);
   // all levels read the same state and write only their own leaves
@@ -647,8 +706,10 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     ++launches_;
     AF_CUDA(cudaGetLastError());
   }
-  if (profile_)
+  if (profile_) {
     AF_CUDA(cudaEventRecordWithFlags(e1, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
+    note_event_node_();
+  }
   AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
                stage == 2);
 }
@@ -878,7 +939,7 @@ void MR::coarsen() {
     const int csm = small_coarsen_ ? small_hi_ : -1;
     for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l)
       if (band_count_[l])
-        AF_MR_LAUNCH(mr_coarsen_level, AF_TGRID(band_count_[l] << D_), d_V_, d_st_, g_, l,
+        AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, band_count_[l], 1 << D_), d_V_, d_st_, g_, l,
                      eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
     const int shi = std::min(L_ - 1, csm);
     if (shi >= min_leaf_) {
@@ -983,89 +1044,277 @@ void MR::check_error_(long step) {
   throw Error(AF_E_NONPHYSICAL, last_.message);
 }
 
+// ------------------------------------------------------- whole-cycle graph --
+// Appends a WHILE conditional node to the graph being captured on stream_
+// and captures body(handle) into it (on side_stream_). The handle is 1 at
+// every graph launch; the body ends with mr_while_cond, which re-arms it.
+// During a capture: remember the event-record node just added to stream_.
+void MR::note_event_node_() {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  AF_CUDA(cudaStreamGetCaptureInfo(stream_, &cs, nullptr, nullptr, &deps, &ndeps));
+  if (cs != cudaStreamCaptureStatusActive) return;
+  if (ndeps != 1) throw Error(AF_E_CUDA, "event record node: unexpected capture dependencies");
+  ev_nodes_.push_back(deps[0]);
+}
+
+template <class F>
+void MR::capture_while_(F&& body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  AF_CUDA(cudaStreamGetCaptureInfo(stream_, &cs, nullptr, &graph, &deps, &ndeps));
+  cudaGraphConditionalHandle h;
+  AF_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  AF_CUDA(cudaGraphAddNode(&node, graph, deps, ndeps, &p));
+  AF_CUDA(cudaStreamUpdateCaptureDependencies(stream_, &node, 1,
+                                              cudaStreamSetCaptureDependencies));
+  cudaGraph_t bodyg = p.conditional.phGraph_out[0];
+  cudaStream_t outer = stream_;
+  stream_ = side_stream_;
+  in_body_ = true;
+  try {
+    AF_CUDA(cudaStreamBeginCaptureToGraph(side_stream_, bodyg, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+    body(h);
+    AF_CUDA(cudaStreamEndCapture(side_stream_, &bodyg));
+  } catch (...) {
+    cudaGraph_t g2 = nullptr;
+    cudaStreamEndCapture(side_stream_, &g2);
+    stream_ = outer;
+    in_body_ = false;
+    throw;
+  }
+  stream_ = outer;
+  in_body_ = false;
+}
+
+// One run_mr cycle with a global step (mr_solver.cpp:339-395), enqueued with
+// device-side counts only (fixed grids): refine + enforce_gradedness (WHILE),
+// lists, predictions, virtual leaves, counts/CFL dt (mr_cycle_begin), the two
+// RK stages, stage records (mr_cycle_end), coarsen sweeps (WHILE), lists.
+void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body) {
+  const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
+  AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
+  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
+                 d_norms_);
+  for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
+  AF_ML_LAUNCH(mr_refine_flag_level, 1, L_ - 1, false, d_st_, d_det_, d_flag_, g_, AF_L, -1.0);
+  AF_ML_LAUNCH(mr_apply_split_level, 1, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
+  AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
+  long b0 = launches_;
+  capture_while_([&](cudaGraphConditionalHandle h) {  // enforce_gradedness (mr_tree.cpp:404-444)
+    AF_ML_LAUNCH(mr_grade_flag_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L);
+    AF_ML_LAUNCH(mr_apply_split_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
+    mr_while_cond<<<1, 1, 0, stream_>>>(h, d_flagi_, 0, d_acc_ + 3);
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+  });
+  *grade_body = launches_ - b0;
+  build_lists_enqueue_();
+  predict_fill_(1, 0);
+  // add_virtual_leaves, leaf/node counts, CFL speed
+  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
+  virtuals_ = true;
+  AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
+  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(d_st_, d_mark_, g_.total_cells,
+                                                                 d_red_);
+  ++launches_;
+  if (cfl > 0.0)
+    AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
+  mr_cycle_begin<<<1, 1, 0, stream_>>>(d_red_, d_lpl_, L_, D_, cfl, fixed_dt, dx_L, d_dt_,
+                                       d_step3_, d_cycctl_, d_cycrec_);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+  // the global step: dt and the step index come from mr_cycle_begin
+  stage_records_.clear();
+  cur_step_ = 0;
+  step_levels_(0, L_, 0.0, 0.0, 0);
+  cur_step_ = -1;
+  mr_cycle_end<<<1, 1, 0, stream_>>>(d_red_ + 64, d_lpl_, L_, cfg_.extent, d_dt_, d_acc_,
+                                     d_cycctl_);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+  virtuals_ = false;
+  // coarsen (mr_tree.cpp:473-510): sweeps while one merged and another can
+  AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
+  b0 = launches_;
+  capture_while_([&](cudaGraphConditionalHandle h) {
+    for (int l = L_ - 1; l >= min_leaf_; --l)
+      AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1), d_norms_,
+                   d_flagi_, AF_BAND(l));
+    predict_fill_(1, 0, min_leaf_ + 1);  // a no-op recompute when nothing merged
+    mr_while_cond<<<1, 1, 0, stream_>>>(h, d_flagi_, full_sweeps_ ? 0 : 1, d_acc_ + 4);
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+  });
+  *sweep_body = launches_ - b0;
+  build_lists_enqueue_();
+}
+
+MR::CycleGraph& MR::cycle_graph_(double cfl, double fixed_dt) {
+  CycleGraph& cg = cyc_[profile_ ? 1 : 0];
+  if (cg.exec && cg.cfl == cfl && cg.fixed_dt == fixed_dt) return cg;
+  if (cg.exec) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaGraphExecDestroy(cg.exec);
+    cudaGraphDestroy(cg.graph);
+    cg = CycleGraph{};
+  }
+  if (!side_stream_) {
+    AF_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+    AF_CUDA(cudaMalloc(&d_ckV_, sizeof(double) * NC_ * g_.total_cells));
+    AF_CUDA(cudaMalloc(&d_ckSt_, g_.total_cells));
+    AF_CUDA(cudaMalloc(&d_cycrec_, sizeof(af_mr_cycle) * kCycBatch));
+    AF_CUDA(cudaMallocHost(&h_cycrec_, sizeof(af_mr_cycle) * kCycBatch));
+    AF_CUDA(cudaMalloc(&d_cycctl_, 2 * sizeof(long long)));
+    AF_CUDA(cudaMalloc(&d_acc_, 8 * sizeof(unsigned long long)));
+    AF_CUDA(cudaMallocHost(&h_small_, 32 * sizeof(unsigned long long)));
+  }
+  harvest_events_();
+  const size_t ev0 = ev_used_;
+  const long l0 = launches_, s0 = stage_launches_, u0 = stage_updates_;
+  long gb = 0, sb = 0;
+  ev_nodes_.clear();
+  fixed_grids_ = true;
+  AF_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_cycle_(cfl, fixed_dt, &gb, &sb);
+  } catch (...) {
+    fixed_grids_ = false;
+    in_body_ = false;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    throw;
+  }
+  AF_CUDA(cudaStreamEndCapture(stream_, &cg.graph));
+  fixed_grids_ = false;
+  AF_CUDA(cudaGraphInstantiate(&cg.exec, cg.graph, 0));
+  cg.launches_fixed = launches_ - l0 - gb - sb;
+  cg.grade_body = gb;
+  cg.sweep_body = sb;
+  launches_ = l0;
+  stage_launches_ = s0;
+  stage_updates_ = u0;
+  cg.ev_nodes = ev_nodes_;  // the stage-timing event nodes, rebound to fresh events per launch
+  if (cg.ev_nodes.size() != ev_used_ - ev0)
+    throw Error(AF_E_CUDA, "cycle graph: stage event nodes not captured");
+  ev_used_ = ev0;  // the captured records never ran
+  cg.cfl = cfl;
+  cg.fixed_dt = fixed_dt;
+  lists_valid_ = true;
+  fresh_ = true;
+  virtuals_ = false;
+  registers_built_ = false;
+  return cg;
+}
+
+// B global-step cycles as B launches of the cycle graph and one host
+// synchronisation. Returns false (state restored to the batch start) when a
+// stage failed inside the batch; the caller replays it synchronously.
+bool MR::run_batch_graph_(long B, double cfl, double fixed_dt, long& done, long& cycle, double& t,
+                          af_mr_cycle* cycles, long max_cycles) {
+  if (!lists_valid_) build_lists_();
+  CycleGraph& cg = cycle_graph_(cfl, fixed_dt);
+  const size_t vbytes = sizeof(double) * NC_ * g_.total_cells;
+  AF_CUDA(cudaMemcpyAsync(d_ckV_, d_V_, vbytes, cudaMemcpyDeviceToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(d_ckSt_, d_st_, g_.total_cells, cudaMemcpyDeviceToDevice, stream_));
+  long long* hc = reinterpret_cast<long long*>(h_small_);
+  unsigned long long* ha = h_small_ + 2;
+  int* he = reinterpret_cast<int*>(h_small_ + 16);
+  hc[0] = done;
+  hc[1] = 0;
+  std::memcpy(&ha[0], &max_cfl_, 8);
+  std::memcpy(&ha[1], &max_wave_, 8);
+  ha[2] = ha[3] = ha[4] = 0;
+  AF_CUDA(cudaMemcpyAsync(d_cycctl_, hc, 2 * sizeof(long long), cudaMemcpyHostToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(d_acc_, ha, 5 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                          stream_));
+  const size_t ev_start = ev_used_;
+  for (long b = 0; b < B; ++b) {
+    if (profile_ && !cg.ev_nodes.empty()) {
+      while (ev_pool_.size() < ev_used_ + cg.ev_nodes.size()) {
+        cudaEvent_t e;
+        AF_CUDA(cudaEventCreate(&e));
+        ev_pool_.push_back(e);
+      }
+      for (size_t i = 0; i < cg.ev_nodes.size(); ++i)
+        AF_CUDA(cudaGraphExecEventRecordNodeSetEvent(cg.exec, cg.ev_nodes[i], ev_pool_[ev_used_ + i]));
+      ev_used_ += cg.ev_nodes.size();
+    }
+    AF_CUDA(cudaGraphLaunch(cg.exec, stream_));
+  }
+  AF_CUDA(cudaMemcpyAsync(h_cycrec_, d_cycrec_, sizeof(af_mr_cycle) * B, cudaMemcpyDeviceToHost,
+                          stream_));
+  AF_CUDA(cudaMemcpyAsync(ha, d_acc_, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          stream_));
+  AF_CUDA(cudaMemcpyAsync(he, d_err_, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  if (he[0] || he[2]) {
+    ev_used_ = ev_start;
+    AF_CUDA(cudaMemcpyAsync(d_V_, d_ckV_, vbytes, cudaMemcpyDeviceToDevice, stream_));
+    AF_CUDA(cudaMemcpyAsync(d_st_, d_ckSt_, g_.total_cells, cudaMemcpyDeviceToDevice, stream_));
+    AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
+    AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
+    lists_valid_ = false;
+    fresh_ = true;
+    virtuals_ = false;
+    return false;
+  }
+  launches_ += B * cg.launches_fixed + (long)ha[3] * cg.grade_body + (long)ha[4] * cg.sweep_body;
+  std::memcpy(&max_cfl_, &ha[0], 8);
+  std::memcpy(&max_wave_, &ha[1], 8);
+  fallbacks_ += (long)ha[2];
+  for (long b = 0; b < B; ++b) {
+    const af_mr_cycle& r = h_cycrec_[b];
+    if (cycles && cycle < max_cycles) cycles[cycle] = r;
+    const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
+    t = t_cycle + static_cast<double>(r.sub) * r.dt;
+    if (profile_) {
+      stage_launches_ += 2;
+      stage_updates_ += r.updates;
+    }
+    ++done;
+    ++cycle;
+  }
+  build_lists_();  // host-side counts for the caller
+  fresh_ = true;
+  virtuals_ = false;
+  return true;
+}
+
 void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, long max_cycles,
              af_run_diag* rd) {
   if (n_steps < 0) throw Error(AF_E_ARGUMENT, "n_steps must be >= 0");
   if (!(cfl > 0.0) && !(fixed_dt > 0.0))
     throw Error(AF_E_ARGUMENT, "either cfl or fixed_dt must be positive");
-  const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
   long done = 0, cycle = 0;
   double t = 0.0;
+  // global time step: whole cycles replay as one graph each (run_batch_graph_)
+  const bool graph = !opt_.local_time && !std::getenv("AF_MR_NO_GRAPH") &&
+                     !std::getenv("AF_MR_NO_CYCLE_GRAPH") && !std::getenv("AF_MR_TIMING");
   while (done < n_steps) {
-    long sub = 1;
-    int top = L_;
-    if (opt_.local_time) {  // mr_solver.cpp:345-354
-      top = std::max(coarsest_leaf_level(), min_leaf_);
-      long span = 1L << (L_ - top);
-      while (span > n_steps - done) {
-        span >>= 1;
-        ++top;
-      }
-      sub = span;
+    if (graph) {
+      const long B = std::min<long>(n_steps - done, kCycBatch);
+      if (run_batch_graph_(B, cfl, fixed_dt, done, cycle, t, cycles, max_cycles)) continue;
+      // a stage failed inside the batch: replay it cycle by cycle from the
+      // checkpoint; the synchronous path throws the reference's error there
+      for (long b = 0; b < B; ++b)
+        cycle_sync_(n_steps, cfl, fixed_dt, done, cycle, t, cycles, max_cycles);
+      throw Error(AF_E_INTERNAL, "a failure inside a graph batch did not recur on replay");
     }
-    const bool timing = std::getenv("AF_MR_TIMING") != nullptr;
-    auto tick = [&](int slot) {
-      if (!timing) return;
-      AF_CUDA(cudaStreamSynchronize(stream_));
-      const double now = std::chrono::duration<double>(
-          std::chrono::steady_clock::now().time_since_epoch()).count();
-      if (slot > 0) phase_s_[slot - 1] += now - phase_t0_;
-      phase_t0_ = now;
-    };
-    tick(0);
-    refine(opt_.local_time ? top : -1);
-    tick(1);
-    add_virtual_leaves();
-    long leaves = 0, nodes = 0;
-    double smax = 0.0;
-    cycle_stats_(&leaves, &nodes, cfl > 0.0 ? &smax : nullptr);
-    double dt = fixed_dt;
-    if (cfl > 0.0) dt = cfl * dx_L / smax;
-    tick(2);
-    cudaEvent_t te0 = nullptr, te1 = nullptr;
-    if (timing) {
-      cudaEventCreate(&te0);
-      cudaEventCreate(&te1);
-      cudaEventRecord(te0, stream_);
-    }
-    if (cycles && cycle < max_cycles) {
-      cycles[cycle].leaves = leaves;
-      cycles[cycle].nodes = nodes;
-      cycles[cycle].sub = sub;
-      cycles[cycle].top = top;
-      cycles[cycle].dt = dt;
-      long upd = 0;
-      for (int l = 0; l <= L_; ++l)
-        upd += 2 * leaves_per_level_[l] * (l > top ? (1L << (l - top)) : 1L);
-      cycles[cycle].updates = upd;
-    }
-    const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
-    cur_step_ = done;
-    if (opt_.local_time) build_registers_(top);
-    if (opt_.local_time)
-      advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
-    else
-      evolve_global(dt, nullptr);
-    if (timing) {
-      cudaEventRecord(te1, stream_);
-      cudaEventSynchronize(te1);
-      float ems = 0.f;
-      cudaEventElapsedTime(&ems, te0, te1);
-      evolve_gpu_ms_ += ems;
-      cudaEventDestroy(te0);
-      cudaEventDestroy(te1);
-    }
-    tick(3);
-    cur_step_ = -1;
-    registers_built_ = false;
-    remove_virtual_leaves();
-    coarsen();
-    build_lists_();
-    tick(4);
-    lists_valid_ = true;
-    done += sub;
-    t = t_cycle + static_cast<double>(sub) * dt;
-    ++cycle;
+    cycle_sync_(n_steps, cfl, fixed_dt, done, cycle, t, cycles, max_cycles);
   }
   if (rd) {
     rd->max_wave_speed = max_wave_;
@@ -1074,6 +1323,86 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
     rd->steps_done = done;
     rd->t = t;
   }
+}
+
+// One run_mr cycle (mr_solver.cpp:339-395) driven from the host.
+void MR::cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long& cycle,
+                     double& t, af_mr_cycle* cycles, long max_cycles) {
+  const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
+  long sub = 1;
+  int top = L_;
+  if (opt_.local_time) {  // mr_solver.cpp:345-354
+    top = std::max(coarsest_leaf_level(), min_leaf_);
+    long span = 1L << (L_ - top);
+    while (span > n_steps - done) {
+      span >>= 1;
+      ++top;
+    }
+    sub = span;
+  }
+  const bool timing = std::getenv("AF_MR_TIMING") != nullptr;
+  auto tick = [&](int slot) {
+    if (!timing) return;
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    const double now = std::chrono::duration<double>(
+        std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (slot > 0) phase_s_[slot - 1] += now - phase_t0_;
+    phase_t0_ = now;
+  };
+  tick(0);
+  refine(opt_.local_time ? top : -1);
+  tick(1);
+  add_virtual_leaves();
+  long leaves = 0, nodes = 0;
+  double smax = 0.0;
+  cycle_stats_(&leaves, &nodes, cfl > 0.0 ? &smax : nullptr);
+  double dt = fixed_dt;
+  if (cfl > 0.0) dt = cfl * dx_L / smax;
+  tick(2);
+  cudaEvent_t te0 = nullptr, te1 = nullptr;
+  if (timing) {
+    cudaEventCreate(&te0);
+    cudaEventCreate(&te1);
+    cudaEventRecord(te0, stream_);
+  }
+  if (cycles && cycle < max_cycles) {
+    cycles[cycle].leaves = leaves;
+    cycles[cycle].nodes = nodes;
+    cycles[cycle].sub = sub;
+    cycles[cycle].top = top;
+    cycles[cycle].dt = dt;
+    long upd = 0;
+    for (int l = 0; l <= L_; ++l)
+      upd += 2 * leaves_per_level_[l] * (l > top ? (1L << (l - top)) : 1L);
+    cycles[cycle].updates = upd;
+  }
+  const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
+  cur_step_ = done;
+  if (opt_.local_time) build_registers_(top);
+  if (opt_.local_time)
+    advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
+  else
+    evolve_global(dt, nullptr);
+  if (timing) {
+    cudaEventRecord(te1, stream_);
+    cudaEventSynchronize(te1);
+    float ems = 0.f;
+    cudaEventElapsedTime(&ems, te0, te1);
+    evolve_gpu_ms_ += ems;
+    cudaEventDestroy(te0);
+    cudaEventDestroy(te1);
+  }
+  tick(3);
+  cur_step_ = -1;
+  registers_built_ = false;
+  remove_virtual_leaves();
+  coarsen();
+  build_lists_();
+  tick(4);
+  lists_valid_ = true;
+  done += sub;
+  t = t_cycle + static_cast<double>(sub) * dt;
+  ++cycle;
 }
 
 long MR::leaf_keys(uint64_t* keys, long cap) {

@@ -47,6 +47,7 @@ class MR {
   void build_lists_();
   bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1) const;
   int coop_blocks_();
+  int level_tiles_(int l) const { return g_.ntx[l] * g_.nty[l] * g_.ntz[l]; }
   void cycle_stats_(long* leaves, long* nodes, double* smax);
   int coop_blocks_cache_ = 0;
   int small_hi_ = 0;
@@ -84,6 +85,39 @@ class MR {
     size_t events = 0;
   };
   GraphCache graphs_[2];
+  // Whole-cycle graph of a global-time-step run (run_batch_graph_): refine
+  // with the gradedness fixpoint and coarsen with its sweep loop as WHILE
+  // conditional nodes, CFL dt and cycle records on the device. One launch per
+  // cycle, one host synchronisation per batch of cycles.
+  struct CycleGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    double cfl = -1.0, fixed_dt = -1.0;
+    std::vector<cudaGraphNode_t> ev_nodes;  // event-record nodes, in capture order
+    long launches_fixed = 0;                // kernels outside the WHILE bodies
+    long grade_body = 0, sweep_body = 0;    // kernels per WHILE iteration
+  };
+  CycleGraph cyc_[2];
+  cudaStream_t side_stream_ = nullptr;
+  bool in_body_ = false;                    // capturing a WHILE body: no cooperative launches
+  double* d_ckV_ = nullptr;                 // batch checkpoint (replay on failure)
+  uint8_t* d_ckSt_ = nullptr;
+  af_mr_cycle* d_cycrec_ = nullptr;
+  af_mr_cycle* h_cycrec_ = nullptr;
+  long long* d_cycctl_ = nullptr;           // [0] step index, [1] record slot
+  unsigned long long* d_acc_ = nullptr;     // max_cfl, max wave, fallbacks, grade/sweep iterations
+  unsigned long long* h_small_ = nullptr;   // pinned staging
+  template <class F>
+  void capture_while_(F&& body);
+  void build_lists_enqueue_();
+  void note_event_node_();
+  std::vector<cudaGraphNode_t> ev_nodes_;  // event-record nodes of the capture in progress
+  void enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body);
+  CycleGraph& cycle_graph_(double cfl, double fixed_dt);
+  bool run_batch_graph_(long B, double cfl, double fixed_dt, long& done, long& cycle, double& t,
+                        af_mr_cycle* cycles, long max_cycles);
+  void cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long& cycle, double& t,
+                   af_mr_cycle* cycles, long max_cycles);
   double norms_host_[5] = {1, 1, 1, 1, 1};
   double eps_at_(int child_level) const;
 
