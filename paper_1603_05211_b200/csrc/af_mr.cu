@@ -27,6 +27,7 @@ namespace af {
 namespace {
 
 constexpr int kGrid = 148 * 8;
+constexpr int kStageGrid = 148 * 2;  // stage kernel: 2 resident blocks per SM
 constexpr int kSmallTiles = 64;      // levels with at most this many tiles: cooperative launch
 
 inline unsigned grid_for(long n, int block = 256) {
@@ -324,7 +325,7 @@ double MR::eps_at_(int child_level) const {
     if (ml_grid_((lo), (hi), (leaf), &grid_, (mult))) {                           \
       const int AF_L = -(std::max((lo), 0) + 1);                                   \
       const int* AF_T = (leaf) ? d_tiles_ : d_band_;                               \
-      const int AF_S = (leaf) ? 1 : 0;                                             \
+      const int AF_S = (std::min((hi), L_) << 1) | ((leaf) ? 1 : 0);              \
       if (D_ == 3)                                                                 \
         kern<3><<<grid_, 256, 0, stream_>>>(__VA_ARGS__, AF_T, AF_S);              \
       else                                                                         \
@@ -452,22 +453,17 @@ void MR::build_lists_enqueue_() {
   AF_CUDA(cudaGetLastError());
 }
 
-// Grid of a multi-level launch over levels [lo, hi] (AF_ML_RESOLVE): x spans
-// the largest list, y the levels. Returns false when every list is empty.
-bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult) const {
-  if (fixed_grids_) {  // graph capture: parameters independent of this cycle's counts
-    if (hi < lo) return false;
-    int mt = 0;
-    for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l) mt = std::max(mt, level_tiles_(l));
-    *grid = dim3((unsigned)std::max(1, std::min(mt * mult, kGrid)),
-                 (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
-    return true;
-  }
-  int mx = 0;
+// Grid of a multi-level launch over levels [lo, hi]: the total tile count of
+// the lists (or its bound during capture), capped. False when all are empty.
+bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult, int cap) const {
+  // one flat range over the tiles of levels [lo, hi] (for_each_tile)
+  if (hi < lo) return false;
+  long sum = 0;
   for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l)
-    mx = std::max(mx, leaf ? tile_count_[l] : band_count_[l]);
-  if (!mx || hi < lo) return false;
-  *grid = dim3((unsigned)std::min(mx * mult, kGrid), (unsigned)(std::min(hi, L_) - std::max(lo, 0) + 1));
+    sum += fixed_grids_ ? level_tiles_(l)  // graph capture: a cycle-invariant bound
+                        : (leaf ? tile_count_[l] : band_count_[l]);
+  if (!sum) return false;
+  *grid = dim3((unsigned)std::min<long>(sum * mult, cap));
   return true;
 }
 
@@ -675,7 +671,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     AF_CUDA(cudaEventRecordWithFlags(e0, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
     note_event_node_();
   }
-  // one launch for every stepping level: blockIdx.y = level (AF_ML_RESOLVE);
+  // one launch for every stepping level (one flat range of leaf tiles);
   // all levels read the same state and write only their own leaves
   for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l)
     if (tile_count_[l] && profile_) {
@@ -683,9 +679,9 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
       stage_updates_ += leaves_per_level_[l];
     }
   dim3 grid;
-  if (ml_grid_(lo, hi, true, &grid)) {
+  if (ml_grid_(lo, hi, true, &grid, 1, kStageGrid)) {
     a.tiles = d_tiles_;
-    a.ntiles = 1;
+    a.ntiles = (std::min(hi, L_) << 1) | 1;
     const int lcode = -(std::max(lo, 0) + 1);
     const int lim = cfg_.limiter;
     if (D_ == 2) {

@@ -45,7 +45,7 @@ class MR {
   void predict_fill_(int lo, int hi, int from = 1);
   void project_range_(int lo, int top);
   void build_lists_();
-  bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1) const;
+  bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1, int cap = 148 * 8) const;
   int coop_blocks_();
   int level_tiles_(int l) const { return g_.ntx[l] * g_.nty[l] * g_.ntz[l]; }
   void cycle_stats_(long* leaves, long* nodes, double* smax);

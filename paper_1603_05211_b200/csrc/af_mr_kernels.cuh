@@ -47,30 +47,79 @@ __device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
   return D == 3 ? ((long)k * n + j) * n + i : (long)j * n + i;
 }
 
-// Cell iteration of a level: over the cells of the listed work tiles (one
-// thread per cell, 256-thread blocks, grid-stride over the list), or over
-// every cell of the level when `tiles` is null. Work then scales with the
-// tree's band of tiles instead of the dense level.
+// Tile iteration of one launch. Single level (l >= 0): the `ntiles` entries
+// of `tiles` (ntiles -1 / -2: the band / leaf-tile count from g.dcnt).
+// Multi-level (l = -(lo+1), ntiles = hi << 1 | sel): the band (sel 0) or leaf
+// (sel 1) lists of levels lo..hi as ONE flat range, so the grid follows the
+// total work instead of levels x the largest level. Each tile is visited
+// `reps` times (rep = 0..reps-1) by different blocks; f(level, tile, rep).
+// The same range without a callback: tile_total() entries, tile_at() maps
+// entry `it` to (level, tile).
+__device__ __forceinline__ int tile_total(const MRLevels& g, int l, int ntiles) {
+  if (l < 0) {
+    const int* cnt = g.dcnt + 17 * (ntiles & 1);
+    int total = 0;
+    for (int k = -l - 1; k <= (ntiles >> 1); ++k) total += cnt[k];
+    return total;
+  }
+  return ntiles < 0 ? (ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l]) : ntiles;
+}
+__device__ __forceinline__ int tile_at(const MRLevels& g, int l, const int* tiles, int ntiles,
+                                       int it, int* level) {
+  if (l < 0) {
+    const int* cnt = g.dcnt + 17 * (ntiles & 1);
+    int k = -l - 1, base = 0;
+    while (it >= base + cnt[k]) base += cnt[k++];
+    *level = k;
+    return tiles[g.tile_off[k] + it - base];
+  }
+  *level = l;
+  return tiles[it];
+}
+
+template <class F>
+__device__ __forceinline__ void for_each_tile(const MRLevels& g, int l, const int* tiles,
+                                              int ntiles, int reps, F&& f) {
+  if (l < 0) {
+    const int lo = -l - 1, hi = ntiles >> 1;
+    const int* cnt = g.dcnt + 17 * (ntiles & 1);
+    int total = 0;
+    for (int k = lo; k <= hi; ++k) total += cnt[k];
+    for (int it = blockIdx.x; it < total * reps; it += gridDim.x) {
+      const int ti = it / reps;
+      int k = lo, base = 0;
+      while (ti >= base + cnt[k]) base += cnt[k++];
+      f(k, tiles[g.tile_off[k] + ti - base], it - ti * reps);
+    }
+  } else {
+    if (ntiles < 0) ntiles = ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l];
+    for (int it = blockIdx.x; it < ntiles * reps; it += gridDim.x) {
+      const int ti = it / reps;
+      f(l, tiles[ti], it - ti * reps);
+    }
+  }
+}
+
+// Cell iteration: one thread per cell of the listed tiles (256-thread
+// blocks), or every cell of level l when `tiles` is null. f(level, cell).
 template <int D, class F>
 __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int* tiles,
                                             int ntiles, F&& f) {
-  const int n = 1 << l;
   if (tiles) {
     constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
-    const int ntx = g.ntx[l], nty = g.nty[l];
     const int tx = threadIdx.x % TX, ty = (threadIdx.x / TX) % TY;
     const int tz = D == 3 ? threadIdx.x / (TX * TY) : 0;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-      const int t = tiles[ti];
+    for_each_tile(g, l, tiles, ntiles, 1, [&](int lv, int t, int) {
+      const int n = 1 << lv, ntx = g.ntx[lv], nty = g.nty[lv];
       const int x = (t % ntx) * TX + tx, y = ((t / ntx) % nty) * TY + ty;
       const int z = D == 3 ? (t / (ntx * nty)) * kTileZ3 + tz : 0;
-      if (x < n && y < n && (D == 2 || z < n)) f(mr_idx(D, n, x, y, z));
-    }
+      if (x < n && y < n && (D == 2 || z < n)) f(lv, mr_idx(D, n, x, y, z));
+    });
   } else {
     const long cells = mr_cells(D, l);
     for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
          c += (long)gridDim.x * blockDim.x)
-      f(c);
+      f(l, c);
   }
 }
 
@@ -80,14 +129,14 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
 template <int D>
 __device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, const MRLevels& g, int l,
     const int* tiles, int ntiles) {
-  AF_ML_RESOLVE();
   constexpr int NC = D + 2;
-  const int n = 1 << l, nf = n << 1;
-  const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
-  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-  const long comp = g.total_cells;
-  const double w = 1.0 / (double)(1 << D);
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, nf = n << 1;
+    const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
+    const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+    const long comp = g.total_cells;
+    const double w = 1.0 / (double)(1 << D);
     if (st[off + c] != ST_INTERNAL) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     double s[NC];
@@ -103,7 +152,6 @@ __device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, 
 #pragma unroll
     for (int m = 0; m < NC; ++m) V[m * comp + off + c] = s[m] * w;
   });
-  (void)fcells;
 }
 
 template <int D>
@@ -215,15 +263,15 @@ template <int D>
 __device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, const uint8_t* vmark,
                                  const MRLevels& g, int l, int lo, int hi,
     const int* tiles, int ntiles) {
-  AF_ML_RESOLVE();
   constexpr int NC = D + 2;
-  const int n = 1 << l, pn = n >> 1;
-  const long cells = mr_cells(D, l);
-  const long off = g.cell_off[l], poff = g.cell_off[l - 1];
-  const long comp = g.total_cells;
-  const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
-  const int bcx = g.bc[0], bcy = g.bc[2], bcz = g.bc[4];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, pn = n >> 1;
+    const long cells = mr_cells(D, l);
+    const long off = g.cell_off[l], poff = g.cell_off[l - 1];
+    const long comp = g.total_cells;
+    const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
+    const int bcx = g.bc[0], bcy = g.bc[2], bcz = g.bc[4];
     if (st[off + c] != ST_ABSENT) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
@@ -269,36 +317,33 @@ __global__ void mr_predict_all(double* V, const uint8_t* st, const uint8_t* vmar
 // detail / detail_between (mr_tree.cpp:291-317): max over children and
 // components of |q_child - pred_child| / norm_k. Zero numerators are returned
 // directly (0/x == 0 exactly) to stay off the division slow path.
-// Child-parallel iteration over the nodes of level l: 2^D consecutive lanes
-// share one node (lane & (2^D-1) = child index, x-fastest), so each child's
-// prediction runs on its own lane and the per-node reductions are 2^D-lane
-// shuffles. Every lane of a warp runs the same trip count (valid=false on
-// the padding), which keeps the shuffles convergent. Blocks are 256 threads.
+// Child-parallel iteration over the nodes: 2^D consecutive lanes share one
+// node (lane & (2^D-1) = child index, x-fastest), so each child's prediction
+// runs on its own lane and the per-node reductions are 2^D-lane shuffles. A
+// tile's 2^D*256 (node, child) items are spread over 2^D blocks. Every lane of
+// a warp runs the same trip count (valid=false on the padding), which keeps
+// the shuffles convergent. Blocks are 256 threads. f(level, node, valid, child).
 template <int D, class F>
 __device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, const int* tiles,
                                                      int ntiles, F&& f) {
   constexpr int NCH = 1 << D;
-  const int n = 1 << l;
   if (tiles) {
-    // block b takes round (b & (2^D-1)) of tile (b >> D): a tile's 2^D*256
-    // (node, child) items are spread over 2^D blocks, one item per thread
     constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
-    const int ntx = g.ntx[l], nty = g.nty[l];
-    for (int tb = blockIdx.x; tb < (ntiles << D); tb += gridDim.x) {
-      const int t = tiles[tb >> D];
+    for_each_tile(g, l, tiles, ntiles, NCH, [&](int lv, int t, int r) {
+      const int n = 1 << lv, ntx = g.ntx[lv], nty = g.nty[lv];
       const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
       const int z0 = D == 3 ? (t / (ntx * nty)) * kTileZ3 : 0;
-      const int item = (tb & (NCH - 1)) * 256 + (int)threadIdx.x, tn = item >> D;
+      const int item = r * 256 + (int)threadIdx.x, tn = item >> D;
       const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
       const bool valid = x < n && y < n && (D == 2 || z < n);
-      f(valid ? mr_idx(D, n, x, y, z) : 0L, valid, item & (NCH - 1));
-    }
+      f(lv, valid ? mr_idx(D, n, x, y, z) : 0L, valid, item & (NCH - 1));
+    });
   } else {
     const long total = mr_cells(D, l) << D;
     for (long base = (long)blockIdx.x * blockDim.x; base < total; base += (long)gridDim.x * blockDim.x) {
       const long item = base + threadIdx.x;
       const bool valid = item < total;
-      f(valid ? item >> D : 0L, valid, (int)(item & (NCH - 1)));
+      f(l, valid ? item >> D : 0L, valid, (int)(item & (NCH - 1)));
     }
   }
 }
@@ -352,10 +397,10 @@ template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
                                 int l, const double* norms,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l;
-  const long off = g.cell_off[l];
-  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](long c, bool valid, int ch) {
+  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv_, long c, bool valid, int ch) {
+    const int l = lv_;
+    const int n = 1 << l;
+    const long off = g.cell_off[l];
     const bool internal = valid && st[off + c] == ST_INTERNAL;
     double r = 0.0;
     if (internal) {
@@ -374,10 +419,10 @@ template <int D>
 __global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
                                      MRLevels g, int l, double eps,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l, pn = n >> 1;
-  const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, pn = n >> 1;
+    const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
     uint8_t f = 0;
     if (st[off + c] == ST_LEAF && l >= 1 && l < g.L) {
       const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
@@ -391,14 +436,14 @@ template <int D>
 __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
                                 MRLevels g, int l, int r,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
   // Target t is inserted iff some detail-flagged source s has map(s + o) == t
   // for an offset o != 0 with |o|_inf <= r. Clamping and folding never move a
   // position farther from s, so scanning the in-domain (or periodically
   // wrapped) sources s = t - o is exhaustive.
-  const int n = 1 << l;
-  const long cells = mr_cells(D, l), off = g.cell_off[l];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l;
+    const long cells = mr_cells(D, l), off = g.cell_off[l];
     uint8_t f = flag[off + c];
     if (!f && st[off + c] == ST_LEAF) {
       const int t[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
@@ -427,10 +472,10 @@ template <int D>
 __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels g, int l,
                                      int* changed,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l, nf = n << 1;
-  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, nf = n << 1;
+    const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
     if (!flag[off + c] || st[off + c] != ST_LEAF) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     st[off + c] = ST_INTERNAL;
@@ -448,10 +493,10 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
 template <int D>
 __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l, nf = n << 1;
-  const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, nf = n << 1;
+    const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
     uint8_t need = 0;
     if (st[off + c] == ST_LEAF && l < g.L) {
       const int idx[3] = {(int)(c % n), (int)((c / n) % n),
@@ -489,13 +534,13 @@ template <int D>
 __device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, const MRLevels& g, int l, double eps,
                                  const double* norms, int* merged,
     const int* tiles, int ntiles) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l, nf = n << 1;
-  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
   // One lane per (node, child). Nodes at one level never interact: a merge
   // turns level-(l+1) LEAFs into ABSENT, and merge_allowed only looks for
   // level-(l+1) INTERNAL cells.
-  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](long c, bool valid, int ch) {
+  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv_, long c, bool valid, int ch) {
+    const int l = lv_;
+    const int n = 1 << l, nf = n << 1;
+    const long off = g.cell_off[l], foff = g.cell_off[l + 1];
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
     int cc[3];
     cc[0] = 2 * idx[0] + (ch & 1);
@@ -636,10 +681,10 @@ __global__ void mr_coarsen_small(const double* V, uint8_t* st, MRLevels g, int l
 template <int D>
 __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
-  const int n = 1 << l, pn = n >> 1;
-  const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const int n = 1 << l, pn = n >> 1;
+    const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
     if (st[off + c] != ST_LEAF) return;
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
     for (int a = 0; a < D; ++a)
@@ -686,11 +731,11 @@ template <int D>
 __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
                                      double gamma, unsigned long long* target,
                                      const int* tiles = nullptr, int ntiles = 0) {
-  AF_ML_RESOLVE();
   __shared__ double red[8];
-  const long off = g.cell_off[l], comp = g.total_cells;
   double best = 0.0;
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
+    const int l = lv_;
+    const long off = g.cell_off[l], comp = g.total_cells;
     if (st[off + c] != ST_LEAF) return;
     Cons<D> q;
     q.rho = V[off + c];

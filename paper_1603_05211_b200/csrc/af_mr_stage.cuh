@@ -174,26 +174,26 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   uint8_t* leaf = ffb + K::NF;            // [NT] leaf mask
   __shared__ int s_fb, s_bad;
 
-  const int* tiles = a.tiles;
-  int ntiles = a.ntiles;
-  AF_ML_RESOLVE();
   const double sdt = a.dt_dev ? a.dt_scale * *a.dt_dev : a.sdt;  // 0.5 * dt, 1.0 * dt == dt
   const int step3 = a.step3_dev ? *a.step3_dev : a.step3;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = 1 << l;
-  const long comp = g.total_cells, off = g.cell_off[l];
-  const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
+  const long comp = g.total_cells;
   const double gamma = a.gamma, gm1 = a.gm1;
-  const double inv_dx = g.inv_dx[l];
   if (tid == 0) {
     s_fb = 0;
     s_bad = 0;
   }
-  double wave = 0.0;  // accumulated over this block's tiles
   int bad = 0, nfb = 0;
   const int tx = tid % TX, ty = (tid / TX) % TY, tz = D == 3 ? tid / (TX * TY) : 0;
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-  const int t = tiles[ti];
+  const int ntotal = tile_total(g, l, a.ntiles);
+  const int lcode = l;
+  for (int it = blockIdx.x; it < ntotal; it += gridDim.x) {
+  const int t = tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
+  const int n = 1 << l;
+  const long off = g.cell_off[l];
+  const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
+  const double inv_dx = g.inv_dx[l];
+  double wave = 0.0;
   const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
   const int z0 = D == 3 ? (t / (ntx * nty)) * TZ : 0;
   // leaf mask of the tile cells
@@ -422,11 +422,16 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
     }
   }
+  // per-level max wave speed of this tile: warp max, one atomic per warp
+  // (non-negative doubles order like their bit patterns)
+  for (int o = 16; o > 0; o >>= 1) wave = fmax(wave, __shfl_xor_sync(0xffffffffu, wave, o));
+  if (lane == 0 && wave > 0.0)
+    atomicMax(a.wave + l, (unsigned long long)__double_as_longlong(wave));
   __syncthreads();  // the next tile reuses the shared-memory staging
   }
   if (bad) atomicOr(&s_bad, bad);
   if (nfb) atomicAdd(&s_fb, nfb);
-  block_max_atomic<K::NT>(wave, red, a.wave + l);
+  __syncthreads();
   if (tid == 0) {
     if (s_bad) {
       // pass-1 failures stop every later launch; a post-step failure only
@@ -611,7 +616,6 @@ template <int D>
 __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8_t* st,
                                      MRLevels g, int l, const int* guard, int promote,
                                      const int* tiles, int ntiles) {
-  AF_ML_RESOLVE();
   if (guard) {
     __shared__ int s;
     if (threadIdx.x == 0) s = guard[0] | guard[2];
@@ -621,8 +625,9 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
       return;
     }
   }
-  const long off = g.cell_off[l], comp = g.total_cells;
-  level_cells<D>(g, l, tiles, ntiles, [&](long c) {
+  const long comp = g.total_cells;
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
+    const long off = g.cell_off[lv];
     if (st[off + c] != ST_LEAF) return;
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) dst[m * comp + off + c] = src[m * comp + off + c];

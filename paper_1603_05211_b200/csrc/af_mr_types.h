@@ -25,20 +25,13 @@ struct MRLevels {
   const int* dcnt;         // device copy of the counts: [l] band, [17 + l] leaf tiles
 };
 
-// Multi-level launch convention: a kernel called with l = -(l0 + 1) runs
-// level l0 + blockIdx.y, with `tiles` the base of the concatenated per-level
-// lists and `ntiles` selecting the band (0) or leaf (1) list counts.
-// The counts are read from device memory (g.dcnt) so a launch's parameters
-// do not change from cycle to cycle (CUDA-graph replay). A single-level launch
-// may pass ntiles = -1 (band) / -2 (leaf tiles) to read its count likewise.
-#define AF_ML_RESOLVE()                                      \
-  if (l < 0) {                                               \
-    l = -l - 1 + (int)blockIdx.y;                            \
-    tiles += g.tile_off[l];                                  \
-    ntiles = ntiles ? g.dcnt[17 + l] : g.dcnt[l];            \
-  } else if (ntiles < 0) {                                   \
-    ntiles = ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l];      \
-  }
+// Multi-level launch convention: a kernel called with l = -(lo + 1) and
+// ntiles = hi << 1 | sel covers the band (sel 0) or leaf-tile (sel 1) lists of
+// levels lo..hi as one flat range (for_each_tile, af_mr_kernels.cuh), `tiles`
+// being the base of the concatenated per-level lists. The counts are read
+// from device memory (g.dcnt) so a launch's parameters do not change from
+// cycle to cycle (CUDA-graph replay). A single-level launch may pass
+// ntiles = -1 (band) / -2 (leaf tiles) to read its count likewise.
 
 constexpr int kTileX2 = 32, kTileY2 = 8;
 constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
