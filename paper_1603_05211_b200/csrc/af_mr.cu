@@ -37,6 +37,7 @@ inline unsigned grid_for(long n, int block = 256) {
 
 template <int D>
 __global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLevels g) {
+  AF_PDL_ENTRY();
   const long cells = mr_cells(D, g.L), off = g.cell_off[g.L], comp = g.total_cells;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
@@ -51,6 +52,7 @@ __global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLe
 
 template <int D>
 __global__ void mr_download_level(const double* V, double* __restrict__ aos, MRLevels g, int l) {
+  AF_PDL_ENTRY();
   const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
@@ -68,6 +70,7 @@ __global__ void mr_download_level(const double* V, double* __restrict__ aos, MRL
 template <int D>
 __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* st,
                                     const uint8_t* mark, MRLevels g, int l) {
+  AF_PDL_ENTRY();
   const int n = 1 << l, pn = n >> 1;
   const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
   const long comp = g.total_cells;
@@ -86,6 +89,7 @@ __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* 
 // and counts the iteration in iters[0].
 __global__ void mr_while_cond(cudaGraphConditionalHandle h, int* flags, int both,
                               unsigned long long* iters) {
+  AF_PDL_ENTRY();
   const bool go = both ? (flags[0] != 0 && flags[1] != 0) : flags[0] != 0;
   flags[0] = 0;
   flags[1] = 0;
@@ -100,6 +104,7 @@ __global__ void mr_while_cond(cudaGraphConditionalHandle h, int* flags, int both
 __global__ void mr_cycle_begin(const unsigned long long* red, const unsigned long long* lpl,
                                int L, int D, double cfl, double fixed_dt, double dx_L,
                                double* dt_out, int* step3, long long* ctl, af_mr_cycle* rec) {
+  AF_PDL_ENTRY();
   const double smax = __longlong_as_double((long long)red[3]);
   double dt = fixed_dt;
   if (cfl > 0.0) dt = cfl * dx_L / smax;
@@ -123,6 +128,7 @@ __global__ void mr_cycle_begin(const unsigned long long* red, const unsigned lon
 __global__ void mr_cycle_end(const unsigned long long* srec, const unsigned long long* lpl, int L,
                              double extent, const double* dt_p, unsigned long long* acc,
                              long long* ctl) {
+  AF_PDL_ENTRY();
   const double dt = *dt_p;
   double mc = __longlong_as_double((long long)acc[0]);
   double mw = __longlong_as_double((long long)acc[1]);
@@ -145,6 +151,24 @@ __global__ void mr_cycle_end(const unsigned long long* srec, const unsigned long
   acc[2] += fbs;
   ++ctl[0];
   ++ctl[1];
+}
+
+// Kernel launch with the programmatic-dependent-launch attribute when `pdl`
+// (see AF_PDL_ENTRY): the launch overlaps the predecessor's tail.
+template <class... P, class... A>
+void launch_k(bool pdl, cudaStream_t s, void (*kern)(P...), dim3 grid, unsigned block,
+              size_t smem, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  AF_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
 }
 
 std::string fmt_f(double v) {
@@ -239,6 +263,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
       if ((long)g_.ntx[l] * g_.nty[l] * g_.ntz[l] <= kSmallTiles) small_hi_ = l;
   small_coarsen_ = std::getenv("AF_MR_SMALL_COARSEN") != nullptr;
   full_sweeps_ = std::getenv("AF_MR_FULL_SWEEPS") != nullptr;
+  pdl_ = std::getenv("AF_MR_NO_PDL") == nullptr;
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
@@ -311,9 +336,9 @@ double MR::eps_at_(int child_level) const {
 #define AF_MR_LAUNCH(kern, grid, ...)                                   \
   do {                                                                  \
     if (D_ == 3)                                                        \
-      kern<3><<<(grid), 256, 0, stream_>>>(__VA_ARGS__);                \
+      launch_k(pdl_, stream_, kern<3>, dim3(grid), 256, 0, __VA_ARGS__); \
     else                                                                \
-      kern<2><<<(grid), 256, 0, stream_>>>(__VA_ARGS__);                \
+      launch_k(pdl_, stream_, kern<2>, dim3(grid), 256, 0, __VA_ARGS__); \
     ++launches_;                                                        \
     AF_CUDA(cudaGetLastError());                                        \
   } while (0)
@@ -327,9 +352,9 @@ double MR::eps_at_(int child_level) const {
       const int* AF_T = (leaf) ? d_tiles_ : d_band_;                               \
       const int AF_S = (std::min((hi), L_) << 1) | ((leaf) ? 1 : 0);              \
       if (D_ == 3)                                                                 \
-        kern<3><<<grid_, 256, 0, stream_>>>(__VA_ARGS__, AF_T, AF_S);              \
+        launch_k(pdl_, stream_, kern<3>, grid_, 256, 0, __VA_ARGS__, AF_T, AF_S);   \
       else                                                                         \
-        kern<2><<<grid_, 256, 0, stream_>>>(__VA_ARGS__, AF_T, AF_S);              \
+        launch_k(pdl_, stream_, kern<2>, grid_, 256, 0, __VA_ARGS__, AF_T, AF_S);   \
       ++launches_;                                                                 \
       AF_CUDA(cudaGetLastError());                                                 \
     }                                                                              \
@@ -378,7 +403,9 @@ int MR::coop_blocks_() {
 // l reads level l-1 only, so after values of levels [lo, hi] change (stage
 // commit + projection) the refresh starts at lo+1.
 void MR::predict_fill_(int lo, int hi, int from) {
-  const int f = std::max(1, from);
+  // levels <= min_leaf are complete (build coarsens above it, refine only
+  // adds): no absent cells there
+  const int f = std::max({1, from, min_leaf_ + 1});
   const uint8_t* vm = virtuals_ ? d_mark_ : nullptr;
   const int small = in_body_ ? -1 : small_hi_;
   if (f <= small) {
@@ -443,11 +470,13 @@ void MR::build_lists_enqueue_() {
   const unsigned gw = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
   const unsigned gt = grid_for(nt);
   if (D_ == 3) {
-    mr_tile_flags_all<3><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
-    mr_tile_lists_all<3><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
+    launch_k(pdl_, stream_, mr_tile_flags_all<3>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_lpl_);
+    launch_k(pdl_, stream_, mr_tile_lists_all<3>, dim3(gt), 256, 0, d_tflag_, g_, d_band_, d_tiles_,
+             d_tile_count_);
   } else {
-    mr_tile_flags_all<2><<<gw, 256, 0, stream_>>>(d_st_, g_, d_tflag_, d_lpl_);
-    mr_tile_lists_all<2><<<gt, 256, 0, stream_>>>(d_tflag_, g_, d_band_, d_tiles_, d_tile_count_);
+    launch_k(pdl_, stream_, mr_tile_flags_all<2>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_lpl_);
+    launch_k(pdl_, stream_, mr_tile_lists_all<2>, dim3(gt), 256, 0, d_tflag_, g_, d_band_, d_tiles_,
+             d_tile_count_);
   }
   launches_ += 2;
   AF_CUDA(cudaGetLastError());
@@ -566,7 +595,7 @@ void MR::remove_virtual_leaves() {
 
 void MR::counts(long* leaves, long* nodes, long* internals) {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 3, stream_));
-  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(
+  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,
       d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
   ++launches_;
   unsigned long long h[3];
@@ -580,7 +609,7 @@ void MR::counts(long* leaves, long* nodes, long* internals) {
 // counts (leaves, nodes incl. virtual) and the CFL speed in one synchronisation
 void MR::cycle_stats_(long* leaves, long* nodes, double* smax) {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
-  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(
+  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,
       d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
   ++launches_;
   if (smax)
@@ -687,17 +716,17 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     if (D_ == 2) {
       const size_t sm = MRTile<2, kTX2, kTY2, 1>::smem_bytes;
       if (lim)
-        mr_stage_kernel<2, 1, kTX2, kTY2, 1><<<grid, kTX2 * kTY2, sm, stream_>>>(a, g_, lcode);
+        launch_k(pdl_, stream_, mr_stage_kernel<2, 1, kTX2, kTY2, 1>, grid, kTX2 * kTY2, sm, a, g_, lcode);
       else
-        mr_stage_kernel<2, 0, kTX2, kTY2, 1><<<grid, kTX2 * kTY2, sm, stream_>>>(a, g_, lcode);
+        launch_k(pdl_, stream_, mr_stage_kernel<2, 0, kTX2, kTY2, 1>, grid, kTX2 * kTY2, sm, a, g_, lcode);
     } else {
       const size_t sm = MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes;
       if (lim)
-        mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>
-            <<<grid, kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, lcode);
+        launch_k(pdl_, stream_, mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>, grid,
+                 kTX3 * kTY3 * kTZ3, sm, a, g_, lcode);
       else
-        mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>
-            <<<grid, kTX3 * kTY3 * kTZ3, sm, stream_>>>(a, g_, lcode);
+        launch_k(pdl_, stream_, mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>, grid,
+                 kTX3 * kTY3 * kTZ3, sm, a, g_, lcode);
     }
     ++launches_;
     AF_CUDA(cudaGetLastError());
@@ -1110,7 +1139,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   capture_while_([&](cudaGraphConditionalHandle h) {  // enforce_gradedness (mr_tree.cpp:404-444)
     AF_ML_LAUNCH(mr_grade_flag_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L);
     AF_ML_LAUNCH(mr_apply_split_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
-    mr_while_cond<<<1, 1, 0, stream_>>>(h, d_flagi_, 0, d_acc_ + 3);
+    launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, h, d_flagi_, 0, d_acc_ + 3);
     ++launches_;
     AF_CUDA(cudaGetLastError());
   });
@@ -1122,12 +1151,12 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
   virtuals_ = true;
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
-  mr_count_kernel<<<grid_for(g_.total_cells), 256, 0, stream_>>>(d_st_, d_mark_, g_.total_cells,
+  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,d_st_, d_mark_, g_.total_cells,
                                                                  d_red_);
   ++launches_;
   if (cfl > 0.0)
     AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
-  mr_cycle_begin<<<1, 1, 0, stream_>>>(d_red_, d_lpl_, L_, D_, cfl, fixed_dt, dx_L, d_dt_,
+  launch_k(pdl_, stream_, mr_cycle_begin, dim3(1), 1, 0, d_red_, d_lpl_, L_, D_, cfl, fixed_dt, dx_L, d_dt_,
                                        d_step3_, d_cycctl_, d_cycrec_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
@@ -1136,7 +1165,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   cur_step_ = 0;
   step_levels_(0, L_, 0.0, 0.0, 0);
   cur_step_ = -1;
-  mr_cycle_end<<<1, 1, 0, stream_>>>(d_red_ + 64, d_lpl_, L_, cfg_.extent, d_dt_, d_acc_,
+  launch_k(pdl_, stream_, mr_cycle_end, dim3(1), 1, 0, d_red_ + 64, d_lpl_, L_, cfg_.extent, d_dt_, d_acc_,
                                      d_cycctl_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
@@ -1149,7 +1178,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
       AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1), d_norms_,
                    d_flagi_, AF_BAND(l));
     predict_fill_(1, 0, min_leaf_ + 1);  // a no-op recompute when nothing merged
-    mr_while_cond<<<1, 1, 0, stream_>>>(h, d_flagi_, full_sweeps_ ? 0 : 1, d_acc_ + 4);
+    launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, h, d_flagi_, full_sweeps_ ? 0 : 1, d_acc_ + 4);
     ++launches_;
     AF_CUDA(cudaGetLastError());
   });
@@ -1436,7 +1465,8 @@ void MR::details(int level, double* out) {
   if (level < 0 || level >= L_) throw Error(AF_E_LEVEL_MISMATCH, "details: bad level");
   const long cells = mr_cells(D_, level);
   AF_CUDA(cudaMemsetAsync(d_det_ + g_.cell_off[level], 0xff, sizeof(double) * cells, stream_));
-  AF_MR_LAUNCH(mr_detail_level, grid_for(cells), d_V_, d_st_, d_det_, g_, level, d_norms_);
+  AF_MR_LAUNCH(mr_detail_level, grid_for(cells), d_V_, d_st_, d_det_, g_, level, d_norms_,
+               (const int*)nullptr, 0);
   AF_CUDA(cudaMemcpyAsync(out, d_det_ + g_.cell_off[level], sizeof(double) * cells,
                           cudaMemcpyDefault, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));

@@ -51,6 +51,7 @@ class MR {
   void cycle_stats_(long* leaves, long* nodes, double* smax);
   int coop_blocks_cache_ = 0;
   int small_hi_ = 0;
+  bool pdl_ = true;             // programmatic dependent launches (AF_MR_NO_PDL turns off)
   bool full_sweeps_ = false;    // AF_MR_FULL_SWEEPS: never skip a coarsen sweep; check the skip test
   bool small_coarsen_ = false;  // coarsest levels [0, small_hi_] use the cooperative small-level kernels
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);

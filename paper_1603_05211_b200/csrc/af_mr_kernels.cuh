@@ -157,6 +157,7 @@ __device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, 
 template <int D>
 __global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   project_level_dev<D>(V, st, g, l, tiles, ntiles);
 }
 
@@ -287,6 +288,7 @@ template <int D>
 __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
                                  MRLevels g, int l, int lo, int hi,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   predict_level_dev<D>(V, st, vmark, g, l, lo, hi, tiles, ntiles);
 }
 
@@ -295,6 +297,7 @@ __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vm
 template <int D>
 __global__ void mr_project_all(double* V, const uint8_t* st, MRLevels g, int lo, int top,
                                const int* band) {
+  AF_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   for (int l = top - 1; l >= lo; --l) {
     if (g.band_cnt[l]) project_level_dev<D>(V, st, g, l, band + g.tile_off[l], g.band_cnt[l]);
@@ -305,6 +308,7 @@ __global__ void mr_project_all(double* V, const uint8_t* st, MRLevels g, int lo,
 template <int D>
 __global__ void mr_predict_all(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
                                int lo, int hi, const int* band) {
+  AF_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   for (int l = 1; l <= g.L; ++l) {
     if (g.band_cnt[l])
@@ -397,6 +401,7 @@ template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
                                 int l, const double* norms,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv_, long c, bool valid, int ch) {
     const int l = lv_;
     const int n = 1 << l;
@@ -419,6 +424,7 @@ template <int D>
 __global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
                                      MRLevels g, int l, double eps,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const int n = 1 << l, pn = n >> 1;
@@ -436,6 +442,7 @@ template <int D>
 __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
                                 MRLevels g, int l, int r,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   // Target t is inserted iff some detail-flagged source s has map(s + o) == t
   // for an offset o != 0 with |o|_inf <= r. Clamping and folding never move a
   // position farther from s, so scanning the in-domain (or periodically
@@ -472,6 +479,7 @@ template <int D>
 __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels g, int l,
                                      int* changed,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const int n = 1 << l, nf = n << 1;
@@ -493,6 +501,7 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
 template <int D>
 __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const int n = 1 << l, nf = n << 1;
@@ -638,6 +647,7 @@ template <int D>
 __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
                                  const double* norms, int* merged,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   coarsen_level_dev<D>(V, st, g, l, eps, norms, merged, tiles, ntiles);
 }
 
@@ -648,6 +658,7 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
 template <int D>
 __global__ void mr_predict_small(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
                                  int lfrom, int lto, int lo, int hi, const int* band) {
+  AF_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   for (int l = lfrom; l <= lto; ++l) {
     predict_level_dev<D>(V, st, vmark, g, l, lo, hi, band + g.tile_off[l], -1);
@@ -658,6 +669,7 @@ __global__ void mr_predict_small(double* V, const uint8_t* st, const uint8_t* vm
 template <int D>
 __global__ void mr_project_small(double* V, const uint8_t* st, MRLevels g, int lhigh, int llow,
                                  const int* band) {
+  AF_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   for (int l = lhigh; l >= llow; --l) {
     project_level_dev<D>(V, st, g, l, band + g.tile_off[l], -1);
@@ -668,6 +680,7 @@ __global__ void mr_project_small(double* V, const uint8_t* st, MRLevels g, int l
 template <int D>
 __global__ void mr_coarsen_small(const double* V, uint8_t* st, MRLevels g, int lhigh, int llow,
                                  const double* norms, int* merged, const int* band) {
+  AF_PDL_ENTRY();
   cg::grid_group grid = cg::this_grid();
   for (int l = lhigh; l >= llow; --l) {
     coarsen_level_dev<D>(V, st, g, l, g.eps_l[l + 1], norms, merged, band + g.tile_off[l], -1);
@@ -681,6 +694,7 @@ __global__ void mr_coarsen_small(const double* V, uint8_t* st, MRLevels g, int l
 template <int D>
 __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels g, int l,
     const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const int n = 1 << l, pn = n >> 1;
@@ -706,6 +720,7 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
 // Counts per level: [0] leaves, [1] internals, [2] virtual-marked parents.
 static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, long n,
                                 unsigned long long* out) {
+  AF_PDL_ENTRY();
   unsigned long long lv = 0, in = 0, vm = 0;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n;
        c += (long)gridDim.x * blockDim.x) {
@@ -731,6 +746,7 @@ template <int D>
 __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
                                      double gamma, unsigned long long* target,
                                      const int* tiles = nullptr, int ntiles = 0) {
+  AF_PDL_ENTRY();
   __shared__ double red[8];
   double best = 0.0;
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
@@ -752,6 +768,7 @@ __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevel
 // Per-component max |q| of the finest level (set_norms_from, mr_tree.cpp:73-87).
 template <int D>
 __global__ void mr_norm_kernel(const double* V, MRLevels g, unsigned long long* out) {
+  AF_PDL_ENTRY();
   constexpr int NC = D + 2;
   const long cells = mr_cells(D, g.L), off = g.cell_off[g.L], comp = g.total_cells;
   double mx[NC];

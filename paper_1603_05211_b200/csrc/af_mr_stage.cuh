@@ -163,6 +163,7 @@ struct MRTile {
 template <int D, int LIM, int TX, int TY, int TZ>
 __global__ void __launch_bounds__(TX* TY* TZ, 2)
     mr_stage_kernel(MRStageArgs a, MRLevels g, int l) {
+  AF_PDL_ENTRY();
   using K = MRTile<D, TX, TY, TZ>;
   constexpr int NC = K::NC;
   if (failed_before(a.err)) return;
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
 template <int D>
 __global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* regbase,
                                    uint8_t* regmask, int* count) {
+  AF_PDL_ENTRY();
   const int n = 1 << l;
   const long cells = mr_cells(D, l), off = g.cell_off[l];
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
@@ -481,6 +483,7 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
                                    const int* regbase, const uint8_t* regmask, const double* regc,
                                    const double* regf, uint8_t* regfc, uint8_t* regff,
                                    double inv_sign_dx, unsigned long long* bad_key, int* err) {
+  AF_PDL_ENTRY();
   constexpr int NC = D + 2;
   if (failed_before(err)) return;
   const int n = 1 << l;
@@ -539,6 +542,7 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
 template <int D>
 __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
                                   unsigned long long* leaves_per_level) {
+  AF_PDL_ENTRY();
   constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
   constexpr int TZ = D == 3 ? kTileZ3 : 1;
   const long total = g.tile_off[g.L + 1];
@@ -577,6 +581,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
 template <int D>
 __global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, int* leaf,
                                   int* counts) {
+  AF_PDL_ENTRY();
   const long total = g.tile_off[g.L + 1];
   for (long tg = blockIdx.x * (long)blockDim.x + threadIdx.x; tg < total;
        tg += (long)gridDim.x * blockDim.x) {
@@ -616,6 +621,7 @@ template <int D>
 __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8_t* st,
                                      MRLevels g, int l, const int* guard, int promote,
                                      const int* tiles, int ntiles) {
+  AF_PDL_ENTRY();
   if (guard) {
     __shared__ int s;
     if (threadIdx.x == 0) s = guard[0] | guard[2];
@@ -639,6 +645,7 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
 template <int D, int TX, int TY, int TZ>
 __global__ void mr_tile_list_kernel(const uint8_t* st, MRLevels g, int l, int* tiles,
                                     int* count) {
+  AF_PDL_ENTRY();
   const int n = 1 << l;
   const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
   const int ntz = D == 3 ? (n + TZ - 1) / TZ : 1;

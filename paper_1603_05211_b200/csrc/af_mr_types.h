@@ -33,6 +33,14 @@ struct MRLevels {
 // cycle to cycle (CUDA-graph replay). A single-level launch may pass
 // ntiles = -1 (band) / -2 (leaf tiles) to read its count likewise.
 
+// Programmatic dependent launch: MR kernels are launched with
+// programmaticStreamSerialization, so a kernel may begin launching while its
+// predecessor runs. Every MR kernel first waits for the predecessor grid to
+// complete and its memory to be visible (griddepcontrol.wait; a no-op for an
+// ordinary launch), then lets its own successor begin launching.
+#define AF_PDL_ENTRY() \
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 constexpr int kTileX2 = 32, kTileY2 = 8;
 constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
 
