@@ -65,6 +65,18 @@ def peaks():
 
 
 # ------------------------------------------------------------------ clocks --
+def fp64_info():
+    """The fp64-pipe side of the roofline: measured fp64
+    throughput (tools/micro/fp64peak.cu) and the stage kernel's fp64-pipe
+    utilisation from its ncu capture (profiles/fp64_peaks.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
+        return {"peak_dadd_per_s": d["dadd_per_s"], "peak_ddiv_per_s": d["ddiv_ieee_per_s"],
+                "stage_pipe_frac": d["fv3d_stage_fp64_pipe_frac"], "source": d["source"]}
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled DURING the timed region, in
     process through NVML (the nvidia-smi query fields clocks.sm,
@@ -390,6 +402,7 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
             "kernel": "fv3d_stage" if dim == 3 else "fv2d_stage",
+            "fp64": fp64_info(),
             "note": "fp64-ALU bound in parity mode (no FMA contraction); see DESIGN.md"}
 
     cpu = None
@@ -499,8 +512,15 @@ def mr_bench(args, rank, world, local, torch, dist):
     # stage kernels: 2.5 S per leaf-cell stage, timed live by
     # CUDA events around each stage's launches on the solver stream
     achieved = 2.5 * S * stage_updates / (stage_ms / 1e3) / 1e9 if stage_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
             "peak_source": src, "kernel": "mr_stage_kernel",
             "kernel_share_of_step": stage_ms / ms if ms > 0 else None,
             "stage_launches": stage_launches,
