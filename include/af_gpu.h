@@ -117,6 +117,11 @@ af_status af_comm_unique_id(unsigned char id[128]);
 af_status af_comm_create(const unsigned char id[128], int n_ranks, int rank, int device,
                          af_comm** out);
 af_status af_comm_destroy(af_comm* comm);
+/* A group of n_ranks communicators for ranks emulated by host threads in one
+ * process on one GPU (halo exchanges become device-to-device copies, the
+ * reductions a host rendezvous). Each rank's calls must run on its own host
+ * thread. Used to test the multi-rank MR path on one GPU. */
+af_status af_comm_create_local(int n_ranks, int device, af_comm** comms);
 
 /* --------------------------------------------------------------- uniform -- */
 typedef struct af_uniform af_uniform;
@@ -197,6 +202,15 @@ typedef struct af_mr_cycle {
 } af_mr_cycle;
 
 af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** out);
+/* One rank of a spatially decomposed tree: the last axis
+ * (y in 2D, z in 3D) is split into slabs of rows from a partition level up;
+ * every call is collective over the ranks of `comm`. Leaf keys, counts and
+ * to_uniform rows refer to this rank's slab (af_mr_local_rows); cycle records,
+ * dt and the run diagnostics are global. */
+af_status af_mr_create_dist(const af_config* cfg, const af_mr_options* opt, af_comm* comm,
+                            af_mr** out);
+/* Rows [lo, hi) of the last axis at `level` that this rank owns. */
+af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi);
 af_status af_mr_destroy(af_mr* m);
 af_status af_mr_set_stream(af_mr* m, void* cuda_stream);
 /* from_uniform(level-L AoS data, 0, bc), norms, min leaf level, coarsen(eps)

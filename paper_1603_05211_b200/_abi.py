@@ -67,6 +67,7 @@ SIGNATURES = {
     "af_comm_unique_id": (C.c_int, [C.c_char_p]),
     "af_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
     "af_comm_destroy": (C.c_int, [_vp]),
+    "af_comm_create_local": (C.c_int, [C.c_int, C.c_int, C.POINTER(_vp)]),
     "af_uniform_create": (C.c_int, [C.POINTER(Config), _vp, C.POINTER(_vp)]),
     "af_uniform_destroy": (C.c_int, [_vp]),
     "af_uniform_set_stream": (C.c_int, [_vp, _vp]),
@@ -84,6 +85,9 @@ SIGNATURES = {
     "af_uniform_run_group": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_long, C.c_double, C.c_double,
                                        _dp, C.POINTER(RunDiag)]),
     "af_mr_create": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), C.POINTER(_vp)]),
+    "af_mr_create_dist": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), _vp,
+                                    C.POINTER(_vp)]),
+    "af_mr_local_rows": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "af_mr_destroy": (C.c_int, [_vp]),
     "af_mr_set_stream": (C.c_int, [_vp, _vp]),
     "af_mr_build": (C.c_int, [_vp, _vp]),

@@ -100,6 +100,22 @@ af_status af_comm_create(const unsigned char id[128], int n_ranks, int rank, int
   });
 }
 
+af_status af_comm_create_local(int n_ranks, int device, af_comm** comms) {
+  return guard(nullptr, [&] {
+    if (!comms || n_ranks < 1) throw af::Error(AF_E_ARGUMENT, "af_comm_create_local: bad argument");
+    auto group = std::make_shared<af::LocalGroup>(n_ranks);
+    for (int r = 0; r < n_ranks; ++r) {
+      auto* c = new af_comm;
+      c->c.n = n_ranks;
+      c->c.rank = r;
+      c->c.device = device;
+      c->c.local = true;
+      c->c.group = group;
+      comms[r] = c;
+    }
+  });
+}
+
 af_status af_comm_destroy(af_comm* comm) {
   if (!comm) return AF_OK;
   if (comm->c.nccl) ncclCommDestroy(comm->c.nccl);
@@ -229,6 +245,31 @@ af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** o
     }
     *out = h;
   });
+}
+
+af_status af_mr_create_dist(const af_config* cfg, const af_mr_options* opt, af_comm* comm,
+                            af_mr** out) {
+  return guard(nullptr, [&] {
+    if (!cfg || !opt || !out) throw af::Error(AF_E_ARGUMENT, "af_mr_create_dist: null argument");
+    auto* h = new af_mr;
+    try {
+      h->impl = new af::MR(*cfg, *opt, comm ? &comm->c : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi) {
+  if (!m || !lo || !hi) return AF_E_ARGUMENT;
+  try {
+    m->impl->local_rows(level, lo, hi);
+  } catch (const af::Error& e) {
+    return e.status;
+  }
+  return AF_OK;
 }
 
 af_status af_mr_destroy(af_mr* m) {

@@ -190,7 +190,7 @@ constexpr int kTX3 = 8, kTY3 = 8, kTZ3 = 4;
 
 }  // namespace
 
-MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
+MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o) {
   if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
   if (c.level < 2 || c.level > 15) throw Error(AF_E_CONFIG, "level must be in [2, 15]");
   if (c.flux != AF_FLUX_AUSM_PLUS || c.integrator != AF_INTEGRATOR_RK2)
@@ -264,6 +264,48 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
   small_coarsen_ = std::getenv("AF_MR_SMALL_COARSEN") != nullptr;
   full_sweeps_ = std::getenv("AF_MR_FULL_SWEEPS") != nullptr;
   pdl_ = std::getenv("AF_MR_NO_PDL") == nullptr;
+  // spatial decomposition: one slab of rows per rank from the partition level
+  // lp_ up (levels below are replicated); one rank owns everything
+  if (comm && comm->n > 1) {
+    if (comm->local && !comm->group)
+      throw Error(AF_E_ARGUMENT, "MR ranks of a local group need af_comm_create_local");
+    comm_ = comm;
+    nranks_ = comm->n;
+    rank_ = comm->rank;
+    dist_ = true;
+    int ml = o.min_leaf_level;
+    if (o.local_time) ml = std::max(ml, std::max(0, L_ - o.lt_gap));
+    lp_ = 0;
+    while ((1 << lp_) < 4 * nranks_ && lp_ < ml) ++lp_;
+    if ((1 << lp_) < nranks_)
+      throw Error(AF_E_CONFIG, "more ranks than slab rows at the minimum leaf level");
+  }
+  g_.lp = lp_;
+  g_.count_rep = rank_ == 0 ? 1 : 0;
+  g_.dist = dist_ ? 1 : 0;
+  for (int l = 0; l <= L_; ++l) {
+    part_rows_(rank_, l, &g_.own_lo[l], &g_.own_hi[l]);
+    const int n = 1 << l;
+    int ml = o.min_leaf_level;
+    if (o.local_time) ml = std::max(ml, std::max(0, L_ - o.lt_gap));
+    if (!dist_ || l < lp_ || (l == lp_ && lp_ == ml)) {
+      // replicated levels, and the partition level when leaves can sit there
+      // (their parents' details read the whole level): every row
+      g_.reg_lo[l] = 0;
+      g_.reg_hi[l] = n;
+    } else {
+      int lo = g_.own_lo[l] - kHalo, hi = g_.own_hi[l] + kHalo;
+      if (c.bc[2 * (D_ - 1)] != AF_BC_PERIODIC) {
+        lo = std::max(lo, 0);
+        hi = std::min(hi, n);
+      } else if (hi - lo >= n) {
+        lo = 0;
+        hi = n;
+      }
+      g_.reg_lo[l] = lo;
+      g_.reg_hi[l] = hi;
+    }
+  }
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
@@ -294,6 +336,7 @@ MR::MR(const af_config& c, const af_mr_options& o) : cfg_(c), opt_(o) {
       AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes));
   }
+  if (dist_) dist_setup_();
 }
 
 MR::~MR() {
@@ -304,6 +347,7 @@ MR::~MR() {
   cudaSetDevice(cfg_.device);
   if (own_stream_) cudaStreamSynchronize(own_stream_);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  dist_free_();
   for (GraphCache& gc : graphs_)
     if (gc.exec) cudaGraphExecDestroy(gc.exec);
   for (CycleGraph& cg : cyc_) {
@@ -428,6 +472,22 @@ void MR::predict_fill_(int lo, int hi, int from) {
 // project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
 void MR::project_range_(int lo, int top) {
   const int hi = std::min(top - 1, L_ - 1);
+  if (g_.dist) {
+    // owned rows of the split levels, then the halo rows (leaf values the
+    // stage just committed and these projections) from their owners, then
+    // the replicated levels below the partition level on every rank
+    for (int l = hi; l >= std::max(lo, lp_); --l)
+      if (AF_HAS(band_count_[l]))
+        AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l,
+                     AF_BAND(l));
+    exchange_(XV);
+    for (int l = std::min(hi, lp_ - 1); l >= lo; --l)
+      if (AF_HAS(band_count_[l]))
+        AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l,
+                     AF_BAND(l));
+    fresh_ = false;
+    return;
+  }
   for (int l = hi; l >= std::max(lo, small_hi_ + 1); --l)
     if (AF_HAS(band_count_[l]))
       AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
@@ -451,6 +511,7 @@ void MR::build_lists_() {
   AF_CUDA(cudaMemcpyAsync(h, d_tile_count_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaMemcpyAsync(lp, d_lpl_, sizeof lp, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) allreduce_(lp, L_ + 1, RED_SUM);  // leaves per level over all ranks
   for (int l = 0; l <= L_; ++l) {
     band_count_[l] = h[l];
     tile_count_[l] = h[17 + l];
@@ -512,8 +573,22 @@ void MR::build(const double* aos) {
   AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
   virtuals_ = false;
+  // every rank holds the whole initial field: project it everywhere, so the
+  // replicated tree starts identical on all ranks
+  const MRLevels gsave = g_;
+  if (dist_) {
+    for (int l = 0; l <= L_; ++l) {
+      g_.own_lo[l] = g_.reg_lo[l] = 0;
+      g_.own_hi[l] = g_.reg_hi[l] = 1 << l;
+    }
+    g_.dist = 0;
+  }
   build_lists_();
   project_range_(0, L_);
+  if (dist_) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    g_ = gsave;
+  }
   // set_norms_from (mr_tree.cpp:73-87)
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 8, stream_));
   AF_MR_LAUNCH(mr_norm_kernel, grid_for(cells), d_V_, g_, d_red_);
@@ -559,6 +634,27 @@ void MR::refine(int top) {
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
   AF_ML_LAUNCH(mr_apply_split_level, 1, L_ - 1, false, d_st_, split, g_, AF_L, d_flagi_);
   // enforce_gradedness (mr_tree.cpp:404-444)
+  if (g_.dist) {
+    // one decide/apply pass per round: the neighbours' splits arrive through
+    // the status halo, and the fixpoint test is over all ranks
+    exchange_(XST);
+    for (;;) {
+      AF_ML_LAUNCH(mr_grade_flag_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L);
+      AF_CUDA(cudaMemsetAsync(d_flagi_, 0, sizeof(int), stream_));
+      AF_ML_LAUNCH(mr_apply_split_level, 0, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
+      exchange_(XST);
+      int changed = 0;
+      AF_CUDA(cudaMemcpyAsync(&changed, d_flagi_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+      AF_CUDA(cudaStreamSynchronize(stream_));
+      unsigned long long ch = changed ? 1 : 0;
+      allreduce_(&ch, 1, RED_MAX);
+      if (!ch) break;
+    }
+    build_lists_();
+    lists_valid_ = true;
+    predict_fill_(1, 0);
+    return;
+  }
   for (;;) {
     // two decide/apply passes per host check: the fixpoint usually needs one
     // pass plus the verifying one, so this saves a synchronisation
@@ -580,7 +676,8 @@ void MR::refine(int top) {
 void MR::add_virtual_leaves() {
   AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
   if (!lists_valid_) build_lists_();
-  AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
+  // with ranks, leaves in halo rows mark owned parents too: scan the band
+  AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, !g_.dist, d_st_, d_mark_, g_, AF_L);
   virtuals_ = true;
 }
 
@@ -596,11 +693,12 @@ void MR::remove_virtual_leaves() {
 void MR::counts(long* leaves, long* nodes, long* internals) {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 3, stream_));
   launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,
-      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
+      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_, g_);
   ++launches_;
   unsigned long long h[3];
   AF_CUDA(cudaMemcpyAsync(h, d_red_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) allreduce_(h, 3, RED_SUM);
   if (leaves) *leaves = (long)h[0];
   if (internals) *internals = (long)h[1];
   if (nodes) *nodes = (long)(h[0] + h[1] + (h[2] << D_));
@@ -610,13 +708,17 @@ void MR::counts(long* leaves, long* nodes, long* internals) {
 void MR::cycle_stats_(long* leaves, long* nodes, double* smax) {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
   launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,
-      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_);
+      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_, g_);
   ++launches_;
   if (smax)
     AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
   unsigned long long h[4];
   AF_CUDA(cudaMemcpyAsync(h, d_red_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) {
+    allreduce_(h, 3, RED_SUM);
+    allreduce_(h + 3, 1, RED_MAX);  // non-negative double: max of the bit patterns
+  }
   *leaves = (long)h[0];
   *nodes = (long)(h[0] + h[1] + (h[2] << D_));
   if (smax) *smax = as_d(h[3]);
@@ -634,6 +736,7 @@ double MR::leaf_speed_sum() {
   unsigned long long b = 0;
   AF_CUDA(cudaMemcpyAsync(&b, d_red_, 8, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) allreduce_(&b, 1, RED_MAX);
   return as_d(b);
 }
 
@@ -783,7 +886,7 @@ void MR::evolve_global(double dt, af_step_diag* d) {
   stage_records_.clear();
   if (!lists_valid_) build_lists_();
   lists_valid_ = true;
-  if (fresh_ && !std::getenv("AF_MR_NO_GRAPH"))
+  if (fresh_ && !g_.dist && !std::getenv("AF_MR_NO_GRAPH"))
     evolve_global_graph_(dt);
   else
     step_levels_(0, L_, 0.0, dt, 0);
@@ -892,6 +995,11 @@ void MR::collect_stage_records_(af_step_diag* d) {
   std::vector<unsigned long long> h(ns * 17);
   AF_CUDA(cudaMemcpyAsync(h.data(), d_red_ + 64, 8 * ns * 17, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist)  // per record: 16 level maxima (wave-speed bits), then the fallback sum
+    for (size_t r = 0; r < ns; ++r) {
+      allreduce_(&h[r * 17], 16, RED_MAX);
+      allreduce_(&h[r * 17 + 16], 1, RED_SUM);
+    }
   double ws = 0.0;
   long fbs = 0;
   for (size_t r = 0; r < ns; ++r) {
@@ -962,10 +1070,13 @@ void MR::coarsen() {
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
     const int csm = small_coarsen_ ? small_hi_ : -1;
-    for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l)
+    for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l) {
       if (band_count_[l])
         AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, band_count_[l], 1 << D_), d_V_, d_st_, g_, l,
                      eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
+      // the next level's merge_allowed reads this level's status in halo rows
+      if (g_.dist) exchange_(XST);
+    }
     const int shi = std::min(L_ - 1, csm);
     if (shi >= min_leaf_) {
       if (D_ == 3)
@@ -979,6 +1090,12 @@ void MR::coarsen() {
     int merged[2] = {0, 0};
     AF_CUDA(cudaMemcpyAsync(merged, d_flagi_, sizeof merged, cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
+    if (g_.dist) {
+      unsigned long long m2[2] = {(unsigned long long)merged[0], (unsigned long long)merged[1]};
+      allreduce_(m2, 2, RED_MAX);
+      merged[0] = (int)m2[0];
+      merged[1] = (int)m2[1];
+    }
     if (full_sweeps_ && clean && merged[0])
       throw Error(AF_E_INTERNAL, "coarsen: a sweep after a clean sweep merged (skip test unsound)");
     if (!merged[0]) break;
@@ -996,6 +1113,16 @@ void MR::check_error_(long step) {
   int h[4];
   AF_CUDA(cudaMemcpyAsync(h, d_err_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) {  // a failure on any rank stops every rank with the same report
+    unsigned long long f[3] = {h[0] ? 1ull : 0ull, h[2] ? 1ull : 0ull, (unsigned)h[3]};
+    allreduce_(f, 3, RED_MAX);
+    unsigned long long code = (unsigned)h[1];
+    allreduce_(&code, 1, RED_MIN);
+    h[0] = (int)f[0];
+    h[2] = (int)f[1];
+    h[3] = (int)f[2];
+    h[1] = (int)code;
+  }
   if (!h[0] && !h[2]) return;
   if (d_badkey_) {
     unsigned long long bk = ~0ull;
@@ -1036,6 +1163,7 @@ void MR::check_error_(long step) {
   const std::string pre = step >= 0 ? "step " + std::to_string(step) + ": " : "";
   std::string msg = pre + "non-physical state";
   // leaves in ascending pack_key order: level, then i, then j, then k
+  // (with ranks: this rank's rows; the global first is the minimum key)
   bool found = false;
   for (int l = lvl_lo; l <= std::min(lvl_hi, L_) && !found; ++l) {
     const int n = 1 << l;
@@ -1044,7 +1172,7 @@ void MR::check_error_(long step) {
       for (int j = 0; j < n && !found; ++j)
         for (int k = 0; k < nk && !found; ++k) {
           const long c = g_.cell_off[l] + (D_ == 3 ? ((long)k * n + j) * n + i : (long)j * n + i);
-          if (hs[c] != ST_LEAF) continue;
+          if (hs[c] != ST_LEAF || !row_owned(g_, l, D_ == 3 ? k : j)) continue;
           const double rho = hv[c];
           double msq = hv[comp + c] * hv[comp + c] + hv[2 * comp + c] * hv[2 * comp + c];
           if (D_ == 3) msq = msq + hv[3 * comp + c] * hv[3 * comp + c];
@@ -1058,12 +1186,39 @@ void MR::check_error_(long step) {
             last_.k = k;
             last_.rho = rho;
             last_.p = p;
-            const std::string node = "level " + std::to_string(l) + " (" + std::to_string(i) +
-                                     "," + std::to_string(j) + "," + std::to_string(k) + ")";
-            msg = kind == 2 ? pre + "post-step " + node
-                            : pre + node + ": rho=" + fmt_f(rho) + " p=" + fmt_f(p);
           }
         }
+  }
+  if (g_.dist) {
+    const auto key_of = [](const af_error& e) {
+      return ((unsigned long long)e.level << 45) | ((unsigned long long)e.i << 30) |
+             ((unsigned long long)e.j << 15) | (unsigned long long)e.k;
+    };
+    unsigned long long key = found ? key_of(last_) : ~0ull;
+    allreduce_(&key, 1, RED_MIN);
+    unsigned long long v[2] = {0, 0};
+    if (found && key_of(last_) == key) {
+      std::memcpy(&v[0], &last_.rho, 8);
+      std::memcpy(&v[1], &last_.p, 8);
+    }
+    allreduce_(v, 2, RED_SUM);  // only the owner contributes
+    found = key != ~0ull;
+    if (found) {
+      const unsigned long long m15 = (1ull << 15) - 1;
+      last_.level = (int)(key >> 45);
+      last_.i = (int)((key >> 30) & m15);
+      last_.j = (int)((key >> 15) & m15);
+      last_.k = (int)(key & m15);
+      std::memcpy(&last_.rho, &v[0], 8);
+      std::memcpy(&last_.p, &v[1], 8);
+    }
+  }
+  if (found) {
+    const std::string node = "level " + std::to_string(last_.level) + " (" +
+                             std::to_string(last_.i) + "," + std::to_string(last_.j) + "," +
+                             std::to_string(last_.k) + ")";
+    msg = kind == 2 ? pre + "post-step " + node
+                    : pre + node + ": rho=" + fmt_f(last_.rho) + " p=" + fmt_f(last_.p);
   }
   std::snprintf(last_.message, sizeof last_.message, "%s", msg.c_str());
   throw Error(AF_E_NONPHYSICAL, last_.message);
@@ -1151,8 +1306,8 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
   virtuals_ = true;
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
-  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,d_st_, d_mark_, g_.total_cells,
-                                                                 d_red_);
+  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0, d_st_,
+           d_mark_, g_.total_cells, d_red_, g_);
   ++launches_;
   if (cfl > 0.0)
     AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
@@ -1327,7 +1482,7 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
   long done = 0, cycle = 0;
   double t = 0.0;
   // global time step: whole cycles replay as one graph each (run_batch_graph_)
-  const bool graph = !opt_.local_time && !std::getenv("AF_MR_NO_GRAPH") &&
+  const bool graph = !opt_.local_time && !dist_ && !std::getenv("AF_MR_NO_GRAPH") &&
                      !std::getenv("AF_MR_NO_CYCLE_GRAPH") && !std::getenv("AF_MR_TIMING");
   while (done < n_steps) {
     if (graph) {
@@ -1441,6 +1596,7 @@ long MR::leaf_keys(uint64_t* keys, long cap) {
     for (long c = 0; c < cells; ++c) {
       if (hs[g_.cell_off[l] + c] != ST_LEAF) continue;
       const uint64_t i = c % n, j = (c / n) % n, k = D_ == 3 ? c / ((long)n * n) : 0;
+      if (!row_counted(g_, l, (int)(D_ == 3 ? k : j))) continue;  // this rank's leaves
       out.push_back(((uint64_t)l << 45) | (i << 30) | (j << 15) | k);  // pack_key
     }
   }

@@ -11,9 +11,19 @@ namespace af {
 
 struct MRStageArgs;
 
+// One contiguous run of whole rows in a halo exchange (af_mr_dist.cu).
+struct MR_XSeg {
+  long cell;   // first cell (concatenated level index)
+  long cells;  // contiguous cells
+  long pos;    // offset in the peer's packed section
+};
+
 class MR {
  public:
-  MR(const af_config& cfg, const af_mr_options& opt);
+  // comm: null or one rank for a single GPU; otherwise this rank's slab of
+  // the spatial decomposition.
+  MR(const af_config& cfg, const af_mr_options& opt, Comm* comm = nullptr);
+  void local_rows(int level, int* lo, int* hi) const;  // slab rows this rank owns
   ~MR();
   MR(const MR&) = delete;
   MR& operator=(const MR&) = delete;
@@ -119,6 +129,30 @@ class MR {
                         af_mr_cycle* cycles, long max_cycles);
   void cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long& cycle, double& t,
                    af_mr_cycle* cycles, long max_cycles);
+  // ---- spatial decomposition (af_mr_dist.cu) ----
+  Comm* comm_ = nullptr;
+  int nranks_ = 1, rank_ = 0;
+  bool dist_ = false;
+  int lp_ = 0;  // partition level: levels >= lp_ are split in slabs of rows
+  using XSeg = MR_XSeg;
+  struct Peer {
+    int rank = 0;
+    std::vector<XSeg> send, recv;
+    long send_cells = 0, recv_cells = 0;
+    XSeg* d_send = nullptr;
+    XSeg* d_recv = nullptr;
+    uint8_t* sbuf = nullptr;
+    uint8_t* rbuf = nullptr;
+  };
+  std::vector<Peer> peers_;
+  unsigned long long* d_xred_ = nullptr;
+  enum { XV = 1, XST = 2, XMARK = 4 };
+  enum { RED_MAX = 0, RED_SUM = 1, RED_MIN = 2 };
+  void part_rows_(int r, int l, int* lo, int* hi) const;
+  void dist_setup_();
+  void dist_free_();
+  void exchange_(int mask);
+  void allreduce_(unsigned long long* v, int k, int op);
   double norms_host_[5] = {1, 1, 1, 1, 1};
   double eps_at_(int child_level) const;
 

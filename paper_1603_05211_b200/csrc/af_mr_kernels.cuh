@@ -137,7 +137,7 @@ __device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, 
     const long off = g.cell_off[l], foff = g.cell_off[l + 1];
     const long comp = g.total_cells;
     const double w = 1.0 / (double)(1 << D);
-    if (st[off + c] != ST_INTERNAL) return;
+    if (st[off + c] != ST_INTERNAL || !row_owned(g, l, mr_row(D, l, c))) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     double s[NC];
 #pragma unroll
@@ -484,7 +484,7 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
     const int l = lv_;
     const int n = 1 << l, nf = n << 1;
     const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-    if (!flag[off + c] || st[off + c] != ST_LEAF) return;
+    if (!flag[off + c] || st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(D, l, c))) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     st[off + c] = ST_INTERNAL;
     for (int ch = 0; ch < (1 << D); ++ch)
@@ -557,7 +557,8 @@ __device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, 
     cc[2] = D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0;
     const long fc = foff + mr_idx(D, nf, cc[0], cc[1], cc[2]);
     // candidate: INTERNAL node whose children are all leaves (mr_tree.cpp:486-497)
-    const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF);
+    const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF &&
+                                        row_owned(g, l, mr_row(D, l, c)));
     double r = 0.0;
     if (cand) r = child_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], ch, norms);
     r = node_group_max<D>(r);
@@ -712,18 +713,23 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
         p[a] = mr_map(p[a], n, g.bc[2 * a], g.bc[2 * a + 1], fl);
         if (st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_ABSENT) continue;
         const long pc = poff + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
-        if (st[pc] == ST_LEAF) mark[pc] = 1;
+        if (st[pc] == ST_LEAF && row_owned(g, l - 1, p[D - 1] >> 1)) mark[pc] = 1;
       }
   });
 }
 
 // Counts per level: [0] leaves, [1] internals, [2] virtual-marked parents.
 static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, long n,
-                                unsigned long long* out) {
+                                unsigned long long* out, MRLevels g) {
   AF_PDL_ENTRY();
   unsigned long long lv = 0, in = 0, vm = 0;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n;
        c += (long)gridDim.x * blockDim.x) {
+    if (g.dist) {  // count each cell on one rank only
+      int l = 0;
+      while (c >= g.cell_off[l + 1]) ++l;
+      if (!row_counted(g, l, mr_row(g.dim, l, c - g.cell_off[l]))) continue;
+    }
     const uint8_t s = st[c];
     lv += s == ST_LEAF;
     in += s == ST_INTERNAL;
@@ -752,7 +758,7 @@ __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevel
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const long off = g.cell_off[l], comp = g.total_cells;
-    if (st[off + c] != ST_LEAF) return;
+    if (st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(D, l, c))) return;
     Cons<D> q;
     q.rho = V[off + c];
 #pragma unroll

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
   const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
-  const bool is_leaf = inside && a.st[own] == ST_LEAF;
+  const bool is_leaf = inside && a.st[own] == ST_LEAF && row_owned(g, l, D == 3 ? cz : cy);
   leaf[tid] = is_leaf;
   for (int idx = tid; idx < K::HP; idx += K::NT) {
     const int ix = idx % K::HX, iy = (idx / K::HX) % K::HY, iz = D == 3 ? idx / (K::HX * K::HY) : 0;
@@ -535,6 +535,18 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
   }
 }
 
+// Does the tile whose slab-axis rows start at r0 hold a row of this rank's
+// region (owned rows + halo)?
+template <int D>
+__device__ __forceinline__ bool tile_in_region(const MRLevels& g, int l, int r0) {
+  if (!g.dist) return true;
+  constexpr int TR = D == 3 ? kTileZ3 : kTileY2;
+  const int n = 1 << l;
+  for (int r = r0; r < r0 + TR && r < n; ++r)
+    if (row_in_region(g, l, r)) return true;
+  return false;
+}
+
 // Work-tile flags over every level at once (one warp per tile): bit 0 the
 // tile holds a leaf, bit 1 it holds a cell whose parent exists (every node's
 // parent exists, so these tiles cover the tree and everything a split can
@@ -557,10 +569,15 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     const int z0 = D == 3 ? (int)(t / ((long)g.ntx[l] * g.nty[l])) * TZ : 0;
     unsigned nleaf = 0;
     bool pex = false;
+    if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
+      if (lane == 0) tflag[tg] = 0;
+      continue;
+    }
     for (int c = lane; c < TX * TY * TZ; c += 32) {
       const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
       if (x >= n || y >= n || (D == 3 && z >= n)) continue;
-      nleaf += st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF;
+      nleaf += st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF &&
+               row_counted(g, l, D == 3 ? z : y);
       pex = pex || l == 0 ||
             st[g.cell_off[l - 1] + mr_idx(D, n >> 1, x >> 1, y >> 1, z >> 1)] != ST_ABSENT;
     }
@@ -608,6 +625,8 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, i
           if (ok && (tflag[g.tile_off[l] + ((long)q[2] * nt[1] + q[1]) * nt[0] + q[0]] & 2))
             in_band = true;
         }
+    if (in_band && !tile_in_region<D>(g, l, tc[D - 1] * (D == 3 ? kTileZ3 : kTileY2)))
+      in_band = false;
     if (in_band) band[g.tile_off[l] + atomicAdd(counts + l, 1)] = (int)t;
     if (tflag[tg] & 1) leaf[g.tile_off[l] + atomicAdd(counts + 17 + l, 1)] = (int)t;
   }
@@ -634,7 +653,7 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
   const long comp = g.total_cells;
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
     const long off = g.cell_off[lv];
-    if (st[off + c] != ST_LEAF) return;
+    if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(D, lv, c))) return;
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
   });

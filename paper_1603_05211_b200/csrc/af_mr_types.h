@@ -23,7 +23,39 @@ struct MRLevels {
   int leaf_cnt[17];        // tiles in the level's leaf-tile list
   double eps_l[17];        // refine threshold for leaves of level l (host-filled)
   const int* dcnt;         // device copy of the counts: [l] band, [17 + l] leaf tiles
+  // Spatial decomposition: slabs of rows along the last
+  // axis (y in 2D, z in 3D). A rank computes and decides for the rows it owns,
+  // [own_lo, own_hi), and keeps up-to-date copies of the rows within
+  // kHalo of them, [reg_lo, reg_hi) (may wrap when that axis is periodic).
+  // Levels below `lp` are replicated (no leaves or absent cells there) and are
+  // counted by rank 0 only (`count_rep`). One rank: everything owned.
+  int own_lo[17], own_hi[17];
+  int reg_lo[17], reg_hi[17];
+  int lp;
+  int count_rep;
+  int dist;                // more than one rank
 };
+
+constexpr int kHalo = 2;  // rows of halo per level (stencil reach)
+
+// Slab row of cell c of level l (the last axis index).
+__host__ __device__ __forceinline__ int mr_row(int dim, int l, long c) {
+  return (int)(c >> ((dim - 1) * l));
+}
+__host__ __device__ __forceinline__ bool row_owned(const MRLevels& g, int l, int r) {
+  return r >= g.own_lo[l] && r < g.own_hi[l];
+}
+__host__ __device__ __forceinline__ bool row_in_region(const MRLevels& g, int l, int r) {
+  const int n = 1 << l, len = g.reg_hi[l] - g.reg_lo[l];
+  if (len >= n) return true;
+  int d = (r - g.reg_lo[l]) % n;
+  if (d < 0) d += n;
+  return d < len;
+}
+// counted once across ranks (leaf/node counts, leaves per level)
+__host__ __device__ __forceinline__ bool row_counted(const MRLevels& g, int l, int r) {
+  return l < g.lp ? g.count_rep != 0 : row_owned(g, l, r);
+}
 
 // Multi-level launch convention: a kernel called with l = -(lo + 1) and
 // ntiles = hi << 1 | sel covers the band (sel 0) or leaf-tile (sel 1) lists of

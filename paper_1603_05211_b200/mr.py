@@ -66,7 +66,9 @@ def eps_levels_scaled(eps: float, level: int, dim: int) -> list:
 class MRSolver:
     def __init__(self, dim: int, level: int, options: MROptions | None = None,
                  scheme: SchemeConfig | None = None, bc=None, gamma: float = 1.4,
-                 extent: float = 1.0, device: int = 0):
+                 extent: float = 1.0, device: int = 0, comm=None):
+        """comm: an af_comm handle for one rank of a spatially decomposed tree
+        (af_mr_create_dist); None for a single GPU."""
         self._lib = _abi.load()
         scheme = scheme or SchemeConfig(limiter=MINMOD)
         options = options or MROptions()
@@ -88,7 +90,10 @@ class MRSolver:
         o.local_time = int(options.local_time)
         o.lt_gap = options.local_time_level_gap
         h = C.c_void_p()
-        st = self._lib.af_mr_create(C.byref(cfg), C.byref(o), C.byref(h))
+        if comm is None:
+            st = self._lib.af_mr_create(C.byref(cfg), C.byref(o), C.byref(h))
+        else:
+            st = self._lib.af_mr_create_dist(C.byref(cfg), C.byref(o), comm, C.byref(h))
         if st:
             e = _abi.ErrorRec()
             self._lib.af_mr_last_error(None, C.byref(e))
@@ -173,6 +178,13 @@ class MRSolver:
         self._check(self._lib.af_mr_to_uniform(self._h, level, C.c_void_p(out.ctypes.data)))
         return out
 
+    def local_rows(self, level: int | None = None):
+        """Rows [lo, hi) of the last axis this rank owns at `level`."""
+        level = self.level if level is None else level
+        lo, hi = C.c_int(), C.c_int()
+        self._check(self._lib.af_mr_local_rows(self._h, level, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
     def details(self, level: int) -> np.ndarray:
         n = 1 << level
         out = np.empty(n ** self.dim, dtype=np.float64)
@@ -207,3 +219,84 @@ class MRSolver:
             nc += 1
         return MRReport(n_steps=d.steps_done, max_cfl=d.max_cfl, fallbacks=d.fallbacks, t=d.t,
                         cycles=np.array(rows, dtype=np.float64).reshape(-1, 6))
+
+
+class MRGroup:
+    """n_ranks slabs of one MR tree, each rank an MRSolver driven by its own
+    host thread on ONE GPU (af_comm_create_local): the multi-rank code path
+    (slab ownership, status/value halo exchanges, reductions) with
+    device-to-device copies in place of NCCL. Used to check that results do
+    not depend on the rank count."""
+
+    def __init__(self, dim: int, level: int, n_ranks: int, options: MROptions | None = None,
+                 scheme: SchemeConfig | None = None, bc=None, gamma: float = 1.4,
+                 extent: float = 1.0, device: int = 0):
+        self._lib = _abi.load()
+        self.n_ranks, self.dim, self.level = n_ranks, dim, level
+        comms = (C.c_void_p * n_ranks)()
+        st = self._lib.af_comm_create_local(n_ranks, device, comms)
+        if st:
+            raise_status(st, "af_comm_create_local failed")
+        self._comms = [comms[r] for r in range(n_ranks)]
+        self.ranks = [MRSolver(dim, level, options, scheme, bc, gamma, extent, device,
+                               comm=c) for c in self._comms]
+
+    def _all(self, fn):
+        import threading
+        out, err = [None] * self.n_ranks, [None] * self.n_ranks
+
+        def one(r):
+            try:
+                out[r] = fn(self.ranks[r])
+            except BaseException as e:  # re-raised on the caller's thread
+                err[r] = e
+
+        ts = [threading.Thread(target=one, args=(r,)) for r in range(self.n_ranks)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return out
+
+    def close(self):
+        for s in getattr(self, "ranks", []):
+            s.close()
+        for c in getattr(self, "_comms", []):
+            self._lib.af_comm_destroy(c)
+        self.ranks, self._comms = [], []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def build(self, aos) -> None:
+        self._all(lambda s: s.build(aos))
+
+    def run(self, n_steps: int, cfl: float = 0.0, fixed_dt: float = 0.0) -> MRReport:
+        reps = self._all(lambda s: s.run(n_steps, cfl=cfl, fixed_dt=fixed_dt))
+        for r in reps[1:]:  # cycle records and diagnostics are global on every rank
+            if not (np.array_equal(r.cycles, reps[0].cycles) and r.max_cfl == reps[0].max_cfl):
+                raise RuntimeError("ranks disagree on the run report")
+        return reps[0]
+
+    def leaves(self) -> np.ndarray:
+        return np.sort(np.concatenate(self._all(lambda s: s.leaves())))
+
+    def to_uniform(self, level: int | None = None) -> np.ndarray:
+        level = self.level if level is None else level
+        n = 1 << level
+        row = n ** (self.dim - 1)
+        parts = self._all(lambda s: (s.local_rows(level), s.to_uniform(level)))
+        out = np.empty((n ** self.dim, 5), dtype=np.float64)
+        covered = 0
+        for (lo, hi), u in parts:
+            out[lo * row:hi * row] = u[lo * row:hi * row]
+            covered += hi - lo
+        if covered != n:
+            raise RuntimeError("rank rows do not tile the level")
+        return out
