@@ -279,6 +279,10 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
     while ((1 << lp_) < 4 * nranks_ && lp_ < ml) ++lp_;
     if ((1 << lp_) < nranks_)
       throw Error(AF_E_CONFIG, "more ranks than slab rows at the minimum leaf level");
+    // halo depth: the stencil reach (2), or the LT refine buffer radius
+    // 2^(l-top-1) at l = L-1 with top >= min leaf level (mr_solver.cpp:358-362)
+    halo_ = 2;
+    if (o.local_time) halo_ = std::max(2, 1 << std::max(0, L_ - ml - 2));
   }
   g_.lp = lp_;
   g_.count_rep = rank_ == 0 ? 1 : 0;
@@ -294,7 +298,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
       g_.reg_lo[l] = 0;
       g_.reg_hi[l] = n;
     } else {
-      int lo = g_.own_lo[l] - kHalo, hi = g_.own_hi[l] + kHalo;
+      int lo = g_.own_lo[l] - halo_, hi = g_.own_hi[l] + halo_;
       if (c.bc[2 * (D_ - 1)] != AF_BC_PERIODIC) {
         lo = std::max(lo, 0);
         hi = std::min(hi, n);
@@ -676,8 +680,10 @@ void MR::refine(int top) {
 void MR::add_virtual_leaves() {
   AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
   if (!lists_valid_) build_lists_();
-  // with ranks, leaves in halo rows mark owned parents too: scan the band
+  // with ranks, leaves in halo rows mark owned parents too: scan the band;
+  // the stage reads the marks of halo parents (MRLT interpolation, registers)
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, !g_.dist, d_st_, d_mark_, g_, AF_L);
+  if (g_.dist) exchange_(XMARK);
   virtuals_ = true;
 }
 
@@ -1129,6 +1135,12 @@ void MR::check_error_(long step) {
     int regerr = 0;
     AF_CUDA(cudaMemcpy(&bk, d_badkey_, sizeof bk, cudaMemcpyDeviceToHost));
     AF_CUDA(cudaMemcpy(&regerr, d_regerr_, sizeof regerr, cudaMemcpyDeviceToHost));
+    if (g_.dist) {
+      allreduce_(&bk, 1, RED_MIN);
+      unsigned long long re = regerr ? 1 : 0;
+      allreduce_(&re, 1, RED_MAX);
+      regerr = (int)re;
+    }
     if (bk != ~0ull) {
       const unsigned long long ck = bk >> 3;
       const unsigned long long mask = (1ull << 15) - 1;

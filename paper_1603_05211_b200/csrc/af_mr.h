@@ -134,6 +134,7 @@ class MR {
   int nranks_ = 1, rank_ = 0;
   bool dist_ = false;
   int lp_ = 0;  // partition level: levels >= lp_ are split in slabs of rows
+  int halo_ = 2;  // halo rows kept per level
   using XSeg = MR_XSeg;
   struct Peer {
     int rank = 0;

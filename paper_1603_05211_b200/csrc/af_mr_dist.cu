@@ -4,7 +4,7 @@
 //
 // Every rank keeps the full-size level arrays (global indexing, so no kernel
 // changes its addressing) but computes and decides only for the rows it owns;
-// rows within kHalo of them are refreshed from their owners. Levels below the
+// rows within halo_ of them are refreshed from their owners. Levels below the
 // partition level are replicated (they hold no leaves and no absent cells).
 // The transport is NCCL (one process per GPU) or, for tests on one GPU, a
 // group of host threads exchanging through device-to-device copies.
@@ -102,7 +102,7 @@ void MR::dist_setup_() {
     }
     int a, b;
     part_rows_(r, l, &a, &b);
-    for (int y = a - kHalo; y < b + kHalo; ++y) {
+    for (int y = a - halo_; y < b + halo_; ++y) {
       int yy = y;
       if (yy < 0 || yy >= n) {
         if (!periodic) continue;

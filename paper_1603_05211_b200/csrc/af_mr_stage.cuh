@@ -202,7 +202,13 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
   const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
   const bool is_leaf = inside && a.st[own] == ST_LEAF && row_owned(g, l, D == 3 ? cz : cy);
-  leaf[tid] = is_leaf;
+  // with ranks, a stage-2 register pass also evaluates the halo-row leaves:
+  // their fine-side register shares for this rank's coarse cells
+  // (face_flux_at, mr_solver.cpp:147-159) are computed here, where those
+  // registers live, from the halo copy of the same inputs
+  const bool is_hleaf = !is_leaf && a.reg_stage && g.dist && inside && a.st[own] == ST_LEAF &&
+                        row_in_region(g, l, D == 3 ? cz : cy);
+  leaf[tid] = is_leaf || is_hleaf;
   for (int idx = tid; idx < K::HP; idx += K::NT) {
     const int ix = idx % K::HX, iy = (idx / K::HX) % K::HY, iz = D == 3 ? idx / (K::HX * K::HY) : 0;
     const bool ccx = ix >= 2 && ix < TX + 2, ccy = iy >= 2 && iy < TY + 2;
@@ -378,7 +384,8 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
             } else if (nst == ST_ABSENT && l >= 1 && l - 1 < a.lo) {
               const int pn = n >> 1;
               const long pc = g.cell_off[l - 1] + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
-              if (a.vmark[pc]) {
+              // (a coarse cell of another rank gets this share from its owner)
+              if (a.vmark[pc] && row_owned(g, l - 1, p[D - 1] >> 1)) {
                 // face into an already-advanced coarser cell: fine register share
                 const int R = reg_index(a.regbase, a.regmask, pc, ax * 2 + (dir > 0 ? 0 : 1));
                 if (R >= 0) {
@@ -422,6 +429,41 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       q.E = o[NC - 1];
       if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
     }
+  } else if (is_hleaf) {
+    const int c[3] = {cx, cy, cz};
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+#pragma unroll
+      for (int dir = -1; dir <= 1; dir += 2) {
+        int p[3] = {c[0], c[1], c[2]};
+        p[ax] += dir;
+        bool flp;
+        p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
+        if (a.st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_ABSENT || l < 1 || l - 1 >= a.lo)
+          continue;
+        const int pn = n >> 1;
+        const long pc = g.cell_off[l - 1] + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+        if (!a.vmark[pc] || !row_owned(g, l - 1, p[D - 1] >> 1)) continue;
+        int fi;
+        if (ax == 0) fi = (tz * TY + ty) * (TX + 1) + tx + (dir > 0);
+        else if (ax == 1) fi = K::NXF + (tz * (TY + 1) + ty + (dir > 0)) * TX + tx;
+        else fi = K::NXF + K::NYF + ((tz + (dir > 0)) * TY + ty) * TX + tx;
+        const int R = reg_index(a.regbase, a.regmask, pc, ax * 2 + (dir > 0 ? 0 : 1));
+        if (R >= 0) {
+          int t = 0;
+#pragma unroll
+          for (int b = 0; b < D; ++b)
+            if (b != ax) t = 2 * t + (c[b] & 1);
+          const double w = a.step_dt * a.share;
+          double* dst = a.regf + (((long)R * 2 + a.sub) * 4 + t) * NC;
+#pragma unroll
+          for (int m = 0; m < NC; ++m) dst[m] = fl[m * K::NF + fi] * w;
+          a.regff[R] = 1;
+        } else {
+          atomicExch(a.regerr, 1);
+        }
+      }
+    }
   }
   // per-level max wave speed of this tile: warp max, one atomic per warp
   // (non-negative doubles order like their bit patterns)
@@ -458,7 +500,7 @@ __global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* re
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
     unsigned mask = 0;
-    if (st[off + c] == ST_LEAF) {
+    if (st[off + c] == ST_LEAF && row_owned(g, l, mr_row(D, l, c))) {
       const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
       for (int ax = 0; ax < D; ++ax)
         for (int side = 0; side < 2; ++side) {
@@ -568,7 +610,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     const int x0 = (int)(t % g.ntx[l]) * TX, y0 = (int)((t / g.ntx[l]) % g.nty[l]) * TY;
     const int z0 = D == 3 ? (int)(t / ((long)g.ntx[l] * g.nty[l])) * TZ : 0;
     unsigned nleaf = 0;
-    bool pex = false;
+    bool pex = false, rleaf = false;
     if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
       if (lane == 0) tflag[tg] = 0;
       continue;
@@ -576,15 +618,19 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     for (int c = lane; c < TX * TY * TZ; c += 32) {
       const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
       if (x >= n || y >= n || (D == 3 && z >= n)) continue;
-      nleaf += st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF &&
-               row_counted(g, l, D == 3 ? z : y);
+      const bool lf = st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF;
+      nleaf += lf && row_counted(g, l, D == 3 ? z : y);
+      rleaf = rleaf || (lf && row_in_region(g, l, D == 3 ? z : y));
       pex = pex || l == 0 ||
             st[g.cell_off[l - 1] + mr_idx(D, n >> 1, x >> 1, y >> 1, z >> 1)] != ST_ABSENT;
     }
     for (int o = 16; o > 0; o >>= 1) nleaf += __shfl_xor_sync(0xffffffffu, nleaf, o);
     pex = __any_sync(0xffffffffu, pex);
+    rleaf = __any_sync(0xffffffffu, rleaf);
     if (lane == 0) {
-      tflag[tg] = (nleaf ? 1 : 0) | (pex ? 2 : 0);
+      // bit 0: the tile holds a leaf this rank steps, or (with ranks) a
+      // halo leaf whose register shares it computes
+      tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0);
       if (nleaf) atomicAdd(leaves_per_level + l, (unsigned long long)nleaf);
     }
   }

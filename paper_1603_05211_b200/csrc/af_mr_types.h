@@ -26,7 +26,7 @@ struct MRLevels {
   // Spatial decomposition: slabs of rows along the last
   // axis (y in 2D, z in 3D). A rank computes and decides for the rows it owns,
   // [own_lo, own_hi), and keeps up-to-date copies of the rows within
-  // kHalo of them, [reg_lo, reg_hi) (may wrap when that axis is periodic).
+  // the halo depth of them, [reg_lo, reg_hi) (may wrap when that axis is periodic).
   // Levels below `lp` are replicated (no leaves or absent cells there) and are
   // counted by rank 0 only (`count_rep`). One rank: everything owned.
   int own_lo[17], own_hi[17];
@@ -36,7 +36,6 @@ struct MRLevels {
   int dist;                // more than one rank
 };
 
-constexpr int kHalo = 2;  // rows of halo per level (stencil reach)
 
 // Slab row of cell c of level l (the last axis index).
 __host__ __device__ __forceinline__ int mr_row(int dim, int l, long c) {

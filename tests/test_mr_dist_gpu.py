@@ -41,6 +41,17 @@ CASES = [
 ]
 
 
+CASES_LT = [
+    (0, 21, 6, 16, 2, dict(local_time=True, min_leaf=0)),
+    (1, 22, 7, 16, 3, dict(local_time=True, min_leaf=0)),                      # cfg3 generator
+    (0, 23, 7, 12, 4, dict(local_time=True, min_leaf=0, gap=2, bc=[1] * 6)),   # periodic wrap
+    (0, 24, 7, 12, 4, dict(local_time=True, min_leaf=0, gap=4, limiter=0)),    # wider buffers
+    (2, 25, 5, 8, 2, dict(local_time=True, min_leaf=0)),                       # 3D
+    (3, 26, 5, 8, 3, dict(local_time=True, min_leaf=1, eps_level=eps_levels(1e-3, 5, 3))),
+]
+CASES = CASES + CASES_LT
+
+
 @pytest.mark.parametrize("kind,seed,level,steps,ranks,kw", CASES,
                          ids=[f"k{c[0]}_L{c[2]}_R{c[4]}_{i}" for i, c in enumerate(CASES)])
 def test_mr_ranks_equal_single(gpu_lib, kind, seed, level, steps, ranks, kw):
