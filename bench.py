@@ -266,6 +266,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mr-multi", default="auto", choices=["auto", "slabs", "replicas"],
+                    help="MR at N>1: slab decomposition or independent replicas "
+                         "(auto: replicas for the single-GPU cfg2, slabs otherwise)")
     ap.add_argument("--cpu-threads", type=int, default=0,
                     help="host threads for the CPU legs (0 = every core this process may use)")
     ap.add_argument("--ref-level", type=int, default=None)
@@ -306,7 +309,7 @@ def main():
         comm = h
 
     if args.workload in MR_OPTS:
-        line = mr_bench(args, rank, world, local, torch, dist)
+        line = mr_bench(args, rank, world, local, comm, torch, dist)
     else:
         line = uniform_bench(args, rank, world, local, comm, torch, dist)
     if rank == 0 and line is not None:
@@ -431,18 +434,40 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
 
 
 
-def mr_bench(args, rank, world, local, torch, dist):
+def mr_partition_level(o, level, world):
+    """The partition level af_mr_create_dist picks (MR::MR): smallest l with
+    2^l >= 4N, capped at the minimum leaf level."""
+    ml = max(o["min_leaf"], max(0, level - o["gap"])) if o["local_time"] else o["min_leaf"]
+    lp = 0
+    while (1 << lp) < 4 * world and lp < ml:
+        lp += 1
+    return lp
+
+
+def mr_decomposed(args, world):
+    """MR at N > 1: the slab decomposition of SURVEY §8(e) (one tree, strong
+    scaling) for the multi-GPU MR configs (cfg3); cfg2 is a single-GPU config
+    in BASELINE.json, so its N > 1 lines run independent replicas (weak)."""
+    if world == 1:
+        return False
+    if args.mr_multi == "auto":
+        return args.workload != "cfg2"
+    return args.mr_multi == "slabs"
+
+
+def mr_bench(args, rank, world, local, comm, torch, dist):
     """MR / MRLT workloads (cfg2, cfg3). A step = one macro cycle of run_mr
     (refine, virtual leaves, evolve, coarsen); value = leaf-cell RK-stage
-    updates actually performed / s. Multi-GPU: independent replicas (the MR
-    domain decomposition of SURVEY §8(e) is not built yet) -> weak scaling."""
+    updates actually performed / s (whole job)."""
     from paper_1603_05211_b200 import mr as M
     from paper_1603_05211_b200 import uniform as U
     idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
     o, epsl = mr_options(args.workload)
     opts = M.MROptions(epsilon=o["eps"], eps_level=epsl, min_leaf_level=o["min_leaf"],
                        local_time=o["local_time"], local_time_level_gap=o["gap"])
-    solver = M.MRSolver(dim, level, opts, scheme=U.SchemeConfig(limiter=U.MINMOD), device=local)
+    slabs = mr_decomposed(args, world)
+    solver = M.MRSolver(dim, level, opts, scheme=U.SchemeConfig(limiter=U.MINMOD), device=local,
+                        comm=comm if slabs else None)
     stream = torch.cuda.Stream(device=local)
     solver.set_stream(stream)
     init_host = U.case_fill(case, seed, level)
@@ -481,7 +506,9 @@ def mr_bench(args, rank, world, local, torch, dist):
     launches = solver.kernel_launches() - l0
     stage_ms, stage_launches, stage_updates = solver.stage_stats()
     solver.profile(False)
-    updates = reduce(float(rep.updates), dist.ReduceOp.SUM if world > 1 else None)
+    # with slabs the cycle records are already global; replicas add up
+    updates = rep.updates if slabs else reduce(float(rep.updates),
+                                               dist.ReduceOp.SUM if world > 1 else None)
     value = updates / (ms / 1e3)
 
     # ---- end to end: pinned host input -> build -> K cycles -> to_uniform ----
@@ -497,7 +524,8 @@ def mr_bench(args, rank, world, local, torch, dist):
         t1.record(stream)
         barrier()
         ems = reduce(t0.elapsed_time(t1), dist.ReduceOp.MAX if world > 1 else None)
-        upd2 = reduce(float(rep2.updates), dist.ReduceOp.SUM if world > 1 else None)
+        upd2 = rep2.updates if slabs else reduce(float(rep2.updates),
+                                                 dist.ReduceOp.SUM if world > 1 else None)
         nbytes = init_host.nbytes
         e2e = {"value": upd2 / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(nbytes * world / args.steps),
@@ -540,11 +568,15 @@ def mr_bench(args, rank, world, local, torch, dist):
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+        "higher_is_better": True, "scaling": "strong" if (slabs or world == 1) else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(workload_config(args.workload, world),
                        leaves_last_cycle=int(rep.cycles[-1, 0]) if len(rep.cycles) else None,
-                       replicas=world),
+                       decomposition=(f"{world} slabs of rows along the last axis from level "
+                                      f"{mr_partition_level(o, level, world)} up, halo "
+                                      "exchange over NCCL" if slabs else
+                                      ("single GPU (per-level dense grids)" if world == 1 else
+                                       f"{world} independent replicas"))),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,
     }

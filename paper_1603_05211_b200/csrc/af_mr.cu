@@ -564,12 +564,10 @@ bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult, int cap) cons
 void MR::build(const double* aos) {
   if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
   const long cells = mr_cells(D_, L_);
-  double* stage = nullptr;
-  AF_CUDA(cudaMalloc(&stage, sizeof(double) * 5 * cells));
+  // staged through the stage-output buffer (NC * total_cells >= 5 * cells of L)
+  double* stage = d_Vs_;
   AF_CUDA(cudaMemcpyAsync(stage, aos, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
-  AF_MR_LAUNCH(mr_upload_finest, grid_for(cells), stage, d_V_, g_);
-  AF_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(stage);
+  AF_MR_LAUNCH(mr_upload_finest, grid_for(cells), (const double*)stage, d_V_, g_);
   // from_uniform (mr_tree.cpp:29-71): leaves at L, internals above.
   AF_CUDA(cudaMemsetAsync(d_st_, ST_INTERNAL, g_.cell_off[L_], stream_));
   AF_CUDA(cudaMemsetAsync(d_st_ + g_.cell_off[L_], ST_LEAF, cells, stream_));
@@ -1621,12 +1619,10 @@ long MR::leaf_keys(uint64_t* keys, long cap) {
 void MR::to_uniform(int level, double* aos) {
   if (level < 0 || level > L_) throw Error(AF_E_LEVEL_MISMATCH, "to_uniform: bad level");
   const long cells = mr_cells(D_, level);
-  double* tmp = nullptr;
-  AF_CUDA(cudaMalloc(&tmp, sizeof(double) * 5 * cells));
-  AF_MR_LAUNCH(mr_download_level, grid_for(cells), d_V_, tmp, g_, level);
+  double* tmp = d_Vs_;  // scratch outside a stage; NC * total_cells >= 5 * cells
+  AF_MR_LAUNCH(mr_download_level, grid_for(cells), (const double*)d_V_, tmp, g_, level);
   AF_CUDA(cudaMemcpyAsync(aos, tmp, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(tmp);
 }
 
 void MR::details(int level, double* out) {
