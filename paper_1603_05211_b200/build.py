@@ -25,7 +25,6 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xcompiler", "-fno-fast-math",
-    "-shared",
 ]
 
 
@@ -63,13 +62,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
     nccl_inc, nccl_lib = _nccl_dirs()
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", CSRC, "-I", os.path.join(ROOT, "include"),
-           "-I", nccl_inc, "-o", LIB + ".tmp", *srcs, "-L", nccl_lib, "-l:libnccl.so.2",
-           "-Xlinker", "-rpath", "-Xlinker", nccl_lib]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc]
+    # one nvcc per translation unit, in parallel, then one link
+    procs, objs = [], []
+    for src in srcs:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), *inc, "-c", src,
+               "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((src, subprocess.Popen(cmd)))
+    bad = [src for src, p in procs if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, "nvcc " + " ".join(bad))
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+            "-Xcompiler", "-fPIC", "-o", LIB + ".tmp", *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+            "-Xlinker", "-rpath", "-Xlinker", nccl_lib]
+    subprocess.run(link, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -193,8 +193,10 @@ constexpr int kTX3 = 8, kTY3 = 8, kTZ3 = 4;
 MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o) {
   if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
   if (c.level < 2 || c.level > 15) throw Error(AF_E_CONFIG, "level must be in [2, 15]");
-  if (c.flux != AF_FLUX_AUSM_PLUS || c.integrator != AF_INTEGRATOR_RK2)
-    throw Error(AF_E_UNSUPPORTED, "the MR device path implements AUSM+ with RK2");
+  if (c.flux != AF_FLUX_AUSM_PLUS && c.flux != AF_FLUX_AUSMDV)
+    throw Error(AF_E_CONFIG, "unknown flux");
+  if (c.integrator != AF_INTEGRATOR_RK2)  // MRSolver::stage is RK2 (mr_solver.cpp:284-316)
+    throw Error(AF_E_UNSUPPORTED, "the MR path steps with RK2");
   if (c.limiter != AF_LIMITER_MINMOD && c.limiter != AF_LIMITER_VAN_ALBADA)
     throw Error(AF_E_CONFIG, "unknown limiter");
   for (int f = 0; f < 6; ++f)
@@ -336,7 +338,9 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   last_.step = -1;
   if (D_ == 3) {
     for (auto fn : {(const void*)mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>,
-                    (const void*)mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>})
+                    (const void*)mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>,
+                    (const void*)mr_stage_kernel<3, 2, kTX3, kTY3, kTZ3>,
+                    (const void*)mr_stage_kernel<3, 3, kTX3, kTY3, kTZ3>})
       AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes));
   }
@@ -819,22 +823,26 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     a.tiles = d_tiles_;
     a.ntiles = (std::min(hi, L_) << 1) | 1;
     const int lcode = -(std::max(lo, 0) + 1);
-    const int lim = cfg_.limiter;
-    if (D_ == 2) {
-      const size_t sm = MRTile<2, kTX2, kTY2, 1>::smem_bytes;
-      if (lim)
-        launch_k(pdl_, stream_, mr_stage_kernel<2, 1, kTX2, kTY2, 1>, grid, kTX2 * kTY2, sm, a, g_, lcode);
-      else
-        launch_k(pdl_, stream_, mr_stage_kernel<2, 0, kTX2, kTY2, 1>, grid, kTX2 * kTY2, sm, a, g_, lcode);
-    } else {
-      const size_t sm = MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes;
-      if (lim)
-        launch_k(pdl_, stream_, mr_stage_kernel<3, 1, kTX3, kTY3, kTZ3>, grid,
-                 kTX3 * kTY3 * kTZ3, sm, a, g_, lcode);
-      else
-        launch_k(pdl_, stream_, mr_stage_kernel<3, 0, kTX3, kTY3, kTZ3>, grid,
-                 kTX3 * kTY3 * kTZ3, sm, a, g_, lcode);
+    const int sch = cfg_.limiter | (cfg_.flux << 1);  // scheme code (af_physics.cuh)
+    const unsigned b2 = kTX2 * kTY2, b3 = kTX3 * kTY3 * kTZ3;
+    const size_t sm2 = MRTile<2, kTX2, kTY2, 1>::smem_bytes;
+    const size_t sm3 = MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes;
+#define AF_ST(S)                                                                           \
+  do {                                                                                     \
+    if (D_ == 2)                                                                           \
+      launch_k(pdl_, stream_, mr_stage_kernel<2, S, kTX2, kTY2, 1>, grid, b2, sm2, a, g_,   \
+               lcode);                                                                     \
+    else                                                                                   \
+      launch_k(pdl_, stream_, mr_stage_kernel<3, S, kTX3, kTY3, kTZ3>, grid, b3, sm3, a, g_, \
+               lcode);                                                                     \
+  } while (0)
+    switch (sch) {
+      case 0: AF_ST(0); break;
+      case 1: AF_ST(1); break;
+      case 2: AF_ST(2); break;
+      default: AF_ST(3); break;
     }
+#undef AF_ST
     ++launches_;
     AF_CUDA(cudaGetLastError());
   }

@@ -98,7 +98,7 @@ __device__ __forceinline__ Cons<D> flux4(const Cons<D>& qa, const Cons<D>& qb, c
                                          const Cons<D>& qd, double gamma, double gm1, int* fb) {
   const Prim<D> wa = primitives(qa, gm1), wb = primitives(qb, gm1);
   const Prim<D> wc = primitives(qc, gm1), wd = primitives(qd, gm1);
-  return face_flux<D, AX, LIM>(qb.E, qc.E, wa, wb, wc, wd, gamma, gm1, fb);
+  return face_flux<D, AX, LIM>(qb, qc, wa, wb, wc, wd, gamma, gm1, fb);
 }
 
 // fine_face_average (mr_solver.cpp:59-95) of leaf (c0,c1,c2) at level l.
@@ -248,8 +248,8 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     if (x < 0 || x >= TX || y < 0 || y >= TY || z < 0 || z >= TZ) return false;
     return leaf[(z * TY + y) * TX + x] != 0;
   };
-  auto energy_at = [&](int x, int y, int z) {
-    return resolve_at<D>(a.eval, comp, g, l, x, y, z, &a).E;
+  auto cons_at = [&](int x, int y, int z) {
+    return resolve_at<D>(a.eval, comp, g, l, x, y, z, &a);
   };
   // Face fluxes needed by a leaf of the tile.
   constexpr int UX = (K::NXF + 31) / 32, UY = (K::NYF + 31) / 32, UZ = (K::NZF + 31) / 32;
@@ -267,11 +267,11 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
           Cons<D> F;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
             fb = 1;
-            F = ausm_plus<D, 0>(energy_at(x0 + fx - 1, y0 + fy, z0 + fz), w0,
-                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+            F = num_flux<D, 0, LIM>(cons_at(x0 + fx - 1, y0 + fy, z0 + fz), w0,
+                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
           } else {
             const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = ausm_plus<D, 0>(ql.E, lft, qr.E, rgt, gamma);
+            F = num_flux<D, 0, LIM>(ql, lft, qr, rgt, gamma);
           }
           fl[f] = F.rho;
 #pragma unroll
@@ -292,11 +292,11 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
           Cons<D> F;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
             fb = 1;
-            F = ausm_plus<D, 1>(energy_at(x0 + fx, y0 + fy - 1, z0 + fz), w0,
-                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+            F = num_flux<D, 1, LIM>(cons_at(x0 + fx, y0 + fy - 1, z0 + fz), w0,
+                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
           } else {
             const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = ausm_plus<D, 1>(ql.E, lft, qr.E, rgt, gamma);
+            F = num_flux<D, 1, LIM>(ql, lft, qr, rgt, gamma);
           }
           const int g2 = K::NXF + f;
           fl[g2] = F.rho;
@@ -318,11 +318,11 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
           Cons<D> F;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
             fb = 1;
-            F = ausm_plus<D, 2>(energy_at(x0 + fx, y0 + fy, z0 + fz - 1), w0,
-                                energy_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+            F = num_flux<D, 2, LIM>(cons_at(x0 + fx, y0 + fy, z0 + fz - 1), w0,
+                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
           } else {
             const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = ausm_plus<D, 2>(ql.E, lft, qr.E, rgt, gamma);
+            F = num_flux<D, 2, LIM>(ql, lft, qr, rgt, gamma);
           }
           const int g3 = K::NXF + K::NYF + f;
           fl[g3] = F.rho;

@@ -82,8 +82,8 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
   if (c.level < 3 || c.level > 15)
     throw Error(AF_E_CONFIG, "level must be in [3, 15] (>= 8 cells per axis)");
-  if (c.flux != AF_FLUX_AUSM_PLUS)
-    throw Error(AF_E_UNSUPPORTED, "only the AUSM+ flux is on the device hot path");
+  if (c.flux != AF_FLUX_AUSM_PLUS && c.flux != AF_FLUX_AUSMDV)
+    throw Error(AF_E_CONFIG, "unknown flux");
   if (c.integrator != AF_INTEGRATOR_RK2)
     throw Error(AF_E_UNSUPPORTED, "only the RK2 integrator is on the device hot path");
   if (c.limiter != AF_LIMITER_MINMOD && c.limiter != AF_LIMITER_VAN_ALBADA)
@@ -125,8 +125,11 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   last_.step = -1;
   const size_t sm3 = Fv3d<1, 32, kTY>::smem_bytes;
   for (auto fn : {(const void*)fv3d_stage<0, 32, kTY>, (const void*)fv3d_stage<1, 32, kTY>,
+                  (const void*)fv3d_stage<2, 32, kTY>, (const void*)fv3d_stage<3, 32, kTY>,
                   (const void*)fv3d_stage<0, 16, kTY>, (const void*)fv3d_stage<1, 16, kTY>,
-                  (const void*)fv3d_stage<0, 8, kTY>, (const void*)fv3d_stage<1, 8, kTY>})
+                  (const void*)fv3d_stage<2, 16, kTY>, (const void*)fv3d_stage<3, 16, kTY>,
+                  (const void*)fv3d_stage<0, 8, kTY>, (const void*)fv3d_stage<1, 8, kTY>,
+                  (const void*)fv3d_stage<2, 8, kTY>, (const void*)fv3d_stage<3, 8, kTY>})
     AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
 }
 
@@ -240,10 +243,19 @@ void Uniform::exchange_halos_(double* q) {
   ck(ncclGroupEnd());
 }
 
+// dispatch on the scheme code sch = limiter | flux << 1
+#define AF_SCHEME(M, TX) \
+  switch (sch) {         \
+    case 0: M(0, TX); break; \
+    case 1: M(1, TX); break; \
+    case 2: M(2, TX); break; \
+    default: M(3, TX); break; \
+  }
+
 void Uniform::launch_stage_(const StageArgs& a) {
   const int n = g_.n;
   const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
-  const int lim = cfg_.limiter;
+  const int sch = cfg_.limiter | (cfg_.flux << 1);  // scheme code (af_physics.cuh)
   if (g_.dim == 3) {
     const long tiles = (long)(n / tx) * (n / kTY);
     const long target = 148L * 2 * 8;
@@ -255,11 +267,11 @@ void Uniform::launch_stage_(const StageArgs& a) {
 #define AF_L3(L, TX)                                                                     \
   fv3d_stage<L, TX, kTY><<<grid, TX * kTY, Fv3d<L, TX, kTY>::smem_bytes, stream_>>>(b, g_)
     if (tx == 32) {
-      if (lim) AF_L3(1, 32); else AF_L3(0, 32);
+      AF_SCHEME(AF_L3, 32);
     } else if (tx == 16) {
-      if (lim) AF_L3(1, 16); else AF_L3(0, 16);
+      AF_SCHEME(AF_L3, 16);
     } else {
-      if (lim) AF_L3(1, 8); else AF_L3(0, 8);
+      AF_SCHEME(AF_L3, 8);
     }
 #undef AF_L3
   } else {
@@ -267,11 +279,11 @@ void Uniform::launch_stage_(const StageArgs& a) {
 #define AF_L2(L, TX) \
   fv2d_stage<L, TX, kTY><<<tiles, TX * kTY, Fv2d<L, TX, kTY>::smem_bytes, stream_>>>(a, g_)
     if (tx == 32) {
-      if (lim) AF_L2(1, 32); else AF_L2(0, 32);
+      AF_SCHEME(AF_L2, 32);
     } else if (tx == 16) {
-      if (lim) AF_L2(1, 16); else AF_L2(0, 16);
+      AF_SCHEME(AF_L2, 16);
     } else {
-      if (lim) AF_L2(1, 8); else AF_L2(0, 8);
+      AF_SCHEME(AF_L2, 8);
     }
 #undef AF_L2
   }

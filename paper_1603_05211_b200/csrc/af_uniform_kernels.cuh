@@ -234,14 +234,22 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     w.p = s[4 * K::HP + idx];
     return w;
   };
-  // Total energy of global cell (x,y,z) of eval: only read on the rare
-  // first-order fallback (scheme.cpp:160-162).
-  auto energy_at = [&](int gx, int gy, int gz) {
-    bool f;
-    const int mx = bc_map(gx, n, g.bc[0], g.bc[1], f);
-    const int my = bc_map(gy, n, g.bc[2], g.bc[3], f);
-    const int zl = slab_map(gz, g, 2, f);
-    return ev[4 * cs + (long)zl * zs + (long)my * n + mx];
+  // Conserved state of global cell (x,y,z) of eval (a reflective ghost with
+  // its momentum flipped, grid.cpp:19-53): only read on the rare first-order
+  // fallback (scheme.cpp:160-162).
+  auto cons_at = [&](int gx, int gy, int gz) {
+    bool fx, fy, fz;
+    const int mx = bc_map(gx, n, g.bc[0], g.bc[1], fx);
+    const int my = bc_map(gy, n, g.bc[2], g.bc[3], fy);
+    const int zl = slab_map(gz, g, 2, fz);
+    const long c = (long)zl * zs + (long)my * n + mx;
+    Cons<D> q;
+    q.rho = ev[c];
+    q.m[0] = fx ? -ev[cs + c] : ev[cs + c];
+    q.m[1] = fy ? -ev[2 * cs + c] : ev[2 * cs + c];
+    q.m[2] = fz ? -ev[3 * cs + c] : ev[3 * cs + c];
+    q.E = ev[4 * cs + c];
+    return q;
   };
   int nfb = 0;
   // z face between planes gz-1 and gz of this thread's column.
@@ -252,11 +260,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     Prim<D> l, r;
     if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
       ++nfb;
-      return ausm_plus<D, 2>(energy_at(x0 + tx, y0 + ty, gz - 1), w0,
-                             energy_at(x0 + tx, y0 + ty, gz), wp1, gamma);
+      return num_flux<D, 2, LIM>(cons_at(x0 + tx, y0 + ty, gz - 1), w0,
+                             cons_at(x0 + tx, y0 + ty, gz), wp1, gamma);
     }
     const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-    return ausm_plus<D, 2>(ql.E, l, qr.E, r, gamma);
+    return num_flux<D, 2, LIM>(ql, l, qr, r, gamma);
   };
 
   // Prologue: planes zc0-2 .. zc0+1 and the chunk's first low z face; the
@@ -291,11 +299,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
           Cons<D> fl;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
             ++nfb;
-            fl = ausm_plus<D, 0>(energy_at(x0 + fxi - 1, y0 + fyi, k), w0,
-                                 energy_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
+            fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi, k), w0,
+                                 cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
             const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-            fl = ausm_plus<D, 0>(ql.E, l, qr.E, r, gamma);
+            fl = num_flux<D, 0, LIM>(ql, l, qr, r, gamma);
           }
           fxs[0 * K::NXF + f] = fl.rho;
           fxs[1 * K::NXF + f] = fl.m[0];
@@ -314,11 +322,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
           Cons<D> fl;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
             ++nfb;
-            fl = ausm_plus<D, 1>(energy_at(x0 + fxi, y0 + fyi - 1, k), w0,
-                                 energy_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
+            fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1, k), w0,
+                                 cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
             const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-            fl = ausm_plus<D, 1>(ql.E, l, qr.E, r, gamma);
+            fl = num_flux<D, 1, LIM>(ql, l, qr, r, gamma);
           }
           fys[0 * K::NYF + f] = fl.rho;
           fys[1 * K::NYF + f] = fl.m[0];
@@ -460,11 +468,17 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
     w.p = pl[3 * K::HP + idx];
     return w;
   };
-  auto energy_at = [&](int gx, int gy) {
-    bool f;
-    const int mx = bc_map(gx, n, g.bc[0], g.bc[1], f);
-    const int yl = slab_map(gy, g, 1, f);
-    return ev[3 * cs + (long)yl * zs + mx];
+  auto cons_at = [&](int gx, int gy) {
+    bool fx, fy;
+    const int mx = bc_map(gx, n, g.bc[0], g.bc[1], fx);
+    const int yl = slab_map(gy, g, 1, fy);
+    const long c = (long)yl * zs + mx;
+    Cons<D> q;
+    q.rho = ev[c];
+    q.m[0] = fx ? -ev[cs + c] : ev[cs + c];
+    q.m[1] = fy ? -ev[2 * cs + c] : ev[2 * cs + c];
+    q.E = ev[3 * cs + c];
+    return q;
   };
   for (int u = warp; u < K::UX + K::UY; u += K::NW) {
     if (u < K::UX) {
@@ -478,11 +492,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
         Cons<D> fl;
         if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
           ++nfb;
-          fl = ausm_plus<D, 0>(energy_at(x0 + fxi - 1, y0 + fyi), w0,
-                               energy_at(x0 + fxi, y0 + fyi), wp1, gamma);
+          fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi), w0,
+                               cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
           const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-          fl = ausm_plus<D, 0>(ql.E, l, qr.E, r, gamma);
+          fl = num_flux<D, 0, LIM>(ql, l, qr, r, gamma);
         }
         fxs[f] = fl.rho;
         fxs[K::NXF + f] = fl.m[0];
@@ -500,11 +514,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
         Cons<D> fl;
         if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
           ++nfb;
-          fl = ausm_plus<D, 1>(energy_at(x0 + fxi, y0 + fyi - 1), w0,
-                               energy_at(x0 + fxi, y0 + fyi), wp1, gamma);
+          fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1), w0,
+                               cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
           const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-          fl = ausm_plus<D, 1>(ql.E, l, qr.E, r, gamma);
+          fl = num_flux<D, 1, LIM>(ql, l, qr, r, gamma);
         }
         fys[f] = fl.rho;
         fys[K::NYF + f] = fl.m[0];

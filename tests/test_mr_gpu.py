@@ -21,7 +21,7 @@ def eps_levels(eps, L, d):
 
 
 def gpu_mr(kind, seed, level, steps, cfl=0.5, fixed_dt=0.0, eps=1e-3, eps_level=None,
-           min_leaf=0, local_time=False, gap=3, limiter=1, bc=None):
+           min_leaf=0, local_time=False, gap=3, limiter=1, bc=None, flux=0):
     from paper_1603_05211_b200 import mr as M
     from paper_1603_05211_b200 import uniform as U
     dim = 3 if kind >= 2 else 2
@@ -29,7 +29,7 @@ def gpu_mr(kind, seed, level, steps, cfl=0.5, fixed_dt=0.0, eps=1e-3, eps_level=
     s = M.MRSolver(dim, level, M.MROptions(epsilon=eps, eps_level=eps_level,
                                            min_leaf_level=min_leaf, local_time=local_time,
                                            local_time_level_gap=gap),
-                   scheme=U.SchemeConfig(limiter=limiter), bc=bc)
+                   scheme=U.SchemeConfig(flux=flux, limiter=limiter), bc=bc)
     s.build(init)
     rep = s.run(steps, cfl=cfl, fixed_dt=fixed_dt)
     out = s.to_uniform()
@@ -39,11 +39,11 @@ def gpu_mr(kind, seed, level, steps, cfl=0.5, fixed_dt=0.0, eps=1e-3, eps_level=
 
 
 def ref_mr(oracle, init, kind, level, steps, cfl=0.5, fixed_dt=0.0, eps=1e-3, eps_level=None,
-           min_leaf=0, local_time=False, gap=3, limiter=1, bc=None):
+           min_leaf=0, local_time=False, gap=3, limiter=1, bc=None, flux=0):
     dim = 3 if kind >= 2 else 2
     p = oracle.make_params(dim, level, steps, cfl=cfl, fixed_dt=fixed_dt, limiter=limiter,
                            bc=bc, eps=eps, eps_level=eps_level, min_leaf_level=min_leaf,
-                           local_time=local_time, lt_gap=gap)
+                           local_time=local_time, lt_gap=gap, flux=flux)
     return oracle.mr_run("ref", p, init)
 
 
@@ -72,6 +72,8 @@ CASES_GLOBAL = [
     (0, 6, 6, 15, dict(eps=1e-3, bc=[2, 2, 0, 0, 0, 0])),
     (2, 7, 4, 6, dict(eps=1e-3, cfl=0.4)),
     (3, 8, 5, 4, dict(eps=1e-3, cfl=0.4, eps_level=eps_levels(1e-3, 5, 3), min_leaf=2)),
+    (0, 31, 7, 20, dict(eps=1e-3, flux=1, min_leaf=3)),                        # AUSMDV
+    (3, 32, 5, 4, dict(eps=1e-3, cfl=0.4, flux=1, limiter=0)),
 ]
 
 
@@ -92,6 +94,7 @@ CASES_LT = [
     (2, 43, 5, 8, dict(eps=1e-3, cfl=0.4, local_time=True)),
     (3, 46, 5, 8, dict(eps=1e-3, cfl=0.4, local_time=True, gap=3,
                        eps_level=eps_levels(1e-3, 5, 3), min_leaf=1)),        # cfg5 rule
+    (1, 47, 7, 12, dict(eps=1e-3, local_time=True, flux=1)),                 # AUSMDV, MRLT
 ]
 
 
