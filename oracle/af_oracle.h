@@ -28,7 +28,7 @@ typedef struct af_oracle_params {
   int level;     /* finest level L, n = 2^L cells per axis */
   int bc[6];     /* per face 2*axis+side: 0 outflow, 1 periodic, 2 reflective (grid.hpp:70) */
   int limiter;   /* 0 van Albada, 1 minmod (scheme.hpp:20) */
-  int flux;      /* 0 AUSM+ (1 AUSMDV: not on the hot path) */
+  int flux;      /* 0 AUSM+, 1 AUSMDV (scheme.hpp:16) */
   double gamma;  /* 1.4 */
   long n_steps;  /* finest-level steps */
   double cfl;    /* > 0: dt = cfl*dx_L / max_leaf sum_a(|v_a|+c) per (macro) step */
@@ -40,6 +40,7 @@ typedef struct af_oracle_params {
   int min_leaf_level;       /* MRTree::set_min_leaf_level (mr_tree.hpp:78) */
   int local_time;           /* 1: MRLT (mr_solver.cpp:325-363) */
   int lt_gap;               /* MROptions::local_time_level_gap (mr_solver.hpp:70) */
+  int integrator;           /* 0 RK2, 1 MUSCL-Hancock (scheme.hpp:18); uniform only */
 } af_oracle_params;
 
 typedef struct af_oracle_result {

@@ -30,6 +30,7 @@ class Params(C.Structure):
         ("flux", C.c_int), ("gamma", C.c_double), ("n_steps", C.c_long), ("cfl", C.c_double),
         ("fixed_dt", C.c_double), ("eps", C.c_double), ("eps_level", C.POINTER(C.c_double)),
         ("min_leaf_level", C.c_int), ("local_time", C.c_int), ("lt_gap", C.c_int),
+        ("integrator", C.c_int),
     ]
 
 
@@ -107,12 +108,13 @@ def case_fill(kind: int, seed: int, level: int, gamma: float = 1.4, z0: int = 0,
 
 def make_params(dim, level, n_steps, cfl=0.5, fixed_dt=0.0, limiter=MINMOD, bc=None,
                 gamma=1.4, eps=0.0, eps_level=None, min_leaf_level=0, local_time=False,
-                lt_gap=3, flux=0):
+                lt_gap=3, flux=0, integrator=0):
     p = Params()
     p.dim, p.level, p.n_steps = dim, level, n_steps
     for f in range(6):
         p.bc[f] = OUTFLOW if bc is None else bc[f]
     p.limiter, p.flux, p.gamma = limiter, flux, gamma
+    p.integrator = integrator
     p.cfl, p.fixed_dt = cfl, fixed_dt
     p.eps = eps
     keep = None

@@ -20,7 +20,7 @@ LIB = os.path.join(LIBDIR, "libafgpu.so")
 SOURCES = ["af_abi.cu", "af_uniform.cu", "af_mr.cu", "af_mr_dist.cu"]
 HEADERS = ["af_physics.cuh", "af_uniform_kernels.cuh", "af_internal.h", "af_uniform.h",
            "af_comm.h", "af_mr.h", "af_mr_kernels.cuh", "af_mr_types.h",
-           "af_mr_stage.cuh"]
+           "af_mr_stage.cuh", "af_hancock.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",

@@ -16,6 +16,7 @@
 
 #include "af_comm.h"
 #include "af_uniform.h"
+#include "af_hancock.cuh"
 #include "af_uniform_kernels.cuh"
 
 namespace af {
@@ -84,8 +85,8 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
     throw Error(AF_E_CONFIG, "level must be in [3, 15] (>= 8 cells per axis)");
   if (c.flux != AF_FLUX_AUSM_PLUS && c.flux != AF_FLUX_AUSMDV)
     throw Error(AF_E_CONFIG, "unknown flux");
-  if (c.integrator != AF_INTEGRATOR_RK2)
-    throw Error(AF_E_UNSUPPORTED, "only the RK2 integrator is on the device hot path");
+  if (c.integrator != AF_INTEGRATOR_RK2 && c.integrator != AF_INTEGRATOR_MUSCL_HANCOCK)
+    throw Error(AF_E_CONFIG, "unknown integrator");
   if (c.limiter != AF_LIMITER_MINMOD && c.limiter != AF_LIMITER_VAN_ALBADA)
     throw Error(AF_E_CONFIG, "unknown limiter");
   for (int f = 0; f < 6; ++f)
@@ -131,6 +132,10 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
                   (const void*)fv3d_stage<0, 8, kTY>, (const void*)fv3d_stage<1, 8, kTY>,
                   (const void*)fv3d_stage<2, 8, kTY>, (const void*)fv3d_stage<3, 8, kTY>})
     AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+  const size_t smh = Hk<3, 8, 8, 4>::smem_bytes;
+  for (auto fn : {(const void*)hancock_step<3, 0, 8, 8, 4>, (const void*)hancock_step<3, 1, 8, 8, 4>,
+                  (const void*)hancock_step<3, 2, 8, 8, 4>, (const void*)hancock_step<3, 3, 8, 8, 4>})
+    AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
 }
 
 Uniform::~Uniform() {
@@ -252,6 +257,34 @@ void Uniform::exchange_halos_(double* q) {
     default: M(3, TX); break; \
   }
 
+// One MUSCL-Hancock step (af_hancock.cuh): eval -> out.
+void Uniform::launch_hancock_(const StageArgs& a) {
+  const int n = g_.n;
+  const int sch = cfg_.limiter | (cfg_.flux << 1);
+  if (g_.dim == 3) {
+    const unsigned tiles = (unsigned)((long)(n / 8) * (n / 8) * ((g_.nzl + 3) / 4));
+    const size_t sm = Hk<3, 8, 8, 4>::smem_bytes;
+#define AF_H3(S, TX) hancock_step<3, S, 8, 8, 4><<<tiles, 256, sm, stream_>>>(a, g_)
+    AF_SCHEME(AF_H3, 8);
+#undef AF_H3
+  } else {
+    const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
+    const unsigned tiles = (unsigned)((n / tx) * (g_.nzl / kTY));
+#define AF_H2(S, TX) \
+  hancock_step<2, S, TX, kTY, 1><<<tiles, TX * kTY, Hk<2, TX, kTY, 1>::smem_bytes, stream_>>>(a, g_)
+    if (tx == 32) {
+      AF_SCHEME(AF_H2, 32);
+    } else if (tx == 16) {
+      AF_SCHEME(AF_H2, 16);
+    } else {
+      AF_SCHEME(AF_H2, 8);
+    }
+#undef AF_H2
+  }
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+}
+
 void Uniform::launch_stage_(const StageArgs& a) {
   const int n = g_.n;
   const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
@@ -321,6 +354,25 @@ void Uniform::enqueue_steps_(long n_steps, double cfl, double fixed_dt) {
   if (a.use_cfl) {
     launch_speed_sum_(d_u_, rec_.smax);
     if (comm_ && comm_->n > 1) allreduce_max_(rec_.smax);
+  }
+  hk_u0_ = d_u_;
+  hk_m0_ = d_mid_;
+  if (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK) {
+    // muscl_hancock_step (step.cpp:148-235): one launch per step, u -> mid,
+    // then the buffers swap roles (the step-s input is hk_u0_ for even s)
+    for (long s = 0; s < n_steps; ++s) {
+      a.step = (int)s;
+      exchange_halos_(d_u_);
+      a.stage = 1;
+      a.dt_scale = 1.0;
+      a.eval = d_u_;
+      a.base = d_u_;
+      a.out = d_mid_;
+      launch_hancock_(a);
+      std::swap(d_u_, d_mid_);
+      if (a.use_cfl && comm_ && comm_->n > 1) allreduce_max_(rec_.smax + s + 1);
+    }
+    return;
   }
   for (long s = 0; s < n_steps; ++s) {
     a.step = (int)s;
@@ -410,7 +462,27 @@ void Uniform::run_group(const std::vector<Uniform*>& R, long n_steps, double cfl
     for (int r = 0; r < P; ++r) R[r]->launch_speed_sum_(R[r]->d_u_, R[r]->rec_.smax);
     group_max(0);
   }
-  for (long s = 0; s < n_steps; ++s) {
+  for (int r = 0; r < P; ++r) {
+    R[r]->hk_u0_ = R[r]->d_u_;
+    R[r]->hk_m0_ = R[r]->d_mid_;
+  }
+  const bool hancock = R[0]->cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK;
+  for (long s = 0; s < n_steps && hancock; ++s) {
+    exchange(0);
+    for (int r = 0; r < P; ++r) {
+      StageArgs& a = A[r];
+      a.step = (int)s;
+      a.stage = 1;
+      a.dt_scale = 1.0;
+      a.eval = R[r]->d_u_;
+      a.base = R[r]->d_u_;
+      a.out = R[r]->d_mid_;
+      R[r]->launch_hancock_(a);
+      std::swap(R[r]->d_u_, R[r]->d_mid_);
+    }
+    if (cfl > 0.0) group_max(s + 1);
+  }
+  for (long s = 0; s < n_steps && !hancock; ++s) {
     exchange(0);
     for (int r = 0; r < P; ++r) {
       StageArgs& a = A[r];
@@ -485,6 +557,7 @@ void Uniform::check_error_() {
   const long step = h[1] / 2;
   const int stage = h[1] % 2 + 1;
   const double* eval = stage == 1 ? d_u_ : d_mid_;
+  if (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK) eval = step % 2 ? hk_m0_ : hk_u0_;
   std::vector<double> hs(g_.total);
   AF_CUDA(cudaMemcpy(hs.data(), eval, sizeof(double) * g_.total, cudaMemcpyDeviceToHost));
   std::memset(&last_, 0, sizeof(last_));

@@ -44,6 +44,7 @@ class Uniform {
   void exchange_halos_(double* q);
   void allreduce_max_(unsigned long long* bits);
   void launch_stage_(const StageArgs& a);
+  void launch_hancock_(const StageArgs& a);
   void launch_speed_sum_(const double* q, unsigned long long* target);
   void enqueue_steps_(long n_steps, double cfl, double fixed_dt);
   void check_error_();
@@ -55,6 +56,8 @@ class Uniform {
   double dx_ = 0.0, inv_dx_ = 0.0;
   double* d_u_ = nullptr;
   double* d_mid_ = nullptr;
+  const double* hk_u0_ = nullptr;  // MUSCL-Hancock: the input buffer of even steps
+  const double* hk_m0_ = nullptr;  // ... and of odd steps
   double* d_stage_ = nullptr;
   size_t stage_bytes_ = 0;
   int* d_err_ = nullptr;

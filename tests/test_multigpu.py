@@ -17,19 +17,21 @@ from test_oracle import bits
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dim,level,ranks,bc,cfl,lim", [
-    (2, 6, 2, None, 0.5, 1),
-    (2, 7, 3, [1] * 6, 0.5, 1),
-    (2, 7, 4, [2, 2, 2, 2, 0, 0], 0.5, 0),
-    (3, 5, 2, None, 0.4, 1),
-    (3, 5, 4, [1] * 6, 0.4, 1),
-    (3, 5, 5, [0, 0, 2, 2, 1, 1], 0.4, 0),
+@pytest.mark.parametrize("dim,level,ranks,bc,cfl,lim,integ", [
+    (2, 6, 2, None, 0.5, 1, 0),
+    (2, 7, 3, [1] * 6, 0.5, 1, 0),
+    (2, 7, 4, [2, 2, 2, 2, 0, 0], 0.5, 0, 0),
+    (3, 5, 2, None, 0.4, 1, 0),
+    (3, 5, 4, [1] * 6, 0.4, 1, 0),
+    (3, 5, 5, [0, 0, 2, 2, 1, 1], 0.4, 0, 0),
+    (2, 7, 3, [1] * 6, 0.5, 1, 1),                 # MUSCL-Hancock
+    (3, 5, 3, [0, 0, 2, 2, 1, 1], 0.3, 0, 1),
 ])
-def test_group_equals_single(gpu_lib, dim, level, ranks, bc, cfl, lim):
+def test_group_equals_single(gpu_lib, dim, level, ranks, bc, cfl, lim, integ):
     from paper_1603_05211_b200 import uniform as U
     kind = 2 if dim == 3 else 0
     init = U.case_fill(kind, 77 + ranks, level)
-    sc = U.SchemeConfig(limiter=lim)
+    sc = U.SchemeConfig(limiter=lim, integrator=integ)
     single = U.UniformSolver(dim, level, scheme=sc, bc=bc)
     single.upload(init)
     r1 = single.run(8, cfl=cfl)

@@ -156,3 +156,47 @@ def test_gpu_ausmdv_matches_reference(gpu_lib, oracle, kind, seed, level, steps,
     assert np.array_equal(bits(rep.dt), bits(dts))
     assert np.array_equal(bits(out), bits(ref))
     assert rep.max_cfl == res["max_cfl"]
+
+
+HANCOCK = [
+    # kind, seed, level, steps, cfl, limiter, flux, bc
+    (0, 51, 7, 40, 0.5, 1, 0, None),
+    (1, 52, 6, 30, 0.5, 0, 1, [2, 2, 1, 1, 0, 0]),   # AUSMDV + van Albada: the AMR preset
+    (0, 53, 5, 20, 0.9, 1, 1, [1, 1, 1, 1, 0, 0]),
+    (2, 54, 5, 10, 0.4, 1, 0, None),
+    (3, 55, 5, 8, 0.4, 0, 1, [1, 1, 2, 2, 0, 0]),
+    (3, 56, 4, 12, 0.8, 1, 0, None),                  # strong ratio, large CFL: fallbacks
+]
+
+
+@pytest.mark.parametrize("kind,seed,level,steps,cfl,lim,flux,bc", HANCOCK,
+                         ids=[f"k{c[0]}_L{c[2]}_{i}" for i, c in enumerate(HANCOCK)])
+def test_gpu_hancock_matches_reference(gpu_lib, oracle, kind, seed, level, steps, cfl, lim, flux,
+                                       bc):
+    """muscl_hancock_step (step.cpp:148-235) against the compiled reference:
+    state, dt history, max_cfl and the fallback count, bit for bit."""
+    from paper_1603_05211_b200 import uniform as U
+    if not oracle.available("ref"):
+        pytest.skip("reference build not present")
+    dim = 3 if kind >= 2 else 2
+    init = U.case_fill(kind, seed, level)
+    sch = U.SchemeConfig(flux=flux, limiter=lim, integrator=U.MUSCL_HANCOCK)
+    s = U.UniformSolver(dim, level, scheme=sch, bc=bc)
+    s.upload(init)
+    p = oracle.make_params(dim, level, steps, cfl=cfl, limiter=lim, bc=bc, flux=flux,
+                           integrator=1)
+    ref, dts, res = oracle.uniform_run("ref", p, init)
+    if res["err_kind"]:
+        from paper_1603_05211_b200.errors import NonPhysicalState
+        with pytest.raises(NonPhysicalState) as e:
+            s.run(steps, cfl=cfl)
+        assert str(e.value) == res["err"]
+        return
+    rep = s.run(steps, cfl=cfl)
+    out = s.download()
+    s.close()
+    assert np.array_equal(bits(rep.dt), bits(dts))
+    assert np.array_equal(bits(out), bits(ref))
+    assert rep.max_cfl == res["max_cfl"]
+    assert rep.max_wave_speed == res["max_wave_speed"]
+    assert rep.fallbacks == res["fallbacks"]
