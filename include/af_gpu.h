@@ -48,7 +48,8 @@ typedef enum af_status {
   AF_E_NCCL = 6,              /* NCCL failure */
   AF_E_ARGUMENT = 7,          /* invalid argument / null pointer */
   AF_E_UNSUPPORTED = 8,       /* option outside the hot path (e.g. AUSMDV) */
-  AF_E_INTERNAL = 9           /* internal invariant check failed (debug switches) */
+  AF_E_INTERNAL = 9,          /* internal invariant check failed (debug switches) */
+  AF_E_IO = 10                /* adaptflow::IoError (errors.hpp:38-41) */
 } af_status;
 
 enum { AF_BC_OUTFLOW = 0, AF_BC_PERIODIC = 1, AF_BC_REFLECTIVE = 2 }; /* BcKind grid.hpp:70 */
@@ -244,6 +245,33 @@ af_status af_mr_profile(af_mr* m, int enable);
 af_status af_mr_stage_stats(af_mr* m, double* ms, long* launches, long* updates);
 af_status af_mr_last_error(const af_mr* m, af_error* err);
 af_status af_mr_kernel_launches(const af_mr* m, long* count);
+
+/* ------------------------------------------- formats and compare path -- */
+/* (SURVEY.md §8(f) "next" #2-3). Cell arrays use the ABI's AoS layout:
+ * 5 doubles per cell (rho, mom0, mom1, mom2, rhoE; mom2 = 0 in 2D), x fastest.
+ * Pointers may be host or device memory. */
+typedef struct af_snapshot_header {
+  int dim;
+  int level;
+  double gamma, time, origin, extent;
+} af_snapshot_header;
+/* write_snapshot (snapshot.cpp:29-59): AFSN v1, little endian. */
+af_status af_snapshot_write(const char* path, const af_snapshot_header* h, const double* aos);
+/* read_snapshot (snapshot.cpp:61-104). aos == NULL reads the header only;
+ * otherwise aos holds 2^(dim*level) cells. */
+af_status af_snapshot_read(const char* path, af_snapshot_header* h, double* aos);
+/* restrict_to_level (grid.cpp:64-93) on the device: fine (level fine_level)
+ * -> out (level target), bit-exact. */
+af_status af_restrict_to_level(int dim, int fine_level, int target, const double* fine,
+                               double* out);
+/* l1_error (metrics.cpp:134-148): per component sum |sol - restrict(ref)| *
+ * cell volume, on the device (summation order differs from the reference's
+ * sequential loop: agreement to round-off, not bitwise). */
+af_status af_l1_error(int dim, int level, double extent, const double* sol, int ref_level,
+                      const double* ref, double out[5]);
+/* MRTree::dump (mr_tree.cpp:623-641) of the device tree (this rank's nodes):
+ * *len in = capacity of buf, out = bytes needed including the terminating 0. */
+af_status af_mr_dump(af_mr* m, char* buf, size_t* len);
 
 #ifdef __cplusplus
 }

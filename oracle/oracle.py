@@ -80,6 +80,15 @@ def _load(kind: str):
         lib.afo_case_fill.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_int,
                                       C.c_int, dp]
         lib.afo_case_fill.restype = C.c_int
+    else:  # formats and compare path of the reference (ref_harness.cpp)
+        for name, args in [
+            ("snapshot_copy", [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]),
+            ("restrict", [C.c_int, C.c_int, C.c_int, dp, dp]),
+            ("l1_error", [C.c_int, C.c_int, C.c_double, dp, C.c_int, dp, dp]),
+        ]:
+            f = getattr(lib, "afref_" + name)
+            f.argtypes = args
+            f.restype = C.c_int
     _libs[kind] = lib
     return lib
 
@@ -157,3 +166,29 @@ def mr_run(kind: str, params: Params, init: np.ndarray, max_cycles: int | None =
         (lib.afref_mr_last_dump if kind == "ref" else lib.afo_mr_last_dump)(
             dump_path.encode())
     return out, keys[: nl.value].copy(), per_cycle[:nc].copy(), dts[:nc].copy(), r
+
+
+def ref_snapshot_copy(src: str, dst: str):
+    """The reference's read_snapshot(src) + write_snapshot(dst); returns the
+    IoError text or None."""
+    lib = _load("ref")
+    err = C.create_string_buffer(512)
+    rc = lib.afref_snapshot_copy(src.encode(), dst.encode(), err, 512)
+    return err.value.decode() if rc else None
+
+
+def ref_restrict(state: np.ndarray, dim: int, level: int, target: int) -> np.ndarray:
+    lib = _load("ref")
+    out = np.zeros(((1 << (dim * target)), 5), dtype=np.float64)
+    if lib.afref_restrict(dim, level, target, _dp(np.ascontiguousarray(state)), _dp(out)):
+        raise ValueError("restrict_to_level failed")
+    return out
+
+
+def ref_l1_error(sol, dim, level, ref, ref_level, extent=1.0) -> np.ndarray:
+    lib = _load("ref")
+    out = np.zeros(5, dtype=np.float64)
+    if lib.afref_l1_error(dim, level, extent, _dp(np.ascontiguousarray(sol)), ref_level,
+                          _dp(np.ascontiguousarray(ref)), _dp(out)):
+        raise ValueError("l1_error failed")
+    return out

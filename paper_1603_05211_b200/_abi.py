@@ -22,6 +22,7 @@ AF_E_NCCL = 6
 AF_E_ARGUMENT = 7
 AF_E_UNSUPPORTED = 8
 AF_E_INTERNAL = 9
+AF_E_IO = 10
 
 
 class Config(C.Structure):
@@ -55,6 +56,11 @@ class MROptions(C.Structure):
 class MRCycle(C.Structure):
     _fields_ = [("leaves", C.c_long), ("nodes", C.c_long), ("sub", C.c_long), ("top", C.c_int),
                 ("dt", C.c_double), ("updates", C.c_long)]
+
+
+class SnapshotHeader(C.Structure):
+    _fields_ = [("dim", C.c_int), ("level", C.c_int), ("gamma", C.c_double),
+                ("time", C.c_double), ("origin", C.c_double), ("extent", C.c_double)]
 
 
 # name -> (restype, argtypes); the complete exported surface of af_gpu.h
@@ -111,6 +117,11 @@ SIGNATURES = {
                                     C.POINTER(C.c_long)]),
     "af_mr_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
     "af_mr_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+    "af_snapshot_write": (C.c_int, [C.c_char_p, C.POINTER(SnapshotHeader), _vp]),
+    "af_snapshot_read": (C.c_int, [C.c_char_p, C.POINTER(SnapshotHeader), _vp]),
+    "af_restrict_to_level": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "af_l1_error": (C.c_int, [C.c_int, C.c_int, C.c_double, _vp, C.c_int, _vp, _dp]),
+    "af_mr_dump": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_size_t)]),
 }
 
 _lib = None

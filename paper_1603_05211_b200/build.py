@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libafgpu.so")
 
-SOURCES = ["af_abi.cu", "af_uniform.cu", "af_mr.cu", "af_mr_dist.cu"]
+SOURCES = ["af_abi.cu", "af_uniform.cu", "af_mr.cu", "af_mr_dist.cu", "af_io.cu"]
 HEADERS = ["af_physics.cuh", "af_uniform_kernels.cuh", "af_internal.h", "af_uniform.h",
            "af_comm.h", "af_mr.h", "af_mr_kernels.cuh", "af_mr_types.h",
            "af_mr_stage.cuh", "af_hancock.cuh"]

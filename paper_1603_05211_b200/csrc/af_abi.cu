@@ -348,3 +348,53 @@ af_status af_mr_kernel_launches(const af_mr* m, long* count) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------- formats and compare path --
+af_status af_snapshot_write(const char* path, const af_snapshot_header* h, const double* aos) {
+  return guard(nullptr, [&] {
+    if (!path || !h || !aos) throw af::Error(AF_E_ARGUMENT, "af_snapshot_write: null argument");
+    const long cells = h->dim == 3 ? 1L << (3 * h->level) : 1L << (2 * h->level);
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, aos) == cudaSuccess && at.type == cudaMemoryTypeDevice) {
+      std::vector<double> host(5 * (size_t)cells);  // device array: stage through the host
+      AF_CUDA(cudaMemcpy(host.data(), aos, host.size() * 8, cudaMemcpyDeviceToHost));
+      af::snapshot_write(path, *h, host.data());
+    } else {
+      cudaGetLastError();
+      af::snapshot_write(path, *h, aos);
+    }
+  });
+}
+
+af_status af_snapshot_read(const char* path, af_snapshot_header* h, double* aos) {
+  return guard(nullptr, [&] {
+    if (!path || !h) throw af::Error(AF_E_ARGUMENT, "af_snapshot_read: null argument");
+    af::snapshot_read(path, h, aos);
+  });
+}
+
+af_status af_restrict_to_level(int dim, int fine_level, int target, const double* fine,
+                               double* out) {
+  return guard(nullptr, [&] {
+    if (!fine || !out) throw af::Error(AF_E_ARGUMENT, "af_restrict_to_level: null argument");
+    af::restrict_to_level(dim, fine_level, target, fine, out);
+  });
+}
+
+af_status af_l1_error(int dim, int level, double extent, const double* sol, int ref_level,
+                      const double* ref, double out[5]) {
+  return guard(nullptr, [&] {
+    if (!sol || !ref || !out) throw af::Error(AF_E_ARGUMENT, "af_l1_error: null argument");
+    af::l1_error(dim, level, extent, sol, ref_level, ref, out);
+  });
+}
+
+af_status af_mr_dump(af_mr* m, char* buf, size_t* len) {
+  if (!m || !len) return AF_E_ARGUMENT;
+  AF_M_GUARD({
+    const std::string s = m->impl->dump();
+    const size_t need = s.size() + 1;
+    if (buf && *len >= need) std::memcpy(buf, s.c_str(), need);
+    *len = need;
+  });
+}

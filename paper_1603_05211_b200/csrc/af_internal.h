@@ -20,6 +20,13 @@ struct Error : std::runtime_error {
   Error(af_status s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 
+// formats and compare path (af_io.cu)
+void snapshot_write(const char* path, const af_snapshot_header& h, const double* aos);
+void snapshot_read(const char* path, af_snapshot_header* h, double* aos);
+void restrict_to_level(int dim, int fine_level, int target, const double* fine, double* out);
+void l1_error(int dim, int level, double extent, const double* sol, int ref_level,
+              const double* ref, double* out5);
+
 #define AF_CUDA(call)                                                                   \
   do {                                                                                  \
     cudaError_t e_ = (call);                                                            \

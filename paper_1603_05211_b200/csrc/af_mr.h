@@ -1,6 +1,7 @@
 // af_mr.h — host class behind af_mr_* (see af_mr.cu).
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "af_comm.h"
@@ -24,6 +25,7 @@ class MR {
   // the spatial decomposition.
   MR(const af_config& cfg, const af_mr_options& opt, Comm* comm = nullptr);
   void local_rows(int level, int* lo, int* hi) const;  // slab rows this rank owns
+  std::string dump();  // MRTree::dump text (af_io.cu)
   ~MR();
   MR(const MR&) = delete;
   MR& operator=(const MR&) = delete;

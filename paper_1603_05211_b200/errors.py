@@ -27,12 +27,16 @@ class DeviceError(Error):
 
 
 class UnsupportedOption(ConfigError):
-    """Scheme option outside the device hot path (e.g. AUSMDV, MUSCL-Hancock)."""
+    """Option outside the device path (e.g. MUSCL-Hancock in the MR solver)."""
+
+
+class IoError(Error):
+    """adaptflow::IoError (errors.hpp:38-41)"""
 
 
 _BY_STATUS = {1: NonPhysicalState, 2: RegisterMismatch, 3: ConfigError, 4: LevelMismatch,
               5: DeviceError, 6: DeviceError, 7: ValueError, 8: UnsupportedOption,
-              9: DeviceError}
+              9: DeviceError, 10: IoError}
 
 
 def raise_status(status: int, message: str) -> None:

@@ -185,6 +185,14 @@ class MRSolver:
         self._check(self._lib.af_mr_local_rows(self._h, level, C.byref(lo), C.byref(hi)))
         return lo.value, hi.value
 
+    def dump(self) -> str:
+        """MRTree::dump (mr_tree.cpp:623-641) of the device tree."""
+        n = C.c_size_t(0)
+        self._check(self._lib.af_mr_dump(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        self._check(self._lib.af_mr_dump(self._h, buf, C.byref(n)))
+        return buf.value.decode()
+
     def details(self, level: int) -> np.ndarray:
         n = 1 << level
         out = np.empty(n ** self.dim, dtype=np.float64)

@@ -31,3 +31,10 @@ def gpu_lib():
         pytest.fail("GPU test selected but no CUDA device is visible")
     import paper_1603_05211_b200 as P
     return P.load_library()
+
+
+@pytest.fixture(scope="session")
+def gpu_lib_cpu():
+    """libafgpu.so for its host-only entry points (the AFSN format); no GPU needed."""
+    import paper_1603_05211_b200 as P
+    return P.load_library()
