@@ -1356,7 +1356,9 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
     AF_CUDA(cudaGetLastError());
   });
   *sweep_body = launches_ - b0;
-  build_lists_enqueue_();
+  // no list rebuild here: the next refine works on this cycle's post-refine
+  // lists, a superset of the coarsened tree's band (every node it holds
+  // existed then), and rebuilds them after its splits
 }
 
 MR::CycleGraph& MR::cycle_graph_(double cfl, double fixed_dt) {

@@ -222,6 +222,25 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       pr[m * K::HP + idx] = m == 0 ? w.rho : (m == NC - 1 ? w.p : w.v[m - 1]);
   }
   // Pass-1 checks of this thread's leaf (mr_solver.cpp:171-178).
+  // early loads for the update phase (step-start values, neighbour status):
+  // issued before the flux work so their latency is hidden behind it
+  double base0[NC];
+  unsigned nbst = 0;  // 2 bits per face (axis*2 + side): the neighbour's status
+  if (is_leaf) {
+#pragma unroll
+    for (int m = 0; m < NC; ++m) base0[m] = a.base[m * comp + own];
+    const int c0[3] = {cx, cy, cz};
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        int p[3] = {c0[0], c0[1], c0[2]};
+        p[ax] += side ? 1 : -1;
+        bool flp;
+        p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
+        nbst |= (unsigned)a.st[off + mr_idx(D, n, p[0], p[1], p[2])] << (2 * (ax * 2 + side));
+      }
+  }
   if (is_leaf) {
     Cons<D> q;
     q.rho = a.eval[own];
@@ -349,8 +368,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         p[ax] += dir;
         bool flp;
         p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
-        const long pcell = off + mr_idx(D, n, p[0], p[1], p[2]);
-        const uint8_t nst = a.st[pcell];
+        const uint8_t nst = (uint8_t)((nbst >> (2 * (ax * 2 + (dir > 0)))) & 3u);
         const bool internal = nst == ST_INTERNAL;
         double F[NC];
         if (internal && l + 1 <= a.hi) {
@@ -419,7 +437,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     double o[NC];
 #pragma unroll
     for (int m = 0; m < NC; ++m) {
-      o[m] = a.base[m * comp + own] + rhs[m] * sdt;
+      o[m] = base0[m] + rhs[m] * sdt;
       a.out[m * comp + own] = o[m];
     }
     if (a.post_check) {  // positivity of the completed step (mr_solver.cpp:290-297)
