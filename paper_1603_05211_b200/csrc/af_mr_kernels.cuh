@@ -238,17 +238,33 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
   for (int ck = 0; ck < NZ; ++ck) {
     const double wk = D == 3 ? axw_w(sz, ck) : 1.0;
     if (wk == 0.0) continue;
+    // the stencil's loads first (positions are always in range) so they are
+    // in flight together, then the ordered accumulation: the whole 3x3 plane
+    // in 2D, one row at a time in 3D (register budget)
+    constexpr int RB = D == 3 ? 1 : 3;  // rows per load batch
 #pragma unroll
-    for (int cj = 0; cj < 3; ++cj) {
-      const double wjk = axw_w(sy, cj) * wk;
-      if (wjk == 0.0) continue;
+    for (int cj0 = 0; cj0 < 3; cj0 += RB) {
+      double v[RB][3][NC];
 #pragma unroll
-      for (int ci = 0; ci < 3; ++ci) {
-        const double w = axw_w(sx, ci) * wjk;
-        if (w == 0.0) continue;
-        const long c = poff + mr_idx(D, pn, axw_p(sx, ci), axw_p(sy, cj), D == 3 ? axw_p(sz, ck) : 0);
+      for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int m = 0; m < NC; ++m) out[m] = out[m] + V[m * comp + c] * w;
+        for (int ci = 0; ci < 3; ++ci) {
+          const long c = poff + mr_idx(D, pn, axw_p(sx, ci), axw_p(sy, cj0 + r),
+                                       D == 3 ? axw_p(sz, ck) : 0);
+#pragma unroll
+          for (int m = 0; m < NC; ++m) v[r][ci][m] = V[m * comp + c];
+        }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double wjk = axw_w(sy, cj0 + r) * wk;
+        if (wjk == 0.0) continue;
+#pragma unroll
+        for (int ci = 0; ci < 3; ++ci) {
+          const double w = axw_w(sx, ci) * wjk;
+          if (w == 0.0) continue;
+#pragma unroll
+          for (int m = 0; m < NC; ++m) out[m] = out[m] + v[r][ci][m] * w;
+        }
       }
     }
   }
