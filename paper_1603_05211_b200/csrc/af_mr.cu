@@ -204,6 +204,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   D_ = c.dim;
   L_ = c.level;
   NC_ = D_ + 2;
+  reg_fine_ = 2 * (1 << (D_ - 1));
   if (o.eps_level) eps_level_.assign(o.eps_level, o.eps_level + L_ + 1);
   opt_.eps_level = nullptr;
   AF_CUDA(cudaSetDevice(c.device));
@@ -1045,18 +1046,34 @@ void MR::build_registers_(int top) {
   int count = 0;
   AF_CUDA(cudaMemcpyAsync(&count, d_regcount_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  static const bool dbg = std::getenv("AF_MR_DEBUG_REGS") != nullptr;
+  if (dbg) std::fprintf(stderr, "registers: %d (capacity %ld)\n", count, reg_cap_);
   if (count > reg_cap_) {
-    for (void* p : {(void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_}) cudaFree(p);
-    reg_cap_ = std::max<long>(count, 1024);
-    AF_CUDA(cudaMalloc(&d_regc_, sizeof(double) * NC_ * reg_cap_));
-    AF_CUDA(cudaMalloc(&d_regf_, sizeof(double) * NC_ * 8 * reg_cap_));
-    AF_CUDA(cudaMalloc(&d_regfc_, reg_cap_));
-    AF_CUDA(cudaMalloc(&d_regff_, reg_cap_));
+    // stream-ordered, geometric growth: no device-wide synchronisation and
+    // few reallocations while the interface grows over the first cycles
+    for (void* p : {(void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_})
+      if (p) AF_CUDA(cudaFreeAsync(p, stream_));
+    // physical memory stays with the pool between reallocations (mapping
+    // fresh memory is what makes a reallocation slow), and the capacity
+    // grows 4x so that happens a few times per run at most
+    cudaMemPool_t pool;
+    AF_CUDA(cudaDeviceGetDefaultMemPool(&pool, cfg_.device));
+    unsigned long long keep = ~0ull;
+    AF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    // first allocation: room for an interface a quarter (2D) / sixteenth (3D)
+    // of the level below the finest
+    const long guess = reg_cap_ ? 0 : mr_cells(D_, L_ - 1) / (D_ == 3 ? 16 : 4);
+    reg_cap_ = std::max<long>({2L * count, 4 * reg_cap_, guess, 1L << 16});
+    AF_CUDA(cudaMallocAsync((void**)&d_regc_, sizeof(double) * NC_ * reg_cap_, stream_));
+    AF_CUDA(cudaMallocAsync((void**)&d_regf_, sizeof(double) * NC_ * reg_fine_ * reg_cap_,
+                            stream_));
+    AF_CUDA(cudaMallocAsync((void**)&d_regfc_, reg_cap_, stream_));
+    AF_CUDA(cudaMallocAsync((void**)&d_regff_, reg_cap_, stream_));
   }
-  if (reg_cap_) {
-    AF_CUDA(cudaMemsetAsync(d_regfc_, 0, reg_cap_, stream_));
-    AF_CUDA(cudaMemsetAsync(d_regff_, 0, reg_cap_, stream_));
-    AF_CUDA(cudaMemsetAsync(d_regf_, 0, sizeof(double) * NC_ * 8 * reg_cap_, stream_));
+  if (count) {  // only the slots this cycle uses
+    AF_CUDA(cudaMemsetAsync(d_regfc_, 0, count, stream_));
+    AF_CUDA(cudaMemsetAsync(d_regff_, 0, count, stream_));
+    AF_CUDA(cudaMemsetAsync(d_regf_, 0, sizeof(double) * NC_ * reg_fine_ * count, stream_));
   }
   AF_CUDA(cudaMemsetAsync(d_regerr_, 0, sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(d_badkey_, 0xff, sizeof(unsigned long long), stream_));
@@ -1547,6 +1564,9 @@ void MR::cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long
     const double now = std::chrono::duration<double>(
         std::chrono::steady_clock::now().time_since_epoch()).count();
     if (slot > 0) phase_s_[slot - 1] += now - phase_t0_;
+    static const bool per_cycle = std::getenv("AF_MR_TIMING")[0] == '2';
+    if (per_cycle && slot > 0)
+      std::fprintf(stderr, "cycle %ld phase %d: %.3f ms\n", cycle, slot, 1e3 * (now - phase_t0_));
     phase_t0_ = now;
   };
   tick(0);
@@ -1579,6 +1599,13 @@ void MR::cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long
   const double t_cycle = cfl > 0.0 ? t : static_cast<double>(done) * fixed_dt;
   cur_step_ = done;
   if (opt_.local_time) build_registers_(top);
+  if (timing && std::getenv("AF_MR_TIMING")[0] == '2') {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    std::fprintf(stderr, "cycle %ld registers built: %.3f ms since phase 2\n", cycle,
+                 1e3 * (std::chrono::duration<double>(
+                            std::chrono::steady_clock::now().time_since_epoch()).count() -
+                        phase_t0_));
+  }
   if (opt_.local_time)
     advance_local(top, t_cycle, static_cast<double>(sub) * dt, nullptr);
   else

@@ -192,6 +192,7 @@ class MR {
   int* d_regerr_ = nullptr;
   unsigned long long* d_badkey_ = nullptr;
   long reg_cap_ = 0;
+  int reg_fine_ = 0;  // fine slots per register: 2 substeps x 2^(d-1) sub-faces
   bool registers_built_ = false;
   unsigned long long* d_red_ = nullptr;  // scratch reductions
   std::vector<long> tile_off_;           // per-level offset into d_tiles_

@@ -11,6 +11,8 @@
 // its asymmetric low-face stencil (p-2, p-1 | p, p+2) (mr_solver.cpp:80).
 #pragma once
 
+#include <type_traits>
+
 #include "af_mr_kernels.cuh"
 
 namespace af {
@@ -46,7 +48,7 @@ struct MRStageArgs {
   const int* regbase;        // per cell: first register of the cell
   const uint8_t* regmask;    // per cell: faces (axis*2+side) holding a register
   double* regc;              // [R][NC] coarse provisional flux * step_dt
-  double* regf;              // [R][2 substeps][4 sub-faces][NC]
+  double* regf;              // [R][2 substeps][2^(d-1) sub-faces][NC]
   uint8_t* regfc;            // [R] has_coarse
   uint8_t* regff;            // [R] has_fine
   int* regerr;               // fine contribution without a register slot
@@ -270,87 +272,72 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   auto cons_at = [&](int x, int y, int z) {
     return resolve_at<D>(a.eval, comp, g, l, x, y, z, &a);
   };
-  // Face fluxes needed by a leaf of the tile.
-  constexpr int UX = (K::NXF + 31) / 32, UY = (K::NYF + 31) / 32, UZ = (K::NZF + 31) / 32;
-  for (int u = warp; u < UX + UY + UZ; u += K::NT / 32) {
+  // Status of the bc-mapped cell (x, y, z) of this level (global coords).
+  auto status_at = [&](int x, int y, int z) {
+    bool f;
+    const int mx = mr_map(x, n, g.bc[0], g.bc[1], f);
+    const int my = mr_map(y, n, g.bc[2], g.bc[3], f);
+    const int mz = D == 3 ? mr_map(z, n, g.bc[4], g.bc[5], f) : 0;
+    return a.st[off + mr_idx(D, n, mx, my, mz)];
+  };
+  const bool fine_ok = l + 1 <= a.hi;  // the finer level steps in this call
+  // Face fluxes needed by a leaf of the tile. A face between a leaf and an
+  // INTERNAL same-level neighbour whose children step now gets the coarse
+  // side of the interface rule, the fine sub-face average
+  // (fine_face_average, mr_solver.cpp:59-95), here: one thread per face, so
+  // the sub-face fluxes of different faces run in parallel.
+  auto do_face = [&](auto axc, int fx, int fy, int fz, int slot) {
+    constexpr int AX = decltype(axc)::value;
+    const int ex = AX == 0, ey = AX == 1, ez = AX == 2;
+    const bool lL = leaf_at(fx - ex, fy - ey, fz - ez), lR = leaf_at(fx, fy, fz);
+    if (!lL && !lR) return;
     int fb = 0;
-    if (u < UX) {
-      const int f = u * 32 + lane;
-      if (f < K::NXF) {
-        const int fx = f % (TX + 1), fy = (f / (TX + 1)) % TY, fz = D == 3 ? f / ((TX + 1) * TY) : 0;
-        if (leaf_at(fx - 1, fy, fz) || leaf_at(fx, fy, fz)) {
-          const int iy = fy + 2, iz = D == 3 ? fz + 2 : 0;
-          const Prim<D> wm1 = P(fx, iy, iz), w0 = P(fx + 1, iy, iz), wp1 = P(fx + 2, iy, iz),
-                        wp2 = P(fx + 3, iy, iz);
-          Prim<D> lft, rgt;
-          Cons<D> F;
-          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
-            fb = 1;
-            F = num_flux<D, 0, LIM>(cons_at(x0 + fx - 1, y0 + fy, z0 + fz), w0,
-                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
-          } else {
-            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = num_flux<D, 0, LIM>(ql, lft, qr, rgt, gamma);
-          }
-          fl[f] = F.rho;
-#pragma unroll
-          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + f] = F.m[d];
-          fl[(NC - 1) * K::NF + f] = F.E;
-          ffb[f] = fb;
-        }
+    Cons<D> F;
+    int side = 0;  // +1: leaf on the low side, INTERNAL high; -1: the reverse
+    if (fine_ok && lL != lR) {
+      const int ox = x0 + (lL ? fx : fx - ex), oy = y0 + (lL ? fy : fy - ey);
+      const int oz = z0 + (lL ? fz : fz - ez);
+      if (status_at(ox, oy, oz) == ST_INTERNAL) side = lL ? 1 : -1;
+    }
+    if (side) {
+      const int c[3] = {x0 + (side > 0 ? fx - ex : fx), y0 + (side > 0 ? fy - ey : fy),
+                        z0 + (side > 0 ? fz - ez : fz)};
+      F = fine_face_average<D, AX, LIM>(a.eval, comp, g, l, c, side, gamma, gm1, &fb);
+    } else {
+      // stencil along AX in halo-box coordinates: cells fx-2 .. fx+1
+      const int ix = fx + 2, iy = fy + 2, iz = D == 3 ? fz + 2 : 0;
+      const Prim<D> wm1 = P(ix - 2 * ex, iy - 2 * ey, iz - 2 * ez);
+      const Prim<D> w0 = P(ix - ex, iy - ey, iz - ez);
+      const Prim<D> wp1 = P(ix, iy, iz);
+      const Prim<D> wp2 = P(ix + ex, iy + ey, iz + ez);
+      Prim<D> lft, rgt;
+      if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
+        fb = 1;
+        F = num_flux<D, AX, LIM>(cons_at(x0 + fx - ex, y0 + fy - ey, z0 + fz - ez), w0,
+                                 cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
+      } else {
+        const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
+        F = num_flux<D, AX, LIM>(ql, lft, qr, rgt, gamma);
       }
-    } else if (u < UX + UY) {
-      const int f = (u - UX) * 32 + lane;
-      if (f < K::NYF) {
-        const int fx = f % TX, fy = (f / TX) % (TY + 1), fz = D == 3 ? f / (TX * (TY + 1)) : 0;
-        if (leaf_at(fx, fy - 1, fz) || leaf_at(fx, fy, fz)) {
-          const int ix = fx + 2, iz = D == 3 ? fz + 2 : 0;
-          const Prim<D> wm1 = P(ix, fy, iz), w0 = P(ix, fy + 1, iz), wp1 = P(ix, fy + 2, iz),
-                        wp2 = P(ix, fy + 3, iz);
-          Prim<D> lft, rgt;
-          Cons<D> F;
-          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
-            fb = 1;
-            F = num_flux<D, 1, LIM>(cons_at(x0 + fx, y0 + fy - 1, z0 + fz), w0,
-                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
-          } else {
-            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = num_flux<D, 1, LIM>(ql, lft, qr, rgt, gamma);
-          }
-          const int g2 = K::NXF + f;
-          fl[g2] = F.rho;
+    }
+    fl[slot] = F.rho;
 #pragma unroll
-          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + g2] = F.m[d];
-          fl[(NC - 1) * K::NF + g2] = F.E;
-          ffb[g2] = fb;
-        }
-      }
+    for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + slot] = F.m[d];
+    fl[(NC - 1) * K::NF + slot] = F.E;
+    ffb[slot] = (uint8_t)fb;
+  };
+  for (int f = tid; f < K::NF; f += K::NT) {
+    if (f < K::NXF) {
+      const int fx = f % (TX + 1), fy = (f / (TX + 1)) % TY, fz = D == 3 ? f / ((TX + 1) * TY) : 0;
+      do_face(std::integral_constant<int, 0>(), fx, fy, fz, f);
+    } else if (f < K::NXF + K::NYF) {
+      const int h = f - K::NXF;
+      const int fx = h % TX, fy = (h / TX) % (TY + 1), fz = D == 3 ? h / (TX * (TY + 1)) : 0;
+      do_face(std::integral_constant<int, 1>(), fx, fy, fz, f);
     } else if constexpr (D == 3) {
-      const int f = (u - UX - UY) * 32 + lane;
-      if (f < K::NZF) {
-        const int fx = f % TX, fy = (f / TX) % TY, fz = f / (TX * TY);
-        if (leaf_at(fx, fy, fz - 1) || leaf_at(fx, fy, fz)) {
-          const int ix = fx + 2, iy = fy + 2;
-          const Prim<D> wm1 = P(ix, iy, fz), w0 = P(ix, iy, fz + 1), wp1 = P(ix, iy, fz + 2),
-                        wp2 = P(ix, iy, fz + 3);
-          Prim<D> lft, rgt;
-          Cons<D> F;
-          if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, lft, rgt)) {
-            fb = 1;
-            F = num_flux<D, 2, LIM>(cons_at(x0 + fx, y0 + fy, z0 + fz - 1), w0,
-                                cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
-          } else {
-            const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-            F = num_flux<D, 2, LIM>(ql, lft, qr, rgt, gamma);
-          }
-          const int g3 = K::NXF + K::NYF + f;
-          fl[g3] = F.rho;
-#pragma unroll
-          for (int d = 0; d < D; ++d) fl[(1 + d) * K::NF + g3] = F.m[d];
-          fl[(NC - 1) * K::NF + g3] = F.E;
-          ffb[g3] = fb;
-        }
-      }
+      const int h = f - K::NXF - K::NYF;
+      const int fx = h % TX, fy = (h / TX) % TY, fz = h / (TX * TY);
+      do_face(std::integral_constant<int, 2>(), fx, fy, fz, f);
     }
   }
   __syncthreads();
@@ -371,16 +358,9 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         const uint8_t nst = (uint8_t)((nbst >> (2 * (ax * 2 + (dir > 0)))) & 3u);
         const bool internal = nst == ST_INTERNAL;
         double F[NC];
-        if (internal && l + 1 <= a.hi) {
-          Cons<D> f;
-          if (ax == 0) f = fine_face_average<D, 0, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
-          else if (ax == 1) f = fine_face_average<D, 1, LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
-          else f = fine_face_average<D, (D == 3 ? 2 : 1), LIM>(a.eval, comp, g, l, c, dir, gamma, gm1, &nfb);
-          F[0] = f.rho;
-#pragma unroll
-          for (int d = 0; d < D; ++d) F[1 + d] = f.m[d];
-          F[NC - 1] = f.E;
-        } else {
+        {
+          // the face array holds the same-level flux, or at an interface whose
+          // finer side steps now, the fine sub-face average (face phase)
           int fi;
           if (ax == 0) fi = (tz * TY + ty) * (TX + 1) + tx + (dir > 0);
           else if (ax == 1) fi = K::NXF + (tz * (TY + 1) + ty + (dir > 0)) * TX + tx;
@@ -388,7 +368,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
 #pragma unroll
           for (int m = 0; m < NC; ++m) F[m] = fl[m * K::NF + fi];
           nfb += ffb[fi];
-          if (a.reg_stage) {
+          if (a.reg_stage && !(internal && l + 1 <= a.hi)) {
             if (internal) {
               // finer neighbour advancing later: provisional flux, coarse register
               const int R = reg_index(a.regbase, a.regmask, own, ax * 2 + (dir > 0));
@@ -413,7 +393,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
                   for (int b = 0; b < D; ++b)
                     if (b != ax) t = 2 * t + (c[b] & 1);
                   const double w = a.step_dt * a.share;
-                  double* dst = a.regf + (((long)R * 2 + a.sub) * 4 + t) * NC;
+                  double* dst = a.regf + (((long)R * 2 + a.sub) * (D == 3 ? 4 : 2) + t) * NC;
 #pragma unroll
                   for (int m = 0; m < NC; ++m) dst[m] = F[m] * w;
                   a.regff[R] = 1;
@@ -473,7 +453,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
           for (int b = 0; b < D; ++b)
             if (b != ax) t = 2 * t + (c[b] & 1);
           const double w = a.step_dt * a.share;
-          double* dst = a.regf + (((long)R * 2 + a.sub) * 4 + t) * NC;
+          double* dst = a.regf + (((long)R * 2 + a.sub) * (D == 3 ? 4 : 2) + t) * NC;
 #pragma unroll
           for (int m = 0; m < NC; ++m) dst[m] = fl[m * K::NF + fi] * w;
           a.regff[R] = 1;
@@ -581,7 +561,7 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
       for (int m = 0; m < NC; ++m) {
         double f = 0.0;
         for (int sub = 0; sub < 2; ++sub)
-          for (int t = 0; t < nsub; ++t) f = f + regf[(((long)R * 2 + sub) * 4 + t) * NC + m];
+          for (int t = 0; t < nsub; ++t) f = f + regf[(((long)R * 2 + sub) * nsub + t) * NC + m];
         q[m] = q[m] + (regc[(long)R * NC + m] - f) * s;
       }
       regfc[R] = 0;
