@@ -749,16 +749,13 @@ double MR::leaf_speed_sum() {
   return as_d(b);
 }
 
-void MR::snapshot_(int lo, int hi) {
-  AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_V_, d_Qold_, d_st_, g_, AF_L, nullptr, 0);
-}
-
 // One RK stage for the leaves of levels [lo, hi] (MRSolver::stage,
 // mr_solver.cpp:163-193): all levels read the same state, then commit.
 void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   MRStageArgs a{};
   a.eval = d_V_;
   a.base = d_Qold_;
+  a.snap = stage == 1 ? d_Qold_ : nullptr;  // stage 1 writes the q_old snapshot
   a.out = d_Vs_;
   a.st = d_st_;
   a.gamma = cfg_.gamma;
@@ -859,7 +856,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
 // parent's two substeps this call is (the fine register slot).
 void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
   const int top = std::min(hi, L_);
-  snapshot_(lo, top);
+  // (the q_old snapshot of the stepping leaves is written by stage 1)
   for (int l = lo; l <= top; ++l) {
     t_old_[l] = t;
     t_new_[l] = t + dt;

@@ -69,7 +69,6 @@ class MR {
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);
   void build_registers_(int top);
-  void snapshot_(int lo, int hi);
   void check_error_(long step);
   void collect_stage_records_(af_step_diag* d);
   void apply_registers_(int coarse_level);

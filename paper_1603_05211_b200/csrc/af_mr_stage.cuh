@@ -20,6 +20,7 @@ namespace af {
 struct MRStageArgs {
   const double* eval;  // concatenated level values the fluxes read
   const double* base;  // step-start values (q_old)
+  double* snap;        // stage 1: q_old snapshot target (base is then eval itself)
   double* out;         // stage output (leaves of this level)
   const uint8_t* st;
   double gamma, gm1;
@@ -229,8 +230,14 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   double base0[NC];
   unsigned nbst = 0;  // 2 bits per face (axis*2 + side): the neighbour's status
   if (is_leaf) {
+    // stage 1 takes the step-start values from eval and writes the q_old
+    // snapshot of its leaves (step_levels, mr_solver.cpp:235-239)
 #pragma unroll
-    for (int m = 0; m < NC; ++m) base0[m] = a.base[m * comp + own];
+    for (int m = 0; m < NC; ++m) base0[m] = (a.snap ? a.eval : a.base)[m * comp + own];
+    if (a.snap) {
+#pragma unroll
+      for (int m = 0; m < NC; ++m) a.snap[m * comp + own] = base0[m];
+    }
     const int c0[3] = {cx, cy, cz};
 #pragma unroll
     for (int ax = 0; ax < D; ++ax)
