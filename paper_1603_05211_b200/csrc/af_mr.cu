@@ -625,9 +625,10 @@ void MR::refine(int top) {
   if (!lists_valid_) build_lists_();
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
   AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
-  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L, d_norms_);
+  // details with the refine flags of their leaf children (one launch)
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
-  AF_ML_LAUNCH(mr_refine_flag_level, 1, L_ - 1, false, d_st_, d_det_, d_flag_, g_, AF_L, -1.0);
+  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
+                 d_norms_, d_flag_);
   uint8_t* split = d_flag_;
   if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
     for (int l = 1; l <= L_ - 1; ++l) {
@@ -1316,10 +1317,9 @@ void MR::capture_while_(F&& body) {
 void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body) {
   const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
-  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
-                 d_norms_);
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
-  AF_ML_LAUNCH(mr_refine_flag_level, 1, L_ - 1, false, d_st_, d_det_, d_flag_, g_, AF_L, -1.0);
+  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
+                 d_norms_, d_flag_);
   AF_ML_LAUNCH(mr_apply_split_level, 1, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
   long b0 = launches_;
@@ -1664,7 +1664,7 @@ void MR::details(int level, double* out) {
   const long cells = mr_cells(D_, level);
   AF_CUDA(cudaMemsetAsync(d_det_ + g_.cell_off[level], 0xff, sizeof(double) * cells, stream_));
   AF_MR_LAUNCH(mr_detail_level, grid_for(cells), d_V_, d_st_, d_det_, g_, level, d_norms_,
-               (const int*)nullptr, 0);
+               (uint8_t*)nullptr, (const int*)nullptr, 0);
   AF_CUDA(cudaMemcpyAsync(out, d_det_ + g_.cell_off[level], sizeof(double) * cells,
                           cudaMemcpyDefault, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));

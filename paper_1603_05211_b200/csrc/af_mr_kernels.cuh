@@ -413,9 +413,12 @@ __device__ __forceinline__ double child_detail(const double* V, long comp, const
 }
 
 // Detail of every INTERNAL node at level l (child-parallel).
+// With `flag`, each child lane also takes refine's decision for its child
+// (mr_tree.cpp:364-372): a LEAF child at level l+1 in [1, L-1] is flagged
+// when the parent's detail is >= eps_{l+1} (flag[] zeroed beforehand).
 template <int D>
 __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det, MRLevels g,
-                                int l, const double* norms,
+                                int l, const double* norms, uint8_t* flag,
     const int* tiles = nullptr, int ntiles = 0) {
   AF_PDL_ENTRY();
   level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv_, long c, bool valid, int ch) {
@@ -423,37 +426,23 @@ __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det,
     const int n = 1 << l;
     const long off = g.cell_off[l];
     const bool internal = valid && st[off + c] == ST_INTERNAL;
+    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     double r = 0.0;
-    if (internal) {
-      const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-      r = child_detail<D>(V, g.total_cells, g, l, i, j, k, ch, norms);
-    }
+    if (internal) r = child_detail<D>(V, g.total_cells, g, l, i, j, k, ch, norms);
     r = node_group_max<D>(r);
     if (internal && ch == 0) det[off + c] = r;
+    if (flag && internal && l + 1 <= g.L - 1) {
+      const long fc = g.cell_off[l + 1] +
+                      mr_idx(D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                             D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+      if (st[fc] == ST_LEAF) flag[fc] = r >= g.eps_l[l + 1] ? 1 : 0;
+    }
   });
 }
 
 // Buffer dilation of the LT refine (mr_tree.cpp:374-396): every leaf within
 // Chebyshev radius r of a flagged leaf (same level, bc-mapped) is flagged too.
 // flag[] holds 1 for detail-flagged leaves; this pass writes 2 for dilated.
-template <int D>
-__global__ void mr_refine_flag_level(const uint8_t* st, const double* det, uint8_t* flag,
-                                     MRLevels g, int l, double eps,
-    const int* tiles = nullptr, int ntiles = 0) {
-  AF_PDL_ENTRY();
-  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
-    const int l = lv_;
-    const int n = 1 << l, pn = n >> 1;
-    const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
-    uint8_t f = 0;
-    if (st[off + c] == ST_LEAF && l >= 1 && l < g.L) {
-      const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-      f = det[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)] >= (eps < 0.0 ? g.eps_l[l] : eps) ? 1 : 0;
-    }
-    flag[off + c] = f;
-  });
-}
-
 template <int D>
 __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t* flag2,
                                 MRLevels g, int l, int r,
