@@ -1272,15 +1272,25 @@ void MR::note_event_node_() {
   ev_nodes_.push_back(deps[0]);
 }
 
+// The handle of a WHILE node: `def` on every graph launch (1: the body runs
+// at least once), or with def = 0 set by a kernel ahead of the node.
+cudaGraphConditionalHandle MR::make_cond_(unsigned def) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t graph = nullptr;
+  AF_CUDA(cudaStreamGetCaptureInfo(stream_, &cs, nullptr, &graph, nullptr, nullptr));
+  cudaGraphConditionalHandle h;
+  AF_CUDA(cudaGraphConditionalHandleCreate(&h, graph, def, cudaGraphCondAssignDefault));
+  return h;
+}
+
 template <class F>
-void MR::capture_while_(F&& body) {
+void MR::capture_while_(F&& body, cudaGraphConditionalHandle h, bool have_h) {
   cudaStreamCaptureStatus cs;
   cudaGraph_t graph = nullptr;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
+  if (!have_h) h = make_cond_(1);
   AF_CUDA(cudaStreamGetCaptureInfo(stream_, &cs, nullptr, &graph, &deps, &ndeps));
-  cudaGraphConditionalHandle h;
-  AF_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
   cudaGraphNodeParams p{};
   p.type = cudaGraphNodeTypeConditional;
   p.conditional.handle = h;
@@ -1357,18 +1367,32 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   ++launches_;
   AF_CUDA(cudaGetLastError());
   virtuals_ = false;
-  // coarsen (mr_tree.cpp:473-510): sweeps while one merged and another can
+  // coarsen (mr_tree.cpp:473-510): the first sweep and its prediction
+  // refresh unconditionally, further sweeps (a WHILE node) only while one
+  // merged and another can (the re-sweep test of coarsen_level_dev)
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
+  for (int l = L_ - 1; l >= min_leaf_; --l)
+    AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1),
+                 d_norms_, d_flagi_, AF_BAND(l));
+  predict_fill_(1, 0, min_leaf_ + 1);
+  const cudaGraphConditionalHandle hc = make_cond_(0);
+  launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, hc, d_flagi_, full_sweeps_ ? 0 : 1,
+           d_acc_ + 5);
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
   b0 = launches_;
-  capture_while_([&](cudaGraphConditionalHandle h) {
-    for (int l = L_ - 1; l >= min_leaf_; --l)
-      AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1), d_norms_,
-                   d_flagi_, AF_BAND(l));
-    predict_fill_(1, 0, min_leaf_ + 1);  // a no-op recompute when nothing merged
-    launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, h, d_flagi_, full_sweeps_ ? 0 : 1, d_acc_ + 4);
-    ++launches_;
-    AF_CUDA(cudaGetLastError());
-  });
+  capture_while_(
+      [&](cudaGraphConditionalHandle h) {
+        for (int l = L_ - 1; l >= min_leaf_; --l)
+          AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l,
+                       eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
+        predict_fill_(1, 0, min_leaf_ + 1);  // a no-op recompute when nothing merged
+        launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, h, d_flagi_, full_sweeps_ ? 0 : 1,
+                 d_acc_ + 4);
+        ++launches_;
+        AF_CUDA(cudaGetLastError());
+      },
+      hc, true);
   *sweep_body = launches_ - b0;
   // no list rebuild here: the next refine works on this cycle's post-refine
   // lists, a superset of the coarsened tree's band (every node it holds
@@ -1487,6 +1511,10 @@ bool MR::run_batch_graph_(long B, double cfl, double fixed_dt, long& done, long&
     return false;
   }
   launches_ += B * cg.launches_fixed + (long)ha[3] * cg.grade_body + (long)ha[4] * cg.sweep_body;
+  static const bool dbg = std::getenv("AF_MR_DEBUG_LOOPS") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "batch of %ld cycles: %llu gradedness passes, %llu coarsen sweeps\n", B,
+                 ha[3], ha[4]);
   std::memcpy(&max_cfl_, &ha[0], 8);
   std::memcpy(&max_wave_, &ha[1], 8);
   fallbacks_ += (long)ha[2];

@@ -120,7 +120,8 @@ class MR {
   unsigned long long* d_acc_ = nullptr;     // max_cfl, max wave, fallbacks, grade/sweep iterations
   unsigned long long* h_small_ = nullptr;   // pinned staging
   template <class F>
-  void capture_while_(F&& body);
+  void capture_while_(F&& body, cudaGraphConditionalHandle h = 0, bool have_h = false);
+  cudaGraphConditionalHandle make_cond_(unsigned def);
   void build_lists_enqueue_();
   void note_event_node_();
   std::vector<cudaGraphNode_t> ev_nodes_;  // event-record nodes of the capture in progress
