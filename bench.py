@@ -296,7 +296,8 @@ def main():
     lib = _abi.load()
     idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
     comm = None
-    if world > 1:
+    needs_comm = world > 1 and (args.workload not in MR_OPTS or mr_decomposed(args, world))
+    if needs_comm:  # NCCL only where the path exchanges (not for MR replicas)
         uid = (C.c_ubyte * 128)()
         if rank == 0:
             assert lib.af_comm_unique_id(C.cast(uid, C.c_char_p)) == 0
