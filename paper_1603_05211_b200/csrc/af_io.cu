@@ -235,13 +235,12 @@ void l1_error(int dim, int level, double extent, const double* sol, int ref_leve
 std::string MR::dump() {
   std::vector<uint8_t> hs(g_.total_cells);
   std::vector<double> hv((size_t)NC_ * g_.total_cells);
-  AF_CUDA(cudaMemcpyAsync(hs.data(), d_st_, hs.size(), cudaMemcpyDeviceToHost, stream_));
-  AF_CUDA(cudaMemcpyAsync(hv.data(), d_V_, hv.size() * 8, cudaMemcpyDeviceToHost, stream_));
-  AF_CUDA(cudaStreamSynchronize(stream_));
+  wtohost_(hs.data(), d_st_, 1, 1);
+  wtohost_(hv.data(), d_V_, 8, NC_);
   std::vector<uint8_t> vm;
   if (virtuals_) {
     vm.resize(g_.total_cells);
-    AF_CUDA(cudaMemcpy(vm.data(), d_mark_, vm.size(), cudaMemcpyDeviceToHost));
+    wtohost_(vm.data(), d_mark_, 1, 1);
   }
   const long comp = g_.total_cells;
   std::string out;

@@ -35,10 +35,14 @@ inline unsigned grid_for(long n, int block = 256) {
   return (unsigned)std::max<long>(1, std::min<long>(b, kGrid));
 }
 
+// Level-L cells of rows [r0, r1) from a compact AoS holding those rows.
 template <int D>
-__global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLevels g) {
+__global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLevels g, int r0,
+                                 int r1) {
   AF_PDL_ENTRY();
-  const long cells = mr_cells(D, g.L), off = g.cell_off[g.L], comp = g.total_cells;
+  const long rowlen = D == 3 ? 1L << (2 * g.L) : 1L << g.L;
+  const long cells = (long)(r1 - r0) * rowlen, comp = g.total_cells;
+  const long off = g.cell_off[g.L] + (long)r0 * rowlen;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
     const double* q = aos + 5 * c;
@@ -50,10 +54,14 @@ __global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLe
   }
 }
 
+// Level-l cells of rows [r0, r1) into a compact AoS.
 template <int D>
-__global__ void mr_download_level(const double* V, double* __restrict__ aos, MRLevels g, int l) {
+__global__ void mr_download_level(const double* V, double* __restrict__ aos, MRLevels g, int l,
+                                  int r0, int r1) {
   AF_PDL_ENTRY();
-  const long cells = mr_cells(D, l), off = g.cell_off[l], comp = g.total_cells;
+  const long rowlen = D == 3 ? 1L << (2 * l) : 1L << l;
+  const long cells = (long)(r1 - r0) * rowlen, comp = g.total_cells;
+  const long off = g.cell_off[l] + (long)r0 * rowlen;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
     double* q = aos + 5 * c;
@@ -76,6 +84,7 @@ __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* 
   const long comp = g.total_cells;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
+    if (g.dist && !row_in_region(g, l, mr_row(D, l, c))) continue;  // this rank's rows
     if (st[off + c] != ST_ABSENT) continue;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     if (!mark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
@@ -222,23 +231,11 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   g_.cell_off[L_ + 1] = tot;
   g_.total_cells = tot;
   for (int l = 0; l <= L_; ++l) g_.eps_l[l] = eps_at_(l);
-  const size_t vbytes = sizeof(double) * NC_ * tot;
-  AF_CUDA(cudaMalloc(&d_st_, tot));
-  AF_CUDA(cudaMalloc(&d_mark_, tot));
-  AF_CUDA(cudaMalloc(&d_flag_, tot));
-  AF_CUDA(cudaMalloc(&d_flag2_, tot));
-  AF_CUDA(cudaMalloc(&d_V_, vbytes));
-  AF_CUDA(cudaMalloc(&d_Vs_, vbytes));
-  AF_CUDA(cudaMalloc(&d_Qold_, vbytes));
   if (o.local_time) {
-    AF_CUDA(cudaMalloc(&d_VQold_, vbytes));
-    AF_CUDA(cudaMalloc(&d_regbase_, sizeof(int) * tot));
-    AF_CUDA(cudaMalloc(&d_regmask_, tot));
     AF_CUDA(cudaMalloc(&d_regcount_, sizeof(int)));
     AF_CUDA(cudaMalloc(&d_regerr_, sizeof(int)));
     AF_CUDA(cudaMalloc(&d_badkey_, sizeof(unsigned long long)));
   }
-  AF_CUDA(cudaMalloc(&d_det_, sizeof(double) * tot));
   AF_CUDA(cudaMalloc(&d_norms_, sizeof(double) * 5));
   AF_CUDA(cudaMalloc(&d_err_, 4 * sizeof(int)));
   AF_CUDA(cudaMalloc(&d_flagi_, 2 * sizeof(int)));
@@ -313,6 +310,28 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
       g_.reg_hi[l] = hi;
     }
   }
+  // per-cell arrays: windowed with ranks (AF_MR_NO_WINDOWS maps everything)
+  windows_ = dist_ && std::getenv("AF_MR_NO_WINDOWS") == nullptr;
+  win_setup_();
+  d_st_ = static_cast<uint8_t*>(walloc_(1, 1));
+  d_mark_ = static_cast<uint8_t*>(walloc_(1, 1));
+  d_flag_ = static_cast<uint8_t*>(walloc_(1, 1));
+  d_flag2_ = static_cast<uint8_t*>(walloc_(1, 1));
+  d_V_ = static_cast<double*>(walloc_(8, NC_));
+  d_Vs_ = static_cast<double*>(walloc_(8, NC_));
+  d_Qold_ = static_cast<double*>(walloc_(8, NC_));
+  d_det_ = static_cast<double*>(walloc_(8, 1));
+  if (o.local_time) {
+    d_VQold_ = static_cast<double*>(walloc_(8, NC_));
+    d_regbase_ = static_cast<int*>(walloc_(4, 1));
+    d_regmask_ = static_cast<uint8_t*>(walloc_(1, 1));
+  }
+  {  // stream-ordered scratch allocations keep their memory
+    cudaMemPool_t pool;
+    AF_CUDA(cudaDeviceGetDefaultMemPool(&pool, c.device));
+    unsigned long long keep = ~0ull;
+    AF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
@@ -325,11 +344,11 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   AF_CUDA(cudaMalloc(&d_lpl_, sizeof(unsigned long long) * 17));
   AF_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
-  AF_CUDA(cudaMemsetAsync(d_st_, ST_ABSENT, tot, stream_));
-  AF_CUDA(cudaMemsetAsync(d_mark_, 0, tot, stream_));
-  AF_CUDA(cudaMemsetAsync(d_V_, 0, vbytes, stream_));
-  AF_CUDA(cudaMemsetAsync(d_Vs_, 0, vbytes, stream_));
-  AF_CUDA(cudaMemsetAsync(d_Qold_, 0, vbytes, stream_));
+  wset_(d_st_, 1, 1, ST_ABSENT, 0, L_);
+  wset_(d_mark_, 1, 1, 0, 0, L_);
+  wset_(d_V_, 8, NC_, 0, 0, L_);
+  wset_(d_Vs_, 8, NC_, 0, 0, L_);
+  wset_(d_Qold_, 8, NC_, 0, 0, L_);
   AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
   t_old_.assign(L_ + 1, 0.0);
@@ -369,13 +388,18 @@ MR::~MR() {
   for (void* p : {(void*)d_ckV_, (void*)d_ckSt_, (void*)d_cycrec_, (void*)d_cycctl_, (void*)d_acc_})
     cudaFree(p);
   if (h_dt_step_) cudaFreeHost(h_dt_step_);
-  for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
-                  (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
-                  (void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
+  if (windows_) {
+    wfree_all_();
+  } else {
+    for (void* p : {(void*)d_st_, (void*)d_mark_, (void*)d_flag_, (void*)d_flag2_, (void*)d_V_,
+                    (void*)d_Vs_, (void*)d_Qold_, (void*)d_VQold_, (void*)d_det_,
+                    (void*)d_regbase_, (void*)d_regmask_})
+      cudaFree(p);
+  }
+  for (void* p : {(void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
                   (void*)d_band_, (void*)d_tflag_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
-                  (void*)d_flagi_, (void*)d_red_, (void*)d_regbase_, (void*)d_regmask_,
-                  (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_, (void*)d_regff_,
-                  (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
+                  (void*)d_flagi_, (void*)d_red_, (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_,
+                  (void*)d_regff_, (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
     cudaFree(p);
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
@@ -569,39 +593,36 @@ bool MR::ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult, int cap) cons
 void MR::build(const double* aos) {
   if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
   const long cells = mr_cells(D_, L_);
-  // staged through the stage-output buffer (NC * total_cells >= 5 * cells of L)
-  double* stage = d_Vs_;
-  AF_CUDA(cudaMemcpyAsync(stage, aos, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
-  AF_MR_LAUNCH(mr_upload_finest, grid_for(cells), (const double*)stage, d_V_, g_);
+  const long rowlen = D_ == 3 ? 1L << (2 * L_) : 1L << L_;
+  // this rank's rows of level L (every row on one rank), staged through a
+  // scratch buffer: the caller's array may be host or device memory
+  int r0 = 0, r1 = 1 << L_;
+  if (dist_) part_rows_(rank_, L_, &r0, &r1);
+  const long ucells = (long)(r1 - r0) * rowlen;
+  double* stage = nullptr;
+  AF_CUDA(cudaMallocAsync((void**)&stage, sizeof(double) * 5 * ucells, stream_));
+  AF_CUDA(cudaMemcpyAsync(stage, aos + 5 * (long)r0 * rowlen, sizeof(double) * 5 * ucells,
+                          cudaMemcpyDefault, stream_));
+  AF_MR_LAUNCH(mr_upload_finest, grid_for(ucells), (const double*)stage, d_V_, g_, r0, r1);
+  AF_CUDA(cudaFreeAsync(stage, stream_));
   // from_uniform (mr_tree.cpp:29-71): leaves at L, internals above.
-  AF_CUDA(cudaMemsetAsync(d_st_, ST_INTERNAL, g_.cell_off[L_], stream_));
-  AF_CUDA(cudaMemsetAsync(d_st_ + g_.cell_off[L_], ST_LEAF, cells, stream_));
-  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  wset_(d_st_, 1, 1, ST_INTERNAL, 0, L_ - 1);
+  wset_(d_st_, 1, 1, ST_LEAF, L_, L_);
+  wset_(d_mark_, 1, 1, 0, 0, L_);
   AF_CUDA(cudaMemsetAsync(d_err_, 0, 4 * sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(d_err_ + 1, 0x7f, sizeof(int), stream_));
   virtuals_ = false;
-  // every rank holds the whole initial field: project it everywhere, so the
-  // replicated tree starts identical on all ranks
-  const MRLevels gsave = g_;
-  if (dist_) {
-    for (int l = 0; l <= L_; ++l) {
-      g_.own_lo[l] = g_.reg_lo[l] = 0;
-      g_.own_hi[l] = g_.reg_hi[l] = 1 << l;
-    }
-    g_.dist = 0;
-  }
+  // with ranks: owned projections, the halo rows from their owners, the
+  // replicated levels on every rank (project_range_)
   build_lists_();
   project_range_(0, L_);
-  if (dist_) {
-    AF_CUDA(cudaStreamSynchronize(stream_));
-    g_ = gsave;
-  }
   // set_norms_from (mr_tree.cpp:73-87)
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 8, stream_));
   AF_MR_LAUNCH(mr_norm_kernel, grid_for(cells), d_V_, g_, d_red_);
   unsigned long long nb[5] = {0, 0, 0, 0, 0};
   AF_CUDA(cudaMemcpyAsync(nb, d_red_, 8 * NC_, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  if (g_.dist) allreduce_(nb, NC_, RED_MAX);  // per-component max over all ranks' rows
   double n[5] = {0, 0, 0, 0, 0};
   n[0] = as_d(nb[0]);
   for (int a = 0; a < D_; ++a) n[1 + a] = as_d(nb[1 + a]);
@@ -623,8 +644,8 @@ void MR::build(const double* aos) {
 void MR::refine(int top) {
   registers_built_ = false;
   if (!lists_valid_) build_lists_();
-  AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
-  AF_CUDA(cudaMemsetAsync(d_flag2_, 0, g_.total_cells, stream_));
+  wset_(d_flag_, 1, 1, 0, 0, L_);
+  wset_(d_flag2_, 1, 1, 0, 0, L_);
   // details with the refine flags of their leaf children (one launch)
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
   AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
@@ -682,7 +703,7 @@ void MR::refine(int top) {
 }
 
 void MR::add_virtual_leaves() {
-  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  wset_(d_mark_, 1, 1, 0, 0, L_);
   if (!lists_valid_) build_lists_();
   // with ranks, leaves in halo rows mark owned parents too: scan the band;
   // the stage reads the marks of halo parents (MRLT interpolation, registers)
@@ -1036,7 +1057,7 @@ void MR::collect_stage_records_(af_step_diag* d) {
 // neighbour (valid until the tree changes at the end of the cycle).
 void MR::build_registers_(int top) {
   if (!d_regbase_) throw Error(AF_E_CONFIG, "registers need local_time");
-  AF_CUDA(cudaMemsetAsync(d_regmask_, 0, g_.total_cells, stream_));
+  wset_(d_regmask_, 1, 1, 0, 0, L_);
   AF_CUDA(cudaMemsetAsync(d_regcount_, 0, sizeof(int), stream_));
   for (int l = std::max(top, 0); l <= L_ - 1; ++l)
     AF_MR_LAUNCH(mr_reg_build_level, grid_for(mr_cells(D_, l)), d_st_, g_, l, d_regbase_,
@@ -1185,8 +1206,8 @@ void MR::check_error_(long step) {
   const double* src = d_V_;
   std::vector<double> hv((size_t)NC_ * g_.total_cells);
   std::vector<uint8_t> hs(g_.total_cells);
-  AF_CUDA(cudaMemcpy(hv.data(), kind == 2 ? d_Vs_ : src, hv.size() * 8, cudaMemcpyDeviceToHost));
-  AF_CUDA(cudaMemcpy(hs.data(), d_st_, hs.size(), cudaMemcpyDeviceToHost));
+  wtohost_(hv.data(), kind == 2 ? d_Vs_ : src, 8, NC_);
+  wtohost_(hs.data(), d_st_, 1, 1);
   const double gm1 = cfg_.gamma - 1.0;
   const long comp = g_.total_cells;
   std::memset(&last_, 0, sizeof(last_));
@@ -1326,7 +1347,7 @@ void MR::capture_while_(F&& body, cudaGraphConditionalHandle h, bool have_h) {
 // RK stages, stage records (mr_cycle_end), coarsen sweeps (WHILE), lists.
 void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body) {
   const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
-  AF_CUDA(cudaMemsetAsync(d_flag_, 0, g_.total_cells, stream_));
+  wset_(d_flag_, 1, 1, 0, 0, L_);
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
   AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
                  d_norms_, d_flag_);
@@ -1344,7 +1365,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   build_lists_enqueue_();
   predict_fill_(1, 0);
   // add_virtual_leaves, leaf/node counts, CFL speed
-  AF_CUDA(cudaMemsetAsync(d_mark_, 0, g_.total_cells, stream_));
+  wset_(d_mark_, 1, 1, 0, 0, L_);
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
   virtuals_ = true;
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
@@ -1659,7 +1680,7 @@ void MR::cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long
 
 long MR::leaf_keys(uint64_t* keys, long cap) {
   std::vector<uint8_t> hs(g_.total_cells);
-  AF_CUDA(cudaMemcpyAsync(hs.data(), d_st_, hs.size(), cudaMemcpyDeviceToHost, stream_));
+  wtohost_(hs.data(), d_st_, 1, 1);
   AF_CUDA(cudaStreamSynchronize(stream_));
   std::vector<uint64_t> out;
   for (int l = 0; l <= L_; ++l) {
@@ -1678,12 +1699,28 @@ long MR::leaf_keys(uint64_t* keys, long cap) {
   return (long)out.size();
 }
 
+// With ranks, only this rank's rows (af_mr_local_rows) are written.
 void MR::to_uniform(int level, double* aos) {
   if (level < 0 || level > L_) throw Error(AF_E_LEVEL_MISMATCH, "to_uniform: bad level");
-  const long cells = mr_cells(D_, level);
-  double* tmp = d_Vs_;  // scratch outside a stage; NC * total_cells >= 5 * cells
-  AF_MR_LAUNCH(mr_download_level, grid_for(cells), (const double*)d_V_, tmp, g_, level);
-  AF_CUDA(cudaMemcpyAsync(aos, tmp, sizeof(double) * 5 * cells, cudaMemcpyDefault, stream_));
+  const long rowlen = D_ == 3 ? 1L << (2 * level) : 1L << level;
+  int r0 = 0, r1 = 1 << level;
+  if (dist_) local_rows(level, &r0, &r1);
+  const long cells = (long)(r1 - r0) * rowlen;
+  if (cells <= 0) return;
+  // value_at for every cell: the band keeps predictions current only near the
+  // tree; absent cells farther away get theirs here, coarsest first
+  // (MRTree::to_uniform / value_at, mr_tree.cpp:171-180,608-621)
+  for (int l = std::max(1, min_leaf_ + 1); l <= level; ++l)
+    AF_MR_LAUNCH(mr_predict_level, grid_for(mr_cells(D_, l)), d_V_, (const uint8_t*)d_st_,
+                 (const uint8_t*)(virtuals_ ? d_mark_ : nullptr), g_, l, 0, L_, (const int*)nullptr,
+                 0);
+  fresh_ = false;
+  double* tmp = nullptr;
+  AF_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double) * 5 * cells, stream_));
+  AF_MR_LAUNCH(mr_download_level, grid_for(cells), (const double*)d_V_, tmp, g_, level, r0, r1);
+  AF_CUDA(cudaMemcpyAsync(aos + 5 * (long)r0 * rowlen, tmp, sizeof(double) * 5 * cells,
+                          cudaMemcpyDefault, stream_));
+  AF_CUDA(cudaFreeAsync(tmp, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
 }
 

@@ -152,6 +152,23 @@ class MR {
   enum { XV = 1, XST = 2, XMARK = 4 };
   enum { RED_MAX = 0, RED_SUM = 1, RED_MIN = 2 };
   void part_rows_(int r, int l, int* lo, int* hi) const;
+  // Windowed arrays (ranks): each per-cell array reserves its full virtual
+  // size but maps physical memory only for every level's window rows (the
+  // region plus the tile and stencil overhang); global indexing is unchanged.
+  bool windows_ = false;
+  std::vector<std::vector<std::pair<long, long>>> win_;  // per level: cell ranges [c0, c1)
+  struct WinMap {
+    unsigned long long base = 0;
+    size_t reserved = 0;
+    std::vector<std::pair<unsigned long long, size_t>> maps;  // address, bytes
+    std::vector<unsigned long long> handles;
+  };
+  std::vector<WinMap> wmaps_;
+  void win_setup_();
+  void* walloc_(size_t elem, int ncomp);
+  void wfree_all_();
+  void wset_(void* p, size_t elem, int ncomp, int value, int lev_lo, int lev_hi);
+  void wtohost_(void* dst, const void* src, size_t elem, int ncomp);
   void dist_setup_();
   void dist_free_();
   void exchange_(int mask);

@@ -8,6 +8,8 @@
 // partition level are replicated (they hold no leaves and no absent cells).
 // The transport is NCCL (one process per GPU) or, for tests on one GPU, a
 // group of host threads exchanging through device-to-device copies.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -239,6 +241,181 @@ void MR::exchange_(int mask) {
       ++launches_;
       AF_CUDA(cudaGetLastError());
     }
+}
+
+// ---- windowed arrays --------------------------------------------------------
+namespace {
+// Driver-API virtual memory entry points, resolved through the runtime
+// (cudaGetDriverEntryPoint) so the library does not link libcuda and still
+// loads on a machine without a driver (the CPU test suite).
+struct VmmApi {
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemSetAccess) access = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemAddressFree) free_ = nullptr;
+};
+const VmmApi& vmm() {
+  static VmmApi api = [] {
+    VmmApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      AF_CUDA(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !*fn)
+        throw Error(AF_E_CUDA, std::string("driver entry point missing: ") + name);
+    };
+    get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.granularity));
+    get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve));
+    get("cuMemCreate", reinterpret_cast<void**>(&a.create));
+    get("cuMemMap", reinterpret_cast<void**>(&a.map));
+    get("cuMemSetAccess", reinterpret_cast<void**>(&a.access));
+    get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap));
+    get("cuMemRelease", reinterpret_cast<void**>(&a.release));
+    get("cuMemAddressFree", reinterpret_cast<void**>(&a.free_));
+    return a;
+  }();
+  return api;
+}
+void check_cu(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS)
+    throw Error(AF_E_CUDA, std::string(what) + ": driver error " + std::to_string((int)r));
+}
+}  // namespace
+
+// Per-level window rows: the region widened by the tile height plus the
+// stencil reach, so tile-based kernels (whose tiles may overhang the region)
+// and the stage's 2-cell gather stay inside mapped memory; whole levels below
+// the partition level and where the window covers the level.
+void MR::win_setup_() {
+  const int TR = D_ == 3 ? kTileZ3 : kTileY2;
+  const bool periodic = cfg_.bc[2 * (D_ - 1)] == AF_BC_PERIODIC;
+  win_.assign(L_ + 1, {});
+  for (int l = 0; l <= L_; ++l) {
+    const int n = 1 << l;
+    const long rowlen = D_ == 3 ? 1L << (2 * l) : 1L << l;
+    const long off = g_.cell_off[l];
+    int lo = g_.reg_lo[l] - TR - 2 - halo_, hi = g_.reg_hi[l] + TR + 2 + halo_;
+    if (!dist_ || hi - lo >= n || (g_.reg_hi[l] - g_.reg_lo[l]) >= n) {
+      win_[l].push_back({off, off + (long)n * rowlen});
+      continue;
+    }
+    if (!periodic) {
+      lo = std::max(lo, 0);
+      hi = std::min(hi, n);
+      win_[l].push_back({off + lo * rowlen, off + hi * rowlen});
+    } else {  // may wrap: up to two intervals
+      const int a = ((lo % n) + n) % n, len = hi - lo;
+      if (a + len <= n) {
+        win_[l].push_back({off + a * rowlen, off + (a + len) * rowlen});
+      } else {
+        win_[l].push_back({off + a * rowlen, off + (long)n * rowlen});
+        win_[l].push_back({off, off + (long)(a + len - n) * rowlen});
+      }
+    }
+  }
+}
+
+void* MR::walloc_(size_t elem, int ncomp) {
+  const size_t bytes = elem * (size_t)ncomp * (size_t)g_.total_cells;
+  if (!windows_) {
+    void* p = nullptr;
+    AF_CUDA(cudaMalloc(&p, bytes));
+    return p;
+  }
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = cfg_.device;
+  size_t gran = 0;
+  check_cu(vmm().granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED),
+           "cuMemGetAllocationGranularity");
+  WinMap w;
+  w.reserved = (bytes + gran - 1) / gran * gran;
+  CUdeviceptr base = 0;
+  check_cu(vmm().reserve(&base, w.reserved, gran, 0, 0), "cuMemAddressReserve");
+  w.base = base;
+  // byte ranges of every component's windows, granule-aligned and merged
+  std::vector<std::pair<size_t, size_t>> r;
+  for (int m = 0; m < ncomp; ++m)
+    for (int l = 0; l <= L_; ++l)
+      for (const auto& c : win_[l]) {
+        const size_t b0 = ((size_t)m * g_.total_cells + c.first) * elem;
+        const size_t b1 = ((size_t)m * g_.total_cells + c.second) * elem;
+        r.push_back({b0 / gran * gran, std::min(w.reserved, (b1 + gran - 1) / gran * gran)});
+      }
+  std::sort(r.begin(), r.end());
+  std::vector<std::pair<size_t, size_t>> mr;
+  for (const auto& x : r) {
+    if (!mr.empty() && x.first <= mr.back().second) mr.back().second = std::max(mr.back().second, x.second);
+    else mr.push_back(x);
+  }
+  CUmemAccessDesc acc{};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (const auto& x : mr) {
+    const size_t sz = x.second - x.first;
+    CUmemGenericAllocationHandle h;
+    check_cu(vmm().create(&h, sz, &prop, 0), "cuMemCreate");
+    check_cu(vmm().map(base + x.first, sz, 0, h, 0), "cuMemMap");
+    check_cu(vmm().access(base + x.first, sz, &acc, 1), "cuMemSetAccess");
+    w.maps.push_back({base + x.first, sz});
+    w.handles.push_back(h);
+  }
+  wmaps_.push_back(w);
+  return reinterpret_cast<void*>(base);
+}
+
+void MR::wfree_all_() {
+  for (WinMap& w : wmaps_) {
+    for (size_t i = 0; i < w.maps.size(); ++i) {
+      vmm().unmap(w.maps[i].first, w.maps[i].second);
+      vmm().release(w.handles[i]);
+    }
+    vmm().free_(w.base, w.reserved);
+  }
+  wmaps_.clear();
+}
+
+// memset of levels [lev_lo, lev_hi] of a per-cell array (every component),
+// restricted to the windows
+void MR::wset_(void* p, size_t elem, int ncomp, int value, int lev_lo, int lev_hi) {
+  if (lev_hi < lev_lo) return;
+  uint8_t* b = static_cast<uint8_t*>(p);
+  for (int m = 0; m < ncomp; ++m) {
+    const size_t cbase = (size_t)m * g_.total_cells;
+    if (!windows_) {
+      const long c0 = g_.cell_off[lev_lo], c1 = g_.cell_off[lev_hi + 1];
+      AF_CUDA(cudaMemsetAsync(b + (cbase + c0) * elem, value, (c1 - c0) * elem, stream_));
+      continue;
+    }
+    for (int l = lev_lo; l <= lev_hi; ++l)
+      for (const auto& c : win_[l])
+        AF_CUDA(cudaMemsetAsync(b + (cbase + c.first) * elem, value, (c.second - c.first) * elem,
+                                stream_));
+  }
+}
+
+// copy of a per-cell array to a full-size host buffer (windows only; the
+// rest of dst is left as it is)
+void MR::wtohost_(void* dst, const void* src, size_t elem, int ncomp) {
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  if (!windows_) {
+    AF_CUDA(cudaMemcpyAsync(d, s, elem * ncomp * (size_t)g_.total_cells, cudaMemcpyDeviceToHost,
+                            stream_));
+  } else {
+    for (int m = 0; m < ncomp; ++m)
+      for (int l = 0; l <= L_; ++l)
+        for (const auto& c : win_[l]) {
+          const size_t o = ((size_t)m * g_.total_cells + c.first) * elem;
+          AF_CUDA(cudaMemcpyAsync(d + o, s + o, (c.second - c.first) * elem,
+                                  cudaMemcpyDeviceToHost, stream_));
+        }
+  }
+  AF_CUDA(cudaStreamSynchronize(stream_));
 }
 
 // In-place reduction of k unsigned 64-bit values over the ranks (max / sum /

@@ -289,6 +289,7 @@ __device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, 
     const long comp = g.total_cells;
     const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
     const int bcx = g.bc[0], bcy = g.bc[2], bcz = g.bc[4];
+    if (!tiles && g.dist && !row_in_region(g, l, mr_row(D, l, c))) return;  // dense: own rows
     if (st[off + c] != ST_ABSENT) return;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
     if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
@@ -787,6 +788,7 @@ __global__ void mr_norm_kernel(const double* V, MRLevels g, unsigned long long* 
   for (int m = 0; m < NC; ++m) mx[m] = 0.0;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
+    if (g.dist && !row_owned(g, g.L, mr_row(D, g.L, c))) continue;  // max over ranks after
 #pragma unroll
     for (int m = 0; m < NC; ++m) mx[m] = fmax(mx[m], fabs(V[m * comp + off + c]));
   }

@@ -504,8 +504,9 @@ __global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* re
   const long cells = mr_cells(D, l), off = g.cell_off[l];
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
+    if (!row_owned(g, l, mr_row(D, l, c))) continue;  // registers live with their owner
     unsigned mask = 0;
-    if (st[off + c] == ST_LEAF && row_owned(g, l, mr_row(D, l, c))) {
+    if (st[off + c] == ST_LEAF) {
       const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
       for (int ax = 0; ax < D; ++ax)
         for (int side = 0; side < 2; ++side) {
@@ -538,6 +539,7 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
   const int nsub = D == 3 ? 4 : 2;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
+    if (!row_owned(g, l, mr_row(D, l, c))) continue;
     const unsigned mask = regmask[off + c];
     if (!mask) continue;
     const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};

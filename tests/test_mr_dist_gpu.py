@@ -49,7 +49,14 @@ CASES_LT = [
     (2, 25, 5, 8, 2, dict(local_time=True, min_leaf=0)),                       # 3D
     (3, 26, 5, 8, 3, dict(local_time=True, min_leaf=1, eps_level=eps_levels(1e-3, 5, 3))),
 ]
-CASES = CASES + CASES_LT
+# large enough that every rank's windowed arrays leave unmapped memory at the
+# finest levels: an access outside a window would fault
+CASES_WIN = [
+    (0, 31, 10, 4, 4, dict(eps_level=eps_levels(1e-3, 10, 2))),                # cfg2 rule, L=10
+    (1, 32, 9, 4, 3, dict(local_time=True, min_leaf=0)),                       # MRLT
+    (2, 33, 7, 2, 4, dict(min_leaf=3)),                                        # 3D
+]
+CASES = CASES + CASES_LT + CASES_WIN
 
 
 @pytest.mark.parametrize("kind,seed,level,steps,ranks,kw", CASES,

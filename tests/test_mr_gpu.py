@@ -73,6 +73,7 @@ CASES_GLOBAL = [
     (2, 7, 4, 6, dict(eps=1e-3, cfl=0.4)),
     (3, 8, 5, 4, dict(eps=1e-3, cfl=0.4, eps_level=eps_levels(1e-3, 5, 3), min_leaf=2)),
     (0, 31, 7, 20, dict(eps=1e-3, flux=1, min_leaf=3)),                        # AUSMDV
+    (0, 33, 7, 3, dict(eps=2e-2, min_leaf=2)),       # heavy coarsening: to_uniform's far field
     (3, 32, 5, 4, dict(eps=1e-3, cfl=0.4, flux=1, limiter=0)),
 ]
 
