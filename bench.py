@@ -39,11 +39,18 @@ WORKLOADS = {
     "cfg2": (1, 0, 2, 10, 0.5, 1, 500),
     "cfg3": (2, 1, 2, 13, 0.5, 1, 64),
     "cfg4": (3, 2, 3, 9, 0.4, 1, 100),
+    # 3D MRLT at 1024^3 is an 8-GPU config (one rank's windowed share is ~1/5 of
+    # the ~217 GB tree); --level runs it smaller
+    "cfg5": (4, 3, 3, 10, 0.4, 1, 16),
 }
+BASE_LEVEL = {k: v[3] for k, v in WORKLOADS.items()}
 # MR options per MR workload (BASELINE.json configs[1], configs[2])
 MR_OPTS = {
     "cfg2": dict(eps=1e-3, eps_scaled=True, min_leaf=3, local_time=False, gap=3),
     "cfg3": dict(eps=1e-3, eps_scaled=False, min_leaf=0, local_time=True, gap=3),
+    # coarsest 16^3 = min leaf level 4 with gap = L - 4 (the gap
+    # of 3 would otherwise force leaves to level >= 7)
+    "cfg5": dict(eps=1e-3, eps_scaled=True, min_leaf=4, local_time=True, gap=6),
 }
 
 
@@ -150,7 +157,7 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
         # The reference's from_uniform + coarsen (its recursive predictions)
         # takes minutes at L >= 8 for cfg2's level thresholds, so the bounded
         # sample uses L=7 (cfg2) / L=8 (cfg3); the timed loop excludes the build.
-        lvl = {"cfg2": 7, "cfg3": 8}[workload]
+        lvl = {"cfg2": 7, "cfg3": 8, "cfg5": 5}[workload]
     else:
         lvl = 7 if dim == 3 else level
     init = O.case_fill(case, seed, lvl)
@@ -245,6 +252,8 @@ def workload_config(workload, n_gpus):
          "l2": "inputs larger than L2 (no flush)" if (n ** dim) * 40 > 126e6
                else "working set fits in L2 (latency-bound config)",
          "parity_mode": "bit-exact (--fmad=false)"}
+    if BASE_LEVEL.get(workload, level) != level:
+        c["level_override"] = f"finest level {level} instead of the config's {BASE_LEVEL[workload]}"
     if workload in MR_OPTS:
         o = MR_OPTS[workload]
         c.update({"method": "MRLT" if o["local_time"] else "MR (global dt)",
@@ -266,6 +275,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--level", type=int, default=None,
+                    help="run the workload at another finest level (not the config's own)")
     ap.add_argument("--mr-multi", default="auto", choices=["auto", "slabs", "replicas"],
                     help="MR at N>1: slab decomposition or independent replicas "
                          "(auto: replicas for the single-GPU cfg2, slabs otherwise)")
@@ -275,6 +286,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if args.level is not None:
+        w = list(WORKLOADS[args.workload])
+        w[3] = args.level
+        WORKLOADS[args.workload] = tuple(w)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
