@@ -637,8 +637,16 @@ void MR::build(const double* aos) {
   max_cfl_ = 0.0;
   fallbacks_ = 0;
   max_wave_ = 0.0;
+  const bool timing = std::getenv("AF_MR_TIMING") && std::getenv("AF_MR_TIMING")[0] == '2';
+  auto now_ms = [&] {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    return 1e3 * std::chrono::duration<double>(
+                     std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = timing ? now_ms() : 0.0;
   coarsen();
   build_lists_();
+  if (timing) std::fprintf(stderr, "build: initial coarsen + lists %.3f ms\n", now_ms() - t0);
 }
 
 void MR::refine(int top) {
