@@ -224,7 +224,6 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     for (int m = 0; m < NC; ++m)
       pr[m * K::HP + idx] = m == 0 ? w.rho : (m == NC - 1 ? w.p : w.v[m - 1]);
   }
-  // Pass-1 checks of this thread's leaf (mr_solver.cpp:171-178).
   // early loads for the update phase (step-start values, neighbour status):
   // issued before the flux work so their latency is hidden behind it
   double base0[NC];
@@ -250,18 +249,6 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         nbst |= (unsigned)a.st[off + mr_idx(D, n, p[0], p[1], p[2])] << (2 * (ax * 2 + side));
       }
   }
-  if (is_leaf) {
-    Cons<D> q;
-    q.rho = a.eval[own];
-#pragma unroll
-    for (int d = 0; d < D; ++d) q.m[d] = a.eval[(1 + d) * comp + own];
-    q.E = a.eval[(D + 1) * comp + own];
-    const Prim<D> w = primitives(q, gm1);
-    if (!cell_ok(q, w)) bad = 1;
-    double s, m;
-    wave_speeds(w, gamma, s, m);
-    wave = fmax(wave, m);
-  }
   __syncthreads();
   auto P = [&](int ix, int iy, int iz) {
     const int idx = (iz * K::HY + iy) * K::HX + ix;
@@ -272,6 +259,18 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     w.p = pr[(NC - 1) * K::HP + idx];
     return w;
   };
+  // Pass-1 checks of this thread's leaf (mr_solver.cpp:171-178) on the
+  // primitives the gather staged (a leaf is never a flipped ghost or an
+  // interpolated virtual cell, so they are primitives(q) of its own q)
+  if (is_leaf) {
+    const Prim<D> w = P(tx + 2, ty + 2, D == 3 ? tz + 2 : 0);
+    Cons<D> q;
+    q.rho = w.rho;
+    if (!cell_ok(q, w)) bad = 1;
+    double s, m;
+    wave_speeds(w, gamma, s, m);
+    wave = fmax(wave, m);
+  }
   auto leaf_at = [&](int x, int y, int z) {  // tile-local coords, -1/T allowed
     if (x < 0 || x >= TX || y < 0 || y >= TY || z < 0 || z >= TZ) return false;
     return leaf[(z * TY + y) * TX + x] != 0;
