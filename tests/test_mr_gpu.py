@@ -161,3 +161,21 @@ def test_mr_sweep_skip_is_sound(gpu_lib, monkeypatch, kind, seed, level, steps, 
     full = gpu_mr(kind, seed, level, steps, **kw)
     assert np.array_equal(base[2], full[2])
     assert np.array_equal(bits(base[1]), bits(full[1]))
+
+
+EDGE = [
+    (0, 61, 2, 6, dict(eps=1e-3)),                         # the smallest tree (4x4)
+    (2, 62, 2, 4, dict(eps=1e-3, cfl=0.4)),                # 3D 4^3
+    (0, 63, 6, 6, dict(eps=10.0, min_leaf=2)),             # everything coarsens to min_leaf
+    (0, 64, 5, 8, dict(eps=0.0, local_time=True)),         # full tree under MRLT
+    (1, 65, 6, 6, dict(eps=1e-3, min_leaf=6)),             # min_leaf = L: a uniform leaf set
+]
+
+
+@pytest.mark.parametrize("kind,seed,level,steps,kw", EDGE,
+                         ids=[f"edge{i}" for i in range(len(EDGE))])
+def test_mr_edge_cases_match_reference(gpu_lib, oracle, kind, seed, level, steps, kw):
+    if not oracle.available("ref"):
+        pytest.skip("reference build not present")
+    init, out, keys, rep = gpu_mr(kind, seed, level, steps, **kw)
+    compare(init, out, keys, rep, ref_mr(oracle, init, kind, level, steps, **kw))
