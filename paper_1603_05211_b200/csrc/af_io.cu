@@ -233,6 +233,7 @@ void l1_error(int dim, int level, double extent, const double* sol, int ref_leve
 // MRTree::dump (mr_tree.cpp:623-641): every node in ascending key order,
 // "level i j k status rho mom0 mom1 mom2 rhoE" with 17 significant digits.
 std::string MR::dump() {
+  refresh_coarse_();
   std::vector<uint8_t> hs(g_.total_cells);
   std::vector<double> hv((size_t)NC_ * g_.total_cells);
   wtohost_(hs.data(), d_st_, 1, 1);

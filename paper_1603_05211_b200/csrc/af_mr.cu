@@ -504,6 +504,13 @@ void MR::predict_fill_(int lo, int hi, int from) {
 
 // project_range (mr_solver.cpp:268-282): internals of levels [lo, top-1], finest first.
 void MR::project_range_(int lo, int top) {
+  // Internal values below min_leaf-1 are read by nothing on the cycle path
+  // (details from min_leaf-1 up feed refine; merges start at min_leaf);
+  // to_uniform and dump bring them up to date on demand (refresh_coarse_).
+  if (lo < min_leaf_ - 1) {
+    lo = min_leaf_ - 1;
+    coarse_stale_ = true;
+  }
   const int hi = std::min(top - 1, L_ - 1);
   if (g_.dist) {
     // owned rows of the split levels, then the halo rows (leaf values the
@@ -656,8 +663,8 @@ void MR::refine(int top) {
   wset_(d_flag2_, 1, 1, 0, 0, L_);
   // details with the refine flags of their leaf children (one launch)
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
-  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
-                 d_norms_, d_flag_);
+  AF_ML_LAUNCH_M(mr_detail_level, std::max(0, min_leaf_ - 1), L_ - 2, false, 1 << D_, d_V_,
+                 d_st_, d_det_, g_, AF_L, d_norms_, d_flag_);
   uint8_t* split = d_flag_;
   if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
     for (int l = 1; l <= L_ - 1; ++l) {
@@ -1357,8 +1364,8 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
   wset_(d_flag_, 1, 1, 0, 0, L_);
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
-  AF_ML_LAUNCH_M(mr_detail_level, 0, L_ - 2, false, 1 << D_, d_V_, d_st_, d_det_, g_, AF_L,
-                 d_norms_, d_flag_);
+  AF_ML_LAUNCH_M(mr_detail_level, std::max(0, min_leaf_ - 1), L_ - 2, false, 1 << D_, d_V_,
+                 d_st_, d_det_, g_, AF_L, d_norms_, d_flag_);
   AF_ML_LAUNCH(mr_apply_split_level, 1, L_ - 1, false, d_st_, d_flag_, g_, AF_L, d_flagi_);
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
   long b0 = launches_;
@@ -1707,9 +1714,20 @@ long MR::leaf_keys(uint64_t* keys, long cap) {
   return (long)out.size();
 }
 
+// The projections project_range_ skipped (levels below min_leaf-1), finest first.
+void MR::refresh_coarse_() {
+  if (!coarse_stale_) return;
+  if (!lists_valid_) build_lists_();
+  for (int l = std::min(min_leaf_ - 2, L_ - 1); l >= 0; --l)
+    if (AF_HAS(band_count_[l]))
+      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+  coarse_stale_ = false;
+}
+
 // With ranks, only this rank's rows (af_mr_local_rows) are written.
 void MR::to_uniform(int level, double* aos) {
   if (level < 0 || level > L_) throw Error(AF_E_LEVEL_MISMATCH, "to_uniform: bad level");
+  if (level < min_leaf_ - 1) refresh_coarse_();
   const long rowlen = D_ == 3 ? 1L << (2 * level) : 1L << level;
   int r0 = 0, r1 = 1 << level;
   if (dist_) local_rows(level, &r0, &r1);

@@ -216,6 +216,8 @@ class MR {
   std::vector<int> tile_count_;  // leaf tiles per level
   std::vector<int> band_count_;  // band tiles per level
   bool fresh_ = false;
+  bool coarse_stale_ = false;  // internal values below min_leaf-1 not projected (refresh_coarse_)
+  void refresh_coarse_();
   bool lists_valid_ = false;
   double phase_s_[4] = {0, 0, 0, 0};
   double phase_t0_ = 0.0;
