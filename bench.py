@@ -505,10 +505,16 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
 
     # ---- device-resident throughput ------------------------------------------
     solver.build(init_dev)
-    if args.warmup:
-        solver.run(args.warmup, cfl=cfl)        # W untimed warm-up cycles
-    l0 = solver.kernel_launches()
+    # W untimed warm-up cycles. The solver keeps one cycle graph per profiling
+    # mode (the timed run records stage events, the e2e run does not), so the
+    # warm-up instantiates both: W-1 cycles unprofiled, then one profiled.
+    if args.warmup > 1:
+        solver.run(args.warmup - 1, cfl=cfl)
     solver.profile(True)
+    if args.warmup:
+        solver.run(1, cfl=cfl)
+    l0 = solver.kernel_launches()
+    solver.profile(True)                        # resets the stage statistics
     sampler = ClockSampler(local)
     barrier()
     sampler.start()

@@ -141,7 +141,7 @@ static int build_primitives(const afo_block* b, double gamma, afo_prim* w, doubl
 }
 
 /* step.cpp:57-89 accumulate_rhs */
-static void accumulate_rhs(const afo_block* e, const afo_prim* w, double dx, int limiter,
+static void accumulate_rhs(const afo_block* e, const afo_prim* w, double dx, int limiter, int flux,
                            double gamma, afo_state* rhs, long* fallbacks) {
   const double inv_dx = 1.0 / dx;
   memset(rhs, 0, sizeof(afo_state) * (size_t)e->total);
@@ -157,11 +157,11 @@ static void accumulate_rhs(const afo_block* e, const afo_prim* w, double dx, int
         const long base = blk_index(e, c[0], c[1], c[2]);
         for (int f = 0; f <= e->n[axis]; ++f) {
           const long cell = base + (long)f * s;
-          const afo_state flux =
+          const afo_state fx =
               afo_face_flux_w(&q[cell - s], &q[cell], &w[cell - 2 * s], &w[cell - s],
-                              &w[cell], &w[cell + s], axis, limiter, gamma, fallbacks);
+                              &w[cell], &w[cell + s], axis, limiter, flux, gamma, fallbacks);
           for (int m = 0; m < 5; ++m) {
-            const double fm = flux.v[m] * inv_dx;
+            const double fm = fx.v[m] * inv_dx;
             if (f > 0) rhs[cell - s].v[m] -= fm;
             if (f < e->n[axis]) rhs[cell].v[m] += fm;
           }
@@ -172,10 +172,10 @@ static void accumulate_rhs(const afo_block* e, const afo_prim* w, double dx, int
 
 /* step.cpp:93-109 rk2_stage */
 static int rk2_stage(const afo_block* base, const afo_block* eval, afo_block* out, double dx,
-                     double stage_dt, int limiter, double gamma, afo_prim* w, afo_state* rhs,
+                     double stage_dt, int limiter, int flux, double gamma, afo_prim* w, afo_state* rhs,
                      double* max_speed, long* fallbacks, char* err, size_t errlen) {
   if (build_primitives(eval, gamma, w, max_speed, err, errlen)) return 1;
-  accumulate_rhs(eval, w, dx, limiter, gamma, rhs, fallbacks);
+  accumulate_rhs(eval, w, dx, limiter, flux, gamma, rhs, fallbacks);
   for (int k = 0; k < base->n[2]; ++k)
     for (int j = 0; j < base->n[1]; ++j)
       for (int i = 0; i < base->n[0]; ++i) {
@@ -197,9 +197,9 @@ static double now_s(void) {
 int afo_uniform_run(const af_oracle_params* p, const double* init, double* out,
                     double* dt_hist, af_oracle_result* res) {
   memset(res, 0, sizeof(*res));
-  if (p->flux != 0) {
+  if (p->integrator != 0) {
     res->err_kind = 9;
-    snprintf(res->err, sizeof res->err, "oracle: only AUSM+ is restated");
+    snprintf(res->err, sizeof res->err, "oracle: only the RK2 integrator is restated");
     return 9;
   }
   const int n = 1 << p->level;
@@ -236,11 +236,11 @@ int afo_uniform_run(const af_oracle_params* p, const double* init, double* out,
     memcpy(mid.d, u.d, sizeof(afo_state) * (size_t)u.total);
     double s1 = 0.0, s2 = 0.0;
     long fb = 0;
-    int bad = rk2_stage(&u, &u, &mid, dx, 0.5 * dt, p->limiter, p->gamma, w, rhs, &s1, &fb, err,
+    int bad = rk2_stage(&u, &u, &mid, dx, 0.5 * dt, p->limiter, p->flux, p->gamma, w, rhs, &s1, &fb, err,
                         sizeof err);
     if (!bad) {
       fill_ghosts(&mid, p->bc);
-      bad = rk2_stage(&u, &mid, &u, dx, dt, p->limiter, p->gamma, w, rhs, &s2, &fb, err,
+      bad = rk2_stage(&u, &mid, &u, dx, dt, p->limiter, p->flux, p->gamma, w, rhs, &s2, &fb, err,
                       sizeof err);
     }
     if (bad) {

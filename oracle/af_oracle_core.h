@@ -139,19 +139,78 @@ static inline afo_state afo_ausm_plus_w(const afo_state* ql, const afo_prim* wl,
   return f;
 }
 
-/* scheme.cpp:155-167 face_flux_w (AUSM+ only) */
+/* scheme.cpp:96-153 ausmdv_w: AUSMD/AUSMV blend with switch 10. std::max(a, b)
+ * is (a < b ? b : a) and std::min(a, b) is (b < a ? b : a). */
+static inline afo_state afo_ausmdv_w(const afo_state* ql, const afo_prim* wl, const afo_state* qr,
+                                     const afo_prim* wr, int axis, double gamma) {
+  const double ul = wl->v[axis];
+  const double ur = wr->v[axis];
+  const double sl = afo_sound_speed(wl, gamma), sr = afo_sound_speed(wr, gamma);
+  const double am = sl < sr ? sr : sl;
+  const double pol = wl->p / wl->rho;
+  const double por = wr->p / wr->rho;
+  const double alpha_l = 2.0 * pol / (pol + por);
+  const double alpha_r = 2.0 * por / (pol + por);
+  double u_plus, u_minus, p_plus, p_minus;
+  if (fabs(ul) <= am) {
+    const double t = (ul + am) / (2.0 * am);
+    u_plus = alpha_l * ((ul + am) * (ul + am) / (4.0 * am) - 0.5 * (ul + fabs(ul))) +
+             0.5 * (ul + fabs(ul));
+    p_plus = wl->p * t * t * (2.0 - ul / am);
+  } else {
+    u_plus = 0.5 * (ul + fabs(ul));
+    p_plus = ul > 0.0 ? wl->p : 0.0;
+  }
+  if (fabs(ur) <= am) {
+    const double t = (ur - am) / (2.0 * am);
+    u_minus = alpha_r * (-(ur - am) * (ur - am) / (4.0 * am) - 0.5 * (ur - fabs(ur))) +
+              0.5 * (ur - fabs(ur));
+    p_minus = wr->p * t * t * (2.0 + ur / am);
+  } else {
+    u_minus = 0.5 * (ur - fabs(ur));
+    p_minus = ur < 0.0 ? wr->p : 0.0;
+  }
+  const double mdot = u_plus * wl->rho + u_minus * wr->rho;
+  const double p_half = p_plus + p_minus;
+  const double pmin = wr->p < wl->p ? wr->p : wl->p;
+  const double sw = 10.0 * fabs(wr->p - wl->p) / pmin;
+  const double s = 0.5 * (sw < 1.0 ? sw : 1.0);
+  const double mom_v = u_plus * ql->v[1 + axis] + u_minus * qr->v[1 + axis];
+  const double mom_d = 0.5 * (mdot * (ul + ur) - fabs(mdot) * (ur - ul));
+  const double mom_n = (0.5 + s) * mom_v + (0.5 - s) * mom_d;
+  const double hl = (ql->v[4] + wl->p) / wl->rho;
+  const double hr = (qr->v[4] + wr->p) / wr->rho;
+  afo_state f;
+  f.v[0] = mdot;
+  for (int a = 0; a < 3; ++a)
+    f.v[1 + a] = 0.5 * (mdot * (wl->v[a] + wr->v[a]) - fabs(mdot) * (wr->v[a] - wl->v[a]));
+  f.v[1 + axis] = mom_n + p_half;
+  f.v[4] = 0.5 * (mdot * (hl + hr) - fabs(mdot) * (hr - hl));
+  return f;
+}
+
+/* scheme.cpp numerical_flux_w dispatch; flux 0 AUSM+, 1 AUSMDV (scheme.hpp:16) */
+static inline afo_state afo_num_flux_w(int flux, const afo_state* ql, const afo_prim* wl,
+                                       const afo_state* qr, const afo_prim* wr, int axis,
+                                       double gamma) {
+  return flux == 1 ? afo_ausmdv_w(ql, wl, qr, wr, axis, gamma)
+                   : afo_ausm_plus_w(ql, wl, qr, wr, axis, gamma);
+}
+
+/* scheme.cpp:155-167 face_flux_w */
 static inline afo_state afo_face_flux_w(const afo_state* q0, const afo_state* qp1,
                                         const afo_prim* wm1, const afo_prim* w0,
                                         const afo_prim* wp1, const afo_prim* wp2, int axis,
-                                        int limiter, double gamma, long* fallback_count) {
+                                        int limiter, int flux, double gamma,
+                                        long* fallback_count) {
   afo_prim l, r;
   if (afo_muscl_recon(wm1, w0, wp1, wp2, limiter, &l, &r)) {
     if (fallback_count) ++(*fallback_count);
-    return afo_ausm_plus_w(q0, w0, qp1, wp1, axis, gamma);
+    return afo_num_flux_w(flux, q0, w0, qp1, wp1, axis, gamma);
   }
   const afo_state ql = afo_conserved(&l, gamma);
   const afo_state qr = afo_conserved(&r, gamma);
-  return afo_ausm_plus_w(&ql, &l, &qr, &r, axis, gamma);
+  return afo_num_flux_w(flux, &ql, &l, &qr, &r, axis, gamma);
 }
 
 #endif /* AF_ORACLE_CORE_H */
