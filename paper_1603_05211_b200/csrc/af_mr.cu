@@ -449,13 +449,28 @@ double MR::eps_at_(int child_level) const {
 #define AF_TGRID(l, cnt) AF_TGRIDL(l, cnt, 1)
 #define AF_HAS(cnt) (fixed_grids_ || (cnt) > 0)
 
-// Cooperative launch of an all-levels kernel (grid-wide barrier per level).
-template <class K, class... A>
-static void coop_launch(K kern, int blocks, cudaStream_t s, A... args) {
-  void* argv[] = {static_cast<void*>(&args)...};
-  AF_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks),
-                                      dim3(256), argv, 0, s));
+// Cooperative launch of an all-levels kernel (grid-wide barrier per level),
+// with programmatic dependent launch like every other MR kernel.
+template <class... P, class... A>
+static void coop_launch(bool pdl, void (*kern)(P...), int blocks, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  AF_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
 }
+
+// Prefetch permissions of the next launch (kPreList | kPreSt, af_mr_types.h):
+// granted when the launch just before it in stream order writes neither
+// (v_only_at_ marks a value-only launch; any later launch revokes it).
+int MR::pre_() const { return launches_ == v_only_at_ ? (kPreList | kPreSt) : 0; }
 
 int MR::coop_blocks_() {
   if (coop_blocks_cache_ > 0) return coop_blocks_cache_;
@@ -487,18 +502,23 @@ void MR::predict_fill_(int lo, int hi, int from) {
   const int small = in_body_ ? -1 : small_hi_;
   if (f <= small) {
     const int to = std::min(small_hi_, L_);
+    const int pre = pre_();
     if (D_ == 3)
-      coop_launch(mr_predict_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm, g_,
-                  f, to, lo, hi, (const int*)d_band_);
+      coop_launch(pdl_, mr_predict_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm,
+                  g_, f, to, lo, hi, (const int*)d_band_, pre);
     else
-      coop_launch(mr_predict_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm, g_,
-                  f, to, lo, hi, (const int*)d_band_);
-    ++launches_;
+      coop_launch(pdl_, mr_predict_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm,
+                  g_, f, to, lo, hi, (const int*)d_band_, pre);
+    AF_CUDA(cudaGetLastError());
+    v_only_at_ = ++launches_;
   }
   for (int l = std::max(f, small + 1); l <= L_; ++l)
-    if (AF_HAS(band_count_[l]))
+    if (AF_HAS(band_count_[l])) {
+      const int pre = pre_();
       AF_MR_LAUNCH(mr_predict_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, vm, g_, l, lo, hi,
-                   AF_BAND(l));
+                   AF_BAND(l), pre);
+      v_only_at_ = launches_;
+    }
   fresh_ = (!virtuals_ || (lo == 0 && hi >= L_)) && from <= 1;
 }
 
@@ -519,27 +539,33 @@ void MR::project_range_(int lo, int top) {
     for (int l = hi; l >= std::max(lo, lp_); --l)
       if (AF_HAS(band_count_[l]))
         AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l,
-                     AF_BAND(l));
+                     AF_BAND(l), 0);
     exchange_(XV);
     for (int l = std::min(hi, lp_ - 1); l >= lo; --l)
       if (AF_HAS(band_count_[l]))
         AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l,
-                     AF_BAND(l));
+                     AF_BAND(l), 0);
     fresh_ = false;
     return;
   }
   for (int l = hi; l >= std::max(lo, small_hi_ + 1); --l)
-    if (AF_HAS(band_count_[l]))
-      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+    if (AF_HAS(band_count_[l])) {
+      const int pre = pre_();
+      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l),
+                   pre);
+      v_only_at_ = launches_;
+    }
   const int shi = std::min(hi, small_hi_);
   if (shi >= lo) {
+    const int pre = pre_();
     if (D_ == 3)
-      coop_launch(mr_project_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_, shi,
-                  lo, (const int*)d_band_);
+      coop_launch(pdl_, mr_project_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_,
+                  shi, lo, (const int*)d_band_, pre);
     else
-      coop_launch(mr_project_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_, shi,
-                  lo, (const int*)d_band_);
-    ++launches_;
+      coop_launch(pdl_, mr_project_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_,
+                  shi, lo, (const int*)d_band_, pre);
+    AF_CUDA(cudaGetLastError());
+    v_only_at_ = ++launches_;
   }
   fresh_ = false;
 }
@@ -887,6 +913,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   }
   AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
                stage == 2);
+  v_only_at_ = launches_;
 }
 
 // MRSolver::step_levels (mr_solver.cpp:232-316). `sub` is which of the
@@ -1143,10 +1170,10 @@ void MR::coarsen() {
     const int shi = std::min(L_ - 1, csm);
     if (shi >= min_leaf_) {
       if (D_ == 3)
-        coop_launch(mr_coarsen_small<3>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
+        coop_launch(pdl_, mr_coarsen_small<3>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
                     min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
       else
-        coop_launch(mr_coarsen_small<2>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
+        coop_launch(pdl_, mr_coarsen_small<2>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
                     min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
       ++launches_;
     }
@@ -1720,7 +1747,7 @@ void MR::refresh_coarse_() {
   if (!lists_valid_) build_lists_();
   for (int l = std::min(min_leaf_ - 2, L_ - 1); l >= 0; --l)
     if (AF_HAS(band_count_[l]))
-      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l));
+      AF_MR_LAUNCH(mr_project_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, g_, l, AF_BAND(l), 0);
   coarse_stale_ = false;
 }
 
@@ -1739,7 +1766,7 @@ void MR::to_uniform(int level, double* aos) {
   for (int l = std::max(1, min_leaf_ + 1); l <= level; ++l)
     AF_MR_LAUNCH(mr_predict_level, grid_for(mr_cells(D_, l)), d_V_, (const uint8_t*)d_st_,
                  (const uint8_t*)(virtuals_ ? d_mark_ : nullptr), g_, l, 0, L_, (const int*)nullptr,
-                 0);
+                 0, 0);
   fresh_ = false;
   double* tmp = nullptr;
   AF_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double) * 5 * cells, stream_));

@@ -62,6 +62,8 @@ class MR {
   int level_tiles_(int l) const { return g_.ntx[l] * g_.nty[l] * g_.ntz[l]; }
   void cycle_stats_(long* leaves, long* nodes, double* smax);
   int coop_blocks_cache_ = 0;
+  int pre_() const;       // prefetch permissions of the next launch (kPreList | kPreSt)
+  long v_only_at_ = -1;   // launches_ right after a launch that writes only values
   int small_hi_ = 0;
   bool pdl_ = true;             // programmatic dependent launches (AF_MR_NO_PDL turns off)
   bool full_sweeps_ = false;    // AF_MR_FULL_SWEEPS: never skip a coarsen sweep; check the skip test

@@ -126,39 +126,96 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
 // ------------------------------------------------------------ projection --
 // project_internals / project_range (mr_tree.cpp:319-338, mr_solver.cpp:268-282):
 // internal q = (sum over children, x-fastest child order) * (1/2^d).
+// One internal node's projection (s: its status).
+template <int D>
+__device__ __forceinline__ void project_cell(double* V, const MRLevels& g, int l, long c, uint8_t s) {
+  constexpr int NC = D + 2;
+  const int n = 1 << l, nf = n << 1;
+  const long foff = g.cell_off[l + 1];
+  const long comp = g.total_cells;
+  const double w = 1.0 / (double)(1 << D);
+  if (s != ST_INTERNAL || !row_owned(g, l, mr_row(D, l, c))) return;
+  const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+  double sm[NC];
+#pragma unroll
+  for (int m = 0; m < NC; ++m) sm[m] = 0.0;
+#pragma unroll
+  for (int ch = 0; ch < (1 << D); ++ch) {
+    const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                                  D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+#pragma unroll
+    for (int m = 0; m < NC; ++m) sm[m] = sm[m] + V[m * comp + fc];
+  }
+#pragma unroll
+  for (int m = 0; m < NC; ++m) V[m * comp + g.cell_off[l] + c] = sm[m] * w;
+}
+
 template <int D>
 __device__ __forceinline__ void project_level_dev(double* V, const uint8_t* st, const MRLevels& g, int l,
     const int* tiles, int ntiles) {
-  constexpr int NC = D + 2;
-  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
-    const int l = lv_;
-    const int n = 1 << l, nf = n << 1;
-    const long cells = mr_cells(D, l), fcells = mr_cells(D, l + 1);
-    const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-    const long comp = g.total_cells;
-    const double w = 1.0 / (double)(1 << D);
-    if (st[off + c] != ST_INTERNAL || !row_owned(g, l, mr_row(D, l, c))) return;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-    double s[NC];
-#pragma unroll
-    for (int m = 0; m < NC; ++m) s[m] = 0.0;
-#pragma unroll
-    for (int ch = 0; ch < (1 << D); ++ch) {
-      const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
-                                    D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
-#pragma unroll
-      for (int m = 0; m < NC; ++m) s[m] = s[m] + V[m * comp + fc];
-    }
-#pragma unroll
-    for (int m = 0; m < NC; ++m) V[m * comp + off + c] = s[m] * w;
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
+    project_cell<D>(V, g, lv, c, st[g.cell_off[lv] + c]);
   });
+}
+
+// Cell of this thread in entry `it` of a band/leaf tile range (tile_at
+// conventions), -1 when outside the level or past the range.
+template <int D>
+__device__ __forceinline__ long tile_cell(const MRLevels& g, int l, const int* tiles, int ntiles,
+                                          int it, int* lv) {
+  constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
+  const int tx = threadIdx.x % TX, ty = (threadIdx.x / TX) % TY;
+  const int tz = D == 3 ? threadIdx.x / (TX * TY) : 0;
+  const int t = tile_at(g, l, tiles, ntiles, it, lv);
+  const int n = 1 << *lv, ntx = g.ntx[*lv], nty = g.nty[*lv];
+  const int x = (t % ntx) * TX + tx, y = ((t / ntx) % nty) * TY + ty;
+  const int z = D == 3 ? (t / (ntx * nty)) * kTileZ3 + tz : 0;
+  return (x < n && y < n && (D == 2 || z < n)) ? mr_idx(D, n, x, y, z) : -1L;
+}
+
+// Band/leaf-tile cell iteration (tiles non-null) whose first tile lookup and
+// status load are issued before the PDL wait when `pre` allows (kPreList,
+// kPreSt): the dependent chain count -> tile -> status then overlaps the
+// predecessor kernel. Includes AF_PDL_ENTRY. f(level, cell, status).
+template <int D, class F>
+__device__ __forceinline__ void band_cells_pdl(const MRLevels& g, int l, const int* tiles,
+                                               int ntiles, const uint8_t* st, int pre, F&& f) {
+  int total = 0, lv0 = 0, s0 = -1;
+  long c0 = -1;
+  if (pre & kPreList) {
+    total = tile_total(g, l, ntiles);
+    if ((int)blockIdx.x < total) {
+      c0 = tile_cell<D>(g, l, tiles, ntiles, blockIdx.x, &lv0);
+      if ((pre & kPreSt) && c0 >= 0) s0 = st[g.cell_off[lv0] + c0];
+    }
+  }
+  AF_PDL_ENTRY();
+  if (!(pre & kPreList)) total = tile_total(g, l, ntiles);
+  for (int it = blockIdx.x; it < total; it += gridDim.x) {
+    int lv = lv0, s = -1;
+    long c;
+    if (it == (int)blockIdx.x && (pre & kPreList)) {
+      c = c0;
+      s = s0;
+    } else {
+      c = tile_cell<D>(g, l, tiles, ntiles, it, &lv);
+    }
+    if (c < 0) continue;
+    if (s < 0) s = st[g.cell_off[lv] + c];
+    f(lv, c, (uint8_t)s);
+  }
 }
 
 template <int D>
 __global__ void mr_project_level(double* V, const uint8_t* st, MRLevels g, int l,
-    const int* tiles = nullptr, int ntiles = 0) {
-  AF_PDL_ENTRY();
-  project_level_dev<D>(V, st, g, l, tiles, ntiles);
+    const int* tiles = nullptr, int ntiles = 0, int pre = 0) {
+  if (!tiles) {
+    AF_PDL_ENTRY();
+    project_level_dev<D>(V, st, g, l, tiles, ntiles);
+    return;
+  }
+  band_cells_pdl<D>(g, l, tiles, ntiles, st, pre,
+                    [&](int lv, long c, uint8_t s) { project_cell<D>(V, g, lv, c, s); });
 }
 
 // ------------------------------------------------------------ prediction --
@@ -276,37 +333,57 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
 // by add_virtual_leaves, mr_tree.cpp:513-551) keep their stored value unless
 // their parent level is in [lo, hi] — refresh_virtuals (mr_solver.cpp:195-208)
 // re-predicts only the virtual children of the stepping leaves.
+// One cell of predict_level_dev (s: its status; `dense`: a launch over the
+// whole level rather than band tiles).
+template <int D>
+__device__ __forceinline__ void predict_cell(double* V, const uint8_t* vmark, const MRLevels& g,
+                                             int l, long c, uint8_t s, int lo, int hi, bool dense) {
+  constexpr int NC = D + 2;
+  const int n = 1 << l, pn = n >> 1;
+  const long off = g.cell_off[l], poff = g.cell_off[l - 1];
+  const long comp = g.total_cells;
+  const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
+  if (dense && g.dist && !row_in_region(g, l, mr_row(D, l, c))) return;  // dense: own rows
+  if (s != ST_ABSENT) return;
+  const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+  if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
+  const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
+  double q[NC];
+  predict_child<D>(V, comp, poff, pn, g.bc[0], g.bc[2], g.bc[4], i >> 1, j >> 1, k >> 1, ch, q);
+#pragma unroll
+  for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
+}
+
+// Fills ABSENT cells of level l (l >= 1) with their prediction from level
+// l-1: value_at / predict_single for absent nodes (mr_tree.cpp:171-180,
+// 281-289). Virtual leaves (children of a leaf marked in `vmark`, materialised
+// by add_virtual_leaves, mr_tree.cpp:513-551) keep their stored value unless
+// their parent level is in [lo, hi] — refresh_virtuals (mr_solver.cpp:195-208)
+// re-predicts only the virtual children of the stepping leaves.
 template <int D>
 __device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, const uint8_t* vmark,
                                  const MRLevels& g, int l, int lo, int hi,
     const int* tiles, int ntiles) {
-  constexpr int NC = D + 2;
-  level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
-    const int l = lv_;
-    const int n = 1 << l, pn = n >> 1;
-    const long cells = mr_cells(D, l);
-    const long off = g.cell_off[l], poff = g.cell_off[l - 1];
-    const long comp = g.total_cells;
-    const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
-    const int bcx = g.bc[0], bcy = g.bc[2], bcz = g.bc[4];
-    if (!tiles && g.dist && !row_in_region(g, l, mr_row(D, l, c))) return;  // dense: own rows
-    if (st[off + c] != ST_ABSENT) return;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
-    if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
-    const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
-    double q[NC];
-    predict_child<D>(V, comp, poff, pn, bcx, bcy, bcz, i >> 1, j >> 1, k >> 1, ch, q);
-#pragma unroll
-    for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
+    // dense launches stay in this rank's rows (windowed arrays are unmapped
+    // elsewhere): the region test comes before the status load
+    if (!tiles && g.dist && !row_in_region(g, lv, mr_row(D, lv, c))) return;
+    predict_cell<D>(V, vmark, g, lv, c, st[g.cell_off[lv] + c], lo, hi, false);
   });
 }
 
 template <int D>
 __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vmark,
                                  MRLevels g, int l, int lo, int hi,
-    const int* tiles = nullptr, int ntiles = 0) {
-  AF_PDL_ENTRY();
-  predict_level_dev<D>(V, st, vmark, g, l, lo, hi, tiles, ntiles);
+    const int* tiles = nullptr, int ntiles = 0, int pre = 0) {
+  if (!tiles) {
+    AF_PDL_ENTRY();
+    predict_level_dev<D>(V, st, vmark, g, l, lo, hi, tiles, ntiles);
+    return;
+  }
+  band_cells_pdl<D>(g, l, tiles, ntiles, st, pre, [&](int lv, long c, uint8_t s) {
+    predict_cell<D>(V, vmark, g, lv, c, s, lo, hi, false);
+  });
 }
 
 // All levels in one cooperative launch (grid-wide barrier between levels):
@@ -661,25 +738,73 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
 // The coarse levels (a few tiles each) in one cooperative launch with a
 // grid-wide barrier between levels: their per-level work is shorter than a
 // kernel launch, and the level order (prediction coarsest-first, projection
-// and coarsening finest-first) is kept by the barrier.
+// and coarsening finest-first) is kept by the barrier. A level here has at
+// most gridDim.x band tiles, so a block holds one tile per level: every
+// level's tile lookup and status load are issued together up front (before
+// the PDL wait when `pre` allows), leaving the value loads to each level.
+constexpr int kSmallLevels = 16;
+
+template <int D>
+__device__ __forceinline__ long small_cell(const MRLevels& g, int l, const int* band) {
+  if ((int)blockIdx.x >= g.dcnt[l]) return -1;
+  int lv;
+  return tile_cell<D>(g, l, band + g.tile_off[l], -1, blockIdx.x, &lv);
+}
+
 template <int D>
 __global__ void mr_predict_small(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
-                                 int lfrom, int lto, int lo, int hi, const int* band) {
-  AF_PDL_ENTRY();
+                                 int lfrom, int lto, int lo, int hi, const int* band, int pre) {
   cg::grid_group grid = cg::this_grid();
-  for (int l = lfrom; l <= lto; ++l) {
-    predict_level_dev<D>(V, st, vmark, g, l, lo, hi, band + g.tile_off[l], -1);
+  long cs[kSmallLevels];
+  auto fetch = [&] {
+#pragma unroll
+    for (int i = 0; i < kSmallLevels; ++i) {
+      const int l = lfrom + i;
+      cs[i] = -1;
+      if (l <= lto) {
+        const long c = small_cell<D>(g, l, band);
+        if (c >= 0 && st[g.cell_off[l] + c] == ST_ABSENT) cs[i] = c;
+      }
+    }
+  };
+  const bool early = (pre & (kPreList | kPreSt)) == (kPreList | kPreSt);
+  if (early) fetch();
+  AF_PDL_ENTRY();
+  if (!early) fetch();
+#pragma unroll
+  for (int i = 0; i < kSmallLevels; ++i) {
+    const int l = lfrom + i;
+    if (l > lto) break;
+    if (cs[i] >= 0) predict_cell<D>(V, vmark, g, l, cs[i], ST_ABSENT, lo, hi, false);
     grid.sync();
   }
 }
 
 template <int D>
 __global__ void mr_project_small(double* V, const uint8_t* st, MRLevels g, int lhigh, int llow,
-                                 const int* band) {
-  AF_PDL_ENTRY();
+                                 const int* band, int pre) {
   cg::grid_group grid = cg::this_grid();
-  for (int l = lhigh; l >= llow; --l) {
-    project_level_dev<D>(V, st, g, l, band + g.tile_off[l], -1);
+  long cs[kSmallLevels];
+  auto fetch = [&] {
+#pragma unroll
+    for (int i = 0; i < kSmallLevels; ++i) {
+      const int l = lhigh - i;
+      cs[i] = -1;
+      if (l >= llow) {
+        const long c = small_cell<D>(g, l, band);
+        if (c >= 0 && st[g.cell_off[l] + c] == ST_INTERNAL) cs[i] = c;
+      }
+    }
+  };
+  const bool early = (pre & (kPreList | kPreSt)) == (kPreList | kPreSt);
+  if (early) fetch();
+  AF_PDL_ENTRY();
+  if (!early) fetch();
+#pragma unroll
+  for (int i = 0; i < kSmallLevels; ++i) {
+    const int l = lhigh - i;
+    if (l < llow) break;
+    if (cs[i] >= 0) project_cell<D>(V, g, l, cs[i], ST_INTERNAL);
     grid.sync();
   }
 }

@@ -72,6 +72,12 @@ __host__ __device__ __forceinline__ bool row_counted(const MRLevels& g, int l, i
 #define AF_PDL_ENTRY() \
   asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
 
+// What a kernel may read BEFORE its griddepcontrol.wait, i.e. while its
+// immediate predecessor still runs (every earlier kernel has completed: a
+// kernel lets its dependents launch only after its own wait). The host sets
+// the bits the predecessor does not write.
+enum : int { kPreList = 1, kPreSt = 2 };  // tile lists + counts, statuses
+
 constexpr int kTileX2 = 32, kTileY2 = 8;
 constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
 
