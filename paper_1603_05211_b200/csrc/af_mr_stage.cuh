@@ -98,16 +98,18 @@ __device__ __forceinline__ Cons<D> resolve_at(const double* V, long comp, const 
 
 template <int D, int AX, int LIM>
 __device__ __forceinline__ Cons<D> flux4(const Cons<D>& qa, const Cons<D>& qb, const Cons<D>& qc,
-                                         const Cons<D>& qd, double gamma, double gm1, int* fb) {
+                                         const Cons<D>& qd, double gamma, double gm1, int* fb,
+                                         double rgm1) {
   const Prim<D> wa = primitives(qa, gm1), wb = primitives(qb, gm1);
   const Prim<D> wc = primitives(qc, gm1), wd = primitives(qd, gm1);
-  return face_flux<D, AX, LIM>(qb, qc, wa, wb, wc, wd, gamma, gm1, fb);
+  return face_flux<D, AX, LIM>(qb, qc, wa, wb, wc, wd, gamma, gm1, fb, rgm1);
 }
 
 // fine_face_average (mr_solver.cpp:59-95) of leaf (c0,c1,c2) at level l.
 template <int D, int AX, int LIM>
 __device__ Cons<D> fine_face_average(const double* V, long comp, const MRLevels& g, int l,
-                                     const int* c, int dir, double gamma, double gm1, int* fb) {
+                                     const int* c, int dir, double gamma, double gm1, int* fb,
+                                     double rgm1) {
   constexpr int b1 = AX == 0 ? 1 : 0;
   constexpr int b2 = AX == 2 ? 1 : 2;
   const int fl = l + 1;
@@ -135,7 +137,7 @@ __device__ Cons<D> fine_face_average(const double* V, long comp, const MRLevels&
       const Cons<D> qb = resolve_at<D>(V, comp, g, fl, B[0], B[1], B[2]);
       const Cons<D> qc = resolve_at<D>(V, comp, g, fl, Cc[0], Cc[1], Cc[2]);
       const Cons<D> qd = resolve_at<D>(V, comp, g, fl, Dd[0], Dd[1], Dd[2]);
-      const Cons<D> f = flux4<D, AX, LIM>(qa, qb, qc, qd, gamma, gm1, fb);
+      const Cons<D> f = flux4<D, AX, LIM>(qa, qb, qc, qd, gamma, gm1, fb, rgm1);
       sum.rho = sum.rho + f.rho;
 #pragma unroll
       for (int a = 0; a < D; ++a) sum.m[a] = sum.m[a] + f.m[a];
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long comp = g.total_cells;
   const double gamma = a.gamma, gm1 = a.gm1;
+  const double rgm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rcp
   if (tid == 0) {
     s_fb = 0;
     s_bad = 0;
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     if (side) {
       const int c[3] = {x0 + (side > 0 ? fx - ex : fx), y0 + (side > 0 ? fy - ey : fy),
                         z0 + (side > 0 ? fz - ez : fz)};
-      F = fine_face_average<D, AX, LIM>(a.eval, comp, g, l, c, side, gamma, gm1, &fb);
+      F = fine_face_average<D, AX, LIM>(a.eval, comp, g, l, c, side, gamma, gm1, &fb, rgm1);
     } else {
       // stencil along AX in halo-box coordinates: cells fx-2 .. fx+1
       const int ix = fx + 2, iy = fy + 2, iz = D == 3 ? fz + 2 : 0;
@@ -322,8 +325,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         F = num_flux<D, AX, LIM>(cons_at(x0 + fx - ex, y0 + fy - ey, z0 + fz - ez), w0,
                                  cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
       } else {
-        const Cons<D> ql = conserved(lft, gm1), qr = conserved(rgt, gm1);
-        F = num_flux<D, AX, LIM>(ql, lft, qr, rgt, gamma);
+        F = recon_flux<D, AX, LIM>(lft, rgt, gamma, gm1, rgm1);
       }
     }
     fl[slot] = F.rho;

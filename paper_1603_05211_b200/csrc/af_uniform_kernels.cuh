@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   const int zc0 = g.zlo + blockIdx.y * a.zchunk;
   const int zc1 = min(zc0 + a.zchunk, g.zlo + g.nzl);
   const double gamma = a.gamma, gm1 = a.gm1, inv_dx = a.inv_dx;
+  const double rgm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rcp
   const double sdt = a.dt_scale * stage_dt_of(a);
   if (tid == 0) {
     s_fb = 0;
@@ -263,8 +264,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
       return num_flux<D, 2, LIM>(cons_at(x0 + tx, y0 + ty, gz - 1), w0,
                              cons_at(x0 + tx, y0 + ty, gz), wp1, gamma);
     }
-    const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-    return num_flux<D, 2, LIM>(ql, l, qr, r, gamma);
+    return recon_flux<D, 2, LIM>(l, r, gamma, gm1, rgm1);
   };
 
   // Prologue: planes zc0-2 .. zc0+1 and the chunk's first low z face; the
@@ -302,8 +302,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
             fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
-            const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-            fl = num_flux<D, 0, LIM>(ql, l, qr, r, gamma);
+            fl = recon_flux<D, 0, LIM>(l, r, gamma, gm1, rgm1);
           }
           fxs[0 * K::NXF + f] = fl.rho;
           fxs[1 * K::NXF + f] = fl.m[0];
@@ -325,8 +324,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
             fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
-            const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-            fl = num_flux<D, 1, LIM>(ql, l, qr, r, gamma);
+            fl = recon_flux<D, 1, LIM>(l, r, gamma, gm1, rgm1);
           }
           fys[0 * K::NYF + f] = fl.rho;
           fys[1 * K::NYF + f] = fl.m[0];
@@ -414,6 +412,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
   const int x0 = (blockIdx.x % tiles_x) * TX;
   const int y0 = g.zlo + (blockIdx.x / tiles_x) * TY;  // slab axis = y
   const double gamma = a.gamma, gm1 = a.gm1, inv_dx = a.inv_dx;
+  const double rgm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rcp
   const double sdt = a.dt_scale * stage_dt_of(a);
   if (tid == 0) {
     s_fb = 0;
@@ -495,8 +494,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
           fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
-          const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-          fl = num_flux<D, 0, LIM>(ql, l, qr, r, gamma);
+          fl = recon_flux<D, 0, LIM>(l, r, gamma, gm1, rgm1);
         }
         fxs[f] = fl.rho;
         fxs[K::NXF + f] = fl.m[0];
@@ -517,8 +515,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
           fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
-          const Cons<D> ql = conserved(l, gm1), qr = conserved(r, gm1);
-          fl = num_flux<D, 1, LIM>(ql, l, qr, r, gamma);
+          fl = recon_flux<D, 1, LIM>(l, r, gamma, gm1, rgm1);
         }
         fys[f] = fl.rho;
         fys[K::NYF + f] = fl.m[0];
