@@ -383,6 +383,9 @@ MR::~MR() {
     if (cg.graph) cudaGraphDestroy(cg.graph);
   }
   if (side_stream_) cudaStreamDestroy(side_stream_);
+  if (fork_stream_) cudaStreamDestroy(fork_stream_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   if (h_cycrec_) cudaFreeHost(h_cycrec_);
   if (h_small_) cudaFreeHost(h_small_);
   for (void* p : {(void*)d_ckV_, (void*)d_ckSt_, (void*)d_cycrec_, (void*)d_cycctl_, (void*)d_acc_})
@@ -1405,11 +1408,16 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   });
   *grade_body = launches_ - b0;
   build_lists_enqueue_();
+  // Fork: the prediction refresh (writes values of absent cells) runs beside
+  // add_virtual_leaves / counts / CFL speed / cycle record (statuses, marks,
+  // leaf values); both finish before the first stage.
+  AF_CUDA(cudaEventRecord(ev_fork_, stream_));
   predict_fill_(1, 0);
-  // add_virtual_leaves, leaf/node counts, CFL speed
+  cudaStream_t main = stream_;
+  stream_ = fork_stream_;
+  AF_CUDA(cudaStreamWaitEvent(stream_, ev_fork_, 0));
   wset_(d_mark_, 1, 1, 0, 0, L_);
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
-  virtuals_ = true;
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
   launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0, d_st_,
            d_mark_, g_.total_cells, d_red_, g_);
@@ -1420,6 +1428,10 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
                                        d_step3_, d_cycctl_, d_cycrec_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
+  AF_CUDA(cudaEventRecord(ev_join_, stream_));
+  stream_ = main;
+  AF_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+  virtuals_ = true;
   // the global step: dt and the step index come from mr_cycle_begin
   stage_records_.clear();
   cur_step_ = 0;
@@ -1473,6 +1485,9 @@ MR::CycleGraph& MR::cycle_graph_(double cfl, double fixed_dt) {
   }
   if (!side_stream_) {
     AF_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+    AF_CUDA(cudaStreamCreateWithFlags(&fork_stream_, cudaStreamNonBlocking));
+    AF_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    AF_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     AF_CUDA(cudaMalloc(&d_ckV_, sizeof(double) * NC_ * g_.total_cells));
     AF_CUDA(cudaMalloc(&d_ckSt_, g_.total_cells));
     AF_CUDA(cudaMalloc(&d_cycrec_, sizeof(af_mr_cycle) * kCycBatch));

@@ -113,6 +113,8 @@ class MR {
   };
   CycleGraph cyc_[2];
   cudaStream_t side_stream_ = nullptr;
+  cudaStream_t fork_stream_ = nullptr;      // cycle graph: work beside the prediction refresh
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool in_body_ = false;                    // capturing a WHILE body: no cooperative launches
   double* d_ckV_ = nullptr;                 // batch checkpoint (replay on failure)
   uint8_t* d_ckSt_ = nullptr;
