@@ -835,6 +835,11 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   }
   a.stage = stage;
   a.post_check = stage == 2;
+  // graph capture of a global step (a failing batch is replayed on the
+  // synchronous path, which commits through the guarded copy)
+  swap_ = cycle_capture_ && !opt_.local_time && !g_.dist && lo == 0 && hi >= L_ &&
+          std::getenv("AF_MR_NO_SWAP") == nullptr;
+  a.post_stops = swap_ ? 1 : 0;
   a.err = d_err_;
   a.lo = lo;
   a.hi = hi;
@@ -913,6 +918,14 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   if (profile_) {
     AF_CUDA(cudaEventRecordWithFlags(e1, stream_, fixed_grids_ ? cudaEventRecordExternal : 0));
     note_event_node_();
+  }
+  if (swap_) {
+    // The output buffer becomes the state: the projection and prediction that
+    // follow write every other cell a later stage reads (internal nodes, and
+    // the absent band cells), so no commit copy is needed. Two stages per
+    // global step swap back.
+    std::swap(d_V_, d_Vs_);
+    return;
   }
   AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
                stage == 2);
@@ -1503,9 +1516,12 @@ MR::CycleGraph& MR::cycle_graph_(double cfl, double fixed_dt) {
   ev_nodes_.clear();
   fixed_grids_ = true;
   AF_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  cycle_capture_ = true;
   try {
     enqueue_cycle_(cfl, fixed_dt, &gb, &sb);
+    cycle_capture_ = false;
   } catch (...) {
+    cycle_capture_ = false;
     fixed_grids_ = false;
     in_body_ = false;
     cudaGraph_t g = nullptr;

@@ -113,7 +113,9 @@ class MR {
   };
   CycleGraph cyc_[2];
   cudaStream_t side_stream_ = nullptr;
-  cudaStream_t fork_stream_ = nullptr;      // cycle graph: work beside the prediction refresh
+  cudaStream_t fork_stream_ = nullptr;
+  bool swap_ = false;
+  bool cycle_capture_ = false;              // capturing the whole-cycle graph (swap allowed)                       // stage_: output buffer becomes the state (no commit copy)      // cycle graph: work beside the prediction refresh
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   bool in_body_ = false;                    // capturing a WHILE body: no cooperative launches
   double* d_ckV_ = nullptr;                 // batch checkpoint (replay on failure)

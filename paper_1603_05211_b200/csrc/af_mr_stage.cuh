@@ -31,6 +31,7 @@ struct MRStageArgs {
   int step3;           // error code base: 3*step; + stage-1 for pass 1, + 2 for post-step
   int stage;
   int post_check;      // stage 2: positivity of the completed step
+  int post_stops;      // a post-step failure also stops later launches (graph mode, no commit kernel)
   unsigned long long* wave;  // per-level max (|v_a|+c) of the evaluated leaves
   unsigned long long* fb;    // fallbacks
   int* err;                  // [0] flag, [1] min code
@@ -487,6 +488,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       // stops the commit, so a pass-1 failure of a later level of the same
       // stage (which the reference reports first) is still detected
       atomicExch(a.err + ((s_bad & 1) ? 0 : 2), 1);
+      if (a.post_stops) atomicExch(a.err, 1);
       atomicMin(a.err + 1, step3 + ((s_bad & 1) ? a.stage - 1 : 2));
       atomicCAS(a.err + 3, 0, ((a.lo << 8) | a.hi) + 1);
     }
