@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         F = num_flux<D, AX, LIM>(cons_at(x0 + fx - ex, y0 + fy - ey, z0 + fz - ez), w0,
                                  cons_at(x0 + fx, y0 + fy, z0 + fz), wp1, gamma);
       } else {
-        F = recon_flux<D, AX, LIM>(lft, rgt, gamma, gm1, rgm1);
+        F = recon_flux_fast<D, AX, LIM>(lft, rgt, gamma, gm1, rgm1);
       }
     }
     fl[slot] = F.rho;

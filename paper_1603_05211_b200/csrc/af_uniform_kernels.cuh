@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
       return num_flux<D, 2, LIM>(cons_at(x0 + tx, y0 + ty, gz - 1), w0,
                              cons_at(x0 + tx, y0 + ty, gz), wp1, gamma);
     }
-    return recon_flux<D, 2, LIM>(l, r, gamma, gm1, rgm1);
+    return recon_flux_fast<D, 2, LIM>(l, r, gamma, gm1, rgm1);
   };
 
   // Prologue: planes zc0-2 .. zc0+1 and the chunk's first low z face; the
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
             fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
-            fl = recon_flux<D, 0, LIM>(l, r, gamma, gm1, rgm1);
+            fl = recon_flux_fast<D, 0, LIM>(l, r, gamma, gm1, rgm1);
           }
           fxs[0 * K::NXF + f] = fl.rho;
           fxs[1 * K::NXF + f] = fl.m[0];
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
             fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
-            fl = recon_flux<D, 1, LIM>(l, r, gamma, gm1, rgm1);
+            fl = recon_flux_fast<D, 1, LIM>(l, r, gamma, gm1, rgm1);
           }
           fys[0 * K::NYF + f] = fl.rho;
           fys[1 * K::NYF + f] = fl.m[0];
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
           fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
-          fl = recon_flux<D, 0, LIM>(l, r, gamma, gm1, rgm1);
+          fl = recon_flux_fast<D, 0, LIM>(l, r, gamma, gm1, rgm1);
         }
         fxs[f] = fl.rho;
         fxs[K::NXF + f] = fl.m[0];
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
           fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
-          fl = recon_flux<D, 1, LIM>(l, r, gamma, gm1, rgm1);
+          fl = recon_flux_fast<D, 1, LIM>(l, r, gamma, gm1, rgm1);
         }
         fys[f] = fl.rho;
         fys[K::NYF + f] = fl.m[0];
