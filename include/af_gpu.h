@@ -273,6 +273,15 @@ af_status af_l1_error(int dim, int level, double extent, const double* sol, int 
  * *len in = capacity of buf, out = bytes needed including the terminating 0. */
 af_status af_mr_dump(af_mr* m, char* buf, size_t* len);
 
+/* Self-check of the inline fast-path division and square root the face
+ * fluxes use (CUDA's fast-path sequences with their range tests; see
+ * DESIGN.md §3) against IEEE a/b and sqrt on n random operands with binary
+ * exponents in [emin, emax] (and [2 emin, 2 emax] for sqrt). out[0] division
+ * mismatches, out[1] divisions the range test sends to the IEEE path, out[2]
+ * and out[3] the same for sqrt. Not a reference entry point: diagnostics. */
+af_status af_check_division(long n, uint64_t seed, int emin, int emax,
+                            unsigned long long out[4]);
+
 #ifdef __cplusplus
 }
 #endif

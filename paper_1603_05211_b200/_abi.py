@@ -121,6 +121,8 @@ SIGNATURES = {
     "af_snapshot_read": (C.c_int, [C.c_char_p, C.POINTER(SnapshotHeader), _vp]),
     "af_restrict_to_level": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "af_l1_error": (C.c_int, [C.c_int, C.c_int, C.c_double, _vp, C.c_int, _vp, _dp]),
+    "af_check_division": (C.c_int, [C.c_long, C.c_uint64, C.c_int, C.c_int,
+                                    C.POINTER(C.c_ulonglong)]),
     "af_mr_dump": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_size_t)]),
 }
 

@@ -16,6 +16,7 @@
 
 #include "af_internal.h"
 #include "af_mr.h"
+#include "af_physics.cuh"
 
 namespace af {
 
@@ -274,4 +275,59 @@ std::string MR::dump() {
   return out;
 }
 
+// Self-check of the fast-path division and square root (af_physics.cuh fdiv /
+// fsqrt) against the IEEE operations on n random operand pairs whose binary
+// exponents lie in [emin, emax]: out = {division mismatches, divisions left
+// to the IEEE path, sqrt mismatches, sqrts left to the IEEE path}.
+namespace {
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ double rand_double(uint64_t& s, int emin, int emax) {
+  s = mix64(s);
+  const uint64_t m = s & ((1ull << 52) - 1);
+  const int e = emin + (int)((s >> 52) % (uint64_t)(emax - emin + 1));
+  uint64_t b = ((uint64_t)(e + 1023) << 52) | m;
+  if (mix64(s) & 1) b |= 1ull << 63;
+  return __longlong_as_double((long long)b);
+}
+__global__ void fastdiv_check_kernel(uint64_t seed, long n, int emin, int emax,
+                                     unsigned long long* out) {
+  unsigned long long c[4] = {0, 0, 0, 0};
+  uint64_t s = mix64(seed ^ (blockIdx.x * 0x100000001ull + threadIdx.x));
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    const double a = rand_double(s, emin, emax), b = rand_double(s, emin, emax);
+    bool ok = true;
+    const double q = fdiv(a, b, ok);
+    if (!ok) ++c[1];
+    else if (__double_as_longlong(q) != __double_as_longlong(a / b)) ++c[0];
+    const double x = fabs(rand_double(s, 2 * emin, 2 * emax));
+    bool ok2 = true;
+    const double r = fsqrt(x, ok2);
+    if (!ok2) ++c[3];
+    else if (__double_as_longlong(r) != __double_as_longlong(sqrt(x))) ++c[2];
+  }
+  for (int k = 0; k < 4; ++k)
+    if (c[k]) atomicAdd(out + k, c[k]);
+}
+}  // namespace
+
 }  // namespace af
+
+extern "C" af_status af_check_division(long n, uint64_t seed, int emin, int emax,
+                                       unsigned long long out[4]) {
+  if (!out || n < 0 || emin > emax || emin < -1022 || emax > 1023 || 2 * emin < -1022 ||
+      2 * emax > 1023)
+    return AF_E_ARGUMENT;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return AF_E_CUDA;
+  cudaMemset(d, 0, 4 * sizeof(unsigned long long));
+  af::fastdiv_check_kernel<<<148 * 8, 256>>>(seed, n, emin, emax, d);
+  const cudaError_t e = cudaMemcpy(out, d, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? AF_OK : AF_E_CUDA;
+}

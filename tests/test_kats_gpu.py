@@ -95,3 +95,16 @@ def test_details_vanish_on_linear_data(gpu_lib, dim, level):
         d = d[~np.isnan(d)]
         assert d.size and np.all(d == 0.0), (lv, d.max())
     s.close()
+
+
+@pytest.mark.parametrize("emin,emax", [(-4, 4), (-300, 300), (-511, 511)])
+def test_fast_division_matches_ieee(gpu_lib, emin, emax):
+    """The inline fast-path division/sqrt of the face fluxes (fdiv/fsqrt,
+    af_physics.cuh) equal IEEE a/b and sqrt wherever their range test lets
+    them through; inside [2^-300, 2^300] the test never fails."""
+    import ctypes as C
+    out = (C.c_ulonglong * 4)()
+    assert gpu_lib.af_check_division(1 << 27, 7 + emax, emin, emax, out) == 0
+    assert out[0] == 0 and out[2] == 0, list(out)
+    if emax <= 300:
+        assert out[1] == 0 and out[3] == 0, list(out)
