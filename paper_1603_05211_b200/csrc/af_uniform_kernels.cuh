@@ -169,6 +169,27 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   double ssum = 0.0;  // stage 2: max of sum_a(|v_a|+c) over the updated cells
   int bad = 0;
 
+  // This thread's halo-box cells (idx = tid + t*NT) and their x/y boundary
+  // mapping, which is the same on every plane: in-plane offset of the source
+  // cell, or -1 for corners (never on an axis stencil) and idx >= HP; the
+  // reflective momentum flips as bit 0 (x) and bit 1 (y).
+  constexpr int HPT = (K::HP + K::NT - 1) / K::NT;
+  int hoff[HPT];
+  unsigned hflip = 0;
+#pragma unroll
+  for (int t = 0; t < HPT; ++t) {
+    const int idx = tid + t * K::NT;
+    hoff[t] = -1;
+    if (idx >= K::HP) continue;
+    const int ix = idx % K::HX, iy = idx / K::HX;
+    const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
+    if (!cx && !cy) continue;
+    bool fx, fy;
+    const int mx = bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
+    const int my = bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
+    hoff[t] = my * n + mx;
+    hflip |= ((fx ? 1u : 0u) | (fy ? 2u : 0u)) << (2 * t);
+  }
   // Plane gz of eval -> primitives of ring slot gz&3, in two halves so the
   // global loads of plane k+3 overlap the flux work of plane k: issue_plane
   // starts cp.async copies of the conserved values of this thread's cells,
@@ -176,14 +197,11 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   auto issue_plane = [&](int gz) {
     bool fz;
     const int zl = slab_map(gz, g, 2, fz);
-    for (int idx = tid; idx < K::HP; idx += K::NT) {
-      const int ix = idx % K::HX, iy = idx / K::HX;
-      const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
-      if (!cx && !cy) continue;  // corner: never on an axis stencil
-      bool fx, fy;
-      const int mx = bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
-      const int my = bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
-      const long off = (long)zl * zs + (long)my * n + mx;
+#pragma unroll
+    for (int t = 0; t < HPT; ++t) {
+      if (hoff[t] < 0) continue;
+      const int idx = tid + t * K::NT;
+      const long off = (long)zl * zs + hoff[t];
 #pragma unroll
       for (int m = 0; m < 5; ++m) cp_async8(raw + m * K::HP + idx, ev + m * cs + off);
     }
@@ -195,13 +213,12 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     (void)slab_map(gz, g, 2, fz);
     double* dst = ring + ((gz + 4) & 3) * (K::NC * K::HP);
     const bool own = gz >= zc0 && gz < zc1;
-    for (int idx = tid; idx < K::HP; idx += K::NT) {
+#pragma unroll
+    for (int t = 0; t < HPT; ++t) {
+      if (hoff[t] < 0) continue;
+      const int idx = tid + t * K::NT;
       const int ix = idx % K::HX, iy = idx / K::HX;
       const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
-      if (!cx && !cy) continue;
-      bool fx, fy;
-      (void)bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
-      (void)bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
       Cons<D> q;
       q.rho = raw[idx];
       q.m[0] = raw[K::HP + idx];
@@ -215,8 +232,9 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
         wave_speeds(w, gamma, s, m);
         wave = fmax(wave, m);
       }
-      if (fx) w.v[0] = -w.v[0];
-      if (fy) w.v[1] = -w.v[1];
+      const unsigned fl = hflip >> (2 * t);
+      if (fl & 1u) w.v[0] = -w.v[0];
+      if (fl & 2u) w.v[1] = -w.v[1];
       if (fz) w.v[2] = -w.v[2];
       dst[0 * K::HP + idx] = w.rho;
       dst[1 * K::HP + idx] = w.v[0];
