@@ -463,6 +463,18 @@ __device__ __forceinline__ bool node_group_all(bool b) {
   return (m & gm) == gm;
 }
 
+// |d| / norm for the detail (d >= 0, norm > 0): exactly 0 for d == 0 (most
+// cells of piecewise-constant data), else the correctly rounded quotient on
+// the fast-path division (fdiv), with the IEEE division of the same nonzero
+// numerator when fdiv's range test fails. Neither path divides a zero.
+__device__ __forceinline__ double detail_ratio(double d, double norm) {
+  const double num = d == 0.0 ? 1.0 : d;
+  bool ok = true;
+  double q = fdiv(num, norm, ok);
+  if (!ok) asm("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"(num), "d"(norm));
+  return d == 0.0 ? 0.0 : q;
+}
+
 // MRTree::detail / detail_between (mr_tree.cpp:291-317) restricted to ONE child:
 // max over components of |q_child - prediction| / norm. The node's detail is
 // the max of this over its 2^d children (node_group_max); every term is >= 0,
@@ -484,7 +496,7 @@ __device__ __forceinline__ double child_detail(const double* V, long comp, const
     const double d = fabs(V[m * comp + fc] - pred[m]);
     // norms index: rho 0, mom 1..D, rhoE 4 (the 2D mom2 term is 0/global == 0)
     const int ni = m == NC - 1 ? 4 : m;
-    const double r = d == 0.0 ? 0.0 : d / norms[ni];
+    const double r = detail_ratio(d, norms[ni]);
     mag = mag > r ? mag : r;  // std::max(mag, r)
   }
   return mag;
