@@ -121,15 +121,19 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2) hancock_step(StageArgs a, UGrid
   const double* ev = a.eval;
   const long cs = g.cs, zs = g.zs;
   // element offset of global cell (x, y, z) and its reflective flips
+  // A slab whose height is not a multiple of TZ gets a last tile reaching
+  // past its two halo planes; those planes are never read by an owned cell's
+  // stencil, so they are clamped to the last stored plane (the slab is
+  // allocated with nzl + 4 planes) instead of addressed past the allocation.
   auto locate = [&](int x, int y, int z, bool* f) {
     f[0] = f[1] = f[2] = false;
     const int mx = bc_map(x, n, g.bc[0], g.bc[1], f[0]);
     if (D == 3) {
       const int my = bc_map(y, n, g.bc[2], g.bc[3], f[1]);
-      const int zl = slab_map(z, g, 2, f[2]);
+      const int zl = min(slab_map(z, g, 2, f[2]), g.nzl + 3);
       return (long)zl * zs + (long)my * n + mx;
     }
-    const int yl = slab_map(y, g, 1, f[1]);
+    const int yl = min(slab_map(y, g, 1, f[1]), g.nzl + 3);
     return (long)yl * zs + mx;
   };
   auto cons_at = [&](int x, int y, int z) {
