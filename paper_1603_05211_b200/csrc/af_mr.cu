@@ -28,7 +28,6 @@ namespace {
 
 constexpr int kGrid = 148 * 8;
 constexpr int kStageGrid = 148 * 2;  // stage kernel: 2 resident blocks per SM
-constexpr int kSmallTiles = 64;      // levels with at most this many tiles: cooperative launch
 
 inline unsigned grid_for(long n, int block = 256) {
   long b = (n + block - 1) / block;
@@ -256,17 +255,15 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   }
   tile_off_[L_ + 1] = toff;
   g_.tile_off[L_ + 1] = toff;
-  // AF_MR_SMALL: coarse levels with few tiles go through one cooperative
-  // launch with grid-wide barriers. Off by default: inside the cycle graph the
-  // per-level launches with programmatic dependent launch are faster (cfg2
-  // 0.415 -> 0.360 ms/cycle on B200).
+  // the coarsest levels (at most kTinyCells cells) run as one single-CTA
+  // launch (mr_*_tiny); with ranks every level is a launch of its own
   small_hi_ = -1;
-  if (std::getenv("AF_MR_SMALL"))
+  if (!std::getenv("AF_MR_NO_TINY"))
     for (int l = 0; l <= L_; ++l)
-      if ((long)g_.ntx[l] * g_.nty[l] * g_.ntz[l] <= kSmallTiles) small_hi_ = l;
-  small_coarsen_ = std::getenv("AF_MR_SMALL_COARSEN") != nullptr;
+      if (mr_cells(D_, l) <= kTinyCells) small_hi_ = l;
   full_sweeps_ = std::getenv("AF_MR_FULL_SWEEPS") != nullptr;
   pdl_ = std::getenv("AF_MR_NO_PDL") == nullptr;
+  phases_ = std::getenv("AF_MR_PHASES") != nullptr;
   // spatial decomposition: one slab of rows per rank from the partition level
   // lp_ up (levels below are replicated); one rank owns everything
   if (comm && comm->n > 1) {
@@ -377,6 +374,15 @@ MR::~MR() {
                  1e3 * phase_s_[1], 1e3 * phase_s_[2], 1e3 * phase_s_[3], evolve_gpu_ms_);
   cudaSetDevice(cfg_.device);
   if (own_stream_) cudaStreamSynchronize(own_stream_);
+  if (phase_n_ > 0) {
+    double tot = 0.0;
+    for (size_t i = 1; i < phase_ms_.size(); ++i) tot += phase_ms_[i];
+    std::fprintf(stderr, "AF_MR_PHASES: %ld cycles, %.1f us/cycle between the first and last mark\n",
+                 phase_n_, 1e3 * tot / phase_n_);
+    for (size_t i = 1; i < phase_ms_.size(); ++i)
+      std::fprintf(stderr, "  %-30s %8.1f us\n", phase_ev_[i].first, 1e3 * phase_ms_[i] / phase_n_);
+  }
+  for (auto& pe : phase_ev_) cudaEventDestroy(pe.second);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   dist_free_();
   for (GraphCache& gc : graphs_)
@@ -455,24 +461,6 @@ double MR::eps_at_(int child_level) const {
 #define AF_TGRID(l, cnt) AF_TGRIDL(l, cnt, 1)
 #define AF_HAS(cnt) (fixed_grids_ || (cnt) > 0)
 
-// Cooperative launch of an all-levels kernel (grid-wide barrier per level),
-// with programmatic dependent launch like every other MR kernel.
-template <class... P, class... A>
-static void coop_launch(bool pdl, void (*kern)(P...), int blocks, cudaStream_t s, A&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(256);
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 2 : 1;
-  AF_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
-}
-
 // Prefetch permissions of the next launch (kPreList | kPreSt, af_mr_types.h):
 // granted when the launch just before it in stream order writes neither
 // (v_only_at_ marks a value-only launch; any later launch revokes it).
@@ -481,25 +469,10 @@ int MR::pre_() const {
   return !off && launches_ == v_only_at_ ? (kPreList | kPreSt) : 0;
 }
 
-int MR::coop_blocks_() {
-  if (coop_blocks_cache_ > 0) return coop_blocks_cache_;
-  int dev = 0, sms = 0, nb1 = 0, nb2 = 0;
-  AF_CUDA(cudaGetDevice(&dev));
-  AF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (D_ == 3) {
-    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, mr_predict_all<3>, 256, 0));
-    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, mr_project_all<3>, 256, 0));
-  } else {
-    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, mr_predict_all<2>, 256, 0));
-    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, mr_project_all<2>, 256, 0));
-  }
-  coop_blocks_cache_ = sms * std::max(1, std::min({nb1, nb2, 4}));
-  return coop_blocks_cache_;
-}
-
-// Prediction refresh over the band tiles, coarsest level first (one launch
-// per level: the all-levels cooperative variant with grid-wide barriers,
-// mr_predict_all, measured slower on B200 for both cfg2 and cfg3).
+// Prediction refresh over the band tiles, coarsest level first: the tiny
+// levels in one single-CTA launch, then one launch per level. (Cooperative
+// launches with grid-wide barriers between levels were slower on B200 inside
+// the cycle graph than per-level launches with programmatic dependent launch.)
 // Only levels above `from` can hold stale predictions: a prediction at level
 // l reads level l-1 only, so after values of levels [lo, hi] change (stage
 // commit + projection) the refresh starts at lo+1.
@@ -508,16 +481,16 @@ void MR::predict_fill_(int lo, int hi, int from) {
   // adds): no absent cells there
   const int f = std::max({1, from, min_leaf_ + 1});
   const uint8_t* vm = virtuals_ ? d_mark_ : nullptr;
-  const int small = in_body_ ? -1 : small_hi_;
+  // dist_: the small levels of a rank are windowed, so every level is its own launch
+  const int small = dist_ ? -1 : small_hi_;
   if (f <= small) {
     const int to = std::min(small_hi_, L_);
-    const int pre = pre_();
     if (D_ == 3)
-      coop_launch(pdl_, mr_predict_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm,
-                  g_, f, to, lo, hi, (const int*)d_band_, pre);
+      launch_k(pdl_, stream_, mr_predict_tiny<3>, dim3(1), kTinyThreads, 0, d_V_,
+               (const uint8_t*)d_st_, vm, g_, f, to, lo, hi);
     else
-      coop_launch(pdl_, mr_predict_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, vm,
-                  g_, f, to, lo, hi, (const int*)d_band_, pre);
+      launch_k(pdl_, stream_, mr_predict_tiny<2>, dim3(1), kTinyThreads, 0, d_V_,
+               (const uint8_t*)d_st_, vm, g_, f, to, lo, hi);
     AF_CUDA(cudaGetLastError());
     v_only_at_ = ++launches_;
   }
@@ -566,13 +539,12 @@ void MR::project_range_(int lo, int top) {
     }
   const int shi = std::min(hi, small_hi_);
   if (shi >= lo) {
-    const int pre = pre_();
     if (D_ == 3)
-      coop_launch(pdl_, mr_project_small<3>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_,
-                  shi, lo, (const int*)d_band_, pre);
+      launch_k(pdl_, stream_, mr_project_tiny<3>, dim3(1), kTinyThreads, 0, d_V_,
+               (const uint8_t*)d_st_, g_, shi, lo);
     else
-      coop_launch(pdl_, mr_project_small<2>, kSmallTiles, stream_, d_V_, (const uint8_t*)d_st_, g_,
-                  shi, lo, (const int*)d_band_, pre);
+      launch_k(pdl_, stream_, mr_project_tiny<2>, dim3(1), kTinyThreads, 0, d_V_,
+               (const uint8_t*)d_st_, g_, shi, lo);
     AF_CUDA(cudaGetLastError());
     v_only_at_ = ++launches_;
   }
@@ -958,13 +930,19 @@ void MR::step_levels_(int lo, int hi, double t, double dt, int sub) {
   step_dt_ = dt;
   sub_ = sub;
   stage_(lo, top, t, 0.5 * dt, 1, cur_step_);
+  phase_("stage 1");
   project_range_(lo, top);
+  phase_("project 1");
   predict_fill_(lo, top, lo + 1);
+  phase_("predict 1");
   step_dt_ = dt;
   sub_ = sub;
   stage_(lo, top, t + 0.5 * dt, dt, 2, cur_step_);
+  phase_("stage 2");
   project_range_(lo, top);
+  phase_("project 2");
   predict_fill_(lo, top, lo + 1);
+  phase_("predict 2");
   for (size_t r = r0; r < stage_records_.size(); ++r) stage_records_[r].step_dt = dt;
   bool deeper = false;
   for (int l = top + 1; l <= L_; ++l) deeper = deeper || leaves_per_level_[l] > 0;
@@ -1181,23 +1159,12 @@ void MR::coarsen() {
   bool clean = false;  // the previous sweep raised no re-sweep flag
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
-    const int csm = small_coarsen_ ? small_hi_ : -1;
-    for (int l = L_ - 1; l >= std::max(min_leaf_, csm + 1); --l) {
+    for (int l = L_ - 1; l >= min_leaf_; --l) {
       if (band_count_[l])
         AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, band_count_[l], 1 << D_), d_V_, d_st_, g_, l,
                      eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
       // the next level's merge_allowed reads this level's status in halo rows
       if (g_.dist) exchange_(XST);
-    }
-    const int shi = std::min(L_ - 1, csm);
-    if (shi >= min_leaf_) {
-      if (D_ == 3)
-        coop_launch(pdl_, mr_coarsen_small<3>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
-                    min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
-      else
-        coop_launch(pdl_, mr_coarsen_small<2>, kSmallTiles, stream_, (const double*)d_V_, d_st_, g_, shi,
-                    min_leaf_, (const double*)d_norms_, d_flagi_, (const int*)d_band_);
-      ++launches_;
     }
     int merged[2] = {0, 0};
     AF_CUDA(cudaMemcpyAsync(merged, d_flagi_, sizeof merged, cudaMemcpyDeviceToHost, stream_));
@@ -1409,8 +1376,17 @@ void MR::capture_while_(F&& body, cudaGraphConditionalHandle h, bool have_h) {
 // device-side counts only (fixed grids): refine + enforce_gradedness (WHILE),
 // lists, predictions, virtual leaves, counts/CFL dt (mr_cycle_begin), the two
 // RK stages, stage records (mr_cycle_end), coarsen sweeps (WHILE), lists.
+void MR::phase_(const char* name) {
+  if (!phases_ || !cycle_capture_) return;
+  cudaEvent_t e;
+  AF_CUDA(cudaEventCreate(&e));
+  AF_CUDA(cudaEventRecordWithFlags(e, stream_, cudaEventRecordExternal));
+  phase_ev_.push_back({name, e});
+}
+
 void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body) {
   const double dx_L = cfg_.extent / static_cast<double>(1 << L_);
+  phase_("start");
   wset_(d_flag_, 1, 1, 0, 0, L_);
   for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
   AF_ML_LAUNCH_M(mr_detail_level, std::max(0, min_leaf_ - 1), L_ - 2, false, 1 << D_, d_V_,
@@ -1426,7 +1402,9 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
     AF_CUDA(cudaGetLastError());
   });
   *grade_body = launches_ - b0;
+  phase_("refine+grade");
   build_lists_enqueue_();
+  phase_("lists");
   // Fork: the prediction refresh (writes values of absent cells) runs beside
   // add_virtual_leaves / counts / CFL speed / cycle record (statuses, marks,
   // leaf values); both finish before the first stage.
@@ -1451,6 +1429,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   stream_ = main;
   AF_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
   virtuals_ = true;
+  phase_("predict || virtual+counts+dt");
   // the global step: dt and the step index come from mr_cycle_begin
   stage_records_.clear();
   cur_step_ = 0;
@@ -1465,10 +1444,13 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   // refresh unconditionally, further sweeps (a WHILE node) only while one
   // merged and another can (the re-sweep test of coarsen_level_dev)
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
+  phase_("cycle end");
   for (int l = L_ - 1; l >= min_leaf_; --l)
     AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1),
                  d_norms_, d_flagi_, AF_BAND(l));
+  phase_("coarsen sweep");
   predict_fill_(1, 0, min_leaf_ + 1);
+  phase_("predict after coarsen");
   const cudaGraphConditionalHandle hc = make_cond_(0);
   launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, hc, d_flagi_, full_sweeps_ ? 0 : 1,
            d_acc_ + 5);
@@ -1488,6 +1470,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
       },
       hc, true);
   *sweep_body = launches_ - b0;
+  phase_("re-sweeps");
   // no list rebuild here: the next refine works on this cycle's post-refine
   // lists, a superset of the coarsened tree's band (every node it holds
   // existed then), and rebuilds them after its splits
@@ -1611,6 +1594,15 @@ bool MR::run_batch_graph_(long B, double cfl, double fixed_dt, long& done, long&
     return false;
   }
   launches_ += B * cg.launches_fixed + (long)ha[3] * cg.grade_body + (long)ha[4] * cg.sweep_body;
+  if (phases_ && phase_ev_.size() > 1) {
+    phase_ms_.resize(phase_ev_.size(), 0.0);
+    for (size_t i = 1; i < phase_ev_.size(); ++i) {
+      float ms = 0.f;
+      AF_CUDA(cudaEventElapsedTime(&ms, phase_ev_[i - 1].second, phase_ev_[i].second));
+      phase_ms_[i] += ms;
+    }
+    ++phase_n_;
+  }
   static const bool dbg = std::getenv("AF_MR_DEBUG_LOOPS") != nullptr;
   if (dbg)
     std::fprintf(stderr, "batch of %ld cycles: %llu gradedness passes, %llu coarsen sweeps\n", B,
@@ -1648,7 +1640,7 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
                      !std::getenv("AF_MR_NO_CYCLE_GRAPH") && !std::getenv("AF_MR_TIMING");
   while (done < n_steps) {
     if (graph) {
-      const long B = std::min<long>(n_steps - done, kCycBatch);
+      const long B = phases_ ? 1 : std::min<long>(n_steps - done, kCycBatch);
       if (run_batch_graph_(B, cfl, fixed_dt, done, cycle, t, cycles, max_cycles)) continue;
       // a stage failed inside the batch: replay it cycle by cycle from the
       // checkpoint; the synchronous path throws the reference's error there

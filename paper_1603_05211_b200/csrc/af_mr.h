@@ -58,16 +58,13 @@ class MR {
   void project_range_(int lo, int top);
   void build_lists_();
   bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1, int cap = 148 * 8) const;
-  int coop_blocks_();
   int level_tiles_(int l) const { return g_.ntx[l] * g_.nty[l] * g_.ntz[l]; }
   void cycle_stats_(long* leaves, long* nodes, double* smax);
-  int coop_blocks_cache_ = 0;
   int pre_() const;       // prefetch permissions of the next launch (kPreList | kPreSt)
   long v_only_at_ = -1;   // launches_ right after a launch that writes only values
   int small_hi_ = 0;
   bool pdl_ = true;             // programmatic dependent launches (AF_MR_NO_PDL turns off)
   bool full_sweeps_ = false;    // AF_MR_FULL_SWEEPS: never skip a coarsen sweep; check the skip test
-  bool small_coarsen_ = false;  // coarsest levels [0, small_hi_] use the cooperative small-level kernels
   void stage_(int lo, int hi, double tau, double sdt, int stage, long step);
   void step_levels_(int lo, int hi, double t, double dt, int sub);
   void build_registers_(int top);
@@ -115,9 +112,16 @@ class MR {
   cudaStream_t side_stream_ = nullptr;
   cudaStream_t fork_stream_ = nullptr;
   bool swap_ = false;
+  // AF_MR_PHASES: event marks between the phases of the captured cycle graph
+  // (one cycle per batch), averaged and printed at destruction
+  void phase_(const char* name);
+  bool phases_ = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> phase_ev_;
+  std::vector<double> phase_ms_;
+  long phase_n_ = 0;
   bool cycle_capture_ = false;              // capturing the whole-cycle graph (swap allowed)                       // stage_: output buffer becomes the state (no commit copy)      // cycle graph: work beside the prediction refresh
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
-  bool in_body_ = false;                    // capturing a WHILE body: no cooperative launches
+  bool in_body_ = false;                    // capturing a WHILE body
   double* d_ckV_ = nullptr;                 // batch checkpoint (replay on failure)
   uint8_t* d_ckSt_ = nullptr;
   af_mr_cycle* d_cycrec_ = nullptr;

@@ -386,31 +386,6 @@ __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vm
   });
 }
 
-// All levels in one cooperative launch (grid-wide barrier between levels):
-// projection finest-first over [lo, top-1], prediction refresh coarsest-first.
-template <int D>
-__global__ void mr_project_all(double* V, const uint8_t* st, MRLevels g, int lo, int top,
-                               const int* band) {
-  AF_PDL_ENTRY();
-  cg::grid_group grid = cg::this_grid();
-  for (int l = top - 1; l >= lo; --l) {
-    if (g.band_cnt[l]) project_level_dev<D>(V, st, g, l, band + g.tile_off[l], g.band_cnt[l]);
-    grid.sync();
-  }
-}
-
-template <int D>
-__global__ void mr_predict_all(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
-                               int lo, int hi, const int* band) {
-  AF_PDL_ENTRY();
-  cg::grid_group grid = cg::this_grid();
-  for (int l = 1; l <= g.L; ++l) {
-    if (g.band_cnt[l])
-      predict_level_dev<D>(V, st, vmark, g, l, lo, hi, band + g.tile_off[l], g.band_cnt[l]);
-    grid.sync();
-  }
-}
-
 // ---------------------------------------------------------------- detail --
 // detail / detail_between (mr_tree.cpp:291-317): max over children and
 // components of |q_child - pred_child| / norm_k. Zero numerators are returned
@@ -747,88 +722,39 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
   coarsen_level_dev<D>(V, st, g, l, eps, norms, merged, tiles, ntiles);
 }
 
-// The coarse levels (a few tiles each) in one cooperative launch with a
-// grid-wide barrier between levels: their per-level work is shorter than a
-// kernel launch, and the level order (prediction coarsest-first, projection
-// and coarsening finest-first) is kept by the barrier. A level here has at
-// most gridDim.x band tiles, so a block holds one tile per level: every
-// level's tile lookup and status load are issued together up front (before
-// the PDL wait when `pre` allows), leaving the value loads to each level.
-constexpr int kSmallLevels = 16;
+// The coarsest levels (at most kTinyCells cells each: 2D up to level 5,
+// 3D up to level 3) in ONE single-CTA launch, a __syncthreads between levels
+// keeping the level order (prediction coarsest first, projection finest
+// first). Each of these levels is shorter than a kernel launch; as separate
+// launches they cost ~4 us apiece in the cycle graph. (Coarsening stays one
+// launch per level: its child-parallel details on one CTA were slower.)
+// Every cell of such a level is visited (a superset of its band tiles).
+// Not used with ranks (windowed arrays: dense visits would leave the rows).
+constexpr int kTinyCells = 1024;
+constexpr int kTinyThreads = 512;  // 128 registers a thread (the predictions need them)
 
 template <int D>
-__device__ __forceinline__ long small_cell(const MRLevels& g, int l, const int* band) {
-  if ((int)blockIdx.x >= g.dcnt[l]) return -1;
-  int lv;
-  return tile_cell<D>(g, l, band + g.tile_off[l], -1, blockIdx.x, &lv);
-}
-
-template <int D>
-__global__ void mr_predict_small(double* V, const uint8_t* st, const uint8_t* vmark, MRLevels g,
-                                 int lfrom, int lto, int lo, int hi, const int* band, int pre) {
-  cg::grid_group grid = cg::this_grid();
-  long cs[kSmallLevels];
-  auto fetch = [&] {
-#pragma unroll
-    for (int i = 0; i < kSmallLevels; ++i) {
-      const int l = lfrom + i;
-      cs[i] = -1;
-      if (l <= lto) {
-        const long c = small_cell<D>(g, l, band);
-        if (c >= 0 && st[g.cell_off[l] + c] == ST_ABSENT) cs[i] = c;
-      }
-    }
-  };
-  const bool early = (pre & (kPreList | kPreSt)) == (kPreList | kPreSt);
-  if (early) fetch();
+__global__ void __launch_bounds__(kTinyThreads) mr_predict_tiny(double* V, const uint8_t* st,
+                                                                const uint8_t* vmark, MRLevels g,
+                                                                int lfrom, int lto, int lo, int hi) {
   AF_PDL_ENTRY();
-  if (!early) fetch();
-#pragma unroll
-  for (int i = 0; i < kSmallLevels; ++i) {
-    const int l = lfrom + i;
-    if (l > lto) break;
-    if (cs[i] >= 0) predict_cell<D>(V, vmark, g, l, cs[i], ST_ABSENT, lo, hi, false);
-    grid.sync();
+  for (int l = lfrom; l <= lto; ++l) {
+    const long cells = mr_cells(D, l);
+    for (long c = threadIdx.x; c < cells; c += blockDim.x)
+      predict_cell<D>(V, vmark, g, l, c, st[g.cell_off[l] + c], lo, hi, false);
+    __syncthreads();
   }
 }
 
 template <int D>
-__global__ void mr_project_small(double* V, const uint8_t* st, MRLevels g, int lhigh, int llow,
-                                 const int* band, int pre) {
-  cg::grid_group grid = cg::this_grid();
-  long cs[kSmallLevels];
-  auto fetch = [&] {
-#pragma unroll
-    for (int i = 0; i < kSmallLevels; ++i) {
-      const int l = lhigh - i;
-      cs[i] = -1;
-      if (l >= llow) {
-        const long c = small_cell<D>(g, l, band);
-        if (c >= 0 && st[g.cell_off[l] + c] == ST_INTERNAL) cs[i] = c;
-      }
-    }
-  };
-  const bool early = (pre & (kPreList | kPreSt)) == (kPreList | kPreSt);
-  if (early) fetch();
+__global__ void __launch_bounds__(kTinyThreads) mr_project_tiny(double* V, const uint8_t* st,
+                                                                MRLevels g, int lhigh, int llow) {
   AF_PDL_ENTRY();
-  if (!early) fetch();
-#pragma unroll
-  for (int i = 0; i < kSmallLevels; ++i) {
-    const int l = lhigh - i;
-    if (l < llow) break;
-    if (cs[i] >= 0) project_cell<D>(V, g, l, cs[i], ST_INTERNAL);
-    grid.sync();
-  }
-}
-
-template <int D>
-__global__ void mr_coarsen_small(const double* V, uint8_t* st, MRLevels g, int lhigh, int llow,
-                                 const double* norms, int* merged, const int* band) {
-  AF_PDL_ENTRY();
-  cg::grid_group grid = cg::this_grid();
   for (int l = lhigh; l >= llow; --l) {
-    coarsen_level_dev<D>(V, st, g, l, g.eps_l[l + 1], norms, merged, band + g.tile_off[l], -1);
-    grid.sync();
+    const long cells = mr_cells(D, l);
+    for (long c = threadIdx.x; c < cells; c += blockDim.x)
+      project_cell<D>(V, g, l, c, st[g.cell_off[l] + c]);
+    __syncthreads();
   }
 }
 
