@@ -111,8 +111,10 @@ __global__ void mr_while_cond(cudaGraphConditionalHandle h, int* flags, int both
 // ctl[0] = global step index, ctl[1] = record slot in the batch.
 __global__ void mr_cycle_begin(const unsigned long long* red, const unsigned long long* lpl,
                                int L, int D, double cfl, double fixed_dt, double dx_L,
-                               double* dt_out, int* step3, long long* ctl, af_mr_cycle* rec) {
+                               double* dt_out, int* step3, long long* ctl, af_mr_cycle* rec,
+                               unsigned long long* srec, int nsrec) {
   AF_PDL_ENTRY();
+  for (int i = 0; i < nsrec; ++i) srec[i] = 0;  // this cycle's stage records (stage_)
   const double smax = __longlong_as_double((long long)red[3]);
   double dt = fixed_dt;
   if (cfl > 0.0) dt = cfl * dx_L / smax;
@@ -395,6 +397,8 @@ MR::~MR() {
   if (fork_stream_) cudaStreamDestroy(fork_stream_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  for (cudaEvent_t e : ev_aux_)
+    if (e) cudaEventDestroy(e);
   if (h_cycrec_) cudaFreeHost(h_cycrec_);
   if (h_small_) cudaFreeHost(h_small_);
   for (void* p : {(void*)d_ckV_, (void*)d_ckSt_, (void*)d_cycrec_, (void*)d_cycctl_, (void*)d_acc_})
@@ -843,7 +847,8 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   stage_records_.push_back({slot, 0.0, lo, hi});
   unsigned long long* wave = d_red_ + 64 + slot * 17;
   unsigned long long* fb = d_red_ + 64 + slot * 17 + 16;
-  AF_CUDA(cudaMemsetAsync(wave, 0, sizeof(unsigned long long) * 17, stream_));
+  // (in the cycle graph mr_cycle_begin clears both stages' records)
+  if (!cycle_capture_) AF_CUDA(cudaMemsetAsync(wave, 0, sizeof(unsigned long long) * 17, stream_));
   a.wave = wave;
   a.fb = fb;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1421,8 +1426,8 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   ++launches_;
   if (cfl > 0.0)
     AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
-  launch_k(pdl_, stream_, mr_cycle_begin, dim3(1), 1, 0, d_red_, d_lpl_, L_, D_, cfl, fixed_dt, dx_L, d_dt_,
-                                       d_step3_, d_cycctl_, d_cycrec_);
+  launch_k(pdl_, stream_, mr_cycle_begin, dim3(1), 1, 0, d_red_, d_lpl_, L_, D_, cfl, fixed_dt,
+           dx_L, d_dt_, d_step3_, d_cycctl_, d_cycrec_, d_red_ + 64, 2 * 17);
   ++launches_;
   AF_CUDA(cudaGetLastError());
   AF_CUDA(cudaEventRecord(ev_join_, stream_));
@@ -1435,10 +1440,15 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   cur_step_ = 0;
   step_levels_(0, L_, 0.0, 0.0, 0);
   cur_step_ = -1;
-  launch_k(pdl_, stream_, mr_cycle_end, dim3(1), 1, 0, d_red_ + 64, d_lpl_, L_, cfg_.extent, d_dt_, d_acc_,
-                                     d_cycctl_);
+  // the stage records (mr_cycle_end) beside the coarsen sweep; joined at the
+  // end of the cycle
+  AF_CUDA(cudaEventRecord(ev_aux_[0], stream_));
+  AF_CUDA(cudaStreamWaitEvent(fork_stream_, ev_aux_[0], 0));
+  launch_k(pdl_, fork_stream_, mr_cycle_end, dim3(1), 1, 0, d_red_ + 64, d_lpl_, L_, cfg_.extent,
+           d_dt_, d_acc_, d_cycctl_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
+  AF_CUDA(cudaEventRecord(ev_aux_[1], fork_stream_));
   virtuals_ = false;
   // coarsen (mr_tree.cpp:473-510): the first sweep and its prediction
   // refresh unconditionally, further sweeps (a WHILE node) only while one
@@ -1449,13 +1459,19 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
     AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1),
                  d_norms_, d_flagi_, AF_BAND(l));
   phase_("coarsen sweep");
-  predict_fill_(1, 0, min_leaf_ + 1);
-  phase_("predict after coarsen");
+  // the re-sweep decision (mr_while_cond reads the sweep's flags) beside the
+  // prediction refresh
   const cudaGraphConditionalHandle hc = make_cond_(0);
-  launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, hc, d_flagi_, full_sweeps_ ? 0 : 1,
+  AF_CUDA(cudaEventRecord(ev_aux_[2], stream_));
+  AF_CUDA(cudaStreamWaitEvent(fork_stream_, ev_aux_[2], 0));
+  launch_k(pdl_, fork_stream_, mr_while_cond, dim3(1), 1, 0, hc, d_flagi_, full_sweeps_ ? 0 : 1,
            d_acc_ + 5);
   ++launches_;
   AF_CUDA(cudaGetLastError());
+  AF_CUDA(cudaEventRecord(ev_aux_[3], fork_stream_));
+  predict_fill_(1, 0, min_leaf_ + 1);
+  AF_CUDA(cudaStreamWaitEvent(stream_, ev_aux_[3], 0));
+  phase_("predict after coarsen");
   b0 = launches_;
   capture_while_(
       [&](cudaGraphConditionalHandle h) {
@@ -1470,6 +1486,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
       },
       hc, true);
   *sweep_body = launches_ - b0;
+  AF_CUDA(cudaStreamWaitEvent(stream_, ev_aux_[1], 0));  // mr_cycle_end
   phase_("re-sweeps");
   // no list rebuild here: the next refine works on this cycle's post-refine
   // lists, a superset of the coarsened tree's band (every node it holds
@@ -1490,6 +1507,7 @@ MR::CycleGraph& MR::cycle_graph_(double cfl, double fixed_dt) {
     AF_CUDA(cudaStreamCreateWithFlags(&fork_stream_, cudaStreamNonBlocking));
     AF_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     AF_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    for (cudaEvent_t& e : ev_aux_) AF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     AF_CUDA(cudaMalloc(&d_ckV_, sizeof(double) * NC_ * g_.total_cells));
     AF_CUDA(cudaMalloc(&d_ckSt_, g_.total_cells));
     AF_CUDA(cudaMalloc(&d_cycrec_, sizeof(af_mr_cycle) * kCycBatch));

@@ -121,6 +121,7 @@ class MR {
   long phase_n_ = 0;
   bool cycle_capture_ = false;              // capturing the whole-cycle graph (swap allowed)                       // stage_: output buffer becomes the state (no commit copy)      // cycle graph: work beside the prediction refresh
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  cudaEvent_t ev_aux_[4] = {nullptr, nullptr, nullptr, nullptr};  // cycle_end / re-sweep decision forks
   bool in_body_ = false;                    // capturing a WHILE body
   double* d_ckV_ = nullptr;                 // batch checkpoint (replay on failure)
   uint8_t* d_ckSt_ = nullptr;
