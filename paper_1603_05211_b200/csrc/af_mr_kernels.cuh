@@ -492,16 +492,17 @@ __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det,
     const long off = g.cell_off[l];
     const bool internal = valid && st[off + c] == ST_INTERNAL;
     const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    const long fc = g.cell_off[l + 1] +
+                    mr_idx(D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                           D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+    // refine reads the details of the parents of splittable leaves only
+    const bool split_leaf = flag && internal && l + 1 <= g.L - 1 && st[fc] == ST_LEAF;
+    const bool need = flag ? !node_group_all<D>(!split_leaf) : internal;
     double r = 0.0;
-    if (internal) r = child_detail<D>(V, g.total_cells, g, l, i, j, k, ch, norms);
+    if (need && internal) r = child_detail<D>(V, g.total_cells, g, l, i, j, k, ch, norms);
     r = node_group_max<D>(r);
-    if (internal && ch == 0) det[off + c] = r;
-    if (flag && internal && l + 1 <= g.L - 1) {
-      const long fc = g.cell_off[l + 1] +
-                      mr_idx(D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
-                             D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
-      if (st[fc] == ST_LEAF) flag[fc] = r >= g.eps_l[l + 1] ? 1 : 0;
-    }
+    if (!flag && internal && ch == 0) det[off + c] = r;
+    if (split_leaf) flag[fc] = r >= g.eps_l[l + 1] ? 1 : 0;
   });
 }
 
