@@ -337,6 +337,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
+  AF_CUDA(cudaMalloc(&d_tleaf_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 34));
   AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 34));
   g_.dcnt = d_tile_count_;
@@ -413,7 +414,7 @@ MR::~MR() {
       cudaFree(p);
   }
   for (void* p : {(void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
-                  (void*)d_band_, (void*)d_tflag_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
+                  (void*)d_band_, (void*)d_tflag_, (void*)d_tleaf_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
                   (void*)d_flagi_, (void*)d_red_, (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_,
                   (void*)d_regff_, (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
     cudaFree(p);
@@ -576,19 +577,20 @@ void MR::build_lists_() {
 // Band / leaf tile lists and leaves per level, device side only (counts in
 // d_tile_count_ == g_.dcnt and d_lpl_).
 void MR::build_lists_enqueue_() {
-  AF_CUDA(cudaMemsetAsync(d_tile_count_, 0, sizeof(int) * 34, stream_));
-  AF_CUDA(cudaMemsetAsync(d_lpl_, 0, sizeof(unsigned long long) * 17, stream_));
+  // (the counts and leaves per level are cleared by mr_tile_flags_all)
   const long nt = tile_off_[L_ + 1];
   const unsigned gw = (unsigned)std::max<long>(1, std::min<long>((nt + 7) / 8, kGrid));
   const unsigned gt = grid_for(nt);
   if (D_ == 3) {
-    launch_k(pdl_, stream_, mr_tile_flags_all<3>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_lpl_);
-    launch_k(pdl_, stream_, mr_tile_lists_all<3>, dim3(gt), 256, 0, d_tflag_, g_, d_band_, d_tiles_,
-             d_tile_count_);
+    launch_k(pdl_, stream_, mr_tile_flags_all<3>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
+             d_tile_count_, d_lpl_);
+    launch_k(pdl_, stream_, mr_tile_lists_all<3>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_tile_count_, d_lpl_);
   } else {
-    launch_k(pdl_, stream_, mr_tile_flags_all<2>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_lpl_);
-    launch_k(pdl_, stream_, mr_tile_lists_all<2>, dim3(gt), 256, 0, d_tflag_, g_, d_band_, d_tiles_,
-             d_tile_count_);
+    launch_k(pdl_, stream_, mr_tile_flags_all<2>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
+             d_tile_count_, d_lpl_);
+    launch_k(pdl_, stream_, mr_tile_lists_all<2>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_tile_count_, d_lpl_);
   }
   launches_ += 2;
   AF_CUDA(cudaGetLastError());

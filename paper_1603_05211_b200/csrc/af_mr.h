@@ -205,6 +205,7 @@ class MR {
   int* d_tiles_ = nullptr;       // per-level leaf-tile lists (tile_off_ regions)
   int* d_band_ = nullptr;        // per-level band-tile lists
   uint8_t* d_tflag_ = nullptr;
+  int* d_tleaf_ = nullptr;  // leaves per tile (mr_tile_flags_all -> mr_tile_lists_all)
   int* d_tile_count_ = nullptr;  // [0..16] band counts, [17..33] leaf-tile counts
   unsigned long long* d_lpl_ = nullptr;  // leaves per level
   int* d_err_ = nullptr;

@@ -604,9 +604,12 @@ __device__ __forceinline__ bool tile_in_region(const MRLevels& g, int l, int r0)
 // parent exists, so these tiles cover the tree and everything a split can
 // create). Leaves per level are counted on the way.
 template <int D>
-__global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
-                                  unsigned long long* leaves_per_level) {
+__global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag, int* tleaf,
+                                  int* counts, unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
+  // the list counts and leaves per level mr_tile_lists_all accumulates
+  if (blockIdx.x == 0 && threadIdx.x < 34) counts[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 17) leaves_per_level[threadIdx.x] = 0;
   constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
   constexpr int TZ = D == 3 ? kTileZ3 : 1;
   const long total = g.tile_off[g.L + 1];
@@ -622,7 +625,10 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     unsigned nleaf = 0;
     bool pex = false, rleaf = false;
     if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
-      if (lane == 0) tflag[tg] = 0;
+      if (lane == 0) {
+        tflag[tg] = 0;
+        tleaf[tg] = 0;
+      }
       continue;
     }
     for (int c = lane; c < TX * TY * TZ; c += 32) {
@@ -641,7 +647,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
       // bit 0: the tile holds a leaf this rank steps, or (with ranks) a
       // halo leaf whose register shares it computes
       tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0);
-      if (nleaf) atomicAdd(leaves_per_level + l, (unsigned long long)nleaf);
+      tleaf[tg] = (int)nleaf;
     }
   }
 }
@@ -652,8 +658,8 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
 // within the stencil reach (<= 3 cells) of a node, so this band is where
 // projections, predictions, details and merges are evaluated.
 template <int D>
-__global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, int* leaf,
-                                  int* counts) {
+__global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLevels g, int* band,
+                                  int* leaf, int* counts, unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
   const long total = g.tile_off[g.L + 1];
   for (long tg = blockIdx.x * (long)blockDim.x + threadIdx.x; tg < total;
@@ -685,6 +691,7 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, MRLevels g, int* band, i
       in_band = false;
     if (in_band) band[g.tile_off[l] + atomicAdd(counts + l, 1)] = (int)t;
     if (tflag[tg] & 1) leaf[g.tile_off[l] + atomicAdd(counts + 17 + l, 1)] = (int)t;
+    if (tleaf[tg]) atomicAdd(leaves_per_level + l, (unsigned long long)tleaf[tg]);
   }
 }
 
