@@ -1,15 +1,17 @@
 #!/usr/bin/env python3
 """bench.py — throughput of the B200 MR/FV Euler hot path (and the reference arm).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg3|cfg4|cfg1]
     python bench.py --impl reference ...      # the reference's own CPU path
 
-Default workload (BASELINE.json configs[3], "cfg4"): 3D Euler, 512^3 uniform
-mesh, fp64, unit cube, outflow, seeded ellipsoid blast, AUSM+/minmod/RK2,
-CFL 0.4 (sum-over-axes rule). A "step" is one RK2 step (two
-stages) over the whole mesh. Metric: cell-updates/s = cells x 2 stages x K /
-time (BASELINE.json metric). Multi-GPU (torchrun): z-slabs, NCCL halo
-exchange, strong scaling (the mesh is fixed).
+Default workload: "cfg2" (BASELINE.json configs[1], the config the metric is
+quoted on): 2D MR, finest level 10 (1024^2), coarsest leaf level 3, level
+thresholds 1e-3*2^(2(l-L)), global time step, CFL 0.5, seeded four-quadrant
+Riemann data. A "step" is one run_mr cycle (refine, virtual leaves, the RK2
+step, coarsen); the default K is the config's own step count (cfg2: 500).
+Metric: leaf-cell RK-stage updates / s (BASELINE.json metric). The uniform
+workloads (cfg1, cfg4) time RK2 steps over the whole mesh. Multi-GPU
+(torchrun): slabs with NCCL halo exchange.
 
 Rank 0 prints ONE JSON line.
 """
@@ -271,7 +273,9 @@ def workload_config(workload, n_gpus):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the config's own step count, e.g. cfg2's 500 "
+                         "cycles, cfg4's 100 steps)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
@@ -286,6 +290,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = WORKLOADS[args.workload][6]
     if args.level is not None:
         w = list(WORKLOADS[args.workload])
         w[3] = args.level
