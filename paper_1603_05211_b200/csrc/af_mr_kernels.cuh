@@ -77,19 +77,39 @@ __device__ __forceinline__ int tile_at(const MRLevels& g, int l, const int* tile
   return tiles[it];
 }
 
+// Entry -> (level, tile) of a multi-level range for a block whose entries
+// increase from call to call: the level cursor only moves forward, so the
+// walk over the per-level counts is paid once per block, not once per entry.
+struct TileWalker {
+  int k, base, cnt_k;
+  const int* cnt;
+  __device__ __forceinline__ TileWalker(const MRLevels& g, int l, int ntiles) {
+    cnt = g.dcnt + 17 * (ntiles & 1);
+    k = -l - 1;
+    base = 0;
+    cnt_k = cnt[k];
+  }
+  __device__ __forceinline__ int at(const MRLevels& g, const int* tiles, int ti, int* level) {
+    while (ti >= base + cnt_k) {
+      base += cnt_k;
+      cnt_k = cnt[++k];
+    }
+    *level = k;
+    return tiles[g.tile_off[k] + ti - base];
+  }
+};
+
 template <class F>
 __device__ __forceinline__ void for_each_tile(const MRLevels& g, int l, const int* tiles,
                                               int ntiles, int reps, F&& f) {
   if (l < 0) {
-    const int lo = -l - 1, hi = ntiles >> 1;
-    const int* cnt = g.dcnt + 17 * (ntiles & 1);
-    int total = 0;
-    for (int k = lo; k <= hi; ++k) total += cnt[k];
+    const int total = tile_total(g, l, ntiles);
+    TileWalker w(g, l, ntiles);
     for (int it = blockIdx.x; it < total * reps; it += gridDim.x) {
       const int ti = it / reps;
-      int k = lo, base = 0;
-      while (ti >= base + cnt[k]) base += cnt[k++];
-      f(k, tiles[g.tile_off[k] + ti - base], it - ti * reps);
+      int k;
+      const int t = w.at(g, tiles, ti, &k);
+      f(k, t, it - ti * reps);
     }
   } else {
     if (ntiles < 0) ntiles = ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l];

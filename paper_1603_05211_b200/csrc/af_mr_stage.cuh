@@ -195,8 +195,9 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int tx = tid % TX, ty = (tid / TX) % TY, tz = D == 3 ? tid / (TX * TY) : 0;
   const int ntotal = tile_total(g, l, a.ntiles);
   const int lcode = l;
+  TileWalker walk(g, lcode < 0 ? lcode : -1, a.ntiles);  // (used in multi-level mode only)
   for (int it = blockIdx.x; it < ntotal; it += gridDim.x) {
-  const int t = tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
+  const int t = lcode < 0 ? walk.at(g, a.tiles, it, &l) : tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
   const int n = 1 << l;
   const long off = g.cell_off[l];
   const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
