@@ -85,7 +85,7 @@ __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* 
        c += (long)gridDim.x * blockDim.x) {
     if (g.dist && !row_in_region(g, l, mr_row(D, l, c))) continue;  // this rank's rows
     if (st[off + c] != ST_ABSENT) continue;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
     if (!mark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
     for (int m = 0; m < D + 2; ++m) VQ[m * comp + off + c] = V[m * comp + off + c];
   }

@@ -131,8 +131,9 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
     const int tz = D == 3 ? threadIdx.x / (TX * TY) : 0;
     for_each_tile(g, l, tiles, ntiles, 1, [&](int lv, int t, int) {
       const int n = 1 << lv, ntx = g.ntx[lv], nty = g.nty[lv];
-      const int x = (t % ntx) * TX + tx, y = ((t / ntx) % nty) * TY + ty;
-      const int z = D == 3 ? (t / (ntx * nty)) * kTileZ3 + tz : 0;
+      const int sx = ilog2i(ntx), sy = ilog2i(nty);  // tile counts are powers of two
+      const int x = (t & (ntx - 1)) * TX + tx, y = ((t >> sx) & (nty - 1)) * TY + ty;
+      const int z = D == 3 ? (t >> (sx + sy)) * kTileZ3 + tz : 0;
       if (x < n && y < n && (D == 2 || z < n)) f(lv, mr_idx(D, n, x, y, z));
     });
   } else {
@@ -155,7 +156,7 @@ __device__ __forceinline__ void project_cell(double* V, const MRLevels& g, int l
   const long comp = g.total_cells;
   const double w = 1.0 / (double)(1 << D);
   if (s != ST_INTERNAL || !row_owned(g, l, mr_row(D, l, c))) return;
-  const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+  const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
   double sm[NC];
 #pragma unroll
   for (int m = 0; m < NC; ++m) sm[m] = 0.0;
@@ -188,8 +189,9 @@ __device__ __forceinline__ long tile_cell(const MRLevels& g, int l, const int* t
   const int tz = D == 3 ? threadIdx.x / (TX * TY) : 0;
   const int t = tile_at(g, l, tiles, ntiles, it, lv);
   const int n = 1 << *lv, ntx = g.ntx[*lv], nty = g.nty[*lv];
-  const int x = (t % ntx) * TX + tx, y = ((t / ntx) % nty) * TY + ty;
-  const int z = D == 3 ? (t / (ntx * nty)) * kTileZ3 + tz : 0;
+  const int sx = ilog2i(ntx), sy = ilog2i(nty);  // tile counts are powers of two
+  const int x = (t & (ntx - 1)) * TX + tx, y = ((t >> sx) & (nty - 1)) * TY + ty;
+  const int z = D == 3 ? (t >> (sx + sy)) * kTileZ3 + tz : 0;
   return (x < n && y < n && (D == 2 || z < n)) ? mr_idx(D, n, x, y, z) : -1L;
 }
 
@@ -365,7 +367,7 @@ __device__ __forceinline__ void predict_cell(double* V, const uint8_t* vmark, co
   const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
   if (dense && g.dist && !row_in_region(g, l, mr_row(D, l, c))) return;  // dense: own rows
   if (s != ST_ABSENT) return;
-  const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+  const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
   if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
   const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
   double q[NC];
@@ -424,8 +426,9 @@ __device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, c
     constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
     for_each_tile(g, l, tiles, ntiles, NCH, [&](int lv, int t, int r) {
       const int n = 1 << lv, ntx = g.ntx[lv], nty = g.nty[lv];
-      const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
-      const int z0 = D == 3 ? (t / (ntx * nty)) * kTileZ3 : 0;
+      const int sx = ilog2i(ntx), sy = ilog2i(nty);
+      const int x0 = (t & (ntx - 1)) * TX, y0 = ((t >> sx) & (nty - 1)) * TY;
+      const int z0 = D == 3 ? (t >> (sx + sy)) * kTileZ3 : 0;
       const int item = r * 256 + (int)threadIdx.x, tn = item >> D;
       const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
       const bool valid = x < n && y < n && (D == 2 || z < n);
@@ -481,14 +484,18 @@ __device__ __forceinline__ double child_detail(const double* V, long comp, const
   constexpr int NC = D + 2;
   const int n = 1 << l, nf = n << 1;
   const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-  double pred[NC];
-  predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
+  // the child's own values first: their loads overlap the stencil's
   const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                                 D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
+  double cv[NC];
+#pragma unroll
+  for (int m = 0; m < NC; ++m) cv[m] = V[m * comp + fc];
+  double pred[NC];
+  predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
   double mag = 0.0;
 #pragma unroll
   for (int m = 0; m < NC; ++m) {
-    const double d = fabs(V[m * comp + fc] - pred[m]);
+    const double d = fabs(cv[m] - pred[m]);
     // norms index: rho 0, mom 1..D, rhoE 4 (the 2D mom2 term is 0/global == 0)
     const int ni = m == NC - 1 ? 4 : m;
     const double r = detail_ratio(d, norms[ni]);
@@ -511,7 +518,7 @@ __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det,
     const int n = 1 << l;
     const long off = g.cell_off[l];
     const bool internal = valid && st[off + c] == ST_INTERNAL;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
     const long fc = g.cell_off[l + 1] +
                     mr_idx(D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                            D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
@@ -544,7 +551,7 @@ __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t*
     const long cells = mr_cells(D, l), off = g.cell_off[l];
     uint8_t f = flag[off + c];
     if (!f && st[off + c] == ST_LEAF) {
-      const int t[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+      const int t[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
       const int rz = D == 3 ? r : 0;
       for (int dk = -rz; dk <= rz && !f; ++dk)
         for (int dj = -r; dj <= r && !f; ++dj)
@@ -576,7 +583,7 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
     const int n = 1 << l, nf = n << 1;
     const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
     if (!flag[off + c] || st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(D, l, c))) return;
-    const int i = (int)(c % n), j = (int)((c / n) % n), k = D == 3 ? (int)(c / ((long)n * n)) : 0;
+    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
     st[off + c] = ST_INTERNAL;
     for (int ch = 0; ch < (1 << D); ++ch)
       st[foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
@@ -599,8 +606,8 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
     const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
     uint8_t need = 0;
     if (st[off + c] == ST_LEAF && l < g.L) {
-      const int idx[3] = {(int)(c % n), (int)((c / n) % n),
-                          D == 3 ? (int)(c / ((long)n * n)) : 0};
+      const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)),
+                          D == 3 ? (int)(c >> (2 * l)) : 0};
       for (int a = 0; a < D && !need; ++a)
         for (int dir = -1; dir <= 1 && !need; dir += 2) {
           int p[3] = {idx[0], idx[1], idx[2]};
@@ -641,7 +648,7 @@ __device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, 
     const int l = lv_;
     const int n = 1 << l, nf = n << 1;
     const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
     int cc[3];
     cc[0] = 2 * idx[0] + (ch & 1);
     cc[1] = 2 * idx[1] + ((ch >> 1) & 1);
@@ -791,7 +798,7 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
     const int n = 1 << l, pn = n >> 1;
     const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
     if (st[off + c] != ST_LEAF) return;
-    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
     for (int a = 0; a < D; ++a)
       for (int o = -2; o <= 2; ++o) {
         if (o == 0) continue;

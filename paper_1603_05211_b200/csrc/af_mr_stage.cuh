@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
   const double inv_dx = g.inv_dx[l];
   double wave = 0.0;
-  const int x0 = (t % ntx) * TX, y0 = ((t / ntx) % nty) * TY;
-  const int z0 = D == 3 ? (t / (ntx * nty)) * TZ : 0;
+  const int sx = ilog2i(ntx), sy = ilog2i(nty);  // powers of two
+  const int x0 = (t & (ntx - 1)) * TX, y0 = ((t >> sx) & (nty - 1)) * TY;
+  const int z0 = D == 3 ? (t >> (sx + sy)) * TZ : 0;
   // leaf mask of the tile cells
   const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
@@ -511,7 +512,7 @@ __global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* re
     if (!row_owned(g, l, mr_row(D, l, c))) continue;  // registers live with their owner
     unsigned mask = 0;
     if (st[off + c] == ST_LEAF) {
-      const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+      const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
       for (int ax = 0; ax < D; ++ax)
         for (int side = 0; side < 2; ++side) {
           int p[3] = {idx[0], idx[1], idx[2]};
@@ -546,7 +547,7 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
     if (!row_owned(g, l, mr_row(D, l, c))) continue;
     const unsigned mask = regmask[off + c];
     if (!mask) continue;
-    const int idx[3] = {(int)(c % n), (int)((c / n) % n), D == 3 ? (int)(c / ((long)n * n)) : 0};
+    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
     const unsigned long long key = ((unsigned long long)l << 45) |
                                    ((unsigned long long)idx[0] << 30) |
                                    ((unsigned long long)idx[1] << 15) | (unsigned long long)idx[2];
@@ -621,8 +622,9 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     while (tg >= g.tile_off[l + 1]) ++l;
     const long t = tg - g.tile_off[l];
     const int n = 1 << l;
-    const int x0 = (int)(t % g.ntx[l]) * TX, y0 = (int)((t / g.ntx[l]) % g.nty[l]) * TY;
-    const int z0 = D == 3 ? (int)(t / ((long)g.ntx[l] * g.nty[l])) * TZ : 0;
+    const int sx = ilog2i(g.ntx[l]), sy = ilog2i(g.nty[l]);  // powers of two
+    const int x0 = (int)(t & (g.ntx[l] - 1)) * TX, y0 = (int)((t >> sx) & (g.nty[l] - 1)) * TY;
+    const int z0 = D == 3 ? (int)(t >> (sx + sy)) * TZ : 0;
     unsigned nleaf = 0;
     bool pex = false, rleaf = false;
     if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
@@ -669,8 +671,9 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLeve
     while (tg >= g.tile_off[l + 1]) ++l;
     const long t = tg - g.tile_off[l];
     const int nt[3] = {g.ntx[l], g.nty[l], D == 3 ? g.ntz[l] : 1};
-    const int tc[3] = {(int)(t % nt[0]), (int)((t / nt[0]) % nt[1]),
-                       D == 3 ? (int)(t / ((long)nt[0] * nt[1])) : 0};
+    const int sx = ilog2i(nt[0]), sy = ilog2i(nt[1]);  // powers of two
+    const int tc[3] = {(int)(t & (nt[0] - 1)), (int)((t >> sx) & (nt[1] - 1)),
+                       D == 3 ? (int)(t >> (sx + sy)) : 0};
     bool in_band = false;
     const int rz = D == 3 ? 1 : 0;
     for (int dz = -rz; dz <= rz && !in_band; ++dz)
@@ -736,8 +739,9 @@ __global__ void mr_tile_list_kernel(const uint8_t* st, MRLevels g, int l, int* t
   const long off = g.cell_off[l];
   for (long t = blockIdx.x * (long)(blockDim.x / 32) + threadIdx.x / 32; t < ntiles;
        t += (long)gridDim.x * (blockDim.x / 32)) {
-    const int x0 = (int)(t % ntx) * TX, y0 = (int)((t / ntx) % nty) * TY;
-    const int z0 = D == 3 ? (int)(t / ((long)ntx * nty)) * TZ : 0;
+    const int sx = ilog2i(ntx), sy = ilog2i(nty);  // powers of two
+    const int x0 = (int)(t & (ntx - 1)) * TX, y0 = (int)((t >> sx) & (nty - 1)) * TY;
+    const int z0 = D == 3 ? (int)(t >> (sx + sy)) * TZ : 0;
     bool any = false;
     for (int c = threadIdx.x & 31; c < TX * TY * TZ; c += 32) {
       const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);

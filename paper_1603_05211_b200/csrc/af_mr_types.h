@@ -79,6 +79,10 @@ __host__ __device__ __forceinline__ bool row_counted(const MRLevels& g, int l, i
 enum : int { kPreList = 1, kPreSt = 2 };  // tile lists + counts, statuses
 
 constexpr int kTileX2 = 32, kTileY2 = 8;
+
+// log2 of a power of two (tile counts and level sizes: index arithmetic
+// becomes shifts and masks instead of 32/64-bit divisions)
+__device__ __forceinline__ int ilog2i(int x) { return 31 - __clz(x); }
 constexpr int kTileX3 = 8, kTileY3 = 8, kTileZ3 = 4;
 
 __host__ __device__ __forceinline__ long mr_cells(int dim, int l) {
