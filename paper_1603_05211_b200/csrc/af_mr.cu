@@ -469,6 +469,16 @@ double MR::eps_at_(int child_level) const {
 // Prefetch permissions of the next launch (kPreList | kPreSt, af_mr_types.h):
 // granted when the launch just before it in stream order writes neither
 // (v_only_at_ marks a value-only launch; any later launch revokes it).
+// A coarsen sweep's level below the finest: the previous launch is the next
+// finer level of the same sweep, which writes only statuses of levels l+1 and
+// l+2 (and the merge flags), so values, lists and level-l statuses may be read
+// before the PDL wait (mr_coarsen_level). Not with ranks (halo exchanges sit
+// between the levels) or a launch that is not the sweep's continuation.
+int MR::coarsen_pre_(int l) const {
+  static const bool off = std::getenv("AF_MR_NO_PRE") != nullptr;
+  return (!off && !g_.dist && l < L_ - 1) ? kPreV : 0;
+}
+
 int MR::pre_() const {
   static const bool off = std::getenv("AF_MR_NO_PRE") != nullptr;
   return !off && launches_ == v_only_at_ ? (kPreList | kPreSt) : 0;
@@ -1169,7 +1179,7 @@ void MR::coarsen() {
     for (int l = L_ - 1; l >= min_leaf_; --l) {
       if (band_count_[l])
         AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, band_count_[l], 1 << D_), d_V_, d_st_, g_, l,
-                     eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
+                     eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l), coarsen_pre_(l));
       // the next level's merge_allowed reads this level's status in halo rows
       if (g_.dist) exchange_(XST);
     }
@@ -1459,7 +1469,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   phase_("cycle end");
   for (int l = L_ - 1; l >= min_leaf_; --l)
     AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1),
-                 d_norms_, d_flagi_, AF_BAND(l));
+                 d_norms_, d_flagi_, AF_BAND(l), coarsen_pre_(l));
   phase_("coarsen sweep");
   // the re-sweep decision (mr_while_cond reads the sweep's flags) beside the
   // prediction refresh
@@ -1479,7 +1489,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
       [&](cudaGraphConditionalHandle h) {
         for (int l = L_ - 1; l >= min_leaf_; --l)
           AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l,
-                       eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l));
+                       eps_at_(l + 1), d_norms_, d_flagi_, AF_BAND(l), coarsen_pre_(l));
         predict_fill_(1, 0, min_leaf_ + 1);  // a no-op recompute when nothing merged
         launch_k(pdl_, stream_, mr_while_cond, dim3(1), 1, 0, h, d_flagi_, full_sweeps_ ? 0 : 1,
                  d_acc_ + 4);

@@ -60,7 +60,8 @@ class MR {
   bool ml_grid_(int lo, int hi, bool leaf, dim3* grid, int mult = 1, int cap = 148 * 8) const;
   int level_tiles_(int l) const { return g_.ntx[l] * g_.nty[l] * g_.ntz[l]; }
   void cycle_stats_(long* leaves, long* nodes, double* smax);
-  int pre_() const;       // prefetch permissions of the next launch (kPreList | kPreSt)
+  int pre_() const;
+  int coarsen_pre_(int l) const;  // kPreV for a sweep's levels below the finest       // prefetch permissions of the next launch (kPreList | kPreSt)
   long v_only_at_ = -1;   // launches_ right after a launch that writes only values
   int small_hi_ = 0;
   bool pdl_ = true;             // programmatic dependent launches (AF_MR_NO_PDL turns off)

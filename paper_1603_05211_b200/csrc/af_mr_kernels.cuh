@@ -418,6 +418,24 @@ __global__ void mr_predict_level(double* V, const uint8_t* st, const uint8_t* vm
 // tile's 2^D*256 (node, child) items are spread over 2^D blocks. Every lane of
 // a warp runs the same trip count (valid=false on the padding), which keeps
 // the shuffles convergent. Blocks are 256 threads. f(level, node, valid, child).
+// Entry (tile t of level l, repetition r) of the child-parallel iteration:
+// this lane's node c (valid: inside the level) and child index ch.
+template <int D>
+__device__ __forceinline__ void node_child_entry(const MRLevels& g, int l, int t, int r, long* c,
+                                                 bool* valid, int* ch) {
+  constexpr int NCH = 1 << D;
+  constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
+  const int n = 1 << l, ntx = g.ntx[l], nty = g.nty[l];
+  const int sx = ilog2i(ntx), sy = ilog2i(nty);
+  const int x0 = (t & (ntx - 1)) * TX, y0 = ((t >> sx) & (nty - 1)) * TY;
+  const int z0 = D == 3 ? (t >> (sx + sy)) * kTileZ3 : 0;
+  const int item = r * 256 + (int)threadIdx.x, tn = item >> D;
+  const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
+  *valid = x < n && y < n && (D == 2 || z < n);
+  *c = *valid ? mr_idx(D, n, x, y, z) : 0L;
+  *ch = item & (NCH - 1);
+}
+
 template <int D, class F>
 __device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, const int* tiles,
                                                      int ntiles, F&& f) {
@@ -425,14 +443,11 @@ __device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, c
   if (tiles) {
     constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
     for_each_tile(g, l, tiles, ntiles, NCH, [&](int lv, int t, int r) {
-      const int n = 1 << lv, ntx = g.ntx[lv], nty = g.nty[lv];
-      const int sx = ilog2i(ntx), sy = ilog2i(nty);
-      const int x0 = (t & (ntx - 1)) * TX, y0 = ((t >> sx) & (nty - 1)) * TY;
-      const int z0 = D == 3 ? (t >> (sx + sy)) * kTileZ3 : 0;
-      const int item = r * 256 + (int)threadIdx.x, tn = item >> D;
-      const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
-      const bool valid = x < n && y < n && (D == 2 || z < n);
-      f(lv, valid ? mr_idx(D, n, x, y, z) : 0L, valid, item & (NCH - 1));
+      long c;
+      bool valid;
+      int ch;
+      node_child_entry<D>(g, lv, t, r, &c, &valid, &ch);
+      f(lv, c, valid, ch);
     });
   } else {
     const long total = mr_cells(D, l) << D;
@@ -637,6 +652,111 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
 // coarsen (mr_tree.cpp:446-511), one level of one finest-first sweep:
 // an INTERNAL node at level l >= min_leaf merges iff all children are leaves,
 // detail < eps_{l+1}, and no face-ring cell at level l+1 is INTERNAL.
+// One (node, child) lane of a coarsen sweep at level l. rpre: the node's
+// detail (node_group_max'd) when the caller computed it already.
+template <int D>
+__device__ __forceinline__ void coarsen_node(const double* V, uint8_t* st, const MRLevels& g,
+                                             int l, double eps, const double* norms, int* merged,
+                                             long c, bool valid, int ch, const double* rpre) {
+  const int n = 1 << l, nf = n << 1;
+  const long off = g.cell_off[l], foff = g.cell_off[l + 1];
+  const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+  int cc[3];
+  cc[0] = 2 * idx[0] + (ch & 1);
+  cc[1] = 2 * idx[1] + ((ch >> 1) & 1);
+  cc[2] = D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0;
+  const long fc = foff + mr_idx(D, nf, cc[0], cc[1], cc[2]);
+  // candidate: INTERNAL node whose children are all leaves (mr_tree.cpp:486-497)
+  const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF &&
+                                      row_owned(g, l, mr_row(D, l, c)));
+  double r = 0.0;
+  if (rpre) {
+    r = *rpre;  // computed before the PDL wait for every INTERNAL node
+  } else {
+    if (cand) r = child_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], ch, norms);
+    r = node_group_max<D>(r);
+  }
+  bool allowed = true;
+  if (cand && r < eps) {
+    // merge_allowed (mr_tree.cpp:446-471): no INTERNAL level-(l+1) cell
+    // face-adjacent to the children. This lane checks its child's D outward
+    // neighbours; the 2^d lanes together cover every position.
+#pragma unroll
+    for (int a = 0; a < D; ++a) {  // unrolled: g.bc[] stays in the param space
+      int q[3] = {cc[0], cc[1], cc[2]};
+      q[a] = ((ch >> a) & 1) ? 2 * idx[a] + 2 : 2 * idx[a] - 1;
+      const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+      if (!per && (q[a] < 0 || q[a] >= nf)) continue;
+      bool fl;
+      q[a] = mr_map(q[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
+      if (st[foff + mr_idx(D, nf, q[0], q[1], q[2])] == ST_INTERNAL) allowed = false;
+    }
+  }
+  const bool merge = node_group_all<D>(cand && r < eps && allowed);
+  if (merge) {
+    // merged q = mean of the children == the projection already stored
+    st[fc] = ST_ABSENT;
+    if (ch == 0) {
+      st[off + c] = ST_LEAF;
+      merged[0] = 1;
+    }
+    // Another sweep can only merge more if an erased child lies in the
+    // prediction stencil (predict_children / axis_stencil, mr_tree.cpp:199-253)
+    // of a level-(l+1) merge candidate that this sweep already evaluated:
+    // that candidate's detail now sees a predicted value. Per axis the
+    // stencil is {p-1, p, p+1}, or one-sided {0,1,2} / {n-3,n-2,n-1} at a
+    // non-periodic wall, so the candidates within reach of child position p
+    // are p-1..p+1 plus 0 (p == 2) or n-1 (p == n-3). Flag merged[1] when
+    // any of them is a candidate (INTERNAL with all-leaf children).
+    if (l + 2 <= g.L) {
+      const long ffoff = g.cell_off[l + 2];
+      const int nff = nf << 1;
+      int pos[3][4];
+      bool okp[3][4];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a >= D) {
+          pos[a][0] = 0, okp[a][0] = true;
+          pos[a][1] = pos[a][2] = pos[a][3] = 0;
+          okp[a][1] = okp[a][2] = okp[a][3] = false;
+          continue;
+        }
+        const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
+        const int p = cc[a];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          int q = p - 1 + t;
+          bool ok = true;
+          if (q < 0 || q >= nf) {
+            if (per) q = (q + nf) % nf;
+            else ok = false;
+          }
+          pos[a][t] = q, okp[a][t] = ok;
+        }
+        pos[a][3] = p == 2 ? 0 : nf - 1;
+        okp[a][3] = !per && nf > 2 && (p == 2 || p == nf - 3);
+      }
+      bool hit = false;
+#pragma unroll
+      for (int tz = 0; tz < (D == 3 ? 4 : 1); ++tz)
+#pragma unroll
+        for (int ty = 0; ty < 4; ++ty)
+#pragma unroll
+          for (int tx = 0; tx < 4; ++tx) {
+            if (!(okp[0][tx] && okp[1][ty] && okp[2][tz])) continue;
+            const int q0 = pos[0][tx], q1 = pos[1][ty], q2 = pos[2][tz];
+            if (st[foff + mr_idx(D, nf, q0, q1, q2)] != ST_INTERNAL) continue;
+            bool all = true;
+            for (int c2 = 0; c2 < (1 << D) && all; ++c2)
+              all = st[ffoff + mr_idx(D, nff, 2 * q0 + (c2 & 1), 2 * q1 + ((c2 >> 1) & 1),
+                                      D == 3 ? 2 * q2 + ((c2 >> 2) & 1) : 0)] == ST_LEAF;
+            hit = hit || all;
+          }
+      if (hit) merged[1] = 1;
+    }
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, const MRLevels& g, int l, double eps,
                                  const double* norms, int* merged,
@@ -644,110 +764,54 @@ __device__ __forceinline__ void coarsen_level_dev(const double* V, uint8_t* st, 
   // One lane per (node, child). Nodes at one level never interact: a merge
   // turns level-(l+1) LEAFs into ABSENT, and merge_allowed only looks for
   // level-(l+1) INTERNAL cells.
-  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv_, long c, bool valid, int ch) {
-    const int l = lv_;
-    const int n = 1 << l, nf = n << 1;
-    const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
-    int cc[3];
-    cc[0] = 2 * idx[0] + (ch & 1);
-    cc[1] = 2 * idx[1] + ((ch >> 1) & 1);
-    cc[2] = D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0;
-    const long fc = foff + mr_idx(D, nf, cc[0], cc[1], cc[2]);
-    // candidate: INTERNAL node whose children are all leaves (mr_tree.cpp:486-497)
-    const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF &&
-                                        row_owned(g, l, mr_row(D, l, c)));
-    double r = 0.0;
-    if (cand) r = child_detail<D>(V, g.total_cells, g, l, idx[0], idx[1], idx[2], ch, norms);
-    r = node_group_max<D>(r);
-    bool allowed = true;
-    if (cand && r < eps) {
-      // merge_allowed (mr_tree.cpp:446-471): no INTERNAL level-(l+1) cell
-      // face-adjacent to the children. This lane checks its child's D outward
-      // neighbours; the 2^d lanes together cover every position.
-#pragma unroll
-      for (int a = 0; a < D; ++a) {  // unrolled: g.bc[] stays in the param space
-        int q[3] = {cc[0], cc[1], cc[2]};
-        q[a] = ((ch >> a) & 1) ? 2 * idx[a] + 2 : 2 * idx[a] - 1;
-        const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
-        if (!per && (q[a] < 0 || q[a] >= nf)) continue;
-        bool fl;
-        q[a] = mr_map(q[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
-        if (st[foff + mr_idx(D, nf, q[0], q[1], q[2])] == ST_INTERNAL) allowed = false;
-      }
-    }
-    const bool merge = node_group_all<D>(cand && r < eps && allowed);
-    if (merge) {
-      // merged q = mean of the children == the projection already stored
-      st[fc] = ST_ABSENT;
-      if (ch == 0) {
-        st[off + c] = ST_LEAF;
-        merged[0] = 1;
-      }
-      // Another sweep can only merge more if an erased child lies in the
-      // prediction stencil (predict_children / axis_stencil, mr_tree.cpp:199-253)
-      // of a level-(l+1) merge candidate that this sweep already evaluated:
-      // that candidate's detail now sees a predicted value. Per axis the
-      // stencil is {p-1, p, p+1}, or one-sided {0,1,2} / {n-3,n-2,n-1} at a
-      // non-periodic wall, so the candidates within reach of child position p
-      // are p-1..p+1 plus 0 (p == 2) or n-1 (p == n-3). Flag merged[1] when
-      // any of them is a candidate (INTERNAL with all-leaf children).
-      if (l + 2 <= g.L) {
-        const long ffoff = g.cell_off[l + 2];
-        const int nff = nf << 1;
-        int pos[3][4];
-        bool okp[3][4];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          if (a >= D) {
-            pos[a][0] = 0, okp[a][0] = true;
-            pos[a][1] = pos[a][2] = pos[a][3] = 0;
-            okp[a][1] = okp[a][2] = okp[a][3] = false;
-            continue;
-          }
-          const bool per = g.bc[2 * a] == AF_BC_PERIODIC;
-          const int p = cc[a];
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            int q = p - 1 + t;
-            bool ok = true;
-            if (q < 0 || q >= nf) {
-              if (per) q = (q + nf) % nf;
-              else ok = false;
-            }
-            pos[a][t] = q, okp[a][t] = ok;
-          }
-          pos[a][3] = p == 2 ? 0 : nf - 1;
-          okp[a][3] = !per && nf > 2 && (p == 2 || p == nf - 3);
-        }
-        bool hit = false;
-#pragma unroll
-        for (int tz = 0; tz < (D == 3 ? 4 : 1); ++tz)
-#pragma unroll
-          for (int ty = 0; ty < 4; ++ty)
-#pragma unroll
-            for (int tx = 0; tx < 4; ++tx) {
-              if (!(okp[0][tx] && okp[1][ty] && okp[2][tz])) continue;
-              const int q0 = pos[0][tx], q1 = pos[1][ty], q2 = pos[2][tz];
-              if (st[foff + mr_idx(D, nf, q0, q1, q2)] != ST_INTERNAL) continue;
-              bool all = true;
-              for (int c2 = 0; c2 < (1 << D) && all; ++c2)
-                all = st[ffoff + mr_idx(D, nff, 2 * q0 + (c2 & 1), 2 * q1 + ((c2 >> 1) & 1),
-                                        D == 3 ? 2 * q2 + ((c2 >> 2) & 1) : 0)] == ST_LEAF;
-              hit = hit || all;
-            }
-        if (hit) merged[1] = 1;
-      }
-    }
+  level_nodes_by_child<D>(g, l, tiles, ntiles, [&](const int lv, long c, bool valid, int ch) {
+    coarsen_node<D>(V, st, g, lv, eps, norms, merged, c, valid, ch, nullptr);
   });
 }
 
+// With kPreV (the previous launch is the next finer level's sweep, which
+// writes only statuses of levels l+1 and l+2), the block's first (node, child)
+// entry evaluates its detail before the PDL wait: values, tile lists and this
+// level's statuses are final, so the stencil loads overlap the previous
+// level's kernel. The candidate and ring tests (level-(l+1) statuses) follow
+// the wait.
 template <int D>
 __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l, double eps,
                                  const double* norms, int* merged,
-    const int* tiles = nullptr, int ntiles = 0) {
+    const int* tiles = nullptr, int ntiles = 0, int pre = 0) {
+  constexpr int NCH = 1 << D;
+  if (!tiles || l < 0 || !(pre & kPreV)) {
+    AF_PDL_ENTRY();
+    coarsen_level_dev<D>(V, st, g, l, eps, norms, merged, tiles, ntiles);
+    return;
+  }
+  const int total = (ntiles < 0 ? g.dcnt[l] : ntiles) * NCH;
+  long c0 = 0;
+  bool valid0 = false;
+  int ch0 = 0;
+  double r0 = 0.0;
+  if ((int)blockIdx.x < total) {  // block-uniform
+    const int ti = blockIdx.x / NCH;
+    node_child_entry<D>(g, l, tiles[ti], blockIdx.x - ti * NCH, &c0, &valid0, &ch0);
+    const int n = 1 << l;
+    if (valid0 && st[g.cell_off[l] + c0] == ST_INTERNAL)
+      r0 = child_detail<D>(V, g.total_cells, g, l, (int)(c0 & (n - 1)), (int)((c0 >> l) & (n - 1)),
+                           D == 3 ? (int)(c0 >> (2 * l)) : 0, ch0, norms);
+    r0 = node_group_max<D>(r0);
+  }
   AF_PDL_ENTRY();
-  coarsen_level_dev<D>(V, st, g, l, eps, norms, merged, tiles, ntiles);
+  for (int it = blockIdx.x; it < total; it += gridDim.x) {
+    if (it == (int)blockIdx.x) {
+      coarsen_node<D>(V, st, g, l, eps, norms, merged, c0, valid0, ch0, &r0);
+    } else {
+      const int ti = it / NCH;
+      long c;
+      bool valid;
+      int ch;
+      node_child_entry<D>(g, l, tiles[ti], it - ti * NCH, &c, &valid, &ch);
+      coarsen_node<D>(V, st, g, l, eps, norms, merged, c, valid, ch, nullptr);
+    }
+  }
 }
 
 // The coarsest levels (at most kTinyCells cells each: 2D up to level 5,

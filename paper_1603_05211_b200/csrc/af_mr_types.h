@@ -76,7 +76,7 @@ __host__ __device__ __forceinline__ bool row_counted(const MRLevels& g, int l, i
 // immediate predecessor still runs (every earlier kernel has completed: a
 // kernel lets its dependents launch only after its own wait). The host sets
 // the bits the predecessor does not write.
-enum : int { kPreList = 1, kPreSt = 2 };  // tile lists + counts, statuses
+enum : int { kPreList = 1, kPreSt = 2, kPreV = 4 };  // tile lists + counts, statuses, values
 
 constexpr int kTileX2 = 32, kTileY2 = 8;
 
