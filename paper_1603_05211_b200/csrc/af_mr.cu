@@ -1433,11 +1433,17 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   wset_(d_mark_, 1, 1, 0, 0, L_);
   AF_ML_LAUNCH(mr_virtual_mark_level, 1, L_, true, d_st_, d_mark_, g_, AF_L);
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
-  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0, d_st_,
-           d_mark_, g_.total_cells, d_red_, g_);
+  // counts and the CFL speed in one pass (mr_cycle_begin ignores the speed
+  // under a fixed dt)
+  if (D_ == 3)
+    launch_k(pdl_, stream_, mr_count_speed_kernel<3>, dim3(grid_for(g_.total_cells)), 256, 0,
+             (const uint8_t*)d_st_, (const uint8_t*)d_mark_, g_.total_cells, d_red_, g_,
+             (const double*)d_V_, cfg_.gamma);
+  else
+    launch_k(pdl_, stream_, mr_count_speed_kernel<2>, dim3(grid_for(g_.total_cells)), 256, 0,
+             (const uint8_t*)d_st_, (const uint8_t*)d_mark_, g_.total_cells, d_red_, g_,
+             (const double*)d_V_, cfg_.gamma);
   ++launches_;
-  if (cfl > 0.0)
-    AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
   launch_k(pdl_, stream_, mr_cycle_begin, dim3(1), 1, 0, d_red_, d_lpl_, L_, D_, cfl, fixed_dt,
            dx_L, d_dt_, d_step3_, d_cycctl_, d_cycrec_, d_red_ + 64, 2 * 17);
   ++launches_;

@@ -908,6 +908,47 @@ static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, l
   }
 }
 
+// mr_count_kernel and, in the same pass over the cells, the CFL rule's max
+// over leaves of sum_a(|v_a|+c) into out[3] (one rank: the cycle graph).
+template <int D>
+__global__ void mr_count_speed_kernel(const uint8_t* st, const uint8_t* mark, long n,
+                                      unsigned long long* out, MRLevels g, const double* V,
+                                      double gamma) {
+  AF_PDL_ENTRY();
+  unsigned long long lv = 0, in = 0, vm = 0;
+  double best = 0.0;
+  const long comp = g.total_cells;
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < n;
+       c += (long)gridDim.x * blockDim.x) {
+    const uint8_t s = st[c];
+    lv += s == ST_LEAF;
+    in += s == ST_INTERNAL;
+    vm += mark[c];
+    if (s == ST_LEAF) {
+      Cons<D> q;
+      q.rho = V[c];
+#pragma unroll
+      for (int a = 0; a < D; ++a) q.m[a] = V[(1 + a) * comp + c];
+      q.E = V[(D + 1) * comp + c];
+      double sum, m;
+      wave_speeds(primitives(q, gamma - 1.0), gamma, sum, m);
+      best = fmax(best, sum);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    in += __shfl_xor_sync(0xffffffffu, in, o);
+    vm += __shfl_xor_sync(0xffffffffu, vm, o);
+  }
+  best = warp_max(best);
+  if ((threadIdx.x & 31) == 0) {
+    if (lv) atomicAdd(out, lv);
+    if (in) atomicAdd(out + 1, in);
+    if (vm) atomicAdd(out + 2, vm);
+    if (best > 0.0) atomicMax(out + 3, dbits(best));
+  }
+}
+
 // Max over leaves of sum_a(|v_a|+c) (CFL rule) for the leaves of level l.
 template <int D>
 __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevels g, int l,
