@@ -693,9 +693,25 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLeve
         }
     if (in_band && !tile_in_region<D>(g, l, tc[D - 1] * (D == 3 ? kTileZ3 : kTileY2)))
       in_band = false;
-    if (in_band) band[g.tile_off[l] + atomicAdd(counts + l, 1)] = (int)t;
-    if (tflag[tg] & 1) leaf[g.tile_off[l] + atomicAdd(counts + 17 + l, 1)] = (int)t;
-    if (tleaf[tg]) atomicAdd(leaves_per_level + l, (unsigned long long)tleaf[tg]);
+    // list appends aggregated over the lanes of a warp on the same level (one
+    // atomic per group: at L=13 a per-tile atomic on one counter serialises)
+    const unsigned grp = __match_any_sync(__activemask(), l);
+    const int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
+    const unsigned below = (1u << lane) - 1u;
+    const bool in_leaf = (tflag[tg] & 1) != 0;
+    const unsigned bb = __ballot_sync(grp, in_band) & grp;
+    const unsigned lb = __ballot_sync(grp, in_leaf) & grp;
+    const unsigned nl = __reduce_add_sync(grp, (unsigned)tleaf[tg]);
+    int bbase = 0, lbase = 0;
+    if (lane == leader) {
+      if (bb) bbase = atomicAdd(counts + l, __popc(bb));
+      if (lb) lbase = atomicAdd(counts + 17 + l, __popc(lb));
+      if (nl) atomicAdd(leaves_per_level + l, (unsigned long long)nl);
+    }
+    bbase = __shfl_sync(grp, bbase, leader);
+    lbase = __shfl_sync(grp, lbase, leader);
+    if (in_band) band[g.tile_off[l] + bbase + __popc(bb & below)] = (int)t;
+    if (in_leaf) leaf[g.tile_off[l] + lbase + __popc(lb & below)] = (int)t;
   }
 }
 
