@@ -776,11 +776,24 @@ void MR::counts(long* leaves, long* nodes, long* internals) {
 // counts (leaves, nodes incl. virtual) and the CFL speed in one synchronisation
 void MR::cycle_stats_(long* leaves, long* nodes, double* smax) {
   AF_CUDA(cudaMemsetAsync(d_red_, 0, sizeof(unsigned long long) * 4, stream_));
-  launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0,
-      d_st_, virtuals_ ? d_mark_ : nullptr, g_.total_cells, d_red_, g_);
-  ++launches_;
-  if (smax)
-    AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
+  const uint8_t* vm = virtuals_ ? d_mark_ : nullptr;
+  if (!g_.dist) {  // one pass over the cells
+    if (D_ == 3)
+      launch_k(pdl_, stream_, mr_count_speed_kernel<3>, dim3(grid_for(g_.total_cells)), 256, 0,
+               (const uint8_t*)d_st_, vm, g_.total_cells, d_red_, g_, (const double*)d_V_,
+               cfg_.gamma, smax ? 1 : 0);
+    else
+      launch_k(pdl_, stream_, mr_count_speed_kernel<2>, dim3(grid_for(g_.total_cells)), 256, 0,
+               (const uint8_t*)d_st_, vm, g_.total_cells, d_red_, g_, (const double*)d_V_,
+               cfg_.gamma, smax ? 1 : 0);
+    ++launches_;
+  } else {
+    launch_k(pdl_, stream_, mr_count_kernel, dim3(grid_for(g_.total_cells)), 256, 0, d_st_, vm,
+             g_.total_cells, d_red_, g_);
+    ++launches_;
+    if (smax)
+      AF_ML_LAUNCH(mr_leaf_speed_kernel, 0, L_, true, d_V_, d_st_, g_, AF_L, cfg_.gamma, d_red_ + 3);
+  }
   unsigned long long h[4];
   AF_CUDA(cudaMemcpyAsync(h, d_red_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
@@ -1438,11 +1451,11 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   if (D_ == 3)
     launch_k(pdl_, stream_, mr_count_speed_kernel<3>, dim3(grid_for(g_.total_cells)), 256, 0,
              (const uint8_t*)d_st_, (const uint8_t*)d_mark_, g_.total_cells, d_red_, g_,
-             (const double*)d_V_, cfg_.gamma);
+             (const double*)d_V_, cfg_.gamma, 1);
   else
     launch_k(pdl_, stream_, mr_count_speed_kernel<2>, dim3(grid_for(g_.total_cells)), 256, 0,
              (const uint8_t*)d_st_, (const uint8_t*)d_mark_, g_.total_cells, d_red_, g_,
-             (const double*)d_V_, cfg_.gamma);
+             (const double*)d_V_, cfg_.gamma, 1);
   ++launches_;
   launch_k(pdl_, stream_, mr_cycle_begin, dim3(1), 1, 0, d_red_, d_lpl_, L_, D_, cfl, fixed_dt,
            dx_L, d_dt_, d_step3_, d_cycctl_, d_cycrec_, d_red_ + 64, 2 * 17);

@@ -908,12 +908,12 @@ static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, l
   }
 }
 
-// mr_count_kernel and, in the same pass over the cells, the CFL rule's max
-// over leaves of sum_a(|v_a|+c) into out[3] (one rank: the cycle graph).
+// mr_count_kernel and, in the same pass over the cells (with `speed`), the
+// CFL rule's max over leaves of sum_a(|v_a|+c) into out[3] (one rank).
 template <int D>
 __global__ void mr_count_speed_kernel(const uint8_t* st, const uint8_t* mark, long n,
                                       unsigned long long* out, MRLevels g, const double* V,
-                                      double gamma) {
+                                      double gamma, int speed) {
   AF_PDL_ENTRY();
   unsigned long long lv = 0, in = 0, vm = 0;
   double best = 0.0;
@@ -923,8 +923,8 @@ __global__ void mr_count_speed_kernel(const uint8_t* st, const uint8_t* mark, lo
     const uint8_t s = st[c];
     lv += s == ST_LEAF;
     in += s == ST_INTERNAL;
-    vm += mark[c];
-    if (s == ST_LEAF) {
+    if (mark) vm += mark[c];
+    if (speed && s == ST_LEAF) {
       Cons<D> q;
       q.rho = V[c];
 #pragma unroll
