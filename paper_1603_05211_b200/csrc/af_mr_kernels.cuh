@@ -441,7 +441,6 @@ __device__ __forceinline__ void level_nodes_by_child(const MRLevels& g, int l, c
                                                      int ntiles, F&& f) {
   constexpr int NCH = 1 << D;
   if (tiles) {
-    constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
     for_each_tile(g, l, tiles, ntiles, NCH, [&](int lv, int t, int r) {
       long c;
       bool valid;

@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
 
   const double sdt = a.dt_dev ? a.dt_scale * *a.dt_dev : a.sdt;  // 0.5 * dt, 1.0 * dt == dt
   const int step3 = a.step3_dev ? *a.step3_dev : a.step3;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const long comp = g.total_cells;
   const double gamma = a.gamma, gm1 = a.gm1;
   const double rgm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rcp
