@@ -196,13 +196,27 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int ntotal = tile_total(g, l, a.ntiles);
   const int lcode = l;
   TileWalker walk(g, lcode < 0 ? lcode : -1, a.ntiles);  // (used in multi-level mode only)
+  // per-level max wave speed of this block's leaves: a warp max and one atomic
+  // per warp when the level changes (non-negative doubles order like their bits)
+  double wave = 0.0;
+  int wave_l = -1;
+  auto flush_wave = [&] {
+    if (wave_l < 0) return;
+    for (int o = 16; o > 0; o >>= 1) wave = fmax(wave, __shfl_xor_sync(0xffffffffu, wave, o));
+    if (lane == 0 && wave > 0.0)
+      atomicMax(a.wave + wave_l, (unsigned long long)__double_as_longlong(wave));
+    wave = 0.0;
+  };
   for (int it = blockIdx.x; it < ntotal; it += gridDim.x) {
   const int t = lcode < 0 ? walk.at(g, a.tiles, it, &l) : tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
   const int n = 1 << l;
   const long off = g.cell_off[l];
   const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
   const double inv_dx = g.inv_dx[l];
-  double wave = 0.0;
+  if (l != wave_l) {  // block-uniform: the tiles of a block come in level order
+    flush_wave();
+    wave_l = l;
+  }
   const int sx = ilog2i(ntx), sy = ilog2i(nty);  // powers of two
   const int x0 = (t & (ntx - 1)) * TX, y0 = ((t >> sx) & (nty - 1)) * TY;
   const int z0 = D == 3 ? (t >> (sx + sy)) * TZ : 0;
@@ -474,13 +488,9 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       }
     }
   }
-  // per-level max wave speed of this tile: warp max, one atomic per warp
-  // (non-negative doubles order like their bit patterns)
-  for (int o = 16; o > 0; o >>= 1) wave = fmax(wave, __shfl_xor_sync(0xffffffffu, wave, o));
-  if (lane == 0 && wave > 0.0)
-    atomicMax(a.wave + l, (unsigned long long)__double_as_longlong(wave));
   __syncthreads();  // the next tile reuses the shared-memory staging
   }
+  flush_wave();
   if (bad) atomicOr(&s_bad, bad);
   if (nfb) atomicAdd(&s_fb, nfb);
   __syncthreads();
