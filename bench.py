@@ -1,17 +1,18 @@
 #!/usr/bin/env python3
 """bench.py — throughput of the B200 MR/FV Euler hot path (and the reference arm).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg3|cfg4|cfg1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4|cfg2|cfg3|cfg1|cfg5]
     python bench.py --impl reference ...      # the reference's own CPU path
 
-Default workload: "cfg2" (BASELINE.json configs[1], the config the metric is
-quoted on): 2D MR, finest level 10 (1024^2), coarsest leaf level 3, level
-thresholds 1e-3*2^(2(l-L)), global time step, CFL 0.5, seeded four-quadrant
-Riemann data. A "step" is one run_mr cycle (refine, virtual leaves, the RK2
-step, coarsen); the default K is the config's own step count (cfg2: 500).
-Metric: leaf-cell RK-stage updates / s (BASELINE.json metric). The uniform
-workloads (cfg1, cfg4) time RK2 steps over the whole mesh. Multi-GPU
-(torchrun): slabs with NCCL halo exchange.
+Default workload: "cfg4" (BASELINE.json configs[3]), the largest config that
+fits one GPU and the one north_star's scaling target names: 3D Euler on the
+uniform 512^3 mesh, fp64, seeded ellipsoid, outflow BCs, MUSCL/minmod +
+AUSM+ + RK2, CFL 0.4. A "step" is one RK2 step over the whole mesh (two fused
+stage launches); the default K is the config's own 100 steps. The state (5.4
+GB) is far larger than L2, so no flush is needed between steps. The metric
+is BASELINE.json's: leaf-cell RK-stage updates / s. The MR workloads (cfg2,
+cfg3) time run_mr cycles (refine, virtual leaves, the RK2 step, coarsen).
+Multi-GPU (torchrun): slabs with NCCL halo exchange.
 
 Rank 0 prints ONE JSON line.
 """
@@ -142,23 +143,67 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU legs -----
+CORE_RATE_3D = 4.5e6   # reference cell-stage updates/s per core on the 3D path (r01 B200 host)
+PLANE_BYTES_3D = 4 * 40  # u, step_block's mid, rk2_stage's rhs and w per ghosted cell
+
+
+def window_plan(n: int, threads: int, steps: int, budget_s: float):
+    """z-window of the n^3 mesh the multi-core reference arm steps: the whole
+    mesh when K steps fit the time budget and host memory, else the largest
+    centred window that does (a multiple of the thread count)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16e9
+    per_plane = PLANE_BYTES_3D * (n + 4) ** 2
+    mem_planes = int(0.5 * avail / per_plane) - 4 * threads
+    time_planes = int(budget_s * threads * CORE_RATE_3D / (2.0 * n * n * max(1, steps)))
+    nz = max(threads, min(n, mem_planes, time_planes))
+    nz = max(threads, nz - nz % threads)
+    return (n - nz) // 2, nz
+
+
 def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, threads: int,
-                       level_override: int | None = None):
+                       level_override: int | None = None, budget_s: float = 150.0):
     """Times the CPU implementation (`kind` "reference" = oracle/_ref, the
     reference library compiled from its own sources; "port" = the C
-    restatement) on a bounded sample of the workload: the same generator and
-    scheme at a smaller level (per-cell work of a uniform mesh is
-    size-independent), `threads` independent copies run concurrently (the
-    reference is single-threaded). Returns (rate, sample description)."""
+    restatement). Returns (rate, sample description, wall, ran) where `ran`
+    says exactly what was stepped.
+
+    3D uniform (cfg4): the config's own n^3 mesh, or a centred z-window of it
+    when K steps of the whole mesh would not fit `budget_s`, split into one
+    z-slab per thread, each stepped by the reference's own step_block
+    (oracle/ref_harness.cpp afref_uniform_window_run; bit-identical to the
+    single-domain run on the whole mesh). Other workloads: `threads`
+    independent single-threaded copies of the same generator at a smaller
+    level (MR: the reference's from_uniform + coarsen takes minutes at L >= 8)."""
     from oracle import oracle as O
     _, case, dim, level, cfl, seed, _ = WORKLOADS[workload]
     is_mr = workload in MR_OPTS
+    if dim == 3 and not is_mr and kind == "reference" and level_override is None:
+        n = 1 << level
+        z0, nz = window_plan(n, threads, steps + min(warmup, 1), budget_s)
+        init = O.window_init(case, seed, level, z0, nz)
+        p = O.make_params(dim, level, steps, cfl=cfl)
+        _, res = O.uniform_window_run(p, init, z0, nz, threads, min(warmup, 1))
+        if res["err_kind"]:
+            raise RuntimeError(res["err"])
+        wall = res["wall_seconds"]
+        work = nz * n * n * 2 * steps
+        whole = nz == n
+        ran = {"mesh": f"{n}x{n}x{n}", "z_window": [z0, z0 + nz], "whole_mesh": whole,
+               "threads": threads, "steps_timed": steps, "warmup_steps": min(warmup, 1)}
+        sample = (f"{'the whole' if whole else f'z-planes [{z0},{z0 + nz}) of the'} "
+                  f"{n}^3 {workload} mesh ({nz * n * n} cells), split into {threads} z-slabs, "
+                  f"one thread each running the reference's step_block (unigrid.cpp:39) with "
+                  f"neighbour ghost planes between stages; {steps} RK2 steps timed after "
+                  f"{min(warmup, 1)} warm-up; steady_clock around the step loop; value = "
+                  f"cell RK-stage updates / s")
+        return work / wall, sample, wall, ran
     if level_override is not None:
         lvl = level_override
     elif is_mr:
-        # The reference's from_uniform + coarsen (its recursive predictions)
-        # takes minutes at L >= 8 for cfg2's level thresholds, so the bounded
-        # sample uses L=7 (cfg2) / L=8 (cfg3); the timed loop excludes the build.
         lvl = {"cfg2": 7, "cfg3": 8, "cfg5": 5}[workload]
     else:
         lvl = 7 if dim == 3 else level
@@ -180,8 +225,6 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
 
     def one(i):
         if is_mr:
-            # warm-up cycles then the timed cycles, continuing is not exposed by
-            # the harness: time `steps` cycles from the start after a warm-up run
             if warmup:
                 O.mr_run(lib_kind, params(warmup), init)
             _, _, cyc, _, res = O.mr_run(lib_kind, params(steps), init)
@@ -201,11 +244,14 @@ def reference_cpu_rate(kind: str, workload: str, steps: int, warmup: int, thread
     wall = max(r["wall_seconds"] for r in results)
     rate = sum(work) / wall
     what = "MR cycles (refine/evolve/coarsen)" if is_mr else "RK2 steps"
+    n = 1 << lvl
+    ran = {"mesh": "x".join([str(n)] * dim), "finest_level": lvl, "copies": threads,
+           "threads": threads, "steps_timed": steps, "warmup_steps": warmup}
     sample = (f"{threads} independent single-threaded copies of the {workload} generator at "
               f"level {lvl} ({cells} finest cells), {steps} {what} each after {warmup} "
               f"warm-up; steady_clock around the step loop only (unigrid.cpp:31-48, "
               f"mr_solver.cpp:339-395); value = leaf-cell RK-stage updates / s")
-    return rate, sample, wall
+    return rate, sample, wall, ran
 
 
 def host_threads(req: int) -> int:
@@ -227,9 +273,9 @@ def run_reference_arm(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle libraries not built"}))
         return
     threads = host_threads(args.cpu_threads)
-    rate, sample, wall = reference_cpu_rate(kind, args.workload, max(1, args.steps),
-                                            max(0, args.warmup), threads,
-                                            level_override=args.ref_level)
+    rate, sample, wall, ran = reference_cpu_rate(kind, args.workload, max(1, args.steps),
+                                                 max(0, args.warmup), threads,
+                                                 level_override=args.ref_level)
     idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 0,
@@ -238,7 +284,7 @@ def run_reference_arm(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload, 1),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads,
-                         "kind": kind, "sample": sample},
+                         "kind": kind, "sample": sample, "ran": ran},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -278,7 +324,7 @@ def main():
                          "cycles, cfg4's 100 steps)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
     ap.add_argument("--level", type=int, default=None,
                     help="run the workload at another finest level (not the config's own)")
     ap.add_argument("--mr-multi", default="auto", choices=["auto", "slabs", "replicas"],
@@ -440,9 +486,10 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
             from oracle import oracle as O
             kind = "reference" if O.available("ref") else "port"
             threads = host_threads(args.cpu_threads)
-            rate, sample, _ = reference_cpu_rate(kind, args.workload, 2, 1, threads)
+            rate, sample, _, ran = reference_cpu_rate(kind, args.workload, 2, 1, threads,
+                                                      budget_s=20.0)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-                   "sample": sample}
+                   "sample": sample, "ran": ran}
         except Exception as e:  # the CPU leg must not sink the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"unavailable: {e}"}
@@ -598,8 +645,9 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
             from oracle import oracle as O
             kind = "reference" if O.available("ref") else "port"
             threads = host_threads(args.cpu_threads)
-            rate, sample, _ = reference_cpu_rate(kind, args.workload, 8, 2, threads)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+            rate, sample, _, ran = reference_cpu_rate(kind, args.workload, 8, 2, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+                   "ran": ran}
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"unavailable: {e}"}

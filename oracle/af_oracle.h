@@ -65,6 +65,18 @@ int afo_uniform_run(const af_oracle_params* p, const double* init, double* out,
                     double* dt_hist, af_oracle_result* res);
 
 /*
+ * The uniform 3D run on the window z in [z0, z0+nz) of the n^3 mesh, split
+ * into `threads` z-slabs that each call the reference's step_block on their
+ * own BlockData (ref_harness.cpp; bench.py's multi-core CPU arm). init: the
+ * (nz+4) planes z0-2 .. z0+nz+1 clamped into the mesh, AoS. n_warm untimed
+ * steps, then p->n_steps timed ones (res->wall_seconds). out: nz planes
+ * (nullable). With z0 = 0, nz = n this is afref_uniform_run bit for bit.
+ */
+int afref_uniform_window_run(const af_oracle_params* p, int z0, int nz, int threads,
+                             long n_warm, const double* init, double* out,
+                             af_oracle_result* res);
+
+/*
  * MR / MRLT run (mr_solver.cpp:318-400 loop). out: to_uniform(L) of the final
  * tree (n^dim*5). leaf_keys: sorted pack_key leaves of the final tree
  * (capacity *n_leaves on entry, count on exit; nullable). per_cycle: for each

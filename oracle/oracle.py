@@ -85,6 +85,8 @@ def _load(kind: str):
             ("snapshot_copy", [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]),
             ("restrict", [C.c_int, C.c_int, C.c_int, dp, dp]),
             ("l1_error", [C.c_int, C.c_int, C.c_double, dp, C.c_int, dp, dp]),
+            ("uniform_window_run", [C.POINTER(Params), C.c_int, C.c_int, C.c_int, C.c_long,
+                                    dp, dp, C.POINTER(Result)]),
         ]:
             f = getattr(lib, "afref_" + name)
             f.argtypes = args
@@ -143,6 +145,28 @@ def uniform_run(kind: str, params: Params, init: np.ndarray):
     fn = lib.afref_uniform_run if kind == "ref" else lib.afo_uniform_run
     fn(C.byref(params), _dp(np.ascontiguousarray(init)), _dp(out), _dp(dts), C.byref(res))
     return out, dts[: params.n_steps], res.as_dict()
+
+
+def window_init(kind: int, seed: int, level: int, z0: int, nz: int) -> np.ndarray:
+    """The planes z0-2 .. z0+nz+1 (clamped into the mesh) of the seeded 3D
+    initial state, as afref_uniform_window_run takes them."""
+    n = 1 << level
+    lo, hi = max(0, z0 - 2), min(n, z0 + nz + 2)
+    return case_fill(kind, seed, level, z0=lo, nz=hi - lo)
+
+
+def uniform_window_run(params: Params, init: np.ndarray, z0: int, nz: int, threads: int,
+                       n_warm: int = 0, want_out: bool = False):
+    """The reference's step_block on `threads` z-slabs of the window
+    [z0, z0+nz) of the 3D mesh (ref_harness.cpp). Returns (out or None, result)."""
+    lib = _load("ref")
+    n = 1 << params.level
+    out = np.zeros((nz * n * n, 5)) if want_out else None
+    res = Result()
+    lib.afref_uniform_window_run(C.byref(params), z0, nz, threads, n_warm,
+                                 _dp(np.ascontiguousarray(init)),
+                                 _dp(out) if want_out else None, C.byref(res))
+    return out, res.as_dict()
 
 
 def mr_run(kind: str, params: Params, init: np.ndarray, max_cycles: int | None = None,

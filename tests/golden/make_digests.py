@@ -1,0 +1,100 @@
+"""Writes tests/golden/digest_*.npz: digests (tests/digests.py) of the
+COMPILED REFERENCE (oracle/_ref, built from /root/reference sources by
+oracle/Makefile) run on BASELINE.json's configs at their own sizes, or at the
+largest size the single-threaded reference finishes here (SURVEY.md §8(c)
+oracle limits). Run in the build container, where /root/reference exists:
+
+    python tests/golden/make_digests.py [name ...]      # default: all
+
+The GPU tests (tests/test_digests_gpu.py) run the CUDA path on the same
+seeded inputs and compare against these files; /root/reference is never read
+on the GPU box.
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from oracle import oracle as O  # noqa: E402
+import digests as D  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def eps_levels(eps, L, d):
+    return [eps * 2.0 ** (d * (l - L)) for l in range(L + 1)]
+
+
+# name: dict(kind, seed, level, steps, cfl, [MR: eps, eps_level, min_leaf, local_time, gap],
+#            coarse = level of the stored averaged state)
+DIGESTS = {
+    # cfg1 at its own size: 2D uniform 256^2, 200 steps
+    "cfg1": dict(kind=0, seed=1, level=8, steps=200, cfl=0.5, coarse=6),
+    # cfg2 at its own size: 2D MR L=10, level thresholds, min leaf 3, 500 cycles
+    "cfg2": dict(kind=0, seed=1, level=10, steps=500, cfl=0.5, eps=1e-3,
+                 eps_level=eps_levels(1e-3, 10, 2), min_leaf=3, local_time=0, gap=3,
+                 coarse=6),
+    # cfg4 generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of reference time)
+    "cfg4_128": dict(kind=2, seed=1, level=7, steps=100, cfl=0.4, coarse=4),
+    # cfg3 generator, MRLT at L=10 (steps count finest-level steps: 32 = four
+    # macro-cycles of 2^gap fine steps) and one L=13 macro-cycle
+    "cfg3_L10": dict(kind=1, seed=1, level=10, steps=32, cfl=0.5, eps=1e-3, eps_level=None,
+                     min_leaf=0, local_time=1, gap=3, coarse=6),
+    "cfg3_L13": dict(kind=1, seed=1, level=13, steps=8, cfl=0.5, eps=1e-3, eps_level=None,
+                     min_leaf=0, local_time=1, gap=3, coarse=6),
+    # cfg5 rules at L=7: 3D MRLT, level thresholds 1e-3*2^(3(l-L)), coarsest 16^3
+    # (min leaf 4, gap L-4), pressure-ratio ellipsoid
+    "cfg5_L7": dict(kind=3, seed=1, level=7, steps=32, cfl=0.4, eps=1e-3,
+                    eps_level=eps_levels(1e-3, 7, 3), min_leaf=4, local_time=1, gap=3,
+                    coarse=4),
+}
+
+BITMAP_MAX_CELLS = 1 << 21
+
+
+def run(name, c):
+    dim = 3 if c["kind"] >= 2 else 2
+    init = O.case_fill(c["kind"], c["seed"], c["level"])
+    t0 = time.time()
+    rec = dict(name=name, kind=c["kind"], seed=c["seed"], level=c["level"], steps=c["steps"],
+               cfl=c["cfl"], coarse_level=c["coarse"], dim=dim)
+    if "eps" in c:
+        p = O.make_params(dim, c["level"], c["steps"], cfl=c["cfl"], eps=c["eps"],
+                          eps_level=c["eps_level"], min_leaf_level=c["min_leaf"],
+                          local_time=c["local_time"], lt_gap=c["gap"])
+        out, keys, cyc, dts, res = O.mr_run("ref", p, init)
+        rec.update(mr=1, eps=c["eps"], has_eps_level=int(c["eps_level"] is not None),
+                   eps_level=np.array(c["eps_level"] or [0.0]), min_leaf=c["min_leaf"],
+                   local_time=c["local_time"], gap=c["gap"], cycles=cyc, dt=dts,
+                   keys_sha=D.keys_sha(keys), n_keys=len(keys),
+                   leaves_per_level=D.leaves_per_level(keys, c["level"]))
+        if init.shape[0] <= BITMAP_MAX_CELLS:
+            rec["leaf_bitmaps"] = D.leaf_bitmaps(keys, dim, c["level"])
+            assert np.array_equal(D.bitmaps_to_keys(rec["leaf_bitmaps"], dim, c["level"]), keys)
+    else:
+        p = O.make_params(dim, c["level"], c["steps"], cfl=c["cfl"])
+        out, dts, res = O.uniform_run("ref", p, init)
+        rec.update(mr=0, dt=dts, max_wave_speed=res["max_wave_speed"])
+    assert res["err_kind"] == 0, res["err"]
+    rec.update(max_cfl=res["max_cfl"], fallbacks=res["fallbacks"],
+               state_sha=D.state_sha(out), state_l1=D.state_l1(out),
+               coarse=D.coarse(out, dim, c["level"], c["coarse"]),
+               ref_wall_s=time.time() - t0)
+    np.savez_compressed(os.path.join(HERE, f"digest_{name}.npz"), **rec)
+    print(f"{name}: {time.time() - t0:.0f} s, max_cfl {res['max_cfl']:.6f}"
+          + (f", {len(keys)} leaves" if rec["mr"] else ""), flush=True)
+
+
+def main():
+    O.build()
+    names = sys.argv[1:] or list(DIGESTS)
+    for n in names:
+        run(n, DIGESTS[n])
+
+
+if __name__ == "__main__":
+    main()
