@@ -282,7 +282,7 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, 1),
+        "config": workload_config(args.workload, 1, args.numerics),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads,
                          "kind": kind, "sample": sample, "ran": ran},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -290,7 +290,13 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(workload, n_gpus):
+NUMERICS = {"tolerance": "tolerance: within 1e-10 relative L1 per field of the bit-exact result "
+                         "(BASELINE.json north_star bar; reciprocal estimates + FMA, "
+                         "tests/test_tolerance_gpu.py)",
+            "exact": "bit-exact (--fmad=false, the reference's operations)"}
+
+
+def workload_config(workload, n_gpus, numerics="exact"):
     idx, case, dim, level, cfl, seed, steps = WORKLOADS[workload]
     n = 1 << level
     c = {"workload": f"{workload}: BASELINE.json configs[{idx}]",
@@ -299,7 +305,9 @@ def workload_config(workload, n_gpus):
          "bc": "outflow",
          "l2": "inputs larger than L2 (no flush)" if (n ** dim) * 40 > 126e6
                else "working set fits in L2 (latency-bound config)",
-         "parity_mode": "bit-exact (--fmad=false)"}
+         "parity_mode": NUMERICS["exact"]}
+    if dim == 3 and workload not in MR_OPTS:
+        c["parity_mode"] = NUMERICS[numerics]
     if BASE_LEVEL.get(workload, level) != level:
         c["level_override"] = f"finest level {level} instead of the config's {BASE_LEVEL[workload]}"
     if workload in MR_OPTS:
@@ -335,6 +343,12 @@ def main():
     ap.add_argument("--ref-level", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-other-numerics", action="store_true")
+    ap.add_argument("--numerics", default="tolerance", choices=["tolerance", "exact"],
+                    help="3D uniform stage numerics: 'tolerance' (reciprocal estimates + FMA, "
+                         "within BASELINE.json's 1e-10 relative L1 per field of the exact result; "
+                         "tests/test_tolerance_gpu.py) or 'exact' (bit-identical to the "
+                         "reference). The other mode is timed too and reported beside it.")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = WORKLOADS[args.workload][6]
@@ -392,6 +406,8 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
     idx, case, dim, level, cfl, seed, _ = WORKLOADS[args.workload]
     solver = U.UniformSolver(dim, level, scheme=U.SchemeConfig(limiter=U.MINMOD),
                              device=local, comm=comm)
+    tol = dim == 3 and args.numerics == "tolerance"
+    solver.set_numerics(tol)
     # A dedicated (non-default) stream: the solver's kernels and the timing
     # events must be on the same stream.
     stream = torch.cuda.Stream(device=local)
@@ -458,6 +474,26 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
                "what": "one run_uniform-equivalent call: upload of the initial state from "
                        "pinned host memory, K steps, download of the final state"}
 
+    # ---- the other 3D numerics mode, same steps, for reference ---------------
+    other = None
+    if dim == 3 and not args.no_other_numerics:
+        solver.set_numerics(not tol)
+        solver.upload(init_dev)
+        solver.run(max(1, args.warmup), cfl=cfl, collect=False)
+        barrier()
+        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        o0.record(stream)
+        solver.run(args.steps, cfl=cfl, collect=False)
+        o1.record(stream)
+        barrier()
+        oms = max_over_ranks(o0.elapsed_time(o1))
+        solver.set_numerics(tol)
+        oname = "exact" if tol else "tolerance"
+        other = {"numerics": NUMERICS[oname], "value": cells_total * 2 * args.steps / (oms / 1e3),
+                 "unit": UNIT, "ms_per_step": oms / args.steps,
+                 "kernel": "fv3d_stage (legacy 32x8 tile)" if oname == "exact" else
+                           "fv3d_tile<16x15, tolerance>"}
+
     if rank != 0:
         return None
 
@@ -476,7 +512,8 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-            "kernel": "fv3d_stage" if dim == 3 else "fv2d_stage",
+            "kernel": ("fv3d_tile<16x15, tolerance>" if tol else "fv3d_stage") if dim == 3
+                      else "fv2d_stage",
             "fp64": fp64_info(),
             "note": "fp64-ALU bound in parity mode (no FMA contraction); see DESIGN.md"}
 
@@ -498,9 +535,9 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args.workload, world),
+        "data": "synthetic", "config": workload_config(args.workload, world, args.numerics),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clocks,
+        "clocks": clocks, "other_numerics": other,
     }
     return line
 

@@ -134,6 +134,15 @@ typedef struct af_uniform af_uniform;
 af_status af_uniform_create(const af_config* cfg, af_comm* comm, af_uniform** out);
 af_status af_uniform_destroy(af_uniform* u);
 af_status af_uniform_set_stream(af_uniform* u, void* cuda_stream);
+/* Numerics of the 3D RK2 stage (the reference has one: its own operations).
+ * AF_NUMERICS_EXACT (default): the reference's operations in its association
+ * order without FMA contraction, bit-identical to step_block (step.cpp:93-109).
+ * AF_NUMERICS_TOLERANCE: reciprocal/rsqrt estimates with Newton corrections
+ * and FMA contraction; within BASELINE.json's 1e-10 relative L1 per field of
+ * the exact result (tests/test_tolerance_gpu.py), not bit-identical. 2D and
+ * MUSCL-Hancock steps always run exact. */
+enum { AF_NUMERICS_EXACT = 0, AF_NUMERICS_TOLERANCE = 1 };
+af_status af_uniform_set_numerics(af_uniform* u, int numerics);
 af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz);
 
 /* AoS state transfer of the rank's slab (host or device pointer). */
@@ -220,6 +229,13 @@ af_status af_mr_build(af_mr* m, const double* aos);
 /* MRTree::refine (mr_tree.cpp:361-402); top >= 0 applies the LT buffer
  * radii of mr_solver.cpp:358-362 for that top level. */
 af_status af_mr_refine(af_mr* m, int top);
+/* MRTree::refine(double eps, const std::vector<int>& buffer_radius_per_level)
+ * (mr_tree.hpp:141, mr_tree.cpp:361-402): threshold eps at every level (the
+ * instance's level table is not used), and the split set dilated by
+ * buffer[l] same-level leaves (Chebyshev radius) at level l; n = 0 (no
+ * buffer) dilates nothing. Distributed instances reject radii above their
+ * halo depth (AF_E_CONFIG). */
+af_status af_mr_refine_buffer(af_mr* m, double eps, const int* buffer_radius_per_level, int n);
 af_status af_mr_add_virtual_leaves(af_mr* m);
 af_status af_mr_remove_virtual_leaves(af_mr* m);
 af_status af_mr_coarsen(af_mr* m);

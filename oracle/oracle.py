@@ -87,6 +87,8 @@ def _load(kind: str):
             ("l1_error", [C.c_int, C.c_int, C.c_double, dp, C.c_int, dp, dp]),
             ("uniform_window_run", [C.POINTER(Params), C.c_int, C.c_int, C.c_int, C.c_long,
                                     dp, dp, C.POINTER(Result)]),
+            ("mr_refine_once", [C.POINTER(Params), dp, C.c_double, C.POINTER(C.c_int), C.c_int,
+                                dp, C.POINTER(C.c_uint64), C.POINTER(C.c_long)]),
         ]:
             f = getattr(lib, "afref_" + name)
             f.argtypes = args
@@ -167,6 +169,22 @@ def uniform_window_run(params: Params, init: np.ndarray, z0: int, nz: int, threa
                                  _dp(np.ascontiguousarray(init)),
                                  _dp(out) if want_out else None, C.byref(res))
     return out, res.as_dict()
+
+
+def ref_mr_refine_once(params: Params, init: np.ndarray, eps: float, buffer):
+    """The reference's MRTree::refine(eps, buffer) once on run_mr's starting
+    tree: (to_uniform(L), sorted leaf keys)."""
+    lib = _load("ref")
+    out = np.zeros_like(init)
+    keys = np.zeros(init.shape[0] + 1, dtype=np.uint64)
+    nl = C.c_long(keys.shape[0])
+    buf = (C.c_int * max(1, len(buffer)))(*[int(b) for b in buffer])
+    rc = lib.afref_mr_refine_once(C.byref(params), _dp(np.ascontiguousarray(init)), eps, buf,
+                                  len(buffer), _dp(out),
+                                  keys.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(nl))
+    if rc:
+        raise RuntimeError("afref_mr_refine_once failed")
+    return out, keys[: nl.value].copy()
 
 
 def mr_run(kind: str, params: Params, init: np.ndarray, max_cycles: int | None = None,

@@ -77,6 +77,7 @@ SIGNATURES = {
     "af_uniform_create": (C.c_int, [C.POINTER(Config), _vp, C.POINTER(_vp)]),
     "af_uniform_destroy": (C.c_int, [_vp]),
     "af_uniform_set_stream": (C.c_int, [_vp, _vp]),
+    "af_uniform_set_numerics": (C.c_int, [_vp, C.c_int]),
     "af_uniform_local_extent": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "af_uniform_upload": (C.c_int, [_vp, _vp]),
     "af_uniform_download": (C.c_int, [_vp, _vp]),
@@ -98,6 +99,7 @@ SIGNATURES = {
     "af_mr_set_stream": (C.c_int, [_vp, _vp]),
     "af_mr_build": (C.c_int, [_vp, _vp]),
     "af_mr_refine": (C.c_int, [_vp, C.c_int]),
+    "af_mr_refine_buffer": (C.c_int, [_vp, C.c_double, C.POINTER(C.c_int), C.c_int]),
     "af_mr_add_virtual_leaves": (C.c_int, [_vp]),
     "af_mr_remove_virtual_leaves": (C.c_int, [_vp]),
     "af_mr_coarsen": (C.c_int, [_vp]),

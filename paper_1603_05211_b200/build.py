@@ -17,10 +17,13 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libafgpu.so")
 
-SOURCES = ["af_abi.cu", "af_uniform.cu", "af_mr.cu", "af_mr_dist.cu", "af_io.cu"]
+SOURCES = ["af_abi.cu", "af_uniform.cu", "af_fv3d_tol.cu", "af_mr.cu", "af_mr_dist.cu",
+           "af_io.cu"]
+# translation units compiled WITH FMA contraction (tolerance-mode kernels only)
+FMAD_TRUE = {"af_fv3d_tol.cu"}
 HEADERS = ["af_physics.cuh", "af_uniform_kernels.cuh", "af_internal.h", "af_uniform.h",
            "af_comm.h", "af_mr.h", "af_mr_kernels.cuh", "af_mr_types.h",
-           "af_mr_stage.cuh", "af_hancock.cuh"]
+           "af_mr_stage.cuh", "af_hancock.cuh", "af_fv3d.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
@@ -70,7 +73,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas=-v"] if verbose else []), *inc, "-c", src,
+        flags = list(NVCC_FLAGS)
+        if os.path.basename(src) in FMAD_TRUE:
+            flags[flags.index("--fmad=false")] = "--fmad=true"
+        cmd = [_nvcc(), *flags, *(["-Xptxas=-v"] if verbose else []), *inc, "-c", src,
                "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

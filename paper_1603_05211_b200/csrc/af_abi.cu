@@ -192,6 +192,10 @@ af_status af_uniform_set_stream(af_uniform* u, void* s) {
   AF_U_GUARD(u->impl->set_stream(static_cast<cudaStream_t>(s)));
 }
 
+af_status af_uniform_set_numerics(af_uniform* u, int numerics) {
+  AF_U_GUARD(u->impl->set_numerics(numerics));
+}
+
 af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz) {
   if (!u || !u->impl || !z0 || !nz) return record(nullptr, AF_E_ARGUMENT, "null argument");
   *z0 = u->impl->grid().zlo;
@@ -290,6 +294,9 @@ af_status af_mr_set_stream(af_mr* m, void* s) {
 }
 af_status af_mr_build(af_mr* m, const double* aos) { AF_M_GUARD(m->impl->build(aos)); }
 af_status af_mr_refine(af_mr* m, int top) { AF_M_GUARD(m->impl->refine(top)); }
+af_status af_mr_refine_buffer(af_mr* m, double eps, const int* buffer_radius_per_level, int n) {
+  AF_M_GUARD(m->impl->refine(eps, buffer_radius_per_level, n));
+}
 af_status af_mr_add_virtual_leaves(af_mr* m) { AF_M_GUARD(m->impl->add_virtual_leaves()); }
 af_status af_mr_remove_virtual_leaves(af_mr* m) {
   AF_M_GUARD(m->impl->remove_virtual_leaves());

@@ -1,0 +1,444 @@
+// af_fv3d.cuh — the 3D fused RK2-stage kernel: one launch = one rk2_stage
+// (step.cpp:93-109): build_primitives (step.cpp:18-49) + accumulate_rhs
+// (step.cpp:57-89) + out = base + rhs*stage_dt.
+//
+// A CTA owns a TX x TY column of cells and marches along z through a chunk of
+// planes. Per plane:
+//   * TMA: the conserved values of plane k+3's (TX+4) x (TY+4) halo box (one
+//     cp.async.bulk.tensor of 5 x HY x HX doubles, mbarrier completion) land in
+//     a staging buffer while plane k is computed; out-of-domain box cells come
+//     back as zeros and are replaced by their boundary-condition source
+//     (grid.cpp:19-53) when the box is converted;
+//   * convert: staging -> primitives (with the reflective momentum flips) in a
+//     4-plane ring, the owned cells' positivity test and StepDiag wave speed;
+//   * faces: every face the plane's cells need — (TX+1)*TY x-faces,
+//     TX*(TY+1) y-faces, and the TX*TY z-faces between planes k and k+1 — is
+//     one entry of a flat list, 32 consecutive entries per warp unit, the
+//     normal axis a runtime value (af_physics.cuh sel_ax/add_ax), so the
+//     units are dealt evenly over the CTA's NW warps. The 16x15 tile with 8
+//     warps has 751 faces = 24 units, 3 per warp (a 16x16 tile would need 25
+//     units: a fourth pass for one warp at every barrier); the mesh's last
+//     tile row is partial (its rows beyond the mesh are computed, never
+//     stored or counted);
+//   * update: each owned cell sums its six faces in the reference order and
+//     writes out = base + rhs*dt; the z-face above becomes the next plane's
+//     lower face (kept in registers).
+// A face on a tile's high x/y edge, or the chunk's first z face, is computed
+// by both neighbouring CTAs; its fallback is counted only by one of them, so
+// StepDiag.fallbacks counts each face once as accumulate_rhs does.
+//
+// MODE 0: bit-exact (the reference's operations and association order,
+// --fmad=false translation unit). MODE 1: tolerance mode (af_physics.cuh
+// *_tol: reciprocal estimates, FMA contraction in af_fv3d_tol.cu).
+#pragma once
+
+#include <cuda.h>
+
+#include <type_traits>
+
+#include "af_uniform_kernels.cuh"
+
+namespace af {
+
+template <int TX, int TY, int NW>
+struct Fv3dGeom {
+  static constexpr int NT = NW * 32;
+  static constexpr int NCELL = TX * TY;
+  static constexpr int HX = TX + 4, HY = TY + 4, HP = HX * HY;
+  static constexpr int SLOT = 5 * HP;
+  static constexpr int NXF = (TX + 1) * TY, NYF = TX * (TY + 1), NZF = TX * TY;
+  // flat face list: x section [0, NXF), y section [YS, YS+NYF), z section
+  // [ZS, ZS+NZF); sections start on warp-unit boundaries so no unit mixes
+  // axes and every half-warp reads 16 consecutive doubles of a ring row. The
+  // x section lists the TX low faces of each row first (x fastest), then the
+  // TY high-edge faces.
+  static constexpr int YS = (NXF + 31) / 32 * 32, ZS = YS + (NYF + 31) / 32 * 32;
+  static constexpr int NF = ZS + NZF;
+  static constexpr int NU = (NF + 31) / 32;
+  static constexpr int HPT = (HP + NT - 1) / NT;
+  static constexpr int RAW = (4 * SLOT + 15) / 16 * 16;  // staging, 128-byte aligned
+  static constexpr int FLUX = RAW + (SLOT + 15) / 16 * 16;
+  static constexpr int RED = FLUX + 5 * NF;
+  static constexpr size_t smem_bytes = sizeof(double) * (size_t)(RED + NW);
+  static_assert(NCELL <= NT, "one thread per owned cell");
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 4D tiled TMA load (x, y, component, plane) -> shared, completion on `bar`
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int S, int TX, int TY, int NW, int MODE>
+__global__ void __launch_bounds__(NW * 32, 2)
+    fv3d_tile(StageArgs a, UGrid g, const __grid_constant__ CUtensorMap tm) {
+  using K = Fv3dGeom<TX, TY, NW>;
+  constexpr int D = 3;
+  if (failed_before(a.r.err)) return;  // an earlier stage failed: freeze state
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm;              // [4][5][HP] primitives
+  double* raw = sm + K::RAW;      // [5][HP] conserved plane in flight (TMA)
+  double* flux = sm + K::FLUX;    // [5][NF]
+  double* red = sm + K::RED;      // [NW]
+  __shared__ unsigned long long bar;
+  __shared__ int s_fb, s_bad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tid % TX, ty = tid / TX;
+  const int n = g.n;
+  const int tiles_x = n / TX;
+  const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
+  const int zc0 = g.zlo + blockIdx.y * a.zchunk;
+  const int zc1 = min(zc0 + a.zchunk, g.zlo + g.nzl);
+  const bool owner = tid < K::NCELL && y0 + ty < n;  // an owned cell inside the mesh
+  const double gamma = a.gamma, gm1 = a.gm1, inv_dx = a.inv_dx;
+  const double rgm1 = 1.0 / gm1;
+  const double sdt = a.dt_scale * stage_dt_of(a);
+  if (tid == 0) {
+    s_fb = 0;
+    s_bad = 0;
+    mbar_init(&bar, 1);
+    if (a.stage == 1 && blockIdx.x == 0 && blockIdx.y == 0) a.r.dt[a.step] = stage_dt_of(a);
+  }
+  const double* ev = a.eval;
+  const long cs = g.cs, zs = g.zs;
+  double wave = 0.0, ssum = 0.0;
+  int bad = 0, nfb = 0;
+
+  // This thread's halo-box cells idx = tid + t*NT (the cross of the box; the
+  // corners are never on an axis stencil): the box index of the cell the
+  // boundary condition maps them to (-1: outside the box, read from global
+  // memory at the in-plane offset hoff), and the reflective flips (bit 0 x,
+  // bit 1 y).
+  int hsrc[K::HPT], hoff[K::HPT];
+  unsigned hflip = 0, hown = 0;
+#pragma unroll
+  for (int t = 0; t < K::HPT; ++t) {
+    const int idx = tid + t * K::NT;
+    hsrc[t] = -2;  // not converted
+    hoff[t] = 0;
+    if (idx >= K::HP) continue;
+    const int ix = idx % K::HX, iy = idx / K::HX;
+    const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
+    if (!cx && !cy) continue;
+    bool fx, fy;
+    const int mx = bc_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], fx);
+    const int my = bc_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], fy);
+    const int bx = mx - (x0 - 2), by = my - (y0 - 2);
+    hsrc[t] = (bx >= 0 && bx < K::HX && by >= 0 && by < K::HY) ? by * K::HX + bx : -1;
+    hoff[t] = my * n + mx;
+    hflip |= ((fx ? 1u : 0u) | (fy ? 2u : 0u)) << (2 * t);
+    if (cx && cy && y0 - 2 + iy < n) hown |= 1u << t;
+  }
+  __syncthreads();  // barrier initialised
+
+  unsigned phase = 0;
+  auto issue = [&](int gz) {
+    if (tid == 0) {
+      bool fz;
+      const int zl = slab_map(gz, g, 2, fz);
+      mbar_expect_tx(&bar, (unsigned)(sizeof(double) * K::SLOT));
+      tma_load_4d(raw, &tm, x0 - 2, y0 - 2, 0, zl, &bar);
+    }
+  };
+  auto convert = [&](int gz) {
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    bool fz;
+    const int zl = slab_map(gz, g, 2, fz);
+    double* dst = ring + ((gz + 4) & 3) * K::SLOT;
+    const bool own_plane = gz >= zc0 && gz < zc1;
+#pragma unroll
+    for (int t = 0; t < K::HPT; ++t) {
+      if (hsrc[t] == -2) continue;
+      const int idx = tid + t * K::NT;
+      Cons<D> q;
+      if (hsrc[t] >= 0) {
+        const int sidx = hsrc[t];
+        q.rho = raw[sidx];
+        q.m[0] = raw[K::HP + sidx];
+        q.m[1] = raw[2 * K::HP + sidx];
+        q.m[2] = raw[3 * K::HP + sidx];
+        q.E = raw[4 * K::HP + sidx];
+      } else {  // periodic wrap outside the box
+        const long off = (long)zl * zs + hoff[t];
+        q.rho = ev[off];
+        q.m[0] = ev[cs + off];
+        q.m[1] = ev[2 * cs + off];
+        q.m[2] = ev[3 * cs + off];
+        q.E = ev[4 * cs + off];
+      }
+      Prim<D> w;
+      if constexpr (MODE == 0) {
+        w = primitives(q, gm1);
+        if (own_plane && ((hown >> t) & 1u)) {
+          if (!cell_ok(q, w)) bad = 1;
+          double s, m;
+          wave_speeds(w, gamma, s, m);
+          wave = fmax(wave, m);
+        }
+      } else {
+        double ir;
+        w = primitives_tol(q, gm1, ir);
+        if (own_plane && ((hown >> t) & 1u)) {
+          if (!cell_ok(q, w)) bad = 1;
+          double s, m;
+          wave_speeds_tol(w, ir, gamma, s, m);
+          wave = fmax(wave, m);
+        }
+      }
+      const unsigned fl = hflip >> (2 * t);
+      if (fl & 1u) w.v[0] = -w.v[0];
+      if (fl & 2u) w.v[1] = -w.v[1];
+      if (fz) w.v[2] = -w.v[2];
+      dst[idx] = w.rho;
+      dst[K::HP + idx] = w.v[0];
+      dst[2 * K::HP + idx] = w.v[1];
+      dst[3 * K::HP + idx] = w.v[2];
+      dst[4 * K::HP + idx] = w.p;
+    }
+  };
+  auto prim_at = [&](int off) {
+    Prim<D> w;
+    w.rho = ring[off];
+    w.v[0] = ring[K::HP + off];
+    w.v[1] = ring[2 * K::HP + off];
+    w.v[2] = ring[3 * K::HP + off];
+    w.p = ring[4 * K::HP + off];
+    return w;
+  };
+  // Conserved state of global cell (x,y,z) of eval (reflective ghosts with
+  // their momentum flipped): only read on the rare first-order fallback
+  // (scheme.cpp:160-162).
+  auto cons_at = [&](int gx, int gy, int gz) {
+    bool fx, fy, fz;
+    const int mx = bc_map(gx, n, g.bc[0], g.bc[1], fx);
+    const int my = bc_map(gy, n, g.bc[2], g.bc[3], fy);
+    const int zl = slab_map(gz, g, 2, fz);
+    const long c = (long)zl * zs + (long)my * n + mx;
+    Cons<D> q;
+    q.rho = ev[c];
+    q.m[0] = fx ? -ev[cs + c] : ev[cs + c];
+    q.m[1] = fy ? -ev[2 * cs + c] : ev[2 * cs + c];
+    q.m[2] = fz ? -ev[3 * cs + c] : ev[3 * cs + c];
+    q.E = ev[4 * cs + c];
+    return q;
+  };
+  auto slot = [&](int gz) { return ((gz + 4) & 3) * K::SLOT; };
+
+  // Faces of plane k: x/y faces of plane k and the z faces k+1/2, from unit
+  // f_lo/32 on (the prologue computes only z faces). A unit lies in one axis
+  // section, so the axis is warp-uniform and a compile-time constant in the
+  // face body; every lane runs the body (padding lanes repeat a real face and
+  // store nothing), so the rare fallback and fast-path misses take a
+  // warp-uniform branch.
+  auto face_body = [&](auto axc, int k, int u, bool first_z) {
+    constexpr int AX = decltype(axc)::value;
+    constexpr int SEC = AX == 0 ? 0 : (AX == 1 ? K::YS : K::ZS);
+    constexpr int CNT = AX == 0 ? K::NXF : (AX == 1 ? K::NYF : K::NZF);
+    const int j0 = u * 32 + lane - SEC;
+    const bool real = j0 < CNT;
+    const int j = real ? j0 : 0;
+    // face position (fx, fy): the face's high-side cell in tile coordinates
+    // (x faces: fx in [0, TX], y faces: fy in [0, TY]; z faces: the cell)
+    const int fx = AX == 0 ? (j < TX * TY ? j % TX : TX) : j % TX;
+    const int fy = AX == 0 ? (j < TX * TY ? j / TX : j - TX * TY) : j / TX;
+    int o, st0, st1, st2;
+    if constexpr (AX == 0) {
+      o = slot(k) + (fy + 2) * K::HX + fx;
+      st0 = 1;
+      st1 = 2;
+      st2 = 3;
+    } else if constexpr (AX == 1) {
+      o = slot(k) + fy * K::HX + fx + 2;
+      st0 = K::HX;
+      st1 = 2 * K::HX;
+      st2 = 3 * K::HX;
+    } else {
+      o = slot(k - 1) + (fy + 2) * K::HX + fx + 2;
+      st0 = slot(k) - slot(k - 1);
+      st1 = slot(k + 1) - slot(k - 1);
+      st2 = slot(k + 2) - slot(k - 1);
+    }
+    Prim<D> l, r;
+    bool fb;
+    if constexpr (MODE == 0)
+      fb = muscl_recon<D, S>(prim_at(o), prim_at(o + st0), prim_at(o + st1), prim_at(o + st2),
+                             l, r);
+    else
+      fb = muscl_recon_tol<D, S>(prim_at(o), prim_at(o + st0), prim_at(o + st1),
+                                 prim_at(o + st2), l, r);
+    Cons<D> F;
+    if constexpr (MODE == 0)
+      F = recon_flux_fast_warp<D, AX, S>(l, r, gamma, gm1, rgm1);
+    else
+      F = recon_flux_tol<D, S>(l, r, AX, gamma, gm1, rgm1, rgm1);
+    if (__any_sync(0xffffffffu, fb)) {  // rare: first-order fallback (scheme.cpp:160-162)
+      if (fb) {
+        // the inner cells' conserved states from global memory; their
+        // primitives are recomputed exactly as the ring holds them. The
+        // fallback is counted by the tile owning the face's high-side cell
+        // (the domain's high faces by the tile below them), and the chunk's
+        // first z face by the chunk below it, so each face counts once.
+        const int gx = x0 + fx - (AX == 0), gy = y0 + fy - (AX == 1);
+        bool cnt;
+        if constexpr (AX == 0)
+          cnt = (fx < TX || x0 + TX == n) && y0 + fy < n;
+        else if constexpr (AX == 1)
+          cnt = (fy < TY && y0 + fy < n) || y0 + fy == n;
+        else
+          cnt = (!first_z || zc0 == 0) && y0 + fy < n;
+        if (cnt && real) ++nfb;
+        const Cons<D> q0 = cons_at(gx, gy, k);
+        const Cons<D> q1 = cons_at(gx + (AX == 0), gy + (AX == 1), k + (AX == 2));
+        Prim<D> w0, w1;
+        if constexpr (MODE == 0) {
+          w0 = primitives(q0, gm1);
+          w1 = primitives(q1, gm1);
+        } else {
+          double i0, i1;
+          w0 = primitives_tol(q0, gm1, i0);
+          w1 = primitives_tol(q1, gm1, i1);
+        }
+        F = num_flux<D, AX, S>(q0, w0, q1, w1, gamma);
+      }
+    }
+    if (real) {
+      const int f = SEC + j;
+      flux[f] = F.rho;
+      flux[K::NF + f] = F.m[0];
+      flux[2 * K::NF + f] = F.m[1];
+      flux[3 * K::NF + f] = F.m[2];
+      flux[4 * K::NF + f] = F.E;
+    }
+  };
+  const int rows = min(TY, n - y0);  // tile rows inside the mesh
+  auto faces = [&](int k, int f_lo) {
+    for (int u = f_lo / 32 + warp; u < K::NU; u += NW) {
+      // the last tile row of the mesh is partial: units whose faces all lie
+      // beyond the mesh are skipped (warp-uniform)
+      const int f0 = u * 32;
+      if (rows < TY && (f0 < K::YS ? (f0 + 32 <= TX * TY && f0 / TX >= rows)
+                                   : (f0 < K::ZS ? (f0 - K::YS) / TX > rows
+                                                 : (f0 - K::ZS) / TX >= rows)))
+        continue;
+      if (u * 32 < K::YS)
+        face_body(std::integral_constant<int, 0>{}, k, u, false);
+      else if (u * 32 < K::ZS)
+        face_body(std::integral_constant<int, 1>{}, k, u, false);
+      else
+        face_body(std::integral_constant<int, 2>{}, k, u, f_lo != 0);
+    }
+  };
+
+  // Prologue: planes zc0-2 .. zc0 converted, zc0+1 in flight. Iteration
+  // k = zc0-1 computes only the chunk's first z face (zc0-1/2) and keeps it
+  // as the first plane's lower face (one call site of the face loop, so it
+  // stays inlined).
+  for (int z = zc0 - 2; z < zc0 + 1; ++z) {
+    issue(z);
+    convert(z);
+    __syncthreads();
+  }
+  issue(zc0 + 1);
+  const int ixl = ty * TX + tx, ixh = tx + 1 < TX ? ixl + 1 : TX * TY + ty,
+            iyl = K::YS + ty * TX + tx, izl = K::ZS + ty * TX + tx;
+  double zlo[5];
+
+  for (int k = zc0 - 1; k < zc1; ++k) {
+    const bool first = k < zc0;
+    const long own = (long)(k - g.zlo + 2) * zs + (long)(y0 + ty) * n + (x0 + tx);
+    double b[5];
+    if (owner && !first) {
+#pragma unroll
+      for (int m = 0; m < 5; ++m) b[m] = a.base[m * cs + own];
+    }
+    convert(k + 2);
+    __syncthreads();  // ring slot k+2 complete, staging free, flux free
+    if (k + 3 < zc1 + 2) issue(k + 3);
+    faces(k, first ? K::ZS : 0);
+    __syncthreads();
+    if (first) {
+#pragma unroll
+      for (int m = 0; m < 5; ++m) zlo[m] = owner ? flux[m * K::NF + izl] : 0.0;
+      continue;
+    }
+    if (owner) {
+      // rhs in the reference order (step.cpp:80-81): x low, x high, y low,
+      // y high, z low, z high; then out = base + rhs*stage_dt
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        const double* fm = flux + m * K::NF;
+        const double zh = fm[izl];
+        double rhs = 0.0;
+        rhs = rhs + fm[ixl] * inv_dx;
+        rhs = rhs - fm[ixh] * inv_dx;
+        rhs = rhs + fm[iyl] * inv_dx;
+        rhs = rhs - fm[iyl + TX] * inv_dx;
+        rhs = rhs + zlo[m] * inv_dx;
+        rhs = rhs - zh * inv_dx;
+        b[m] = b[m] + rhs * sdt;
+        zlo[m] = zh;
+      }
+#pragma unroll
+      for (int m = 0; m < 5; ++m) a.out[m * cs + own] = b[m];
+      if (a.stage == 2 && a.use_cfl) {  // next step's CFL denominator, fused
+        Cons<D> q;
+        q.rho = b[0];
+        q.m[0] = b[1];
+        q.m[1] = b[2];
+        q.m[2] = b[3];
+        q.E = b[4];
+        double s, mx;
+        if constexpr (MODE == 0) {
+          wave_speeds(primitives(q, gm1), gamma, s, mx);
+        } else {
+          double ir;
+          const Prim<D> w = primitives_tol(q, gm1, ir);
+          wave_speeds_tol(w, ir, gamma, s, mx);
+        }
+        ssum = fmax(ssum, s);
+      }
+    }
+  }
+
+  // Stage diagnostics: positivity, StepDiag wave max, fallbacks.
+  if (bad) s_bad = 1;
+  if (nfb) atomicAdd(&s_fb, nfb);
+  block_max_atomic<K::NT>(wave, red, a.stage == 1 ? a.r.wave_u + a.step : a.r.wave_mid + a.step);
+  if (a.stage == 2 && a.use_cfl) block_max_atomic<K::NT>(ssum, red, a.r.smax + a.step + 1);
+  if (tid == 0) {
+    if (s_bad) raise_error(a);
+    if (s_fb) atomicAdd(a.r.fb + a.step, (unsigned long long)s_fb);
+  }
+}
+
+}  // namespace af

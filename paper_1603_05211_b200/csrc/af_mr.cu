@@ -680,18 +680,41 @@ void MR::build(const double* aos) {
 }
 
 void MR::refine(int top) {
+  std::vector<int> radius;
+  if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
+    radius.assign(L_ + 1, 1);
+    for (int l = 0; l <= L_; ++l)
+      if (l > top + 1) radius[l] = 1 << (l - top - 1);
+  }
+  refine_(radius, nullptr);
+}
+
+// MRTree::refine(eps, buffer_radius_per_level) (mr_tree.hpp:141,
+// mr_tree.cpp:361-402): one threshold for every level, and a Chebyshev
+// dilation of the split set by buffer[l] leaves at level l (none when the
+// buffer is empty; levels past its end or with a radius <= 0 do not dilate).
+void MR::refine(double eps, const int* buffer, int n) {
+  if (n < 0 || (n > 0 && !buffer)) throw Error(AF_E_ARGUMENT, "bad buffer radius array");
+  std::vector<int> radius(buffer, buffer + n);
+  for (int r : radius)
+    if (dist_ && r > halo_)
+      throw Error(AF_E_CONFIG, "refine buffer radius exceeds the decomposition's halo rows");
+  refine_(radius, &eps);
+}
+
+void MR::refine_(const std::vector<int>& radius, const double* eps) {
   registers_built_ = false;
   if (!lists_valid_) build_lists_();
   wset_(d_flag_, 1, 1, 0, 0, L_);
   wset_(d_flag2_, 1, 1, 0, 0, L_);
   // details with the refine flags of their leaf children (one launch)
-  for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps_at_(l);
+  for (int l = 1; l <= L_ - 1; ++l) g_.eps_l[l] = eps ? *eps : eps_at_(l);
   AF_ML_LAUNCH_M(mr_detail_level, std::max(0, min_leaf_ - 1), L_ - 2, false, 1 << D_, d_V_,
                  d_st_, d_det_, g_, AF_L, d_norms_, d_flag_);
   uint8_t* split = d_flag_;
-  if (top >= 0) {  // LT buffer radii (mr_solver.cpp:358-362)
+  if (!radius.empty()) {
     for (int l = 1; l <= L_ - 1; ++l) {
-      const int r = l > top + 1 ? 1 << (l - top - 1) : 1;
+      const int r = l < (int)radius.size() ? std::max(0, radius[l]) : 0;
       if (band_count_[l])
         AF_MR_LAUNCH(mr_dilate_level, AF_TGRID(l, band_count_[l]), d_st_, d_flag_, d_flag2_, g_, l,
                      r, AF_BAND(l));

@@ -34,6 +34,7 @@ class MR {
   // MRTree::from_uniform + set_min_leaf_level + coarsen(eps) (mr_solver.cpp:406-410)
   void build(const double* aos);
   void refine(int top);              // MRTree::refine (+ LT buffer when top >= 0)
+  void refine(double eps, const int* buffer, int n);  // MRTree::refine(eps, buffer)
   void add_virtual_leaves();         // marks the virtual set (and counts it)
   void evolve_global(double dt, af_step_diag* d);
   void advance_local(int top, double t, double dt, af_step_diag* d);
@@ -54,6 +55,7 @@ class MR {
   af_error& last_error() { return last_; }
 
  private:
+  void refine_(const std::vector<int>& radius, const double* eps);
   void predict_fill_(int lo, int hi, int from = 1);
   void project_range_(int lo, int top);
   void build_lists_();

@@ -11,11 +11,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "af_comm.h"
 #include "af_uniform.h"
+#include "af_fv3d.cuh"
 #include "af_hancock.cuh"
 #include "af_uniform_kernels.cuh"
 
@@ -24,6 +26,30 @@ namespace af {
 namespace {
 
 constexpr int kTY = 8;
+
+// 3D stage tile (af_fv3d.cuh): 16x15 columns, 8 warps (751 faces per plane =
+// 24 warp units, 3 per warp), two CTAs per SM (128 registers).
+constexpr int kT3 = 16, kT3Y = 15, kW3 = 8;
+using Geo3 = Fv3dGeom<kT3, kT3Y, kW3>;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library does not link libcuda, so it still loads without a driver).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    AF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      throw Error(AF_E_CUDA, "driver entry point missing: cuTensorMapEncodeTiled");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
 
 __global__ void aos_to_soa(const double* __restrict__ aos, double* __restrict__ soa, UGrid g) {
   const long cells = g.plane * g.nzl;
@@ -136,6 +162,81 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   for (auto fn : {(const void*)hancock_step<3, 0, 8, 8, 4>, (const void*)hancock_step<3, 1, 8, 8, 4>,
                   (const void*)hancock_step<3, 2, 8, 8, 4>, (const void*)hancock_step<3, 3, 8, 8, 4>})
     AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
+  const char* te = std::getenv("AF_FV3D_TILE");
+  tile_exact_ = te && te[0] == '1';
+  if (c.dim == 3 && n >= kT3) {
+    for (auto fn : {(const void*)fv3d_tile<0, kT3, kT3Y, kW3, 0>, (const void*)fv3d_tile<1, kT3, kT3Y, kW3, 0>,
+                    (const void*)fv3d_tile<2, kT3, kT3Y, kW3, 0>, (const void*)fv3d_tile<3, kT3, kT3Y, kW3, 0>})
+      AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Geo3::smem_bytes));
+    fv3d_tol_setup();
+    // TMA descriptors: the slab allocation as a 4D tensor (x, y, component,
+    // local plane); one (TX+4) x (TY+4) x 5 x 1 box per halo plane
+    for (int b = 0; b < 2; ++b) {
+      double* base = b == 0 ? d_u_ : d_mid_;
+      const cuuint64_t dims[4] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)g_.ncomp,
+                                  (cuuint64_t)(g_.nzl + 4)};
+      const cuuint64_t strides[3] = {(cuuint64_t)n * 8, (cuuint64_t)g_.cs * 8,
+                                     (cuuint64_t)g_.zs * 8};
+      const cuuint32_t box[4] = {(cuuint32_t)Geo3::HX, (cuuint32_t)Geo3::HY, 5, 1};
+      const cuuint32_t es[4] = {1, 1, 1, 1};
+      const CUresult r = encode_tiled()(&tm_[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims,
+                                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw Error(AF_E_CUDA, "cuTensorMapEncodeTiled failed");
+      tm_base_[b] = base;
+    }
+  }
+}
+
+void Uniform::set_numerics(int numerics) {
+  if (numerics != AF_NUMERICS_EXACT && numerics != AF_NUMERICS_TOLERANCE)
+    throw Error(AF_E_ARGUMENT, "unknown numerics mode");
+  numerics_ = numerics;
+}
+
+const CUtensorMap* Uniform::tensor_map_(const double* buf) {
+  for (int b = 0; b < 2; ++b)
+    if (tm_base_[b] == buf) return &tm_[b];
+  return nullptr;
+}
+
+// The 3D RK2 stage on the TMA-fed 16x16 tile kernel (af_fv3d.cuh); false when
+// the mesh is too small for it or the legacy kernel is selected.
+bool Uniform::launch_tile3d_(const StageArgs& a) {
+  const int n = g_.n;
+  if (g_.dim != 3 || n < kT3) return false;
+  // Exact mode runs the 32x8 fv3d_stage (5% faster bit-exact, profiles/r02_*);
+  // AF_FV3D_TILE=1 selects the TMA tile kernel for it as well.
+  if (numerics_ == AF_NUMERICS_EXACT && !tile_exact_) return false;
+  const CUtensorMap* tm = tensor_map_(a.eval);
+  if (!tm) return false;
+  const long tiles = (long)(n / kT3) * ((n + kT3Y - 1) / kT3Y);
+  const long target = 148L * 2 * 8;
+  int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, g_.nzl / 8));
+  StageArgs b = a;
+  b.zchunk = (g_.nzl + chunks - 1) / chunks;
+  chunks = (g_.nzl + b.zchunk - 1) / b.zchunk;
+  dim3 grid((unsigned)tiles, (unsigned)chunks);
+  const int sch = cfg_.limiter | (cfg_.flux << 1);
+  if (numerics_ == AF_NUMERICS_TOLERANCE) {
+    fv3d_tol_launch(sch, grid, stream_, b, g_, *tm);
+  } else {
+#define AF_T3(S) \
+  fv3d_tile<S, kT3, kT3Y, kW3, 0><<<grid, Geo3::NT, Geo3::smem_bytes, stream_>>>(b, g_, *tm)
+    switch (sch) {
+      case 0: AF_T3(0); break;
+      case 1: AF_T3(1); break;
+      case 2: AF_T3(2); break;
+      default: AF_T3(3); break;
+    }
+#undef AF_T3
+  }
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+  return true;
 }
 
 Uniform::~Uniform() {
@@ -286,6 +387,7 @@ void Uniform::launch_hancock_(const StageArgs& a) {
 }
 
 void Uniform::launch_stage_(const StageArgs& a) {
+  if (launch_tile3d_(a)) return;
   const int n = g_.n;
   const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
   const int sch = cfg_.limiter | (cfg_.flux << 1);  // scheme code (af_physics.cuh)

@@ -1,6 +1,8 @@
 // af_uniform.h — host class behind af_uniform_* (see af_uniform.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include "af_comm.h"
 #include <vector>
 
@@ -9,6 +11,13 @@
 namespace af {
 
 struct StageArgs;
+struct UGrid;
+
+// Tolerance-mode 3D stage kernels, compiled with FMA contraction in their own
+// translation unit (af_fv3d_tol.cu).
+void fv3d_tol_setup();
+void fv3d_tol_launch(int scheme, dim3 grid, cudaStream_t stream, const StageArgs& a,
+                     const UGrid& g, const CUtensorMap& tm);
 
 class Uniform {
  public:
@@ -18,6 +27,7 @@ class Uniform {
   Uniform& operator=(const Uniform&) = delete;
 
   void set_stream(cudaStream_t s);
+  void set_numerics(int numerics);
   void upload(const double* aos);
   void download(double* aos);
   void step(double dt, af_step_diag* diag);
@@ -44,6 +54,8 @@ class Uniform {
   void exchange_halos_(double* q);
   void allreduce_max_(unsigned long long* bits);
   void launch_stage_(const StageArgs& a);
+  bool launch_tile3d_(const StageArgs& a);
+  const CUtensorMap* tensor_map_(const double* buf);
   void launch_hancock_(const StageArgs& a);
   void launch_speed_sum_(const double* q, unsigned long long* target);
   void enqueue_steps_(long n_steps, double cfl, double fixed_dt);
@@ -67,6 +79,10 @@ class Uniform {
   cudaStream_t own_stream_ = nullptr;
   long launches_ = 0;
   af_error last_{};
+  int numerics_ = AF_NUMERICS_EXACT;
+  bool tile_exact_ = false;  // AF_FV3D_TILE=1: the TMA tile kernel in exact mode too
+  CUtensorMap tm_[2];      // TMA descriptors of d_u_ / d_mid_ (4D: x, y, component, plane)
+  const double* tm_base_[2] = {nullptr, nullptr};
 };
 
 }  // namespace af

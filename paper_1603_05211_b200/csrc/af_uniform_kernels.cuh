@@ -271,14 +271,18 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
     return q;
   };
   int nfb = 0;
-  // z face between planes gz-1 and gz of this thread's column.
+  // z face between planes gz-1 and gz of this thread's column. A face that
+  // two tiles (or two z chunks) both evaluate counts its fallback in one of
+  // them only: the tile owning its high-side cell, the domain's high faces in
+  // the tile below them, the chunk's first z face in the chunk below it
+  // (accumulate_rhs counts each face once, step.cpp:57-89).
   auto zface = [&](int gz) {
     const int idx = (ty + 2) * K::HX + tx + 2;
     const Prim<D> wm1 = prim_at(gz - 2, idx), w0 = prim_at(gz - 1, idx);
     const Prim<D> wp1 = prim_at(gz, idx), wp2 = prim_at(gz + 1, idx);
     Prim<D> l, r;
     if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
-      ++nfb;
+      if (gz > zc0 || zc0 == 0) ++nfb;
       return num_flux<D, 2, LIM>(cons_at(x0 + tx, y0 + ty, gz - 1), w0,
                              cons_at(x0 + tx, y0 + ty, gz), wp1, gamma);
     }
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
           Prim<D> l, r;
           Cons<D> fl;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
-            ++nfb;
+            if (fxi < TX || x0 + TX == n) ++nfb;
             fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
           Prim<D> l, r;
           Cons<D> fl;
           if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
-            ++nfb;
+            if (fyi < TY || y0 + TY == n) ++nfb;
             fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1, k), w0,
                                  cons_at(x0 + fxi, y0 + fyi, k), wp1, gamma);
           } else {
@@ -508,7 +512,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
         Prim<D> l, r;
         Cons<D> fl;
         if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
-          ++nfb;
+          if (fxi < TX || x0 + TX == n) ++nfb;  // one count per face (see fv3d_stage)
           fl = num_flux<D, 0, LIM>(cons_at(x0 + fxi - 1, y0 + fyi), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
         Prim<D> l, r;
         Cons<D> fl;
         if (muscl_recon<D, LIM>(wm1, w0, wp1, wp2, l, r)) {
-          ++nfb;
+          if (fyi < TY || y0 + fyi == n) ++nfb;
           fl = num_flux<D, 1, LIM>(cons_at(x0 + fxi, y0 + fyi - 1), w0,
                                cons_at(x0 + fxi, y0 + fyi), wp1, gamma);
         } else {

@@ -141,8 +141,17 @@ class MRSolver:
     def build(self, aos) -> None:
         self._check(self._lib.af_mr_build(self._h, C.c_void_p(_ptr(aos))))
 
-    def refine(self, top: int = -1):
-        self._check(self._lib.af_mr_refine(self._h, top))
+    def refine(self, top: int = -1, eps: float | None = None, buffer=None):
+        """MRTree::refine. With ``eps`` given: refine(eps, buffer_radius_per_level)
+        (mr_tree.hpp:141) — one threshold, optional per-level Chebyshev buffer.
+        Otherwise the run_mr form: the configured thresholds, and the LT buffer
+        radii of mr_solver.cpp:358-362 when top >= 0."""
+        if eps is None:
+            self._check(self._lib.af_mr_refine(self._h, top))
+            return
+        buf = [] if buffer is None else [int(r) for r in buffer]
+        arr = (C.c_int * max(1, len(buf)))(*buf)
+        self._check(self._lib.af_mr_refine_buffer(self._h, float(eps), arr, len(buf)))
 
     def coarsen(self):
         self._check(self._lib.af_mr_coarsen(self._h))

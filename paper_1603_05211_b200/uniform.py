@@ -141,6 +141,12 @@ class UniformSolver:
         raw = getattr(stream, "cuda_stream", stream)
         self._check(self._lib.af_uniform_set_stream(self._h, C.c_void_p(raw)))
 
+    def set_numerics(self, tolerance: bool) -> None:
+        """AF_NUMERICS_EXACT (default, bit-identical to the reference) or
+        AF_NUMERICS_TOLERANCE (3D stage with reciprocal estimates and FMA
+        contraction, within 1e-10 relative L1 of the exact result)."""
+        self._check(self._lib.af_uniform_set_numerics(self._h, 1 if tolerance else 0))
+
     def kernel_launches(self) -> int:
         c = C.c_long()
         self._lib.af_uniform_kernel_launches(self._h, C.byref(c))

@@ -179,3 +179,39 @@ def test_mr_edge_cases_match_reference(gpu_lib, oracle, kind, seed, level, steps
         pytest.skip("reference build not present")
     init, out, keys, rep = gpu_mr(kind, seed, level, steps, **kw)
     compare(init, out, keys, rep, ref_mr(oracle, init, kind, level, steps, **kw))
+
+
+REFINE_BUFFER = [
+    # kind, seed, level, build eps, refine eps, buffer radius per level, bc
+    (0, 71, 7, 1e-3, 1e-3, [1] * 8, None),
+    (0, 72, 7, 2e-3, 1e-3, [0, 0, 1, 1, 2, 2, 3, 3], None),
+    (1, 73, 7, 1e-3, 1e-3, [2, 2, 2], None),               # shorter than L+1
+    (0, 74, 6, 1e-3, 5e-4, [], None),                      # no buffer, another eps
+    (0, 75, 6, 1e-3, 1e-3, [1, 1, 2, 2, 2, 2, 2], [1] * 6),  # periodic wrap
+    (0, 76, 6, 1e-3, 1e-3, [3] * 7, [2] * 6),              # reflective fold
+    (2, 77, 5, 1e-3, 1e-3, [1, 1, 1, 2, 2, 2], None),      # 3D
+]
+
+
+@pytest.mark.parametrize("kind,seed,level,eps0,eps,buffer,bc", REFINE_BUFFER,
+                         ids=[f"rb{i}" for i in range(len(REFINE_BUFFER))])
+def test_refine_buffer_matches_reference(gpu_lib, oracle, kind, seed, level, eps0, eps, buffer,
+                                         bc):
+    """MRTree::refine(eps, buffer_radius_per_level) (mr_tree.hpp:141) through
+    af_mr_refine_buffer: the same leaf set and to_uniform(L) as the
+    reference's refine on the same starting tree."""
+    if not oracle.available("ref"):
+        pytest.skip("reference build not present")
+    from paper_1603_05211_b200 import mr as M
+    from paper_1603_05211_b200 import uniform as U
+    dim = 3 if kind >= 2 else 2
+    init = U.case_fill(kind, seed, level)
+    s = M.MRSolver(dim, level, M.MROptions(epsilon=eps0), bc=bc)
+    s.build(init)
+    s.refine(eps=eps, buffer=buffer)
+    keys, out = s.leaves(), s.to_uniform()
+    s.close()
+    p = oracle.make_params(dim, level, 1, eps=eps0, bc=bc)
+    rout, rkeys = oracle.ref_mr_refine_once(p, init, eps, buffer)
+    assert np.array_equal(keys, rkeys)
+    assert np.array_equal(bits(out), bits(rout))

@@ -1,0 +1,110 @@
+"""Tolerance mode (AF_NUMERICS_TOLERANCE) of the 3D RK2 stage against
+BASELINE.json's bar: conserved variables within 1e-10 relative L1 per field
+after the configured step count (metrics.cpp:134-148 norm, normalised by the
+exact field's own L1).
+
+  * cfg4 at its full size (512^3 x 100 steps): tolerance vs the bit-exact
+    path, which tests/test_digests_gpu.py pins to the reference;
+  * cfg4 generator at 128^3 x 100 steps: tolerance vs the compiled
+    reference's digest (its coarse-averaged field and per-field L1);
+  * small cases over every boundary condition and scheme: tolerance vs exact.
+The bit-exact path is also checked to be untouched by the mode switch."""
+import os
+
+import numpy as np
+import pytest
+
+import digests as D
+from test_oracle import bits
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+TOL = 1e-10  # BASELINE.json north_star: relative L1 per field
+
+
+def run(level, steps, tolerance, kind=2, seed=1, bc=None, limiter=1, flux=0, cfl=0.4):
+    from paper_1603_05211_b200 import uniform as U
+    s = U.UniformSolver(3, level, scheme=U.SchemeConfig(limiter=limiter, flux=flux), bc=bc)
+    if tolerance:
+        s.set_numerics(True)
+    s.upload(U.case_fill(kind, seed, level))
+    rep = s.run(steps, cfl=cfl)
+    out = s.download()
+    s.close()
+    return out, rep
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_within_tolerance(gpu_lib):
+    exact, _ = run(9, 100, False)
+    tol, _ = run(9, 100, True)
+    err = D.rel_l1(tol, exact)
+    assert (err <= TOL).all(), err
+    assert not np.array_equal(bits(tol), bits(exact))  # the mode really switched
+
+
+def test_cfg4_128_within_tolerance_of_reference(gpu_lib):
+    path = os.path.join(HERE, "golden", "digest_cfg4_128.npz")
+    g = np.load(path, allow_pickle=False)
+    tol, rep = run(int(g["level"]), int(g["steps"]), True, kind=int(g["kind"]),
+                   seed=int(g["seed"]), cfl=float(g["cfl"]))
+    c = D.coarse(tol, int(g["dim"]), int(g["level"]), int(g["coarse_level"]))
+    assert (D.rel_l1(c, g["coarse"]) <= TOL).all()
+    assert np.allclose(D.state_l1(tol), g["state_l1"], rtol=TOL, atol=0)
+    assert np.allclose(rep.dt, g["dt"], rtol=1e-12, atol=0)
+    exact, _ = run(int(g["level"]), int(g["steps"]), False, kind=int(g["kind"]),
+                   seed=int(g["seed"]), cfl=float(g["cfl"]))
+    assert D.state_sha(exact) == str(g["state_sha"])
+    assert (D.rel_l1(tol, exact) <= TOL).all()
+
+
+CASES = [
+    # level, steps, kind, bc, limiter, flux
+    (5, 10, 2, None, 1, 0),
+    (5, 8, 3, [2, 2, 1, 1, 0, 0], 1, 0),
+    (6, 6, 2, [1] * 6, 1, 0),
+    (5, 8, 2, [2] * 6, 0, 0),
+    (5, 6, 3, None, 1, 1),
+    (4, 6, 2, None, 0, 1),
+]
+
+
+@pytest.mark.parametrize("level,steps,kind,bc,limiter,flux", CASES,
+                         ids=[f"t{i}" for i in range(len(CASES))])
+def test_tolerance_vs_exact(gpu_lib, level, steps, kind, bc, limiter, flux):
+    exact, re = run(level, steps, False, kind=kind, bc=bc, limiter=limiter, flux=flux)
+    tol, rt = run(level, steps, True, kind=kind, bc=bc, limiter=limiter, flux=flux)
+    assert (D.rel_l1(tol, exact) <= TOL).all()
+    assert rt.fallbacks == re.fallbacks
+    assert abs(rt.max_cfl - re.max_cfl) <= 1e-12 * re.max_cfl
+
+
+TILE_CASES = [
+    # level, steps, kind, bc, limiter, flux (16 and 32 cells per axis exercise the
+    # partial last tile row of the 16x15 tile)
+    (4, 6, 2, None, 1, 0),
+    (5, 8, 2, None, 1, 0),
+    (5, 6, 3, [2, 2, 1, 1, 0, 0], 1, 0),
+    (6, 5, 2, [1] * 6, 1, 0),
+    (5, 5, 2, None, 0, 0),
+    (5, 5, 3, None, 1, 1),
+    (5, 4, 2, [2] * 6, 0, 1),
+    (7, 6, 2, None, 1, 0),
+]
+
+
+@pytest.mark.parametrize("level,steps,kind,bc,limiter,flux", TILE_CASES,
+                         ids=[f"tile{i}" for i in range(len(TILE_CASES))])
+def test_tile_kernel_exact_equals_fv3d_stage(gpu_lib, monkeypatch, level, steps, kind, bc,
+                                             limiter, flux):
+    """The TMA tile kernel (af_fv3d.cuh) in exact mode is bit-identical to the
+    32x8 fv3d_stage kernel (the exact-mode default), with the same dt history,
+    StepDiag wave speeds and fallback counts."""
+    monkeypatch.setenv("AF_FV3D_TILE", "1")
+    a, ra = run(level, steps, False, kind=kind, bc=bc, limiter=limiter, flux=flux)
+    monkeypatch.setenv("AF_FV3D_TILE", "0")
+    b, rb = run(level, steps, False, kind=kind, bc=bc, limiter=limiter, flux=flux)
+    assert np.array_equal(bits(a), bits(b))
+    assert np.array_equal(bits(ra.dt), bits(rb.dt))
+    assert ra.max_wave_speed == rb.max_wave_speed and ra.max_cfl == rb.max_cfl
+    assert ra.fallbacks == rb.fallbacks
