@@ -247,6 +247,9 @@ af_status af_mr_advance_local(af_mr* m, int top, double t, double dt, af_step_di
 af_status af_mr_run(af_mr* m, long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles,
                     long max_cycles, af_run_diag* diag);
 af_status af_mr_counts(af_mr* m, long* leaves, long* nodes, long* internals);
+/* MRSolver::max_cfl() / fallbacks() (mr_solver.hpp): accumulated over every
+ * evolve_global / advance_local / run since af_mr_build (either may be NULL). */
+af_status af_mr_solver_stats(af_mr* m, double* max_cfl, long* fallbacks);
 af_status af_mr_coarsest_leaf_level(af_mr* m, int* level);
 /* Sorted pack_key (mr_tree.hpp:26-30) of every leaf; *n: capacity in, count out. */
 af_status af_mr_leaf_keys(af_mr* m, uint64_t* keys, size_t* n);

@@ -100,6 +100,7 @@ SIGNATURES = {
     "af_mr_build": (C.c_int, [_vp, _vp]),
     "af_mr_refine": (C.c_int, [_vp, C.c_int]),
     "af_mr_refine_buffer": (C.c_int, [_vp, C.c_double, C.POINTER(C.c_int), C.c_int]),
+    "af_mr_solver_stats": (C.c_int, [_vp, _dp, C.POINTER(C.c_long)]),
     "af_mr_add_virtual_leaves": (C.c_int, [_vp]),
     "af_mr_remove_virtual_leaves": (C.c_int, [_vp]),
     "af_mr_coarsen": (C.c_int, [_vp]),

@@ -294,6 +294,12 @@ af_status af_mr_set_stream(af_mr* m, void* s) {
 }
 af_status af_mr_build(af_mr* m, const double* aos) { AF_M_GUARD(m->impl->build(aos)); }
 af_status af_mr_refine(af_mr* m, int top) { AF_M_GUARD(m->impl->refine(top)); }
+af_status af_mr_solver_stats(af_mr* m, double* max_cfl, long* fallbacks) {
+  AF_M_GUARD({
+    if (max_cfl) *max_cfl = m->impl->max_cfl();
+    if (fallbacks) *fallbacks = m->impl->fallbacks();
+  });
+}
 af_status af_mr_refine_buffer(af_mr* m, double eps, const int* buffer_radius_per_level, int n) {
   AF_M_GUARD(m->impl->refine(eps, buffer_radius_per_level, n));
 }

@@ -830,6 +830,10 @@ void MR::cycle_stats_(long* leaves, long* nodes, double* smax) {
 }
 
 int MR::coarsest_leaf_level() {
+  if (!lists_valid_) {  // a coarsen since the last list build changed the counts
+    build_lists_();
+    lists_valid_ = true;
+  }
   for (int l = 0; l <= L_; ++l)
     if (leaves_per_level_[l]) return l;
   return L_;

@@ -48,6 +48,8 @@ class MR {
   void to_uniform(int level, double* aos);
   void details(int level, double* out);
   double leaf_speed_sum();
+  double max_cfl() const { return max_cfl_; }  // MRSolver::max_cfl (mr_solver.hpp)
+  long fallbacks() const { return fallbacks_; }
 
   long launches() const { return launches_; }
   void profile(bool on);

@@ -15,8 +15,12 @@
 //                     final to_uniform(L) grid instead of the host MRTree)
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <functional>
+#include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -121,11 +125,51 @@ class UniformDevice {
   af_uniform* h_ = nullptr;
 };
 
-// step_block (step.hpp:77-79) for one block whose ghosts follow `bc`.
+// The device context step_block reuses across calls: one per host thread,
+// rebuilt only when the geometry, gas, boundary condition or scheme changes.
+struct StepBlockCache {
+  std::unique_ptr<UniformDevice> dev;
+  int dim = 0, level = -1, bc[6] = {0, 0, 0, 0, 0, 0}, flux = -1, limiter = -1, integ = -1;
+  double origin = 0.0, extent = 0.0, gamma = 0.0;
+  long creations = 0;  // contexts built so far (tests/cpp/shim_parity.cpp)
+
+  UniformDevice& get(const UniformGrid& g, const GasModel& gas, const BoundaryCondition& b,
+                     const SchemeConfig& s) {
+    const af_config c = make_config(g.dim(), g.level(), g.origin(), g.extent(), gas, b, s);
+    bool same = dev && dim == c.dim && level == c.level && origin == c.origin &&
+                extent == c.extent && gamma == c.gamma && flux == c.flux &&
+                limiter == c.limiter && integ == c.integrator;
+    for (int f = 0; f < 6 && same; ++f) same = bc[f] == c.bc[f];
+    if (!same) {
+      dev.reset();
+      dev = std::make_unique<UniformDevice>(g, gas, b, s);
+      dim = c.dim;
+      level = c.level;
+      origin = c.origin;
+      extent = c.extent;
+      gamma = c.gamma;
+      flux = c.flux;
+      limiter = c.limiter;
+      integ = c.integrator;
+      for (int f = 0; f < 6; ++f) bc[f] = c.bc[f];
+      ++creations;
+    }
+    return *dev;
+  }
+};
+
+inline StepBlockCache& step_block_cache() {
+  static thread_local StepBlockCache cache;
+  return cache;
+}
+
+// step_block (step.hpp:77-79) for one block whose ghosts follow `bc`. The
+// block lives in host memory, so each call uploads it and downloads the
+// result; the device context is cached per thread (step_block_cache).
 inline StepDiag step_block(BlockData& u, const UniformGrid& geometry, double dt,
                            const SchemeConfig& cfg, const GasModel& gas,
                            const BoundaryCondition& bc) {
-  UniformDevice dev(geometry, gas, bc, cfg);
+  UniformDevice& dev = step_block_cache().get(geometry, gas, bc, cfg);
   dev.upload(u);
   const StepDiag d = dev.step(dt);
   dev.download(u);
@@ -181,60 +225,207 @@ struct MRDeviceResult {
   std::vector<NodeKey> leaves;  // MRTree::leaves() of the final tree
 };
 
+// A device-resident MR tree: the MRTree calls of the hot path (mr_tree.hpp)
+// on libafgpu, with host views of the leaf set and the uniform projection.
+class MRDevice {
+ public:
+  MRDevice(int dim, int level, double origin, double extent, const GasModel& gas,
+           const BoundaryCondition& bc, const SchemeConfig& s, const af_mr_options& o,
+           int device = 0)
+      : dim_(dim), level_(level), origin_(origin), extent_(extent) {
+    const af_config c = make_config(dim, level, origin, extent, gas, bc, s, device);
+    check(af_mr_create(&c, &o, &m_));
+  }
+  ~MRDevice() { af_mr_destroy(m_); }
+  MRDevice(const MRDevice&) = delete;
+  MRDevice& operator=(const MRDevice&) = delete;
+
+  // MRTree::from_uniform + set_min_leaf_level + coarsen (mr_solver.cpp:323-328)
+  void build(const UniformGrid& g) { check(af_mr_build(m_, to_aos(g.block()).data())); }
+  // MRTree::refine(eps, buffer_radius_per_level) (mr_tree.hpp:141)
+  void refine(double eps, const std::vector<int>& buffer = {}) {
+    check(af_mr_refine_buffer(m_, eps, buffer.data(), static_cast<int>(buffer.size())));
+  }
+  void refine_lt(int top) { check(af_mr_refine(m_, top)); }  // run_mr's LT form
+  void add_virtual_leaves() { check(af_mr_add_virtual_leaves(m_)); }
+  void remove_virtual_leaves() { check(af_mr_remove_virtual_leaves(m_)); }
+  void coarsen() { check(af_mr_coarsen(m_)); }
+  double evolve_global(double dt) {
+    af_step_diag d{};
+    check(af_mr_evolve_global(m_, dt, &d));
+    return d.max_wave_speed;
+  }
+  double advance_local(int top, double t, double dt) {
+    af_step_diag d{};
+    check(af_mr_advance_local(m_, top, t, dt, &d));
+    return d.max_wave_speed;
+  }
+  long leaf_count() {
+    long lv = 0, nd = 0, in = 0;
+    check(af_mr_counts(m_, &lv, &nd, &in));
+    return lv;
+  }
+  long node_count() {
+    long lv = 0, nd = 0, in = 0;
+    check(af_mr_counts(m_, &lv, &nd, &in));
+    return nd;
+  }
+  int coarsest_leaf_level() {
+    int l = 0;
+    check(af_mr_coarsest_leaf_level(m_, &l));
+    return l;
+  }
+  // MRTree::leaves() (sorted pack_key)
+  std::vector<NodeKey> leaves() {
+    size_t n = 0;
+    check(af_mr_leaf_keys(m_, nullptr, &n));
+    std::vector<NodeKey> out(n);
+    check(af_mr_leaf_keys(m_, reinterpret_cast<uint64_t*>(out.data()), &n));
+    return out;
+  }
+  // MRTree::to_uniform(level) (mr_tree.cpp:608-621)
+  UniformGrid to_uniform(int level) {
+    UniformGrid g(dim_, level, origin_, extent_);
+    std::vector<double> aos(static_cast<size_t>(g.block().interior_cells()) * 5);
+    check(af_mr_to_uniform(m_, level, aos.data()));
+    from_aos(aos, g.block());
+    return g;
+  }
+  int dim() const { return dim_; }
+  int max_level() const { return level_; }
+  double origin() const { return origin_; }
+  double extent() const { return extent_; }
+  double dx(int level) const { return extent_ / static_cast<double>(1 << level); }
+  af_mr* handle() { return m_; }
+  void check(af_status st) {
+    if (st == AF_OK) return;
+    af_error e{};
+    af_mr_last_error(m_, &e);
+    rethrow(st, e);
+  }
+
+ private:
+  af_mr* m_ = nullptr;
+  int dim_, level_;
+  double origin_, extent_;
+};
+
+// The tree as MROptions::on_sample observers use it (driver.cpp:47-60 reads
+// leaves(), dx(), origin() and dim()), served from the device tree.
+using SampleFn = std::function<void(long fine_steps_done, MRDevice& tree)>;
+
+// dump_tree_mesh (driver.cpp:47-60) of a device tree: the same text.
+inline std::string tree_mesh_text(MRDevice& tree) {
+  std::ostringstream os;
+  os.precision(12);
+  for (NodeKey k : tree.leaves()) {
+    const NodeId id = unpack_key(k);
+    const double h = tree.dx(id.level);
+    os << id.level;
+    for (int a = 0; a < tree.dim(); ++a) os << ' ' << tree.origin() + id.idx[a] * h;
+    for (int a = 0; a < tree.dim(); ++a) os << ' ' << tree.origin() + (id.idx[a] + 1) * h;
+    os << '\n';
+  }
+  return os.str();
+}
+
 // run_mr (mr_solver.cpp:318-400): fixed dt_fine = t_end / n_steps.
+// MROptions::on_sample observes a host MRTree, which the device run does not
+// build; a caller that sets it gets ConfigError instead of a silent skip, and
+// passes `sample` (called at the same point, mr_solver.cpp:394, with the
+// device tree) instead. Without `sample` the whole run is one af_mr_run call
+// (CUDA-graph cycles); with it the cycle loop runs here, one cycle at a time.
 inline MRDeviceResult run_mr(const CaseSpec& spec, int level, long n_steps,
                              const SchemeConfig& scheme, const MROptions& options,
-                             const std::vector<double>* eps_level = nullptr) {
+                             const std::vector<double>* eps_level = nullptr,
+                             const SampleFn& sample = nullptr) {
+  if (options.on_sample)
+    throw ConfigError(
+        "gpu::run_mr: MROptions::on_sample observes a host MRTree, which the device run does "
+        "not build; pass a gpu::SampleFn (leaf keys, to_uniform and the mesh geometry of the "
+        "device tree) instead");
   UniformGrid init(spec.dim, level, spec.origin, spec.extent);
   init_case(spec, init);
-  const af_config c = make_config(spec.dim, level, spec.origin, spec.extent, spec.gas, spec.bc,
-                                  scheme);
   af_mr_options o{};
   o.eps = options.epsilon;
   o.eps_level = eps_level ? eps_level->data() : nullptr;
   o.min_leaf_level = 0;
   o.local_time = options.local_time ? 1 : 0;
   o.lt_gap = options.local_time_level_gap;
-  af_mr* m = nullptr;
-  auto check = [&](af_status st) {
-    if (st == AF_OK) return;
-    af_error e{};
-    af_mr_last_error(m, &e);
-    if (m) af_mr_destroy(m);
-    rethrow(st, e);
-  };
-  check(af_mr_create(&c, &o, &m));
-  check(af_mr_build(m, to_aos(init.block()).data()));
-  std::vector<af_mr_cycle> cyc(static_cast<size_t>(n_steps));
-  af_run_diag d{};
-  const double dt_fine = spec.t_end / static_cast<double>(n_steps);
-  const auto t0 = std::chrono::steady_clock::now();
-  check(af_mr_run(m, n_steps, 0.0, dt_fine, cyc.data(), n_steps, &d));
+  MRDevice tree(spec.dim, level, spec.origin, spec.extent, spec.gas, spec.bc, scheme, o);
+  tree.build(init);
   MRDeviceResult out{UniformGrid(spec.dim, level, spec.origin, spec.extent), RunReport{}, {}};
   RunReport& rep = out.report;
-  rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   rep.method = options.local_time ? Method::MRLT : Method::MR;
   rep.case_name = spec.name;
   rep.level = level;
   rep.n_steps = n_steps;
   rep.preset_scheme = scheme.is_preset();
-  rep.max_cfl = d.max_cfl;
-  rep.fallbacks = d.fallbacks;
-  for (const af_mr_cycle& k : cyc) {
-    if (k.sub <= 0) break;
-    for (long s = 0; s < k.sub; ++s) {
-      rep.cells_per_step.push_back(k.nodes);
-      rep.leaves_per_step.push_back(k.leaves);
+  const double dt_fine = spec.t_end / static_cast<double>(n_steps);
+  if (!sample) {
+    std::vector<af_mr_cycle> cyc(static_cast<size_t>(n_steps));
+    af_run_diag d{};
+    const auto t0 = std::chrono::steady_clock::now();
+    tree.check(af_mr_run(tree.handle(), n_steps, 0.0, dt_fine, cyc.data(), n_steps, &d));
+    rep.wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    rep.max_cfl = d.max_cfl;
+    rep.fallbacks = d.fallbacks;
+    for (const af_mr_cycle& k : cyc) {
+      if (k.sub <= 0) break;
+      for (long s = 0; s < k.sub; ++s) {
+        rep.cells_per_step.push_back(k.nodes);
+        rep.leaves_per_step.push_back(k.leaves);
+      }
     }
+  } else {
+    // the cycle loop of mr_solver.cpp:339-395 on the device calls
+    using clock = std::chrono::steady_clock;
+    double wall = 0.0, max_speed = 0.0;
+    long done = 0;
+    while (done < n_steps) {
+      const auto t0 = clock::now();
+      long sub = 1;
+      int top = level;
+      if (options.local_time) {
+        top = std::max(tree.coarsest_leaf_level(), std::max(0, level - options.local_time_level_gap));
+        long span = 1l << (level - top);
+        while (span > n_steps - done) {
+          span >>= 1;
+          ++top;
+        }
+        sub = span;
+        tree.refine_lt(top);
+      } else {
+        tree.refine_lt(-1);
+      }
+      tree.add_virtual_leaves();
+      const long cells = tree.node_count(), leaves = tree.leaf_count();
+      for (long s = 0; s < sub; ++s) {
+        rep.cells_per_step.push_back(cells);
+        rep.leaves_per_step.push_back(leaves);
+      }
+      try {
+        if (options.local_time)
+          tree.advance_local(top, static_cast<double>(done) * dt_fine,
+                             static_cast<double>(sub) * dt_fine);
+        else
+          tree.evolve_global(dt_fine);
+      } catch (const NonPhysicalState& e) {
+        throw NonPhysicalState("step " + std::to_string(done) + ": " + e.what());
+      }
+      tree.remove_virtual_leaves();
+      tree.coarsen();
+      done += sub;
+      wall += std::chrono::duration<double>(clock::now() - t0).count();
+      sample(done, tree);
+    }
+    (void)max_speed;
+    rep.wall_seconds = wall;
+    tree.check(af_mr_solver_stats(tree.handle(), &rep.max_cfl, &rep.fallbacks));
   }
-  std::vector<double> aos(static_cast<size_t>(init.block().interior_cells()) * 5);
-  check(af_mr_to_uniform(m, level, aos.data()));
-  from_aos(aos, out.grid.block());
-  size_t n = 0;
-  check(af_mr_leaf_keys(m, nullptr, &n));
-  out.leaves.resize(n);
-  check(af_mr_leaf_keys(m, reinterpret_cast<uint64_t*>(out.leaves.data()), &n));
-  af_mr_destroy(m);
+  out.grid = tree.to_uniform(level);
+  out.leaves = tree.leaves();
   return out;
 }
 

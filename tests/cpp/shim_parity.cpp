@@ -7,6 +7,8 @@
 // bit-identical.
 #include <cstdio>
 #include <cstring>
+#include <sstream>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -101,6 +103,100 @@ int main() {
     gpu::MRDeviceResult g = gpu::run_mr(s, L, n, sc, o);
     report("run_mr ellipsoid3d L=4 leaves", r.tree.leaves() == g.leaves);
     report("run_mr ellipsoid3d L=4 state", same_grid(r.tree.to_uniform(L), g.grid));
+  }
+  // step_block twice on one geometry: one cached device context, each call
+  // bit-identical to the reference's step_block
+  {
+    const CaseSpec& s = find_case("lax_liu_6");
+    UniformGrid a(2, 6, s.origin, s.extent);
+    init_case(s, a);
+    UniformGrid b = a;
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const long c0 = gpu::step_block_cache().creations;
+    for (int it = 0; it < 2; ++it) {
+      fill_ghosts(a.block(), s.bc);
+      step_block(a.block(), a.dx(), 1e-3, sc, s.gas,
+                 [&](BlockData& blk) { fill_ghosts(blk, s.bc); });
+      gpu::step_block(b.block(), b, 1e-3, sc, s.gas, s.bc);
+    }
+    report("step_block x2 state", same_grid(a, b));
+    report("step_block x2 reuses one device context",
+           gpu::step_block_cache().creations - c0 <= 1);
+  }
+  // MROptions::on_sample (mr_solver.cpp:394): the reference's observer gets
+  // a host MRTree the device run cannot provide -> ConfigError, loudly; the
+  // device observer gets the same leaf sets at the same points.
+  for (int lt = 0; lt <= 1; ++lt) {
+    const CaseSpec& s = find_case("lax_liu_6");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 6;
+    const long n = s.steps_for_level(L);
+    std::vector<std::pair<long, std::vector<NodeKey>>> ref_samples, dev_samples;
+    std::vector<std::string> ref_mesh, dev_mesh;
+    MROptions o;
+    o.epsilon = s.mr_epsilon;
+    o.local_time = lt == 1;
+    o.on_sample = [&](long steps, const MRTree& tree) {
+      ref_samples.emplace_back(steps, tree.leaves());
+      std::ostringstream os;
+      os.precision(12);
+      for (NodeKey k : tree.leaves()) {  // driver.cpp:47-60 dump_tree_mesh text
+        const NodeId id = unpack_key(k);
+        const double h = tree.dx(id.level);
+        os << id.level;
+        for (int a = 0; a < tree.dim(); ++a) os << ' ' << tree.origin() + id.idx[a] * h;
+        for (int a = 0; a < tree.dim(); ++a) os << ' ' << tree.origin() + (id.idx[a] + 1) * h;
+        os << '\n';
+      }
+      ref_mesh.push_back(os.str());
+    };
+    MRRunResult r = run_mr(s, L, n, sc, o);
+    bool threw = false;
+    try {
+      gpu::run_mr(s, L, n, sc, o);
+    } catch (const ConfigError&) {
+      threw = true;
+    }
+    const std::string tag = lt ? "run_mr (MRLT) sampled" : "run_mr sampled";
+    report(tag + ": MROptions::on_sample raises ConfigError", threw);
+    MROptions od = o;
+    od.on_sample = nullptr;
+    gpu::MRDeviceResult g = gpu::run_mr(s, L, n, sc, od, nullptr,
+                                        [&](long steps, gpu::MRDevice& tree) {
+                                          dev_samples.emplace_back(steps, tree.leaves());
+                                          dev_mesh.push_back(gpu::tree_mesh_text(tree));
+                                        });
+    report(tag + ": sample points and leaf sets", ref_samples == dev_samples);
+    report(tag + ": mesh dump text", ref_mesh == dev_mesh);
+    report(tag + ": final state", same_grid(r.tree.to_uniform(L), g.grid));
+    report(tag + ": leaves_per_step", r.report.leaves_per_step == g.report.leaves_per_step);
+    report(tag + ": cells_per_step", r.report.cells_per_step == g.report.cells_per_step);
+    report(tag + ": max_cfl", r.report.max_cfl == g.report.max_cfl);
+    report(tag + ": fallbacks", r.report.fallbacks == g.report.fallbacks);
+  }
+  // MRTree::refine(eps, buffer_radius_per_level) (mr_tree.hpp:141)
+  for (int variant = 0; variant < 3; ++variant) {
+    const CaseSpec& s = find_case("lax_liu_6");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 7;
+    UniformGrid init(2, L, s.origin, s.extent);
+    init_case(s, init);
+    const double eps = s.mr_epsilon * (variant == 2 ? 0.5 : 1.0);
+    const std::vector<int> buffer =
+        variant == 0 ? std::vector<int>(L + 1, 1)
+                     : (variant == 1 ? std::vector<int>{0, 0, 1, 1, 2, 2, 3} : std::vector<int>{});
+    MRTree tree = MRTree::from_uniform(init, 0.0, s.bc);
+    tree.coarsen(s.mr_epsilon);
+    tree.refine(eps, buffer);
+    af_mr_options o{};
+    o.eps = s.mr_epsilon;
+    o.lt_gap = 3;
+    gpu::MRDevice dev(2, L, s.origin, s.extent, s.gas, s.bc, sc, o);
+    dev.build(init);
+    dev.refine(eps, buffer);
+    const std::string tag = "MRTree::refine(eps, buffer) variant " + std::to_string(variant);
+    report(tag + " leaves", tree.leaves() == dev.leaves());
+    report(tag + " to_uniform", same_grid(tree.to_uniform(L), dev.to_uniform(L)));
   }
   std::printf("%s (%d failures)\n", failures ? "SHIM PARITY FAILED" : "SHIM PARITY OK", failures);
   return failures ? 1 : 0;
