@@ -890,6 +890,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   a.regfc = d_regfc_;
   a.regff = d_regff_;
   a.regerr = d_regerr_;
+  a.tflag = std::getenv("AF_MR_NO_FULL") ? nullptr : d_tflag_;  // full-tile fast path
   for (int lv = 0; lv <= L_ && lv < 17; ++lv) {
     const double denom = t_new_[lv] - t_old_[lv];
     a.theta[lv] = denom > 0.0 ? std::clamp((tau - t_old_[lv]) / denom, 0.0, 1.0) : 1.0;

@@ -37,6 +37,7 @@ struct MRStageArgs {
   int* err;                  // [0] flag, [1] min code
   const int* tiles;
   int ntiles;          // tiles in the list (or the leaf-list selector 1 in multi-level mode)
+  const uint8_t* tflag;  // per-tile flags of the last list build (bit 2: a "full" tile)
   // local time stepping: virtual leaves whose parent level is below `lo`
   // read as q_old*(1-theta) + q*theta (resolve, mr_solver.cpp:43-50)
   int lo, hi;
@@ -224,7 +225,14 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
   const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
-  const bool is_leaf = inside && a.st[own] == ST_LEAF && row_owned(g, l, D == 3 ? cz : cy);
+  // A full tile (mr_tile_flags_all bit 2): every cell and every face
+  // neighbour of the tile is a leaf of this level, so every face is a plain
+  // same-level face (no fine sub-face average, no flux register) and every
+  // cell is updated: the per-face leaf and status tests are skipped.
+  // (2D only: in 3D the extra live state makes the kernel spill)
+  const bool full = D == 2 && a.tflag && (a.tflag[g.tile_off[l] + t] & 4);
+  const bool is_leaf =
+      full || (inside && a.st[own] == ST_LEAF && row_owned(g, l, D == 3 ? cz : cy));
   // with ranks, a stage-2 register pass also evaluates the halo-row leaves:
   // their fine-side register shares for this rank's coarse cells
   // (face_flux_at, mr_solver.cpp:147-159) are computed here, where those
@@ -232,17 +240,42 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   const bool is_hleaf = !is_leaf && a.reg_stage && g.dist && inside && a.st[own] == ST_LEAF &&
                         row_in_region(g, l, D == 3 ? cz : cy);
   leaf[tid] = is_leaf || is_hleaf;
-  for (int idx = tid; idx < K::HP; idx += K::NT) {
-    const int ix = idx % K::HX, iy = (idx / K::HX) % K::HY, iz = D == 3 ? idx / (K::HX * K::HY) : 0;
+  // Halo gather. In 2D both of a thread's cells are loaded before either is
+  // converted, so their global-memory round trips overlap; in 3D (five cells
+  // per thread) the loop stays rolled, as the extra registers would spill.
+  auto halo_xyz = [&](int idx, int& ix, int& iy, int& iz) {
+    ix = idx % K::HX;
+    iy = (idx / K::HX) % K::HY;
+    iz = D == 3 ? idx / (K::HX * K::HY) : 0;
     const bool ccx = ix >= 2 && ix < TX + 2, ccy = iy >= 2 && iy < TY + 2;
     const bool ccz = D == 2 || (iz >= 2 && iz < TZ + 2);
-    if ((int)!ccx + (int)!ccy + (int)!ccz > 1) continue;  // never on an axis stencil
-    const Cons<D> q = resolve_at<D>(a.eval, comp, g, l, x0 - 2 + ix, y0 - 2 + iy,
-                                    D == 3 ? z0 - 2 + iz : 0, &a);
+    return idx < K::HP && (int)!ccx + (int)!ccy + (int)!ccz <= 1;  // on an axis stencil
+  };
+  auto put_prim = [&](int idx, const Cons<D>& q) {
     const Prim<D> w = primitives(q, gm1);
 #pragma unroll
     for (int m = 0; m < NC; ++m)
       pr[m * K::HP + idx] = m == 0 ? w.rho : (m == NC - 1 ? w.p : w.v[m - 1]);
+  };
+  if constexpr (D == 2) {
+    static_assert((K::HP + K::NT - 1) / K::NT == 2, "2D: two halo cells per thread");
+    Cons<D> gq[2];
+    bool on[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int ix, iy, iz;
+      on[h] = halo_xyz(tid + h * K::NT, ix, iy, iz);
+      if (on[h]) gq[h] = resolve_at<D>(a.eval, comp, g, l, x0 - 2 + ix, y0 - 2 + iy, 0, &a);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (on[h]) put_prim(tid + h * K::NT, gq[h]);
+  } else {
+    for (int idx = tid; idx < K::HP; idx += K::NT) {
+      int ix, iy, iz;
+      if (!halo_xyz(idx, ix, iy, iz)) continue;
+      put_prim(idx, resolve_at<D>(a.eval, comp, g, l, x0 - 2 + ix, y0 - 2 + iy, z0 - 2 + iz, &a));
+    }
   }
   // early loads for the update phase (step-start values, neighbour status):
   // issued before the flux work so their latency is hidden behind it
@@ -258,8 +291,9 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
       for (int m = 0; m < NC; ++m) a.snap[m * comp + own] = base0[m];
     }
     const int c0[3] = {cx, cy, cz};
+    if (full) nbst = 0x555u & ((1u << (4 * D)) - 1u);  // every neighbour a leaf
 #pragma unroll
-    for (int ax = 0; ax < D; ++ax)
+    for (int ax = 0; ax < D && !full; ++ax)
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
         int p[3] = {c0[0], c0[1], c0[2]};
@@ -315,12 +349,13 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   auto do_face = [&](auto axc, int fx, int fy, int fz, int slot) {
     constexpr int AX = decltype(axc)::value;
     const int ex = AX == 0, ey = AX == 1, ez = AX == 2;
-    const bool lL = leaf_at(fx - ex, fy - ey, fz - ez), lR = leaf_at(fx, fy, fz);
+    const bool lL = full || leaf_at(fx - ex, fy - ey, fz - ez);
+    const bool lR = full || leaf_at(fx, fy, fz);
     if (!lL && !lR) return;
     int fb = 0;
     Cons<D> F;
     int side = 0;  // +1: leaf on the low side, INTERNAL high; -1: the reverse
-    if (fine_ok && lL != lR) {
+    if (!full && fine_ok && lL != lR) {
       const int ox = x0 + (lL ? fx : fx - ex), oy = y0 + (lL ? fy : fy - ey);
       const int oz = z0 + (lL ? fz : fz - ez);
       if (status_at(ox, oy, oz) == ST_INTERNAL) side = lL ? 1 : -1;
@@ -636,7 +671,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     const int x0 = (int)(t & (g.ntx[l] - 1)) * TX, y0 = (int)((t >> sx) & (g.nty[l] - 1)) * TY;
     const int z0 = D == 3 ? (int)(t >> (sx + sy)) * TZ : 0;
     unsigned nleaf = 0;
-    bool pex = false, rleaf = false;
+    bool pex = false, rleaf = false, notleaf = false;
     if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
       if (lane == 0) {
         tflag[tg] = 0;
@@ -646,8 +681,12 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     }
     for (int c = lane; c < TX * TY * TZ; c += 32) {
       const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
-      if (x >= n || y >= n || (D == 3 && z >= n)) continue;
+      if (x >= n || y >= n || (D == 3 && z >= n)) {
+        notleaf = true;
+        continue;
+      }
       const bool lf = st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF;
+      notleaf = notleaf || !lf;
       nleaf += lf && row_counted(g, l, D == 3 ? z : y);
       rleaf = rleaf || (lf && row_in_region(g, l, D == 3 ? z : y));
       pex = pex || l == 0 ||
@@ -656,10 +695,32 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     for (int o = 16; o > 0; o >>= 1) nleaf += __shfl_xor_sync(0xffffffffu, nleaf, o);
     pex = __any_sync(0xffffffffu, pex);
     rleaf = __any_sync(0xffffffffu, rleaf);
+    // bit 2, a full tile: every cell a leaf and every face neighbour of the
+    // tile (bc-mapped, same level) a leaf too (one rank only)
+    bool full = !g.dist && !__any_sync(0xffffffffu, notleaf);
+    if (full) {
+      constexpr int RX = TY * TZ, RY = TX * TZ, RZ = D == 3 ? TX * TY : 0;
+      bool ok = true;
+      for (int c = lane; c < 2 * (RX + RY + RZ); c += 32) {
+        int q[3], a, side, r;
+        if (c < 2 * RX) { a = 0; side = c / RX; r = c % RX; }
+        else if (c < 2 * (RX + RY)) { a = 1; side = (c - 2 * RX) / RY; r = (c - 2 * RX) % RY; }
+        else { a = 2; side = (c - 2 * (RX + RY)) / RZ; r = (c - 2 * (RX + RY)) % RZ; }
+        const int T[3] = {TX, TY, TZ};
+        const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
+        q[a] = (a == 0 ? x0 : (a == 1 ? y0 : z0)) + (side ? T[a] : -1);
+        q[b1] = (b1 == 0 ? x0 : y0) + r % T[b1];
+        q[b2] = D == 3 ? ((b2 == 1 ? y0 : z0) + r / T[b1]) : 0;
+        bool f;
+        for (int d = 0; d < D; ++d) q[d] = mr_map(q[d], n, g.bc[2 * d], g.bc[2 * d + 1], f);
+        ok = ok && st[g.cell_off[l] + mr_idx(D, n, q[0], q[1], q[2])] == ST_LEAF;
+      }
+      full = __all_sync(0xffffffffu, ok);
+    }
     if (lane == 0) {
       // bit 0: the tile holds a leaf this rank steps, or (with ranks) a
       // halo leaf whose register shares it computes
-      tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0);
+      tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0) | (full ? 4 : 0);
       tleaf[tg] = (int)nleaf;
     }
   }

@@ -11,6 +11,7 @@ stepping). The switches are read when a solver is created.
   AF_MR_NO_SWAP         stage commit copy instead of the buffer swap
   AF_MR_NO_TINY         one launch per coarse level instead of the single-CTA kernels
   AF_MR_FULL_SWEEPS     every coarsen sweep, no re-sweep skip test
+  AF_MR_NO_FULL         the general stage path for full tiles too (no fast path)
 """
 import os
 
@@ -22,7 +23,7 @@ from test_oracle import bits
 pytestmark = pytest.mark.gpu
 
 SWITCHES = ["AF_MR_NO_CYCLE_GRAPH", "AF_MR_NO_GRAPH", "AF_MR_NO_PDL", "AF_MR_NO_PRE",
-            "AF_MR_NO_SWAP", "AF_MR_NO_TINY", "AF_MR_FULL_SWEEPS"]
+            "AF_MR_NO_SWAP", "AF_MR_NO_TINY", "AF_MR_FULL_SWEEPS", "AF_MR_NO_FULL"]
 
 
 def run(switch, kind, level, steps, **kw):
