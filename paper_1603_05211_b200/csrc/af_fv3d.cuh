@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(NW * 32, 2)
   const int n = g.n;
   const int tiles_x = n / TX;
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const int zc0 = g.zlo + blockIdx.y * a.zchunk;
-  const int zc1 = min(zc0 + a.zchunk, g.zlo + g.nzl);
+  const int zc0 = a.zbeg + blockIdx.y * a.zchunk;
+  const int zc1 = min(zc0 + a.zchunk, a.zend);
   const bool owner = tid < K::NCELL && y0 + ty < n;  // an owned cell inside the mesh
   const double gamma = a.gamma, gm1 = a.gm1, inv_dx = a.inv_dx;
   const double rgm1 = 1.0 / gm1;

@@ -150,6 +150,15 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   reset_error_();
   std::memset(&last_, 0, sizeof(last_));
   last_.step = -1;
+  // NCCL ranks in 3D: the halo exchange runs on its own stream, overlapped
+  // with the interior planes of each stage (stage3d_overlapped_)
+  overlap_ = comm && comm->n > 1 && !comm->local && c.dim == 3 && g_.nzl >= 6 &&
+             !std::getenv("AF_UNIFORM_NO_OVERLAP");
+  if (overlap_) {
+    AF_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+    AF_CUDA(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming));
+    AF_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
+  }
   const size_t sm3 = Fv3d<1, 32, kTY>::smem_bytes;
   for (auto fn : {(const void*)fv3d_stage<0, 32, kTY>, (const void*)fv3d_stage<1, 32, kTY>,
                   (const void*)fv3d_stage<2, 32, kTY>, (const void*)fv3d_stage<3, 32, kTY>,
@@ -205,7 +214,7 @@ const CUtensorMap* Uniform::tensor_map_(const double* buf) {
 
 // The 3D RK2 stage on the TMA-fed 16x16 tile kernel (af_fv3d.cuh); false when
 // the mesh is too small for it or the legacy kernel is selected.
-bool Uniform::launch_tile3d_(const StageArgs& a) {
+bool Uniform::launch_tile3d_(const StageArgs& a, int zbeg, int zend) {
   const int n = g_.n;
   if (g_.dim != 3 || n < kT3) return false;
   // Exact mode runs the 32x8 fv3d_stage (5% faster bit-exact, profiles/r02_*);
@@ -215,10 +224,13 @@ bool Uniform::launch_tile3d_(const StageArgs& a) {
   if (!tm) return false;
   const long tiles = (long)(n / kT3) * ((n + kT3Y - 1) / kT3Y);
   const long target = 148L * 2 * 8;
-  int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, g_.nzl / 8));
+  const int nz = zend - zbeg;
+  int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, nz / 8));
   StageArgs b = a;
-  b.zchunk = (g_.nzl + chunks - 1) / chunks;
-  chunks = (g_.nzl + b.zchunk - 1) / b.zchunk;
+  b.zbeg = zbeg;
+  b.zend = zend;
+  b.zchunk = (nz + chunks - 1) / chunks;
+  chunks = (nz + b.zchunk - 1) / b.zchunk;
   dim3 grid((unsigned)tiles, (unsigned)chunks);
   const int sch = cfg_.limiter | (cfg_.flux << 1);
   if (numerics_ == AF_NUMERICS_TOLERANCE) {
@@ -247,6 +259,12 @@ Uniform::~Uniform() {
   cudaFree(d_err_);
   cudaFree(d_stage_);
   free_records_();
+  if (comm_stream_) {
+    cudaStreamSynchronize(comm_stream_);
+    cudaStreamDestroy(comm_stream_);
+  }
+  if (ev_ready_) cudaEventDestroy(ev_ready_);
+  if (ev_halo_) cudaEventDestroy(ev_halo_);
   if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -326,8 +344,9 @@ void Uniform::download(double* aos) {
 
 // Halo planes of `q` along the slab axis: 2 planes to each neighbour, one
 // NCCL message per direction (per-plane SoA keeps them contiguous).
-void Uniform::exchange_halos_(double* q) {
+void Uniform::exchange_halos_(double* q, cudaStream_t st) {
   if (!comm_ || comm_->n == 1) return;
+  if (!st) st = stream_;
   if (comm_->local) throw Error(AF_E_ARGUMENT, "ranks of a local group run via af_uniform_run_group");
   const int r = comm_->rank, P = comm_->n;
   const bool periodic = g_.bc[2 * (g_.dim - 1)] == AF_BC_PERIODIC &&
@@ -342,10 +361,10 @@ void Uniform::exchange_halos_(double* q) {
   // Posting order (top->hi, low halo<-lo, bottom->lo, high halo<-hi) keeps the
   // pairwise send/recv matching right when lo == hi (two periodic ranks).
   ck(ncclGroupStart());
-  if (hi >= 0) ck(ncclSend(q + (long)g_.nzl * g_.zs, cnt, ncclDouble, hi, nc, stream_));
-  if (lo >= 0) ck(ncclRecv(q, cnt, ncclDouble, lo, nc, stream_));
-  if (lo >= 0) ck(ncclSend(q + 2 * g_.zs, cnt, ncclDouble, lo, nc, stream_));
-  if (hi >= 0) ck(ncclRecv(q + (long)(g_.nzl + 2) * g_.zs, cnt, ncclDouble, hi, nc, stream_));
+  if (hi >= 0) ck(ncclSend(q + (long)g_.nzl * g_.zs, cnt, ncclDouble, hi, nc, st));
+  if (lo >= 0) ck(ncclRecv(q, cnt, ncclDouble, lo, nc, st));
+  if (lo >= 0) ck(ncclSend(q + 2 * g_.zs, cnt, ncclDouble, lo, nc, st));
+  if (hi >= 0) ck(ncclRecv(q + (long)(g_.nzl + 2) * g_.zs, cnt, ncclDouble, hi, nc, st));
   ck(ncclGroupEnd());
 }
 
@@ -386,18 +405,23 @@ void Uniform::launch_hancock_(const StageArgs& a) {
   AF_CUDA(cudaGetLastError());
 }
 
-void Uniform::launch_stage_(const StageArgs& a) {
-  if (launch_tile3d_(a)) return;
+void Uniform::launch_stage_(const StageArgs& a0, int zbeg, int zend) {
+  StageArgs a = a0;
+  a.zbeg = zbeg < 0 ? g_.zlo : zbeg;
+  a.zend = zend < 0 ? g_.zlo + g_.nzl : zend;
+  if (a.zend <= a.zbeg) return;
+  if (launch_tile3d_(a, a.zbeg, a.zend)) return;
   const int n = g_.n;
   const int tx = n >= 32 ? 32 : (n >= 16 ? 16 : 8);
   const int sch = cfg_.limiter | (cfg_.flux << 1);  // scheme code (af_physics.cuh)
   if (g_.dim == 3) {
     const long tiles = (long)(n / tx) * (n / kTY);
     const long target = 148L * 2 * 8;
-    int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, g_.nzl / 8));
+    const int nz = a.zend - a.zbeg;
+    int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, nz / 8));
     StageArgs b = a;
-    b.zchunk = (g_.nzl + chunks - 1) / chunks;
-    chunks = (g_.nzl + b.zchunk - 1) / b.zchunk;
+    b.zchunk = (nz + chunks - 1) / chunks;
+    chunks = (nz + b.zchunk - 1) / b.zchunk;
     dim3 grid((unsigned)tiles, (unsigned)chunks);
 #define AF_L3(L, TX)                                                                     \
   fv3d_stage<L, TX, kTY><<<grid, TX * kTY, Fv3d<L, TX, kTY>::smem_bytes, stream_>>>(b, g_)
@@ -478,22 +502,47 @@ void Uniform::enqueue_steps_(long n_steps, double cfl, double fixed_dt) {
   }
   for (long s = 0; s < n_steps; ++s) {
     a.step = (int)s;
-    exchange_halos_(d_u_);
     a.stage = 1;
     a.dt_scale = 0.5;
     a.eval = d_u_;
     a.base = d_u_;
     a.out = d_mid_;
-    launch_stage_(a);
-    exchange_halos_(d_mid_);
+    if (overlap_) {
+      stage3d_overlapped_(a, d_u_);
+    } else {
+      exchange_halos_(d_u_);
+      launch_stage_(a);
+    }
     a.stage = 2;
     a.dt_scale = 1.0;
     a.eval = d_mid_;
     a.base = d_u_;
     a.out = d_u_;
-    launch_stage_(a);
+    if (overlap_) {
+      stage3d_overlapped_(a, d_mid_);
+    } else {
+      exchange_halos_(d_mid_);
+      launch_stage_(a);
+    }
     if (a.use_cfl && comm_ && comm_->n > 1) allreduce_max_(rec_.smax + s + 1);
   }
+}
+
+// One 3D RK stage with the halo exchange of `eval` overlapped: the interior
+// planes [zlo+2, zlo+nzl-2) read no halo plane, so they run while NCCL moves
+// the halo planes on comm_stream_; the two planes at each slab end follow
+// once the halos have arrived. Per stage and neighbour the
+// exchange carries 2 planes x 5 components x n^2 doubles (21 MB at 512^2).
+void Uniform::stage3d_overlapped_(const StageArgs& a, double* eval) {
+  AF_CUDA(cudaEventRecord(ev_ready_, stream_));
+  AF_CUDA(cudaStreamWaitEvent(comm_stream_, ev_ready_, 0));
+  exchange_halos_(eval, comm_stream_);
+  AF_CUDA(cudaEventRecord(ev_halo_, comm_stream_));
+  const int z0 = g_.zlo, z1 = g_.zlo + g_.nzl;
+  launch_stage_(a, z0 + 2, z1 - 2);
+  AF_CUDA(cudaStreamWaitEvent(stream_, ev_halo_, 0));
+  launch_stage_(a, z0, z0 + 2);
+  launch_stage_(a, z1 - 2, z1);
 }
 
 namespace {
@@ -584,28 +633,37 @@ void Uniform::run_group(const std::vector<Uniform*>& R, long n_steps, double cfl
     }
     if (cfl > 0.0) group_max(s + 1);
   }
+  // 3D: the interior planes of every rank first, then the exchange, then the
+  // slab-end planes (the launch split of stage3d_overlapped_; on one stream
+  // here, so it checks the split, not the overlap)
+  const bool split = g0.dim == 3 && P > 1;
+  auto stage_all = [&](int which) {
+    for (int r = 0; r < P; ++r) {
+      StageArgs& a = A[r];
+      a.stage = which + 1;
+      a.dt_scale = which ? 1.0 : 0.5;
+      a.eval = which ? R[r]->d_mid_ : R[r]->d_u_;
+      a.base = R[r]->d_u_;
+      a.out = which ? R[r]->d_u_ : R[r]->d_mid_;
+      const int z0 = R[r]->g_.zlo, z1 = z0 + R[r]->g_.nzl;
+      if (split && z1 - z0 >= 6) R[r]->launch_stage_(a, z0 + 2, z1 - 2);
+    }
+    exchange(which);
+    for (int r = 0; r < P; ++r) {
+      StageArgs& a = A[r];
+      const int z0 = R[r]->g_.zlo, z1 = z0 + R[r]->g_.nzl;
+      if (split && z1 - z0 >= 6) {
+        R[r]->launch_stage_(a, z0, z0 + 2);
+        R[r]->launch_stage_(a, z1 - 2, z1);
+      } else {
+        R[r]->launch_stage_(a);
+      }
+    }
+  };
   for (long s = 0; s < n_steps && !hancock; ++s) {
-    exchange(0);
-    for (int r = 0; r < P; ++r) {
-      StageArgs& a = A[r];
-      a.step = (int)s;
-      a.stage = 1;
-      a.dt_scale = 0.5;
-      a.eval = R[r]->d_u_;
-      a.base = R[r]->d_u_;
-      a.out = R[r]->d_mid_;
-      R[r]->launch_stage_(a);
-    }
-    exchange(1);
-    for (int r = 0; r < P; ++r) {
-      StageArgs& a = A[r];
-      a.stage = 2;
-      a.dt_scale = 1.0;
-      a.eval = R[r]->d_mid_;
-      a.base = R[r]->d_u_;
-      a.out = R[r]->d_u_;
-      R[r]->launch_stage_(a);
-    }
+    for (int r = 0; r < P; ++r) A[r].step = (int)s;
+    stage_all(0);
+    stage_all(1);
     if (cfl > 0.0) group_max(s + 1);
   }
   // per-rank records -> the run's diagnostics (max/sum over ranks)

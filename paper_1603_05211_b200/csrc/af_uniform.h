@@ -51,10 +51,11 @@ class Uniform {
   void free_records_();
   void ensure_records_(long n);
   void ensure_staging_();
-  void exchange_halos_(double* q);
+  void exchange_halos_(double* q, cudaStream_t st = nullptr);
   void allreduce_max_(unsigned long long* bits);
-  void launch_stage_(const StageArgs& a);
-  bool launch_tile3d_(const StageArgs& a);
+  void launch_stage_(const StageArgs& a, int zbeg = -1, int zend = -1);
+  bool launch_tile3d_(const StageArgs& a, int zbeg, int zend);
+  void stage3d_overlapped_(const StageArgs& a, double* eval);
   const CUtensorMap* tensor_map_(const double* buf);
   void launch_hancock_(const StageArgs& a);
   void launch_speed_sum_(const double* q, unsigned long long* target);
@@ -83,6 +84,10 @@ class Uniform {
   bool tile_exact_ = false;  // AF_FV3D_TILE=1: the TMA tile kernel in exact mode too
   CUtensorMap tm_[2];      // TMA descriptors of d_u_ / d_mid_ (4D: x, y, component, plane)
   const double* tm_base_[2] = {nullptr, nullptr};
+  // halo exchange overlapped with the interior planes (3D, NCCL ranks)
+  cudaStream_t comm_stream_ = nullptr;
+  cudaEvent_t ev_ready_ = nullptr, ev_halo_ = nullptr;
+  bool overlap_ = false;
 };
 
 }  // namespace af

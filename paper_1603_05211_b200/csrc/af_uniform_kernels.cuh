@@ -30,6 +30,7 @@ struct StageArgs {
   double dt_scale;  // 0.5 (stage 1) or 1.0 (stage 2): stage_dt = dt_scale*dt (step.cpp:240,242)
   int step, stage;
   int zchunk;
+  int zbeg, zend;  // 3D: the planes [zbeg, zend) this launch updates (chunks of zchunk)
   RunRecords r;
 };
 
@@ -153,8 +154,8 @@ __global__ void __launch_bounds__(TX* TY, 2) fv3d_stage(StageArgs a, UGrid g) {
   const int n = g.n;
   const int tiles_x = n / TX;
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
-  const int zc0 = g.zlo + blockIdx.y * a.zchunk;
-  const int zc1 = min(zc0 + a.zchunk, g.zlo + g.nzl);
+  const int zc0 = a.zbeg + blockIdx.y * a.zchunk;
+  const int zc1 = min(zc0 + a.zchunk, a.zend);
   const double gamma = a.gamma, gm1 = a.gm1, inv_dx = a.inv_dx;
   const double rgm1 = 1.0 / gm1;  // RN(1/(gamma-1)) for div_rcp
   const double sdt = a.dt_scale * stage_dt_of(a);
