@@ -10,14 +10,18 @@
 //     back as zeros and are replaced by their boundary-condition source
 //     (grid.cpp:19-53) when the box is converted;
 //   * convert: staging -> primitives (with the reflective momentum flips) in a
-//     4-plane ring, the owned cells' positivity test and StepDiag wave speed;
-//   * faces: every face the plane's cells need — (TX+1)*TY x-faces,
-//     TX*(TY+1) y-faces, and the TX*TY z-faces between planes k and k+1 — is
-//     one entry of a flat list, 32 consecutive entries per warp unit, the
-//     normal axis a runtime value (af_physics.cuh sel_ax/add_ax), so the
-//     units are dealt evenly over the CTA's NW warps. The 16x15 tile with 8
-//     warps has 751 faces = 24 units, 3 per warp (a 16x16 tile would need 25
-//     units: a fourth pass for one warp at every barrier); the mesh's last
+//     3-plane ring (planes k, k+1, k+2), the owned cells' positivity test and
+//     StepDiag wave speed;
+//   * x/y faces: the (TX+1)*TY x-faces and TX*(TY+1) y-faces of plane k are
+//     one flat list, 32 consecutive entries per warp unit, dealt evenly over
+//     the CTA's NW warps;
+//   * z faces: the thread of each column computes the face k+1/2 above its
+//     cell. A cell's limited slope along z serves both of its z faces
+//     (muscl_recon evaluates the same limiter twice, on the same operands),
+//     so the column carries its next l state and last z difference from plane
+//     to plane: one new difference and one limiter per variable per face
+//     instead of three and two. The 16x15 tile with 8 warps has 511 x/y
+//     faces = 16 units (2 per warp) plus one z unit per warp; the mesh's last
 //     tile row is partial (its rows beyond the mesh are computed, never
 //     stored or counted);
 //   * update: each owned cell sums its six faces in the reference order and
@@ -46,17 +50,18 @@ struct Fv3dGeom {
   static constexpr int NCELL = TX * TY;
   static constexpr int HX = TX + 4, HY = TY + 4, HP = HX * HY;
   static constexpr int SLOT = 5 * HP;
-  static constexpr int NXF = (TX + 1) * TY, NYF = TX * (TY + 1), NZF = TX * TY;
-  // flat face list: x section [0, NXF), y section [YS, YS+NYF), z section
-  // [ZS, ZS+NZF); sections start on warp-unit boundaries so no unit mixes
-  // axes and every half-warp reads 16 consecutive doubles of a ring row. The
-  // x section lists the TX low faces of each row first (x fastest), then the
-  // TY high-edge faces.
-  static constexpr int YS = (NXF + 31) / 32 * 32, ZS = YS + (NYF + 31) / 32 * 32;
-  static constexpr int NF = ZS + NZF;
+  static constexpr int NXF = (TX + 1) * TY, NYF = TX * (TY + 1);
+  // flat x/y face list: x section [0, NXF), y section [YS, YS+NYF); sections
+  // start on warp-unit boundaries so no unit mixes axes and every half-warp
+  // reads 16 consecutive doubles of a ring row. The x section lists the TX
+  // low faces of each row first (x fastest), then the TY high-edge faces.
+  // The z faces are not in the list: each column's thread computes its own.
+  static constexpr int YS = (NXF + 31) / 32 * 32;
+  static constexpr int NF = YS + NYF;
   static constexpr int NU = (NF + 31) / 32;
   static constexpr int HPT = (HP + NT - 1) / NT;
-  static constexpr int RAW = (4 * SLOT + 15) / 16 * 16;  // staging, 128-byte aligned
+  static constexpr int RING = 3;  // primitive planes k, k+1, k+2
+  static constexpr int RAW = (RING * SLOT + 15) / 16 * 16;  // staging, 128-byte aligned
   static constexpr int FLUX = RAW + (SLOT + 15) / 16 * 16;
   static constexpr int RED = FLUX + 5 * NF;
   static constexpr size_t smem_bytes = sizeof(double) * (size_t)(RED + NW);
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
     phase ^= 1u;
     bool fz;
     const int zl = slab_map(gz, g, 2, fz);
-    double* dst = ring + ((gz + 4) & 3) * K::SLOT;
+    double* dst = ring + ((gz + 6) % K::RING) * K::SLOT;
     const bool own_plane = gz >= zc0 && gz < zc1;
 #pragma unroll
     for (int t = 0; t < K::HPT; ++t) {
@@ -252,50 +257,33 @@ __global__ void __launch_bounds__(NW * 32, 2)
     q.E = ev[4 * cs + c];
     return q;
   };
-  auto slot = [&](int gz) { return ((gz + 4) & 3) * K::SLOT; };
+  auto slot = [&](int gz) { return ((gz + 6) % K::RING) * K::SLOT; };
 
-  // Faces of plane k: x/y faces of plane k and the z faces k+1/2, from unit
-  // f_lo/32 on (the prologue computes only z faces). A unit lies in one axis
-  // section, so the axis is warp-uniform and a compile-time constant in the
-  // face body; every lane runs the body (padding lanes repeat a real face and
-  // store nothing), so the rare fallback and fast-path misses take a
-  // warp-uniform branch.
-  auto face_body = [&](auto axc, int k, int u, bool first_z) {
+  // x/y faces of plane k from unit u (a unit lies in one axis section, so the
+  // axis is warp-uniform and a compile-time constant in the face body; every
+  // lane runs the body (padding lanes repeat a real face and store nothing),
+  // so the rare fallback and fast-path misses take a warp-uniform branch.
+  auto face_body = [&](auto axc, int k, int u) {
     constexpr int AX = decltype(axc)::value;
-    constexpr int SEC = AX == 0 ? 0 : (AX == 1 ? K::YS : K::ZS);
-    constexpr int CNT = AX == 0 ? K::NXF : (AX == 1 ? K::NYF : K::NZF);
+    constexpr int SEC = AX == 0 ? 0 : K::YS;
+    constexpr int CNT = AX == 0 ? K::NXF : K::NYF;
     const int j0 = u * 32 + lane - SEC;
     const bool real = j0 < CNT;
     const int j = real ? j0 : 0;
     // face position (fx, fy): the face's high-side cell in tile coordinates
-    // (x faces: fx in [0, TX], y faces: fy in [0, TY]; z faces: the cell)
+    // (x faces: fx in [0, TX], y faces: fy in [0, TY])
     const int fx = AX == 0 ? (j < TX * TY ? j % TX : TX) : j % TX;
     const int fy = AX == 0 ? (j < TX * TY ? j / TX : j - TX * TY) : j / TX;
-    int o, st0, st1, st2;
-    if constexpr (AX == 0) {
-      o = slot(k) + (fy + 2) * K::HX + fx;
-      st0 = 1;
-      st1 = 2;
-      st2 = 3;
-    } else if constexpr (AX == 1) {
-      o = slot(k) + fy * K::HX + fx + 2;
-      st0 = K::HX;
-      st1 = 2 * K::HX;
-      st2 = 3 * K::HX;
-    } else {
-      o = slot(k - 1) + (fy + 2) * K::HX + fx + 2;
-      st0 = slot(k) - slot(k - 1);
-      st1 = slot(k + 1) - slot(k - 1);
-      st2 = slot(k + 2) - slot(k - 1);
-    }
+    constexpr int st = AX == 0 ? 1 : K::HX;
+    const int o = AX == 0 ? slot(k) + (fy + 2) * K::HX + fx : slot(k) + fy * K::HX + fx + 2;
     Prim<D> l, r;
     bool fb;
     if constexpr (MODE == 0)
-      fb = muscl_recon<D, S>(prim_at(o), prim_at(o + st0), prim_at(o + st1), prim_at(o + st2),
-                             l, r);
+      fb = muscl_recon<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
+                             prim_at(o + 3 * st), l, r);
     else
-      fb = muscl_recon_tol<D, S>(prim_at(o), prim_at(o + st0), prim_at(o + st1),
-                                 prim_at(o + st2), l, r);
+      fb = muscl_recon_tol<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
+                                 prim_at(o + 3 * st), l, r);
     Cons<D> F;
     if constexpr (MODE == 0)
       F = recon_flux_fast_warp<D, AX, S>(l, r, gamma, gm1, rgm1);
@@ -306,19 +294,17 @@ __global__ void __launch_bounds__(NW * 32, 2)
         // the inner cells' conserved states from global memory; their
         // primitives are recomputed exactly as the ring holds them. The
         // fallback is counted by the tile owning the face's high-side cell
-        // (the domain's high faces by the tile below them), and the chunk's
-        // first z face by the chunk below it, so each face counts once.
+        // (the domain's high faces by the tile below them), so each face
+        // counts once.
         const int gx = x0 + fx - (AX == 0), gy = y0 + fy - (AX == 1);
         bool cnt;
         if constexpr (AX == 0)
           cnt = (fx < TX || x0 + TX == n) && y0 + fy < n;
-        else if constexpr (AX == 1)
-          cnt = (fy < TY && y0 + fy < n) || y0 + fy == n;
         else
-          cnt = (!first_z || zc0 == 0) && y0 + fy < n;
+          cnt = (fy < TY && y0 + fy < n) || y0 + fy == n;
         if (cnt && real) ++nfb;
         const Cons<D> q0 = cons_at(gx, gy, k);
-        const Cons<D> q1 = cons_at(gx + (AX == 0), gy + (AX == 1), k + (AX == 2));
+        const Cons<D> q1 = cons_at(gx + (AX == 0), gy + (AX == 1), k);
         Prim<D> w0, w1;
         if constexpr (MODE == 0) {
           w0 = primitives(q0, gm1);
@@ -341,37 +327,101 @@ __global__ void __launch_bounds__(NW * 32, 2)
     }
   };
   const int rows = min(TY, n - y0);  // tile rows inside the mesh
-  auto faces = [&](int k, int f_lo) {
-    for (int u = f_lo / 32 + warp; u < K::NU; u += NW) {
+  auto faces = [&](int k) {
+    for (int u = warp; u < K::NU; u += NW) {
       // the last tile row of the mesh is partial: units whose faces all lie
       // beyond the mesh are skipped (warp-uniform)
       const int f0 = u * 32;
       if (rows < TY && (f0 < K::YS ? (f0 + 32 <= TX * TY && f0 / TX >= rows)
-                                   : (f0 < K::ZS ? (f0 - K::YS) / TX > rows
-                                                 : (f0 - K::ZS) / TX >= rows)))
+                                   : (f0 - K::YS) / TX > rows))
         continue;
       if (u * 32 < K::YS)
-        face_body(std::integral_constant<int, 0>{}, k, u, false);
-      else if (u * 32 < K::ZS)
-        face_body(std::integral_constant<int, 1>{}, k, u, false);
+        face_body(std::integral_constant<int, 0>{}, k, u);
       else
-        face_body(std::integral_constant<int, 2>{}, k, u, f_lo != 0);
+        face_body(std::integral_constant<int, 1>{}, k, u);
     }
   };
 
-  // Prologue: planes zc0-2 .. zc0 converted, zc0+1 in flight. Iteration
-  // k = zc0-1 computes only the chunk's first z face (zc0-1/2) and keeps it
-  // as the first plane's lower face (one call site of the face loop, so it
-  // stays inlined).
+  // z faces: the thread of column (tx, ty) computes the face k+1/2 above its
+  // cell of plane k. Each cell's limited z slope serves both of its z faces
+  // (cell_face_states), so the column carries the l state of the next face
+  // (zl) and the difference w(k+1) - w(k) (zd) from plane to plane.
+  const int oc = (ty + 2) * K::HX + tx + 2;  // the column's cell in a ring plane
+  double zl[5], zd[5];
+  auto zface = [&](int k, bool first) {
+    double rr[5], nl[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const double w1 = ring[slot(k + 1) + m * K::HP + oc];
+      const double w2 = ring[slot(k + 2) + m * K::HP + oc];
+      const double d2 = w2 - w1;
+      cell_face_states<S, MODE>(w1, zd[m], d2, rr[m], nl[m]);
+      zd[m] = d2;
+    }
+    Prim<D> l, r;
+    l.rho = zl[0];
+    l.v[0] = zl[1];
+    l.v[1] = zl[2];
+    l.v[2] = zl[3];
+    l.p = zl[4];
+    r.rho = rr[0];
+    r.v[0] = rr[1];
+    r.v[1] = rr[2];
+    r.v[2] = rr[3];
+    r.p = rr[4];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) zl[m] = nl[m];
+    const bool fb = !physical(l) || !physical(r);
+    Cons<D> F;
+    if constexpr (MODE == 0)
+      F = recon_flux_fast_warp<D, 2, S>(l, r, gamma, gm1, rgm1);
+    else
+      F = recon_flux_tol<D, S>(l, r, 2, gamma, gm1, rgm1, rgm1);
+    if (__any_sync(0xffffffffu, fb)) {
+      if (fb) {
+        // counted by the chunk above the face (the chunk's first face by the
+        // chunk below it, except at the domain's low boundary)
+        if ((!first || zc0 == 0) && owner) ++nfb;
+        const Cons<D> q0 = cons_at(x0 + tx, y0 + ty, k);
+        const Cons<D> q1 = cons_at(x0 + tx, y0 + ty, k + 1);
+        Prim<D> w0, w1;
+        if constexpr (MODE == 0) {
+          w0 = primitives(q0, gm1);
+          w1 = primitives(q1, gm1);
+        } else {
+          double i0, i1;
+          w0 = primitives_tol(q0, gm1, i0);
+          w1 = primitives_tol(q1, gm1, i1);
+        }
+        F = num_flux<D, 2, S>(q0, w0, q1, w1, gamma);
+      }
+    }
+    return F;
+  };
+
+  // Prologue: planes zc0-2 .. zc0 converted, zc0+1 in flight; the column's z
+  // state starts from the slope of plane zc0-1. Iteration k = zc0-1 computes
+  // only the chunk's first z face (zc0-1/2) and keeps it as the first
+  // plane's lower face.
   for (int z = zc0 - 2; z < zc0 + 1; ++z) {
     issue(z);
     convert(z);
     __syncthreads();
   }
   issue(zc0 + 1);
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    const double w0 = ring[slot(zc0 - 2) + m * K::HP + oc];
+    const double w1 = ring[slot(zc0 - 1) + m * K::HP + oc];
+    const double w2 = ring[slot(zc0) + m * K::HP + oc];
+    double unused;
+    zd[m] = w2 - w1;
+    cell_face_states<S, MODE>(w1, w1 - w0, zd[m], unused, zl[m]);
+  }
   const int ixl = ty * TX + tx, ixh = tx + 1 < TX ? ixl + 1 : TX * TY + ty,
-            iyl = K::YS + ty * TX + tx, izl = K::ZS + ty * TX + tx;
+            iyl = K::YS + ty * TX + tx;
   double zlo[5];
+  const double fdt = inv_dx * sdt;  // tolerance mode: rhs*inv_dx*dt folded
 
   for (int k = zc0 - 1; k < zc1; ++k) {
     const bool first = k < zc0;
@@ -384,29 +434,35 @@ __global__ void __launch_bounds__(NW * 32, 2)
     convert(k + 2);
     __syncthreads();  // ring slot k+2 complete, staging free, flux free
     if (k + 3 < zc1 + 2) issue(k + 3);
-    faces(k, first ? K::ZS : 0);
-    __syncthreads();
+    if (!first) faces(k);
+    const Cons<D> Fz = zface(k, first);
+    const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
     if (first) {
 #pragma unroll
-      for (int m = 0; m < 5; ++m) zlo[m] = owner ? flux[m * K::NF + izl] : 0.0;
+      for (int m = 0; m < 5; ++m) zlo[m] = zh[m];
       continue;
     }
+    __syncthreads();  // x/y fluxes of plane k complete
     if (owner) {
-      // rhs in the reference order (step.cpp:80-81): x low, x high, y low,
-      // y high, z low, z high; then out = base + rhs*stage_dt
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
         const double* fm = flux + m * K::NF;
-        const double zh = fm[izl];
-        double rhs = 0.0;
-        rhs = rhs + fm[ixl] * inv_dx;
-        rhs = rhs - fm[ixh] * inv_dx;
-        rhs = rhs + fm[iyl] * inv_dx;
-        rhs = rhs - fm[iyl + TX] * inv_dx;
-        rhs = rhs + zlo[m] * inv_dx;
-        rhs = rhs - zh * inv_dx;
-        b[m] = b[m] + rhs * sdt;
-        zlo[m] = zh;
+        if constexpr (MODE == 0) {
+          // rhs in the reference order (step.cpp:80-81): x low, x high, y
+          // low, y high, z low, z high; then out = base + rhs*stage_dt
+          double rhs = 0.0;
+          rhs = rhs + fm[ixl] * inv_dx;
+          rhs = rhs - fm[ixh] * inv_dx;
+          rhs = rhs + fm[iyl] * inv_dx;
+          rhs = rhs - fm[iyl + TX] * inv_dx;
+          rhs = rhs + zlo[m] * inv_dx;
+          rhs = rhs - zh[m] * inv_dx;
+          b[m] = b[m] + rhs * sdt;
+        } else {
+          const double s = ((fm[ixl] - fm[ixh]) + (fm[iyl] - fm[iyl + TX])) + (zlo[m] - zh[m]);
+          b[m] = __fma_rn(s, fdt, b[m]);
+        }
+        zlo[m] = zh[m];
       }
 #pragma unroll
       for (int m = 0; m < 5; ++m) a.out[m * cs + own] = b[m];

@@ -179,6 +179,11 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
       AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Geo3::smem_bytes));
     fv3d_tol_setup();
+    int per_sm = 0, sms = 0;
+    AF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, fv3d_tile<1, kT3, kT3Y, kW3, 0>, Geo3::NT, Geo3::smem_bytes));
+    AF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    tile_slots_ = std::max(1, per_sm * sms);
     // TMA descriptors: the slab allocation as a 4D tensor (x, y, component,
     // local plane); one (TX+4) x (TY+4) x 5 x 1 box per halo plane
     for (int b = 0; b < 2; ++b) {
@@ -223,9 +228,25 @@ bool Uniform::launch_tile3d_(const StageArgs& a, int zbeg, int zend) {
   const CUtensorMap* tm = tensor_map_(a.eval);
   if (!tm) return false;
   const long tiles = (long)(n / kT3) * ((n + kT3Y - 1) / kT3Y);
-  const long target = 148L * 2 * 8;
   const int nz = zend - zbeg;
-  int chunks = (int)std::max<long>(1, std::min<long>(target / tiles, nz / 8));
+  // z chunks per tile column: all CTAs take about the same time, so pick the
+  // count that minimises waves x (chunk planes + the 3-plane prologue) over
+  // the resident CTA slots (wave quantisation against prologue overhead)
+  int chunks = 1;
+  if (const char* e = std::getenv("AF_FV3D_CHUNKS")) chunks = std::max(1, std::atoi(e));
+  else {
+    const long slots = (long)tile_slots_;
+    double best = 1e300;
+    for (int c = 1; c <= 16 && c <= std::max(1, nz / 8); ++c) {
+      const long zc = (nz + c - 1) / c;
+      const long cc = (nz + zc - 1) / zc;
+      const double cost = (double)((tiles * cc + slots - 1) / slots) * (double)(zc + 3);
+      if (cost < best * 0.999) {
+        best = cost;
+        chunks = (int)cc;
+      }
+    }
+  }
   StageArgs b = a;
   b.zbeg = zbeg;
   b.zend = zend;

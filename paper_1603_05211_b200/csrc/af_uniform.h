@@ -81,6 +81,7 @@ class Uniform {
   long launches_ = 0;
   af_error last_{};
   int numerics_ = AF_NUMERICS_EXACT;
+  int tile_slots_ = 296;      // resident fv3d_tile CTAs on the device
   bool tile_exact_ = false;  // AF_FV3D_TILE=1: the TMA tile kernel in exact mode too
   CUtensorMap tm_[2];      // TMA descriptors of d_u_ / d_mid_ (4D: x, y, component, plane)
   const double* tm_base_[2] = {nullptr, nullptr};
