@@ -491,7 +491,7 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
         oname = "exact" if tol else "tolerance"
         other = {"numerics": NUMERICS[oname], "value": cells_total * 2 * args.steps / (oms / 1e3),
                  "unit": UNIT, "ms_per_step": oms / args.steps,
-                 "kernel": "fv3d_stage (legacy 32x8 tile)" if oname == "exact" else
+                 "kernel": "fv3d_tile<16x15, exact>" if oname == "exact" else
                            "fv3d_tile<16x15, tolerance>"}
 
     if rank != 0:
@@ -512,10 +512,11 @@ def uniform_bench(args, rank, world, local, comm, torch, dist):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-            "kernel": ("fv3d_tile<16x15, tolerance>" if tol else "fv3d_stage") if dim == 3
-                      else "fv2d_stage",
+            "kernel": ("fv3d_tile<16x15, tolerance>" if tol else "fv3d_tile<16x15, exact>")
+                      if dim == 3 else "fv2d_stage",
             "fp64": fp64_info(),
-            "note": "fp64-ALU bound in parity mode (no FMA contraction); see DESIGN.md"}
+            "note": "fp64-pipe and issue bound (~400 fp64 instructions per cell-stage), not "
+                    "HBM bound; see DESIGN.md"}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -63,7 +63,8 @@ struct Fv3dGeom {
   static constexpr int RING = 3;  // primitive planes k, k+1, k+2
   static constexpr int RAW = (RING * SLOT + 15) / 16 * 16;  // staging, 128-byte aligned
   static constexpr int FLUX = RAW + (SLOT + 15) / 16 * 16;
-  static constexpr int RED = FLUX + 5 * NF;
+  static constexpr int OWN = FLUX + (5 * NF + 15) / 16 * 16;  // [2][5][NCELL] base values
+  static constexpr int RED = OWN + 2 * 5 * NCELL;
   static constexpr size_t smem_bytes = sizeof(double) * (size_t)(RED + NW);
   static_assert(NCELL <= NT, "one thread per owned cell");
 };
@@ -104,7 +105,8 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 
 template <int S, int TX, int TY, int NW, int MODE>
 __global__ void __launch_bounds__(NW * 32, 2)
-    fv3d_tile(StageArgs a, UGrid g, const __grid_constant__ CUtensorMap tm) {
+    fv3d_tile(StageArgs a, UGrid g, const __grid_constant__ CUtensorMap tm,
+              const __grid_constant__ CUtensorMap tb) {
   using K = Fv3dGeom<TX, TY, NW>;
   constexpr int D = 3;
   if (failed_before(a.r.err)) return;  // an earlier stage failed: freeze state
@@ -112,8 +114,9 @@ __global__ void __launch_bounds__(NW * 32, 2)
   double* ring = sm;              // [4][5][HP] primitives
   double* raw = sm + K::RAW;      // [5][HP] conserved plane in flight (TMA)
   double* flux = sm + K::FLUX;    // [5][NF]
+  double* bown = sm + K::OWN;     // [2][5][NCELL] base values of the owned cells (TMA)
   double* red = sm + K::RED;      // [NW]
-  __shared__ unsigned long long bar;
+  __shared__ unsigned long long bar, bbar[2];
   __shared__ int s_fb, s_bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -131,6 +134,8 @@ __global__ void __launch_bounds__(NW * 32, 2)
     s_fb = 0;
     s_bad = 0;
     mbar_init(&bar, 1);
+    mbar_init(&bbar[0], 1);
+    mbar_init(&bbar[1], 1);
     if (a.stage == 1 && blockIdx.x == 0 && blockIdx.y == 0) a.r.dt[a.step] = stage_dt_of(a);
   }
   const double* ev = a.eval;
@@ -174,6 +179,15 @@ __global__ void __launch_bounds__(NW * 32, 2)
       tma_load_4d(raw, &tm, x0 - 2, y0 - 2, 0, zl, &bar);
     }
   };
+  // base values of the owned cells of plane gz into buffer gz&1, issued one
+  // plane ahead of the update that reads them
+  auto issue_base = [&](int gz) {
+    if (tid == 0) {
+      mbar_expect_tx(&bbar[gz & 1], (unsigned)(sizeof(double) * 5 * K::NCELL));
+      tma_load_4d(bown + (gz & 1) * 5 * K::NCELL, &tb, x0, y0, 0, gz - g.zlo + 2, &bbar[gz & 1]);
+    }
+  };
+  unsigned bphase = 0;  // bit j: parity of buffer j's next completion
   auto convert = [&](int gz) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
@@ -426,14 +440,11 @@ __global__ void __launch_bounds__(NW * 32, 2)
   for (int k = zc0 - 1; k < zc1; ++k) {
     const bool first = k < zc0;
     const long own = (long)(k - g.zlo + 2) * zs + (long)(y0 + ty) * n + (x0 + tx);
-    double b[5];
-    if (owner && !first) {
-#pragma unroll
-      for (int m = 0; m < 5; ++m) b[m] = a.base[m * cs + own];
-    }
     convert(k + 2);
     __syncthreads();  // ring slot k+2 complete, staging free, flux free
     if (k + 3 < zc1 + 2) issue(k + 3);
+    // its buffer was last read by the update of plane k-1 (before the barrier)
+    if (k + 1 < zc1) issue_base(k + 1);
     if (!first) faces(k);
     const Cons<D> Fz = zface(k, first);
     const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
@@ -443,7 +454,12 @@ __global__ void __launch_bounds__(NW * 32, 2)
       continue;
     }
     __syncthreads();  // x/y fluxes of plane k complete
+    mbar_wait(&bbar[k & 1], (bphase >> (k & 1)) & 1u);
+    bphase ^= 1u << (k & 1);
     if (owner) {
+      double b[5];
+#pragma unroll
+      for (int m = 0; m < 5; ++m) b[m] = bown[(k & 1) * 5 * K::NCELL + m * K::NCELL + tid];
 #pragma unroll
       for (int m = 0; m < 5; ++m) {
         const double* fm = flux + m * K::NF;

@@ -19,8 +19,8 @@ void fv3d_tol_setup() {
 }
 
 void fv3d_tol_launch(int sch, dim3 grid, cudaStream_t st, const StageArgs& a, const UGrid& g,
-                     const CUtensorMap& tm) {
-#define AF_T3(S) fv3d_tile<S, kT3, kT3Y, kW3, 1><<<grid, Geo3::NT, Geo3::smem_bytes, st>>>(a, g, tm)
+                     const CUtensorMap& tm, const CUtensorMap& tb) {
+#define AF_T3(S) fv3d_tile<S, kT3, kT3Y, kW3, 1><<<grid, Geo3::NT, Geo3::smem_bytes, st>>>(a, g, tm, tb)
   switch (sch) {
     case 0: AF_T3(0); break;
     case 1: AF_T3(1); break;

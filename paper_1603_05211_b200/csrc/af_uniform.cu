@@ -172,7 +172,7 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
                   (const void*)hancock_step<3, 2, 8, 8, 4>, (const void*)hancock_step<3, 3, 8, 8, 4>})
     AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smh));
   const char* te = std::getenv("AF_FV3D_TILE");
-  tile_exact_ = te && te[0] == '1';
+  tile_exact_ = !(te && te[0] == '0');
   if (c.dim == 3 && n >= kT3) {
     for (auto fn : {(const void*)fv3d_tile<0, kT3, kT3Y, kW3, 0>, (const void*)fv3d_tile<1, kT3, kT3Y, kW3, 0>,
                     (const void*)fv3d_tile<2, kT3, kT3Y, kW3, 0>, (const void*)fv3d_tile<3, kT3, kT3Y, kW3, 0>})
@@ -194,12 +194,15 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
                                      (cuuint64_t)g_.zs * 8};
       const cuuint32_t box[4] = {(cuuint32_t)Geo3::HX, (cuuint32_t)Geo3::HY, 5, 1};
       const cuuint32_t es[4] = {1, 1, 1, 1};
-      const CUresult r = encode_tiled()(&tm_[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims,
-                                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        CU_TENSOR_MAP_SWIZZLE_NONE,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw Error(AF_E_CUDA, "cuTensorMapEncodeTiled failed");
+      const cuuint32_t obox[4] = {(cuuint32_t)kT3, (cuuint32_t)kT3Y, 5, 1};
+      for (int own = 0; own < 2; ++own) {
+        const CUresult r = encode_tiled()(own ? &tmo_[b] : &tm_[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                          4, base, dims, strides, own ? obox : box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(AF_E_CUDA, "cuTensorMapEncodeTiled failed");
+      }
       tm_base_[b] = base;
     }
   }
@@ -211,9 +214,9 @@ void Uniform::set_numerics(int numerics) {
   numerics_ = numerics;
 }
 
-const CUtensorMap* Uniform::tensor_map_(const double* buf) {
+const CUtensorMap* Uniform::tensor_map_(const double* buf, bool own) {
   for (int b = 0; b < 2; ++b)
-    if (tm_base_[b] == buf) return &tm_[b];
+    if (tm_base_[b] == buf) return own ? &tmo_[b] : &tm_[b];
   return nullptr;
 }
 
@@ -222,11 +225,12 @@ const CUtensorMap* Uniform::tensor_map_(const double* buf) {
 bool Uniform::launch_tile3d_(const StageArgs& a, int zbeg, int zend) {
   const int n = g_.n;
   if (g_.dim != 3 || n < kT3) return false;
-  // Exact mode runs the 32x8 fv3d_stage (5% faster bit-exact, profiles/r02_*);
-  // AF_FV3D_TILE=1 selects the TMA tile kernel for it as well.
+  // AF_FV3D_TILE=0 runs exact mode on the legacy 32x8 fv3d_stage instead
+  // (bit-identical; tools/gpu/fv3d_check.py compares the two).
   if (numerics_ == AF_NUMERICS_EXACT && !tile_exact_) return false;
   const CUtensorMap* tm = tensor_map_(a.eval);
-  if (!tm) return false;
+  const CUtensorMap* tb = tensor_map_(a.base, true);
+  if (!tm || !tb) return false;
   const long tiles = (long)(n / kT3) * ((n + kT3Y - 1) / kT3Y);
   const int nz = zend - zbeg;
   // z chunks per tile column: all CTAs take about the same time, so pick the
@@ -255,10 +259,10 @@ bool Uniform::launch_tile3d_(const StageArgs& a, int zbeg, int zend) {
   dim3 grid((unsigned)tiles, (unsigned)chunks);
   const int sch = cfg_.limiter | (cfg_.flux << 1);
   if (numerics_ == AF_NUMERICS_TOLERANCE) {
-    fv3d_tol_launch(sch, grid, stream_, b, g_, *tm);
+    fv3d_tol_launch(sch, grid, stream_, b, g_, *tm, *tb);
   } else {
 #define AF_T3(S) \
-  fv3d_tile<S, kT3, kT3Y, kW3, 0><<<grid, Geo3::NT, Geo3::smem_bytes, stream_>>>(b, g_, *tm)
+  fv3d_tile<S, kT3, kT3Y, kW3, 0><<<grid, Geo3::NT, Geo3::smem_bytes, stream_>>>(b, g_, *tm, *tb)
     switch (sch) {
       case 0: AF_T3(0); break;
       case 1: AF_T3(1); break;

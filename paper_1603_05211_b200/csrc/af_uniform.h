@@ -17,7 +17,7 @@ struct UGrid;
 // translation unit (af_fv3d_tol.cu).
 void fv3d_tol_setup();
 void fv3d_tol_launch(int scheme, dim3 grid, cudaStream_t stream, const StageArgs& a,
-                     const UGrid& g, const CUtensorMap& tm);
+                     const UGrid& g, const CUtensorMap& tm, const CUtensorMap& tb);
 
 class Uniform {
  public:
@@ -56,7 +56,7 @@ class Uniform {
   void launch_stage_(const StageArgs& a, int zbeg = -1, int zend = -1);
   bool launch_tile3d_(const StageArgs& a, int zbeg, int zend);
   void stage3d_overlapped_(const StageArgs& a, double* eval);
-  const CUtensorMap* tensor_map_(const double* buf);
+  const CUtensorMap* tensor_map_(const double* buf, bool own = false);
   void launch_hancock_(const StageArgs& a);
   void launch_speed_sum_(const double* q, unsigned long long* target);
   void enqueue_steps_(long n_steps, double cfl, double fixed_dt);
@@ -82,8 +82,9 @@ class Uniform {
   af_error last_{};
   int numerics_ = AF_NUMERICS_EXACT;
   int tile_slots_ = 296;      // resident fv3d_tile CTAs on the device
-  bool tile_exact_ = false;  // AF_FV3D_TILE=1: the TMA tile kernel in exact mode too
+  bool tile_exact_ = true;   // AF_FV3D_TILE=0: exact mode on the legacy fv3d_stage
   CUtensorMap tm_[2];      // TMA descriptors of d_u_ / d_mid_ (4D: x, y, component, plane)
+  CUtensorMap tmo_[2];     // the same buffers with the owned-tile box (base values)
   const double* tm_base_[2] = {nullptr, nullptr};
   // halo exchange overlapped with the interior planes (3D, NCCL ranks)
   cudaStream_t comm_stream_ = nullptr;

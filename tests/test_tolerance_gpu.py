@@ -98,7 +98,7 @@ TILE_CASES = [
 def test_tile_kernel_exact_equals_fv3d_stage(gpu_lib, monkeypatch, level, steps, kind, bc,
                                              limiter, flux):
     """The TMA tile kernel (af_fv3d.cuh) in exact mode is bit-identical to the
-    32x8 fv3d_stage kernel (the exact-mode default), with the same dt history,
+    32x8 fv3d_stage kernel (AF_FV3D_TILE=0), with the same dt history,
     StepDiag wave speeds and fallback counts."""
     monkeypatch.setenv("AF_FV3D_TILE", "1")
     a, ra = run(level, steps, False, kind=kind, bc=bc, limiter=limiter, flux=flux)

@@ -1,5 +1,4 @@
-# one ncu --set full capture of the tolerance-mode fv3d kernel + SASS source export
+# one ncu --set full capture of the tolerance-mode fv3d kernel + SASS/source export
 ncu --set full --import-source on --clock-control none -k regex:fv3d -s 2 -c 1 -o gpurun_out/p_tol -f python tools/gpu/fv3d_one.py 9 2 tol > gpurun_out/p_tol.log 2>&1
-ncu -i gpurun_out/p_tol.ncu-rep --page source --csv --print-source sass > gpurun_out/p_tol_sass.csv 2>/dev/null
+ncu -i gpurun_out/p_tol.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/p_tol_mix.csv 2>/dev/null
 ncu -i gpurun_out/p_tol.ncu-rep --page raw --csv > gpurun_out/p_tol_raw.csv 2>/dev/null
-ls -la gpurun_out
