@@ -244,6 +244,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   tile_off_.assign(L_ + 2, 0);
   tile_count_.assign(L_ + 1, 0);
   band_count_.assign(L_ + 1, 0);
+  pband_count_.assign(L_ + 1, 0);
   long toff = 0;
   for (int l = 0; l <= L_; ++l) {
     tile_off_[l] = toff;
@@ -336,10 +337,11 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   }
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
+  AF_CUDA(cudaMalloc(&d_pband_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
   AF_CUDA(cudaMalloc(&d_tleaf_, sizeof(int) * toff));
-  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 34));
-  AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 34));
+  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 51));
+  AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 51));
   g_.dcnt = d_tile_count_;
   AF_CUDA(cudaMalloc(&d_dt_, sizeof(double)));
   AF_CUDA(cudaMalloc(&d_step3_, sizeof(int)));
@@ -414,7 +416,7 @@ MR::~MR() {
       cudaFree(p);
   }
   for (void* p : {(void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
-                  (void*)d_band_, (void*)d_tflag_, (void*)d_tleaf_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
+                  (void*)d_band_, (void*)d_pband_, (void*)d_tflag_, (void*)d_tleaf_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
                   (void*)d_flagi_, (void*)d_red_, (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_,
                   (void*)d_regff_, (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
     cudaFree(p);
@@ -458,6 +460,7 @@ double MR::eps_at_(int child_level) const {
 
 // band / leaf tile list of level l and a grid for it
 #define AF_BAND(l) d_band_ + tile_off_[l], (fixed_grids_ ? -1 : band_count_[l])
+#define AF_PBAND(l) d_pband_ + tile_off_[l], (fixed_grids_ ? -3 : pband_count_[l])
 #define AF_LEAFT(l) d_tiles_ + tile_off_[l], (fixed_grids_ ? -2 : tile_count_[l])
 // per-level tile-list grid: the live count, or in graph capture (device-side
 // counts) the level's tile total as the cycle-invariant bound
@@ -509,8 +512,18 @@ void MR::predict_fill_(int lo, int hi, int from) {
     AF_CUDA(cudaGetLastError());
     v_only_at_ = ++launches_;
   }
+  // While the statuses are those the lists were built from, only the band
+  // tiles holding an absent cell have anything to predict (a dense level has
+  // none); after merges every band tile is visited.
   for (int l = std::max(f, small + 1); l <= L_; ++l)
-    if (AF_HAS(band_count_[l])) {
+    if (pband_ok_) {
+      if (AF_HAS(pband_count_[l])) {
+        const int pre = pre_();
+        AF_MR_LAUNCH(mr_predict_level, AF_TGRID(l, pband_count_[l]), d_V_, d_st_, vm, g_, l, lo,
+                     hi, AF_PBAND(l), pre);
+        v_only_at_ = launches_;
+      }
+    } else if (AF_HAS(band_count_[l])) {
       const int pre = pre_();
       AF_MR_LAUNCH(mr_predict_level, AF_TGRID(l, band_count_[l]), d_V_, d_st_, vm, g_, l, lo, hi,
                    AF_BAND(l), pre);
@@ -568,7 +581,7 @@ void MR::project_range_(int lo, int top) {
 
 void MR::build_lists_() {
   build_lists_enqueue_();
-  int h[34];
+  int h[51];
   unsigned long long lp[17];
   AF_CUDA(cudaMemcpyAsync(h, d_tile_count_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaMemcpyAsync(lp, d_lpl_, sizeof lp, cudaMemcpyDeviceToHost, stream_));
@@ -577,6 +590,7 @@ void MR::build_lists_() {
   for (int l = 0; l <= L_; ++l) {
     band_count_[l] = h[l];
     tile_count_[l] = h[17 + l];
+    pband_count_[l] = h[34 + l];
     leaves_per_level_[l] = (long)lp[l];
     g_.band_cnt[l] = h[l];
     g_.leaf_cnt[l] = h[17 + l];
@@ -595,15 +609,16 @@ void MR::build_lists_enqueue_() {
     launch_k(pdl_, stream_, mr_tile_flags_all<3>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
              d_tile_count_, d_lpl_);
     launch_k(pdl_, stream_, mr_tile_lists_all<3>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
-             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_tile_count_, d_lpl_);
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_tile_count_, d_lpl_);
   } else {
     launch_k(pdl_, stream_, mr_tile_flags_all<2>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
              d_tile_count_, d_lpl_);
     launch_k(pdl_, stream_, mr_tile_lists_all<2>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
-             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_tile_count_, d_lpl_);
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_tile_count_, d_lpl_);
   }
   launches_ += 2;
   AF_CUDA(cudaGetLastError());
+  pband_ok_ = true;
 }
 
 // Grid of a multi-level launch over levels [lo, hi]: the total tile count of
@@ -1215,6 +1230,7 @@ void MR::coarsen() {
     lists_valid_ = true;
   }
   bool clean = false;  // the previous sweep raised no re-sweep flag
+  pband_ok_ = false;   // merges turn leaves into absent cells
   for (;;) {
     AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
     for (int l = L_ - 1; l >= min_leaf_; --l) {
@@ -1513,6 +1529,7 @@ void MR::enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* swe
   // refresh unconditionally, further sweeps (a WHILE node) only while one
   // merged and another can (the re-sweep test of coarsen_level_dev)
   AF_CUDA(cudaMemsetAsync(d_flagi_, 0, 2 * sizeof(int), stream_));
+  pband_ok_ = false;  // merges turn leaves into absent cells
   phase_("cycle end");
   for (int l = L_ - 1; l >= min_leaf_; --l)
     AF_MR_LAUNCH(mr_coarsen_level, AF_TGRIDL(l, 0, 1 << D_), d_V_, d_st_, g_, l, eps_at_(l + 1),

@@ -209,6 +209,7 @@ class MR {
   double* d_norms_ = nullptr;
   int* d_tiles_ = nullptr;       // per-level leaf-tile lists (tile_off_ regions)
   int* d_band_ = nullptr;        // per-level band-tile lists
+  int* d_pband_ = nullptr;       // band tiles holding an absent cell (prediction work)
   uint8_t* d_tflag_ = nullptr;
   int* d_tleaf_ = nullptr;  // leaves per tile (mr_tile_flags_all -> mr_tile_lists_all)
   int* d_tile_count_ = nullptr;  // [0..16] band counts, [17..33] leaf-tile counts
@@ -232,6 +233,8 @@ class MR {
   std::vector<long> tile_off_;           // per-level offset into d_tiles_
   std::vector<int> tile_count_;  // leaf tiles per level
   std::vector<int> band_count_;  // band tiles per level
+  std::vector<int> pband_count_; // band tiles with an absent cell per level
+  bool pband_ok_ = false;        // statuses unchanged since the lists were built
   bool fresh_ = false;
   bool coarse_stale_ = false;  // internal values below min_leaf-1 not projected (refresh_coarse_)
   void refresh_coarse_();

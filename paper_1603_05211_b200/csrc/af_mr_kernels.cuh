@@ -48,7 +48,8 @@ __device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
 }
 
 // Tile iteration of one launch. Single level (l >= 0): the `ntiles` entries
-// of `tiles` (ntiles -1 / -2: the band / leaf-tile count from g.dcnt).
+// of `tiles` (ntiles -1 / -2 / -3: the band / leaf-tile / absent-band count
+// from g.dcnt).
 // Multi-level (l = -(lo+1), ntiles = hi << 1 | sel): the band (sel 0) or leaf
 // (sel 1) lists of levels lo..hi as ONE flat range, so the grid follows the
 // total work instead of levels x the largest level. Each tile is visited
@@ -62,7 +63,7 @@ __device__ __forceinline__ int tile_total(const MRLevels& g, int l, int ntiles) 
     for (int k = -l - 1; k <= (ntiles >> 1); ++k) total += cnt[k];
     return total;
   }
-  return ntiles < 0 ? (ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l]) : ntiles;
+  return ntiles < 0 ? g.dcnt[17 * (-ntiles - 1) + l] : ntiles;
 }
 __device__ __forceinline__ int tile_at(const MRLevels& g, int l, const int* tiles, int ntiles,
                                        int it, int* level) {
@@ -112,7 +113,7 @@ __device__ __forceinline__ void for_each_tile(const MRLevels& g, int l, const in
       f(k, t, it - ti * reps);
     }
   } else {
-    if (ntiles < 0) ntiles = ntiles == -1 ? g.dcnt[l] : g.dcnt[17 + l];
+    if (ntiles < 0) ntiles = g.dcnt[17 * (-ntiles - 1) + l];
     for (int it = blockIdx.x; it < ntiles * reps; it += gridDim.x) {
       const int ti = it / reps;
       f(l, tiles[ti], it - ti * reps);

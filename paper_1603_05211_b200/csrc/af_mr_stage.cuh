@@ -655,7 +655,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
                                   int* counts, unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
   // the list counts and leaves per level mr_tile_lists_all accumulates
-  if (blockIdx.x == 0 && threadIdx.x < 34) counts[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 51) counts[threadIdx.x] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 17) leaves_per_level[threadIdx.x] = 0;
   constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
   constexpr int TZ = D == 3 ? kTileZ3 : 1;
@@ -671,7 +671,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     const int x0 = (int)(t & (g.ntx[l] - 1)) * TX, y0 = (int)((t >> sx) & (g.nty[l] - 1)) * TY;
     const int z0 = D == 3 ? (int)(t >> (sx + sy)) * TZ : 0;
     unsigned nleaf = 0;
-    bool pex = false, rleaf = false, notleaf = false;
+    bool pex = false, rleaf = false, notleaf = false, absent = false;
     if (!tile_in_region<D>(g, l, D == 3 ? z0 : y0)) {
       if (lane == 0) {
         tflag[tg] = 0;
@@ -685,8 +685,10 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
         notleaf = true;
         continue;
       }
-      const bool lf = st[g.cell_off[l] + mr_idx(D, n, x, y, z)] == ST_LEAF;
+      const uint8_t s = st[g.cell_off[l] + mr_idx(D, n, x, y, z)];
+      const bool lf = s == ST_LEAF;
       notleaf = notleaf || !lf;
+      absent = absent || s == ST_ABSENT;
       nleaf += lf && row_counted(g, l, D == 3 ? z : y);
       rleaf = rleaf || (lf && row_in_region(g, l, D == 3 ? z : y));
       pex = pex || l == 0 ||
@@ -695,6 +697,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     for (int o = 16; o > 0; o >>= 1) nleaf += __shfl_xor_sync(0xffffffffu, nleaf, o);
     pex = __any_sync(0xffffffffu, pex);
     rleaf = __any_sync(0xffffffffu, rleaf);
+    absent = __any_sync(0xffffffffu, absent);
     // bit 2, a full tile: every cell a leaf and every face neighbour of the
     // tile (bc-mapped, same level) a leaf too (one rank only)
     bool full = !g.dist && !__any_sync(0xffffffffu, notleaf);
@@ -720,7 +723,8 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     if (lane == 0) {
       // bit 0: the tile holds a leaf this rank steps, or (with ranks) a
       // halo leaf whose register shares it computes
-      tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0) | (full ? 4 : 0);
+      tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0) | (full ? 4 : 0) |
+                  (absent ? 8 : 0);
       tleaf[tg] = (int)nleaf;
     }
   }
@@ -733,7 +737,8 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
 // projections, predictions, details and merges are evaluated.
 template <int D>
 __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLevels g, int* band,
-                                  int* leaf, int* counts, unsigned long long* leaves_per_level) {
+                                  int* leaf, int* pband, int* counts,
+                                  unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
   const long total = g.tile_off[g.L + 1];
   for (long tg = blockIdx.x * (long)blockDim.x + threadIdx.x; tg < total;
@@ -772,17 +777,22 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLeve
     const bool in_leaf = (tflag[tg] & 1) != 0;
     const unsigned bb = __ballot_sync(grp, in_band) & grp;
     const unsigned lb = __ballot_sync(grp, in_leaf) & grp;
+    const bool in_pband = in_band && (tflag[tg] & 8) != 0;
+    const unsigned pb = __ballot_sync(grp, in_pband) & grp;
     const unsigned nl = __reduce_add_sync(grp, (unsigned)tleaf[tg]);
-    int bbase = 0, lbase = 0;
+    int bbase = 0, lbase = 0, pbase = 0;
     if (lane == leader) {
       if (bb) bbase = atomicAdd(counts + l, __popc(bb));
       if (lb) lbase = atomicAdd(counts + 17 + l, __popc(lb));
+      if (pb) pbase = atomicAdd(counts + 34 + l, __popc(pb));
       if (nl) atomicAdd(leaves_per_level + l, (unsigned long long)nl);
     }
     bbase = __shfl_sync(grp, bbase, leader);
     lbase = __shfl_sync(grp, lbase, leader);
+    pbase = __shfl_sync(grp, pbase, leader);
     if (in_band) band[g.tile_off[l] + bbase + __popc(bb & below)] = (int)t;
     if (in_leaf) leaf[g.tile_off[l] + lbase + __popc(lb & below)] = (int)t;
+    if (in_pband) pband[g.tile_off[l] + pbase + __popc(pb & below)] = (int)t;
   }
 }
 
