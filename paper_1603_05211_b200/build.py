@@ -21,9 +21,8 @@ SOURCES = ["af_abi.cu", "af_uniform.cu", "af_fv3d_tol.cu", "af_mr.cu", "af_mr_di
            "af_io.cu"]
 # translation units compiled WITH FMA contraction (tolerance-mode kernels only)
 FMAD_TRUE = {"af_fv3d_tol.cu"}
-HEADERS = ["af_physics.cuh", "af_uniform_kernels.cuh", "af_internal.h", "af_uniform.h",
-           "af_comm.h", "af_mr.h", "af_mr_kernels.cuh", "af_mr_types.h",
-           "af_mr_stage.cuh", "af_hancock.cuh", "af_fv3d.cuh"]
+HEADERS = sorted(f for f in os.listdir(os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc"))
+                 if f.endswith((".cuh", ".h")))
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",

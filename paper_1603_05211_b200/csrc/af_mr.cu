@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "af_mr.h"
+#include "af_mr_full.cuh"
 #include "af_mr_stage.cuh"
 
 namespace af {
@@ -245,6 +246,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   tile_count_.assign(L_ + 1, 0);
   band_count_.assign(L_ + 1, 0);
   pband_count_.assign(L_ + 1, 0);
+  full_count_.assign(L_ + 1, 0);
   long toff = 0;
   for (int l = 0; l <= L_; ++l) {
     tile_off_[l] = toff;
@@ -338,10 +340,12 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
   AF_CUDA(cudaMalloc(&d_tiles_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_band_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_pband_, sizeof(int) * toff));
+  AF_CUDA(cudaMalloc(&d_lpart_, sizeof(int) * toff));
+  AF_CUDA(cudaMalloc(&d_lfull_, sizeof(int) * toff));
   AF_CUDA(cudaMalloc(&d_tflag_, toff));
   AF_CUDA(cudaMalloc(&d_tleaf_, sizeof(int) * toff));
-  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 51));
-  AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 51));
+  AF_CUDA(cudaMalloc(&d_tile_count_, sizeof(int) * 85));
+  AF_CUDA(cudaMemset(d_tile_count_, 0, sizeof(int) * 85));
   g_.dcnt = d_tile_count_;
   AF_CUDA(cudaMalloc(&d_dt_, sizeof(double)));
   AF_CUDA(cudaMalloc(&d_step3_, sizeof(int)));
@@ -368,6 +372,11 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
                     (const void*)mr_stage_kernel<3, 3, kTX3, kTY3, kTZ3>})
       AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)MRTile<3, kTX3, kTY3, kTZ3>::smem_bytes));
+  } else {
+    for (auto fn : {(const void*)mr_stage_full2d<0>, (const void*)mr_stage_full2d<1>,
+                    (const void*)mr_stage_full2d<2>, (const void*)mr_stage_full2d<3>})
+      AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)MRFull2::smem_bytes));
   }
   if (dist_) dist_setup_();
 }
@@ -416,7 +425,7 @@ MR::~MR() {
       cudaFree(p);
   }
   for (void* p : {(void*)d_norms_, (void*)d_tiles_, (void*)d_tile_count_, (void*)d_err_,
-                  (void*)d_band_, (void*)d_pband_, (void*)d_tflag_, (void*)d_tleaf_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
+                  (void*)d_band_, (void*)d_pband_, (void*)d_lpart_, (void*)d_lfull_, (void*)d_tflag_, (void*)d_tleaf_, (void*)d_lpl_, (void*)d_dt_, (void*)d_step3_,
                   (void*)d_flagi_, (void*)d_red_, (void*)d_regc_, (void*)d_regf_, (void*)d_regfc_,
                   (void*)d_regff_, (void*)d_regcount_, (void*)d_regerr_, (void*)d_badkey_})
     cudaFree(p);
@@ -446,7 +455,7 @@ double MR::eps_at_(int child_level) const {
     if (ml_grid_((lo), (hi), (leaf), &grid_, (mult))) {                           \
       const int AF_L = -(std::max((lo), 0) + 1);                                   \
       const int* AF_T = (leaf) ? d_tiles_ : d_band_;                               \
-      const int AF_S = (std::min((hi), L_) << 1) | ((leaf) ? 1 : 0);              \
+      const int AF_S = (std::min((hi), L_) << 3) | ((leaf) ? 1 : 0);              \
       if (D_ == 3)                                                                 \
         launch_k(pdl_, stream_, kern<3>, grid_, 256, 0, __VA_ARGS__, AF_T, AF_S);   \
       else                                                                         \
@@ -581,7 +590,7 @@ void MR::project_range_(int lo, int top) {
 
 void MR::build_lists_() {
   build_lists_enqueue_();
-  int h[51];
+  int h[85];
   unsigned long long lp[17];
   AF_CUDA(cudaMemcpyAsync(h, d_tile_count_, sizeof h, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaMemcpyAsync(lp, d_lpl_, sizeof lp, cudaMemcpyDeviceToHost, stream_));
@@ -591,6 +600,7 @@ void MR::build_lists_() {
     band_count_[l] = h[l];
     tile_count_[l] = h[17 + l];
     pband_count_[l] = h[34 + l];
+    full_count_[l] = h[68 + l];
     leaves_per_level_[l] = (long)lp[l];
     g_.band_cnt[l] = h[l];
     g_.leaf_cnt[l] = h[17 + l];
@@ -609,12 +619,14 @@ void MR::build_lists_enqueue_() {
     launch_k(pdl_, stream_, mr_tile_flags_all<3>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
              d_tile_count_, d_lpl_);
     launch_k(pdl_, stream_, mr_tile_lists_all<3>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
-             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_tile_count_, d_lpl_);
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_lpart_, d_lfull_,
+             d_tile_count_, d_lpl_);
   } else {
     launch_k(pdl_, stream_, mr_tile_flags_all<2>, dim3(gw), 256, 0, d_st_, g_, d_tflag_, d_tleaf_,
              d_tile_count_, d_lpl_);
     launch_k(pdl_, stream_, mr_tile_lists_all<2>, dim3(gt), 256, 0, (const uint8_t*)d_tflag_,
-             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_tile_count_, d_lpl_);
+             (const int*)d_tleaf_, g_, d_band_, d_tiles_, d_pband_, d_lpart_, d_lfull_,
+             d_tile_count_, d_lpl_);
   }
   launches_ += 2;
   AF_CUDA(cudaGetLastError());
@@ -938,10 +950,40 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
       ++stage_launches_;
       stage_updates_ += leaves_per_level_[l];
     }
+  // Full 2D tiles (every cell and face neighbour a leaf of the level) run on
+  // mr_stage_full2d, the other leaf tiles on mr_stage_kernel (AF_MR_NO_FULLK:
+  // every leaf tile on mr_stage_kernel, with its own full-tile fast path).
+  const bool fullk = D_ == 2 && !g_.dist && a.tflag && !std::getenv("AF_MR_NO_FULLK");
+  long nfull = 0, npart = 0;
+  for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l) {
+    const long tot = fixed_grids_ ? level_tiles_(l) : tile_count_[l];
+    const long fu = fixed_grids_ ? level_tiles_(l) : full_count_[l];
+    nfull += fu;
+    npart += fixed_grids_ ? tot : tot - fu;
+  }
+  if (fullk && nfull > 0) {
+    MRStageArgs f = a;
+    f.tiles = d_lfull_;
+    f.ntiles = (std::min(hi, L_) << 3) | 4;
+    const dim3 gf((unsigned)std::min<long>(nfull, kStageGrid));
+    const int lcode = -(std::max(lo, 0) + 1);
+    const int sch = cfg_.limiter | (cfg_.flux << 1);
+    const size_t smf = MRFull2::smem_bytes;
+    switch (sch) {
+      case 0: launch_k(pdl_, stream_, mr_stage_full2d<0>, gf, MRFull2::NT, smf, f, g_, lcode); break;
+      case 1: launch_k(pdl_, stream_, mr_stage_full2d<1>, gf, MRFull2::NT, smf, f, g_, lcode); break;
+      case 2: launch_k(pdl_, stream_, mr_stage_full2d<2>, gf, MRFull2::NT, smf, f, g_, lcode); break;
+      default: launch_k(pdl_, stream_, mr_stage_full2d<3>, gf, MRFull2::NT, smf, f, g_, lcode); break;
+    }
+    ++launches_;
+    AF_CUDA(cudaGetLastError());
+  }
   dim3 grid;
-  if (ml_grid_(lo, hi, true, &grid, 1, kStageGrid)) {
-    a.tiles = d_tiles_;
-    a.ntiles = (std::min(hi, L_) << 1) | 1;
+  const bool part_only = fullk;
+  if (part_only ? npart > 0 && (grid = dim3((unsigned)std::min<long>(npart, kStageGrid)), true)
+                : ml_grid_(lo, hi, true, &grid, 1, kStageGrid)) {
+    a.tiles = part_only ? d_lpart_ : d_tiles_;
+    a.ntiles = (std::min(hi, L_) << 3) | (part_only ? 3 : 1);
     const int lcode = -(std::max(lo, 0) + 1);
     const int sch = cfg_.limiter | (cfg_.flux << 1);  // scheme code (af_physics.cuh)
     const unsigned b2 = kTX2 * kTY2, b3 = kTX3 * kTY3 * kTZ3;

@@ -210,6 +210,8 @@ class MR {
   int* d_tiles_ = nullptr;       // per-level leaf-tile lists (tile_off_ regions)
   int* d_band_ = nullptr;        // per-level band-tile lists
   int* d_pband_ = nullptr;       // band tiles holding an absent cell (prediction work)
+  int* d_lpart_ = nullptr;       // leaf tiles that are not full (mr_stage_kernel)
+  int* d_lfull_ = nullptr;       // full leaf tiles (mr_stage_full2d)
   uint8_t* d_tflag_ = nullptr;
   int* d_tleaf_ = nullptr;  // leaves per tile (mr_tile_flags_all -> mr_tile_lists_all)
   int* d_tile_count_ = nullptr;  // [0..16] band counts, [17..33] leaf-tile counts
@@ -234,6 +236,7 @@ class MR {
   std::vector<int> tile_count_;  // leaf tiles per level
   std::vector<int> band_count_;  // band tiles per level
   std::vector<int> pband_count_; // band tiles with an absent cell per level
+  std::vector<int> full_count_;  // full leaf tiles per level
   bool pband_ok_ = false;        // statuses unchanged since the lists were built
   bool fresh_ = false;
   bool coarse_stale_ = false;  // internal values below min_leaf-1 not projected (refresh_coarse_)

@@ -1,0 +1,302 @@
+// af_mr_full.cuh — the MR stage on FULL 2D tiles (sm_100a).
+//
+// A full tile (mr_tile_flags_all bit 2) is a 32x8 tile of level l whose
+// cells and face neighbours are all leaves of l: every face is a plain
+// same-level face of MRSolver::stage (mr_solver.cpp:163-193) — no fine
+// sub-face average, no flux register, no leaf tests. Dense regions of a tree
+// (cfg3's finest level is all leaves) are made of them, so they get their own
+// kernel, pipelined like the uniform fv3d_tile:
+//   * the next tile's halo box (the 36x12 cross of the tile, bc-mapped as
+//     map_position, mr_tree.cpp:146-169) and its step-start values are copied
+//     into shared memory with cp.async while the current tile is computed
+//     (double-buffered), so the gather latency is off the critical path;
+//   * convert: box -> primitives (reflective momentum flips; MRLT virtual
+//     leaves over an advanced coarser leaf interpolated in time exactly as
+//     resolve_at does, mr_solver.cpp:43-50);
+//   * faces: the 264 x-faces and 288 y-faces of the tile as one flat list,
+//     32 per warp unit, the axis warp-uniform (18 units over 8 warps);
+//   * update: each leaf sums its four faces in the reference order and
+//     writes out = base + rhs*stage_dt (+ the stage-1 q_old snapshot and the
+//     stage-2 positivity check).
+// Every operation and its order are those of mr_stage_kernel, so the two are
+// bit-identical (tests/test_mr_switches_gpu.py compares them); the generic
+// kernel handles the other leaf tiles of the same stage.
+#pragma once
+
+#include "af_mr_stage.cuh"
+
+namespace af {
+
+struct MRFull2 {
+  // 8 warps, one thread per cell (a 9-warp variant that deals the 18 face
+  // units two per warp measured 40% slower on B200)
+  static constexpr int TX = kTileX2, TY = kTileY2, NCELL = TX * TY, NW = 8, NT = NW * 32, NC = 4;
+  static constexpr int HX = TX + 4, HY = TY + 4, HP = HX * HY;
+  static constexpr int NXF = (TX + 1) * TY, NYF = TX * (TY + 1);
+  static constexpr int YS = (NXF + 31) / 32 * 32, NF = YS + NYF, NU = (NF + 31) / 32;
+  static constexpr int HPT = (HP + NT - 1) / NT;
+  // shared memory (doubles): raw[2][NC][HP], base[2][NC][NCELL], pr[NC][HP], fl[NC][NF]
+  static constexpr int RAW = 0, BASE = 2 * NC * HP, PR = BASE + 2 * NC * NCELL, FL = PR + NC * HP;
+  static constexpr int RED = FL + NC * NF;
+  static constexpr size_t smem_bytes = sizeof(double) * (size_t)(RED + NW) + NF;
+};
+
+template <int S>
+__global__ void __launch_bounds__(MRFull2::NT, 2)
+    mr_stage_full2d(MRStageArgs a, MRLevels g, int lcode) {
+  AF_PDL_ENTRY();
+  using K = MRFull2;
+  constexpr int D = 2, NC = K::NC, TX = K::TX, TY = K::TY;
+  if (failed_before(a.err)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* raw = sm + K::RAW;
+  double* bsm = sm + K::BASE;
+  double* pr = sm + K::PR;
+  double* fl = sm + K::FL;
+  double* red = sm + K::RED;
+  uint8_t* ffb = reinterpret_cast<uint8_t*>(red + K::NW);
+  __shared__ int s_fb, s_bad;
+  (void)red;
+
+  const double sdt = a.dt_dev ? a.dt_scale * *a.dt_dev : a.sdt;
+  const int step3 = a.step3_dev ? *a.step3_dev : a.step3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tid % TX, ty = tid / TX;
+  const bool owner = tid < K::NCELL;
+  const long comp = g.total_cells;
+  const double gamma = a.gamma, gm1 = a.gm1;
+  const double rgm1 = 1.0 / gm1;
+  if (tid == 0) {
+    s_fb = 0;
+    s_bad = 0;
+  }
+  int bad = 0, nfb = 0;
+  const int ntotal = tile_total(g, lcode, a.ntiles);
+  TileWalker walk(g, lcode < 0 ? lcode : -1, a.ntiles);
+  double wave = 0.0;
+  int wave_l = -1;
+  auto flush_wave = [&] {
+    if (wave_l < 0) return;
+    for (int o = 16; o > 0; o >>= 1) wave = fmax(wave, __shfl_xor_sync(0xffffffffu, wave, o));
+    if (lane == 0 && wave > 0.0)
+      atomicMax(a.wave + wave_l, (unsigned long long)__double_as_longlong(wave));
+    wave = 0.0;
+  };
+  const double* basesrc = a.snap ? a.eval : a.base;  // stage 1: q_old is eval itself
+
+  // tile `it` of the launch's range -> level, origin (walk: entries increase)
+  auto locate = [&](int it, int& l, int& x0, int& y0) {
+    const int t = lcode < 0 ? walk.at(g, a.tiles, it, &l) : tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
+    const int sx = ilog2i(g.ntx[l]);
+    x0 = (t & (g.ntx[l] - 1)) * TX;
+    y0 = ((t >> sx) & (g.nty[l] - 1)) * TY;
+  };
+  auto on_cross = [&](int idx, int& ix, int& iy) {
+    ix = idx % K::HX;
+    iy = idx / K::HX;
+    const bool cx = ix >= 2 && ix < TX + 2, cy = iy >= 2 && iy < TY + 2;
+    return idx < K::HP && (cx || cy);
+  };
+  // cp.async of tile (l, x0, y0) into buffer b: the box cross of eval and the
+  // owned cells' step-start values
+  auto issue = [&](int l, int x0, int y0, int b) {
+    const int n = 1 << l;
+    const long off = g.cell_off[l];
+    double* rb = raw + b * NC * K::HP;
+#pragma unroll
+    for (int t = 0; t < K::HPT; ++t) {
+      const int idx = tid + t * K::NT;
+      int ix, iy;
+      if (!on_cross(idx, ix, iy)) continue;
+      bool f;
+      const int mi = mr_map(x0 - 2 + ix, n, g.bc[0], g.bc[1], f);
+      const int mj = mr_map(y0 - 2 + iy, n, g.bc[2], g.bc[3], f);
+      const long c = off + (long)mj * n + mi;
+#pragma unroll
+      for (int m = 0; m < NC; ++m) cp_async8(rb + m * K::HP + idx, a.eval + m * comp + c);
+    }
+    if (owner) {
+      const long own = off + (long)(y0 + ty) * n + (x0 + tx);
+#pragma unroll
+      for (int m = 0; m < NC; ++m)
+        cp_async8(bsm + b * NC * K::NCELL + m * K::NCELL + tid, basesrc + m * comp + own);
+    }
+  };
+  auto P = [&](int ix, int iy) {
+    const int idx = iy * K::HX + ix;
+    Prim<D> w;
+    w.rho = pr[idx];
+    w.v[0] = pr[K::HP + idx];
+    w.v[1] = pr[2 * K::HP + idx];
+    w.p = pr[3 * K::HP + idx];
+    return w;
+  };
+
+  int l = 0, x0 = 0, y0 = 0;
+  if ((int)blockIdx.x < ntotal) {
+    locate(blockIdx.x, l, x0, y0);
+    issue(l, x0, y0, 0);
+  }
+  cp_async_commit();
+  int k = 0;
+  for (int it = blockIdx.x; it < ntotal; it += gridDim.x, ++k) {
+    const int b = k & 1;
+    const int cl = l, cx0 = x0, cy0 = y0;  // this tile
+    const int nit = it + (int)gridDim.x;
+    if (nit < ntotal) {
+      locate(nit, l, x0, y0);
+      issue(l, x0, y0, b ^ 1);
+    }
+    cp_async_commit();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();  // this tile's copies from every thread have landed
+    const int n = 1 << cl;
+    const long off = g.cell_off[cl];
+    const double inv_dx = g.inv_dx[cl];
+    if (cl != wave_l) {
+      flush_wave();
+      wave_l = cl;
+    }
+    // convert the box to primitives (resolve_at's flips and MRLT interpolation)
+    const double* rb = raw + b * NC * K::HP;
+    const bool interp = cl >= 1 && cl - 1 < a.lo;
+#pragma unroll
+    for (int t = 0; t < K::HPT; ++t) {
+      const int idx = tid + t * K::NT;
+      int ix, iy;
+      if (!on_cross(idx, ix, iy)) continue;
+      Cons<D> q;
+      q.rho = rb[idx];
+      q.m[0] = rb[K::HP + idx];
+      q.m[1] = rb[2 * K::HP + idx];
+      q.E = rb[3 * K::HP + idx];
+      bool fi, fj;
+      const int mi = mr_map(cx0 - 2 + ix, n, g.bc[0], g.bc[1], fi);
+      const int mj = mr_map(cy0 - 2 + iy, n, g.bc[2], g.bc[3], fj);
+      if (interp) {
+        const long c = off + (long)mj * n + mi;
+        const long pc = g.cell_off[cl - 1] + (long)(mj >> 1) * (n >> 1) + (mi >> 1);
+        if (a.vmark[pc] && a.st[c] == ST_ABSENT) {
+          const double th = a.theta[cl - 1], om = 1.0 - th;
+          q.rho = a.vq_old[c] * om + q.rho * th;
+          q.m[0] = a.vq_old[comp + c] * om + q.m[0] * th;
+          q.m[1] = a.vq_old[2 * comp + c] * om + q.m[1] * th;
+          q.E = a.vq_old[3 * comp + c] * om + q.E * th;
+        }
+      }
+      if (fi) q.m[0] = -q.m[0];
+      if (fj) q.m[1] = -q.m[1];
+      const Prim<D> w = primitives(q, gm1);
+      pr[idx] = w.rho;
+      pr[K::HP + idx] = w.v[0];
+      pr[2 * K::HP + idx] = w.v[1];
+      pr[3 * K::HP + idx] = w.p;
+    }
+    __syncthreads();
+    // pass-1 checks of this thread's leaf (mr_solver.cpp:171-178)
+    if (owner) {
+      const Prim<D> w = P(tx + 2, ty + 2);
+      Cons<D> q;
+      q.rho = w.rho;
+      if (!cell_ok(q, w)) bad = 1;
+      double s, m;
+      wave_speeds(w, gamma, s, m);
+      wave = fmax(wave, m);
+    }
+    auto cons_at = [&](int x, int y) { return resolve_at<D>(a.eval, comp, g, cl, x, y, 0, &a); };
+    auto face = [&](auto axc, int u) {
+      constexpr int AX = decltype(axc)::value;
+      constexpr int SEC = AX == 0 ? 0 : K::YS;
+      constexpr int CNT = AX == 0 ? K::NXF : K::NYF;
+      const int j0 = u * 32 + lane - SEC;
+      const bool real = j0 < CNT;
+      const int j = real ? j0 : 0;
+      // (fx, fy): the face's high-side cell in tile coordinates
+      const int fx = AX == 0 ? (j < TX * TY ? j % TX : TX) : j % TX;
+      const int fy = AX == 0 ? (j < TX * TY ? j / TX : j - TX * TY) : j / TX;
+      Prim<D> wm1, w0, wp1, wp2;
+      if constexpr (AX == 0) {
+        wm1 = P(fx, fy + 2);
+        w0 = P(fx + 1, fy + 2);
+        wp1 = P(fx + 2, fy + 2);
+        wp2 = P(fx + 3, fy + 2);
+      } else {
+        wm1 = P(fx + 2, fy);
+        w0 = P(fx + 2, fy + 1);
+        wp1 = P(fx + 2, fy + 2);
+        wp2 = P(fx + 2, fy + 3);
+      }
+      Prim<D> lft, rgt;
+      const bool fb = muscl_recon<D, S>(wm1, w0, wp1, wp2, lft, rgt);
+      Cons<D> F = recon_flux_fast_warp<D, AX, S>(lft, rgt, gamma, gm1, rgm1);
+      if (__any_sync(0xffffffffu, fb)) {
+        if (fb) {
+          const int gx = cx0 + fx, gy = cy0 + fy;
+          F = num_flux<D, AX, S>(cons_at(gx - (AX == 0), gy - (AX == 1)), w0, cons_at(gx, gy), wp1,
+                                 gamma);
+        }
+      }
+      if (real) {
+        const int f = SEC + j;
+        fl[f] = F.rho;
+        fl[K::NF + f] = F.m[0];
+        fl[2 * K::NF + f] = F.m[1];
+        fl[3 * K::NF + f] = F.E;
+        ffb[f] = (uint8_t)fb;
+      }
+    };
+    for (int u = warp; u < K::NU; u += K::NW) {
+      if (u * 32 < K::YS)
+        face(std::integral_constant<int, 0>{}, u);
+      else
+        face(std::integral_constant<int, 1>{}, u);
+    }
+    __syncthreads();
+    if (owner) {
+      const long own = off + (long)(cy0 + ty) * n + (cx0 + tx);
+      const int fxl = ty * TX + tx, fxh = tx + 1 < TX ? fxl + 1 : TX * TY + ty;
+      const int fyl = K::YS + ty * TX + tx, fyh = fyl + TX;
+      const double* bb = bsm + b * NC * K::NCELL;
+      double o[NC];
+#pragma unroll
+      for (int m = 0; m < NC; ++m) {
+        const double* fm = fl + m * K::NF;
+        double rhs = 0.0;
+        rhs = rhs + fm[fxl] * inv_dx;
+        rhs = rhs - fm[fxh] * inv_dx;
+        rhs = rhs + fm[fyl] * inv_dx;
+        rhs = rhs - fm[fyh] * inv_dx;
+        const double base0 = bb[m * K::NCELL + tid];
+        if (a.snap) a.snap[m * comp + own] = base0;
+        o[m] = base0 + rhs * sdt;
+        a.out[m * comp + own] = o[m];
+      }
+      nfb += ffb[fxl] + ffb[fxh] + ffb[fyl] + ffb[fyh];
+      if (a.post_check) {
+        Cons<D> q;
+        q.rho = o[0];
+        q.m[0] = o[1];
+        q.m[1] = o[2];
+        q.E = o[3];
+        if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
+      }
+    }
+    __syncthreads();  // the next iteration refills the buffer this tile read
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  flush_wave();
+  if (bad) atomicOr(&s_bad, bad);
+  if (nfb) atomicAdd(&s_fb, nfb);
+  __syncthreads();
+  if (tid == 0) {
+    if (s_bad) {
+      atomicExch(a.err + ((s_bad & 1) ? 0 : 2), 1);
+      if (a.post_stops) atomicExch(a.err, 1);
+      atomicMin(a.err + 1, step3 + ((s_bad & 1) ? a.stage - 1 : 2));
+      atomicCAS(a.err + 3, 0, ((a.lo << 8) | a.hi) + 1);
+    }
+    if (s_fb) atomicAdd(a.fb, (unsigned long long)s_fb);
+  }
+}
+
+}  // namespace af

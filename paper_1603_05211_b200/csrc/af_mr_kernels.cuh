@@ -50,17 +50,18 @@ __device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
 // Tile iteration of one launch. Single level (l >= 0): the `ntiles` entries
 // of `tiles` (ntiles -1 / -2 / -3: the band / leaf-tile / absent-band count
 // from g.dcnt).
-// Multi-level (l = -(lo+1), ntiles = hi << 1 | sel): the band (sel 0) or leaf
-// (sel 1) lists of levels lo..hi as ONE flat range, so the grid follows the
+// Multi-level (l = -(lo+1), ntiles = hi << 3 | sel): the band (sel 0), leaf
+// (sel 1), absent-band (sel 2), partial-leaf (sel 3) or full-leaf (sel 4)
+// lists of levels lo..hi as ONE flat range, so the grid follows the
 // total work instead of levels x the largest level. Each tile is visited
 // `reps` times (rep = 0..reps-1) by different blocks; f(level, tile, rep).
 // The same range without a callback: tile_total() entries, tile_at() maps
 // entry `it` to (level, tile).
 __device__ __forceinline__ int tile_total(const MRLevels& g, int l, int ntiles) {
   if (l < 0) {
-    const int* cnt = g.dcnt + 17 * (ntiles & 1);
+    const int* cnt = g.dcnt + 17 * (ntiles & 7);
     int total = 0;
-    for (int k = -l - 1; k <= (ntiles >> 1); ++k) total += cnt[k];
+    for (int k = -l - 1; k <= (ntiles >> 3); ++k) total += cnt[k];
     return total;
   }
   return ntiles < 0 ? g.dcnt[17 * (-ntiles - 1) + l] : ntiles;
@@ -68,7 +69,7 @@ __device__ __forceinline__ int tile_total(const MRLevels& g, int l, int ntiles) 
 __device__ __forceinline__ int tile_at(const MRLevels& g, int l, const int* tiles, int ntiles,
                                        int it, int* level) {
   if (l < 0) {
-    const int* cnt = g.dcnt + 17 * (ntiles & 1);
+    const int* cnt = g.dcnt + 17 * (ntiles & 7);
     int k = -l - 1, base = 0;
     while (it >= base + cnt[k]) base += cnt[k++];
     *level = k;
@@ -85,7 +86,7 @@ struct TileWalker {
   int k, base, cnt_k;
   const int* cnt;
   __device__ __forceinline__ TileWalker(const MRLevels& g, int l, int ntiles) {
-    cnt = g.dcnt + 17 * (ntiles & 1);
+    cnt = g.dcnt + 17 * (ntiles & 7);
     k = -l - 1;
     base = 0;
     cnt_k = cnt[k];

@@ -655,7 +655,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
                                   int* counts, unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
   // the list counts and leaves per level mr_tile_lists_all accumulates
-  if (blockIdx.x == 0 && threadIdx.x < 51) counts[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 85) counts[threadIdx.x] = 0;
   if (blockIdx.x == 0 && threadIdx.x < 17) leaves_per_level[threadIdx.x] = 0;
   constexpr int TX = D == 3 ? kTileX3 : kTileX2, TY = D == 3 ? kTileY3 : kTileY2;
   constexpr int TZ = D == 3 ? kTileZ3 : 1;
@@ -737,7 +737,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
 // projections, predictions, details and merges are evaluated.
 template <int D>
 __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLevels g, int* band,
-                                  int* leaf, int* pband, int* counts,
+                                  int* leaf, int* pband, int* lpart, int* lfull, int* counts,
                                   unsigned long long* leaves_per_level) {
   AF_PDL_ENTRY();
   const long total = g.tile_off[g.L + 1];
@@ -779,20 +779,30 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLeve
     const unsigned lb = __ballot_sync(grp, in_leaf) & grp;
     const bool in_pband = in_band && (tflag[tg] & 8) != 0;
     const unsigned pb = __ballot_sync(grp, in_pband) & grp;
+    // leaf tiles split into full (bit 2: mr_stage_full2d) and the rest
+    const bool in_full = in_leaf && (tflag[tg] & 4) != 0, in_part = in_leaf && !in_full;
+    const unsigned fb = __ballot_sync(grp, in_full) & grp;
+    const unsigned qb = __ballot_sync(grp, in_part) & grp;
     const unsigned nl = __reduce_add_sync(grp, (unsigned)tleaf[tg]);
-    int bbase = 0, lbase = 0, pbase = 0;
+    int bbase = 0, lbase = 0, pbase = 0, fbase = 0, qbase = 0;
     if (lane == leader) {
       if (bb) bbase = atomicAdd(counts + l, __popc(bb));
       if (lb) lbase = atomicAdd(counts + 17 + l, __popc(lb));
       if (pb) pbase = atomicAdd(counts + 34 + l, __popc(pb));
+      if (qb) qbase = atomicAdd(counts + 51 + l, __popc(qb));
+      if (fb) fbase = atomicAdd(counts + 68 + l, __popc(fb));
       if (nl) atomicAdd(leaves_per_level + l, (unsigned long long)nl);
     }
     bbase = __shfl_sync(grp, bbase, leader);
     lbase = __shfl_sync(grp, lbase, leader);
     pbase = __shfl_sync(grp, pbase, leader);
+    qbase = __shfl_sync(grp, qbase, leader);
+    fbase = __shfl_sync(grp, fbase, leader);
     if (in_band) band[g.tile_off[l] + bbase + __popc(bb & below)] = (int)t;
     if (in_leaf) leaf[g.tile_off[l] + lbase + __popc(lb & below)] = (int)t;
     if (in_pband) pband[g.tile_off[l] + pbase + __popc(pb & below)] = (int)t;
+    if (in_part) lpart[g.tile_off[l] + qbase + __popc(qb & below)] = (int)t;
+    if (in_full) lfull[g.tile_off[l] + fbase + __popc(fb & below)] = (int)t;
   }
 }
 
