@@ -898,8 +898,7 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   a.post_check = stage == 2;
   // graph capture of a global step (a failing batch is replayed on the
   // synchronous path, which commits through the guarded copy)
-  swap_ = cycle_capture_ && !opt_.local_time && !g_.dist && lo == 0 && hi >= L_ &&
-          std::getenv("AF_MR_NO_SWAP") == nullptr;
+  swap_ = !g_.dist && lo == 0 && hi >= L_ && std::getenv("AF_MR_NO_SWAP") == nullptr;
   a.post_stops = swap_ ? 1 : 0;
   a.err = d_err_;
   a.lo = lo;
@@ -1013,11 +1012,19 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     note_event_node_();
   }
   if (swap_) {
-    // The output buffer becomes the state: the projection and prediction that
-    // follow write every other cell a later stage reads (internal nodes, and
-    // the absent band cells), so no commit copy is needed. Two stages per
-    // global step swap back.
+    // Every leaf steps (levels 0..L): the output buffer becomes the state.
+    // The projection and prediction that follow write every other cell a
+    // later stage reads (internal nodes, and the absent band cells), so no
+    // commit copy is needed; two stages per step swap back. Off the cycle
+    // graph (whose failing batches are replayed from a checkpoint) a guarded
+    // kernel puts the committed leaf values back when the stage failed, as
+    // the skipped commit copy leaves them.
     std::swap(d_V_, d_Vs_);
+    if (!cycle_capture_) {
+      AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
+                   (stage == 2 ? 1 : 0) | 2);
+      v_only_at_ = launches_;
+    }
     return;
   }
   AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,

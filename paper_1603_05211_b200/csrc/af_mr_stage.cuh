@@ -819,8 +819,30 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
     __shared__ int s;
     if (threadIdx.x == 0) s = guard[0] | guard[2];
     __syncthreads();
+    // promote bit 1, restore mode (after a buffer swap): only when a failure
+    // is pending, exchange the leaf values of src and dst, putting the last
+    // committed values back into dst and the failed stage's output into src
+    // (where the commit-copy path leaves it for the error report)
+    const bool restore = (promote & 2) != 0;
     if (s) {
-      if (promote && blockIdx.x == 0 && threadIdx.x == 0) atomicExch((int*)guard, 1);
+      if ((promote & 1) && blockIdx.x == 0 && threadIdx.x == 0) atomicExch((int*)guard, 1);
+      if (!restore) return;
+    } else if (restore) {
+      return;
+    }
+    if (restore) {
+      double* s2 = const_cast<double*>(src);
+      const long comp = g.total_cells;
+      level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
+        const long off = g.cell_off[lv];
+        if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(D, lv, c))) return;
+#pragma unroll
+        for (int m = 0; m < D + 2; ++m) {
+          const double t = dst[m * comp + off + c];
+          dst[m * comp + off + c] = s2[m * comp + off + c];
+          s2[m * comp + off + c] = t;
+        }
+      });
       return;
     }
   }
