@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kGrid = 148 * 8;
 constexpr int kStageGrid = 148 * 2;  // stage kernel: 2 resident blocks per SM
+constexpr long kFullMin = 148 * 2 * 4;  // full tiles that justify mr_stage_full2d
 
 inline unsigned grid_for(long n, int block = 256) {
   long b = (n + block - 1) / block;
@@ -952,7 +953,13 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   // Full 2D tiles (every cell and face neighbour a leaf of the level) run on
   // mr_stage_full2d, the other leaf tiles on mr_stage_kernel (AF_MR_NO_FULLK:
   // every leaf tile on mr_stage_kernel, with its own full-tile fast path).
-  const bool fullk = D_ == 2 && !g_.dist && a.tflag && !std::getenv("AF_MR_NO_FULLK");
+  // A few full tiles are not worth a second launch (cfg2's sparse levels):
+  // the split is used when the last list build found at least kFullMin of
+  // them among the stepping levels (host counts; also at graph capture).
+  long nfull_host = 0;
+  for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l) nfull_host += full_count_[l];
+  const bool fullk = D_ == 2 && !g_.dist && a.tflag && !std::getenv("AF_MR_NO_FULLK") &&
+                     (nfull_host >= kFullMin || std::getenv("AF_MR_FULLK"));
   long nfull = 0, npart = 0;
   for (int l = std::max(lo, 0); l <= std::min(hi, L_); ++l) {
     const long tot = fixed_grids_ ? level_tiles_(l) : tile_count_[l];

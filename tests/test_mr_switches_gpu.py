@@ -14,6 +14,8 @@ stepping). The switches are read when a solver is created.
   AF_MR_NO_FULL         the general stage path for full tiles too (no fast path)
   AF_MR_NO_FULLK        full 2D tiles on mr_stage_kernel's fast path instead of
                         the pipelined mr_stage_full2d kernel
+  AF_MR_FULLK           mr_stage_full2d for any number of full tiles (by default
+                        only when a stage has enough of them to fill the GPU)
 """
 import os
 
@@ -26,7 +28,7 @@ pytestmark = pytest.mark.gpu
 
 SWITCHES = ["AF_MR_NO_CYCLE_GRAPH", "AF_MR_NO_GRAPH", "AF_MR_NO_PDL", "AF_MR_NO_PRE",
             "AF_MR_NO_SWAP", "AF_MR_NO_TINY", "AF_MR_FULL_SWEEPS", "AF_MR_NO_FULL",
-            "AF_MR_NO_FULLK"]
+            "AF_MR_NO_FULLK", "AF_MR_FULLK"]
 
 
 def run(switch, kind, level, steps, bc=None, **kw):
