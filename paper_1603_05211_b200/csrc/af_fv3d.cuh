@@ -188,12 +188,12 @@ __global__ void __launch_bounds__(NW * 32, 2)
     }
   };
   unsigned bphase = 0;  // bit j: parity of buffer j's next completion
-  auto convert = [&](int gz) {
+  auto convert = [&](int gz, int dslot) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
     bool fz;
     const int zl = slab_map(gz, g, 2, fz);
-    double* dst = ring + ((gz + 6) % K::RING) * K::SLOT;
+    double* dst = ring + dslot;
     const bool own_plane = gz >= zc0 && gz < zc1;
 #pragma unroll
     for (int t = 0; t < K::HPT; ++t) {
@@ -273,23 +273,45 @@ __global__ void __launch_bounds__(NW * 32, 2)
   };
   auto slot = [&](int gz) { return ((gz + 6) % K::RING) * K::SLOT; };
 
-  // x/y faces of plane k from unit u (a unit lies in one axis section, so the
-  // axis is warp-uniform and a compile-time constant in the face body; every
-  // lane runs the body (padding lanes repeat a real face and store nothing),
-  // so the rare fallback and fast-path misses take a warp-uniform branch.
-  auto face_body = [&](auto axc, int k, int u) {
+  // x/y faces: each warp owns one x unit (warp) and one y unit (NW + warp)
+  // of the flat list (a unit lies in one axis section, so the axis is
+  // warp-uniform and a compile-time constant in the face body). Every lane
+  // runs the body (padding lanes repeat a real face and store nothing), so
+  // the rare fallback and fast-path misses take a warp-uniform branch. The
+  // per-lane face geometry is fixed for the whole chunk and computed once.
+  static_assert(K::NU == 2 * NW, "two x/y face units per warp");
+  struct FaceLane {
+    int j, fx, fy, o;  // list entry (section-relative), position, ring offset in a slot
+    bool real, skip;   // a listed face; the unit lies beyond the mesh (partial tile row)
+  };
+  const int rows = min(TY, n - y0);  // tile rows inside the mesh
+  auto face_lane = [&](auto axc) {
     constexpr int AX = decltype(axc)::value;
     constexpr int SEC = AX == 0 ? 0 : K::YS;
     constexpr int CNT = AX == 0 ? K::NXF : K::NYF;
+    const int u = AX == 0 ? warp : NW + warp;
+    FaceLane f;
     const int j0 = u * 32 + lane - SEC;
-    const bool real = j0 < CNT;
-    const int j = real ? j0 : 0;
+    f.real = j0 < CNT;
+    f.j = f.real ? j0 : 0;
     // face position (fx, fy): the face's high-side cell in tile coordinates
     // (x faces: fx in [0, TX], y faces: fy in [0, TY])
-    const int fx = AX == 0 ? (j < TX * TY ? j % TX : TX) : j % TX;
-    const int fy = AX == 0 ? (j < TX * TY ? j / TX : j - TX * TY) : j / TX;
+    f.fx = AX == 0 ? (f.j < TX * TY ? f.j % TX : TX) : f.j % TX;
+    f.fy = AX == 0 ? (f.j < TX * TY ? f.j / TX : f.j - TX * TY) : f.j / TX;
+    f.o = AX == 0 ? (f.fy + 2) * K::HX + f.fx : f.fy * K::HX + f.fx + 2;
+    const int f0 = u * 32;
+    f.skip = rows < TY && (AX == 0 ? (f0 + 32 <= TX * TY && f0 / TX >= rows)
+                                   : (f0 - K::YS) / TX > rows);
+    return f;
+  };
+  const FaceLane flx = face_lane(std::integral_constant<int, 0>{});
+  const FaceLane fly = face_lane(std::integral_constant<int, 1>{});
+  auto face_body = [&](auto axc, const FaceLane& fl, int k, int sk) {
+    constexpr int AX = decltype(axc)::value;
+    constexpr int SEC = AX == 0 ? 0 : K::YS;
     constexpr int st = AX == 0 ? 1 : K::HX;
-    const int o = AX == 0 ? slot(k) + (fy + 2) * K::HX + fx : slot(k) + fy * K::HX + fx + 2;
+    const int fx = fl.fx, fy = fl.fy;
+    const int o = sk + fl.o;
     Prim<D> l, r;
     bool fb;
     if constexpr (MODE == 0)
@@ -316,7 +338,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
           cnt = (fx < TX || x0 + TX == n) && y0 + fy < n;
         else
           cnt = (fy < TY && y0 + fy < n) || y0 + fy == n;
-        if (cnt && real) ++nfb;
+        if (cnt && fl.real) ++nfb;
         const Cons<D> q0 = cons_at(gx, gy, k);
         const Cons<D> q1 = cons_at(gx + (AX == 0), gy + (AX == 1), k);
         Prim<D> w0, w1;
@@ -331,8 +353,8 @@ __global__ void __launch_bounds__(NW * 32, 2)
         F = num_flux<D, AX, S>(q0, w0, q1, w1, gamma);
       }
     }
-    if (real) {
-      const int f = SEC + j;
+    if (fl.real) {
+      const int f = SEC + fl.j;
       flux[f] = F.rho;
       flux[K::NF + f] = F.m[0];
       flux[2 * K::NF + f] = F.m[1];
@@ -340,20 +362,9 @@ __global__ void __launch_bounds__(NW * 32, 2)
       flux[4 * K::NF + f] = F.E;
     }
   };
-  const int rows = min(TY, n - y0);  // tile rows inside the mesh
-  auto faces = [&](int k) {
-    for (int u = warp; u < K::NU; u += NW) {
-      // the last tile row of the mesh is partial: units whose faces all lie
-      // beyond the mesh are skipped (warp-uniform)
-      const int f0 = u * 32;
-      if (rows < TY && (f0 < K::YS ? (f0 + 32 <= TX * TY && f0 / TX >= rows)
-                                   : (f0 - K::YS) / TX > rows))
-        continue;
-      if (u * 32 < K::YS)
-        face_body(std::integral_constant<int, 0>{}, k, u);
-      else
-        face_body(std::integral_constant<int, 1>{}, k, u);
-    }
+  auto faces = [&](int k, int sk) {
+    if (!flx.skip) face_body(std::integral_constant<int, 0>{}, flx, k, sk);
+    if (!fly.skip) face_body(std::integral_constant<int, 1>{}, fly, k, sk);
   };
 
   // z faces: the thread of column (tx, ty) computes the face k+1/2 above its
@@ -362,12 +373,12 @@ __global__ void __launch_bounds__(NW * 32, 2)
   // (zl) and the difference w(k+1) - w(k) (zd) from plane to plane.
   const int oc = (ty + 2) * K::HX + tx + 2;  // the column's cell in a ring plane
   double zl[5], zd[5];
-  auto zface = [&](int k, bool first) {
+  auto zface = [&](int k, bool first, int s1, int s2) {
     double rr[5], nl[5];
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
-      const double w1 = ring[slot(k + 1) + m * K::HP + oc];
-      const double w2 = ring[slot(k + 2) + m * K::HP + oc];
+      const double w1 = ring[s1 + m * K::HP + oc];
+      const double w2 = ring[s2 + m * K::HP + oc];
       const double d2 = w2 - w1;
       cell_face_states<S, MODE>(w1, zd[m], d2, rr[m], nl[m]);
       zd[m] = d2;
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
   // plane's lower face.
   for (int z = zc0 - 2; z < zc0 + 1; ++z) {
     issue(z);
-    convert(z);
+    convert(z, slot(z));
     __syncthreads();
   }
   issue(zc0 + 1);
@@ -437,16 +448,25 @@ __global__ void __launch_bounds__(NW * 32, 2)
   double zlo[5];
   const double fdt = inv_dx * sdt;  // tolerance mode: rhs*inv_dx*dt folded
 
-  for (int k = zc0 - 1; k < zc1; ++k) {
+  // ring slots of planes k, k+1, k+2 (rotated each plane) and the owned
+  // cell's offset in the slab arrays
+  int sk = slot(zc0 - 1), sk1 = slot(zc0), sk2 = slot(zc0 + 1);
+  long own = (long)(zc0 - 1 - g.zlo + 2) * zs + (long)(y0 + ty) * n + (x0 + tx);
+  for (int k = zc0 - 1; k < zc1; ++k, own += zs) {
     const bool first = k < zc0;
-    const long own = (long)(k - g.zlo + 2) * zs + (long)(y0 + ty) * n + (x0 + tx);
-    convert(k + 2);
+    convert(k + 2, sk2);
     __syncthreads();  // ring slot k+2 complete, staging free, flux free
     if (k + 3 < zc1 + 2) issue(k + 3);
     // its buffer was last read by the update of plane k-1 (before the barrier)
     if (k + 1 < zc1) issue_base(k + 1);
-    if (!first) faces(k);
-    const Cons<D> Fz = zface(k, first);
+    if (!first) faces(k, sk);
+    const Cons<D> Fz = zface(k, first, sk1, sk2);
+    {
+      const int t = sk;
+      sk = sk1;
+      sk1 = sk2;
+      sk2 = t;
+    }
     const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
     if (first) {
 #pragma unroll
