@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _abi
 from .errors import raise_status
-from .uniform import MINMOD, OUTFLOW, SchemeConfig, StepDiag, _ptr
+from .uniform import MINMOD, OUTFLOW, SchemeConfig, StepDiag, _state_ptr
 
 
 @dataclass
@@ -139,7 +139,8 @@ class MRSolver:
 
     # MRTree
     def build(self, aos) -> None:
-        self._check(self._lib.af_mr_build(self._h, C.c_void_p(_ptr(aos))))
+        cells = 1 << (self.dim * self.level)
+        self._check(self._lib.af_mr_build(self._h, C.c_void_p(_state_ptr(aos, cells))))
 
     def refine(self, top: int = -1, eps: float | None = None, buffer=None):
         """MRTree::refine. With ``eps`` given: refine(eps, buffer_radius_per_level)

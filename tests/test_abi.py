@@ -66,3 +66,19 @@ def test_no_cpu_fallback_without_gpu():
     from paper_1603_05211_b200.errors import DeviceError
     with pytest.raises(DeviceError):
         U.UniformSolver(2, 6)
+
+
+def test_state_buffers_are_validated_before_the_abi():
+    """Host states reach the C ABI as raw pointers to cells x 5 doubles, so the
+    Python mirror rejects any other shape, dtype or layout first."""
+    import numpy as np
+    import pytest as _pt
+    from paper_1603_05211_b200.uniform import _state_ptr
+    cells = 64
+    ok = np.zeros((cells, 5))
+    assert _state_ptr(ok, cells) == ok.ctypes.data
+    assert _state_ptr(np.zeros(cells * 5), cells)
+    for bad in (np.zeros((cells, 4)), np.zeros((cells - 1, 5)), np.zeros((cells, 5), np.float32),
+                np.zeros((5, cells)).T, np.zeros(cells * 5 - 1)):
+        with _pt.raises((ValueError, TypeError)):
+            _state_ptr(bad, cells)
