@@ -899,7 +899,14 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
   a.post_check = stage == 2;
   // graph capture of a global step (a failing batch is replayed on the
   // synchronous path, which commits through the guarded copy)
-  swap_ = !g_.dist && lo == 0 && hi >= L_ && std::getenv("AF_MR_NO_SWAP") == nullptr;
+  // MRLT substeps of the finest level alone (lo = hi = L) swap as well: the
+  // stage writes every leaf of L, the level has no internal cells, and its
+  // absent cells (virtual leaves, predictions) are copied over after the
+  // swap (mr_copy_absent_tiles over the band tiles holding one)
+  const bool swap_fine = !g_.dist && lo == L_ && hi >= L_ && pband_ok_ && !cycle_capture_ &&
+                         std::getenv("AF_MR_NO_SWAP") == nullptr;
+  swap_ = (!g_.dist && lo == 0 && hi >= L_ && std::getenv("AF_MR_NO_SWAP") == nullptr) ||
+          swap_fine;
   a.post_stops = swap_ ? 1 : 0;
   a.err = d_err_;
   a.lo = lo;
@@ -1030,6 +1037,11 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     if (!cycle_capture_) {
       AF_ML_LAUNCH(mr_copy_leaves_tiles, lo, hi, true, d_Vs_, d_V_, d_st_, g_, AF_L, d_err_,
                    (stage == 2 ? 1 : 0) | 2);
+      v_only_at_ = launches_;
+    }
+    if (swap_fine && AF_HAS(pband_count_[L_])) {
+      AF_MR_LAUNCH(mr_copy_absent_tiles, AF_TGRID(L_, pband_count_[L_]), d_Vs_, d_V_, d_st_, g_,
+                   L_, AF_PBAND(L_));
       v_only_at_ = launches_;
     }
     return;

@@ -855,6 +855,23 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
   });
 }
 
+// Copies the values of the ABSENT cells of the listed tiles of level l from
+// src to dst: after a buffer swap on the finest level's substeps (MRLT), the
+// virtual and predicted cells the next stage's stencils read come back from
+// the buffer that holds them.
+template <int D>
+__global__ void mr_copy_absent_tiles(const double* src, double* dst, const uint8_t* st,
+                                     MRLevels g, int l, const int* tiles, int ntiles) {
+  AF_PDL_ENTRY();
+  const long comp = g.total_cells;
+  level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
+    const long off = g.cell_off[lv];
+    if (st[off + c] != ST_ABSENT) return;
+#pragma unroll
+    for (int m = 0; m < D + 2; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
+  });
+}
+
 // Tiles of level l holding at least one leaf (order irrelevant: every tile
 // writes only its own leaves).
 template <int D, int TX, int TY, int TZ>
