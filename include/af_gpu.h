@@ -49,7 +49,8 @@ typedef enum af_status {
   AF_E_ARGUMENT = 7,          /* invalid argument / null pointer */
   AF_E_UNSUPPORTED = 8,       /* option outside the hot path (e.g. AUSMDV) */
   AF_E_INTERNAL = 9,          /* internal invariant check failed (debug switches) */
-  AF_E_IO = 10                /* adaptflow::IoError (errors.hpp:38-41) */
+  AF_E_IO = 10,               /* adaptflow::IoError (errors.hpp:38-41) */
+  AF_E_DOMAIN = 11            /* adaptflow::DivisionDomain (errors.hpp:49-52) */
 } af_status;
 
 enum { AF_BC_OUTFLOW = 0, AF_BC_PERIODIC = 1, AF_BC_REFLECTIVE = 2 }; /* BcKind grid.hpp:70 */
@@ -152,6 +153,22 @@ af_status af_uniform_download(af_uniform* u, double* aos);
 /* step_block (step.hpp:77-79) for RK2: one step of size dt. diag may be
  * NULL (then the call is asynchronous). */
 af_status af_uniform_step(af_uniform* u, double dt, af_step_diag* diag);
+
+/* rk2_stage (step.hpp:62-64, step.cpp:93-109): out = base + stage_dt * rhs(eval)
+ * for AoS states of this solver's mesh (cells x 5 doubles, host or device
+ * pointers; eval's ghosts are the configured boundary conditions, as after
+ * fill_ghosts, grid.cpp:9-62). out may alias base or eval. capture
+ * (nullable, host or device): the stage's numerical fluxes in the layout of
+ * FluxField (step.hpp:16-50) — per axis a, (n_a+1) x n_b x n_c FluxVectors
+ * of 5 doubles (rho, mom[3], rhoE; the 2D mom[2] is +0), face i along a
+ * between cells i-1 and i, x fastest, the axes concatenated — the seam the
+ * AMR refluxing captures through (amr_hierarchy.cpp:476,488). Replaces the
+ * solver's state. Single-rank solvers; capture needs exact numerics
+ * (AF_E_UNSUPPORTED otherwise). A non-physical eval raises AF_E_NONPHYSICAL
+ * with the reference's text ("cell (i,j[,k])[ (ghost)]: rho=... p=..."). */
+af_status af_uniform_rk2_stage(af_uniform* u, const double* base, const double* eval,
+                               double* out, double stage_dt, double* capture,
+                               af_step_diag* diag);
 
 /* n_steps steps entirely on the device. cfl > 0: dt_s = cfl*dx / max over
  * cells of sum_a(|v_a|+c) of the state at the start of step s (computed on
@@ -291,6 +308,24 @@ af_status af_l1_error(int dim, int level, double extent, const double* sol, int 
 /* MRTree::dump (mr_tree.cpp:623-641) of the device tree (this rank's nodes):
  * *len in = capacity of buf, out = bytes needed including the terminating 0. */
 af_status af_mr_dump(af_mr* m, char* buf, size_t* len);
+
+/* Paper §3 rates (metrics.cpp:91-132): rates(adaptive, fv, n_c) from the
+ * RunReport fields they read (sum_cells / sum_leaves = the accumulated
+ * cells_per_step / leaves_per_step, l1_rho = l1.rho). Host arithmetic in the
+ * reference's operation order; its DivisionDomain texts as AF_E_DOMAIN
+ * (errors via af_uniform_last_error(NULL, ...)). */
+typedef struct af_run_summary {
+  double wall_seconds;
+  double sum_cells;
+  double sum_leaves;
+  long n_steps;
+  double l1_rho;
+} af_run_summary;
+typedef struct af_rates {
+  double cpu_compression, memory_compression, mesh_compression, perturbation, overhead;
+} af_rates;
+af_status af_rates_compute(const af_run_summary* adaptive, const af_run_summary* fv, double n_c,
+                           af_rates* out);
 
 /* Self-check of the inline fast-path division and square root the face
  * fluxes use (CUDA's fast-path sequences with their range tests; see

@@ -63,6 +63,10 @@ int afref_uniform_run(const af_oracle_params* p, const double* init, double* out
                       double* dt_hist, af_oracle_result* res);
 int afo_uniform_run(const af_oracle_params* p, const double* init, double* out,
                     double* dt_hist, af_oracle_result* res);
+/* The reference's rk2_stage (step.hpp:62-64) with FluxField capture (cap
+ * nullable; per axis (n_a+1) x n_b x n_c faces of 5 doubles, x fastest). */
+int afref_rk2_stage(const af_oracle_params* p, const double* base, const double* eval,
+                    double stage_dt, double* out, double* cap, af_oracle_result* res);
 
 /*
  * The uniform 3D run on the window z in [z0, z0+nz) of the n^3 mesh, split

@@ -89,6 +89,8 @@ def _load(kind: str):
                                     dp, dp, C.POINTER(Result)]),
             ("mr_refine_once", [C.POINTER(Params), dp, C.c_double, C.POINTER(C.c_int), C.c_int,
                                 dp, C.POINTER(C.c_uint64), C.POINTER(C.c_long)]),
+            ("rk2_stage", [C.POINTER(Params), dp, dp, C.c_double, dp, dp, C.POINTER(Result)]),
+            ("rates", [dp, C.c_long, dp, C.c_long, C.c_double, dp, C.c_char_p, C.c_int]),
         ]:
             f = getattr(lib, "afref_" + name)
             f.argtypes = args
@@ -147,6 +149,30 @@ def uniform_run(kind: str, params: Params, init: np.ndarray):
     fn = lib.afref_uniform_run if kind == "ref" else lib.afo_uniform_run
     fn(C.byref(params), _dp(np.ascontiguousarray(init)), _dp(out), _dp(dts), C.byref(res))
     return out, dts[: params.n_steps], res.as_dict()
+
+
+def rk2_stage(params: Params, base: np.ndarray, eval_: np.ndarray, stage_dt: float,
+              capture: bool = False):
+    """The reference's rk2_stage (step.hpp:62-64) on the level-`params.level`
+    mesh (ref_harness.cpp). Returns (out, result, flux) with flux the
+    FluxField capture as per-axis arrays of shape (n_c, n_b, n_a+1, 5)."""
+    lib = _load("ref")
+    out = np.zeros_like(base)
+    n, dim = 1 << params.level, params.dim
+    per = (n + 1) * n ** (dim - 1)
+    cap = np.zeros(dim * per * 5) if capture else None
+    res = Result()
+    lib.afref_rk2_stage(C.byref(params), _dp(np.ascontiguousarray(base)),
+                        _dp(np.ascontiguousarray(eval_)), stage_dt, _dp(out),
+                        _dp(cap) if cap is not None else None, C.byref(res))
+    flux = None
+    if cap is not None:
+        flux = []
+        for a in range(dim):
+            shape = [n] * dim
+            shape[a] += 1
+            flux.append(cap[a * per * 5:(a + 1) * per * 5].reshape(*shape[::-1], 5))
+    return out, res.as_dict(), flux
 
 
 def window_init(kind: int, seed: int, level: int, z0: int, nz: int) -> np.ndarray:
@@ -234,3 +260,20 @@ def ref_l1_error(sol, dim, level, ref, ref_level, extent=1.0) -> np.ndarray:
                           _dp(np.ascontiguousarray(ref)), _dp(out)):
         raise ValueError("l1_error failed")
     return out
+
+
+def rates(adaptive: dict, fv: dict, n_c: float):
+    """The reference's rates() (metrics.cpp:91-132). Returns (dict, None) or
+    (None, the DivisionDomain text)."""
+    lib = _load("ref")
+
+    def vec(d):
+        return np.array([d["wall_seconds"], d["sum_cells"], d["sum_leaves"], d["l1_rho"]])
+    out = np.zeros(5)
+    err = C.create_string_buffer(512)
+    a, f = vec(adaptive), vec(fv)
+    if lib.afref_rates(_dp(a), int(adaptive["n_steps"]), _dp(f), int(fv["n_steps"]), n_c, _dp(out),
+                       err, 512):
+        return None, err.value.decode()
+    keys = ["cpu_compression", "memory_compression", "mesh_compression", "perturbation", "overhead"]
+    return dict(zip(keys, out.tolist())), None

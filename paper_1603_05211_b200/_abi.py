@@ -33,6 +33,17 @@ class Config(C.Structure):
     ]
 
 
+class RunSummary(C.Structure):
+    _fields_ = [("wall_seconds", C.c_double), ("sum_cells", C.c_double),
+                ("sum_leaves", C.c_double), ("n_steps", C.c_long), ("l1_rho", C.c_double)]
+
+
+class Rates(C.Structure):
+    _fields_ = [("cpu_compression", C.c_double), ("memory_compression", C.c_double),
+                ("mesh_compression", C.c_double), ("perturbation", C.c_double),
+                ("overhead", C.c_double)]
+
+
 class StepDiag(C.Structure):
     _fields_ = [("max_wave_speed", C.c_double), ("fallbacks", C.c_long)]
 
@@ -82,6 +93,9 @@ SIGNATURES = {
     "af_uniform_upload": (C.c_int, [_vp, _vp]),
     "af_uniform_download": (C.c_int, [_vp, _vp]),
     "af_uniform_step": (C.c_int, [_vp, C.c_double, C.POINTER(StepDiag)]),
+    "af_rates_compute": (C.c_int, [C.POINTER(RunSummary), C.POINTER(RunSummary), C.c_double,
+                                   C.POINTER(Rates)]),
+    "af_uniform_rk2_stage": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp, C.POINTER(StepDiag)]),
     "af_uniform_run": (C.c_int, [_vp, C.c_long, C.c_double, C.c_double, _dp,
                                  C.POINTER(RunDiag)]),
     "af_uniform_speed_sum": (C.c_int, [_vp, _dp]),

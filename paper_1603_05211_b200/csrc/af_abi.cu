@@ -4,6 +4,7 @@
 // without one) for af_*_last_error.
 #include <nccl.h>
 
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -211,6 +212,12 @@ af_status af_uniform_step(af_uniform* u, double dt, af_step_diag* diag) {
   AF_U_GUARD(u->impl->step(dt, diag));
 }
 
+af_status af_uniform_rk2_stage(af_uniform* u, const double* base, const double* eval,
+                               double* out, double stage_dt, double* capture,
+                               af_step_diag* diag) {
+  AF_U_GUARD(u->impl->rk2_stage(base, eval, out, stage_dt, capture, diag));
+}
+
 af_status af_uniform_run(af_uniform* u, long n_steps, double cfl, double fixed_dt,
                          double* dt_hist, af_run_diag* diag) {
   AF_U_GUARD(u->impl->run(n_steps, cfl, fixed_dt, dt_hist, diag));
@@ -409,5 +416,32 @@ af_status af_mr_dump(af_mr* m, char* buf, size_t* len) {
     const size_t need = s.size() + 1;
     if (buf && *len >= need) std::memcpy(buf, s.c_str(), need);
     *len = need;
+  });
+}
+
+// rates (metrics.cpp:91-132): the reference's formulas and their order, its
+// DivisionDomain texts.
+extern "C" af_status af_rates_compute(const af_run_summary* ad, const af_run_summary* fv,
+                                      double n_c, af_rates* out) {
+  return guard(nullptr, [&] {
+    if (!ad || !fv || !out) throw af::Error(AF_E_ARGUMENT, "null argument");
+    auto domain = [](const char* what) { throw af::Error(AF_E_DOMAIN, what); };
+    if (fv->n_steps == 0 || n_c == 0.0) domain("rates: zero baseline size");
+    af_rates r{};
+    if (fv->wall_seconds == 0.0) domain("cpu_compression: zero baseline time");
+    r.cpu_compression = ad->wall_seconds / fv->wall_seconds;
+    if (ad->n_steps == 0 || n_c == 0.0) domain("memory_compression: zero step or cell count");
+    r.memory_compression = ad->sum_cells / static_cast<double>(ad->n_steps) / n_c;
+    if (ad->n_steps == 0 || n_c == 0.0) domain("mesh_compression: zero step or cell count");
+    r.mesh_compression = ad->sum_leaves / static_cast<double>(ad->n_steps) / n_c;
+    if (fv->l1_rho == 0.0) domain("accuracy_perturbation: zero baseline error");
+    r.perturbation = std::abs(fv->l1_rho - ad->l1_rho) / fv->l1_rho;
+    const double fv_cell_steps = static_cast<double>(fv->n_steps) * n_c;
+    if (ad->sum_leaves == 0.0 || fv->wall_seconds == 0.0 || fv_cell_steps == 0.0)
+      domain("overhead: zero denominator");
+    const double gamma_a = ad->wall_seconds / ad->sum_leaves;
+    const double gamma_fv = fv->wall_seconds / fv_cell_steps;
+    r.overhead = gamma_a / gamma_fv - 1.0;
+    *out = r;
   });
 }

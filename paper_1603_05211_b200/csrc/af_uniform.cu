@@ -283,6 +283,7 @@ Uniform::~Uniform() {
   cudaFree(d_mid_);
   cudaFree(d_err_);
   cudaFree(d_stage_);
+  cudaFree(d_cap_);
   free_records_();
   if (comm_stream_) {
     cudaStreamSynchronize(comm_stream_);
@@ -335,6 +336,11 @@ void Uniform::ensure_staging_() {
 }
 
 void Uniform::upload(const double* aos) {
+  upload_to_(aos, d_u_);
+  reset_error_();
+}
+
+void Uniform::upload_to_(const double* aos, double* dst) {
   if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
   const size_t bytes = sizeof(double) * 5 * g_.plane * g_.nzl;
   const double* src = aos;
@@ -343,24 +349,25 @@ void Uniform::upload(const double* aos) {
     AF_CUDA(cudaMemcpyAsync(d_stage_, aos, bytes, cudaMemcpyHostToDevice, stream_));
     src = d_stage_;
   }
-  aos_to_soa<<<4 * 148, 256, 0, stream_>>>(src, d_u_, g_);
+  aos_to_soa<<<4 * 148, 256, 0, stream_>>>(src, dst, g_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
-  reset_error_();
 }
 
-void Uniform::download(double* aos) {
+void Uniform::download(double* aos) { download_from_(d_u_, aos); }
+
+void Uniform::download_from_(const double* q, double* aos) {
   if (!aos) throw Error(AF_E_ARGUMENT, "null state pointer");
   const size_t bytes = sizeof(double) * 5 * g_.plane * g_.nzl;
   if (is_device_ptr(aos)) {
-    soa_to_aos<<<4 * 148, 256, 0, stream_>>>(d_u_, aos, g_);
+    soa_to_aos<<<4 * 148, 256, 0, stream_>>>(q, aos, g_);
     ++launches_;
     AF_CUDA(cudaGetLastError());
     AF_CUDA(cudaStreamSynchronize(stream_));
     return;
   }
   ensure_staging_();
-  soa_to_aos<<<4 * 148, 256, 0, stream_>>>(d_u_, d_stage_, g_);
+  soa_to_aos<<<4 * 148, 256, 0, stream_>>>(q, d_stage_, g_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
   AF_CUDA(cudaMemcpyAsync(aos, d_stage_, bytes, cudaMemcpyDeviceToHost, stream_));
@@ -743,6 +750,7 @@ void Uniform::check_error_() {
   const int stage = h[1] % 2 + 1;
   const double* eval = stage == 1 ? d_u_ : d_mid_;
   if (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK) eval = step % 2 ? hk_m0_ : hk_u0_;
+  if (err_eval_) eval = err_eval_;
   std::vector<double> hs(g_.total);
   AF_CUDA(cudaMemcpy(hs.data(), eval, sizeof(double) * g_.total, cudaMemcpyDeviceToHost));
   std::memset(&last_, 0, sizeof(last_));
@@ -799,7 +807,7 @@ void Uniform::check_error_() {
           std::string cs = "(" + std::to_string(i) + "," + std::to_string(j);
           if (dim == 3) cs += "," + std::to_string(k);
           cs += ")";
-          const std::string msg = "step " + std::to_string(step) + ": cell " + cs +
+          const std::string msg = (seam_msg_ ? std::string() : "step " + std::to_string(step) + ": ") + "cell " + cs +
                                   (ghost ? " (ghost)" : "") + ": rho=" + fmt_f(rho) +
                                   " p=" + fmt_f(p);
           std::snprintf(last_.message, sizeof last_.message, "%s", msg.c_str());
@@ -846,6 +854,97 @@ void Uniform::collect_(long n_steps, double* dt_hist, af_run_diag* rd, af_step_d
     sd->max_wave_speed = max_ws;
     sd->fallbacks = fbs;
   }
+}
+
+void Uniform::launch_flux_capture_(const double* q, double* dst) {
+  const int sch = cfg_.limiter | (cfg_.flux << 1);
+  const unsigned grid = 148 * 8;
+#define AF_CAP(D)                                                                         \
+  switch (sch) {                                                                          \
+    case 0: flux_capture_kernel<D, 0><<<grid, 256, 0, stream_>>>(q, g_, dst, cfg_.gamma); break; \
+    case 1: flux_capture_kernel<D, 1><<<grid, 256, 0, stream_>>>(q, g_, dst, cfg_.gamma); break; \
+    case 2: flux_capture_kernel<D, 2><<<grid, 256, 0, stream_>>>(q, g_, dst, cfg_.gamma); break; \
+    default: flux_capture_kernel<D, 3><<<grid, 256, 0, stream_>>>(q, g_, dst, cfg_.gamma); break; \
+  }
+  if (g_.dim == 3) {
+    AF_CAP(3)
+  } else {
+    AF_CAP(2)
+  }
+#undef AF_CAP
+  ++launches_;
+  AF_CUDA(cudaGetLastError());
+}
+
+// rk2_stage (step.hpp:62-64, step.cpp:93-109): out = base + stage_dt * rhs(eval)
+// with eval's ghosts the configured boundary conditions (fill_ghosts,
+// grid.cpp:9-62). base goes to d_u_, eval to d_mid_, the stage writes d_u_.
+// capture: the stage's face fluxes in FluxField layout (step.hpp:16-50),
+// recomputed by flux_capture (the same operations as the stage kernels, so the
+// same bits). The reference's NonPhysicalState text has no step prefix here.
+void Uniform::rk2_stage(const double* base, const double* eval, double* out, double stage_dt,
+                        double* capture, af_step_diag* diag) {
+  if (comm_ && comm_->n > 1)
+    throw Error(AF_E_UNSUPPORTED, "rk2_stage: single-rank solvers only");
+  if (!base || !eval || !out) throw Error(AF_E_ARGUMENT, "null state pointer");
+  if (capture && numerics_ == AF_NUMERICS_TOLERANCE && g_.dim == 3)
+    throw Error(AF_E_UNSUPPORTED, "rk2_stage: flux capture needs exact numerics");
+  upload_to_(base, d_u_);
+  upload_to_(eval, d_mid_);
+  reset_error_();
+  ensure_records_(1);
+  AF_CUDA(cudaMemsetAsync(rec_.smax, 0, sizeof(unsigned long long) * 2, stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.wave_u, 0, sizeof(unsigned long long), stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.wave_mid, 0, sizeof(unsigned long long), stream_));
+  AF_CUDA(cudaMemsetAsync(rec_.fb, 0, sizeof(unsigned long long), stream_));
+  StageArgs a{};
+  a.dx = dx_;
+  a.inv_dx = inv_dx_;
+  a.gamma = cfg_.gamma;
+  a.gm1 = cfg_.gamma - 1.0;
+  a.fixed_dt = stage_dt;
+  a.use_cfl = 0;
+  a.r = rec_;
+  a.r.err = d_err_;
+  a.step = 0;
+  a.stage = 1;
+  a.dt_scale = 1.0;
+  a.eval = d_mid_;
+  a.base = d_u_;
+  a.out = d_u_;
+  launch_stage_(a);
+  if (capture) {
+    const int n = g_.n, dim = g_.dim;
+    const long per = dim == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
+    const long faces = dim * per;
+    double* dst = capture;
+    if (!is_device_ptr(capture)) {
+      if (cap_cap_ < faces) {
+        cudaFree(d_cap_);
+        AF_CUDA(cudaMalloc(&d_cap_, sizeof(double) * 5 * faces));
+        cap_cap_ = faces;
+      }
+      dst = d_cap_;
+    }
+    launch_flux_capture_(d_mid_, dst);
+    if (dst != capture)
+      AF_CUDA(cudaMemcpyAsync(capture, dst, sizeof(double) * 5 * faces, cudaMemcpyDeviceToHost,
+                              stream_));
+  }
+  err_eval_ = d_mid_;
+  seam_msg_ = true;
+  try {
+    af_step_diag d{};
+    collect_(1, nullptr, nullptr, &d);
+    if (diag) *diag = d;
+  } catch (...) {
+    err_eval_ = nullptr;
+    seam_msg_ = false;
+    throw;
+  }
+  err_eval_ = nullptr;
+  seam_msg_ = false;
+  download_from_(d_u_, out);
 }
 
 void Uniform::step(double dt, af_step_diag* diag) {

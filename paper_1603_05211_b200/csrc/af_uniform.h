@@ -31,6 +31,10 @@ class Uniform {
   void upload(const double* aos);
   void download(double* aos);
   void step(double dt, af_step_diag* diag);
+  // rk2_stage (step.hpp:62-64) on AoS states (host or device); optional
+  // FluxField capture (step.hpp:16-50). Overwrites the solver's buffers.
+  void rk2_stage(const double* base, const double* eval, double* out, double stage_dt,
+                 double* capture, af_step_diag* diag);
   void run(long n_steps, double cfl, double fixed_dt, double* dt_hist, af_run_diag* diag);
   double speed_sum();
   void sync();
@@ -59,8 +63,11 @@ class Uniform {
   const CUtensorMap* tensor_map_(const double* buf, bool own = false);
   void launch_hancock_(const StageArgs& a);
   void launch_speed_sum_(const double* q, unsigned long long* target);
+  void launch_flux_capture_(const double* q, double* dst);
   void enqueue_steps_(long n_steps, double cfl, double fixed_dt);
   void check_error_();
+  void upload_to_(const double* aos, double* dst);
+  void download_from_(const double* src, double* aos);
   void collect_(long n_steps, double* dt_hist, af_run_diag* rd, af_step_diag* sd);
 
   af_config cfg_;
@@ -72,6 +79,10 @@ class Uniform {
   const double* hk_u0_ = nullptr;  // MUSCL-Hancock: the input buffer of even steps
   const double* hk_m0_ = nullptr;  // ... and of odd steps
   double* d_stage_ = nullptr;
+  double* d_cap_ = nullptr;        // FluxField capture staging (rk2_stage)
+  long cap_cap_ = 0;
+  const double* err_eval_ = nullptr;  // rk2_stage: the stage's eval buffer for the error scan
+  bool seam_msg_ = false;             // rk2_stage: the reference's message has no step prefix
   size_t stage_bytes_ = 0;
   int* d_err_ = nullptr;
   RunRecords rec_{};

@@ -611,4 +611,75 @@ __global__ void __launch_bounds__(256) speed_sum_kernel(const double* q, UGrid g
   block_max_atomic<256>(best, red, target);
 }
 
+// FluxField capture (step.hpp:16-50) of one stage's numerical fluxes on `q`:
+// one thread per face, face i along axis a between cells i-1 and i, the
+// stencil cells bc-mapped as the stage kernels map them (reflective momentum
+// flipped before primitives), muscl_recon + the numerical flux of the
+// reconstructed states, or the first-order fallback (scheme.cpp:155-167).
+// The same operations as the exact stage kernels, so the same bits. Output:
+// per axis an (n_a+1) x n_b x n_c array of FluxVectors (5 doubles; the 2D
+// third momentum is +0), x fastest, the axes concatenated.
+template <int D, int S>
+__global__ void __launch_bounds__(256) flux_capture_kernel(const double* q, UGrid g, double* cap,
+                                                           double gamma) {
+  const int n = g.n;
+  const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
+  const long total = D * per;
+  const double gm1 = gamma - 1.0, rgm1 = 1.0 / gm1;
+  const long cs = g.cs, zs = g.zs;
+  auto load = [&](int x, int y, int z) {
+    bool fx, fy, fz = false;
+    const int mx = bc_map(x, n, g.bc[0], g.bc[1], fx);
+    long off;
+    if constexpr (D == 3) {
+      const int my = bc_map(y, n, g.bc[2], g.bc[3], fy);
+      const int zl = slab_map(z, g, 2, fz);
+      off = (long)zl * zs + (long)my * n + mx;
+    } else {
+      const int yl = slab_map(y, g, 1, fy);
+      off = (long)yl * zs + mx;
+    }
+    Cons<D> c;
+    c.rho = q[off];
+    c.m[0] = q[cs + off];
+    c.m[1] = q[2 * cs + off];
+    if constexpr (D == 3) c.m[2] = q[3 * cs + off];
+    c.E = q[(D + 1) * cs + off];
+    if (fx) c.m[0] = -c.m[0];
+    if (fy) c.m[1] = -c.m[1];
+    if (D == 3 && fz) c.m[D - 1] = -c.m[D - 1];
+    return c;
+  };
+  for (long f = blockIdx.x * (long)blockDim.x + threadIdx.x; f < total;
+       f += (long)gridDim.x * blockDim.x) {
+    const int ax = (int)(f / per);
+    const long r = f - ax * per;
+    const int fn0 = ax == 0 ? n + 1 : n, fn1 = ax == 1 ? n + 1 : n;
+    int p[3];
+    p[0] = (int)(r % fn0);
+    const long t = r / fn0;
+    p[1] = (int)(t % fn1);
+    p[2] = D == 3 ? (int)(t / fn1) : 0;
+    Cons<D> qs[4];
+    Prim<D> ws[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      int c[3] = {p[0], p[1], p[2]};
+      c[ax] += s - 2;
+      qs[s] = load(c[0], c[1], c[2]);
+      ws[s] = primitives(qs[s], gm1);
+    }
+    Prim<D> l, rr;
+    const bool fb = muscl_recon<D, S>(ws[0], ws[1], ws[2], ws[3], l, rr);
+    const Cons<D> F = fb ? num_flux<D, S>(qs[1], ws[1], qs[2], ws[2], ax, gamma)
+                         : recon_flux_fast<D, S>(l, rr, ax, gamma, gm1, rgm1);
+    double* o = cap + 5 * f;
+    o[0] = F.rho;
+    o[1] = F.m[0];
+    o[2] = F.m[1];
+    o[3] = D == 3 ? F.m[D - 1] : 0.0;
+    o[4] = F.E;
+  }
+}
+
 }  // namespace af

@@ -34,9 +34,13 @@ class IoError(Error):
     """adaptflow::IoError (errors.hpp:38-41)"""
 
 
+class DivisionDomain(Error):
+    """adaptflow::DivisionDomain (errors.hpp:49-52)."""
+
+
 _BY_STATUS = {1: NonPhysicalState, 2: RegisterMismatch, 3: ConfigError, 4: LevelMismatch,
               5: DeviceError, 6: DeviceError, 7: ValueError, 8: UnsupportedOption,
-              9: DeviceError, 10: IoError}
+              9: DeviceError, 10: IoError, 11: DivisionDomain}
 
 
 def raise_status(status: int, message: str) -> None:

@@ -7,6 +7,7 @@
 // run_uniform / step_block / run_mr forward here.
 //
 // Reference seams mirrored:
+//   gpu::rk2_stage    step.hpp:62-64 with FluxField capture (step.hpp:16-50)
 //   gpu::step_block   step.hpp:77-79 (RK2 branch, step.cpp:237-251); the
 //                     ghost refill callback becomes the BoundaryCondition the
 //                     device folds into its stencil mapping (grid.cpp:9-62)
@@ -106,6 +107,16 @@ class UniformDevice {
     check(af_uniform_download(h_, aos.data()));
     from_aos(aos, b);
   }
+  // rk2_stage on host AoS states; capture (nullable): FluxField-layout buffer
+  StepDiag stage(const std::vector<double>& base, const std::vector<double>& eval,
+                 std::vector<double>& out, double stage_dt, double* capture) {
+    af_step_diag d{};
+    check(af_uniform_rk2_stage(h_, base.data(), eval.data(), out.data(), stage_dt, capture, &d));
+    StepDiag r;
+    r.max_wave_speed = d.max_wave_speed;
+    r.fallbacks = d.fallbacks;
+    return r;
+  }
   StepDiag step(double dt) {
     af_step_diag d{};
     check(af_uniform_step(h_, dt, &d));
@@ -173,6 +184,41 @@ inline StepDiag step_block(BlockData& u, const UniformGrid& geometry, double dt,
   dev.upload(u);
   const StepDiag d = dev.step(dt);
   dev.download(u);
+  return d;
+}
+
+// rk2_stage (step.hpp:62-64): out = base + stage_dt * rhs(eval) for host
+// blocks on `geometry`, eval's ghosts following `bc` (the reference expects
+// them filled; the device maps them from bc). capture: the stage's fluxes
+// into the caller's FluxField (step.hpp:16-50), as the AMR hierarchy's
+// refluxing reads them (amr_hierarchy.cpp:476,488). out may alias base or
+// eval. The device context is the step_block cache's.
+inline StepDiag rk2_stage(const BlockData& base, const BlockData& eval, BlockData& out,
+                          const UniformGrid& geometry, double stage_dt, const SchemeConfig& cfg,
+                          const GasModel& gas, const BoundaryCondition& bc,
+                          FluxField* capture = nullptr) {
+  UniformDevice& dev = step_block_cache().get(geometry, gas, bc, cfg);
+  const int dim = geometry.dim(), n = 1 << geometry.level();
+  std::vector<double> o(static_cast<size_t>(out.interior_cells()) * 5), cap;
+  if (capture) {
+    cap.resize(static_cast<size_t>(dim) * (n + 1) * (dim == 3 ? (long)n * n : (long)n) * 5);
+    if (capture->dim() != dim || capture->cells()[0] != n)
+      *capture = FluxField(dim, {n, n, dim == 3 ? n : 1});
+  }
+  const StepDiag d = dev.stage(to_aos(base), to_aos(eval), o, stage_dt,
+                               capture ? cap.data() : nullptr);
+  from_aos(o, out);
+  if (capture) {
+    size_t f = 0;
+    for (int a = 0; a < dim; ++a) {
+      int fn[3] = {n, n, dim == 3 ? n : 1};
+      fn[a] += 1;
+      for (int k = 0; k < fn[2]; ++k)
+        for (int j = 0; j < fn[1]; ++j)
+          for (int i = 0; i < fn[0]; ++i, ++f)
+            std::memcpy(&capture->face(a, i, j, k), &cap[5 * f], sizeof(FluxVector));
+    }
+  }
   return d;
 }
 

@@ -75,3 +75,23 @@ def l1_error(sol, dim: int, level: int, ref, ref_level: int, extent: float = 1.0
     if st:
         _raise_last(st, "l1_error")
     return out
+
+
+def rates(adaptive: dict, fv: dict, n_c: float) -> dict:
+    """Paper §3 rates (metrics.cpp:91-132) through af_rates_compute. `adaptive`
+    and `fv` hold the RunReport fields the formulas read: wall_seconds,
+    sum_cells, sum_leaves, n_steps, l1_rho. Raises DivisionDomain with the
+    reference's text on a zero denominator."""
+    lib = _abi.load()
+
+    def summ(d):
+        return _abi.RunSummary(float(d.get("wall_seconds", 0.0)), float(d.get("sum_cells", 0.0)),
+                               float(d.get("sum_leaves", 0.0)), int(d.get("n_steps", 0)),
+                               float(d.get("l1_rho", 0.0)))
+    out = _abi.Rates()
+    st = lib.af_rates_compute(C.byref(summ(adaptive)), C.byref(summ(fv)), float(n_c), C.byref(out))
+    if st:
+        e = _abi.ErrorRec()
+        lib.af_uniform_last_error(None, C.byref(e))
+        raise_status(st, e.message.decode())
+    return {k: getattr(out, k) for k, _ in _abi.Rates._fields_}

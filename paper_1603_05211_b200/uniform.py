@@ -175,6 +175,33 @@ class UniformSolver:
         return out
 
     # -- stepping ---------------------------------------------------------
+    def rk2_stage(self, base, eval_, stage_dt: float, capture: bool = False):
+        """rk2_stage (step.hpp:62-64): out = base + stage_dt * rhs(eval) of AoS
+        states (eval's ghosts = the configured BCs). Returns (out, StepDiag,
+        flux) with flux the FluxField capture (step.hpp:16-50) as a list of
+        per-axis arrays of shape (n_c, n_b, n_a + 1, 5), or None. Replaces
+        the solver's state."""
+        out = np.empty((self.cells, 5), dtype=np.float64)
+        cap = None
+        if capture:
+            n = self.n
+            per = (n + 1) * n ** (self.dim - 1)
+            cap = np.empty(self.dim * per * 5, dtype=np.float64)
+        d = _abi.StepDiag()
+        self._check(self._lib.af_uniform_rk2_stage(
+            self._h, C.c_void_p(_state_ptr(base, self.cells)),
+            C.c_void_p(_state_ptr(eval_, self.cells)), C.c_void_p(out.ctypes.data),
+            float(stage_dt), C.c_void_p(cap.ctypes.data if cap is not None else 0), C.byref(d)))
+        flux = None
+        if cap is not None:
+            n, per = self.n, (self.n + 1) * self.n ** (self.dim - 1)
+            flux = []
+            for a in range(self.dim):
+                shape = [n] * self.dim
+                shape[a] += 1
+                flux.append(cap[a * per * 5:(a + 1) * per * 5].reshape(*shape[::-1], 5))
+        return out, StepDiag(d.max_wave_speed, d.fallbacks), flux
+
     def step_block(self, dt: float, diag: bool = True) -> StepDiag | None:
         """step_block (step.hpp:77-79): one RK2 step of size dt."""
         if not diag:

@@ -123,6 +123,43 @@ int main() {
     report("step_block x2 reuses one device context",
            gpu::step_block_cache().creations - c0 <= 1);
   }
+  // rk2_stage with FluxField capture (the AMR refluxing seam), 2D and 3D:
+  // the explicit midpoint's two stages through the shim against the
+  // reference's rk2_stage, states and every captured face flux
+  for (const char* name : {"lax_liu_6", "ellipsoid3d"}) {
+    const CaseSpec& s = find_case(name);
+    const int L = s.dim == 3 ? 4 : 6;
+    UniformGrid u(s.dim, L, s.origin, s.extent);
+    init_case(s, u);
+    UniformGrid m_ref = u, o_ref = u, m_gpu = u, o_gpu = u;
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int n = 1 << L;
+    const std::array<int, 3> cells = {n, n, s.dim == 3 ? n : 1};
+    FluxField fr1(s.dim, cells), fr2(s.dim, cells), fg1, fg2;
+    fill_ghosts(u.block(), s.bc);
+    rk2_stage(u.block(), u.block(), m_ref.block(), u.dx(), 5e-4, sc, s.gas, &fr1);
+    fill_ghosts(m_ref.block(), s.bc);
+    rk2_stage(u.block(), m_ref.block(), o_ref.block(), u.dx(), 1e-3, sc, s.gas, &fr2);
+    gpu::rk2_stage(u.block(), u.block(), m_gpu.block(), u, 5e-4, sc, s.gas, s.bc, &fg1);
+    gpu::rk2_stage(u.block(), m_gpu.block(), o_gpu.block(), u, 1e-3, sc, s.gas, s.bc, &fg2);
+    bool same_flux = fg1.dim() == s.dim && fg2.dim() == s.dim;
+    for (int a = 0; a < s.dim && same_flux; ++a) {
+      std::array<int, 3> fn = cells;
+      fn[a] += 1;
+      for (int k = 0; k < fn[2]; ++k)
+        for (int j = 0; j < fn[1]; ++j)
+          for (int i = 0; i < fn[0]; ++i)
+            for (const auto* pr : {&fr1, &fr2}) {
+              const FluxField& g = pr == &fr1 ? fg1 : fg2;
+              const FluxVector& x = pr->face(a, i, j, k);
+              const FluxVector& y = g.face(a, i, j, k);
+              same_flux = same_flux && x.rho == y.rho && x.mom[0] == y.mom[0] &&
+                          x.mom[1] == y.mom[1] && x.mom[2] == y.mom[2] && x.rhoE == y.rhoE;
+            }
+    }
+    report(std::string("rk2_stage ") + name + " states", same_grid(m_ref, m_gpu) && same_grid(o_ref, o_gpu));
+    report(std::string("rk2_stage ") + name + " FluxField capture", same_flux);
+  }
   // MROptions::on_sample (mr_solver.cpp:394): the reference's observer gets
   // a host MRTree the device run cannot provide -> ConfigError, loudly; the
   // device observer gets the same leaf sets at the same points.

@@ -38,6 +38,11 @@ DIGESTS = {
     "cfg2": dict(kind=0, seed=1, level=10, steps=500, cfl=0.5, eps=1e-3,
                  eps_level=eps_levels(1e-3, 10, 2), min_leaf=3, local_time=0, gap=3,
                  coarse=6),
+    # cfg2's tree and thresholds over its first 50 cycles (the full 500-cycle
+    # reference run takes hours on one core)
+    "cfg2_c50": dict(kind=0, seed=1, level=10, steps=50, cfl=0.5, eps=1e-3,
+                     eps_level=eps_levels(1e-3, 10, 2), min_leaf=3, local_time=0, gap=3,
+                     coarse=6),
     # cfg4 generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of reference time)
     "cfg4_128": dict(kind=2, seed=1, level=7, steps=100, cfl=0.4, coarse=4),
     # cfg3 generator, MRLT at L=10 (steps count finest-level steps: 32 = four

@@ -97,3 +97,38 @@ def test_mr_dump_matches_reference(gpu_lib, oracle, tmp_path, kind, level, steps
                            local_time=kw.get("local_time", False))
     oracle.mr_run("ref", p, init, dump_path=path)
     assert ours == open(path).read()
+
+
+def test_rates_match_reference():
+    """Paper §3 rates (metrics.cpp:91-132) through af_rates_compute against the
+    reference's rates(): same values bit for bit, same DivisionDomain texts.
+    Host arithmetic: runs without a GPU."""
+    from oracle import oracle as O
+    from paper_1603_05211_b200 import io
+    from paper_1603_05211_b200.errors import DivisionDomain
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        ad = dict(wall_seconds=float(rng.uniform(0.1, 9)), sum_cells=float(rng.integers(1, 10**9)),
+                  sum_leaves=float(rng.integers(1, 10**8)), n_steps=int(rng.integers(1, 5000)),
+                  l1_rho=float(rng.uniform(1e-6, 1e-2)))
+        fv = dict(wall_seconds=float(rng.uniform(0.1, 9)), sum_cells=0.0, sum_leaves=0.0,
+                  n_steps=int(rng.integers(1, 5000)), l1_rho=float(rng.uniform(1e-6, 1e-2)))
+        n_c = float(4 ** int(rng.integers(3, 12)))
+        ref, err = O.rates(ad, fv, n_c)
+        assert err is None
+        got = io.rates(ad, fv, n_c)
+        for k, v in ref.items():
+            assert got[k] == v, k
+    base = dict(wall_seconds=1.0, sum_cells=1e6, sum_leaves=5e5, n_steps=10, l1_rho=1e-3)
+    for bad_ad, bad_fv, n_c in ((base, dict(base, n_steps=0), 1e4), (base, base, 0.0),
+                                (base, dict(base, wall_seconds=0.0), 1e4),
+                                (dict(base, n_steps=0), base, 1e4),
+                                (base, dict(base, l1_rho=0.0), 1e4),
+                                (dict(base, sum_leaves=0.0), base, 1e4)):
+        _, err = O.rates(bad_ad, bad_fv, n_c)
+        assert err is not None
+        with pytest.raises(DivisionDomain) as e:
+            io.rates(bad_ad, bad_fv, n_c)
+        assert str(e.value) == err

@@ -90,3 +90,20 @@ def test_spec_kats():
     c = np.sqrt(1.4)
     assert dts[0] == 0.5 * (1.0 / 64) / (c + c)
     assert res["max_wave_speed"] == c
+
+
+def test_reference_rk2_stage_harness_is_step_block():
+    """afref_rk2_stage (the seam's checker) composes to the reference's own
+    step_block: stage(u,u,mid,dt/2), stage(u,mid,u,dt) == one fixed-dt step."""
+    from oracle import oracle as O
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    for dim, level, kind in ((2, 5, 0), (3, 4, 2)):
+        init = O.case_fill(kind, 3, level)
+        p = O.make_params(dim, level, 1, cfl=0.0, fixed_dt=1e-3)
+        ref, _, res = O.uniform_run("ref", p, init)
+        mid, r1, _ = O.rk2_stage(p, init, init, 0.5e-3)
+        out, r2, flux = O.rk2_stage(p, init, mid, 1e-3, capture=True)
+        assert np.array_equal(bits(out), bits(ref))
+        assert max(r1["max_wave_speed"], r2["max_wave_speed"]) == res["max_wave_speed"]
+        assert len(flux) == dim
