@@ -34,15 +34,15 @@ def eps_levels(eps, L, d):
 DIGESTS = {
     # cfg1 at its own size: 2D uniform 256^2, 200 steps
     "cfg1": dict(kind=0, seed=1, level=8, steps=200, cfl=0.5, coarse=6),
-    # cfg2 at its own size: 2D MR L=10, level thresholds, min leaf 3, 500 cycles
+    # cfg2 at its own size: 2D MR L=10, level thresholds, min leaf 3, 500 cycles.
+    # Not committed: the reference did not finish it in 90 CPU-minutes here (nor
+    # a 50-cycle prefix in 20: its from_uniform + first coarsen of the full
+    # 1024^2 tree dominates, value_at recursing through absent levels); cfg2's
+    # rules are pinned at L=7 (tests/golden/mr_quad_L7_epsl_min3.npz, the
+    # test_mr_gpu cases) and its full-size properties in test_fullsize_gpu.py
     "cfg2": dict(kind=0, seed=1, level=10, steps=500, cfl=0.5, eps=1e-3,
                  eps_level=eps_levels(1e-3, 10, 2), min_leaf=3, local_time=0, gap=3,
                  coarse=6),
-    # cfg2's tree and thresholds over its first 50 cycles (the full 500-cycle
-    # reference run takes hours on one core)
-    "cfg2_c50": dict(kind=0, seed=1, level=10, steps=50, cfl=0.5, eps=1e-3,
-                     eps_level=eps_levels(1e-3, 10, 2), min_leaf=3, local_time=0, gap=3,
-                     coarse=6),
     # cfg4 generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of reference time)
     "cfg4_128": dict(kind=2, seed=1, level=7, steps=100, cfl=0.4, coarse=4),
     # cfg3 generator, MRLT at L=10 (steps count finest-level steps: 32 = four
