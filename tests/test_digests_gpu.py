@@ -5,7 +5,9 @@ written by tests/golden/make_digests.py from oracle/_ref; the reference is
 not on the GPU box):
 
   * cfg1  2D uniform 256^2 x 200 steps;
-  * cfg2  2D MR L=10 (1024^2), level thresholds, min leaf 3, 500 cycles;
+  * cfg2  rules (level thresholds, min leaf 3, global dt) over the config's own
+          500 cycles at L=8 (the reference does not finish L=10 on one core
+          here, tests/golden/make_digests.py);
   * cfg4  3D uniform generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of
           reference time; the full size is covered by tests/test_tolerance_gpu.py
           and tests/test_fullsize_gpu.py properties);
