@@ -15,7 +15,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg2")
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--level", type=int, default=None)
 a = ap.parse_args()
+if a.level is not None:
+    w = list(bench.WORKLOADS[a.workload])
+    w[3] = a.level
+    bench.WORKLOADS[a.workload] = tuple(w)
 idx, case, dim, level, cfl, seed, _ = bench.WORKLOADS[a.workload]
 o, epsl = bench.mr_options(a.workload)
 s = M.MRSolver(dim, level, M.MROptions(epsilon=o["eps"], eps_level=epsl,
