@@ -308,6 +308,10 @@ def workload_config(workload, n_gpus, numerics="exact"):
          "parity_mode": NUMERICS["exact"]}
     if dim == 3 and workload not in MR_OPTS:
         c["parity_mode"] = NUMERICS[numerics]
+    if dim == 2 and workload in MR_OPTS and numerics == "tolerance":
+        c["parity_mode"] = ("tolerance: full-tile stages with reciprocal estimates + FMA, within "
+                            "1e-10 relative L1 per field of the bit-exact run with identical leaf "
+                            "sets (tests/test_mr_tolerance_gpu.py)")
     if BASE_LEVEL.get(workload, level) != level:
         c["level_override"] = f"finest level {level} instead of the config's {BASE_LEVEL[workload]}"
     if workload in MR_OPTS:
@@ -344,12 +348,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-other-numerics", action="store_true")
-    ap.add_argument("--numerics", default="tolerance", choices=["tolerance", "exact"],
+    ap.add_argument("--numerics", default=None, choices=["tolerance", "exact"],
                     help="3D uniform stage numerics: 'tolerance' (reciprocal estimates + FMA, "
                          "within BASELINE.json's 1e-10 relative L1 per field of the exact result; "
                          "tests/test_tolerance_gpu.py) or 'exact' (bit-identical to the "
                          "reference). The other mode is timed too and reported beside it.")
     args = ap.parse_args()
+    if args.numerics is None:  # uniform 3D: tolerance; MR: exact (its established bar)
+        args.numerics = "exact" if args.workload in MR_OPTS else "tolerance"
     if args.steps is None:
         args.steps = WORKLOADS[args.workload][6]
     if args.level is not None:
@@ -581,6 +587,8 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
                         comm=comm if slabs else None)
     stream = torch.cuda.Stream(device=local)
     solver.set_stream(stream)
+    if dim == 2 and args.numerics == "tolerance":
+        solver.set_numerics(True)
     init_host = U.case_fill(case, seed, level)
     init_pinned = torch.from_numpy(init_host).pin_memory()
     init_dev = init_pinned.to(f"cuda:{local}")
@@ -694,7 +702,7 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong" if (slabs or world == 1) else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args.workload, world),
+        "config": dict(workload_config(args.workload, world, args.numerics),
                        leaves_last_cycle=int(rep.cycles[-1, 0]) if len(rep.cycles) else None,
                        decomposition=(f"{world} slabs of rows along the last axis from level "
                                       f"{mr_partition_level(o, level, world)} up, halo "

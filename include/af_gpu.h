@@ -237,6 +237,12 @@ af_status af_mr_create(const af_config* cfg, const af_mr_options* opt, af_mr** o
 af_status af_mr_create_dist(const af_config* cfg, const af_mr_options* opt, af_comm* comm,
                             af_mr** out);
 /* Rows [lo, hi) of the last axis at `level` that this rank owns. */
+/* Numerics of the MR stage (AF_NUMERICS_EXACT default, bit-identical to the
+ * reference). AF_NUMERICS_TOLERANCE runs the 2D full-tile stage kernel with
+ * the uniform tolerance physics (reciprocal estimates, FMA): within 1e-10
+ * relative L1 per field of the exact run with the same leaf sets
+ * (tests/test_mr_tolerance_gpu.py); every other MR kernel stays exact. */
+af_status af_mr_set_numerics(af_mr* m, int numerics);
 af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi);
 af_status af_mr_destroy(af_mr* m);
 af_status af_mr_set_stream(af_mr* m, void* cuda_stream);

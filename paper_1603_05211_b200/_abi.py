@@ -108,6 +108,7 @@ SIGNATURES = {
     "af_mr_create": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), C.POINTER(_vp)]),
     "af_mr_create_dist": (C.c_int, [C.POINTER(Config), C.POINTER(MROptions), _vp,
                                     C.POINTER(_vp)]),
+    "af_mr_set_numerics": (C.c_int, [_vp, C.c_int]),
     "af_mr_local_rows": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "af_mr_destroy": (C.c_int, [_vp]),
     "af_mr_set_stream": (C.c_int, [_vp, _vp]),

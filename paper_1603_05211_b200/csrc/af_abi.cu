@@ -273,6 +273,11 @@ af_status af_mr_create_dist(const af_config* cfg, const af_mr_options* opt, af_c
   });
 }
 
+af_status af_mr_set_numerics(af_mr* m, int numerics) {
+  if (!m || !m->impl) return record(nullptr, AF_E_ARGUMENT, "null solver");
+  return guard(&m->impl->last_error(), [&] { m->impl->set_numerics(numerics); });
+}
+
 af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi) {
   if (!m || !lo || !hi) return AF_E_ARGUMENT;
   try {

@@ -378,6 +378,7 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
                     (const void*)mr_stage_full2d<2>, (const void*)mr_stage_full2d<3>})
       AF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)MRFull2::smem_bytes));
+    mr_full_tol_setup();
   }
   if (dist_) dist_setup_();
 }
@@ -434,6 +435,28 @@ MR::~MR() {
 }
 
 void MR::set_stream(cudaStream_t s) { stream_ = s ? s : own_stream_; }
+
+void MR::invalidate_graphs_() {
+  AF_CUDA(cudaStreamSynchronize(stream_));
+  for (GraphCache& gc : graphs_) {
+    if (gc.exec) cudaGraphExecDestroy(gc.exec);
+    gc = GraphCache{};
+  }
+  for (CycleGraph& cg : cyc_) {
+    if (cg.exec) cudaGraphExecDestroy(cg.exec);
+    if (cg.graph) cudaGraphDestroy(cg.graph);
+    cg = CycleGraph{};
+  }
+}
+
+void MR::set_numerics(int numerics) {
+  if (numerics != AF_NUMERICS_EXACT && numerics != AF_NUMERICS_TOLERANCE)
+    throw Error(AF_E_ARGUMENT, "unknown numerics mode");
+  if (numerics != numerics_) {  // captured cycle graphs hold the other kernels
+    numerics_ = numerics;
+    invalidate_graphs_();
+  }
+}
 
 double MR::eps_at_(int child_level) const {
   return eps_level_.empty() ? opt_.eps : eps_level_[child_level];
@@ -982,7 +1005,9 @@ void MR::stage_(int lo, int hi, double tau, double sdt, int stage, long step) {
     const int lcode = -(std::max(lo, 0) + 1);
     const int sch = cfg_.limiter | (cfg_.flux << 1);
     const size_t smf = MRFull2::smem_bytes;
-    switch (sch) {
+    if (numerics_ == AF_NUMERICS_TOLERANCE) {
+      mr_full_tol_launch(sch, gf, stream_, pdl_, f, g_, lcode);
+    } else switch (sch) {
       case 0: launch_k(pdl_, stream_, mr_stage_full2d<0>, gf, MRFull2::NT, smf, f, g_, lcode); break;
       case 1: launch_k(pdl_, stream_, mr_stage_full2d<1>, gf, MRFull2::NT, smf, f, g_, lcode); break;
       case 2: launch_k(pdl_, stream_, mr_stage_full2d<2>, gf, MRFull2::NT, smf, f, g_, lcode); break;

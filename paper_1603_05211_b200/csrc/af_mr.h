@@ -12,6 +12,11 @@ namespace af {
 
 struct MRStageArgs;
 
+// Tolerance-mode full-tile stage kernels (af_mr_full_tol.cu, FMA contraction).
+void mr_full_tol_setup();
+void mr_full_tol_launch(int scheme, dim3 grid, cudaStream_t stream, bool pdl,
+                        const MRStageArgs& a, const MRLevels& g, int lcode);
+
 // One contiguous run of whole rows in a halo exchange (af_mr_dist.cu).
 struct MR_XSeg {
   long cell;   // first cell (concatenated level index)
@@ -21,6 +26,9 @@ struct MR_XSeg {
 
 class MR {
  public:
+  // AF_NUMERICS_EXACT (bit-identical) / AF_NUMERICS_TOLERANCE (the full-tile
+  // 2D stage kernel with the tolerance physics; 1e-10 relative L1)
+  void set_numerics(int numerics);
   // comm: null or one rank for a single GPU; otherwise this rank's slab of
   // the spatial decomposition.
   MR(const af_config& cfg, const af_mr_options& opt, Comm* comm = nullptr);
@@ -143,6 +151,7 @@ class MR {
   std::vector<cudaGraphNode_t> ev_nodes_;  // event-record nodes of the capture in progress
   void enqueue_cycle_(double cfl, double fixed_dt, long* grade_body, long* sweep_body);
   CycleGraph& cycle_graph_(double cfl, double fixed_dt);
+  void invalidate_graphs_();
   bool run_batch_graph_(long B, double cfl, double fixed_dt, long& done, long& cycle, double& t,
                         af_mr_cycle* cycles, long max_cycles);
   void cycle_sync_(long n_steps, double cfl, double fixed_dt, long& done, long& cycle, double& t,
@@ -238,6 +247,7 @@ class MR {
   std::vector<int> pband_count_; // band tiles with an absent cell per level
   std::vector<int> full_count_;  // full leaf tiles per level
   bool pband_ok_ = false;        // statuses unchanged since the lists were built
+  int numerics_ = 0;             // AF_NUMERICS_EXACT / AF_NUMERICS_TOLERANCE
   bool fresh_ = false;
   bool coarse_stale_ = false;  // internal values below min_leaf-1 not projected (refresh_coarse_)
   void refresh_coarse_();

@@ -18,9 +18,13 @@
 //   * update: each leaf sums its four faces in the reference order and
 //     writes out = base + rhs*stage_dt (+ the stage-1 q_old snapshot and the
 //     stage-2 positivity check).
-// Every operation and its order are those of mr_stage_kernel, so the two are
-// bit-identical (tests/test_mr_switches_gpu.py compares them); the generic
-// kernel handles the other leaf tiles of the same stage.
+// MODE 0: every operation and its order are those of mr_stage_kernel, so the
+// two are bit-identical (tests/test_mr_switches_gpu.py compares them); the
+// generic kernel handles the other leaf tiles of the same stage. MODE 1
+// (tolerance, af_mr_full_tol.cu, FMA contraction): the face physics of the
+// uniform tolerance kernels (reciprocal estimates, af_physics.cuh *_tol) and
+// a folded update; within 1e-10 relative L1 of the exact run with the same
+// leaf sets (tests/test_mr_tolerance_gpu.py).
 #pragma once
 
 #include "af_mr_stage.cuh"
@@ -41,7 +45,7 @@ struct MRFull2 {
   static constexpr size_t smem_bytes = sizeof(double) * (size_t)(RED + NW) + NF;
 };
 
-template <int S>
+template <int S, int MODE = 0>
 __global__ void __launch_bounds__(MRFull2::NT, 2)
     mr_stage_full2d(MRStageArgs a, MRLevels g, int lcode) {
   AF_PDL_ENTRY();
@@ -186,7 +190,13 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
       }
       if (fi) q.m[0] = -q.m[0];
       if (fj) q.m[1] = -q.m[1];
-      const Prim<D> w = primitives(q, gm1);
+      Prim<D> w;
+      if constexpr (MODE == 0) {
+        w = primitives(q, gm1);
+      } else {
+        double ir;
+        w = primitives_tol(q, gm1, ir);
+      }
       pr[idx] = w.rho;
       pr[K::HP + idx] = w.v[0];
       pr[2 * K::HP + idx] = w.v[1];
@@ -200,7 +210,11 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
       q.rho = w.rho;
       if (!cell_ok(q, w)) bad = 1;
       double s, m;
-      wave_speeds(w, gamma, s, m);
+      if constexpr (MODE == 0) {
+        wave_speeds(w, gamma, s, m);
+      } else {
+        wave_speeds_tol(w, rcp_tol(w.rho), gamma, s, m);
+      }
       wave = fmax(wave, m);
     }
     auto cons_at = [&](int x, int y) { return resolve_at<D>(a.eval, comp, g, cl, x, y, 0, &a); };
@@ -227,8 +241,15 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
         wp2 = P(fx + 2, fy + 3);
       }
       Prim<D> lft, rgt;
-      const bool fb = muscl_recon<D, S>(wm1, w0, wp1, wp2, lft, rgt);
-      Cons<D> F = recon_flux_fast_warp<D, AX, S>(lft, rgt, gamma, gm1, rgm1);
+      bool fb;
+      Cons<D> F;
+      if constexpr (MODE == 0) {
+        fb = muscl_recon<D, S>(wm1, w0, wp1, wp2, lft, rgt);
+        F = recon_flux_fast_warp<D, AX, S>(lft, rgt, gamma, gm1, rgm1);
+      } else {
+        fb = muscl_recon_tol<D, S>(wm1, w0, wp1, wp2, lft, rgt);
+        F = recon_flux_tol<D, S>(lft, rgt, AX, gamma, gm1, rgm1, rgm1);
+      }
       if (__any_sync(0xffffffffu, fb)) {
         if (fb) {
           const int gx = cx0 + fx, gy = cy0 + fy;
@@ -261,14 +282,18 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
 #pragma unroll
       for (int m = 0; m < NC; ++m) {
         const double* fm = fl + m * K::NF;
-        double rhs = 0.0;
-        rhs = rhs + fm[fxl] * inv_dx;
-        rhs = rhs - fm[fxh] * inv_dx;
-        rhs = rhs + fm[fyl] * inv_dx;
-        rhs = rhs - fm[fyh] * inv_dx;
         const double base0 = bb[m * K::NCELL + tid];
         if (a.snap) a.snap[m * comp + own] = base0;
-        o[m] = base0 + rhs * sdt;
+        if constexpr (MODE == 0) {
+          double rhs = 0.0;
+          rhs = rhs + fm[fxl] * inv_dx;
+          rhs = rhs - fm[fxh] * inv_dx;
+          rhs = rhs + fm[fyl] * inv_dx;
+          rhs = rhs - fm[fyh] * inv_dx;
+          o[m] = base0 + rhs * sdt;
+        } else {
+          o[m] = __fma_rn((fm[fxl] - fm[fxh]) + (fm[fyl] - fm[fyh]), inv_dx * sdt, base0);
+        }
         a.out[m * comp + own] = o[m];
       }
       nfb += ffb[fxl] + ffb[fxh] + ffb[fyl] + ffb[fyh];
@@ -278,7 +303,12 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
         q.m[0] = o[1];
         q.m[1] = o[2];
         q.E = o[3];
-        if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
+        if constexpr (MODE == 0) {
+          if (!cell_ok(q, primitives(q, gm1))) bad |= 2;
+        } else {
+          double ir;
+          if (!cell_ok(q, primitives_tol(q, gm1, ir))) bad |= 2;
+        }
       }
     }
     __syncthreads();  // the next iteration refills the buffer this tile read

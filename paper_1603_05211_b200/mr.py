@@ -137,6 +137,11 @@ class MRSolver:
         self._check(self._lib.af_mr_stage_stats(self._h, C.byref(ms), C.byref(la), C.byref(up)))
         return ms.value, la.value, up.value
 
+    def set_numerics(self, tolerance: bool) -> None:
+        """AF_NUMERICS_EXACT (default, bit-identical) or AF_NUMERICS_TOLERANCE
+        (the 2D full-tile stage with the tolerance physics, 1e-10 relative L1)."""
+        self._check(self._lib.af_mr_set_numerics(self._h, 1 if tolerance else 0))
+
     # MRTree
     def build(self, aos) -> None:
         cells = 1 << (self.dim * self.level)
