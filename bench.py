@@ -282,7 +282,8 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(1, args.steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.workload, 1, args.numerics),
+        "config": dict(workload_config(args.workload, 1, "exact"),
+                       parity_mode="the reference's own CPU implementation (oracle/_ref)"),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads,
                          "kind": kind, "sample": sample, "ran": ran},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
