@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "af_comm.h"
@@ -437,6 +438,26 @@ void Uniform::launch_hancock_(const StageArgs& a) {
   AF_CUDA(cudaGetLastError());
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL): the
+// kernel's launch overlaps its predecessor's tail; the kernel waits
+// (griddepcontrol.wait) before it reads anything. Used for the small 2D
+// launches, where launch latency is the step's cost (cfg1).
+template <class... P, class... A>
+void launch_pdl(cudaStream_t s, void (*kern)(P...), dim3 grid, unsigned block, size_t smem,
+                A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  AF_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+}
+
 void Uniform::launch_stage_(const StageArgs& a0, int zbeg, int zend) {
   StageArgs a = a0;
   a.zbeg = zbeg < 0 ? g_.zlo : zbeg;
@@ -468,7 +489,7 @@ void Uniform::launch_stage_(const StageArgs& a0, int zbeg, int zend) {
   } else {
     const unsigned tiles = (unsigned)((n / tx) * (g_.nzl / kTY));
 #define AF_L2(L, TX) \
-  fv2d_stage<L, TX, kTY><<<tiles, TX * kTY, Fv2d<L, TX, kTY>::smem_bytes, stream_>>>(a, g_)
+  launch_pdl(stream_, fv2d_stage<L, TX, kTY>, dim3(tiles), TX * kTY, Fv2d<L, TX, kTY>::smem_bytes, a, g_)
     if (tx == 32) {
       AF_SCHEME(AF_L2, 32);
     } else if (tx == 16) {
@@ -486,7 +507,8 @@ void Uniform::launch_speed_sum_(const double* q, unsigned long long* target) {
   if (g_.dim == 3)
     speed_sum_kernel<3><<<2 * 148, 256, 0, stream_>>>(q, g_, cfg_.gamma, target, d_err_);
   else
-    speed_sum_kernel<2><<<2 * 148, 256, 0, stream_>>>(q, g_, cfg_.gamma, target, d_err_);
+    launch_pdl(stream_, speed_sum_kernel<2>, dim3(2 * 148), 256, 0, q, g_, cfg_.gamma, target,
+               (const int*)d_err_);
   ++launches_;
   AF_CUDA(cudaGetLastError());
 }

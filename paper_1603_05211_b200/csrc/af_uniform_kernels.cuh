@@ -420,6 +420,9 @@ template <int LIM, int TX, int TY>
 __global__ void __launch_bounds__(TX* TY, 2) fv2d_stage(StageArgs a, UGrid g) {
   using K = Fv2d<LIM, TX, TY>;
   constexpr int D = 2;
+  // programmatic dependent launch (a no-op without the launch attribute): the
+  // launch overlaps the predecessor's tail, the wait precedes every read
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
   if (failed_before(a.r.err)) return;
   extern __shared__ double sm[];
   double* pl = sm;                  // [NC][HP]
@@ -589,6 +592,7 @@ __global__ void __launch_bounds__(256) speed_sum_kernel(const double* q, UGrid g
                                                         unsigned long long* target,
                                                         const int* err) {
   __shared__ double red[8];
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
   if (err && failed_before(err)) return;
   const long cells = g.plane * g.nzl;
   const long cs = g.cs;
