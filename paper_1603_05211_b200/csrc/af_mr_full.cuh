@@ -3,7 +3,13 @@
 // A full tile (mr_tile_flags_all bit 2) is a 32x8 tile of level l whose
 // cells and face neighbours are all leaves of l: every face is a plain
 // same-level face of MRSolver::stage (mr_solver.cpp:163-193) — no fine
-// sub-face average, no flux register, no leaf tests. Dense regions of a tree
+// sub-face average, no flux register, no leaf tests. A near-full tile (bit
+// 4) has only leaf cells and no INTERNAL face neighbour: its edge faces may
+// border absent cells (virtual leaves over a coarser leaf, read through V
+// and the MRLT time interpolation as resolve does), which are still plain
+// faces; in a register stage such a face toward an already-advanced coarser
+// cell also deposits its fine register share (face_flux_at,
+// mr_solver.cpp:147-159), as mr_stage_kernel does. Dense regions of a tree
 // (cfg3's finest level is all leaves) are made of them, so they get their own
 // kernel, pipelined like the uniform fv3d_tile:
 //   * the next tile's halo box (the 36x12 cross of the tile, bc-mapped as
@@ -89,11 +95,14 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
   const double* basesrc = a.snap ? a.eval : a.base;  // stage 1: q_old is eval itself
 
   // tile `it` of the launch's range -> level, origin (walk: entries increase)
-  auto locate = [&](int it, int& l, int& x0, int& y0) {
+  // near: the tile is near-full, not full (only those deposit register
+  // shares); read in register stages only
+  auto locate = [&](int it, int& l, int& x0, int& y0, bool& near) {
     const int t = lcode < 0 ? walk.at(g, a.tiles, it, &l) : tile_at(g, lcode, a.tiles, a.ntiles, it, &l);
     const int sx = ilog2i(g.ntx[l]);
     x0 = (t & (g.ntx[l] - 1)) * TX;
     y0 = ((t >> sx) & (g.nty[l] - 1)) * TY;
+    near = a.reg_stage && a.tflag && (a.tflag[g.tile_off[l] + t] & 4) == 0;
   };
   auto on_cross = [&](int idx, int& ix, int& iy) {
     ix = idx % K::HX;
@@ -137,8 +146,9 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
   };
 
   int l = 0, x0 = 0, y0 = 0;
+  bool near = false;
   if ((int)blockIdx.x < ntotal) {
-    locate(blockIdx.x, l, x0, y0);
+    locate(blockIdx.x, l, x0, y0, near);
     issue(l, x0, y0, 0);
   }
   cp_async_commit();
@@ -146,9 +156,10 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
   for (int it = blockIdx.x; it < ntotal; it += gridDim.x, ++k) {
     const int b = k & 1;
     const int cl = l, cx0 = x0, cy0 = y0;  // this tile
+    const bool cnear = near;
     const int nit = it + (int)gridDim.x;
     if (nit < ntotal) {
-      locate(nit, l, x0, y0);
+      locate(nit, l, x0, y0, near);
       issue(l, x0, y0, b ^ 1);
     }
     cp_async_commit();
@@ -297,6 +308,39 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
         a.out[m * comp + own] = o[m];
       }
       nfb += ffb[fxl] + ffb[fxh] + ffb[fyl] + ffb[fyh];
+      // near-full tiles in a register stage: the fine share of an edge face
+      // whose outside cell is absent under an advanced (marked) coarser leaf
+      if (cnear && (tx == 0 || tx == TX - 1 || ty == 0 || ty == TY - 1) && cl >= 1 &&
+          cl - 1 < a.lo) {
+        const int c[2] = {cx0 + tx, cy0 + ty};
+#pragma unroll
+        for (int ax = 0; ax < 2; ++ax)
+#pragma unroll
+          for (int dir = -1; dir <= 1; dir += 2) {
+            const int t_in = ax == 0 ? tx + dir : ty + dir;
+            if (t_in >= 0 && t_in < (ax == 0 ? TX : TY)) continue;  // inside: a leaf
+            int p[2] = {c[0], c[1]};
+            p[ax] += dir;
+            bool flp;
+            p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
+            if (a.st[off + (long)p[1] * n + p[0]] != ST_ABSENT) continue;
+            const int pn = n >> 1;
+            const long pc = g.cell_off[cl - 1] + (long)(p[1] >> 1) * pn + (p[0] >> 1);
+            if (!a.vmark[pc]) continue;
+            const int R = reg_index(a.regbase, a.regmask, pc, ax * 2 + (dir > 0 ? 0 : 1));
+            if (R >= 0) {
+              const int t = c[1 - ax] & 1;  // sub-face slot (ascending pack_key order)
+              const double w = a.step_dt * a.share;
+              double* dst = a.regf + (((long)R * 2 + a.sub) * 2 + t) * NC;
+              const int fi = ax == 0 ? (dir < 0 ? fxl : fxh) : (dir < 0 ? fyl : fyh);
+#pragma unroll
+              for (int m = 0; m < NC; ++m) dst[m] = fl[m * K::NF + fi] * w;
+              a.regff[R] = 1;
+            } else {
+              atomicExch(a.regerr, 1);
+            }
+          }
+      }
       if (a.post_check) {
         Cons<D> q;
         q.rho = o[0];

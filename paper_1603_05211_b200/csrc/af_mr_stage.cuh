@@ -701,9 +701,10 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
     // bit 2, a full tile: every cell a leaf and every face neighbour of the
     // tile (bc-mapped, same level) a leaf too (one rank only)
     bool full = !g.dist && !__any_sync(0xffffffffu, notleaf);
+    bool near = full;  // bit 4: every cell a leaf, no face neighbour INTERNAL (2D)
     if (full) {
       constexpr int RX = TY * TZ, RY = TX * TZ, RZ = D == 3 ? TX * TY : 0;
-      bool ok = true;
+      bool ok = true, nint = true;
       for (int c = lane; c < 2 * (RX + RY + RZ); c += 32) {
         int q[3], a, side, r;
         if (c < 2 * RX) { a = 0; side = c / RX; r = c % RX; }
@@ -716,15 +717,18 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
         q[b2] = D == 3 ? ((b2 == 1 ? y0 : z0) + r / T[b1]) : 0;
         bool f;
         for (int d = 0; d < D; ++d) q[d] = mr_map(q[d], n, g.bc[2 * d], g.bc[2 * d + 1], f);
-        ok = ok && st[g.cell_off[l] + mr_idx(D, n, q[0], q[1], q[2])] == ST_LEAF;
+        const uint8_t s = st[g.cell_off[l] + mr_idx(D, n, q[0], q[1], q[2])];
+        ok = ok && s == ST_LEAF;
+        nint = nint && s != ST_INTERNAL;
       }
       full = __all_sync(0xffffffffu, ok);
+      near = D == 2 && __all_sync(0xffffffffu, nint);
     }
     if (lane == 0) {
       // bit 0: the tile holds a leaf this rank steps, or (with ranks) a
       // halo leaf whose register shares it computes
       tflag[tg] = ((nleaf || (g.dist && rleaf)) ? 1 : 0) | (pex ? 2 : 0) | (full ? 4 : 0) |
-                  (absent ? 8 : 0);
+                  (absent ? 8 : 0) | (near ? 16 : 0);
       tleaf[tg] = (int)nleaf;
     }
   }
@@ -779,8 +783,9 @@ __global__ void mr_tile_lists_all(const uint8_t* tflag, const int* tleaf, MRLeve
     const unsigned lb = __ballot_sync(grp, in_leaf) & grp;
     const bool in_pband = in_band && (tflag[tg] & 8) != 0;
     const unsigned pb = __ballot_sync(grp, in_pband) & grp;
-    // leaf tiles split into full (bit 2: mr_stage_full2d) and the rest
-    const bool in_full = in_leaf && (tflag[tg] & 4) != 0, in_part = in_leaf && !in_full;
+    // leaf tiles split into full or near-full (bits 2 / 4: mr_stage_full2d)
+    // and the rest
+    const bool in_full = in_leaf && (tflag[tg] & (4 | 16)) != 0, in_part = in_leaf && !in_full;
     const unsigned fb = __ballot_sync(grp, in_full) & grp;
     const unsigned qb = __ballot_sync(grp, in_part) & grp;
     const unsigned nl = __reduce_add_sync(grp, (unsigned)tleaf[tg]);
