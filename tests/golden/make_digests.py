@@ -49,6 +49,11 @@ DIGESTS = {
     "cfg2_L8": dict(kind=0, seed=1, level=8, steps=500, cfl=0.5, eps=1e-3,
                     eps_level=eps_levels(1e-3, 8, 2), min_leaf=3, local_time=0, gap=3,
                     coarse=6),
+    # the same at L=9 (~30 CPU-minutes, most of it the reference's initial
+    # from_uniform + coarsen of the full 512^2 tree)
+    "cfg2_L9": dict(kind=0, seed=1, level=9, steps=500, cfl=0.5, eps=1e-3,
+                    eps_level=eps_levels(1e-3, 9, 2), min_leaf=3, local_time=0, gap=3,
+                    coarse=6),
     # cfg4 generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of reference time)
     "cfg4_128": dict(kind=2, seed=1, level=7, steps=100, cfl=0.4, coarse=4),
     # cfg3 generator, MRLT at L=10 (steps count finest-level steps: 32 = four

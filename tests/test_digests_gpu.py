@@ -12,7 +12,8 @@ not on the GPU box):
           reference time; the full size is covered by tests/test_tolerance_gpu.py
           and tests/test_fullsize_gpu.py properties);
   * cfg3  2D MRLT generator (+-1 % density noise) at L=10 (32 finest steps)
-          and one L=13 macro-cycle (8192^2, 8 finest steps);
+          and at its own L=13 for one macro-cycle (8192^2, 8 finest steps,
+          60.8 M leaves; 1.9 h of reference time here);
   * cfg5  3D MRLT rules (level thresholds, coarsest 16^3) at L=7.
 
 Bit-exact mode must reproduce each digest exactly: the to_uniform(L) state's

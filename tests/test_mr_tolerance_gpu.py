@@ -56,12 +56,14 @@ def test_tolerance_matches_exact(gpu_lib, case):
     assert d.max() > 0.0  # the tolerance kernel ran
 
 
-def test_tolerance_matches_reference_digest(gpu_lib):
-    """cfg3's MRLT generator at L=10 (the reference's digest): same leaf set,
-    per-field relative L1 of the digest's restricted state within 1e-10."""
+@pytest.mark.parametrize("name", ["cfg3_L10", "cfg3_L13"])
+def test_tolerance_matches_reference_digest(gpu_lib, name):
+    """cfg3's MRLT generator at L=10 and at its own L=13 (one macro-cycle; the
+    reference's digests): same leaf set, per-field relative L1 of the
+    digest's restricted state within 1e-10."""
     from paper_1603_05211_b200 import mr as M
     from paper_1603_05211_b200 import uniform as U
-    path = os.path.join(HERE, "golden", "digest_cfg3_L10.npz")
+    path = os.path.join(HERE, "golden", f"digest_{name}.npz")
     if not os.path.exists(path):
         pytest.skip("digest missing")
     g = np.load(path, allow_pickle=False)
