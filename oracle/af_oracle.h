@@ -78,7 +78,7 @@ int afref_rk2_stage(const af_oracle_params* p, const double* base, const double*
  */
 int afref_uniform_window_run(const af_oracle_params* p, int z0, int nz, int threads,
                              long n_warm, const double* init, double* out,
-                             af_oracle_result* res);
+                             af_oracle_result* res, double* dt_hist);
 
 /*
  * MR / MRLT run (mr_solver.cpp:318-400 loop). out: to_uniform(L) of the final

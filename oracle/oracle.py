@@ -86,7 +86,7 @@ def _load(kind: str):
             ("restrict", [C.c_int, C.c_int, C.c_int, dp, dp]),
             ("l1_error", [C.c_int, C.c_int, C.c_double, dp, C.c_int, dp, dp]),
             ("uniform_window_run", [C.POINTER(Params), C.c_int, C.c_int, C.c_int, C.c_long,
-                                    dp, dp, C.POINTER(Result)]),
+                                    dp, dp, C.POINTER(Result), dp]),
             ("mr_refine_once", [C.POINTER(Params), dp, C.c_double, C.POINTER(C.c_int), C.c_int,
                                 dp, C.POINTER(C.c_uint64), C.POINTER(C.c_long)]),
             ("rk2_stage", [C.POINTER(Params), dp, dp, C.c_double, dp, dp, C.POINTER(Result)]),
@@ -184,16 +184,22 @@ def window_init(kind: int, seed: int, level: int, z0: int, nz: int) -> np.ndarra
 
 
 def uniform_window_run(params: Params, init: np.ndarray, z0: int, nz: int, threads: int,
-                       n_warm: int = 0, want_out: bool = False):
+                       n_warm: int = 0, want_out: bool = False, want_dt: bool = False):
     """The reference's step_block on `threads` z-slabs of the window
-    [z0, z0+nz) of the 3D mesh (ref_harness.cpp). Returns (out or None, result)."""
+    [z0, z0+nz) of the 3D mesh (ref_harness.cpp). Returns (out or None, result)
+    or, with want_dt, (out or None, dt history, result). With z0 = 0, nz = n
+    this is afref_uniform_run bit for bit, on `threads` host cores."""
     lib = _load("ref")
     n = 1 << params.level
     out = np.zeros((nz * n * n, 5)) if want_out else None
+    dts = np.zeros(max(params.n_steps, 1)) if want_dt else None
     res = Result()
     lib.afref_uniform_window_run(C.byref(params), z0, nz, threads, n_warm,
                                  _dp(np.ascontiguousarray(init)),
-                                 _dp(out) if want_out else None, C.byref(res))
+                                 _dp(out) if want_out else None, C.byref(res),
+                                 _dp(dts) if want_dt else None)
+    if want_dt:
+        return out, dts[: params.n_steps], res.as_dict()
     return out, res.as_dict()
 
 

@@ -54,6 +54,10 @@ DIGESTS = {
     "cfg2_L9": dict(kind=0, seed=1, level=9, steps=500, cfl=0.5, eps=1e-3,
                     eps_level=eps_levels(1e-3, 9, 2), min_leaf=3, local_time=0, gap=3,
                     coarse=6),
+    # cfg4 at its own size: 3D 512^3 x 100 steps, the reference's step_block on
+    # 8 host-thread z-slabs (ref_harness.cpp afref_uniform_window_run, bit for
+    # bit the single-block run; ~15 minutes here)
+    "cfg4": dict(kind=2, seed=1, level=9, steps=100, cfl=0.4, coarse=5, threads=8),
     # cfg4 generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of reference time)
     "cfg4_128": dict(kind=2, seed=1, level=7, steps=100, cfl=0.4, coarse=4),
     # cfg3 generator, MRLT at L=10 (steps count finest-level steps: 32 = four
@@ -93,7 +97,11 @@ def run(name, c):
             assert np.array_equal(D.bitmaps_to_keys(rec["leaf_bitmaps"], dim, c["level"]), keys)
     else:
         p = O.make_params(dim, c["level"], c["steps"], cfl=c["cfl"])
-        out, dts, res = O.uniform_run("ref", p, init)
+        if c.get("threads"):  # the reference's step_block on z-slabs, host threads
+            out, dts, res = O.uniform_window_run(p, init, 0, 1 << c["level"], c["threads"],
+                                                 want_out=True, want_dt=True)
+        else:
+            out, dts, res = O.uniform_run("ref", p, init)
         rec.update(mr=0, dt=dts, max_wave_speed=res["max_wave_speed"])
     assert res["err_kind"] == 0, res["err"]
     rec.update(max_cfl=res["max_cfl"], fallbacks=res["fallbacks"],

@@ -107,3 +107,19 @@ def test_reference_rk2_stage_harness_is_step_block():
         assert np.array_equal(bits(out), bits(ref))
         assert max(r1["max_wave_speed"], r2["max_wave_speed"]) == res["max_wave_speed"]
         assert len(flux) == dim
+
+
+def test_reference_window_run_is_single_block():
+    """afref_uniform_window_run (the reference's step_block on host-thread
+    z-slabs, used for cfg4's full-size digest and the bench's reference arm)
+    equals the reference's single-block run bit for bit: state, dt history,
+    max_cfl, StepDiag wave speed."""
+    from oracle import oracle as O
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    init = O.case_fill(2, 1, 5)
+    p = O.make_params(3, 5, 6, cfl=0.4)
+    a, da, ra = O.uniform_run("ref", p, init)
+    b, db, rb = O.uniform_window_run(p, init, 0, 32, 4, want_out=True, want_dt=True)
+    assert np.array_equal(bits(a), bits(b)) and np.array_equal(bits(da), bits(db))
+    assert ra["max_cfl"] == rb["max_cfl"] and ra["max_wave_speed"] == rb["max_wave_speed"]
