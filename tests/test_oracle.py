@@ -120,6 +120,6 @@ def test_reference_window_run_is_single_block():
     init = O.case_fill(2, 1, 5)
     p = O.make_params(3, 5, 6, cfl=0.4)
     a, da, ra = O.uniform_run("ref", p, init)
-    b, db, rb = O.uniform_window_run(p, init, 0, 32, 4, want_out=True, want_dt=True)
+    b, db, rb = O.uniform_window_run(p, init, 0, 32, 8, want_out=True, want_dt=True)
     assert np.array_equal(bits(a), bits(b)) and np.array_equal(bits(da), bits(db))
     assert ra["max_cfl"] == rb["max_cfl"] and ra["max_wave_speed"] == rb["max_wave_speed"]
