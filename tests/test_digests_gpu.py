@@ -6,8 +6,8 @@ not on the GPU box):
 
   * cfg1  2D uniform 256^2 x 200 steps;
   * cfg2  rules (level thresholds, min leaf 3, global dt) over the config's own
-          500 cycles at L=8 (the reference does not finish L=10 on one core
-          here, tests/golden/make_digests.py);
+          500 cycles at L=8 and at L=9 (the reference does not finish L=10 on
+          one core here, tests/golden/make_digests.py);
   * cfg4  3D uniform generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of
           reference time; the full size is covered by tests/test_tolerance_gpu.py
           and tests/test_fullsize_gpu.py properties);
