@@ -8,9 +8,9 @@ not on the GPU box):
   * cfg2  rules (level thresholds, min leaf 3, global dt) over the config's own
           500 cycles at L=8 and at L=9 (the reference does not finish L=10 on
           one core here, tests/golden/make_digests.py);
-  * cfg4  3D uniform generator at 128^3 x 100 steps (512^3 x 100 is ~3 h of
-          reference time; the full size is covered by tests/test_tolerance_gpu.py
-          and tests/test_fullsize_gpu.py properties);
+  * cfg4  3D uniform at its own size, 512^3 x 100 steps (the reference's
+          step_block on 8 host-thread z-slabs, bit for bit its single-block run;
+          24 minutes here), and its generator at 128^3 x 100;
   * cfg3  2D MRLT generator (+-1 % density noise) at L=10 (32 finest steps)
           and at its own L=13 for one macro-cycle (8192^2, 8 finest steps,
           60.8 M leaves; 1.9 h of reference time here);
