@@ -681,7 +681,7 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-            "peak_source": src, "kernel": "mr_stage_kernel",
+            "peak_source": src, "kernel": "mr_stage_full2d + mr_stage_kernel" if dim == 2 else "mr_stage_kernel",
             "kernel_share_of_step": stage_ms / ms if ms > 0 else None,
             "stage_launches": stage_launches,
             "note": "per-launch average over the timed region; the MR cycle also runs "
