@@ -283,17 +283,23 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
       else
         face(std::integral_constant<int, 1>{}, u);
     }
-    __syncthreads();
+    // the step-start values leave their buffer before the barrier, so the
+    // next iteration may refill it without a fourth barrier per tile
+    double base[NC];
+    if (owner) {
+#pragma unroll
+      for (int m = 0; m < NC; ++m) base[m] = bsm[b * NC * K::NCELL + m * K::NCELL + tid];
+    }
+    __syncthreads();  // fluxes complete; every read of this tile's buffers done
     if (owner) {
       const long own = off + (long)(cy0 + ty) * n + (cx0 + tx);
       const int fxl = ty * TX + tx, fxh = tx + 1 < TX ? fxl + 1 : TX * TY + ty;
       const int fyl = K::YS + ty * TX + tx, fyh = fyl + TX;
-      const double* bb = bsm + b * NC * K::NCELL;
       double o[NC];
 #pragma unroll
       for (int m = 0; m < NC; ++m) {
         const double* fm = fl + m * K::NF;
-        const double base0 = bb[m * K::NCELL + tid];
+        const double base0 = base[m];
         if (a.snap) a.snap[m * comp + own] = base0;
         if constexpr (MODE == 0) {
           double rhs = 0.0;
@@ -355,7 +361,8 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
         }
       }
     }
-    __syncthreads();  // the next iteration refills the buffer this tile read
+    // (no barrier here: the next iteration's first barrier orders its
+    // convert and faces after every thread's update of this tile)
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   flush_wave();
