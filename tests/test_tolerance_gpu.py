@@ -115,3 +115,16 @@ def test_tile_kernel_exact_equals_fv3d_stage(gpu_lib, monkeypatch, level, steps,
     assert np.array_equal(bits(ra.dt), bits(rb.dt))
     assert ra.max_wave_speed == rb.max_wave_speed and ra.max_cfl == rb.max_cfl
     assert ra.fallbacks == rb.fallbacks
+
+
+@pytest.mark.parametrize("tol", [False, True])
+def test_z_chunking_does_not_change_results(gpu_lib, monkeypatch, tol):
+    """fv3d_tile's z-chunk count (wave-quantisation choice, AF_FV3D_CHUNKS)
+    changes only the schedule: every chunk count gives the same bits."""
+    monkeypatch.delenv("AF_FV3D_CHUNKS", raising=False)
+    ref, rr = run(6, 6, tol, kind=3, bc=[2, 2, 0, 0, 1, 1])
+    for ch in ("1", "3", "7"):
+        monkeypatch.setenv("AF_FV3D_CHUNKS", ch)
+        out, rep = run(6, 6, tol, kind=3, bc=[2, 2, 0, 0, 1, 1])
+        assert np.array_equal(bits(out), bits(ref)), ch
+        assert np.array_equal(bits(rep.dt), bits(rr.dt)), ch
