@@ -215,7 +215,19 @@ typedef struct af_mr_options {
   int min_leaf_level;      /* MRTree::set_min_leaf_level (mr_tree.hpp:78) */
   int local_time;          /* MROptions::local_time */
   int lt_gap;              /* MROptions::local_time_level_gap (default 3) */
+  int storage;             /* AF_MR_STORAGE_* (0 = dense per-level grids) */
+  int brick_shift;         /* bricks of 2^brick_shift cells per axis (0: 6) */
 } af_mr_options;
+
+/* Storage of the per-level value arrays (the reference's node map,
+ * mr_tree.hpp:195). DENSE: every level a row-major 2^l-per-axis grid.
+ * BRICKS (3D): levels finer than the brick stored brick after brick, still
+ * fully allocated (the layout on its own). SPARSE (3D, brick_shift 6): the
+ * brick layout with a 2 MiB page behind a brick of a value component only
+ * while the tree reaches it (needed set from the band lists, re-mapped at every
+ * refine); memory follows the tree instead of the finest volume. Results are
+ * bit-identical across the three (tests/test_mr_storage_gpu.py). One rank. */
+enum { AF_MR_STORAGE_DENSE = 0, AF_MR_STORAGE_BRICKS = 1, AF_MR_STORAGE_SPARSE = 2 };
 
 /* Per macro cycle record (RunReport cells/leaves_per_step, mr_solver.cpp:369-374). */
 typedef struct af_mr_cycle {
@@ -244,6 +256,10 @@ af_status af_mr_create_dist(const af_config* cfg, const af_mr_options* opt, af_c
  * (tests/test_mr_tolerance_gpu.py); every other MR kernel stays exact. */
 af_status af_mr_set_numerics(af_mr* m, int numerics);
 af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi);
+/* Device bytes of the tree's per-cell arrays: now, the peak so far, and what
+ * the same tree takes as dense per-level grids (any argument may be null). */
+af_status af_mr_memory(const af_mr* m, unsigned long long* now, unsigned long long* peak,
+                       unsigned long long* dense);
 af_status af_mr_destroy(af_mr* m);
 af_status af_mr_set_stream(af_mr* m, void* cuda_stream);
 /* from_uniform(level-L AoS data, 0, bc), norms, min leaf level, coarsen(eps)

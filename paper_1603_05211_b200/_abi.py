@@ -61,7 +61,8 @@ class ErrorRec(C.Structure):
 
 class MROptions(C.Structure):
     _fields_ = [("eps", C.c_double), ("eps_level", C.POINTER(C.c_double)),
-                ("min_leaf_level", C.c_int), ("local_time", C.c_int), ("lt_gap", C.c_int)]
+                ("min_leaf_level", C.c_int), ("local_time", C.c_int), ("lt_gap", C.c_int),
+                ("storage", C.c_int), ("brick_shift", C.c_int)]
 
 
 class MRCycle(C.Structure):
@@ -110,6 +111,8 @@ SIGNATURES = {
                                     C.POINTER(_vp)]),
     "af_mr_set_numerics": (C.c_int, [_vp, C.c_int]),
     "af_mr_local_rows": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "af_mr_memory": (C.c_int, [_vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong),
+                               C.POINTER(C.c_ulonglong)]),
     "af_mr_destroy": (C.c_int, [_vp]),
     "af_mr_set_stream": (C.c_int, [_vp, _vp]),
     "af_mr_build": (C.c_int, [_vp, _vp]),

@@ -18,7 +18,7 @@ LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libafgpu.so")
 
 SOURCES = ["af_abi.cu", "af_uniform.cu", "af_fv3d_tol.cu", "af_mr.cu", "af_mr_full_tol.cu",
-           "af_mr_dist.cu", "af_io.cu"]
+           "af_mr_dist.cu", "af_io.cu", "af_mr_storage.cu"]
 # translation units compiled WITH FMA contraction (tolerance-mode kernels only)
 FMAD_TRUE = {"af_fv3d_tol.cu", "af_mr_full_tol.cu"}
 HEADERS = sorted(f for f in os.listdir(os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc"))

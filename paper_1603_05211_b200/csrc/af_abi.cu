@@ -278,6 +278,13 @@ af_status af_mr_set_numerics(af_mr* m, int numerics) {
   return guard(&m->impl->last_error(), [&] { m->impl->set_numerics(numerics); });
 }
 
+af_status af_mr_memory(const af_mr* m, unsigned long long* now, unsigned long long* peak,
+                       unsigned long long* dense) {
+  if (!m) return AF_E_ARGUMENT;
+  m->impl->memory(now, peak, dense);
+  return AF_OK;
+}
+
 af_status af_mr_local_rows(const af_mr* m, int level, int* lo, int* hi) {
   if (!m || !lo || !hi) return AF_E_ARGUMENT;
   try {

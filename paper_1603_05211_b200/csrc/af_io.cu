@@ -253,14 +253,12 @@ std::string MR::dump() {
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j)
         for (int k = 0; k < nk; ++k) {
-          const long c = g_.cell_off[l] + (D_ == 3 ? ((long)k * n + j) * n + i : (long)j * n + i);
+          const long c = g_.cell_off[l] + mr_idx(g_, D_, n, i, j, k);
           const uint8_t st = hs[c];
           bool virt = false;
           if (st == ST_ABSENT) {  // virtual leaves: children of a marked leaf
             if (vm.empty() || l == 0) continue;
-            const long pc = g_.cell_off[l - 1] +
-                            (D_ == 3 ? ((long)(k >> 1) * (n >> 1) + (j >> 1)) * (n >> 1) + (i >> 1)
-                                     : (long)(j >> 1) * (n >> 1) + (i >> 1));
+            const long pc = g_.cell_off[l - 1] + mr_idx(g_, D_, n >> 1, i >> 1, j >> 1, k >> 1);
             if (!vm[pc]) continue;
             virt = true;
           }

@@ -43,10 +43,15 @@ __global__ void mr_upload_finest(const double* __restrict__ aos, double* V, MRLe
   AF_PDL_ENTRY();
   const long rowlen = D == 3 ? 1L << (2 * g.L) : 1L << g.L;
   const long cells = (long)(r1 - r0) * rowlen, comp = g.total_cells;
-  const long off = g.cell_off[g.L] + (long)r0 * rowlen;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    const double* q = aos + 5 * c;
+  const int n = 1 << g.L;
+  for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < cells;
+       u += (long)gridDim.x * blockDim.x) {
+    const double* q = aos + 5 * u;
+    // the uniform array is row-major; the level may be bricked (MRLevels::bsh)
+    const long x = u + (long)r0 * rowlen;
+    const long off = g.cell_off[g.L],
+               c = mr_idx(g, D, n, (int)(x & (n - 1)), (int)((x >> g.L) & (n - 1)),
+                          D == 3 ? (int)(x >> (2 * g.L)) : 0);
     V[off + c] = q[0];
     V[comp + off + c] = q[1];
     V[2 * comp + off + c] = q[2];
@@ -62,16 +67,32 @@ __global__ void mr_download_level(const double* V, double* __restrict__ aos, MRL
   AF_PDL_ENTRY();
   const long rowlen = D == 3 ? 1L << (2 * l) : 1L << l;
   const long cells = (long)(r1 - r0) * rowlen, comp = g.total_cells;
-  const long off = g.cell_off[l] + (long)r0 * rowlen;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
-       c += (long)gridDim.x * blockDim.x) {
-    double* q = aos + 5 * c;
+  const int n = 1 << l;
+  for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < cells;
+       u += (long)gridDim.x * blockDim.x) {
+    double* q = aos + 5 * u;
+    const long x = u + (long)r0 * rowlen;  // row-major output, possibly bricked level
+    const long off = g.cell_off[l],
+               c = mr_idx(g, D, n, (int)(x & (n - 1)), (int)((x >> l) & (n - 1)),
+                          D == 3 ? (int)(x >> (2 * l)) : 0);
     q[0] = V[off + c];
     q[1] = V[comp + off + c];
     q[2] = V[2 * comp + off + c];
     q[3] = D == 3 ? V[3 * comp + off + c] : 0.0;
     q[4] = V[(D + 1) * comp + off + c];
   }
+}
+
+// One component of level l in row-major order (details of a bricked level).
+template <int D>
+__global__ void mr_level_rowmajor(const double* src, double* __restrict__ dst, MRLevels g, int l) {
+  AF_PDL_ENTRY();
+  const int n = 1 << l;
+  const long cells = mr_cells(D, l);
+  for (long u = blockIdx.x * (long)blockDim.x + threadIdx.x; u < cells;
+       u += (long)gridDim.x * blockDim.x)
+    dst[u] = src[g.cell_off[l] + mr_idx(g, D, n, (int)(u & (n - 1)), (int)((u >> l) & (n - 1)),
+                                        D == 3 ? (int)(u >> (2 * l)) : 0)];
 }
 
 // Virtual q_old snapshot (mr_solver.cpp:251-266): VQold = V at the virtual
@@ -85,10 +106,11 @@ __global__ void mr_virtual_snapshot(const double* V, double* VQ, const uint8_t* 
   const long comp = g.total_cells;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
-    if (g.dist && !row_in_region(g, l, mr_row(D, l, c))) continue;  // this rank's rows
+    if (g.dist && !row_in_region(g, l, mr_row(g, D, l, c))) continue;  // this rank's rows
     if (st[off + c] != ST_ABSENT) continue;
-    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
-    if (!mark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) continue;
+    int i, j, k;
+  mr_ijk(g, D, l, c, i, j, k);
+    if (!mark[poff + mr_idx(g, D, pn, i >> 1, j >> 1, k >> 1)]) continue;
     for (int m = 0; m < D + 2; ++m) VQ[m * comp + off + c] = V[m * comp + off + c];
   }
 }
@@ -316,21 +338,25 @@ MR::MR(const af_config& c, const af_mr_options& o, Comm* comm) : cfg_(c), opt_(o
       g_.reg_hi[l] = hi;
     }
   }
-  // per-cell arrays: windowed with ranks (AF_MR_NO_WINDOWS maps everything)
+  // cell order and padding of the level arrays (dense / bricks / sparse bricks)
+  storage_setup_(o);
+  // per-cell arrays: windowed with ranks (AF_MR_NO_WINDOWS maps everything);
+  // the value arrays as sparse bricks with AF_MR_STORAGE_SPARSE
   windows_ = dist_ && std::getenv("AF_MR_NO_WINDOWS") == nullptr;
   win_setup_();
-  d_st_ = static_cast<uint8_t*>(walloc_(1, 1));
-  d_mark_ = static_cast<uint8_t*>(walloc_(1, 1));
-  d_flag_ = static_cast<uint8_t*>(walloc_(1, 1));
-  d_flag2_ = static_cast<uint8_t*>(walloc_(1, 1));
-  d_V_ = static_cast<double*>(walloc_(8, NC_));
-  d_Vs_ = static_cast<double*>(walloc_(8, NC_));
-  d_Qold_ = static_cast<double*>(walloc_(8, NC_));
-  d_det_ = static_cast<double*>(walloc_(8, 1));
+  const bool sp = storage_ == AF_MR_STORAGE_SPARSE;
+  d_st_ = static_cast<uint8_t*>(calloc_(1, 1, false));
+  d_mark_ = static_cast<uint8_t*>(calloc_(1, 1, false));
+  d_flag_ = static_cast<uint8_t*>(calloc_(1, 1, false));
+  d_flag2_ = static_cast<uint8_t*>(calloc_(1, 1, false));
+  d_V_ = static_cast<double*>(calloc_(8, NC_, sp));
+  d_Vs_ = static_cast<double*>(calloc_(8, NC_, sp));
+  d_Qold_ = static_cast<double*>(calloc_(8, NC_, sp));
+  d_det_ = static_cast<double*>(calloc_(8, 1, sp));
   if (o.local_time) {
-    d_VQold_ = static_cast<double*>(walloc_(8, NC_));
-    d_regbase_ = static_cast<int*>(walloc_(4, 1));
-    d_regmask_ = static_cast<uint8_t*>(walloc_(1, 1));
+    d_VQold_ = static_cast<double*>(calloc_(8, NC_, sp));
+    d_regbase_ = static_cast<int*>(calloc_(4, 1, false));
+    d_regmask_ = static_cast<uint8_t*>(calloc_(1, 1, false));
   }
   {  // stream-ordered scratch allocations keep their memory
     cudaMemPool_t pool;
@@ -418,6 +444,10 @@ MR::~MR() {
   for (void* p : {(void*)d_ckV_, (void*)d_ckSt_, (void*)d_cycrec_, (void*)d_cycctl_, (void*)d_acc_})
     cudaFree(p);
   if (h_dt_step_) cudaFreeHost(h_dt_step_);
+  if (!sp_.empty()) {  // sparse value arrays: VMM reservations, not cudaMalloc
+    sp_free_all_();
+    d_V_ = d_Vs_ = d_Qold_ = d_VQold_ = d_det_ = nullptr;
+  }
   if (windows_) {
     wfree_all_();
   } else {
@@ -680,6 +710,7 @@ void MR::build(const double* aos) {
   int r0 = 0, r1 = 1 << L_;
   if (dist_) part_rows_(rank_, L_, &r0, &r1);
   const long ucells = (long)(r1 - r0) * rowlen;
+  sp_map_all_(d_V_);  // from_uniform fills and projects every level (sparse: all bricks)
   double* stage = nullptr;
   AF_CUDA(cudaMallocAsync((void**)&stage, sizeof(double) * 5 * ucells, stream_));
   AF_CUDA(cudaMemcpyAsync(stage, aos + 5 * (long)r0 * rowlen, sizeof(double) * 5 * ucells,
@@ -727,6 +758,7 @@ void MR::build(const double* aos) {
   const double t0 = timing ? now_ms() : 0.0;
   coarsen();
   build_lists_();
+  sparse_sync_();  // sparse bricks: release what the coarsened tree does not reach
   if (timing) std::fprintf(stderr, "build: initial coarsen + lists %.3f ms\n", now_ms() - t0);
 }
 
@@ -756,6 +788,7 @@ void MR::refine(double eps, const int* buffer, int n) {
 void MR::refine_(const std::vector<int>& radius, const double* eps) {
   registers_built_ = false;
   if (!lists_valid_) build_lists_();
+  sparse_sync_();  // sparse bricks: map what this cycle can reach (af_mr_storage.cu)
   wset_(d_flag_, 1, 1, 0, 0, L_);
   wset_(d_flag2_, 1, 1, 0, 0, L_);
   // details with the refine flags of their leaf children (one launch)
@@ -1423,7 +1456,7 @@ void MR::check_error_(long step) {
     for (int i = 0; i < n && !found; ++i)
       for (int j = 0; j < n && !found; ++j)
         for (int k = 0; k < nk && !found; ++k) {
-          const long c = g_.cell_off[l] + (D_ == 3 ? ((long)k * n + j) * n + i : (long)j * n + i);
+          const long c = g_.cell_off[l] + mr_idx(g_, D_, n, i, j, k);
           if (hs[c] != ST_LEAF || !row_owned(g_, l, D_ == 3 ? k : j)) continue;
           const double rho = hv[c];
           double msq = hv[comp + c] * hv[comp + c] + hv[2 * comp + c] * hv[2 * comp + c];
@@ -1823,7 +1856,9 @@ void MR::run(long n_steps, double cfl, double fixed_dt, af_mr_cycle* cycles, lon
   long done = 0, cycle = 0;
   double t = 0.0;
   // global time step: whole cycles replay as one graph each (run_batch_graph_)
-  const bool graph = !opt_.local_time && !dist_ && !std::getenv("AF_MR_NO_GRAPH") &&
+  // (sparse bricks re-map between cycles: host-driven cycles)
+  const bool graph = !opt_.local_time && !dist_ && storage_ != AF_MR_STORAGE_SPARSE &&
+                     !std::getenv("AF_MR_NO_GRAPH") &&
                      !std::getenv("AF_MR_NO_CYCLE_GRAPH") && !std::getenv("AF_MR_TIMING");
   while (done < n_steps) {
     if (graph) {
@@ -1946,7 +1981,9 @@ long MR::leaf_keys(uint64_t* keys, long cap) {
     const long cells = mr_cells(D_, l);
     for (long c = 0; c < cells; ++c) {
       if (hs[g_.cell_off[l] + c] != ST_LEAF) continue;
-      const uint64_t i = c % n, j = (c / n) % n, k = D_ == 3 ? c / ((long)n * n) : 0;
+      int ii, jj, kk;
+      mr_ijk(g_, D_, l, c, ii, jj, kk);
+      const uint64_t i = (uint64_t)ii, j = (uint64_t)jj, k = (uint64_t)kk;
       if (!row_counted(g_, l, (int)(D_ == 3 ? k : j))) continue;  // this rank's leaves
       out.push_back(((uint64_t)l << 45) | (i << 30) | (j << 15) | k);  // pack_key
     }
@@ -1976,6 +2013,7 @@ void MR::to_uniform(int level, double* aos) {
   if (dist_) local_rows(level, &r0, &r1);
   const long cells = (long)(r1 - r0) * rowlen;
   if (cells <= 0) return;
+  sp_map_all_(d_V_);  // dense predictions below (sparse: every brick, trimmed at the next refine)
   // value_at for every cell: the band keeps predictions current only near the
   // tree; absent cells farther away get theirs here, coarsest first
   // (MRTree::to_uniform / value_at, mr_tree.cpp:171-180,608-621)
@@ -1996,11 +2034,21 @@ void MR::to_uniform(int level, double* aos) {
 void MR::details(int level, double* out) {
   if (level < 0 || level >= L_) throw Error(AF_E_LEVEL_MISMATCH, "details: bad level");
   const long cells = mr_cells(D_, level);
+  sp_map_all_(d_V_);
+  sp_map_all_(d_det_);
   AF_CUDA(cudaMemsetAsync(d_det_ + g_.cell_off[level], 0xff, sizeof(double) * cells, stream_));
   AF_MR_LAUNCH(mr_detail_level, grid_for(cells), d_V_, d_st_, d_det_, g_, level, d_norms_,
                (uint8_t*)nullptr, (const int*)nullptr, 0);
-  AF_CUDA(cudaMemcpyAsync(out, d_det_ + g_.cell_off[level], sizeof(double) * cells,
-                          cudaMemcpyDefault, stream_));
+  if (g_.bsh && level > g_.bsh) {  // bricked level: back to row-major order
+    double* tmp = nullptr;
+    AF_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double) * cells, stream_));
+    AF_MR_LAUNCH(mr_level_rowmajor, grid_for(cells), (const double*)d_det_, tmp, g_, level);
+    AF_CUDA(cudaMemcpyAsync(out, tmp, sizeof(double) * cells, cudaMemcpyDefault, stream_));
+    AF_CUDA(cudaFreeAsync(tmp, stream_));
+  } else {
+    AF_CUDA(cudaMemcpyAsync(out, d_det_ + g_.cell_off[level], sizeof(double) * cells,
+                            cudaMemcpyDefault, stream_));
+  }
   AF_CUDA(cudaStreamSynchronize(stream_));
 }
 

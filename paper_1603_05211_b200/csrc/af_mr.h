@@ -60,6 +60,8 @@ class MR {
   long fallbacks() const { return fallbacks_; }
 
   long launches() const { return launches_; }
+  // device bytes of the per-cell arrays: now, peak, and as dense level grids
+  void memory(unsigned long long* now, unsigned long long* peak, unsigned long long* dense) const;
   void profile(bool on);
   void stage_stats(double* ms, long* launches, long* updates);
   af_error& last_error() { return last_; }
@@ -198,6 +200,36 @@ class MR {
   void dist_free_();
   void exchange_(int mask);
   void allreduce_(unsigned long long* v, int k, int op);
+  // ---- storage of the per-cell arrays (af_mr_storage.cu) ----
+  static constexpr int kBrickShift3 = 6;  // 64^3-cell bricks: 2 MiB per value component
+  int storage_ = 0;                       // AF_MR_STORAGE_*
+  struct SpArr {                          // one sparse value array (VMM)
+    unsigned long long base = 0;
+    size_t reserved = 0, coarse_bytes = 0;
+    int ncomp = 0;
+    long mapped = 0;
+    std::vector<unsigned long long> coarse;  // per component: the always-mapped coarse block
+    std::vector<unsigned long long> bricks;  // [brick * ncomp + c]: its page (0 = unmapped)
+  };
+  std::vector<SpArr> sp_;
+  long sp_nbricks_ = 0;
+  size_t sp_brick_bytes_ = 0, sp_now_ = 0, sp_peak_ = 0;
+  size_t cell_bytes_ = 0;       // dense per-cell allocations
+  size_t cell_elem_bytes_ = 0;  // bytes per cell over all per-cell arrays
+  uint8_t* d_need_ = nullptr;
+  std::vector<uint8_t> h_need_;
+  void storage_setup_(const af_mr_options& o);
+  int sp_level_(long gb, long* b) const;
+  void* sp_alloc_(int ncomp);
+  SpArr* sp_find_(const void* p);
+  void sp_map_(SpArr& a, long gb);
+  void sp_unmap_(SpArr& a, long gb);
+  void sp_map_all_(const void* p);
+  void sparse_sync_();
+  void sp_free_all_();
+  bool sp_set_(void* p, int value, int lev_lo, int lev_hi);
+  bool sp_tohost_(void* dst, const void* src);
+  void* calloc_(size_t elem, int ncomp, bool sparse);
   double norms_host_[5] = {1, 1, 1, 1, 1};
   double eps_at_(int child_level) const;
 

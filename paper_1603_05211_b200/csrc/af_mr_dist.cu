@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "af_mr.h"
+#include "af_vmm.h"
 
 namespace af {
 
@@ -244,46 +245,6 @@ void MR::exchange_(int mask) {
 }
 
 // ---- windowed arrays --------------------------------------------------------
-namespace {
-// Driver-API virtual memory entry points, resolved through the runtime
-// (cudaGetDriverEntryPoint) so the library does not link libcuda and still
-// loads on a machine without a driver (the CPU test suite).
-struct VmmApi {
-  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
-  decltype(&cuMemAddressReserve) reserve = nullptr;
-  decltype(&cuMemCreate) create = nullptr;
-  decltype(&cuMemMap) map = nullptr;
-  decltype(&cuMemSetAccess) access = nullptr;
-  decltype(&cuMemUnmap) unmap = nullptr;
-  decltype(&cuMemRelease) release = nullptr;
-  decltype(&cuMemAddressFree) free_ = nullptr;
-};
-const VmmApi& vmm() {
-  static VmmApi api = [] {
-    VmmApi a;
-    auto get = [](const char* name, void** fn) {
-      cudaDriverEntryPointQueryResult q;
-      AF_CUDA(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q));
-      if (q != cudaDriverEntryPointSuccess || !*fn)
-        throw Error(AF_E_CUDA, std::string("driver entry point missing: ") + name);
-    };
-    get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.granularity));
-    get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve));
-    get("cuMemCreate", reinterpret_cast<void**>(&a.create));
-    get("cuMemMap", reinterpret_cast<void**>(&a.map));
-    get("cuMemSetAccess", reinterpret_cast<void**>(&a.access));
-    get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap));
-    get("cuMemRelease", reinterpret_cast<void**>(&a.release));
-    get("cuMemAddressFree", reinterpret_cast<void**>(&a.free_));
-    return a;
-  }();
-  return api;
-}
-void check_cu(CUresult r, const char* what) {
-  if (r != CUDA_SUCCESS)
-    throw Error(AF_E_CUDA, std::string(what) + ": driver error " + std::to_string((int)r));
-}
-}  // namespace
 
 // Per-level window rows: the region widened by the tile height plus the
 // stencil reach, so tile-based kernels (whose tiles may overhang the region)
@@ -383,9 +344,16 @@ void MR::wfree_all_() {
 // restricted to the windows
 void MR::wset_(void* p, size_t elem, int ncomp, int value, int lev_lo, int lev_hi) {
   if (lev_hi < lev_lo) return;
+  if (sp_set_(p, value, lev_lo, lev_hi)) return;  // sparse bricks: the mapped ones
   uint8_t* b = static_cast<uint8_t*>(p);
   for (int m = 0; m < ncomp; ++m) {
     const size_t cbase = (size_t)m * g_.total_cells;
+    if (!windows_ && g_.bsh) {  // padded levels: the padding stays ABSENT / zero
+      for (int l = lev_lo; l <= lev_hi; ++l)
+        AF_CUDA(cudaMemsetAsync(b + (cbase + g_.cell_off[l]) * elem, value,
+                                mr_cells(D_, l) * elem, stream_));
+      continue;
+    }
     if (!windows_) {
       const long c0 = g_.cell_off[lev_lo], c1 = g_.cell_off[lev_hi + 1];
       AF_CUDA(cudaMemsetAsync(b + (cbase + c0) * elem, value, (c1 - c0) * elem, stream_));
@@ -401,6 +369,7 @@ void MR::wset_(void* p, size_t elem, int ncomp, int value, int lev_lo, int lev_h
 // copy of a per-cell array to a full-size host buffer (windows only; the
 // rest of dst is left as it is)
 void MR::wtohost_(void* dst, const void* src, size_t elem, int ncomp) {
+  if (sp_tohost_(dst, src)) return;  // sparse bricks: the mapped ones
   uint8_t* d = static_cast<uint8_t*>(dst);
   const uint8_t* s = static_cast<const uint8_t*>(src);
   if (!windows_) {

@@ -43,10 +43,6 @@ __device__ __forceinline__ int mr_map(int c, int n, int lo, int hi, bool& flip) 
   return c;
 }
 
-__device__ __forceinline__ long mr_idx(int D, int n, int i, int j, int k) {
-  return D == 3 ? ((long)k * n + j) * n + i : (long)j * n + i;
-}
-
 // Tile iteration of one launch. Single level (l >= 0): the `ntiles` entries
 // of `tiles` (ntiles -1 / -2 / -3: the band / leaf-tile / absent-band count
 // from g.dcnt).
@@ -136,7 +132,7 @@ __device__ __forceinline__ void level_cells(const MRLevels& g, int l, const int*
       const int sx = ilog2i(ntx), sy = ilog2i(nty);  // tile counts are powers of two
       const int x = (t & (ntx - 1)) * TX + tx, y = ((t >> sx) & (nty - 1)) * TY + ty;
       const int z = D == 3 ? (t >> (sx + sy)) * kTileZ3 + tz : 0;
-      if (x < n && y < n && (D == 2 || z < n)) f(lv, mr_idx(D, n, x, y, z));
+      if (x < n && y < n && (D == 2 || z < n)) f(lv, mr_idx(g, D, n, x, y, z));
     });
   } else {
     const long cells = mr_cells(D, l);
@@ -157,14 +153,15 @@ __device__ __forceinline__ void project_cell(double* V, const MRLevels& g, int l
   const long foff = g.cell_off[l + 1];
   const long comp = g.total_cells;
   const double w = 1.0 / (double)(1 << D);
-  if (s != ST_INTERNAL || !row_owned(g, l, mr_row(D, l, c))) return;
-  const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
+  if (s != ST_INTERNAL || !row_owned(g, l, mr_row(g, D, l, c))) return;
+  int i, j, k;
+  mr_ijk(g, D, l, c, i, j, k);
   double sm[NC];
 #pragma unroll
   for (int m = 0; m < NC; ++m) sm[m] = 0.0;
 #pragma unroll
   for (int ch = 0; ch < (1 << D); ++ch) {
-    const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+    const long fc = foff + mr_idx(g, D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                                   D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
 #pragma unroll
     for (int m = 0; m < NC; ++m) sm[m] = sm[m] + V[m * comp + fc];
@@ -194,7 +191,7 @@ __device__ __forceinline__ long tile_cell(const MRLevels& g, int l, const int* t
   const int sx = ilog2i(ntx), sy = ilog2i(nty);  // tile counts are powers of two
   const int x = (t & (ntx - 1)) * TX + tx, y = ((t >> sx) & (nty - 1)) * TY + ty;
   const int z = D == 3 ? (t >> (sx + sy)) * kTileZ3 + tz : 0;
-  return (x < n && y < n && (D == 2 || z < n)) ? mr_idx(D, n, x, y, z) : -1L;
+  return (x < n && y < n && (D == 2 || z < n)) ? mr_idx(g, D, n, x, y, z) : -1L;
 }
 
 // Band/leaf-tile cell iteration (tiles non-null) whose first tile lookup and
@@ -304,8 +301,8 @@ __device__ __forceinline__ double axw_w(const AxisW& s, int t) { return t == 0 ?
 // mr_tree.cpp:238-279: weights w = wx * (wy * wz), zero weights skipped,
 // accumulation ck -> cj -> ci).
 template <int D>
-__device__ __forceinline__ void predict_child(const double* V, long comp, long poff, int pn,
-                                              int bcx, int bcy, int bcz, int pi, int pj, int pk,
+__device__ __forceinline__ void predict_child(const MRLevels& g, const double* V, long comp,
+                                              long poff, int pn, int bcx, int bcy, int bcz, int pi, int pj, int pk,
                                               int ch, double* out) {
   constexpr int NC = D + 2;
   constexpr int NZ = D == 3 ? 3 : 1;
@@ -330,7 +327,7 @@ __device__ __forceinline__ void predict_child(const double* V, long comp, long p
       for (int r = 0; r < RB; ++r)
 #pragma unroll
         for (int ci = 0; ci < 3; ++ci) {
-          const long c = poff + mr_idx(D, pn, axw_p(sx, ci), axw_p(sy, cj0 + r),
+          const long c = poff + mr_idx(g, D, pn, axw_p(sx, ci), axw_p(sy, cj0 + r),
                                        D == 3 ? axw_p(sz, ck) : 0);
 #pragma unroll
           for (int m = 0; m < NC; ++m) v[r][ci][m] = V[m * comp + c];
@@ -367,13 +364,14 @@ __device__ __forceinline__ void predict_cell(double* V, const uint8_t* vmark, co
   const long off = g.cell_off[l], poff = g.cell_off[l - 1];
   const long comp = g.total_cells;
   const bool refresh_virtual = l - 1 >= lo && l - 1 <= hi;
-  if (dense && g.dist && !row_in_region(g, l, mr_row(D, l, c))) return;  // dense: own rows
+  if (dense && g.dist && !row_in_region(g, l, mr_row(g, D, l, c))) return;  // dense: own rows
   if (s != ST_ABSENT) return;
-  const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
-  if (!refresh_virtual && vmark && vmark[poff + mr_idx(D, pn, i >> 1, j >> 1, k >> 1)]) return;
+  int i, j, k;
+  mr_ijk(g, D, l, c, i, j, k);
+  if (!refresh_virtual && vmark && vmark[poff + mr_idx(g, D, pn, i >> 1, j >> 1, k >> 1)]) return;
   const int ch = (i & 1) | ((j & 1) << 1) | (D == 3 ? ((k & 1) << 2) : 0);
   double q[NC];
-  predict_child<D>(V, comp, poff, pn, g.bc[0], g.bc[2], g.bc[4], i >> 1, j >> 1, k >> 1, ch, q);
+  predict_child<D>(g, V, comp, poff, pn, g.bc[0], g.bc[2], g.bc[4], i >> 1, j >> 1, k >> 1, ch, q);
 #pragma unroll
   for (int m = 0; m < NC; ++m) V[m * comp + off + c] = q[m];
 }
@@ -391,7 +389,7 @@ __device__ __forceinline__ void predict_level_dev(double* V, const uint8_t* st, 
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
     // dense launches stay in this rank's rows (windowed arrays are unmapped
     // elsewhere): the region test comes before the status load
-    if (!tiles && g.dist && !row_in_region(g, lv, mr_row(D, lv, c))) return;
+    if (!tiles && g.dist && !row_in_region(g, lv, mr_row(g, D, lv, c))) return;
     predict_cell<D>(V, vmark, g, lv, c, st[g.cell_off[lv] + c], lo, hi, false);
   });
 }
@@ -434,7 +432,7 @@ __device__ __forceinline__ void node_child_entry(const MRLevels& g, int l, int t
   const int item = r * 256 + (int)threadIdx.x, tn = item >> D;
   const int x = x0 + tn % TX, y = y0 + (tn / TX) % TY, z = D == 3 ? z0 + tn / (TX * TY) : 0;
   *valid = x < n && y < n && (D == 2 || z < n);
-  *c = *valid ? mr_idx(D, n, x, y, z) : 0L;
+  *c = *valid ? mr_idx(g, D, n, x, y, z) : 0L;
   *ch = item & (NCH - 1);
 }
 
@@ -501,13 +499,13 @@ __device__ __forceinline__ double child_detail(const double* V, long comp, const
   const int n = 1 << l, nf = n << 1;
   const long off = g.cell_off[l], foff = g.cell_off[l + 1];
   // the child's own values first: their loads overlap the stencil's
-  const long fc = foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+  const long fc = foff + mr_idx(g, D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                                 D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
   double cv[NC];
 #pragma unroll
   for (int m = 0; m < NC; ++m) cv[m] = V[m * comp + fc];
   double pred[NC];
-  predict_child<D>(V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
+  predict_child<D>(g, V, comp, off, n, g.bc[0], g.bc[2], g.bc[4], i, j, k, ch, pred);
   double mag = 0.0;
 #pragma unroll
   for (int m = 0; m < NC; ++m) {
@@ -534,9 +532,10 @@ __global__ void mr_detail_level(const double* V, const uint8_t* st, double* det,
     const int n = 1 << l;
     const long off = g.cell_off[l];
     const bool internal = valid && st[off + c] == ST_INTERNAL;
-    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
+    int i, j, k;
+  mr_ijk(g, D, l, c, i, j, k);
     const long fc = g.cell_off[l + 1] +
-                    mr_idx(D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+                    mr_idx(g, D, n << 1, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                            D == 3 ? 2 * k + ((ch >> 2) & 1) : 0);
     // refine reads the details of the parents of splittable leaves only
     const bool split_leaf = flag && internal && l + 1 <= g.L - 1 && st[fc] == ST_LEAF;
@@ -567,7 +566,8 @@ __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t*
     const long cells = mr_cells(D, l), off = g.cell_off[l];
     uint8_t f = flag[off + c];
     if (!f && st[off + c] == ST_LEAF) {
-      const int t[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+      int t[3];
+      mr_ijk(g, D, l, c, t[0], t[1], t[2]);
       const int rz = D == 3 ? r : 0;
       for (int dk = -rz; dk <= rz && !f; ++dk)
         for (int dj = -r; dj <= r && !f; ++dj)
@@ -582,7 +582,7 @@ __global__ void mr_dilate_level(const uint8_t* st, const uint8_t* flag, uint8_t*
               else
                 ok = false;
             }
-            if (ok && flag[off + mr_idx(D, n, s[0], s[1], s[2])] == 1) f = 2;
+            if (ok && flag[off + mr_idx(g, D, n, s[0], s[1], s[2])] == 1) f = 2;
           }
     }
     flag2[off + c] = f;
@@ -598,11 +598,12 @@ __global__ void mr_apply_split_level(uint8_t* st, const uint8_t* flag, MRLevels 
     const int l = lv_;
     const int n = 1 << l, nf = n << 1;
     const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
-    if (!flag[off + c] || st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(D, l, c))) return;
-    const int i = (int)(c & (n - 1)), j = (int)((c >> l) & (n - 1)), k = D == 3 ? (int)(c >> (2 * l)) : 0;
+    if (!flag[off + c] || st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(g, D, l, c))) return;
+    int i, j, k;
+  mr_ijk(g, D, l, c, i, j, k);
     st[off + c] = ST_INTERNAL;
     for (int ch = 0; ch < (1 << D); ++ch)
-      st[foff + mr_idx(D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
+      st[foff + mr_idx(g, D, nf, 2 * i + (ch & 1), 2 * j + ((ch >> 1) & 1),
                        D == 3 ? 2 * k + ((ch >> 2) & 1) : 0)] = ST_LEAF;
     *changed = 1;
   });
@@ -622,8 +623,8 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
     const long cells = mr_cells(D, l), off = g.cell_off[l], foff = g.cell_off[l + 1];
     uint8_t need = 0;
     if (st[off + c] == ST_LEAF && l < g.L) {
-      const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)),
-                          D == 3 ? (int)(c >> (2 * l)) : 0};
+      int idx[3];
+      mr_ijk(g, D, l, c, idx[0], idx[1], idx[2]);
       for (int a = 0; a < D && !need; ++a)
         for (int dir = -1; dir <= 1 && !need; dir += 2) {
           int p[3] = {idx[0], idx[1], idx[2]};
@@ -632,7 +633,7 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
           if (!per && (p[a] < 0 || p[a] >= n)) continue;
           bool fl;
           p[a] = mr_map(p[a], n, g.bc[2 * a], g.bc[2 * a + 1], fl);
-          if (st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_INTERNAL) continue;
+          if (st[off + mr_idx(g, D, n, p[0], p[1], p[2])] != ST_INTERNAL) continue;
           const int face_bit = dir > 0 ? 0 : 1;
           const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
           const int tzn = D == 3 ? 2 : 1;
@@ -642,7 +643,7 @@ __global__ void mr_grade_flag_level(const uint8_t* st, uint8_t* flag, MRLevels g
               ci[a] = 2 * p[a] + face_bit;
               ci[b1] = 2 * p[b1] + t1;
               ci[b2] = D == 3 ? 2 * p[b2] + t2 : 0;
-              if (st[foff + mr_idx(D, nf, ci[0], ci[1], ci[2])] == ST_INTERNAL) need = 1;
+              if (st[foff + mr_idx(g, D, nf, ci[0], ci[1], ci[2])] == ST_INTERNAL) need = 1;
             }
         }
     }
@@ -661,15 +662,16 @@ __device__ __forceinline__ void coarsen_node(const double* V, uint8_t* st, const
                                              long c, bool valid, int ch, const double* rpre) {
   const int n = 1 << l, nf = n << 1;
   const long off = g.cell_off[l], foff = g.cell_off[l + 1];
-  const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+  int idx[3];
+      mr_ijk(g, D, l, c, idx[0], idx[1], idx[2]);
   int cc[3];
   cc[0] = 2 * idx[0] + (ch & 1);
   cc[1] = 2 * idx[1] + ((ch >> 1) & 1);
   cc[2] = D == 3 ? 2 * idx[2] + ((ch >> 2) & 1) : 0;
-  const long fc = foff + mr_idx(D, nf, cc[0], cc[1], cc[2]);
+  const long fc = foff + mr_idx(g, D, nf, cc[0], cc[1], cc[2]);
   // candidate: INTERNAL node whose children are all leaves (mr_tree.cpp:486-497)
   const bool cand = node_group_all<D>(valid && st[off + c] == ST_INTERNAL && st[fc] == ST_LEAF &&
-                                      row_owned(g, l, mr_row(D, l, c)));
+                                      row_owned(g, l, mr_row(g, D, l, c)));
   double r = 0.0;
   if (rpre) {
     r = *rpre;  // computed before the PDL wait for every INTERNAL node
@@ -690,7 +692,7 @@ __device__ __forceinline__ void coarsen_node(const double* V, uint8_t* st, const
       if (!per && (q[a] < 0 || q[a] >= nf)) continue;
       bool fl;
       q[a] = mr_map(q[a], nf, g.bc[2 * a], g.bc[2 * a + 1], fl);
-      if (st[foff + mr_idx(D, nf, q[0], q[1], q[2])] == ST_INTERNAL) allowed = false;
+      if (st[foff + mr_idx(g, D, nf, q[0], q[1], q[2])] == ST_INTERNAL) allowed = false;
     }
   }
   const bool merge = node_group_all<D>(cand && r < eps && allowed);
@@ -746,10 +748,10 @@ __device__ __forceinline__ void coarsen_node(const double* V, uint8_t* st, const
           for (int tx = 0; tx < 4; ++tx) {
             if (!(okp[0][tx] && okp[1][ty] && okp[2][tz])) continue;
             const int q0 = pos[0][tx], q1 = pos[1][ty], q2 = pos[2][tz];
-            if (st[foff + mr_idx(D, nf, q0, q1, q2)] != ST_INTERNAL) continue;
+            if (st[foff + mr_idx(g, D, nf, q0, q1, q2)] != ST_INTERNAL) continue;
             bool all = true;
             for (int c2 = 0; c2 < (1 << D) && all; ++c2)
-              all = st[ffoff + mr_idx(D, nff, 2 * q0 + (c2 & 1), 2 * q1 + ((c2 >> 1) & 1),
+              all = st[ffoff + mr_idx(g, D, nff, 2 * q0 + (c2 & 1), 2 * q1 + ((c2 >> 1) & 1),
                                       D == 3 ? 2 * q2 + ((c2 >> 2) & 1) : 0)] == ST_LEAF;
             hit = hit || all;
           }
@@ -795,9 +797,11 @@ __global__ void mr_coarsen_level(const double* V, uint8_t* st, MRLevels g, int l
     const int ti = blockIdx.x / NCH;
     node_child_entry<D>(g, l, tiles[ti], blockIdx.x - ti * NCH, &c0, &valid0, &ch0);
     const int n = 1 << l;
-    if (valid0 && st[g.cell_off[l] + c0] == ST_INTERNAL)
-      r0 = child_detail<D>(V, g.total_cells, g, l, (int)(c0 & (n - 1)), (int)((c0 >> l) & (n - 1)),
-                           D == 3 ? (int)(c0 >> (2 * l)) : 0, ch0, norms);
+    if (valid0 && st[g.cell_off[l] + c0] == ST_INTERNAL) {
+      int i0, j0, k0;
+      mr_ijk(g, D, l, c0, i0, j0, k0);
+      r0 = child_detail<D>(V, g.total_cells, g, l, i0, j0, k0, ch0, norms);
+    }
     r0 = node_group_max<D>(r0);
   }
   AF_PDL_ENTRY();
@@ -863,7 +867,8 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
     const int n = 1 << l, pn = n >> 1;
     const long cells = mr_cells(D, l), off = g.cell_off[l], poff = g.cell_off[l - 1];
     if (st[off + c] != ST_LEAF) return;
-    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+    int idx[3];
+      mr_ijk(g, D, l, c, idx[0], idx[1], idx[2]);
     for (int a = 0; a < D; ++a)
       for (int o = -2; o <= 2; ++o) {
         if (o == 0) continue;
@@ -873,8 +878,8 @@ __global__ void mr_virtual_mark_level(const uint8_t* st, uint8_t* mark, MRLevels
         if (!per && (p[a] < 0 || p[a] >= n)) continue;
         bool fl;
         p[a] = mr_map(p[a], n, g.bc[2 * a], g.bc[2 * a + 1], fl);
-        if (st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_ABSENT) continue;
-        const long pc = poff + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+        if (st[off + mr_idx(g, D, n, p[0], p[1], p[2])] != ST_ABSENT) continue;
+        const long pc = poff + mr_idx(g, D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
         if (st[pc] == ST_LEAF && row_owned(g, l - 1, p[D - 1] >> 1)) mark[pc] = 1;
       }
   });
@@ -890,7 +895,7 @@ static __global__ void mr_count_kernel(const uint8_t* st, const uint8_t* mark, l
     if (g.dist) {  // count each cell on one rank only
       int l = 0;
       while (c >= g.cell_off[l + 1]) ++l;
-      if (!row_counted(g, l, mr_row(g.dim, l, c - g.cell_off[l]))) continue;
+      if (!row_counted(g, l, mr_row(g, g.dim, l, c - g.cell_off[l]))) continue;
     }
     const uint8_t s = st[c];
     lv += s == ST_LEAF;
@@ -961,7 +966,7 @@ __global__ void mr_leaf_speed_kernel(const double* V, const uint8_t* st, MRLevel
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv_, long c) {
     const int l = lv_;
     const long off = g.cell_off[l], comp = g.total_cells;
-    if (st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(D, l, c))) return;
+    if (st[off + c] != ST_LEAF || !row_owned(g, l, mr_row(g, D, l, c))) return;
     Cons<D> q;
     q.rho = V[off + c];
 #pragma unroll
@@ -985,7 +990,7 @@ __global__ void mr_norm_kernel(const double* V, MRLevels g, unsigned long long* 
   for (int m = 0; m < NC; ++m) mx[m] = 0.0;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
-    if (g.dist && !row_owned(g, g.L, mr_row(D, g.L, c))) continue;  // max over ranks after
+    if (g.dist && !row_owned(g, g.L, mr_row(g, D, g.L, c))) continue;  // max over ranks after
 #pragma unroll
     for (int m = 0; m < NC; ++m) mx[m] = fmax(mx[m], fabs(V[m * comp + off + c]));
   }

@@ -75,14 +75,14 @@ __device__ __forceinline__ Cons<D> resolve_at(const double* V, long comp, const 
   const int mi = mr_map(i, n, g.bc[0], g.bc[1], fi);
   const int mj = mr_map(j, n, g.bc[2], g.bc[3], fj);
   const int mk = D == 3 ? mr_map(k, n, g.bc[4], g.bc[5], fk) : 0;
-  const long c = g.cell_off[l] + mr_idx(D, n, mi, mj, mk);
+  const long c = g.cell_off[l] + mr_idx(g, D, n, mi, mj, mk);
   Cons<D> q;
   q.rho = V[c];
 #pragma unroll
   for (int a = 0; a < D; ++a) q.m[a] = V[(1 + a) * comp + c];
   q.E = V[(D + 1) * comp + c];
   if (lt && l - 1 < lt->lo && l >= 1) {
-    const long pc = g.cell_off[l - 1] + mr_idx(D, n >> 1, mi >> 1, mj >> 1, mk >> 1);
+    const long pc = g.cell_off[l - 1] + mr_idx(g, D, n >> 1, mi >> 1, mj >> 1, mk >> 1);
     // a virtual leaf over an already-advanced coarser leaf: interpolate in time
     if (lt->vmark[pc] && lt->st[c] == ST_ABSENT) {
       const double th = lt->theta[l - 1], om = 1.0 - th;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
   // leaf mask of the tile cells
   const int cx = x0 + tx, cy = y0 + ty, cz = z0 + tz;
   const bool inside = cx < n && cy < n && (D == 2 || cz < n);
-  const long own = inside ? off + mr_idx(D, n, cx, cy, cz) : 0;
+  const long own = inside ? off + mr_idx(g, D, n, cx, cy, cz) : 0;
   // A full tile (mr_tile_flags_all bit 2): every cell and every face
   // neighbour of the tile is a leaf of this level, so every face is a plain
   // same-level face (no fine sub-face average, no flux register) and every
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         p[ax] += side ? 1 : -1;
         bool flp;
         p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
-        nbst |= (unsigned)a.st[off + mr_idx(D, n, p[0], p[1], p[2])] << (2 * (ax * 2 + side));
+        nbst |= (unsigned)a.st[off + mr_idx(g, D, n, p[0], p[1], p[2])] << (2 * (ax * 2 + side));
       }
   }
   __syncthreads();
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
     const int mx = mr_map(x, n, g.bc[0], g.bc[1], f);
     const int my = mr_map(y, n, g.bc[2], g.bc[3], f);
     const int mz = D == 3 ? mr_map(z, n, g.bc[4], g.bc[5], f) : 0;
-    return a.st[off + mr_idx(D, n, mx, my, mz)];
+    return a.st[off + mr_idx(g, D, n, mx, my, mz)];
   };
   const bool fine_ok = l + 1 <= a.hi;  // the finer level steps in this call
   // Face fluxes needed by a leaf of the tile. A face between a leaf and an
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
               }
             } else if (nst == ST_ABSENT && l >= 1 && l - 1 < a.lo) {
               const int pn = n >> 1;
-              const long pc = g.cell_off[l - 1] + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+              const long pc = g.cell_off[l - 1] + mr_idx(g, D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
               // (a coarse cell of another rank gets this share from its owner)
               if (a.vmark[pc] && row_owned(g, l - 1, p[D - 1] >> 1)) {
                 // face into an already-advanced coarser cell: fine register share
@@ -497,10 +497,10 @@ __global__ void __launch_bounds__(TX* TY* TZ, 2)
         p[ax] += dir;
         bool flp;
         p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], flp);
-        if (a.st[off + mr_idx(D, n, p[0], p[1], p[2])] != ST_ABSENT || l < 1 || l - 1 >= a.lo)
+        if (a.st[off + mr_idx(g, D, n, p[0], p[1], p[2])] != ST_ABSENT || l < 1 || l - 1 >= a.lo)
           continue;
         const int pn = n >> 1;
-        const long pc = g.cell_off[l - 1] + mr_idx(D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
+        const long pc = g.cell_off[l - 1] + mr_idx(g, D, pn, p[0] >> 1, p[1] >> 1, p[2] >> 1);
         if (!a.vmark[pc] || !row_owned(g, l - 1, p[D - 1] >> 1)) continue;
         int fi;
         if (ax == 0) fi = (tz * TY + ty) * (TX + 1) + tx + (dir > 0);
@@ -554,17 +554,18 @@ __global__ void mr_reg_build_level(const uint8_t* st, MRLevels g, int l, int* re
   const long cells = mr_cells(D, l), off = g.cell_off[l];
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
-    if (!row_owned(g, l, mr_row(D, l, c))) continue;  // registers live with their owner
+    if (!row_owned(g, l, mr_row(g, D, l, c))) continue;  // registers live with their owner
     unsigned mask = 0;
     if (st[off + c] == ST_LEAF) {
-      const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+      int idx[3];
+      mr_ijk(g, D, l, c, idx[0], idx[1], idx[2]);
       for (int ax = 0; ax < D; ++ax)
         for (int side = 0; side < 2; ++side) {
           int p[3] = {idx[0], idx[1], idx[2]};
           p[ax] += side ? 1 : -1;
           bool fl;
           p[ax] = mr_map(p[ax], n, g.bc[2 * ax], g.bc[2 * ax + 1], fl);
-          if (st[off + mr_idx(D, n, p[0], p[1], p[2])] == ST_INTERNAL) mask |= 1u << (ax * 2 + side);
+          if (st[off + mr_idx(g, D, n, p[0], p[1], p[2])] == ST_INTERNAL) mask |= 1u << (ax * 2 + side);
         }
     }
     regmask[off + c] = (uint8_t)mask;
@@ -589,10 +590,11 @@ __global__ void mr_reg_apply_level(double* V, const uint8_t* st, MRLevels g, int
   const int nsub = D == 3 ? 4 : 2;
   for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cells;
        c += (long)gridDim.x * blockDim.x) {
-    if (!row_owned(g, l, mr_row(D, l, c))) continue;
+    if (!row_owned(g, l, mr_row(g, D, l, c))) continue;
     const unsigned mask = regmask[off + c];
     if (!mask) continue;
-    const int idx[3] = {(int)(c & (n - 1)), (int)((c >> l) & (n - 1)), D == 3 ? (int)(c >> (2 * l)) : 0};
+    int idx[3];
+      mr_ijk(g, D, l, c, idx[0], idx[1], idx[2]);
     const unsigned long long key = ((unsigned long long)l << 45) |
                                    ((unsigned long long)idx[0] << 30) |
                                    ((unsigned long long)idx[1] << 15) | (unsigned long long)idx[2];
@@ -685,14 +687,14 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
         notleaf = true;
         continue;
       }
-      const uint8_t s = st[g.cell_off[l] + mr_idx(D, n, x, y, z)];
+      const uint8_t s = st[g.cell_off[l] + mr_idx(g, D, n, x, y, z)];
       const bool lf = s == ST_LEAF;
       notleaf = notleaf || !lf;
       absent = absent || s == ST_ABSENT;
       nleaf += lf && row_counted(g, l, D == 3 ? z : y);
       rleaf = rleaf || (lf && row_in_region(g, l, D == 3 ? z : y));
       pex = pex || l == 0 ||
-            st[g.cell_off[l - 1] + mr_idx(D, n >> 1, x >> 1, y >> 1, z >> 1)] != ST_ABSENT;
+            st[g.cell_off[l - 1] + mr_idx(g, D, n >> 1, x >> 1, y >> 1, z >> 1)] != ST_ABSENT;
     }
     for (int o = 16; o > 0; o >>= 1) nleaf += __shfl_xor_sync(0xffffffffu, nleaf, o);
     pex = __any_sync(0xffffffffu, pex);
@@ -717,7 +719,7 @@ __global__ void mr_tile_flags_all(const uint8_t* st, MRLevels g, uint8_t* tflag,
         q[b2] = D == 3 ? ((b2 == 1 ? y0 : z0) + r / T[b1]) : 0;
         bool f;
         for (int d = 0; d < D; ++d) q[d] = mr_map(q[d], n, g.bc[2 * d], g.bc[2 * d + 1], f);
-        const uint8_t s = st[g.cell_off[l] + mr_idx(D, n, q[0], q[1], q[2])];
+        const uint8_t s = st[g.cell_off[l] + mr_idx(g, D, n, q[0], q[1], q[2])];
         ok = ok && s == ST_LEAF;
         nint = nint && s != ST_INTERNAL;
       }
@@ -840,7 +842,7 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
       const long comp = g.total_cells;
       level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
         const long off = g.cell_off[lv];
-        if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(D, lv, c))) return;
+        if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(g, D, lv, c))) return;
 #pragma unroll
         for (int m = 0; m < D + 2; ++m) {
           const double t = dst[m * comp + off + c];
@@ -854,7 +856,7 @@ __global__ void mr_copy_leaves_tiles(const double* src, double* dst, const uint8
   const long comp = g.total_cells;
   level_cells<D>(g, l, tiles, ntiles, [&](const int lv, long c) {
     const long off = g.cell_off[lv];
-    if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(D, lv, c))) return;
+    if (st[off + c] != ST_LEAF || !row_owned(g, lv, mr_row(g, D, lv, c))) return;
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) dst[m * comp + off + c] = src[m * comp + off + c];
   });
@@ -896,7 +898,7 @@ __global__ void mr_tile_list_kernel(const uint8_t* st, MRLevels g, int l, int* t
     bool any = false;
     for (int c = threadIdx.x & 31; c < TX * TY * TZ; c += 32) {
       const int x = x0 + c % TX, y = y0 + (c / TX) % TY, z = z0 + (D == 3 ? c / (TX * TY) : 0);
-      if (x < n && y < n && (D == 2 || z < n) && st[off + mr_idx(D, n, x, y, z)] == ST_LEAF)
+      if (x < n && y < n && (D == 2 || z < n) && st[off + mr_idx(g, D, n, x, y, z)] == ST_LEAF)
         any = true;
     }
     any = __any_sync(0xffffffffu, any);

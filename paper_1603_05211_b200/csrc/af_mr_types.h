@@ -34,11 +34,61 @@ struct MRLevels {
   int lp;
   int count_rep;
   int dist;                // more than one rank
+  // Cell order inside a level (af_mr_storage.cu). bsh = 0: row-major (x
+  // fastest). bsh > 0 (3D only): levels finer than 2^bsh cells per axis are
+  // stored as dense bricks of 2^bsh cells per axis, brick after brick
+  // (bricks row-major, cells row-major inside a brick), so one brick of one
+  // component is one contiguous, page-aligned run that is mapped to physical
+  // memory only while the tree reaches it (AF_MR_STORAGE_SPARSE).
+  int bsh;
 };
 
 
+__host__ __device__ __forceinline__ int mr_log2(int n) {
+#ifdef __CUDA_ARCH__
+  return __ffs(n) - 1;
+#else
+  return __builtin_ctz((unsigned)n);
+#endif
+}
+
+// Index of cell (i, j, k) inside its level (n = 2^l cells per axis): row-major,
+// or brick-major above the brick size (MRLevels::bsh).
+__host__ __device__ __forceinline__ long mr_idx(const MRLevels& g, int D, int n, int i, int j,
+                                                int k) {
+  if (D == 3 && g.bsh && n > (1 << g.bsh)) {
+    const int s = g.bsh, m = (1 << s) - 1, ls = mr_log2(n) - s;  // log2 bricks per axis
+    const long b = ((long)(k >> s) << (2 * ls)) | ((long)(j >> s) << ls) | (i >> s);
+    return (b << (3 * s)) | ((long)(k & m) << (2 * s)) | ((j & m) << s) | (i & m);
+  }
+  return D == 3 ? ((long)k * n + j) * n + i : (long)j * n + i;
+}
+
+// Inverse of mr_idx at level l.
+__host__ __device__ __forceinline__ void mr_ijk(const MRLevels& g, int D, int l, long c, int& i,
+                                                int& j, int& k) {
+  const int n = 1 << l;
+  if (D == 3 && g.bsh && l > g.bsh) {
+    const int s = g.bsh, m = (1 << s) - 1, ls = l - s, nb = (1 << ls) - 1;
+    const long b = c >> (3 * s);
+    const int in = (int)(c & ((1L << (3 * s)) - 1));
+    i = (int)((b & nb) << s) | (in & m);
+    j = (int)(((b >> ls) & nb) << s) | ((in >> s) & m);
+    k = (int)((b >> (2 * ls)) << s) | (in >> (2 * s));
+    return;
+  }
+  i = (int)(c & (n - 1));
+  j = (int)((c >> l) & (n - 1));
+  k = D == 3 ? (int)(c >> (2 * l)) : 0;
+}
+
 // Slab row of cell c of level l (the last axis index).
-__host__ __device__ __forceinline__ int mr_row(int dim, int l, long c) {
+__host__ __device__ __forceinline__ int mr_row(const MRLevels& g, int dim, int l, long c) {
+  if (dim == 3 && g.bsh && l > g.bsh) {
+    int i, j, k;
+    mr_ijk(g, dim, l, c, i, j, k);
+    return k;
+  }
   return (int)(c >> ((dim - 1) * l));
 }
 __host__ __device__ __forceinline__ bool row_owned(const MRLevels& g, int l, int r) {

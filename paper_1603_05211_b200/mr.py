@@ -31,6 +31,11 @@ class MROptions:
     min_leaf_level: int = 0
     local_time: bool = False
     local_time_level_gap: int = 3
+    # storage of the level arrays (af_gpu.h AF_MR_STORAGE_*): "dense" per-level
+    # grids, "bricks" (3D brick layout, fully allocated) or "sparse" (3D bricks
+    # mapped only where the tree reaches); bit-identical results
+    storage: str = "dense"
+    brick_shift: int = 0
 
 
 @dataclass
@@ -55,6 +60,9 @@ class MRReport:
     def cells_per_step(self):
         c = self.cycles
         return np.repeat(c[:, 1], c[:, 2].astype(np.int64))
+
+
+STORAGE = {"dense": 0, "bricks": 1, "sparse": 2}
 
 
 def eps_levels_scaled(eps: float, level: int, dim: int) -> list:
@@ -89,6 +97,10 @@ class MRSolver:
         o.min_leaf_level = options.min_leaf_level
         o.local_time = int(options.local_time)
         o.lt_gap = options.local_time_level_gap
+        if options.storage not in STORAGE:
+            raise ValueError(f"storage must be one of {sorted(STORAGE)}")
+        o.storage = STORAGE[options.storage]
+        o.brick_shift = options.brick_shift
         h = C.c_void_p()
         if comm is None:
             st = self._lib.af_mr_create(C.byref(cfg), C.byref(o), C.byref(h))
@@ -121,6 +133,12 @@ class MRSolver:
     def set_stream(self, stream):
         raw = getattr(stream, "cuda_stream", stream)
         self._check(self._lib.af_mr_set_stream(self._h, C.c_void_p(raw)))
+
+    def memory(self) -> dict:
+        """Device bytes of the per-cell arrays: now, peak, and as dense level grids."""
+        v = [C.c_ulonglong() for _ in range(3)]
+        self._check(self._lib.af_mr_memory(self._h, *[C.byref(x) for x in v]))
+        return {"now": v[0].value, "peak": v[1].value, "dense": v[2].value}
 
     def kernel_launches(self) -> int:
         c = C.c_long()
