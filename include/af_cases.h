@@ -162,6 +162,32 @@ static inline int af_cases_fill(int kind, uint64_t seed, int level, double gamma
   return 0;
 }
 
+/*
+ * The same initial data as a function of position (an AMR hierarchy samples
+ * the initial condition at the cell centres of every level): the quadrant or
+ * ellipsoid state at (x, y, z) of the unit domain. The per-cell noise of
+ * AF_CASE_QUADRANTS_NOISE has no position form: returns -1 for it.
+ */
+static inline int af_case_point(int kind, const af_case_params* cp, double gamma, double x,
+                                double y, double z, double* q) {
+  if (kind == AF_CASE_QUADRANTS) {
+    const int quad = (x > 0.5 ? 1 : 0) + 2 * (y > 0.5 ? 1 : 0);
+    af_conserved(cp->quad[quad][0], cp->quad[quad][1], cp->quad[quad][2], 0.0, cp->quad[quad][3],
+                 gamma, q);
+    return 0;
+  }
+  if (kind == AF_CASE_ELLIPSOID || kind == AF_CASE_ELLIPSOID_PRATIO) {
+    const double ex = (x - 0.5) / cp->semi[0];
+    const double ey = (y - 0.5) / cp->semi[1];
+    const double ez = (z - 0.5) / cp->semi[2];
+    const int inside = (ex * ex + ey * ey + ez * ez) < 1.0;
+    af_conserved(inside ? cp->rho_in : cp->rho_out, 0.0, 0.0, 0.0, inside ? cp->p_in : cp->p_out,
+                 gamma, q);
+    return 0;
+  }
+  return -1;
+}
+
 #ifdef __cplusplus
 }
 #endif

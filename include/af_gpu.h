@@ -349,6 +349,81 @@ typedef struct af_rates {
 af_status af_rates_compute(const af_run_summary* adaptive, const af_run_summary* fv, double n_c,
                            af_rates* out);
 
+/* ------------------------------------------------------- AMR patch path -- */
+/* Block-structured patch hierarchy with factor-2 refinement, the paper's
+ * comparison method: PatchHierarchy (amr.hpp:123-242,
+ * amr_hierarchy.cpp), flag_cells and cluster (amr.hpp:100-111,
+ * amr_cluster.cpp) and the run_amr cycle (amr_solver.hpp:34-35,
+ * amr_solver.cpp). af_config.level is the base mesh exponent (level l has
+ * 2^(level + l) cells per axis); flux/limiter/integrator select the scheme
+ * update_level steps with (MUSCL-Hancock or the two-stage RK2). Patch data
+ * stay on the device; box lists and level times live on the host; the
+ * clustering runs on the host on the downloaded flag mask. Results are
+ * bit-identical to the reference (tests/test_amr_gpu.py). */
+typedef struct af_amr af_amr;
+
+/* AmrOptions (amr.hpp:113-120) */
+typedef struct af_amr_options {
+  double eps_rho;            /* scaled-gradient thresholds (flag_cells) */
+  double eps_p;
+  double cluster_efficiency; /* minimum flagged/total of a box */
+  int time_refine;           /* 1: halve dt per level (AMRLT) */
+  int flux_correction;       /* 1: conservative coarse-fine flux replacement */
+  int max_levels;            /* refinement levels above the base mesh */
+} af_amr_options;
+
+/* The initial condition PatchHierarchy::initialize takes (amr.hpp:146):
+ * writes the conserved state (rho, mom[3], rhoE) at a cell centre. Called on
+ * the host for the cells of every new patch. */
+typedef void (*af_amr_ic)(double x, double y, double z, double* q5, void* user);
+
+af_status af_amr_create(const af_config* cfg, const af_amr_options* opt, af_amr** out);
+af_status af_amr_destroy(af_amr* h);
+/* initialize (amr_hierarchy.cpp:107-131) */
+af_status af_amr_initialize(af_amr* h, af_amr_ic ic, void* user);
+/* initialize with the seeded case of include/af_cases.h sampled at the cell
+ * centres (af_case_point; the quadrant and ellipsoid kinds) */
+af_status af_amr_initialize_case(af_amr* h, int kind, uint64_t seed, double gamma);
+/* sync_ghosts / remesh / update_level / average_down / flux_correct
+ * (amr.hpp:148-175). update_level synchronises when diag is non-NULL. */
+af_status af_amr_sync_ghosts(af_amr* h, int level, double tau);
+af_status af_amr_remesh(af_amr* h, int level);
+af_status af_amr_update_level(af_amr* h, int level, double dt, af_step_diag* diag);
+af_status af_amr_average_down(af_amr* h, int level);
+af_status af_amr_flux_correct(af_amr* h, int level);
+/* run_amr's cycle loop (amr_solver.cpp:24-60,107-131) after initialize:
+ * n_steps finest-level steps of size dt_finest (a multiple of 2^max_levels
+ * when time-refined, ConfigError otherwise); cells_per_step/leaves_per_step
+ * (n_steps entries, nullable) = RunReport's samples; diag: max_cfl, fallbacks. */
+af_status af_amr_run(af_amr* h, long n_steps, double dt_finest, long* cells_per_step,
+                     long* leaves_per_step, af_run_diag* diag);
+af_status af_amr_n_levels(const af_amr* h, int* n);
+af_status af_amr_level_info(const af_amr* h, int level, int* n_patches, long* cells, double* t,
+                            double* t_old);
+/* the level's boxes, 6 ints each (lo[3], hi[3]), in patch order */
+af_status af_amr_boxes(const af_amr* h, int level, int* boxes6, int capacity);
+/* Patch payloads of a level, patch after patch, AoS x fastest: ghost = 0 the
+ * interiors, 2 the blocks with their ghost layers as each patch holds them
+ * (Patch::data, amr.hpp:115-118); old = 1: Patch::data_old. aos: host or device. */
+af_status af_amr_patch_data_cells(const af_amr* h, int level, int ghost, long* cells);
+af_status af_amr_patch_data(af_amr* h, int level, int ghost, int old, double* aos);
+/* assemble_level (amr_hierarchy.cpp:600-616): AF_E_LEVEL_MISMATCH unless the
+ * level covers the domain */
+af_status af_amr_assemble_level(af_amr* h, int level, double* aos);
+/* total_conserved (amr_hierarchy.cpp:561-581); device tree sums, so equal to
+ * the reference's sequential sums to round-off, not bitwise */
+af_status af_amr_total_conserved(af_amr* h, double out5[5]);
+af_status af_amr_counts(const af_amr* h, long* total_cells, long* composite_cells);
+af_status af_amr_properly_nested(af_amr* h, int* nested);
+/* dump_boxes (amr_hierarchy.cpp:618-629); the text stays valid until the next call */
+af_status af_amr_dump_boxes(af_amr* h, const char** text);
+af_status af_amr_last_error(const af_amr* h, af_error* err);
+af_status af_amr_kernel_launches(const af_amr* h, long* count);
+/* cluster (amr.hpp:110-111): flags/allowed are n0*n1*n2 bytes, x fastest
+ * (allowed nullable); boxes6 nullable to query the count. Host integer work. */
+af_status af_amr_cluster(const unsigned char* flags, const unsigned char* allowed, int dim, int n0,
+                         int n1, int n2, double efficiency, int* boxes6, int capacity, int* n_boxes);
+
 /* Self-check of the inline fast-path division and square root the face
  * fluxes use (CUDA's fast-path sequences with their range tests; see
  * DESIGN.md §3) against IEEE a/b and sqrt on n random operands with binary

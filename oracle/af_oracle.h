@@ -103,6 +103,46 @@ int afo_mr_last_dump(const char* path);
 int afo_case_fill(int kind, uint64_t seed, int level, double gamma, int z0, int nz,
                   double* out);
 
+/* ---- AMR patch path (amr.hpp, amr_solver.hpp), reference side ---- */
+typedef struct af_amr_ref_params {
+  int dim;
+  int level;      /* finest resolution level */
+  int base_exp;   /* base mesh exponent (max_levels = level - base_exp) */
+  int bc[6];
+  int limiter, flux, integrator;
+  double gamma;
+  long n_steps;      /* finest-level steps */
+  double dt_finest;
+  double eps_rho, eps_p, efficiency;
+  int time_refine, flux_correction;
+  int case_kind;     /* include/af_cases.h kind sampled by af_case_point */
+  uint64_t seed;
+  /* 0: the harness loop (PatchHierarchy::initialize with the seeded point
+   *    function, then AmrDriver::advance restated on the public methods);
+   * 1: the same loop on the built-in case `builtin_name` (its initial_state,
+   *    bc and gas; base_exp = amr_base_exp; dt = t_end / n_steps);
+   * 2: the reference's own run_amr on that built-in case. 1 and 2 must agree
+   *    bit for bit, which pins the restated loop. */
+  int mode;
+  const char* builtin_name;
+} af_amr_ref_params;
+
+/* Runs and keeps the hierarchy for the accessors below. res: max_cfl,
+ * fallbacks, err. cells/leaves_per_step: n_steps longs (nullable). */
+int afref_amr_run(const af_amr_ref_params* p, long* cells_per_step, long* leaves_per_step,
+                  af_oracle_result* res);
+int afref_amr_n_levels(void);
+int afref_amr_n_patches(int level);
+int afref_amr_boxes(int level, int* boxes6);
+double afref_amr_time(int level, int old);
+/* patch after patch, AoS x fastest; ghost 0 interiors / 2 blocks with ghosts; old: data_old */
+long afref_amr_patch_data(int level, int ghost, int old, double* aos);
+int afref_amr_total_conserved(double* out5);
+int afref_amr_dump_boxes(char* buf, long cap);
+/* cluster (amr.hpp:110-111) on an n x n (x n) mask; returns the box count */
+int afref_cluster(const unsigned char* flags, const unsigned char* allowed, int dim, int n,
+                  double efficiency, int* boxes6, int capacity);
+
 #ifdef __cplusplus
 }
 #endif

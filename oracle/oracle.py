@@ -283,3 +283,99 @@ def rates(adaptive: dict, fv: dict, n_c: float):
         return None, err.value.decode()
     keys = ["cpu_compression", "memory_compression", "mesh_compression", "perturbation", "overhead"]
     return dict(zip(keys, out.tolist())), None
+
+
+# ---- AMR patch path, reference side (ref_harness.cpp) ----------------------
+class AmrRefParams(C.Structure):
+    _fields_ = [("dim", C.c_int), ("level", C.c_int), ("base_exp", C.c_int), ("bc", C.c_int * 6),
+                ("limiter", C.c_int), ("flux", C.c_int), ("integrator", C.c_int),
+                ("gamma", C.c_double), ("n_steps", C.c_long), ("dt_finest", C.c_double),
+                ("eps_rho", C.c_double), ("eps_p", C.c_double), ("efficiency", C.c_double),
+                ("time_refine", C.c_int), ("flux_correction", C.c_int), ("case_kind", C.c_int),
+                ("seed", C.c_uint64), ("mode", C.c_int), ("builtin_name", C.c_char_p)]
+
+
+def _amr_lib():
+    lib = _load("ref")
+    if not getattr(lib, "_amr_ready", False):
+        dp = C.POINTER(C.c_double)
+        lp = C.POINTER(C.c_long)
+        ip = C.POINTER(C.c_int)
+        lib.afref_amr_run.argtypes = [C.POINTER(AmrRefParams), lp, lp, C.POINTER(Result)]
+        lib.afref_amr_run.restype = C.c_int
+        lib.afref_amr_n_levels.restype = C.c_int
+        lib.afref_amr_n_patches.argtypes = [C.c_int]
+        lib.afref_amr_n_patches.restype = C.c_int
+        lib.afref_amr_boxes.argtypes = [C.c_int, ip]
+        lib.afref_amr_boxes.restype = C.c_int
+        lib.afref_amr_time.argtypes = [C.c_int, C.c_int]
+        lib.afref_amr_time.restype = C.c_double
+        lib.afref_amr_patch_data.argtypes = [C.c_int, C.c_int, C.c_int, dp]
+        lib.afref_amr_patch_data.restype = C.c_long
+        lib.afref_amr_total_conserved.argtypes = [dp]
+        lib.afref_amr_dump_boxes.argtypes = [C.c_char_p, C.c_long]
+        lib.afref_cluster.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double, ip,
+                                      C.c_int]
+        lib.afref_cluster.restype = C.c_int
+        lib._amr_ready = True
+    return lib
+
+
+def ref_amr_run(dim, level, base_exp, n_steps, dt_finest, case_kind=0, seed=1, bc=None,
+                limiter=MINMOD, flux=0, integrator=0, gamma=1.4, eps_rho=0.05, eps_p=0.05,
+                efficiency=0.8, time_refine=True, flux_correction=True, mode=0, builtin=None):
+    """Runs the reference's AMR path (see af_oracle.h af_amr_ref_params) and
+    returns everything the parity tests compare."""
+    lib = _amr_lib()
+    p = AmrRefParams()
+    p.dim, p.level, p.base_exp = dim, level, base_exp
+    for i, b in enumerate(bc if bc is not None else [0] * 6):
+        p.bc[i] = int(b)
+    p.limiter, p.flux, p.integrator, p.gamma = limiter, flux, integrator, gamma
+    p.n_steps, p.dt_finest = n_steps, dt_finest
+    p.eps_rho, p.eps_p, p.efficiency = eps_rho, eps_p, efficiency
+    p.time_refine, p.flux_correction = int(time_refine), int(flux_correction)
+    p.case_kind, p.seed, p.mode = case_kind, seed, mode
+    p.builtin_name = builtin.encode() if builtin else None
+    cps = np.zeros(n_steps, dtype=np.int64)
+    lps = np.zeros(n_steps, dtype=np.int64)
+    res = Result()
+    lp = C.POINTER(C.c_long)
+    lib.afref_amr_run(C.byref(p), cps.ctypes.data_as(lp), lps.ctypes.data_as(lp), C.byref(res))
+    out = {"err_kind": res.err_kind, "err": res.err.decode(errors="replace"),
+           "max_cfl": res.max_cfl, "fallbacks": res.fallbacks, "wall_seconds": res.wall_seconds,
+           "cells_per_step": cps, "leaves_per_step": lps, "levels": []}
+    if res.err_kind:
+        return out
+    buf = C.create_string_buffer(1 << 22)
+    lib.afref_amr_dump_boxes(buf, len(buf))
+    out["dump_boxes"] = buf.value.decode()
+    tot = np.zeros(5)
+    lib.afref_amr_total_conserved(_dp(tot))
+    out["total_conserved"] = tot
+    for l in range(lib.afref_amr_n_levels()):
+        nb = lib.afref_amr_n_patches(l)
+        boxes = np.zeros((max(nb, 1), 6), dtype=np.int32)
+        lib.afref_amr_boxes(l, boxes.ctypes.data_as(C.POINTER(C.c_int)))
+        lv = {"boxes": boxes[:nb], "t": lib.afref_amr_time(l, 0), "t_old": lib.afref_amr_time(l, 1)}
+        for name, ghost, old in (("data", 0, 0), ("blocks", 2, 0), ("blocks_old", 2, 1)):
+            n = lib.afref_amr_patch_data(l, ghost, old, None)
+            a = np.zeros((n, 5))
+            lib.afref_amr_patch_data(l, ghost, old, _dp(a))
+            lv[name] = a
+        out["levels"].append(lv)
+    return out
+
+
+def ref_cluster(flags: np.ndarray, efficiency: float, allowed: np.ndarray | None = None):
+    """The reference's cluster() on a cubic mask indexed [z][y][x] / [y][x]."""
+    lib = _amr_lib()
+    f = np.ascontiguousarray(flags, dtype=np.uint8)
+    a = None if allowed is None else np.ascontiguousarray(allowed, dtype=np.uint8)
+    n = f.shape[-1]
+    cap = int(f.sum()) + 1
+    out = np.zeros((cap, 6), dtype=np.int32)
+    k = lib.afref_cluster(f.ctypes.data_as(C.c_char_p),
+                          None if a is None else a.ctypes.data_as(C.c_char_p), f.ndim, n,
+                          efficiency, out.ctypes.data_as(C.POINTER(C.c_int)), cap)
+    return out[:k]

@@ -70,6 +70,15 @@ class MRCycle(C.Structure):
                 ("dt", C.c_double), ("updates", C.c_long)]
 
 
+class AmrOptions(C.Structure):
+    _fields_ = [("eps_rho", C.c_double), ("eps_p", C.c_double),
+                ("cluster_efficiency", C.c_double), ("time_refine", C.c_int),
+                ("flux_correction", C.c_int), ("max_levels", C.c_int)]
+
+
+AMR_IC = C.CFUNCTYPE(None, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double), C.c_void_p)
+
+
 class SnapshotHeader(C.Structure):
     _fields_ = [("dim", C.c_int), ("level", C.c_int), ("gamma", C.c_double),
                 ("time", C.c_double), ("origin", C.c_double), ("extent", C.c_double)]
@@ -145,6 +154,31 @@ SIGNATURES = {
     "af_check_division": (C.c_int, [C.c_long, C.c_uint64, C.c_int, C.c_int,
                                     C.POINTER(C.c_ulonglong)]),
     "af_mr_dump": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_size_t)]),
+    "af_amr_create": (C.c_int, [C.POINTER(Config), C.POINTER(AmrOptions), C.POINTER(_vp)]),
+    "af_amr_destroy": (C.c_int, [_vp]),
+    "af_amr_initialize": (C.c_int, [_vp, AMR_IC, _vp]),
+    "af_amr_initialize_case": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_double]),
+    "af_amr_sync_ghosts": (C.c_int, [_vp, C.c_int, C.c_double]),
+    "af_amr_remesh": (C.c_int, [_vp, C.c_int]),
+    "af_amr_update_level": (C.c_int, [_vp, C.c_int, C.c_double, C.POINTER(StepDiag)]),
+    "af_amr_average_down": (C.c_int, [_vp, C.c_int]),
+    "af_amr_flux_correct": (C.c_int, [_vp, C.c_int]),
+    "af_amr_run": (C.c_int, [_vp, C.c_long, C.c_double, C.POINTER(C.c_long), C.POINTER(C.c_long),
+                             C.POINTER(RunDiag)]),
+    "af_amr_n_levels": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "af_amr_level_info": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_long), _dp, _dp]),
+    "af_amr_boxes": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_int), C.c_int]),
+    "af_amr_patch_data_cells": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_long)]),
+    "af_amr_patch_data": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),
+    "af_amr_assemble_level": (C.c_int, [_vp, C.c_int, _vp]),
+    "af_amr_total_conserved": (C.c_int, [_vp, _dp]),
+    "af_amr_counts": (C.c_int, [_vp, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
+    "af_amr_properly_nested": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "af_amr_dump_boxes": (C.c_int, [_vp, C.POINTER(C.c_char_p)]),
+    "af_amr_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
+    "af_amr_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+    "af_amr_cluster": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                 C.c_double, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]),
 }
 
 _lib = None

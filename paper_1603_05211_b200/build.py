@@ -18,7 +18,7 @@ LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libafgpu.so")
 
 SOURCES = ["af_abi.cu", "af_uniform.cu", "af_fv3d_tol.cu", "af_mr.cu", "af_mr_full_tol.cu",
-           "af_mr_dist.cu", "af_io.cu", "af_mr_storage.cu"]
+           "af_mr_dist.cu", "af_io.cu", "af_mr_storage.cu", "af_amr.cu"]
 # translation units compiled WITH FMA contraction (tolerance-mode kernels only)
 FMAD_TRUE = {"af_fv3d_tol.cu", "af_mr_full_tol.cu"}
 HEADERS = sorted(f for f in os.listdir(os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc"))
@@ -58,6 +58,21 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
+def _deps(src: str, seen: set | None = None) -> set:
+    """The quoted includes of a translation unit, followed recursively (csrc/ and
+    include/), so that only the objects a change reaches are recompiled."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen or not os.path.exists(src):
+        return seen
+    seen.add(src)
+    with open(src) as f:
+        for name in re.findall(r'^\s*#\s*include\s+"([^"]+)"', f.read(), re.M):
+            for base in (CSRC, os.path.join(ROOT, "include")):
+                _deps(os.path.join(base, name), seen)
+    return seen
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -72,6 +87,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        if (not force and os.path.exists(obj) and
+                all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in _deps(src))
+                and os.path.getmtime(os.path.abspath(__file__)) <= os.path.getmtime(obj)):
+            continue
         flags = list(NVCC_FLAGS)
         if os.path.basename(src) in FMAD_TRUE:
             flags[flags.index("--fmad=false")] = "--fmad=true"
