@@ -33,7 +33,10 @@ enum af_case_kind {
   AF_CASE_QUADRANTS = 0,       /* cfg1/cfg2: seeded four-quadrant Riemann problem (2D) */
   AF_CASE_QUADRANTS_NOISE = 1, /* cfg3: quadrants + rho*(1 + 0.01*U[-1,1]) per cell (2D) */
   AF_CASE_ELLIPSOID = 2,       /* cfg4: axis-aligned ellipsoid blast, p 10 | 0.1 (3D) */
-  AF_CASE_ELLIPSOID_PRATIO = 3 /* cfg5: ellipsoid, p_in/p_out ~ U[10,100], p_out 0.1 (3D) */
+  AF_CASE_ELLIPSOID_PRATIO = 3, /* cfg5: ellipsoid, p_in/p_out ~ U[10,100], p_out 0.1 (3D) */
+  AF_CASE_QUADRANTS_STRESS = 4  /* test-only: quadrants with pressures 10^U[-9,1], rho U[0.01,3],
+                                   |v| up to 3 -- drives the reconstruction / predictor
+                                   fallbacks the BASELINE configs never reach (2D, position form only) */
 };
 
 typedef struct af_rng {
@@ -87,7 +90,17 @@ static inline void af_case_draw(int kind, uint64_t seed, af_case_params* cp, af_
   cp->p_out = 0.1;
   cp->rho_in = 1.0;
   cp->rho_out = 0.125;
-  if (kind == AF_CASE_QUADRANTS || kind == AF_CASE_QUADRANTS_NOISE) {
+  if (kind == AF_CASE_QUADRANTS_STRESS) {
+    for (int q = 0; q < 4; ++q) {
+      cp->quad[q][0] = af_rng_uniform(r, 0.01, 3.0);
+      cp->quad[q][1] = af_rng_uniform(r, -3.0, 3.0);
+      cp->quad[q][2] = af_rng_uniform(r, -3.0, 3.0);
+      double p = 10.0;
+      const int e = (int)(af_rng_u01(r) * 11.0);  /* 10^(1-e), e in 0..10 */
+      for (int i = 0; i < e; ++i) p = p * 0.1;
+      cp->quad[q][3] = p;
+    }
+  } else if (kind == AF_CASE_QUADRANTS || kind == AF_CASE_QUADRANTS_NOISE) {
     for (int q = 0; q < 4; ++q) {
       cp->quad[q][0] = af_rng_uniform(r, 0.5, 3.0);
       cp->quad[q][1] = af_rng_uniform(r, -1.0, 1.0);
@@ -170,7 +183,7 @@ static inline int af_cases_fill(int kind, uint64_t seed, int level, double gamma
  */
 static inline int af_case_point(int kind, const af_case_params* cp, double gamma, double x,
                                 double y, double z, double* q) {
-  if (kind == AF_CASE_QUADRANTS) {
+  if (kind == AF_CASE_QUADRANTS || kind == AF_CASE_QUADRANTS_STRESS) {
     const int quad = (x > 0.5 ? 1 : 0) + 2 * (y > 0.5 ? 1 : 0);
     af_conserved(cp->quad[quad][0], cp->quad[quad][1], cp->quad[quad][2], 0.0, cp->quad[quad][3],
                  gamma, q);

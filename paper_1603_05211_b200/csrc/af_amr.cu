@@ -558,6 +558,9 @@ void Amr::remesh_t(int l) {
 
 void Amr::remesh(int l) {
   if (l < 0 || l >= n_levels()) throw Error(AF_E_ARGUMENT, "remesh: no such level");
+  // a stage that failed earlier in the cycle is reported against the boxes it
+  // ran on, so before they change (remesh synchronises for the flag masks anyway)
+  check();
   if (dim_ == 3) remesh_t<3>(l); else remesh_t<2>(l);
 }
 

@@ -82,6 +82,56 @@ def test_run_amr_matches_reference(case):
     h.close()
 
 
+LONG = [
+    # four levels, 128 finest steps: dozens of patches that follow the waves
+    ("2d_L8_hancock", 2, 5, 8, 128, 1.2e-3, 0, {"seed": 1}),
+    ("2d_L8_hancock_s3", 2, 5, 8, 128, 1.2e-3, 0, {"seed": 3}),
+    ("2d_L8_rk2", 2, 5, 8, 128, 1.0e-3, 0, {"seed": 3, "flux": 0, "integrator": 0}),
+    ("2d_L7_vanalbada", 2, 4, 7, 128, 2.6e-3, 0, {"seed": 8, "limiter": 0}),
+    ("3d_L6_hancock_pratio", 3, 3, 6, 32, 1.5e-3, 3, {"seed": 2}),
+    ("3d_L6_rk2", 3, 3, 6, 32, 0.8e-3, 2, {"seed": 1, "flux": 0, "integrator": 0}),
+]
+
+
+@pytest.mark.parametrize("case", LONG, ids=[c[0] for c in LONG])
+def test_long_runs_match_reference(case):
+    _, dim, base, level, n_steps, dt, kind, kw = case
+    h, ref = _run_both(dim, base, level, n_steps, dt, kind, **kw)
+    h.initialize_case(kind, kw.get("seed", 1))
+    rep = h.run(n_steps, dt)
+    _compare(h, rep, ref)
+    assert max(len(lv["boxes"]) for lv in ref["levels"]) >= 20
+    h.close()
+
+
+@pytest.mark.parametrize("seed,dt", [(12, 3e-3), (15, 3e-3), (19, 3e-3), (25, 3e-3), (59, 1e-3),
+                                     (59, 3e-3)])
+@pytest.mark.parametrize("time_refine", [False, True])
+@pytest.mark.parametrize("flux,limiter", [(1, 0), (0, 1)])
+def test_fallback_counts_match_reference(seed, dt, time_refine, flux, limiter):
+    """the stress quadrants reach the MUSCL-Hancock predictor/corrector
+    fallbacks (step.cpp:170-173,203-212); the reference counts one per patch
+    that evaluates the cell or face"""
+    h, ref = _run_both(2, 4, 6, 4, dt, 4, seed=seed, flux=flux, limiter=limiter, integrator=1,
+                       time_refine=time_refine)
+    if ref["err_kind"]:
+        h.initialize_case(4, seed)
+        with pytest.raises(NonPhysicalState) as e:
+            h.run(4, dt)
+        assert str(e.value) == ref["err"]
+        return
+    h.initialize_case(4, seed)
+    rep = h.run(4, dt)
+    _compare(h, rep, ref)
+    h.close()
+
+
+def test_fallback_cases_do_fall_back():
+    ref = oracle.ref_amr_run(2, 6, 4, 4, 3e-3, case_kind=4, seed=59, flux=1, limiter=0,
+                             integrator=1, time_refine=False)
+    assert ref["err_kind"] == 0 and ref["fallbacks"] >= 5
+
+
 def test_initialize_matches_reference():
     """the hierarchy straight after initialize (n_steps = 0): boxes, ghosts"""
     h, ref = _run_both(2, 4, 7, 0, 1e-3, 0, seed=9)
@@ -151,6 +201,15 @@ def test_errors_match_reference():
     with pytest.raises(NonPhysicalState) as e2:
         h2.run(16, 2.0e-2)
     assert str(e2.value) == ref2["err"]
+    # a failure deep in a long run: level 3, a later cycle; and a ghost cell
+    for args, kw in (((2, 5, 8, 128, 1.2e-3, 0), {"seed": 6}),
+                     ((2, 4, 7, 128, 2.6e-3, 0), {"seed": 11, "limiter": 0})):
+        hh, rr = _run_both(*args, **kw)
+        assert rr["err_kind"] == 1
+        hh.initialize_case(0, kw["seed"])
+        with pytest.raises(NonPhysicalState) as ee:
+            hh.run(args[3], args[4])
+        assert str(ee.value) == rr["err"]
     # 3D RK2 stage-2 failure on a fine patch (the "level L patch P: " prefix)
     h4, ref4 = _run_both(3, 3, 5, 8, 2.0e-3, 2, seed=4, bc=[PER] * 6, flux=0, integrator=0)
     assert ref4["err_kind"] == 1
