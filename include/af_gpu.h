@@ -419,10 +419,21 @@ af_status af_amr_properly_nested(af_amr* h, int* nested);
 af_status af_amr_dump_boxes(af_amr* h, const char** text);
 af_status af_amr_last_error(const af_amr* h, af_error* err);
 af_status af_amr_kernel_launches(const af_amr* h, long* count);
+/* patch-cell stage updates performed by every update_level so far (cells of
+ * the level x 1 for MUSCL-Hancock, x 2 for RK2): the bench metric's numerator */
+af_status af_amr_cell_updates(const af_amr* h, long* updates);
+/* host wall time spent inside remesh (flags, clustering, rebuild; it
+ * synchronises for the masks) and the number of remesh calls so far */
+af_status af_amr_remesh_stats(const af_amr* h, double* seconds, long* calls);
 /* cluster (amr.hpp:110-111): flags/allowed are n0*n1*n2 bytes, x fastest
  * (allowed nullable); boxes6 nullable to query the count. Host integer work. */
 af_status af_amr_cluster(const unsigned char* flags, const unsigned char* allowed, int dim, int n0,
                          int n1, int n2, double efficiency, int* boxes6, int capacity, int* n_boxes);
+/* The same clustering on the device, as remesh runs it (summed-area tables of
+ * the masks, breadth-first bisection, one CTA per box; only the box list
+ * leaves HBM): host masks of an n x n (x n) level are uploaded first. */
+af_status af_amr_cluster_device(const unsigned char* flags, const unsigned char* allowed, int dim,
+                                int n, double efficiency, int* boxes6, int capacity, int* n_boxes);
 
 /* Self-check of the inline fast-path division and square root the face
  * fluxes use (CUDA's fast-path sequences with their range tests; see

@@ -78,6 +78,25 @@ def cluster(flags: np.ndarray, efficiency: float, allowed: np.ndarray | None = N
     return out[:n.value]
 
 
+def cluster_device(flags: np.ndarray, efficiency: float, allowed: np.ndarray | None = None):
+    """cluster() as remesh runs it on the device (cubic masks)."""
+    lib = _abi.load()
+    f = np.ascontiguousarray(flags, dtype=np.uint8)
+    a = None if allowed is None else np.ascontiguousarray(allowed, dtype=np.uint8)
+    n = f.shape[-1]
+    if any(s != n for s in f.shape):
+        raise ValueError("cluster_device: cubic masks only")
+    cap = int(f.sum()) + 1
+    out = np.zeros((cap, 6), dtype=np.int32)
+    k = C.c_int(0)
+    raise_status(lib.af_amr_cluster_device(f.ctypes.data_as(C.c_char_p),
+                                           None if a is None else a.ctypes.data_as(C.c_char_p),
+                                           f.ndim, n, efficiency,
+                                           out.ctypes.data_as(C.POINTER(C.c_int)), cap, C.byref(k)),
+                 "af_amr_cluster_device")
+    return out[:k.value]
+
+
 class PatchHierarchy:
     """PatchHierarchy (amr.hpp:123-242) on the device."""
 
@@ -205,6 +224,17 @@ class PatchHierarchy:
         n = C.c_long()
         self._check(self._lib.af_amr_kernel_launches(self._h, C.byref(n)))
         return n.value
+
+    def cell_updates(self) -> int:
+        n = C.c_long()
+        self._check(self._lib.af_amr_cell_updates(self._h, C.byref(n)))
+        return n.value
+
+    def remesh_stats(self):
+        """(host seconds inside remesh, remesh calls) so far"""
+        sec, n = C.c_double(), C.c_long()
+        self._check(self._lib.af_amr_remesh_stats(self._h, C.byref(sec), C.byref(n)))
+        return sec.value, n.value
 
     # ---- run_amr's cycle loop --------------------------------------------
     def run(self, n_steps: int, dt_finest: float) -> AmrReport:

@@ -4,6 +4,7 @@
 #include "af_amr.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <tuple>
@@ -68,51 +69,6 @@ bool inside_allowed(const ClusterJob& J, const ABox& b) {
   return true;
 }
 
-// The cut a signature proposes (amr_cluster.cpp:130-177): the middle of the
-// longest interior run of empty planes (first such run on ties), else the
-// strongest sign change of the second difference (first on ties); `score`
-// ranks the proposals of the axes. Returns the offset of the cut or -1.
-int propose_cut(const std::vector<long>& sig, int* score) {
-  const int n = (int)sig.size();
-  int gap_len = 0, gap_mid = -1, run = 0;
-  for (int i = 0; i < n; ++i) {
-    if (sig[i] == 0) {
-      ++run;
-      continue;
-    }
-    const int start = i - run;
-    if (run > gap_len && start > 0) {
-      gap_len = run;
-      gap_mid = start + run / 2;
-    }
-    run = 0;
-  }
-  if (gap_mid > 0) {
-    *score = 1000000 + gap_len;
-    return gap_mid;
-  }
-  if (n >= 4) {
-    auto lap = [&](int i) { return (i < 1 || i > n - 2) ? 0L : sig[i - 1] - 2 * sig[i] + sig[i + 1]; };
-    long best = 0;
-    int at = -1;
-    for (int i = 1; i < n - 2; ++i) {
-      const long a = lap(i), b = lap(i + 1);
-      if (!((a < 0 && b > 0) || (a > 0 && b < 0))) continue;
-      const long jump = std::labs(a - b);
-      if (jump > best) {
-        best = jump;
-        at = i + 1;
-      }
-    }
-    if (at > 0) {
-      *score = (int)std::min<long>(best, 999999);
-      return at;
-    }
-  }
-  *score = 0;
-  return -1;
-}
-
 void bisect(const ClusterJob& J, const ABox& region) {
   long flagged = 0;
   const ABox b = shrink(J, region, flagged);
@@ -132,7 +88,7 @@ void bisect(const ClusterJob& J, const ABox& region) {
         for (int i = b.lo[0]; i < b.hi[0]; ++i)
           if (J.flag(i, j, k)) ++sig[(size_t)((a == 0 ? i : a == 1 ? j : k) - b.lo[a])];
     int score = 0;
-    const int off = propose_cut(sig, &score);
+    const int off = propose_cut_t(sig.data(), (int)sig.size(), &score);
     const int pos = off < 0 ? -1 : b.lo[a] + off;
     if (pos > b.lo[a] && pos < b.hi[a] && score > best) {
       best = score;
@@ -167,6 +123,115 @@ std::vector<ABox> amr_cluster(const uint8_t* flags, const uint8_t* allowed, int 
   all.hi[1] = n1;
   all.hi[2] = n2;
   bisect(J, all);
+  std::sort(out.begin(), out.end(), [](const ABox& a, const ABox& b) {
+    return std::tie(a.lo[2], a.lo[1], a.lo[0]) < std::tie(b.lo[2], b.lo[1], b.lo[0]);
+  });
+  return out;
+}
+
+// ------------------------------------------------------- device clustering --
+namespace {
+constexpr int kClusterLevels = 4000;  // frontier counters (the bisection depth bound)
+constexpr int kClusterChunk = 24;     // levels launched between two looks at the frontier
+}  // namespace
+
+DeviceCluster::~DeviceCluster() {
+  cudaFree(Sf_);
+  cudaFree(Sa_);
+  cudaFree(qa_);
+  cudaFree(qb_);
+  cudaFree(out_);
+  cudaFree(hdr_);
+}
+
+std::vector<ABox> DeviceCluster::run(int dim, const uint8_t* d_flags, const uint8_t* d_allowed, int n,
+                                     double efficiency, long* launches) {
+  const long np = n + 1;
+  const long sat = dim == 3 ? np * np * np : np * np;
+  const long cells = dim == 3 ? (long)n * n * n : (long)n * n;
+  if (sat > sat_cap_) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(Sf_);
+    cudaFree(Sa_);
+    AF_CUDA(cudaMalloc(&Sf_, sizeof(int) * sat));
+    AF_CUDA(cudaMalloc(&Sa_, sizeof(int) * sat));
+    sat_cap_ = sat;
+  }
+  const int want = (int)std::min<long>(cells + 2, 1 << 20);
+  if (want > cap_) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(qa_);
+    cudaFree(qb_);
+    cudaFree(out_);
+    AF_CUDA(cudaMalloc(&qa_, sizeof(CBox) * want));
+    AF_CUDA(cudaMalloc(&qb_, sizeof(CBox) * want));
+    AF_CUDA(cudaMalloc(&out_, sizeof(CBox) * want));
+    cap_ = want;
+  }
+  if (!hdr_) AF_CUDA(cudaMalloc(&hdr_, sizeof(int) * (kClusterLevels + 2)));
+  auto sat_build = [&](const uint8_t* mask, int* S) {
+    const long rows = dim == 3 ? (long)n * n : n;
+    if (dim == 3) {
+      amr_sat_x_kernel<3><<<(unsigned)((rows + 127) / 128), 128, 0, stream_>>>(mask, n, S);
+      amr_sat_y_kernel<3><<<(unsigned)((np * n + 127) / 128), 128, 0, stream_>>>(n, S);
+      amr_sat_z_kernel<<<(unsigned)((np * np + 127) / 128), 128, 0, stream_>>>(n, S);
+      *launches += 3;
+    } else {
+      amr_sat_x_kernel<2><<<(unsigned)((rows + 127) / 128), 128, 0, stream_>>>(mask, n, S);
+      amr_sat_y_kernel<2><<<(unsigned)((np + 127) / 128), 128, 0, stream_>>>(n, S);
+      *launches += 2;
+    }
+  };
+  sat_build(d_flags, Sf_);
+  if (d_allowed) sat_build(d_allowed, Sa_);
+  CBox root;
+  for (int a = 0; a < 3; ++a) {
+    root.lo[a] = 0;
+    root.hi[a] = a < dim ? n : 1;
+  }
+  AF_CUDA(cudaMemsetAsync(hdr_, 0, sizeof(int) * (kClusterLevels + 2), stream_));
+  const int one = 1;
+  AF_CUDA(cudaMemcpyAsync(hdr_ + 2, &one, sizeof(int), cudaMemcpyHostToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(qa_, &root, sizeof(CBox), cudaMemcpyHostToDevice, stream_));
+  const size_t smem = sizeof(int) * (size_t)n;
+  if (smem > 48 * 1024) {
+    AF_CUDA(cudaFuncSetAttribute(amr_cluster_level_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AF_CUDA(cudaFuncSetAttribute(amr_cluster_level_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  std::vector<int> hdr((size_t)kClusterLevels + 2);
+  int level = 0;
+  for (;;) {
+    for (int k = 0; k < kClusterChunk && level < kClusterLevels - 1; ++k, ++level) {
+      const CBox* in = static_cast<const CBox*>((level & 1) ? qb_ : qa_);
+      CBox* next = static_cast<CBox*>((level & 1) ? qa_ : qb_);
+      if (dim == 3)
+        amr_cluster_level_kernel<3><<<592, 128, smem, stream_>>>(in, hdr_ + 2 + level, next, hdr_ + 3 + level,
+                                                                 static_cast<CBox*>(out_), hdr_, cap_, Sf_,
+                                                                 d_allowed ? Sa_ : nullptr, n, efficiency, hdr_ + 1);
+      else
+        amr_cluster_level_kernel<2><<<592, 128, smem, stream_>>>(in, hdr_ + 2 + level, next, hdr_ + 3 + level,
+                                                                 static_cast<CBox*>(out_), hdr_, cap_, Sf_,
+                                                                 d_allowed ? Sa_ : nullptr, n, efficiency, hdr_ + 1);
+      ++*launches;
+    }
+    AF_CUDA(cudaGetLastError());
+    AF_CUDA(cudaMemcpyAsync(hdr.data(), hdr_, sizeof(int) * (size_t)(3 + level), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    if (hdr[1]) throw Error(AF_E_INTERNAL, "cluster: box queue overflow");
+    if (hdr[(size_t)2 + level] == 0) break;
+    if (level >= kClusterLevels - 1) throw Error(AF_E_INTERNAL, "cluster: bisection deeper than its bound");
+  }
+  std::vector<CBox> got((size_t)hdr[0]);
+  if (!got.empty()) {
+    AF_CUDA(cudaMemcpyAsync(got.data(), out_, sizeof(CBox) * got.size(), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaStreamSynchronize(stream_));
+  }
+  std::vector<ABox> out(got.size());
+  for (size_t i = 0; i < got.size(); ++i)
+    for (int a = 0; a < 3; ++a) {
+      out[i].lo[a] = got[i].lo[a];
+      out[i].hi[a] = got[i].hi[a];
+    }
   std::sort(out.begin(), out.end(), [](const ABox& a, const ABox& b) {
     return std::tie(a.lo[2], a.lo[1], a.lo[0]) < std::tie(b.lo[2], b.lo[1], b.lo[0]);
   });
@@ -222,6 +287,7 @@ Amr::Amr(const af_config& cfg, const af_amr_options& opt) : cfg_(cfg), opt_(opt)
   AF_CUDA(cudaMalloc(&d_rec_, sizeof(ARec) * kRecCap));
   AF_CUDA(cudaMemset(d_rec_, 0, sizeof(ARec) * kRecCap));
   spare_.resize((size_t)opt.max_levels + 1);
+  clusterer_ = new DeviceCluster(stream_);
   // level 0: one patch over the whole domain (amr_hierarchy.cpp:41-56)
   Level L;
   alloc_level(L, 0);
@@ -239,6 +305,8 @@ Amr::~Amr() {
   cudaStreamSynchronize(stream_);
   for (Level& L : lv_) free_level(L);
   for (Level& L : spare_) free_level(L);
+  delete clusterer_;
+  cudaFree(d_cb_);
   cudaFree(d_err_);
   cudaFree(d_flag_);
   cudaFree(d_rec_);
@@ -339,13 +407,17 @@ void Amr::upload_boxes(Level& L) {
     off[i + 1] = off[i] + L.boxes[i].volume();
   }
   L.total = off[nb];
-  AF_CUDA(cudaStreamSynchronize(stream_));
-  cudaFree(L.d_boxes);
-  cudaFree(L.d_off);
-  AF_CUDA(cudaMalloc(&L.d_boxes, sizeof(int) * 6 * std::max(nb, 1)));
-  AF_CUDA(cudaMalloc(&L.d_off, sizeof(long) * (nb + 1)));
-  AF_CUDA(cudaMemcpy(L.d_boxes, bx.data(), sizeof(int) * 6 * nb, cudaMemcpyHostToDevice));
-  AF_CUDA(cudaMemcpy(L.d_off, off.data(), sizeof(long) * (nb + 1), cudaMemcpyHostToDevice));
+  if (nb + 1 > L.box_cap) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(L.d_boxes);
+    cudaFree(L.d_off);
+    L.box_cap = 2 * (nb + 1) + 64;
+    AF_CUDA(cudaMalloc(&L.d_boxes, sizeof(int) * 6 * L.box_cap));
+    AF_CUDA(cudaMalloc(&L.d_off, sizeof(long) * L.box_cap));
+  }
+  // pageable sources: the copies are staged before the calls return
+  AF_CUDA(cudaMemcpyAsync(L.d_boxes, bx.data(), sizeof(int) * 6 * nb, cudaMemcpyHostToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(L.d_off, off.data(), sizeof(long) * (nb + 1), cudaMemcpyHostToDevice, stream_));
 }
 
 void Amr::copy_field(double* dst, const double* src, long count) {
@@ -455,7 +527,6 @@ void Amr::remesh_t(int l) {
   const ABc b = bc_of(cfg_);
   const double gm1 = cfg_.gamma - 1.0;
   std::vector<std::vector<ABox>> fresh((size_t)top + 2);
-  std::vector<uint8_t> h_masked, h_allowed;
   for (int m = top; m >= l + 1; --m) {
     const int src = m - 1;
     if (src > deepest) continue;
@@ -479,31 +550,22 @@ void Amr::remesh_t(int l) {
         }
         cb.insert(cb.end(), {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]});
       }
-      int* d_cb = nullptr;
-      AF_CUDA(cudaMalloc(&d_cb, sizeof(int) * cb.size()));
-      AF_CUDA(cudaMemcpyAsync(d_cb, cb.data(), sizeof(int) * cb.size(), cudaMemcpyHostToDevice, stream_));
-      amr_setbox_kernel<D><<<g, 256, 0, stream_>>>(d_cb, (int)(cb.size() / 6), S.n, m_masked_);
+      if ((long)cb.size() > cb_cap_) {
+        AF_CUDA(cudaStreamSynchronize(stream_));
+        cudaFree(d_cb_);
+        cb_cap_ = 2 * (long)cb.size() + 384;
+        AF_CUDA(cudaMalloc(&d_cb_, sizeof(int) * cb_cap_));
+      }
+      AF_CUDA(cudaMemcpyAsync(d_cb_, cb.data(), sizeof(int) * cb.size(), cudaMemcpyHostToDevice, stream_));
+      amr_setbox_kernel<D><<<g, 256, 0, stream_>>>(d_cb_, (int)(cb.size() / 6), S.n, m_masked_);
       amr_dilate_kernel<D><<<g, 256, 0, stream_>>>(m_masked_, S.n, b, 1, nullptr, m_nest_);
       launch_count(2);
-      AF_CUDA(cudaStreamSynchronize(stream_));
-      cudaFree(d_cb);
       nest = m_nest_;
     }
     amr_dilate_kernel<D><<<g, 256, 0, stream_>>>(m_tmp_, S.n, b, 1, nest, m_flags_);
-    AF_CUDA(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_));
     amr_allowed_kernel<D><<<g, 256, 0, stream_>>>(S.pid, S.n, b, m_flags_, m_allowed_, m_masked_, d_flag_);
     launch_count(3);
-    int any = 0;
-    AF_CUDA(cudaMemcpyAsync(&any, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-    AF_CUDA(cudaStreamSynchronize(stream_));
-    if (!any) continue;
-    h_masked.resize((size_t)S.cells);
-    h_allowed.resize((size_t)S.cells);
-    AF_CUDA(cudaMemcpyAsync(h_masked.data(), m_masked_, S.cells, cudaMemcpyDeviceToHost, stream_));
-    AF_CUDA(cudaMemcpyAsync(h_allowed.data(), m_allowed_, S.cells, cudaMemcpyDeviceToHost, stream_));
-    AF_CUDA(cudaStreamSynchronize(stream_));
-    for (const ABox& cbx : amr_cluster(h_masked.data(), h_allowed.data(), D, S.n, S.n, D == 3 ? S.n : 1,
-                                       opt_.cluster_efficiency)) {
+    for (const ABox& cbx : cluster_device<D>(m_masked_, m_allowed_, S.n, opt_.cluster_efficiency)) {
       ABox r;  // Box::refined (amr.hpp:49-64)
       for (int a = 0; a < D; ++a) {
         r.lo[a] = 2 * cbx.lo[a];
@@ -551,9 +613,13 @@ void Amr::remesh_t(int l) {
   }
   // registers of the rebuilt pairs restart; pairs below l keep accumulating
   for (int m = l; m < n_levels(); ++m) rebuild_registers(m);
+  // NestingViolation (amr_hierarchy.cpp:340-341), reported by the next check()
+  for (int m = std::max(l, 1); m < n_levels(); ++m) {
+    amr_nested_kernel<D><<<blocks_for(lv_[m].cells), 256, 0, stream_>>>(lv_[m].pid, lv_[m].n, lv_[m - 1].pid,
+                                                                        d_err_ + 2);
+    launch_count();
+  }
   AF_CUDA(cudaGetLastError());
-  if (!properly_nested())
-    throw Error(AF_E_INTERNAL, "remesh produced an improperly nested hierarchy");
 }
 
 void Amr::remesh(int l) {
@@ -561,7 +627,10 @@ void Amr::remesh(int l) {
   // a stage that failed earlier in the cycle is reported against the boxes it
   // ran on, so before they change (remesh synchronises for the flag masks anyway)
   check();
+  const auto t0 = std::chrono::steady_clock::now();
   if (dim_ == 3) remesh_t<3>(l); else remesh_t<2>(l);
+  remesh_seconds_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  ++remesh_calls_;
 }
 
 void Amr::rebuild_registers(int l) {
@@ -572,38 +641,43 @@ void Amr::rebuild_registers(int l) {
     return;
   }
   const Level& Fn = lv_[l + 1];
-  const ABc b = bc_of(cfg_);
-  const unsigned g = blocks_for(L.cells);
-  int count = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    AF_CUDA(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_));
-    long* sc = pass ? L.slot_cell : nullptr;
-    if (dim_ == 3)
-      amr_reg_alloc_kernel<3><<<g, 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask, d_flag_,
-                                                      sc, L.slot_face);
-    else
-      amr_reg_alloc_kernel<2><<<g, 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask, d_flag_,
-                                                      sc, L.slot_face);
-    launch_count();
-    if (pass) break;
-    AF_CUDA(cudaMemcpyAsync(&count, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-    AF_CUDA(cudaStreamSynchronize(stream_));
-    if (!count) return;
-    if (count > L.slot_cap) {
-      cudaFree(L.slot_cell);
-      cudaFree(L.slot_face);
-      cudaFree(L.has);
-      cudaFree(L.Rc);
-      cudaFree(L.Rf);
-      L.slot_cap = count + count / 2 + 64;
-      AF_CUDA(cudaMalloc(&L.slot_cell, sizeof(long) * L.slot_cap));
-      AF_CUDA(cudaMalloc(&L.slot_face, L.slot_cap));
-      AF_CUDA(cudaMalloc(&L.has, L.slot_cap));
-      AF_CUDA(cudaMalloc(&L.Rc, sizeof(double) * (dim_ + 2) * L.slot_cap));
-      AF_CUDA(cudaMalloc(&L.Rf, sizeof(double) * (dim_ + 2) * L.slot_cap));
+  // every register face is a coarse face of a fine box's surface: an upper
+  // bound the host knows without asking the device
+  long bound = 0;
+  for (const ABox& fb : Fn.boxes)
+    for (int a = 0; a < dim_; ++a) {
+      long area = 1;
+      for (int t = 0; t < dim_; ++t)
+        if (t != a) area *= fb.extent(t) / 2;
+      bound += 2 * area;
     }
+  if (bound > L.slot_cap) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(L.slot_cell);
+    cudaFree(L.slot_face);
+    cudaFree(L.has);
+    cudaFree(L.Rc);
+    cudaFree(L.Rf);
+    L.slot_cap = (int)(bound + bound / 2 + 64);
+    AF_CUDA(cudaMalloc(&L.slot_cell, sizeof(long) * L.slot_cap));
+    AF_CUDA(cudaMalloc(&L.slot_face, L.slot_cap));
+    AF_CUDA(cudaMalloc(&L.has, L.slot_cap));
+    AF_CUDA(cudaMalloc(&L.Rc, sizeof(double) * (dim_ + 2) * L.slot_cap));
+    AF_CUDA(cudaMalloc(&L.Rf, sizeof(double) * (dim_ + 2) * L.slot_cap));
   }
-  L.nslots = count;
+  L.nslots = (int)bound;  // slots past the device's count stay unused (face 0xff)
+  const ABc b = bc_of(cfg_);
+  AF_CUDA(cudaMemsetAsync(d_flag_, 0, 2 * sizeof(int), stream_));
+  AF_CUDA(cudaMemsetAsync(L.slot_face, 0xff, L.nslots, stream_));
+  if (dim_ == 3)
+    amr_reg_alloc_kernel<3><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask,
+                                                                      d_flag_, L.slot_cell, L.slot_face, L.nslots,
+                                                                      d_err_);
+  else
+    amr_reg_alloc_kernel<2><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask,
+                                                                      d_flag_, L.slot_cell, L.slot_face, L.nslots,
+                                                                      d_err_);
+  launch_count();
   clear_registers(l);
   AF_CUDA(cudaGetLastError());
 }
@@ -634,6 +708,7 @@ void Amr::update_t(int l, double dt) {
   const double h = dx(l), inv_dx = 1.0 / h, gamma = cfg_.gamma;
   const unsigned gc = blocks_for(L.cells), gf = blocks_for(D * per);
 
+  cell_updates_ += L.total * (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK ? 1 : 2);
   L.t_old = L.t;
   copy_field(L.Uold, L.U, cnt);  // p.data_old = p.data
   copy_field(L.Gold, L.G, cnt);
@@ -732,6 +807,8 @@ void Amr::check() {
     throw Error(AF_E_INTERNAL, prefix_ + "no coarse donor under a fine ghost or new cell (MissingBracketingStates)");
   if (err[0] == 3)
     throw Error(AF_E_REGISTER_MISMATCH, prefix_ + "flux register is missing a side");
+  if (err[2])
+    throw Error(AF_E_INTERNAL, "remesh produced an improperly nested hierarchy");
 }
 
 // The reference's NonPhysicalState text: the first offending cell in the
@@ -1245,6 +1322,53 @@ af_status af_amr_kernel_launches(const af_amr* h, long* count) {
   if (!h || !count) return AF_E_ARGUMENT;
   *count = h->impl->kernel_launches();
   return AF_OK;
+}
+af_status af_amr_remesh_stats(const af_amr* h, double* seconds, long* calls) {
+  if (!h) return AF_E_ARGUMENT;
+  if (seconds) *seconds = h->impl->remesh_seconds();
+  if (calls) *calls = h->impl->remesh_calls();
+  return AF_OK;
+}
+af_status af_amr_cell_updates(const af_amr* h, long* updates) {
+  if (!h || !updates) return AF_E_ARGUMENT;
+  *updates = h->impl->cell_updates();
+  return AF_OK;
+}
+af_status af_amr_cluster_device(const unsigned char* flags, const unsigned char* allowed, int dim,
+                                int n, double efficiency, int* boxes6, int capacity, int* n_boxes) {
+  if (!flags || !n_boxes || (dim != 2 && dim != 3) || n < 1) return AF_E_ARGUMENT;
+  try {
+    const size_t cells = dim == 3 ? (size_t)n * n * n : (size_t)n * n;
+    unsigned char *d_f = nullptr, *d_a = nullptr;
+    AF_CUDA(cudaMalloc(&d_f, cells));
+    AF_CUDA(cudaMemcpy(d_f, flags, cells, cudaMemcpyHostToDevice));
+    if (allowed) {
+      AF_CUDA(cudaMalloc(&d_a, cells));
+      AF_CUDA(cudaMemcpy(d_a, allowed, cells, cudaMemcpyHostToDevice));
+    }
+    std::vector<af::ABox> out;
+    long launches = 0;
+    {
+      af::DeviceCluster dc(nullptr);
+      out = dc.run(dim, d_f, d_a, n, efficiency, &launches);
+    }
+    cudaFree(d_f);
+    cudaFree(d_a);
+    *n_boxes = (int)out.size();
+    if (boxes6) {
+      if ((int)out.size() > capacity) return AF_E_ARGUMENT;
+      for (size_t i = 0; i < out.size(); ++i)
+        for (int a = 0; a < 3; ++a) {
+          boxes6[6 * i + a] = out[i].lo[a];
+          boxes6[6 * i + 3 + a] = out[i].hi[a];
+        }
+    }
+    return AF_OK;
+  } catch (const af::Error& x) {
+    return x.status;
+  } catch (const std::exception&) {
+    return AF_E_ARGUMENT;
+  }
 }
 af_status af_amr_cluster(const unsigned char* flags, const unsigned char* allowed, int dim, int n0,
                          int n1, int n2, double efficiency, int* boxes6, int capacity, int* n_boxes) {

@@ -32,6 +32,27 @@ struct ABox {  // Box (amr.hpp:19-66): half-open [lo, hi), z = [0,1) in 2D
 std::vector<ABox> amr_cluster(const uint8_t* flags, const uint8_t* allowed, int dim, int n0, int n1,
                               int n2, double efficiency);
 
+// The same clustering with the masks staying on the device (summed-area
+// tables + breadth-first bisection, af_amr_kernels.cuh); only the box list
+// comes back. d_flags/d_allowed: device masks of an n x n (x n) level.
+class DeviceCluster {
+ public:
+  explicit DeviceCluster(cudaStream_t stream) : stream_(stream) {}
+  ~DeviceCluster();
+  DeviceCluster(const DeviceCluster&) = delete;
+  DeviceCluster& operator=(const DeviceCluster&) = delete;
+  std::vector<ABox> run(int dim, const uint8_t* d_flags, const uint8_t* d_allowed, int n,
+                        double efficiency, long* launches);
+
+ private:
+  cudaStream_t stream_;
+  long sat_cap_ = 0;
+  int *Sf_ = nullptr, *Sa_ = nullptr;
+  void *qa_ = nullptr, *qb_ = nullptr, *out_ = nullptr;
+  int* hdr_ = nullptr;  // [0] accepted boxes, [1] overflow, [2 + level] frontier sizes
+  int cap_ = 0;
+};
+
 typedef void (*amr_ic_fn)(double x, double y, double z, double* q5, void* user);
 
 class Amr {
@@ -70,6 +91,9 @@ class Amr {
   void run(long n_steps, double dt_finest, long* cells_per_step, long* leaves_per_step,
            af_run_diag* diag);
   long kernel_launches() const { return launches_; }
+  long cell_updates() const { return cell_updates_; }  // patch cells x stages, every update_level
+  double remesh_seconds() const { return remesh_seconds_; }  // host time inside remesh()
+  long remesh_calls() const { return remesh_calls_; }
   const af_error& last_error() const { return err_; }
   af_error& error_slot() { return err_; }
 
@@ -84,6 +108,7 @@ class Amr {
     double *U = nullptr, *Uold = nullptr, *G = nullptr, *Gold = nullptr;
     int* d_boxes = nullptr;
     long* d_off = nullptr;
+    int box_cap = 0;
     long total = 0;  // cells of the boxes
     // flux registers of the pair (this level, next finer)
     int* regbase = nullptr;
@@ -102,6 +127,10 @@ class Amr {
   template <int D> void remesh_t(int l);
   template <int D, int S> void update_t(int l, double dt);
   template <int D> void rebuild_domain_t(int l, bool into_new);
+  template <int D>
+  std::vector<ABox> cluster_device(const uint8_t* d_flags, const uint8_t* d_allowed, int n, double eff) {
+    return clusterer_->run(D, d_flags, d_allowed, n, eff, &launches_);
+  }
   void update_async(int l, double dt);
   void alloc_level(Level& L, int l);
   void free_level(Level& L);
@@ -136,7 +165,13 @@ class Amr {
   double *W_ = nullptr, *DU_ = nullptr, *F_ = nullptr;
   uint8_t *m_flags_ = nullptr, *m_tmp_ = nullptr, *m_nest_ = nullptr, *m_allowed_ = nullptr,
           *m_masked_ = nullptr;
+  DeviceCluster* clusterer_ = nullptr;
+  int* d_cb_ = nullptr;  // nest boxes of remesh
+  long cb_cap_ = 0;
   long launches_ = 0;
+  long cell_updates_ = 0;
+  double remesh_seconds_ = 0.0;
+  long remesh_calls_ = 0;
   af_error err_{};
   std::string prefix_;  // "cycle N: " while run() is stepping
 };

@@ -754,24 +754,26 @@ template <int D>
 __global__ void __launch_bounds__(256) amr_reg_alloc_kernel(const int* pid, const int* fpid, int n,
                                                             ABc b, int* regbase, uint8_t* regmask,
                                                             int* count, long* slot_cell,
-                                                            uint8_t* slot_face) {
+                                                            uint8_t* slot_face, int cap, int* err) {
   const long cells = D == 3 ? (long)n * n * n : (long)n * n;
   const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (c >= cells) return;
   int p[3];
   a_coords<D>(n, c, p);
-  const uint8_t mask = a_reg_mask<D>(pid, fpid, n, b, p);
-  if (!slot_cell) {  // first pass: count
-    regmask[c] = mask;
-    regbase[c] = -1;
-    if (mask) atomicAdd(count, __popc(mask));
-    return;
+  uint8_t mask = a_reg_mask<D>(pid, fpid, n, b, p);
+  int base = -1;
+  if (mask) {
+    base = atomicAdd(count, __popc(mask));
+    if (base + __popc(mask) > cap) {  // cannot happen: cap bounds the fine boxes' surfaces
+      atomicCAS(err, 0, 3);
+      mask = 0;
+      base = -1;
+    }
   }
-  if (!mask) return;
-  const int base = atomicAdd(count, __popc(mask));
+  regmask[c] = mask;
   regbase[c] = base;
   int k = 0;
-  for (int bit = 0; bit < 2 * D; ++bit)
+  for (int bit = 0; bit < 2 * D && mask; ++bit)
     if (mask & (1u << bit)) {
       slot_cell[base + k] = c;
       slot_face[base + k] = (uint8_t)bit;
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(256) amr_reg_coarse_kernel(const long* slot_ce
                                                              int n, const double* F, double dt,
                                                              double* Rc, uint8_t* has, int* err) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nslots || amr_failed(err)) return;
+  if (s >= nslots || amr_failed(err) || slot_face[s] == 0xff) return;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
   const long cs = D * per;
   int p[3];
@@ -808,7 +810,7 @@ __global__ void __launch_bounds__(256) amr_reg_fine_kernel(const long* slot_cell
                                                            double dtshare, double* Rf, uint8_t* has,
                                                            int* err) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nslots || amr_failed(err)) return;
+  if (s >= nslots || amr_failed(err) || slot_face[s] == 0xff) return;
   const long per = D == 3 ? (long)(nf + 1) * nf * nf : (long)(nf + 1) * nf;
   const long cs = D * per;
   int u[3];
@@ -928,6 +930,238 @@ __global__ void __launch_bounds__(256) amr_sum_kernel(ALv<D> lv, const int* fpid
       double s = 0.0;
       for (int w = 0; w < 8; ++w) s += red[w];
       atomicAdd(out + m, s);
+    }
+  }
+}
+
+}  // namespace af
+
+// ------------------------------------------------- clustering on the device --
+// cluster (amr_cluster.cpp:79-232) without the masks leaving HBM: summed-area
+// tables of the flag and allowed masks make every box count, plane signature
+// and allowed test O(1) per entry, and the recursive bisection runs
+// breadth-first, one CTA per box of the current frontier. The reference sorts
+// its result by box corner, so the traversal order does not matter.
+namespace af {
+
+struct CBox {
+  int lo[3], hi[3];
+};
+
+// The cut a signature proposes (amr_cluster.cpp:130-177): the middle of the
+// longest interior run of empty planes (the first on ties), else the strongest
+// sign change of the second difference (the first on ties). Returns the offset
+// of the cut or -1; *score ranks the proposals of the axes.
+template <class T>
+__host__ __device__ inline int propose_cut_t(const T* sig, int n, int* score) {
+  int gap_len = 0, gap_mid = -1, run = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sig[i] == 0) {
+      ++run;
+      continue;
+    }
+    const int start = i - run;
+    if (run > gap_len && start > 0) {
+      gap_len = run;
+      gap_mid = start + run / 2;
+    }
+    run = 0;
+  }
+  if (gap_mid > 0) {
+    *score = 1000000 + gap_len;
+    return gap_mid;
+  }
+  if (n >= 4) {
+    long long best = 0;
+    int at = -1;
+    for (int i = 1; i < n - 2; ++i) {
+      const long long a = (long long)sig[i - 1] - 2 * (long long)sig[i] + (long long)sig[i + 1];
+      const long long b = (long long)sig[i] - 2 * (long long)sig[i + 1] + (long long)sig[i + 2];
+      if (!((a < 0 && b > 0) || (a > 0 && b < 0))) continue;
+      const long long jump = a - b < 0 ? b - a : a - b;
+      if (jump > best) {
+        best = jump;
+        at = i + 1;
+      }
+    }
+    if (at > 0) {
+      *score = (int)(best < 999999 ? best : 999999);
+      return at;
+    }
+  }
+  *score = 0;
+  return -1;
+}
+
+// S has (n+1)^D entries: S[k][j][i] = set cells of the mask in [0,i)x[0,j)x[0,k).
+// Pass x writes the row prefixes, passes y and z accumulate along their axis.
+template <int D>
+__global__ void __launch_bounds__(128) amr_sat_x_kernel(const uint8_t* mask, int n, int* S) {
+  const long rows = D == 3 ? (long)n * n : n;
+  const long r = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int j = (int)(r % n), k = (int)(r / n);
+  const uint8_t* m = mask + r * n;
+  const long np = n + 1;
+  int* s = S + ((D == 3 ? (long)(k + 1) * np : 0) + (j + 1)) * np;
+  int acc = 0;
+  s[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    acc += m[i] != 0;
+    s[i + 1] = acc;
+  }
+}
+template <int D>
+__global__ void __launch_bounds__(128) amr_sat_y_kernel(int n, int* S) {
+  const long np = n + 1;
+  const long cols = D == 3 ? np * n : np;  // (i, k) pairs, k in 1..n
+  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int i = (int)(c % np), k = (int)(c / np);
+  int* s = S + (D == 3 ? (long)(k + 1) * np * np : 0) + i;
+  int acc = 0;
+  s[0] = 0;
+  for (int j = 1; j <= n; ++j) {
+    acc += s[j * np];
+    s[j * np] = acc;
+  }
+}
+__global__ void __launch_bounds__(128) amr_sat_z_kernel(int n, int* S) {
+  const long np = n + 1, plane = np * np;
+  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (c >= plane) return;
+  int acc = 0;
+  S[c] = 0;
+  for (int k = 1; k <= n; ++k) {
+    acc += S[k * plane + c];
+    S[k * plane + c] = acc;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ long sat_count(const int* S, int n, const int* lo, const int* hi) {
+  const long np = n + 1;
+  if (D == 2) {
+    auto at = [&](int i, int j) { return (long)S[j * np + i]; };
+    return at(hi[0], hi[1]) - at(lo[0], hi[1]) - at(hi[0], lo[1]) + at(lo[0], lo[1]);
+  }
+  auto at = [&](int i, int j, int k) { return (long)S[((long)k * np + j) * np + i]; };
+  return at(hi[0], hi[1], hi[2]) - at(lo[0], hi[1], hi[2]) - at(hi[0], lo[1], hi[2]) -
+         at(hi[0], hi[1], lo[2]) + at(lo[0], lo[1], hi[2]) + at(lo[0], hi[1], lo[2]) +
+         at(hi[0], lo[1], lo[2]) - at(lo[0], lo[1], lo[2]);
+}
+
+// One level of the bisection: every box of the frontier `in` is shrunk to its
+// flagged cells and either accepted (out) or cut into two boxes of the next
+// frontier. cnt[0] = boxes in, cnt[1] = boxes of the next frontier, nout =
+// accepted boxes; ovf is raised when a queue is full.
+template <int D>
+__global__ void __launch_bounds__(128) amr_cluster_level_kernel(const CBox* in, const int* cnt_in,
+                                                                CBox* next, int* cnt_next, CBox* out,
+                                                                int* nout, int cap, const int* Sf,
+                                                                const int* Sa, int n, double efficiency,
+                                                                int* ovf) {
+  extern __shared__ int sig[];
+  __shared__ int s_lo[3], s_hi[3], s_cut[3], s_score[3];
+  const int nin = *cnt_in;
+  for (int bi = blockIdx.x; bi < nin; bi += gridDim.x) {
+    const CBox region = in[bi];
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      s_lo[threadIdx.x] = INT32_MAX;
+      s_hi[threadIdx.x] = INT32_MIN;
+    }
+    __syncthreads();
+    const long flagged = sat_count<D>(Sf, n, region.lo, region.hi);
+    if (flagged == 0) continue;
+    // shrink: per axis the first and last plane holding a flagged cell
+    for (int a = 0; a < D; ++a)
+      for (int p = region.lo[a] + threadIdx.x; p < region.hi[a]; p += blockDim.x) {
+        int lo[3] = {region.lo[0], region.lo[1], region.lo[2]};
+        int hi[3] = {region.hi[0], region.hi[1], region.hi[2]};
+        lo[a] = p;
+        hi[a] = p + 1;
+        if (sat_count<D>(Sf, n, lo, hi) > 0) {
+          atomicMin(&s_lo[a], p);
+          atomicMax(&s_hi[a], p + 1);
+        }
+      }
+    __syncthreads();
+    CBox b;
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = a < D ? s_lo[a] : 0;
+      b.hi[a] = a < D ? s_hi[a] : 1;
+    }
+    long vol = 1;
+    for (int a = 0; a < D; ++a) vol *= b.hi[a] - b.lo[a];
+    const double fill = (double)flagged / (double)vol;
+    const bool allowed_ok = !Sa || sat_count<D>(Sa, n, b.lo, b.hi) == vol;
+    if ((fill >= efficiency && allowed_ok) || vol == 1) {
+      if (threadIdx.x == 0) {
+        const int o = atomicAdd(nout, 1);
+        if (o < cap) out[o] = b; else *ovf = 1;
+      }
+      continue;
+    }
+    // the best signature cut over the axes (the first axis on equal scores)
+    for (int a = 0; a < D; ++a) {
+      const int ext = b.hi[a] - b.lo[a];
+      if (threadIdx.x == 0) {
+        s_cut[a] = -1;
+        s_score[a] = -1;
+      }
+      if (ext < 2) continue;
+      __syncthreads();
+      for (int p = threadIdx.x; p < ext; p += blockDim.x) {
+        int lo[3] = {b.lo[0], b.lo[1], b.lo[2]};
+        int hi[3] = {b.hi[0], b.hi[1], b.hi[2]};
+        lo[a] = b.lo[a] + p;
+        hi[a] = b.lo[a] + p + 1;
+        sig[p] = (int)sat_count<D>(Sf, n, lo, hi);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int score = 0;
+        const int off = propose_cut_t(sig, ext, &score);
+        if (off > 0 && off < ext) {
+          s_cut[a] = b.lo[a] + off;
+          s_score[a] = score;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int axis = -1, cut = -1, best = -1;
+      for (int a = 0; a < D; ++a)
+        if (s_cut[a] >= 0 && s_score[a] > best) {
+          best = s_score[a];
+          axis = a;
+          cut = s_cut[a];
+        }
+      bool accept = false;
+      if (axis < 0) {  // halve the longest axis (the first among equals)
+        for (int a = 0; a < D; ++a)
+          if (axis < 0 || b.hi[a] - b.lo[a] > b.hi[axis] - b.lo[axis]) axis = a;
+        if (b.hi[axis] - b.lo[axis] < 2)
+          accept = true;
+        else
+          cut = b.lo[axis] + (b.hi[axis] - b.lo[axis]) / 2;
+      }
+      if (accept) {
+        const int o = atomicAdd(nout, 1);
+        if (o < cap) out[o] = b; else *ovf = 1;
+      } else {
+        CBox l = b, h = b;
+        l.hi[axis] = cut;
+        h.lo[axis] = cut;
+        const int o = atomicAdd(cnt_next, 2);
+        if (o + 1 < cap) {
+          next[o] = l;
+          next[o + 1] = h;
+        } else {
+          *ovf = 1;
+        }
+      }
     }
   }
 }

@@ -132,6 +132,33 @@ def test_fallback_cases_do_fall_back():
     assert ref["err_kind"] == 0 and ref["fallbacks"] >= 5
 
 
+@pytest.mark.parametrize("dim,n", [(2, 16), (2, 64), (2, 256), (3, 8), (3, 32)])
+def test_device_cluster_matches_reference(dim, n):
+    """the clustering remesh runs on the device (summed-area tables, breadth-
+    first bisection) against the reference's recursive cluster()"""
+    from test_amr import _blobs
+    rng = np.random.default_rng(7 * dim + n)
+    shape = (n,) * dim
+    for trial in range(8):
+        flags = _blobs(rng, shape, 1 + trial % 5)
+        allowed = None
+        if trial % 3 == 1:
+            allowed = np.ones(shape, dtype=np.uint8)
+            allowed[tuple(slice(0, 2) for _ in shape)] = 0
+            allowed[(slice(n // 2, n // 2 + 1),) + (slice(None),) * (dim - 1)] = 0
+            flags &= allowed
+        for eff in (0.5, 0.8, 0.95):
+            assert np.array_equal(amr.cluster_device(flags, eff, allowed),
+                                  oracle.ref_cluster(flags, eff, allowed)), (dim, n, trial, eff)
+    empty = np.zeros(shape, dtype=np.uint8)
+    assert len(amr.cluster_device(empty, 0.8)) == 0
+    one = empty.copy()
+    one[(n // 2,) * dim] = 1
+    assert np.array_equal(amr.cluster_device(one, 0.8), oracle.ref_cluster(one, 0.8))
+    assert np.array_equal(amr.cluster_device(np.ones(shape, np.uint8), 0.8),
+                          oracle.ref_cluster(np.ones(shape, np.uint8), 0.8))
+
+
 def test_initialize_matches_reference():
     """the hierarchy straight after initialize (n_steps = 0): boxes, ghosts"""
     h, ref = _run_both(2, 4, 7, 0, 1e-3, 0, seed=9)
