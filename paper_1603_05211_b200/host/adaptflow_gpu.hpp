@@ -14,6 +14,9 @@
 //   gpu::run_uniform  unigrid.hpp:24-26 / unigrid.cpp:7-50
 //   gpu::run_mr       mr_solver.hpp:78-79 / mr_solver.cpp:318-400 (returns the
 //                     final to_uniform(L) grid instead of the host MRTree)
+//   gpu::AmrDevice    PatchHierarchy (amr.hpp:123-242) on the device
+//   gpu::run_amr      amr_solver.hpp:34-35 / amr_solver.cpp:62-133 (returns the
+//                     device hierarchy instead of the host PatchHierarchy)
 #pragma once
 
 #include <algorithm>
@@ -25,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include "adaptflow/amr.hpp"
+#include "adaptflow/amr_solver.hpp"
 #include "adaptflow/cases.hpp"
 #include "adaptflow/errors.hpp"
 #include "adaptflow/grid.hpp"
@@ -472,6 +477,205 @@ inline MRDeviceResult run_mr(const CaseSpec& spec, int level, long n_steps,
   }
   out.grid = tree.to_uniform(level);
   out.leaves = tree.leaves();
+  return out;
+}
+
+// ---------------------------------------------------------------- AMR ----
+// PatchHierarchy (amr.hpp:123-242) whose patch data live on the device.
+class AmrDevice {
+ public:
+  AmrDevice(int dim, int base_exp, double origin, double extent, const BoundaryCondition& bc,
+            const GasModel& gas, const AmrOptions& opts, const SchemeConfig& scheme)
+      : dim_(dim), base_exp_(base_exp) {
+    const af_config c = make_config(dim, base_exp, origin, extent, gas, bc, scheme);
+    af_amr_options o{};
+    o.eps_rho = opts.eps_rho;
+    o.eps_p = opts.eps_p;
+    o.cluster_efficiency = opts.cluster_efficiency;
+    o.time_refine = opts.time_refine ? 1 : 0;
+    o.flux_correction = opts.flux_correction ? 1 : 0;
+    o.max_levels = opts.max_levels;
+    const af_status st = af_amr_create(&c, &o, &h_);
+    if (st != AF_OK) throw ConfigError("af_amr_create failed");
+  }
+  ~AmrDevice() { af_amr_destroy(h_); }
+  AmrDevice(const AmrDevice&) = delete;
+  AmrDevice& operator=(const AmrDevice&) = delete;
+
+  void check(af_status st) const {
+    if (st == AF_OK) return;
+    af_error e{};
+    af_amr_last_error(h_, &e);
+    rethrow(st, e);
+  }
+  af_amr* handle() const { return h_; }
+  int dim() const { return dim_; }
+  int base_exp() const { return base_exp_; }
+
+  void initialize(const std::function<ConservedState(double, double, double)>& ic) {
+    auto thunk = [](double x, double y, double z, double* q, void* user) {
+      const auto& f = *static_cast<const std::function<ConservedState(double, double, double)>*>(user);
+      const ConservedState s = f(x, y, z);
+      q[0] = s.rho;
+      q[1] = s.mom[0];
+      q[2] = s.mom[1];
+      q[3] = s.mom[2];
+      q[4] = s.rhoE;
+    };
+    check(af_amr_initialize(h_, thunk, const_cast<void*>(static_cast<const void*>(&ic))));
+  }
+  void sync_ghosts(int l, double tau) { check(af_amr_sync_ghosts(h_, l, tau)); }
+  void remesh(int l) { check(af_amr_remesh(h_, l)); }
+  StepDiag update_level(int l, double dt) {
+    af_step_diag d{};
+    check(af_amr_update_level(h_, l, dt, &d));
+    StepDiag out;
+    out.max_wave_speed = d.max_wave_speed;
+    out.fallbacks = d.fallbacks;
+    return out;
+  }
+  void average_down(int l) { check(af_amr_average_down(h_, l)); }
+  void flux_correct(int l) { check(af_amr_flux_correct(h_, l)); }
+  int n_levels() const {
+    int n = 0;
+    check(af_amr_n_levels(h_, &n));
+    return n;
+  }
+  std::vector<Box> boxes(int l) const {
+    int np = 0;
+    check(af_amr_level_info(h_, l, &np, nullptr, nullptr, nullptr));
+    std::vector<int> b(static_cast<size_t>(6) * std::max(np, 1));
+    check(af_amr_boxes(h_, l, b.data(), np));
+    std::vector<Box> out(static_cast<size_t>(np));
+    for (int i = 0; i < np; ++i)
+      for (int a = 0; a < 3; ++a) {
+        out[i].lo[a] = b[6 * i + a];
+        out[i].hi[a] = b[6 * i + 3 + a];
+      }
+    return out;
+  }
+  // Patch payloads of a level, patch after patch (ghost 0: interiors, 2: the
+  // blocks with their ghost layers), 5 doubles per cell, x fastest.
+  std::vector<double> patch_data(int l, int ghost = 0, bool old = false) const {
+    long cells = 0;
+    check(af_amr_patch_data_cells(h_, l, ghost, &cells));
+    std::vector<double> out(static_cast<size_t>(5 * cells));
+    check(af_amr_patch_data(h_, l, ghost, old ? 1 : 0, out.data()));
+    return out;
+  }
+  UniformGrid assemble_level(int l, double origin, double extent) const {
+    UniformGrid g(dim_, base_exp_ + l, origin, extent);
+    std::vector<double> aos(static_cast<size_t>(5) * g.block().interior_cells());
+    check(af_amr_assemble_level(h_, l, aos.data()));
+    from_aos(aos, g.block());
+    return g;
+  }
+  ConservedState total_conserved() const {
+    double t[5];
+    check(af_amr_total_conserved(h_, t));
+    ConservedState s;
+    s.rho = t[0];
+    s.mom = {t[1], t[2], t[3]};
+    s.rhoE = t[4];
+    return s;
+  }
+  long total_cells() const {
+    long a = 0, b = 0;
+    check(af_amr_counts(h_, &a, &b));
+    return a;
+  }
+  long composite_cells() const {
+    long a = 0, b = 0;
+    check(af_amr_counts(h_, &a, &b));
+    return b;
+  }
+  bool properly_nested() const {
+    int n = 0;
+    check(af_amr_properly_nested(h_, &n));
+    return n != 0;
+  }
+  std::string dump_boxes() const {
+    const char* t = nullptr;
+    check(af_amr_dump_boxes(h_, &t));
+    return t ? std::string(t) : std::string();
+  }
+
+ private:
+  af_amr* h_ = nullptr;
+  int dim_, base_exp_;
+};
+
+struct AmrDeviceResult {
+  std::unique_ptr<AmrDevice> hierarchy;
+  RunReport report;
+};
+
+// run_amr (amr_solver.cpp:62-133) on the device. AmrRunOptions::on_sample
+// observes a host PatchHierarchy, which this run does not build: the device
+// form of the callback takes the AmrDevice instead.
+using AmrSampleFn = std::function<void(long fine_steps_done, AmrDevice&)>;
+
+inline AmrDeviceResult run_amr(const CaseSpec& spec, int level, long n_steps,
+                               const SchemeConfig& scheme, const AmrRunOptions& options,
+                               const AmrSampleFn& sample = nullptr) {
+  if (options.on_sample)
+    throw ConfigError(
+        "gpu::run_amr: AmrRunOptions::on_sample observes a host PatchHierarchy, which the "
+        "device run does not build; pass a gpu::AmrSampleFn instead");
+  const int base_exp = amr_base_exp(spec.dim, level);
+  if (base_exp < 0) throw ConfigError("amr needs level >= 1, got " + std::to_string(level));
+  AmrOptions opts;
+  opts.max_levels = level - base_exp;
+  opts.time_refine = options.time_refine;
+  opts.flux_correction = options.flux_correction;
+  opts.eps_rho = options.eps_rho >= 0.0 ? options.eps_rho : spec.amr_eps_rho;
+  opts.eps_p = options.eps_p >= 0.0 ? options.eps_p : spec.amr_eps_p;
+  opts.cluster_efficiency = options.eta_tol >= 0.0 ? options.eta_tol : spec.cluster_efficiency;
+
+  AmrDeviceResult out;
+  out.hierarchy = std::make_unique<AmrDevice>(spec.dim, base_exp, spec.origin, spec.extent,
+                                              spec.bc, spec.gas, opts, scheme);
+  AmrDevice& h = *out.hierarchy;
+  RunReport& rep = out.report;
+  rep.method = options.time_refine ? Method::AMRLT : Method::AMR;
+  rep.case_name = spec.name;
+  rep.level = level;
+  rep.n_steps = n_steps;
+  rep.preset_scheme = scheme.is_preset();
+  const double dt_finest = spec.t_end / static_cast<double>(n_steps);
+  const long per_cycle = options.time_refine ? (1l << opts.max_levels) : 1;
+  if (n_steps % per_cycle != 0)
+    throw ConfigError("n_steps=" + std::to_string(n_steps) + " is not a multiple of the " +
+                      std::to_string(per_cycle) + " substeps of one time-refined cycle");
+  h.initialize([&spec](double x, double y, double z) { return spec.initial_state(x, y, z); });
+  rep.cells_per_step.assign(static_cast<size_t>(n_steps), 0);
+  rep.leaves_per_step.assign(static_cast<size_t>(n_steps), 0);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!sample) {
+    af_run_diag d{};
+    h.check(af_amr_run(h.handle(), n_steps, dt_finest, rep.cells_per_step.data(),
+                       rep.leaves_per_step.data(), &d));
+    rep.max_cfl = d.max_cfl;
+    rep.fallbacks = d.fallbacks;
+  } else {  // cycle by cycle, the observer after each (amr_solver.cpp:118-129)
+    for (long done = 0; done < n_steps; done += per_cycle) {
+      af_run_diag d{};
+      try {
+        h.check(af_amr_run(h.handle(), per_cycle, dt_finest, rep.cells_per_step.data() + done,
+                           rep.leaves_per_step.data() + done, &d));
+      } catch (const NonPhysicalState& e) {
+        // the device numbers its cycles per call: restore the run's cycle index
+        const std::string w = e.what();
+        const std::string pre = "cycle 0: ";
+        throw NonPhysicalState("cycle " + std::to_string(done / per_cycle) + ": " +
+                               (w.rfind(pre, 0) == 0 ? w.substr(pre.size()) : w));
+      }
+      rep.max_cfl = std::max(rep.max_cfl, d.max_cfl);
+      rep.fallbacks += d.fallbacks;
+      sample(done + per_cycle, h);
+    }
+  }
+  rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return out;
 }
 
