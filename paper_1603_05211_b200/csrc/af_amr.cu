@@ -240,25 +240,28 @@ std::vector<ABox> DeviceCluster::run(int dim, const uint8_t* d_flags, const uint
 
 // -------------------------------------------------------------- hierarchy --
 namespace {
-template <int D>
-ALv<D> view(int n, long cells, const int* pid, const uint8_t* ring, double* U, double* Uold,
-            double* G, double* Gold) {
+template <int D, class LevelT>
+ALv<D> view(const LevelT& L) {
   ALv<D> v;
-  v.n = n;
-  v.cells = cells;
-  v.pid = pid;
-  v.ring = ring;
-  v.U = U;
-  v.Uold = Uold;
-  v.G = G;
-  v.Gold = Gold;
+  v.n = L.n;
+  v.cells = L.cells;
+  v.pid = L.pid;
+  v.ring = nullptr;
+  v.U = L.U;
+  v.Uold = L.Uold;
+  v.G = L.G;
+  v.Gold = L.Gold;
+  v.boxes = L.d_boxes;
+  v.nb = (int)L.boxes.size();
+  v.off0 = L.d_off;
+  v.off1 = L.d_off + (v.nb + 1);
+  v.off2 = L.d_off + 2 * (v.nb + 1);
+  v.offF = L.d_off + 3 * (v.nb + 1);
+  v.tot0 = L.total;
+  v.tot1 = L.tot1;
+  v.tot2 = L.tot2;
+  v.totF = L.totF;
   return v;
-}
-__global__ void amr_copy_kernel(double* dst, const double* src, long n, const int* err) {
-  if (amr_failed(err)) return;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x)
-    dst[i] = src[i];
 }
 __global__ void amr_clear_regs_kernel(double* Rc, double* Rf, uint8_t* has, long nvals, int nslots) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nvals;
@@ -270,8 +273,7 @@ __global__ void amr_clear_regs_kernel(double* Rc, double* Rf, uint8_t* has, long
 }
 }  // namespace
 
-#define AMR_VIEW(D, L) \
-  view<D>((L).n, (L).cells, (L).pid, (L).ring, (L).U, (L).Uold, (L).G, (L).Gold)
+#define AMR_VIEW(D, L) view<D>(L)
 
 Amr::Amr(const af_config& cfg, const af_amr_options& opt) : cfg_(cfg), opt_(opt) {
   dim_ = cfg.dim;
@@ -307,6 +309,7 @@ Amr::~Amr() {
   for (Level& L : spare_) free_level(L);
   delete clusterer_;
   cudaFree(d_cb_);
+  cudaFree(d_cboff_);
   cudaFree(d_err_);
   cudaFree(d_flag_);
   cudaFree(d_rec_);
@@ -333,7 +336,6 @@ void Amr::alloc_level(Level& L, int l) {
   const size_t fb = sizeof(double) * (size_t)(dim_ + 2) * (size_t)L.cells;
   AF_CUDA(cudaMalloc(&L.pid, sizeof(int) * L.cells));
   AF_CUDA(cudaMalloc(&L.pid_new, sizeof(int) * L.cells));
-  AF_CUDA(cudaMalloc(&L.ring, L.cells));
   AF_CUDA(cudaMalloc(&L.U, fb));
   AF_CUDA(cudaMalloc(&L.Uold, fb));
   AF_CUDA(cudaMalloc(&L.G, fb));
@@ -352,7 +354,6 @@ void Amr::alloc_level(Level& L, int l) {
 void Amr::free_level(Level& L) {
   cudaFree(L.pid);
   cudaFree(L.pid_new);
-  cudaFree(L.ring);
   cudaFree(L.U);
   cudaFree(L.Uold);
   cudaFree(L.G);
@@ -395,45 +396,64 @@ void Amr::ensure_scratch(long cells, int n) {
   scr_cells_ = cells;
 }
 
-void Amr::upload_boxes(Level& L) {
-  const int nb = (int)L.boxes.size();
-  std::vector<int> bx((size_t)6 * nb);
-  std::vector<long> off((size_t)nb + 1, 0);
-  for (int i = 0; i < nb; ++i) {
-    for (int a = 0; a < 3; ++a) {
-      bx[6 * i + a] = L.boxes[i].lo[a];
-      bx[6 * i + 3 + a] = L.boxes[i].hi[a];
-    }
-    off[i + 1] = off[i] + L.boxes[i].volume();
-  }
-  L.total = off[nb];
-  if (nb + 1 > L.box_cap) {
-    AF_CUDA(cudaStreamSynchronize(stream_));
-    cudaFree(L.d_boxes);
-    cudaFree(L.d_off);
-    L.box_cap = 2 * (nb + 1) + 64;
-    AF_CUDA(cudaMalloc(&L.d_boxes, sizeof(int) * 6 * L.box_cap));
-    AF_CUDA(cudaMalloc(&L.d_off, sizeof(long) * L.box_cap));
-  }
-  // pageable sources: the copies are staged before the calls return
-  AF_CUDA(cudaMemcpyAsync(L.d_boxes, bx.data(), sizeof(int) * 6 * nb, cudaMemcpyHostToDevice, stream_));
-  AF_CUDA(cudaMemcpyAsync(L.d_off, off.data(), sizeof(long) * (nb + 1), cudaMemcpyHostToDevice, stream_));
-}
-
-void Amr::copy_field(double* dst, const double* src, long count) {
-  amr_copy_kernel<<<std::min<unsigned>(blocks_for(count), 148 * 16), 256, 0, stream_>>>(dst, src, count,
-                                                                                       d_err_);
-  launch_count();
-}
-
 static ABc bc_of(const af_config& c) {
   ABc b;
   for (int i = 0; i < 6; ++i) b.bc[i] = c.bc[i];
   return b;
 }
 
+void Amr::upload_boxes(Level& L) {
+  const int nb = (int)L.boxes.size();
+  std::vector<int> bx((size_t)6 * nb);
+  const size_t stride = (size_t)nb + 1;
+  std::vector<long> off(3 * stride + (size_t)nb * dim_ + 1, 0);
+  long* o0 = off.data();
+  long* o1 = o0 + stride;
+  long* o2 = o1 + stride;
+  long* oF = o2 + stride;
+  for (int i = 0; i < nb; ++i) {
+    const ABox& b = L.boxes[i];
+    long v1 = 1, v2 = 1;
+    for (int a = 0; a < 3; ++a) {
+      bx[6 * i + a] = b.lo[a];
+      bx[6 * i + 3 + a] = b.hi[a];
+      v1 *= b.extent(a) + (a < dim_ ? 2 : 0);
+      v2 *= b.extent(a) + (a < dim_ ? 4 : 0);
+    }
+    o0[i + 1] = o0[i] + b.volume();
+    o1[i + 1] = o1[i] + v1;
+    o2[i + 1] = o2[i] + v2;
+    for (int a = 0; a < dim_; ++a)
+      oF[i * dim_ + a + 1] = oF[i * dim_ + a] + b.volume() / b.extent(a) * (b.extent(a) + 1);
+  }
+  L.total = o0[nb];
+  L.tot1 = o1[nb];
+  L.tot2 = o2[nb];
+  L.totF = oF[(size_t)nb * dim_];
+  if (nb + 1 > L.box_cap) {
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(L.d_boxes);
+    cudaFree(L.d_off);
+    L.box_cap = 2 * (nb + 1) + 64;
+    AF_CUDA(cudaMalloc(&L.d_boxes, sizeof(int) * 6 * L.box_cap));
+    AF_CUDA(cudaMalloc(&L.d_off, sizeof(long) * 7 * L.box_cap));
+  }
+  // pageable sources: the copies are staged before the calls return
+  AF_CUDA(cudaMemcpyAsync(L.d_boxes, bx.data(), sizeof(int) * 6 * nb, cudaMemcpyHostToDevice, stream_));
+  AF_CUDA(cudaMemcpyAsync(L.d_off, off.data(), sizeof(long) * off.size(), cudaMemcpyHostToDevice, stream_));
+}
+
+void Amr::save_level(int l, bool restore) {
+  Level& L = lv_[l];
+  if (dim_ == 3)
+    amr_save_kernel<3><<<blocks_for(L.tot2), 256, 0, stream_>>>(AMR_VIEW(3, L), bc_of(cfg_), restore ? 1 : 0, d_err_);
+  else
+    amr_save_kernel<2><<<blocks_for(L.tot2), 256, 0, stream_>>>(AMR_VIEW(2, L), bc_of(cfg_), restore ? 1 : 0, d_err_);
+  launch_count();
+}
+
 // rebuild_domain (amr_hierarchy.cpp:58-62): the patch-id map of the level's
-// boxes (into pid_new while the old map is still needed) and the ghost ring
+// boxes (into pid_new while the old map is still needed) and the position lists
 template <int D>
 void Amr::rebuild_domain_t(int l, bool into_new) {
   Level& L = lv_[l];
@@ -444,10 +464,6 @@ void Amr::rebuild_domain_t(int l, bool into_new) {
     amr_setpid_kernel<D><<<blocks_for(L.total), 256, 0, stream_>>>(L.d_boxes, L.d_off,
                                                                    (int)L.boxes.size(), L.total, L.n, pid);
   launch_count();
-  if (!into_new) {
-    amr_ring_kernel<D><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, L.n, bc_of(cfg_), L.ring);
-    launch_count();
-  }
   AF_CUDA(cudaGetLastError());
 }
 
@@ -462,7 +478,7 @@ void Amr::sync_t(int l, double tau) {
   }
   const ALv<D> fine = AMR_VIEW(D, L);
   const ALv<D> coarse = l > 0 ? AMR_VIEW(D, lv_[l - 1]) : fine;
-  amr_sync_kernel<D><<<blocks_for(L.cells), 256, 0, stream_>>>(fine, coarse, l > 0, bc_of(cfg_), theta,
+  amr_sync_kernel<D><<<blocks_for(L.tot2), 256, 0, stream_>>>(fine, coarse, l > 0, bc_of(cfg_), theta,
                                                                cfg_.gamma - 1.0, d_err_);
   launch_count();
   AF_CUDA(cudaGetLastError());
@@ -498,9 +514,7 @@ void Amr::initialize(amr_ic_fn ic, void* user) {
       amr_put_kernel<2><<<blocks_for(L.total), 256, 0, stream_>>>(L.d_boxes, L.d_off, (int)L.boxes.size(),
                                                                   L.total, L.n, L.cells, d, L.U);
     launch_count();
-    const long cnt = (long)(dim_ + 2) * L.cells;
-    copy_field(L.Uold, L.U, cnt);
-    copy_field(L.Gold, L.G, cnt);
+    save_level(l, false);
     AF_CUDA(cudaStreamSynchronize(stream_));
     cudaFree(d);
   };
@@ -512,9 +526,7 @@ void Amr::initialize(amr_ic_fn ic, void* user) {
   }
   for (int l = 0; l < n_levels(); ++l) {
     sync_ghosts(l, 0.0);
-    const long cnt = (long)(dim_ + 2) * lv_[l].cells;
-    copy_field(lv_[l].Uold, lv_[l].U, cnt);
-    copy_field(lv_[l].Gold, lv_[l].G, cnt);
+    save_level(l, false);
   }
   check();
 }
@@ -533,31 +545,44 @@ void Amr::remesh_t(int l) {
     Level& S = lv_[src];
     sync_ghosts(src, S.t);
     const unsigned g = blocks_for(S.cells);
-    amr_flag_kernel<D><<<g, 256, 0, stream_>>>(AMR_VIEW(D, S), b, gm1, opt_.eps_rho, opt_.eps_p, m_tmp_);
+    AF_CUDA(cudaMemsetAsync(m_tmp_, 0, S.cells, stream_));
+    amr_flag_kernel<D><<<blocks_for(S.total), 256, 0, stream_>>>(AMR_VIEW(D, S), b, gm1, opt_.eps_rho, opt_.eps_p,
+                                                                m_tmp_);
     const uint8_t* nest = nullptr;
     if (m + 1 <= top && !fresh[m + 1].empty()) {
       // the next finer level's new boxes, coarsened twice and dilated, stay covered
       std::vector<int> cb;
+      std::vector<long> cboff(1, 0);
       for (const ABox& fb : fresh[m + 1]) {
         int lo[3], hi[3];
+        long vol = 1;
         for (int a = 0; a < 3; ++a) {
-          lo[a] = fb.lo[a] >> 2;
-          hi[a] = (fb.hi[a] + 3) >> 2;
+          lo[a] = std::max(fb.lo[a] >> 2, 0);
+          hi[a] = std::min((fb.hi[a] + 3) >> 2, a < D ? S.n : 1);
+          if (a >= D) {
+            lo[a] = 0;
+            hi[a] = 1;
+          }
+          vol *= std::max(hi[a] - lo[a], 0);
         }
-        if (D == 2) {
-          lo[2] = 0;
-          hi[2] = 1;
-        }
+        if (vol == 0) continue;
         cb.insert(cb.end(), {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]});
+        cboff.push_back(cboff.back() + vol);
       }
       if ((long)cb.size() > cb_cap_) {
         AF_CUDA(cudaStreamSynchronize(stream_));
         cudaFree(d_cb_);
+        cudaFree(d_cboff_);
         cb_cap_ = 2 * (long)cb.size() + 384;
         AF_CUDA(cudaMalloc(&d_cb_, sizeof(int) * cb_cap_));
+        AF_CUDA(cudaMalloc(&d_cboff_, sizeof(long) * (cb_cap_ / 6 + 2)));
       }
       AF_CUDA(cudaMemcpyAsync(d_cb_, cb.data(), sizeof(int) * cb.size(), cudaMemcpyHostToDevice, stream_));
-      amr_setbox_kernel<D><<<g, 256, 0, stream_>>>(d_cb_, (int)(cb.size() / 6), S.n, m_masked_);
+      AF_CUDA(cudaMemcpyAsync(d_cboff_, cboff.data(), sizeof(long) * cboff.size(), cudaMemcpyHostToDevice, stream_));
+      AF_CUDA(cudaMemsetAsync(m_masked_, 0, S.cells, stream_));
+      if (cboff.back())
+        amr_setbox_kernel<D><<<blocks_for(cboff.back()), 256, 0, stream_>>>(d_cb_, d_cboff_, (int)(cb.size() / 6),
+                                                                            cboff.back(), S.n, m_masked_);
       amr_dilate_kernel<D><<<g, 256, 0, stream_>>>(m_masked_, S.n, b, 1, nullptr, m_nest_);
       launch_count(2);
       nest = m_nest_;
@@ -592,16 +617,12 @@ void Amr::remesh_t(int l) {
     rebuild_domain_t<D>(m, /*into_new=*/true);
     ALv<D> nv = AMR_VIEW(D, L);
     nv.pid = L.pid_new;
-    amr_build_kernel<D><<<blocks_for(L.cells), 256, 0, stream_>>>(nv, L.pid, had ? 1 : 0,
+    amr_build_kernel<D><<<blocks_for(L.total), 256, 0, stream_>>>(nv, L.pid, had ? 1 : 0,
                                                                  AMR_VIEW(D, lv_[m - 1]), b, gm1, d_err_);
     launch_count();
     std::swap(L.pid, L.pid_new);
-    amr_ring_kernel<D><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, L.n, b, L.ring);
-    launch_count();
-    const long cnt = (long)(D + 2) * L.cells;
-    copy_field(L.Uold, L.U, cnt);  // p.data_old = p.data before the sync
     sync_ghosts(m, L.t);
-    copy_field(L.Gold, L.G, cnt);
+    save_level(m, false);  // data_old = data, interiors and the fresh ghosts
     new_top = m;
   }
   while (n_levels() - 1 > new_top) {
@@ -615,7 +636,7 @@ void Amr::remesh_t(int l) {
   for (int m = l; m < n_levels(); ++m) rebuild_registers(m);
   // NestingViolation (amr_hierarchy.cpp:340-341), reported by the next check()
   for (int m = std::max(l, 1); m < n_levels(); ++m) {
-    amr_nested_kernel<D><<<blocks_for(lv_[m].cells), 256, 0, stream_>>>(lv_[m].pid, lv_[m].n, lv_[m - 1].pid,
+    amr_nested_kernel<D><<<blocks_for(lv_[m].total), 256, 0, stream_>>>(AMR_VIEW(D, lv_[m]), lv_[m - 1].pid,
                                                                         d_err_ + 2);
     launch_count();
   }
@@ -636,10 +657,7 @@ void Amr::remesh(int l) {
 void Amr::rebuild_registers(int l) {
   Level& L = lv_[l];
   L.nslots = 0;
-  if (l + 1 >= n_levels()) {
-    AF_CUDA(cudaMemsetAsync(L.regmask, 0, L.cells, stream_));
-    return;
-  }
+  if (l + 1 >= n_levels()) return;
   const Level& Fn = lv_[l + 1];
   // every register face is a coarse face of a fine box's surface: an upper
   // bound the host knows without asking the device
@@ -670,11 +688,11 @@ void Amr::rebuild_registers(int l) {
   AF_CUDA(cudaMemsetAsync(d_flag_, 0, 2 * sizeof(int), stream_));
   AF_CUDA(cudaMemsetAsync(L.slot_face, 0xff, L.nslots, stream_));
   if (dim_ == 3)
-    amr_reg_alloc_kernel<3><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask,
+    amr_reg_alloc_kernel<3><<<blocks_for(L.total), 256, 0, stream_>>>(AMR_VIEW(3, L), Fn.pid, b, L.regbase, L.regmask,
                                                                       d_flag_, L.slot_cell, L.slot_face, L.nslots,
                                                                       d_err_);
   else
-    amr_reg_alloc_kernel<2><<<blocks_for(L.cells), 256, 0, stream_>>>(L.pid, Fn.pid, L.n, b, L.regbase, L.regmask,
+    amr_reg_alloc_kernel<2><<<blocks_for(L.total), 256, 0, stream_>>>(AMR_VIEW(2, L), Fn.pid, b, L.regbase, L.regmask,
                                                                       d_flag_, L.slot_cell, L.slot_face, L.nslots,
                                                                       d_err_);
   launch_count();
@@ -701,17 +719,13 @@ void Amr::update_t(int l, double dt) {
   ARec* rec = static_cast<ARec*>(d_rec_) + call;
   const ABc b = bc_of(cfg_);
   const ALv<D> v = AMR_VIEW(D, L);
-  const long cnt = (long)(D + 2) * L.cells;
   const int n = L.n;
-  const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
-  const long np = n + 2, padded = D == 3 ? np * np * np : np * np;
   const double h = dx(l), inv_dx = 1.0 / h, gamma = cfg_.gamma;
-  const unsigned gc = blocks_for(L.cells), gf = blocks_for(D * per);
+  const unsigned gc = blocks_for(L.total), gb = blocks_for(L.tot2), gf = blocks_for(L.totF);
 
   cell_updates_ += L.total * (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK ? 1 : 2);
   L.t_old = L.t;
-  copy_field(L.Uold, L.U, cnt);  // p.data_old = p.data
-  copy_field(L.Gold, L.G, cnt);
+  save_level(l, false);  // p.data_old = p.data
 
   auto registers = [&] {  // accumulate_registers, fine side then coarse side
     if (l > 0 && lv_[l - 1].nslots) {
@@ -728,8 +742,8 @@ void Amr::update_t(int l, double dt) {
   };
 
   if (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK) {
-    amr_prims_kernel<D><<<gc, 256, 0, stream_>>>(v, W_, gamma, rec, d_err_, 2 * call + 1);
-    amr_predict_kernel<D, S><<<blocks_for(padded), 256, 0, stream_>>>(v, b, W_, DU_, 0.5 * dt / h,
+    amr_prims_kernel<D><<<gb, 256, 0, stream_>>>(v, b, W_, gamma, rec, d_err_, 2 * call + 1);
+    amr_predict_kernel<D, S><<<blocks_for(L.tot1), 256, 0, stream_>>>(v, b, W_, DU_, 0.5 * dt / h,
                                                                      gamma - 1.0, rec, d_err_);
     amr_faces_hancock<D, S><<<gf, 256, 0, stream_>>>(v, b, W_, DU_, F_, gamma, rec, d_err_);
     amr_update_kernel<D><<<gc, 256, 0, stream_>>>(v, L.U, F_, inv_dx, dt, d_err_);
@@ -738,16 +752,16 @@ void Amr::update_t(int l, double dt) {
   } else {
     // stage 1 of every patch, the midpoint ghosts, stage 2 (the patch blocks
     // keep the ghosts of time t afterwards: out = saved)
-    amr_prims_kernel<D><<<gc, 256, 0, stream_>>>(v, W_, gamma, rec, d_err_, 2 * call);
+    amr_prims_kernel<D><<<gb, 256, 0, stream_>>>(v, b, W_, gamma, rec, d_err_, 2 * call);
     amr_faces_rk2<D, S><<<gf, 256, 0, stream_>>>(v, b, W_, F_, gamma, rec, d_err_);
     amr_update_kernel<D><<<gc, 256, 0, stream_>>>(v, L.Uold, F_, inv_dx, 0.5 * dt, d_err_);
     launch_count(3);
     sync_ghosts(l, L.t + 0.5 * dt);
-    amr_prims_kernel<D><<<gc, 256, 0, stream_>>>(v, W_, gamma, rec, d_err_, 2 * call + 1);
+    amr_prims_kernel<D><<<gb, 256, 0, stream_>>>(v, b, W_, gamma, rec, d_err_, 2 * call + 1);
     amr_faces_rk2<D, S><<<gf, 256, 0, stream_>>>(v, b, W_, F_, gamma, rec, d_err_);
     amr_update_kernel<D><<<gc, 256, 0, stream_>>>(v, L.Uold, F_, inv_dx, dt, d_err_);
     launch_count(3);
-    copy_field(L.G, L.Gold, cnt);
+    save_level(l, true);
     registers();
   }
   L.t += dt;
@@ -899,9 +913,9 @@ void Amr::average_down(int l) {
   if (std::fabs(Fn.t - C.t) > 1e-12 * std::max(1.0, std::fabs(C.t)))
     throw Error(AF_E_LEVEL_MISMATCH, "average_down: levels at t=" + f6(C.t) + " and t=" + f6(Fn.t));
   if (dim_ == 3)
-    amr_average_down_kernel<3><<<blocks_for(C.cells), 256, 0, stream_>>>(AMR_VIEW(3, C), AMR_VIEW(3, lv_[l + 1]), d_err_);
+    amr_average_down_kernel<3><<<blocks_for(C.total), 256, 0, stream_>>>(AMR_VIEW(3, C), AMR_VIEW(3, lv_[l + 1]), d_err_);
   else
-    amr_average_down_kernel<2><<<blocks_for(C.cells), 256, 0, stream_>>>(AMR_VIEW(2, C), AMR_VIEW(2, lv_[l + 1]), d_err_);
+    amr_average_down_kernel<2><<<blocks_for(C.total), 256, 0, stream_>>>(AMR_VIEW(2, C), AMR_VIEW(2, lv_[l + 1]), d_err_);
   launch_count();
   AF_CUDA(cudaGetLastError());
 }
@@ -913,11 +927,13 @@ void Amr::flux_correct(int l) {
   if (opt_.flux_correction) {
     const double inv_h = 1.0 / dx(l);
     if (dim_ == 3)
-      amr_flux_correct_kernel<3><<<blocks_for(L.cells), 256, 0, stream_>>>(AMR_VIEW(3, L), L.regbase, L.regmask, L.Rc,
-                                                                          L.Rf, L.has, L.nslots, inv_h, d_err_);
+      amr_flux_correct_kernel<3><<<blocks_for(L.nslots), 256, 0, stream_>>>(AMR_VIEW(3, L), L.regbase, L.regmask,
+                                                                           L.slot_cell, L.slot_face, L.Rc, L.Rf, L.has,
+                                                                           L.nslots, inv_h, d_err_);
     else
-      amr_flux_correct_kernel<2><<<blocks_for(L.cells), 256, 0, stream_>>>(AMR_VIEW(2, L), L.regbase, L.regmask, L.Rc,
-                                                                          L.Rf, L.has, L.nslots, inv_h, d_err_);
+      amr_flux_correct_kernel<2><<<blocks_for(L.nslots), 256, 0, stream_>>>(AMR_VIEW(2, L), L.regbase, L.regmask,
+                                                                           L.slot_cell, L.slot_face, L.Rc, L.Rf, L.has,
+                                                                           L.nslots, inv_h, d_err_);
     launch_count();
   }
   clear_registers(l);
@@ -933,7 +949,7 @@ void Amr::total_conserved(double out5[5]) {
     Level& L = lv_[l];
     AF_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * 5, stream_));
     const int* fp = l + 1 < n_levels() ? lv_[l + 1].pid : nullptr;
-    const unsigned g = std::min<unsigned>(blocks_for(L.cells), 1184);
+    const unsigned g = std::min<unsigned>(blocks_for(L.total), 1184);
     if (dim_ == 3)
       amr_sum_kernel<3><<<g, 256, 0, stream_>>>(AMR_VIEW(3, L), fp, d);
     else
@@ -977,9 +993,9 @@ bool Amr::properly_nested() {
   for (int l = 1; l < n_levels(); ++l) {
     const Level& Fn = lv_[l];
     if (dim_ == 3)
-      amr_nested_kernel<3><<<blocks_for(Fn.cells), 256, 0, stream_>>>(Fn.pid, Fn.n, lv_[l - 1].pid, d_flag_);
+      amr_nested_kernel<3><<<blocks_for(Fn.total), 256, 0, stream_>>>(AMR_VIEW(3, Fn), lv_[l - 1].pid, d_flag_);
     else
-      amr_nested_kernel<2><<<blocks_for(Fn.cells), 256, 0, stream_>>>(Fn.pid, Fn.n, lv_[l - 1].pid, d_flag_);
+      amr_nested_kernel<2><<<blocks_for(Fn.total), 256, 0, stream_>>>(AMR_VIEW(2, Fn), lv_[l - 1].pid, d_flag_);
     launch_count();
   }
   int bad = 0;

@@ -104,12 +104,12 @@ class Amr {
     int n = 0;
     long cells = 0;
     int *pid = nullptr, *pid_new = nullptr;
-    uint8_t* ring = nullptr;
     double *U = nullptr, *Uold = nullptr, *G = nullptr, *Gold = nullptr;
     int* d_boxes = nullptr;
-    long* d_off = nullptr;
+    long* d_off = nullptr;  // four prefix arrays: interiors, shells, blocks, faces per (box, axis)
     int box_cap = 0;
     long total = 0;  // cells of the boxes
+    long tot1 = 0, tot2 = 0, totF = 0;
     // flux registers of the pair (this level, next finer)
     int* regbase = nullptr;
     uint8_t* regmask = nullptr;
@@ -136,7 +136,7 @@ class Amr {
   void free_level(Level& L);
   void upload_boxes(Level& L);
   void ensure_scratch(long cells, int n);
-  void copy_field(double* dst, const double* src, long count);
+  void save_level(int l, bool restore);  // data_old = data (or the ghosts back from data_old)
   void rebuild_registers(int l);
   void clear_registers(int l);
   void check();            // synchronise, fold the records, throw a pending error
@@ -167,6 +167,7 @@ class Amr {
           *m_masked_ = nullptr;
   DeviceCluster* clusterer_ = nullptr;
   int* d_cb_ = nullptr;  // nest boxes of remesh
+  long* d_cboff_ = nullptr;
   long cb_cap_ = 0;
   long launches_ = 0;
   long cell_updates_ = 0;

@@ -37,6 +37,14 @@ struct ALv {  // one level
   double* Uold;
   double* G;
   double* Gold;
+  // the level's patches: boxes (6 ints each) and the prefix offsets of four
+  // position lists -- interiors, boxes grown by one cell (the predictor's
+  // shell), by two (the blocks with their ghosts), and the faces per (box,
+  // axis) -- so a launch walks the patches' positions, as the reference does
+  const int* boxes;
+  const long *off0, *off1, *off2, *offF;
+  int nb;
+  long tot0, tot1, tot2, totF;
 };
 
 struct ABc {
@@ -101,6 +109,39 @@ __device__ __forceinline__ bool a_wrap(int n, const ABc& b, int* p) {
     p[a] = ((p[a] % n) + n) % n;
   }
   return true;
+}
+
+// boxes as 6 ints (lo[3], hi[3]); off[i] = positions of the boxes before box i
+__device__ __forceinline__ int a_find_box(const long* off, int nb, long t) {
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ void a_box_cell(const int* bx, long r, int* p) {
+  const int ex = bx[3] - bx[0], ey = bx[4] - bx[1];
+  p[0] = bx[0] + (int)(r % ex);
+  const long t = r / ex;
+  p[1] = bx[1] + (int)(t % ey);
+  p[2] = bx[2] + (int)(t / ey);
+}
+// position t of the list of the boxes grown by `grow` cells along the active
+// axes (unwrapped: it may lie beyond the level's index range); returns the box
+template <int D>
+__device__ __forceinline__ int a_list_pos(const int* boxes, const long* off, int nb, int grow,
+                                          long t, int* p) {
+  const int bi = a_find_box(off, nb, t);
+  int gb[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int g = a < D ? grow : 0;
+    gb[a] = boxes[6 * bi + a] - g;
+    gb[3 + a] = boxes[6 * bi + 3 + a] + g;
+  }
+  a_box_cell(gb, t - off[bi], p);
+  return bi;
 }
 
 template <int D>
@@ -208,48 +249,6 @@ __device__ __forceinline__ bool a_coarse_interp(const ALv<D>& c, const ABc& b, c
 }
 
 // ---------------------------------------------------------------- masks --
-// ring[p] = 1 where p lies outside the domain within Chebyshev distance 2 of it
-template <int D>
-__global__ void __launch_bounds__(256) amr_ring_kernel(const int* pid, int n, ABc b,
-                                                       uint8_t* ring) {
-  const long cells = D == 3 ? (long)n * n * n : (long)n * n;
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= cells) return;
-  uint8_t r = 0;
-  if (pid[c] < 0) {
-    int p[3];
-    a_coords<D>(n, c, p);
-    for (int dk = (D == 3 ? -2 : 0); dk <= (D == 3 ? 2 : 0) && !r; ++dk)
-      for (int dj = -2; dj <= 2 && !r; ++dj)
-        for (int di = -2; di <= 2; ++di) {
-          int q[3] = {p[0] + di, p[1] + dj, p[2] + dk};
-          if (!a_wrap<D>(n, b, q)) continue;
-          if (pid[a_idx<D>(n, q)] >= 0) {
-            r = 1;
-            break;
-          }
-        }
-  }
-  ring[c] = r;
-}
-
-// boxes as 6 ints (lo[3], hi[3]); off[i] = cells of the boxes before box i
-__device__ __forceinline__ int a_find_box(const long* off, int nb, long t) {
-  int lo = 0, hi = nb - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= t) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-__device__ __forceinline__ void a_box_cell(const int* bx, long r, int* p) {
-  const int ex = bx[3] - bx[0], ey = bx[4] - bx[1];
-  p[0] = bx[0] + (int)(r % ex);
-  const long t = r / ex;
-  p[1] = bx[1] + (int)(t % ey);
-  p[2] = bx[2] + (int)(t / ey);
-}
-
 template <int D>
 __global__ void __launch_bounds__(256) amr_setpid_kernel(const int* boxes, const long* off, int nb,
                                                          long total, int n, int* pid) {
@@ -315,16 +314,18 @@ __global__ void __launch_bounds__(256) amr_get_kernel(const int* boxes, const lo
 template <int D>
 __global__ void __launch_bounds__(256) amr_sync_kernel(ALv<D> lv, ALv<D> co, int has_coarse, ABc b,
                                                        double theta, double gm1, int* err) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= lv.cells || amr_failed(err)) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot2 || amr_failed(err)) return;
+  int p[3];
+  a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  if (!a_wrap<D>(lv.n, b, p)) return;  // beyond a physical boundary: read through a_map
+  const long c = a_idx<D>(lv.n, p);
   if (lv.pid[c] >= 0) {
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) lv.G[m * lv.cells + c] = lv.U[m * lv.cells + c];
     return;
   }
-  if (!lv.ring[c] || !has_coarse) return;
-  int p[3];
-  a_coords<D>(lv.n, c, p);
+  if (!has_coarse) return;
   Cons<D> q;
   if (!a_coarse_interp<D>(co, b, p, theta, gm1, q)) {  // MissingBracketingStates
     if (atomicCAS(err, 0, 2) == 0) err[1] = (int)c;
@@ -333,17 +334,41 @@ __global__ void __launch_bounds__(256) amr_sync_kernel(ALv<D> lv, ALv<D> co, int
   a_store<D>(lv.G, lv.cells, c, q);
 }
 
+// Patch::data_old = Patch::data for every patch (interiors and ghosts), and
+// the way back for the ghosts (update_level's RK2 branch leaves the blocks
+// with the ghosts of time t, amr_hierarchy.cpp:508-519)
+template <int D>
+__global__ void __launch_bounds__(256) amr_save_kernel(ALv<D> lv, ABc b, int restore, const int* err) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot2 || amr_failed(err)) return;
+  int p[3];
+  a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  if (!a_wrap<D>(lv.n, b, p)) return;
+  const long c = a_idx<D>(lv.n, p);
+  if (restore) {
+#pragma unroll
+    for (int m = 0; m < D + 2; ++m) lv.G[m * lv.cells + c] = lv.Gold[m * lv.cells + c];
+    return;
+  }
+  const bool dom = lv.pid[c] >= 0;
+#pragma unroll
+  for (int m = 0; m < D + 2; ++m) {
+    lv.Gold[m * lv.cells + c] = lv.G[m * lv.cells + c];
+    if (dom) lv.Uold[m * lv.cells + c] = lv.U[m * lv.cells + c];
+  }
+}
+
 // remesh (amr_hierarchy.cpp:311-320): cells of the new domain keep the old
 // patch value where the level held one, else take the coarse interpolation.
 template <int D>
 __global__ void __launch_bounds__(256) amr_build_kernel(ALv<D> lv, const int* old_pid, int had,
                                                         ALv<D> co, ABc b, double gm1, int* err) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= lv.cells || amr_failed(err)) return;
-  if (lv.pid[c] < 0) return;
-  if (had && old_pid[c] >= 0) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot0 || amr_failed(err)) return;
   int p[3];
-  a_coords<D>(lv.n, c, p);
+  a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+  const long c = a_idx<D>(lv.n, p);
+  if (had && old_pid[c] >= 0) return;
   Cons<D> q;
   if (!a_coarse_interp<D>(co, b, p, 1.0, gm1, q)) {
     if (atomicCAS(err, 0, 2) == 0) err[1] = (int)c;
@@ -353,16 +378,17 @@ __global__ void __launch_bounds__(256) amr_build_kernel(ALv<D> lv, const int* ol
 }
 
 // ------------------------------------------------------------ flag_cells --
-// flag_cells (amr_cluster.cpp:52-77) on the synced level.
+// flag_cells (amr_cluster.cpp:52-77) on the synced level (flags cleared before).
 template <int D>
 __global__ void __launch_bounds__(256) amr_flag_kernel(ALv<D> lv, ABc b, double gm1, double eps_rho,
                                                        double eps_p, uint8_t* flags) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= lv.cells) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot0) return;
+  int p[3];
+  a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+  const long c = a_idx<D>(lv.n, p);
   uint8_t f = 0;
-  if (lv.pid[c] >= 0) {
-    int p[3];
-    a_coords<D>(lv.n, c, p);
+  {
     const Prim<D> w0 = primitives(a_load<D>(lv.G, lv.cells, c), gm1);
     for (int a = 1; a < (1 << D) && !f; ++a) {
       int q[3] = {p[0] + (a & 1), p[1] + ((a >> 1) & 1), p[2] + ((a >> 2) & 1)};
@@ -397,22 +423,16 @@ __global__ void __launch_bounds__(256) amr_dilate_kernel(const uint8_t* in, int 
   out[c] = r;
 }
 
-// set_box of each listed box (clipped to the level), amr_cluster.cpp:20-26
+// set_box of each listed box (clipped to the level by the host; the mask
+// cleared before), amr_cluster.cpp:20-26
 template <int D>
-__global__ void __launch_bounds__(256) amr_setbox_kernel(const int* boxes, int nb, int n,
-                                                         uint8_t* mask) {
-  const long cells = D == 3 ? (long)n * n * n : (long)n * n;
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= cells) return;
+__global__ void __launch_bounds__(256) amr_setbox_kernel(const int* boxes, const long* off, int nb,
+                                                         long total, int n, uint8_t* mask) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= total) return;
   int p[3];
-  a_coords<D>(n, c, p);
-  uint8_t r = 0;
-  for (int i = 0; i < nb && !r; ++i) {
-    const int* bx = boxes + 6 * i;
-    r = p[0] >= bx[0] && p[0] < bx[3] && p[1] >= bx[1] && p[1] < bx[4] && p[2] >= bx[2] &&
-        p[2] < bx[5];
-  }
-  mask[c] = r;
+  a_list_pos<D>(boxes, off, nb, 0, t, p);
+  mask[a_idx<D>(n, p)] = 1;
 }
 
 // allowed (amr_hierarchy.cpp:259-284): domain cells whose whole 3^d
@@ -448,15 +468,13 @@ __global__ void __launch_bounds__(256) amr_allowed_kernel(const int* pid, int n,
 
 // properly_nested (amr_hierarchy.cpp:344-356)
 template <int D>
-__global__ void __launch_bounds__(256) amr_nested_kernel(const int* fine, int nf, const int* coarse,
-                                                         int* bad) {
-  const long cells = D == 3 ? (long)nf * nf * nf : (long)nf * nf;
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= cells || fine[c] < 0) return;
+__global__ void __launch_bounds__(256) amr_nested_kernel(ALv<D> fine, const int* coarse, int* bad) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= fine.tot0) return;
   int p[3];
-  a_coords<D>(nf, c, p);
+  a_list_pos<D>(fine.boxes, fine.off0, fine.nb, 0, t, p);
   int q[3] = {p[0] >> 1, p[1] >> 1, D == 3 ? p[2] >> 1 : 0};
-  if (coarse[a_idx<D>(nf >> 1, q)] < 0) *bad = 1;
+  if (coarse[a_idx<D>(fine.n >> 1, q)] < 0) *bad = 1;
 }
 
 // ------------------------------------------------------------ the update --
@@ -465,17 +483,20 @@ struct ARec {                    // one update_level call
   unsigned long long fallbacks;
 };
 
-// build_primitives (step.cpp:18-49) of every patch block at once: W of the
-// domain and the ring; the speed maximum over the interiors.
+// build_primitives (step.cpp:18-49) of every patch block: W at the blocks'
+// positions; the speed maximum over the interiors.
 template <int D>
-__global__ void __launch_bounds__(256) amr_prims_kernel(ALv<D> lv, double* W, double gamma,
+__global__ void __launch_bounds__(256) amr_prims_kernel(ALv<D> lv, ABc b, double* W, double gamma,
                                                         ARec* rec, int* err, int tag) {
   __shared__ double red[8];
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   double wave = 0.0;
-  if (c < lv.cells && !amr_failed(err)) {
-    const bool dom = lv.pid[c] >= 0;
-    if (dom || lv.ring[c]) {
+  if (t < lv.tot2 && !amr_failed(err)) {
+    int p[3];
+    const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+    const bool inside = a_inrange<D>(lv.n, p);
+    if (a_wrap<D>(lv.n, b, p)) {
+      const long c = a_idx<D>(lv.n, p);
       const Cons<D> q = a_load<D>(lv.G, lv.cells, c);
       const Prim<D> w = primitives(q, gamma - 1.0);
       if (!cell_ok(q, w) && atomicCAS(err, 0, 1) == 0) err[1] = tag;
@@ -483,7 +504,7 @@ __global__ void __launch_bounds__(256) amr_prims_kernel(ALv<D> lv, double* W, do
 #pragma unroll
       for (int d = 0; d < D; ++d) W[(1 + d) * lv.cells + c] = w.v[d];
       W[(D + 1) * lv.cells + c] = w.p;
-      if (dom) {
+      if (inside && lv.pid[c] == bi) {
         double s, m;
         wave_speeds(w, gamma, s, m);
         wave = m;
@@ -499,36 +520,38 @@ __device__ __forceinline__ long a_face_index(int n, int ax, const int* p) {
   return D == 3 ? ((long)p[2] * d1 + p[1]) * d0 + p[0] : (long)p[1] * d0 + p[0];
 }
 
-// how many patches evaluate the face between lo and hi (unwrapped positions)
+// face t of the level's face list: the patch, the axis and the (unwrapped)
+// position of the face's high cell; the face index along the axis is p[ax]
 template <int D>
-__device__ __forceinline__ int a_face_mult(const int* pid, int n, const int* lo, const int* hi) {
-  const int pl = a_inrange<D>(n, lo) ? pid[a_idx<D>(n, lo)] : -1;
-  const int ph = a_inrange<D>(n, hi) ? pid[a_idx<D>(n, hi)] : -1;
-  if (pl < 0 && ph < 0) return 0;
-  return (pl >= 0 && ph >= 0 && pl != ph) ? 2 : 1;
+__device__ __forceinline__ int a_face_pos(const ALv<D>& lv, long t, int* p) {
+  const int e = a_find_box(lv.offF, lv.nb * D, t);
+  const int bi = e / D, ax = e - bi * D;
+  int fb[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    fb[a] = lv.boxes[6 * bi + a];
+    fb[3 + a] = lv.boxes[6 * bi + 3 + a] + (a == ax ? 1 : 0);
+  }
+  a_box_cell(fb, t - lv.offF[e], p);
+  return ax;
 }
 
-// accumulate_rhs' fluxes (step.cpp:57-89) of every face a patch evaluates,
-// one thread per face, into F (SoA, component stride D*per).
+// accumulate_rhs' fluxes (step.cpp:57-89) of every face of every patch, one
+// thread per (patch, face), into F (SoA over the level's faces, component
+// stride D*per). A face on a seam is evaluated by both patches (the same bits
+// twice) and counts its fallback for each, as the reference's patch loop does.
 template <int D, int S>
 __global__ void __launch_bounds__(256) amr_faces_rk2(ALv<D> lv, ABc b, const double* W, double* F,
                                                      double gamma, ARec* rec, int* err) {
   const int n = lv.n;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
-  const long f = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (f >= D * per || amr_failed(err)) return;
-  const int ax = (int)(f / per);
-  const long r = f - ax * per;
-  const int d0 = ax == 0 ? n + 1 : n, d1 = ax == 1 ? n + 1 : n;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.totF || amr_failed(err)) return;
   int p[3];
-  p[0] = (int)(r % d0);
-  const long t = r / d0;
-  p[1] = (int)(t % d1);
-  p[2] = D == 3 ? (int)(t / d1) : 0;
+  const int ax = a_face_pos<D>(lv, t, p);
+  const long f = ax * per + a_face_index<D>(n, ax, p);
   int lo[3] = {p[0], p[1], p[2]};
   lo[ax] -= 1;
-  const int mult = a_face_mult<D>(lv.pid, n, lo, p);
-  if (!mult) return;
   const double gm1 = gamma - 1.0, rgm1 = 1.0 / gm1;
   Prim<D> ws[4];
 #pragma unroll
@@ -544,7 +567,7 @@ __global__ void __launch_bounds__(256) amr_faces_rk2(ALv<D> lv, ABc b, const dou
     const Cons<D> ql = a_ghost<D>(lv.G, n, lv.cells, b, lo);
     const Cons<D> qr = a_ghost<D>(lv.G, n, lv.cells, b, p);
     Fx = num_flux<D, S>(ql, ws[1], qr, ws[2], ax, gamma);
-    atomicAdd(&rec->fallbacks, (unsigned long long)mult);
+    atomicAdd(&rec->fallbacks, 1ull);
   } else {
     Fx = recon_flux_fast<D, S>(l, rr, ax, gamma, gm1, rgm1);
   }
@@ -561,14 +584,14 @@ template <int D>
 __global__ void __launch_bounds__(256) amr_update_kernel(ALv<D> lv, const double* base,
                                                          const double* F, double inv_dx, double sdt,
                                                          int* err) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= lv.cells || amr_failed(err)) return;
-  if (lv.pid[c] < 0) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot0 || amr_failed(err)) return;
   const int n = lv.n;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
   const long cs = D * per;
   int p[3];
-  a_coords<D>(n, c, p);
+  a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+  const long c = a_idx<D>(n, p);
   long fl[D], fh[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -590,34 +613,21 @@ __global__ void __launch_bounds__(256) amr_update_kernel(ALv<D> lv, const double
 }
 
 // MUSCL-Hancock predictor (step.cpp:160-181) over every patch's interior plus
-// its one-cell shell: positions -1..n per axis, DU padded by one cell.
+// its one-cell shell (positions -1..n per axis, DU padded by one cell). A
+// position two patches hold is evaluated by both (the same bits) and counts
+// its fallbacks for each.
 template <int D, int S>
 __global__ void __launch_bounds__(256) amr_predict_kernel(ALv<D> lv, ABc b, const double* W,
                                                           double* DU, double half_dt_dx, double gm1,
                                                           ARec* rec, int* err) {
   const int n = lv.n, np = n + 2;
   const long padded = D == 3 ? (long)np * np * np : (long)np * np;
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= padded || amr_failed(err)) return;
+  const long tl = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (tl >= lv.tot1 || amr_failed(err)) return;
   int q[3];
-  q[0] = (int)(t % np) - 1;
-  const long u = t / np;
-  q[1] = (int)(u % np) - 1;
-  q[2] = D == 3 ? (int)(u / np) - 1 : 0;
-  // the patches whose shell or interior holds q
-  int seen[27], ns = 0;
-  for (int dk = (D == 3 ? -1 : 0); dk <= (D == 3 ? 1 : 0); ++dk)
-    for (int dj = -1; dj <= 1; ++dj)
-      for (int di = -1; di <= 1; ++di) {
-        const int c[3] = {q[0] + di, q[1] + dj, q[2] + dk};
-        if (!a_inrange<D>(n, c)) continue;
-        const int id = lv.pid[a_idx<D>(n, c)];
-        if (id < 0) continue;
-        bool dup = false;
-        for (int s = 0; s < ns; ++s) dup = dup || seen[s] == id;
-        if (!dup) seen[ns++] = id;
-      }
-  if (!ns) return;
+  a_list_pos<D>(lv.boxes, lv.off1, lv.nb, 1, tl, q);
+  const long t = D == 3 ? ((long)(q[2] + 1) * np + (q[1] + 1)) * np + (q[0] + 1)
+                        : (long)(q[1] + 1) * np + (q[0] + 1);
   const Prim<D> w0 = a_ghostw<D>(W, n, lv.cells, b, q);
   double acc[D + 2];
 #pragma unroll
@@ -642,7 +652,7 @@ __global__ void __launch_bounds__(256) amr_predict_kernel(ALv<D> lv, ABc b, cons
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) acc[m] = acc[m] - (fp[m] - fm[m]) * half_dt_dx;
   }
-  if (nfb) atomicAdd(&rec->fallbacks, (unsigned long long)(nfb * ns));
+  if (nfb) atomicAdd(&rec->fallbacks, (unsigned long long)nfb);
 #pragma unroll
   for (int m = 0; m < D + 2; ++m) DU[m * padded + t] = acc[m];
 }
@@ -655,20 +665,13 @@ __global__ void __launch_bounds__(256) amr_faces_hancock(ALv<D> lv, ABc b, const
   const int n = lv.n, np = n + 2;
   const long padded = D == 3 ? (long)np * np * np : (long)np * np;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
-  const long f = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (f >= D * per || amr_failed(err)) return;
-  const int ax = (int)(f / per);
-  const long r = f - ax * per;
-  const int d0 = ax == 0 ? n + 1 : n, d1 = ax == 1 ? n + 1 : n;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.totF || amr_failed(err)) return;
   int cr[3];
-  cr[0] = (int)(r % d0);
-  const long t = r / d0;
-  cr[1] = (int)(t % d1);
-  cr[2] = D == 3 ? (int)(t / d1) : 0;
+  const int ax = a_face_pos<D>(lv, t, cr);
+  const long f = ax * per + a_face_index<D>(n, ax, cr);
   int cl[3] = {cr[0], cr[1], cr[2]};
   cl[ax] -= 1;
-  const int mult = a_face_mult<D>(lv.pid, n, cl, cr);
-  if (!mult) return;
   const double gm1 = gamma - 1.0;
   Prim<D> w[4];
 #pragma unroll
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(256) amr_faces_hancock(ALv<D> lv, ABc b, const
     if (!phys_state(ur, gm1)) ur = qr;
     ++nfb;
   }
-  if (nfb) atomicAdd(&rec->fallbacks, (unsigned long long)(nfb * mult));
+  if (nfb) atomicAdd(&rec->fallbacks, (unsigned long long)nfb);
   const Cons<D> Fx = num_flux<D, S>(ul, primitives(ul, gm1), ur, primitives(ur, gm1), ax, gamma);
   const long cs = D * per;
   F[f] = Fx.rho;
@@ -751,16 +754,16 @@ __device__ __forceinline__ uint8_t a_reg_mask(const int* pid, const int* fpid, i
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) amr_reg_alloc_kernel(const int* pid, const int* fpid, int n,
-                                                            ABc b, int* regbase, uint8_t* regmask,
+__global__ void __launch_bounds__(256) amr_reg_alloc_kernel(ALv<D> lv, const int* fpid, ABc b,
+                                                            int* regbase, uint8_t* regmask,
                                                             int* count, long* slot_cell,
                                                             uint8_t* slot_face, int cap, int* err) {
-  const long cells = D == 3 ? (long)n * n * n : (long)n * n;
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= cells) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= lv.tot0) return;
   int p[3];
-  a_coords<D>(n, c, p);
-  uint8_t mask = a_reg_mask<D>(pid, fpid, n, b, p);
+  a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+  const long c = a_idx<D>(lv.n, p);
+  uint8_t mask = a_reg_mask<D>(lv.pid, fpid, lv.n, b, p);
   int base = -1;
   if (mask) {
     base = atomicAdd(count, __popc(mask));
@@ -844,19 +847,22 @@ __global__ void __launch_bounds__(256) amr_reg_fine_kernel(const long* slot_cell
   has[s] |= 2;
 }
 
-// flux_correct (amr_hierarchy.cpp:532-559): one thread per cell with slots,
-// its faces in sorted-key order
+// flux_correct (amr_hierarchy.cpp:532-559): the thread of a cell's first
+// slot applies the cell's faces in sorted-key order
 template <int D>
 __global__ void __launch_bounds__(256) amr_flux_correct_kernel(ALv<D> lv, const int* regbase,
                                                                const uint8_t* regmask,
+                                                               const long* slot_cell,
+                                                               const uint8_t* slot_face,
                                                                const double* Rc, const double* Rf,
                                                                const uint8_t* has, int nslots,
                                                                double inv_h, int* err) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= lv.cells || amr_failed(err)) return;
+  const int s0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s0 >= nslots || amr_failed(err) || slot_face[s0] == 0xff) return;
+  const long c = slot_cell[s0];
+  if (regbase[c] != s0) return;
   const uint8_t mask = regmask[c];
-  if (!mask) return;
-  int s = regbase[c];
+  int s = s0;
   for (int bit = 0; bit < 2 * D; ++bit) {
     if (!(mask & (1u << bit))) continue;
     if (has[s] != 3) {
@@ -876,11 +882,11 @@ __global__ void __launch_bounds__(256) amr_flux_correct_kernel(ALv<D> lv, const 
 // average_down (amr_hierarchy.cpp:501-530)
 template <int D>
 __global__ void __launch_bounds__(256) amr_average_down_kernel(ALv<D> co, ALv<D> fi, int* err) {
-  const long c = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (c >= co.cells || amr_failed(err)) return;
-  if (co.pid[c] < 0) return;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= co.tot0 || amr_failed(err)) return;
   int p[3];
-  a_coords<D>(co.n, c, p);
+  a_list_pos<D>(co.boxes, co.off0, co.nb, 0, t, p);
+  const long c = a_idx<D>(co.n, p);
   const int f0[3] = {2 * p[0], 2 * p[1], D == 3 ? 2 * p[2] : 0};
   if (fi.pid[a_idx<D>(fi.n, f0)] < 0) return;
   const double w = D == 3 ? 0.125 : 0.25;
@@ -906,12 +912,12 @@ __global__ void __launch_bounds__(256) amr_sum_kernel(ALv<D> lv, const int* fpid
   double acc[D + 2];
 #pragma unroll
   for (int m = 0; m < D + 2; ++m) acc[m] = 0.0;
-  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < lv.cells;
-       c += (long)gridDim.x * blockDim.x) {
-    if (lv.pid[c] < 0) continue;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < lv.tot0;
+       t += (long)gridDim.x * blockDim.x) {
+    int p[3];
+    a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+    const long c = a_idx<D>(lv.n, p);
     if (fpid) {
-      int p[3];
-      a_coords<D>(lv.n, c, p);
       const int f[3] = {2 * p[0], 2 * p[1], D == 3 ? 2 * p[2] : 0};
       if (fpid[a_idx<D>(2 * lv.n, f)] >= 0) continue;
     }
