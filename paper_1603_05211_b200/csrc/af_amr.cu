@@ -132,7 +132,7 @@ std::vector<ABox> amr_cluster(const uint8_t* flags, const uint8_t* allowed, int 
 // ------------------------------------------------------- device clustering --
 namespace {
 constexpr int kClusterLevels = 4000;  // frontier counters (the bisection depth bound)
-constexpr int kClusterChunk = 24;     // levels launched between two looks at the frontier
+constexpr int kClusterChunk = 16;     // levels launched between two looks at the frontier
 }  // namespace
 
 DeviceCluster::~DeviceCluster() {

@@ -317,10 +317,13 @@ __global__ void __launch_bounds__(256) amr_sync_kernel(ALv<D> lv, ALv<D> co, int
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t >= lv.tot2 || amr_failed(err)) return;
   int p[3];
-  a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
-  if (!a_wrap<D>(lv.n, b, p)) return;  // beyond a physical boundary: read through a_map
+  const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  const bool inside = a_inrange<D>(lv.n, p);
+  if (!inside && !a_wrap<D>(lv.n, b, p)) return;  // beyond a physical boundary: read through a_map
   const long c = a_idx<D>(lv.n, p);
-  if (lv.pid[c] >= 0) {
+  const int owner = lv.pid[c];
+  if (owner >= 0) {  // a domain cell is copied once, by its own patch
+    if (owner != bi || !inside) return;
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) lv.G[m * lv.cells + c] = lv.U[m * lv.cells + c];
     return;
@@ -342,15 +345,18 @@ __global__ void __launch_bounds__(256) amr_save_kernel(ALv<D> lv, ABc b, int res
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t >= lv.tot2 || amr_failed(err)) return;
   int p[3];
-  a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
-  if (!a_wrap<D>(lv.n, b, p)) return;
+  const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  const bool inside = a_inrange<D>(lv.n, p);
+  if (!inside && !a_wrap<D>(lv.n, b, p)) return;
   const long c = a_idx<D>(lv.n, p);
+  const int owner = lv.pid[c];
+  if (owner >= 0 && (owner != bi || !inside)) return;  // a domain cell moves once, with its patch
   if (restore) {
 #pragma unroll
     for (int m = 0; m < D + 2; ++m) lv.G[m * lv.cells + c] = lv.Gold[m * lv.cells + c];
     return;
   }
-  const bool dom = lv.pid[c] >= 0;
+  const bool dom = owner >= 0;
 #pragma unroll
   for (int m = 0; m < D + 2; ++m) {
     lv.Gold[m * lv.cells + c] = lv.G[m * lv.cells + c];
