@@ -46,6 +46,14 @@ WORKLOADS = {
     # the ~217 GB tree); --level runs it smaller
     "cfg5": (4, 3, 3, 10, 0.4, 1, 16),
 }
+# The AMR patch path (not a BASELINE.json config: these lines are
+# recorded under profiles/, the default line stays cfg4). The reference's AMR preset
+# (AUSMDV / minmod / MUSCL-Hancock), time-refined, its paper base meshes (64^2, 8^3).
+AMR_WORKLOADS = {
+    # name: (case kind, dim, base_exp, level, dt_finest, seed, cycles)
+    "amr2d": (0, 2, 6, 10, 2.5e-4, 1, 4),
+    "amr3d": (3, 3, 3, 8, 3.5e-4, 1, 2),
+}
 BASE_LEVEL = {k: v[3] for k, v in WORKLOADS.items()}
 # MR options per MR workload (BASELINE.json configs[1], configs[2])
 MR_OPTS = {
@@ -337,7 +345,7 @@ def main():
                          "cycles, cfg4's 100 steps)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS) + sorted(AMR_WORKLOADS))
     ap.add_argument("--level", type=int, default=None,
                     help="run the workload at another finest level (not the config's own)")
     ap.add_argument("--mr-multi", default="auto", choices=["auto", "slabs", "replicas"],
@@ -355,6 +363,9 @@ def main():
                          "tests/test_tolerance_gpu.py) or 'exact' (bit-identical to the "
                          "reference). The other mode is timed too and reported beside it.")
     args = ap.parse_args()
+    if args.workload in AMR_WORKLOADS:
+        amr_main(args)
+        return
     if args.numerics is None:  # uniform 3D: tolerance; MR: exact (its established bar)
         args.numerics = "exact" if args.workload in MR_OPTS else "tolerance"
     if args.steps is None:
@@ -713,6 +724,154 @@ def mr_bench(args, rank, world, local, comm, torch, dist):
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,
     }
+
+
+def amr_main(args):
+    """AMR / AMRLT workloads. A step = one time-refined cycle of run_amr
+    (2^max_levels finest steps: ghost syncs, remesh with the device
+    clustering, patch stepping, average-down, refluxing). value = patch-cell
+    updates / s over the cycle (cells of a level x its substeps). The run is
+    host-driven (box lists come back at every remesh), so the timed region is
+    wall clock between two device synchronisations. One GPU (N>1: replicas)."""
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    from paper_1603_05211_b200 import amr as A
+    from paper_1603_05211_b200 import uniform as U
+    kind, dim, base, level, dt, seed, cycles = AMR_WORKLOADS[args.workload]
+    if args.level is not None:
+        dt = dt * 2.0 ** (level - args.level)
+        level = args.level
+    steps_per_cycle = 1 << (level - base)
+    cycles = args.steps if args.steps is not None else cycles
+    scheme = U.SchemeConfig(1, U.MINMOD, 1)
+    opts = A.AmrOptions(max_levels=level - base)
+
+    def fresh():
+        h = A.PatchHierarchy(dim, base, opts, scheme=scheme, device=local)
+        h.initialize_case(kind, seed)
+        return h
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import oracle as O
+        lv = args.ref_level if args.ref_level is not None else level - 1
+        n = (1 << (lv - base)) * max(1, cycles)
+        r = O.ref_amr_run(dim, lv, base, n, dt * 2.0 ** (level - lv), case_kind=kind, seed=seed,
+                          flux=1, integrator=1)
+        upd = float(sum(r["cells_per_step"]))  # not exact per level; see sample
+        # exact count: every level's cells x its substeps, from the final box lists
+        rate = None
+        if r["err_kind"] == 0:
+            per = sum(len(l["data"]) * (1 << i) for i, l in enumerate(r["levels"]))
+            rate = per * max(1, cycles) / r["wall_seconds"]
+        line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 0,
+                "steps": cycles, "warmup": 0,
+                "ms_per_step": 1e3 * r["wall_seconds"] / max(1, cycles),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": args.workload, "ran": {"finest_level": lv, "base_exp": base,
+                                                              "finest_steps": n, "threads": 1}},
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                                 "sample": f"the reference's PatchHierarchy/advance loop at finest level "
+                                           f"{lv} (one below the workload's {level} unless --ref-level), {n} "
+                                           "finest steps, one thread (the reference is serial); updates "
+                                           "counted from the final box lists"},
+                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    h = fresh()
+    for _ in range(max(args.warmup, 1)):
+        h.run(steps_per_cycle, dt)
+    h.profile(True)
+    u0, l0, r0 = h.cell_updates(), h.kernel_launches(), h.remesh_stats()
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    sampler.start()
+    t0 = time.perf_counter()
+    rep = h.run(steps_per_cycle * cycles, dt)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    upd = h.cell_updates() - u0
+    launches = h.kernel_launches() - l0
+    stage_ms, stage_launches, stage_updates = h.stage_stats()
+    remesh_s = h.remesh_stats()[0] - r0[0]
+    boxes = [h.level_info(l)[0] for l in range(h.n_levels())]
+    cells = [h.level_info(l)[1] for l in range(h.n_levels())]
+    h.close()
+
+    # end to end: initial condition on the host -> hierarchy -> W+K cycles -> every patch back
+    e2e = None
+    if not args.no_e2e:
+        t0 = time.perf_counter()
+        g = fresh()
+        u1 = g.cell_updates()
+        g.run(steps_per_cycle * cycles, dt)
+        out_bytes = 0
+        for l in range(g.n_levels()):
+            out_bytes += g.patch_data(l, 0).nbytes
+        torch.cuda.synchronize()
+        ew = time.perf_counter() - t0
+        e2e = {"value": (g.cell_updates() - u1) / ew, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(cells) * 40 / cycles),
+               "d2h_bytes_per_step": int(out_bytes / cycles),
+               "what": "create + initialize (initial condition evaluated on the host per patch cell, "
+                       "uploaded) + K cycles + download of every patch interior"}
+        g.close()
+    if rank != 0:
+        return
+    hbm, src = peaks()
+    S = (dim + 2) * 8
+    # MUSCL-Hancock step: read u, write u' per patch cell (2 S), as hancock_step's row in DESIGN.md
+    achieved = 2.0 * S * stage_updates / (stage_ms / 1e3) / 1e9 if stage_ms > 0 else None
+    line = {
+        "metric": METRIC, "value": upd * world / wall, "unit": UNIT, "n_gpus": world,
+        "steps": cycles, "warmup": max(args.warmup, 1), "ms_per_step": 1e3 * wall / cycles,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}: AMR patch path (SURVEY.md 8(f) #4), not a BASELINE.json config",
+                   "method": "AMRLT", "dim": dim, "base_mesh": f"{1 << base}^{dim}",
+                   "finest_mesh": f"{1 << level}^{dim}", "levels": level - base + 1,
+                   "scheme": "AUSMDV/minmod/MUSCL-Hancock (the reference's AMR preset)",
+                   "dt_finest": dt, "seed": seed, "bc": "outflow",
+                   "step": f"one time-refined cycle = {steps_per_cycle} finest steps",
+                   "patches_per_level": boxes, "cells_per_level": cells,
+                   "timing": "wall clock between device synchronisations (host-driven recursion)",
+                   "l2": "flushed by the cycle's own traffic (levels re-read between substeps)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                     "peak_source": src,
+                     "kernel": "amr_prims + amr_predict + amr_faces_hancock + amr_update (one update_level)",
+                     "kernel_share_of_step": stage_ms / (1e3 * wall) if wall > 0 else None,
+                     "stage_launches": stage_launches,
+                     "note": "multi-pass global-memory kernels, latency and fp64 bound at these patch "
+                             "counts; remesh (flags, device clustering, rebuild) took "
+                             f"{remesh_s:.3f} s of the {wall:.3f} s"},
+        "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import oracle as O
+            lv = args.ref_level if args.ref_level is not None else level - 1
+            n = 1 << (lv - base)
+            r = O.ref_amr_run(dim, lv, base, n, dt * 2.0 ** (level - lv), case_kind=kind, seed=seed,
+                              flux=1, integrator=1)
+            per = sum(len(l["data"]) * (1 << i) for i, l in enumerate(r["levels"]))
+            line["cpu_baseline"] = {
+                "value": per / r["wall_seconds"], "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"the reference's PatchHierarchy/advance loop at finest level {lv} (one below "
+                          f"the workload's {level}), one cycle of {n} finest steps, one thread (the "
+                          "reference is serial); updates counted from the final box lists",
+                "ran": {"finest_level": lv, "finest_steps": n, "wall_seconds": r["wall_seconds"]}}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -422,6 +422,11 @@ af_status af_amr_kernel_launches(const af_amr* h, long* count);
 /* patch-cell stage updates performed by every update_level so far (cells of
  * the level x 1 for MUSCL-Hancock, x 2 for RK2): the bench metric's numerator */
 af_status af_amr_cell_updates(const af_amr* h, long* updates);
+/* Stepping-kernel timing (CUDA events on the solver stream around the
+ * primitives/predictor/faces/update kernels of every update_level): enable,
+ * then read the accumulated device time, kernel launches and cell updates. */
+af_status af_amr_profile(af_amr* h, int enable);
+af_status af_amr_stage_stats(af_amr* h, double* ms, long* launches, long* updates);
 /* host wall time spent inside remesh (flags, clustering, rebuild; it
  * synchronises for the masks) and the number of remesh calls so far */
 af_status af_amr_remesh_stats(const af_amr* h, double* seconds, long* calls);

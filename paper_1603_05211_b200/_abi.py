@@ -178,6 +178,8 @@ SIGNATURES = {
     "af_amr_last_error": (C.c_int, [_vp, C.POINTER(ErrorRec)]),
     "af_amr_kernel_launches": (C.c_int, [_vp, C.POINTER(C.c_long)]),
     "af_amr_cell_updates": (C.c_int, [_vp, C.POINTER(C.c_long)]),
+    "af_amr_profile": (C.c_int, [_vp, C.c_int]),
+    "af_amr_stage_stats": (C.c_int, [_vp, _dp, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     "af_amr_remesh_stats": (C.c_int, [_vp, _dp, C.POINTER(C.c_long)]),
     "af_amr_cluster_device": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double,
                                         C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]),

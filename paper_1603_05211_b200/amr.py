@@ -230,6 +230,15 @@ class PatchHierarchy:
         self._check(self._lib.af_amr_cell_updates(self._h, C.byref(n)))
         return n.value
 
+    def profile(self, enable: bool = True):
+        self._check(self._lib.af_amr_profile(self._h, int(enable)))
+
+    def stage_stats(self):
+        """(device ms in the stepping kernels, their launches, cell updates) while profiling"""
+        ms, n, u = C.c_double(), C.c_long(), C.c_long()
+        self._check(self._lib.af_amr_stage_stats(self._h, C.byref(ms), C.byref(n), C.byref(u)))
+        return ms.value, n.value, u.value
+
     def remesh_stats(self):
         """(host seconds inside remesh, remesh calls) so far"""
         sec, n = C.c_double(), C.c_long()

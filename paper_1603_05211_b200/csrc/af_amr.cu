@@ -726,6 +726,19 @@ void Amr::update_t(int l, double dt) {
   cell_updates_ += L.total * (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK ? 1 : 2);
   L.t_old = L.t;
   save_level(l, false);  // p.data_old = p.data
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (profile_) {
+    AF_CUDA(cudaEventCreate(&e0));
+    AF_CUDA(cudaEventCreate(&e1));
+    AF_CUDA(cudaEventRecord(e0, stream_));
+  }
+  auto stepped = [&](int kernels) {
+    if (!profile_) return;
+    AF_CUDA(cudaEventRecord(e1, stream_));
+    events_.emplace_back(e0, e1);
+    stage_launches_ += kernels;
+    stage_updates_ += L.total * (cfg_.integrator == AF_INTEGRATOR_MUSCL_HANCOCK ? 1 : 2);
+  };
 
   auto registers = [&] {  // accumulate_registers, fine side then coarse side
     if (l > 0 && lv_[l - 1].nslots) {
@@ -748,6 +761,7 @@ void Amr::update_t(int l, double dt) {
     amr_faces_hancock<D, S><<<gf, 256, 0, stream_>>>(v, b, W_, DU_, F_, gamma, rec, d_err_);
     amr_update_kernel<D><<<gc, 256, 0, stream_>>>(v, L.U, F_, inv_dx, dt, d_err_);
     launch_count(4);
+    stepped(4);
     registers();
   } else {
     // stage 1 of every patch, the midpoint ghosts, stage 2 (the patch blocks
@@ -761,6 +775,7 @@ void Amr::update_t(int l, double dt) {
     amr_faces_rk2<D, S><<<gf, 256, 0, stream_>>>(v, b, W_, F_, gamma, rec, d_err_);
     amr_update_kernel<D><<<gc, 256, 0, stream_>>>(v, L.Uold, F_, inv_dx, dt, d_err_);
     launch_count(3);
+    stepped(7);
     save_level(l, true);
     registers();
   }
@@ -814,6 +829,13 @@ void Amr::check() {
   int err[4] = {0, 0, 0, 0};
   AF_CUDA(cudaMemcpyAsync(err, d_err_, sizeof err, cudaMemcpyDeviceToHost, stream_));
   AF_CUDA(cudaStreamSynchronize(stream_));
+  for (auto& e : events_) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess) stage_ms_ += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  events_.clear();
   if (err[0] == 1) raise_nonphysical(err[1]);
   fold_records();
   calls_.clear();
@@ -1344,6 +1366,15 @@ af_status af_amr_remesh_stats(const af_amr* h, double* seconds, long* calls) {
   if (seconds) *seconds = h->impl->remesh_seconds();
   if (calls) *calls = h->impl->remesh_calls();
   return AF_OK;
+}
+af_status af_amr_profile(af_amr* h, int enable) {
+  if (!h) return AF_E_ARGUMENT;
+  h->impl->set_profile(enable != 0);
+  return AF_OK;
+}
+af_status af_amr_stage_stats(af_amr* h, double* ms, long* launches, long* updates) {
+  if (!h) return AF_E_ARGUMENT;
+  return amr_guard(h, [&] { h->impl->stage_stats(ms, launches, updates); });
 }
 af_status af_amr_cell_updates(const af_amr* h, long* updates) {
   if (!h || !updates) return AF_E_ARGUMENT;

@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "af_internal.h"
@@ -94,6 +95,15 @@ class Amr {
   long cell_updates() const { return cell_updates_; }  // patch cells x stages, every update_level
   double remesh_seconds() const { return remesh_seconds_; }  // host time inside remesh()
   long remesh_calls() const { return remesh_calls_; }
+  // CUDA events around the stepping kernels of every update_level (primitives,
+  // predictor, faces, update; the RK2 midpoint sync included)
+  void set_profile(bool on) { profile_ = on; }
+  void stage_stats(double* ms, long* launches, long* updates) {
+    check();
+    if (ms) *ms = stage_ms_;
+    if (launches) *launches = stage_launches_;
+    if (updates) *updates = stage_updates_;
+  }
   const af_error& last_error() const { return err_; }
   af_error& error_slot() { return err_; }
 
@@ -173,6 +183,10 @@ class Amr {
   long cell_updates_ = 0;
   double remesh_seconds_ = 0.0;
   long remesh_calls_ = 0;
+  bool profile_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;
+  double stage_ms_ = 0.0;
+  long stage_launches_ = 0, stage_updates_ = 0;
   af_error err_{};
   std::string prefix_;  // "cycle N: " while run() is stepping
 };
