@@ -413,6 +413,11 @@ af_status af_amr_assemble_level(af_amr* h, int level, double* aos);
 /* total_conserved (amr_hierarchy.cpp:561-581); device tree sums, so equal to
  * the reference's sequential sums to round-off, not bitwise */
 af_status af_amr_total_conserved(af_amr* h, double out5[5]);
+/* l1_error_amr (amr.hpp:244-245, amr_hierarchy.cpp:631-656): per component the
+ * sum over the composite mesh of |patch - restrict(ref)| * cell volume; ref is
+ * a uniform solution at ref_level (AoS, host or device). Device tree sums
+ * (round-off agreement). AF_E_LEVEL_MISMATCH when ref is coarser than a level. */
+af_status af_amr_l1_error(af_amr* h, int ref_level, const double* ref_aos, double out5[5]);
 af_status af_amr_counts(const af_amr* h, long* total_cells, long* composite_cells);
 af_status af_amr_properly_nested(af_amr* h, int* nested);
 /* dump_boxes (amr_hierarchy.cpp:618-629); the text stays valid until the next call */

@@ -139,6 +139,8 @@ double afref_amr_time(int level, int old);
 long afref_amr_patch_data(int level, int ghost, int old, double* aos);
 int afref_amr_total_conserved(double* out5);
 int afref_amr_dump_boxes(char* buf, long cap);
+/* l1_error_amr (amr.hpp:244-245) of the kept hierarchy; 1 + err text on an exception */
+int afref_amr_l1_error(int ref_level, const double* ref_aos, double* out5, char* err, int errlen);
 /* cluster (amr.hpp:110-111) on an n x n (x n) mask; returns the box count */
 int afref_cluster(const unsigned char* flags, const unsigned char* allowed, int dim, int n,
                   double efficiency, int* boxes6, int capacity);

@@ -314,6 +314,7 @@ def _amr_lib():
         lib.afref_amr_patch_data.restype = C.c_long
         lib.afref_amr_total_conserved.argtypes = [dp]
         lib.afref_amr_dump_boxes.argtypes = [C.c_char_p, C.c_long]
+        lib.afref_amr_l1_error.argtypes = [C.c_int, dp, dp, C.c_char_p, C.c_int]
         lib.afref_cluster.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_double, ip,
                                       C.c_int]
         lib.afref_cluster.restype = C.c_int
@@ -379,3 +380,15 @@ def ref_cluster(flags: np.ndarray, efficiency: float, allowed: np.ndarray | None
                           None if a is None else a.ctypes.data_as(C.c_char_p), f.ndim, n,
                           efficiency, out.ctypes.data_as(C.POINTER(C.c_int)), cap)
     return out[:k]
+
+
+def ref_amr_l1_error(ref: np.ndarray, ref_level: int):
+    """l1_error_amr of the hierarchy the last ref_amr_run kept."""
+    lib = _amr_lib()
+    out = np.zeros(5)
+    err = C.create_string_buffer(512)
+    r = np.ascontiguousarray(ref, dtype=np.float64)
+    rc = lib.afref_amr_l1_error(ref_level, _dp(r), _dp(out), err, len(err))
+    if rc:
+        raise RuntimeError(err.value.decode(errors="replace"))
+    return out

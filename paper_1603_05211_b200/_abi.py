@@ -172,6 +172,7 @@ SIGNATURES = {
     "af_amr_patch_data": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp]),
     "af_amr_assemble_level": (C.c_int, [_vp, C.c_int, _vp]),
     "af_amr_total_conserved": (C.c_int, [_vp, _dp]),
+    "af_amr_l1_error": (C.c_int, [_vp, C.c_int, _vp, _dp]),
     "af_amr_counts": (C.c_int, [_vp, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     "af_amr_properly_nested": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "af_amr_dump_boxes": (C.c_int, [_vp, C.POINTER(C.c_char_p)]),

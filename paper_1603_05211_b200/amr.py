@@ -200,6 +200,16 @@ class PatchHierarchy:
         self._check(self._lib.af_amr_total_conserved(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    def l1_error(self, ref: np.ndarray, ref_level: int) -> np.ndarray:
+        """l1_error_amr (amr.hpp:244-245) against a uniform solution (cells, 5) at ref_level."""
+        r = np.ascontiguousarray(ref, dtype=np.float64)
+        if r.size != 5 * (1 << ref_level) ** self.dim:
+            raise ValueError("l1_error: reference must hold 2^(dim*ref_level) cells x 5")
+        out = np.zeros(5, dtype=np.float64)
+        self._check(self._lib.af_amr_l1_error(self._h, ref_level, r.ctypes.data,
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def total_cells(self) -> int:
         a, b = C.c_long(), C.c_long()
         self._check(self._lib.af_amr_counts(self._h, C.byref(a), C.byref(b)))

@@ -990,6 +990,40 @@ void Amr::total_conserved(double out5[5]) {
   cudaFree(d);
 }
 
+void Amr::l1_error(int ref_level, const double* ref_aos, double out5[5]) {
+  if (!ref_aos || !out5) throw Error(AF_E_ARGUMENT, "l1_error_amr: null pointer");
+  check();
+  for (int m = 0; m < 5; ++m) out5[m] = 0.0;
+  double* d = nullptr;
+  AF_CUDA(cudaMalloc(&d, sizeof(double) * 5));
+  for (int l = 0; l < n_levels(); ++l) {
+    const int res = base_exp_ + l;
+    if (ref_level < res) {
+      cudaFree(d);
+      throw Error(AF_E_LEVEL_MISMATCH, "reference too coarse for hierarchy level " + std::to_string(l));
+    }
+    Level& L = lv_[l];
+    double* r = nullptr;
+    AF_CUDA(cudaMalloc(&r, sizeof(double) * 5 * L.cells));
+    restrict_to_level(dim_, ref_level, res, ref_aos, r);  // device, bit-exact (af_io.cu)
+    AF_CUDA(cudaMemsetAsync(d, 0, sizeof(double) * 5, stream_));
+    const int* fp = l + 1 < n_levels() ? lv_[l + 1].pid : nullptr;
+    const unsigned g = std::min<unsigned>(blocks_for(L.total), 1184);
+    if (dim_ == 3)
+      amr_l1_kernel<3><<<g, 256, 0, stream_>>>(AMR_VIEW(3, L), fp, r, d);
+    else
+      amr_l1_kernel<2><<<g, 256, 0, stream_>>>(AMR_VIEW(2, L), fp, r, d);
+    launch_count();
+    double s[5];
+    AF_CUDA(cudaMemcpyAsync(s, d, sizeof s, cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaStreamSynchronize(stream_));
+    cudaFree(r);
+    const double h = dx(l), vol = dim_ == 3 ? h * h * h : h * h;
+    for (int m = 0; m < 5; ++m) out5[m] += s[m] * vol;
+  }
+  cudaFree(d);
+}
+
 long Amr::total_cells() const {
   long c = 0;
   for (const Level& L : lv_)
@@ -1333,6 +1367,10 @@ af_status af_amr_assemble_level(af_amr* h, int level, double* aos) {
 af_status af_amr_total_conserved(af_amr* h, double out5[5]) {
   if (!h || !out5) return AF_E_ARGUMENT;
   return amr_guard(h, [&] { h->impl->total_conserved(out5); });
+}
+af_status af_amr_l1_error(af_amr* h, int ref_level, const double* ref_aos, double out5[5]) {
+  if (!h) return AF_E_ARGUMENT;
+  return amr_guard(h, [&] { h->impl->l1_error(ref_level, ref_aos, out5); });
 }
 af_status af_amr_counts(const af_amr* h, long* total_cells, long* composite_cells) {
   if (!h) return AF_E_ARGUMENT;

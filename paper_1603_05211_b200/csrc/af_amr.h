@@ -77,6 +77,8 @@ class Amr {
   void average_down(int l);
   void flux_correct(int l);
   void total_conserved(double out5[5]);
+  // l1_error_amr (amr.hpp:244-245): reference = a uniform solution at ref_level (AoS)
+  void l1_error(int ref_level, const double* ref_aos, double out5[5]);
   long total_cells() const;
   long composite_cells() const;
   bool properly_nested();

@@ -129,6 +129,34 @@ __device__ __forceinline__ void a_box_cell(const int* bx, long r, int* p) {
 }
 // position t of the list of the boxes grown by `grow` cells along the active
 // axes (unwrapped: it may lie beyond the level's index range); returns the box
+// The threads of a CTA walk consecutive list positions, which lie in the same
+// or the next few boxes: thread 0 searches the offsets once, the others step
+// forward from its box. Every thread of the CTA must call this (a barrier).
+__device__ __forceinline__ int a_find_box_cta(const long* off, int nb, long t, long total) {
+  __shared__ int s_first;
+  if (threadIdx.x == 0) {
+    const long t0 = blockIdx.x * (long)blockDim.x;
+    s_first = a_find_box(off, nb, t0 < total ? t0 : total - 1);
+  }
+  __syncthreads();
+  int bi = s_first;
+  if (t < total)
+    while (bi + 1 < nb && off[bi + 1] <= t) ++bi;
+  return bi;
+}
+// a_list_pos with the box already known
+template <int D>
+__device__ __forceinline__ void a_box_pos(const int* boxes, const long* off, int bi, int grow,
+                                          long t, int* p) {
+  int gb[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int g = a < D ? grow : 0;
+    gb[a] = boxes[6 * bi + a] - g;
+    gb[3 + a] = boxes[6 * bi + 3 + a] + g;
+  }
+  a_box_cell(gb, t - off[bi], p);
+}
 template <int D>
 __device__ __forceinline__ int a_list_pos(const int* boxes, const long* off, int nb, int grow,
                                           long t, int* p) {
@@ -315,9 +343,10 @@ template <int D>
 __global__ void __launch_bounds__(256) amr_sync_kernel(ALv<D> lv, ALv<D> co, int has_coarse, ABc b,
                                                        double theta, double gm1, int* err) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int bi = a_find_box_cta(lv.off2, lv.nb, t, lv.tot2);
   if (t >= lv.tot2 || amr_failed(err)) return;
   int p[3];
-  const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  a_box_pos<D>(lv.boxes, lv.off2, bi, 2, t, p);
   const bool inside = a_inrange<D>(lv.n, p);
   if (!inside && !a_wrap<D>(lv.n, b, p)) return;  // beyond a physical boundary: read through a_map
   const long c = a_idx<D>(lv.n, p);
@@ -343,9 +372,10 @@ __global__ void __launch_bounds__(256) amr_sync_kernel(ALv<D> lv, ALv<D> co, int
 template <int D>
 __global__ void __launch_bounds__(256) amr_save_kernel(ALv<D> lv, ABc b, int restore, const int* err) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int bi = a_find_box_cta(lv.off2, lv.nb, t, lv.tot2);
   if (t >= lv.tot2 || amr_failed(err)) return;
   int p[3];
-  const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+  a_box_pos<D>(lv.boxes, lv.off2, bi, 2, t, p);
   const bool inside = a_inrange<D>(lv.n, p);
   if (!inside && !a_wrap<D>(lv.n, b, p)) return;
   const long c = a_idx<D>(lv.n, p);
@@ -497,9 +527,10 @@ __global__ void __launch_bounds__(256) amr_prims_kernel(ALv<D> lv, ABc b, double
   __shared__ double red[8];
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   double wave = 0.0;
+  const int bi = a_find_box_cta(lv.off2, lv.nb, t, lv.tot2);
   if (t < lv.tot2 && !amr_failed(err)) {
     int p[3];
-    const int bi = a_list_pos<D>(lv.boxes, lv.off2, lv.nb, 2, t, p);
+    a_box_pos<D>(lv.boxes, lv.off2, bi, 2, t, p);
     const bool inside = a_inrange<D>(lv.n, p);
     if (a_wrap<D>(lv.n, b, p)) {
       const long c = a_idx<D>(lv.n, p);
@@ -530,7 +561,8 @@ __device__ __forceinline__ long a_face_index(int n, int ax, const int* p) {
 // position of the face's high cell; the face index along the axis is p[ax]
 template <int D>
 __device__ __forceinline__ int a_face_pos(const ALv<D>& lv, long t, int* p) {
-  const int e = a_find_box(lv.offF, lv.nb * D, t);
+  const int e = a_find_box_cta(lv.offF, lv.nb * D, t, lv.totF);
+  if (t >= lv.totF) return 0;
   const int bi = e / D, ax = e - bi * D;
   int fb[6];
 #pragma unroll
@@ -552,9 +584,9 @@ __global__ void __launch_bounds__(256) amr_faces_rk2(ALv<D> lv, ABc b, const dou
   const int n = lv.n;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= lv.totF || amr_failed(err)) return;
   int p[3];
   const int ax = a_face_pos<D>(lv, t, p);
+  if (t >= lv.totF || amr_failed(err)) return;
   const long f = ax * per + a_face_index<D>(n, ax, p);
   int lo[3] = {p[0], p[1], p[2]};
   lo[ax] -= 1;
@@ -591,12 +623,13 @@ __global__ void __launch_bounds__(256) amr_update_kernel(ALv<D> lv, const double
                                                          const double* F, double inv_dx, double sdt,
                                                          int* err) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int bi = a_find_box_cta(lv.off0, lv.nb, t, lv.tot0);
   if (t >= lv.tot0 || amr_failed(err)) return;
   const int n = lv.n;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
   const long cs = D * per;
   int p[3];
-  a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+  a_box_pos<D>(lv.boxes, lv.off0, bi, 0, t, p);
   const long c = a_idx<D>(n, p);
   long fl[D], fh[D];
 #pragma unroll
@@ -629,9 +662,10 @@ __global__ void __launch_bounds__(256) amr_predict_kernel(ALv<D> lv, ABc b, cons
   const int n = lv.n, np = n + 2;
   const long padded = D == 3 ? (long)np * np * np : (long)np * np;
   const long tl = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int bi = a_find_box_cta(lv.off1, lv.nb, tl, lv.tot1);
   if (tl >= lv.tot1 || amr_failed(err)) return;
   int q[3];
-  a_list_pos<D>(lv.boxes, lv.off1, lv.nb, 1, tl, q);
+  a_box_pos<D>(lv.boxes, lv.off1, bi, 1, tl, q);
   const long t = D == 3 ? ((long)(q[2] + 1) * np + (q[1] + 1)) * np + (q[0] + 1)
                         : (long)(q[1] + 1) * np + (q[0] + 1);
   const Prim<D> w0 = a_ghostw<D>(W, n, lv.cells, b, q);
@@ -672,9 +706,9 @@ __global__ void __launch_bounds__(256) amr_faces_hancock(ALv<D> lv, ABc b, const
   const long padded = D == 3 ? (long)np * np * np : (long)np * np;
   const long per = D == 3 ? (long)(n + 1) * n * n : (long)(n + 1) * n;
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= lv.totF || amr_failed(err)) return;
   int cr[3];
   const int ax = a_face_pos<D>(lv, t, cr);
+  if (t >= lv.totF || amr_failed(err)) return;
   const long f = ax * per + a_face_index<D>(n, ax, cr);
   int cl[3] = {cr[0], cr[1], cr[2]};
   cl[ax] -= 1;
@@ -933,6 +967,47 @@ __global__ void __launch_bounds__(256) amr_sum_kernel(ALv<D> lv, const int* fpid
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int m = 0; m < D + 2; ++m) {
+    double v = acc[m];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += red[w];
+      atomicAdd(out + m, s);
+    }
+  }
+}
+
+// l1_error_amr (amr_hierarchy.cpp:631-656): per-level sums of |patch - ref|
+// over the cells the next level does not cover; ref is the reference solution
+// restricted to this level (AoS, 5 doubles per cell). Block tree sums.
+template <int D>
+__global__ void __launch_bounds__(256) amr_l1_kernel(ALv<D> lv, const int* fpid, const double* ref,
+                                                     double* out) {
+  __shared__ double red[8];
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < lv.tot0;
+       t += (long)gridDim.x * blockDim.x) {
+    int p[3];
+    a_list_pos<D>(lv.boxes, lv.off0, lv.nb, 0, t, p);
+    const long c = a_idx<D>(lv.n, p);
+    if (fpid) {
+      const int f[3] = {2 * p[0], 2 * p[1], D == 3 ? 2 * p[2] : 0};
+      if (fpid[a_idx<D>(2 * lv.n, f)] >= 0) continue;
+    }
+    const Cons<D> q = a_load<D>(lv.U, lv.cells, c);
+    const double* r = ref + 5 * c;
+    acc[0] += fabs(q.rho - r[0]);
+    acc[1] += fabs(q.m[0] - r[1]);
+    acc[2] += fabs(q.m[1] - r[2]);
+    acc[3] += fabs((D == 3 ? q.m[D - 1] : 0.0) - r[3]);
+    acc[4] += fabs(q.E - r[4]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
     double v = acc[m];
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     __syncthreads();

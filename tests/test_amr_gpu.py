@@ -254,3 +254,18 @@ def test_errors_match_reference():
     if h3.n_levels() > 1:
         with pytest.raises(LevelMismatch):
             h3.assemble_level(1)
+
+
+def test_l1_error_amr_matches_reference():
+    """l1_error_amr (amr_hierarchy.cpp:631-656) against a uniform solution"""
+    h, ref = _run_both(2, 4, 7, 32, 5.0e-4, 0, seed=7, eff=0.7)
+    h.initialize_case(0, 7)
+    h.run(32, 5.0e-4)
+    assert ref["err_kind"] == 0
+    sol = oracle.case_fill(0, 7, 8)  # any level-8 field serves as the reference solution
+    sol[:, 0] *= 1.0 + 0.01 * np.sin(np.arange(len(sol)))
+    mine = h.l1_error(sol, 8)
+    want = oracle.ref_amr_l1_error(sol, 8)
+    assert np.allclose(mine, want, rtol=1e-12, atol=1e-15) and want[0] > 0
+    with pytest.raises(LevelMismatch):
+        h.l1_error(oracle.case_fill(0, 7, 5), 5)
