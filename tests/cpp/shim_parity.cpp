@@ -36,8 +36,75 @@ static void report(const std::string& what, bool ok) {
   if (!ok) ++failures;
 }
 
-int main() {
+// run_amr (amr_solver.hpp:34-35) on a built-in case with its own step
+// schedule: the per-cycle box lists through the sample observers, every patch
+// block with its ghost layers, the report.
+static void amr_case(const char* name, int L, bool time_refine, bool rk2) {
+  const CaseSpec& s = find_case(name);
+  const SchemeConfig sc = rk2 ? SchemeConfig::mr_preset() : SchemeConfig::amr_preset();
+  const long n = s.steps_for_level(L);
+  AmrRunOptions o;
+  o.time_refine = time_refine;
+  std::vector<long> ref_samples, dev_samples;
+  std::vector<std::string> ref_boxes, dev_boxes;
+  AmrRunOptions oref = o;
+  oref.on_sample = [&](long steps, const PatchHierarchy& h) {
+    ref_samples.push_back(steps);
+    ref_boxes.push_back(h.dump_boxes());
+  };
+  AmrRunResult r = run_amr(s, L, n, sc, oref);
+  gpu::AmrDeviceResult g = gpu::run_amr(s, L, n, sc, o, [&](long steps, gpu::AmrDevice& h) {
+    dev_samples.push_back(steps);
+    dev_boxes.push_back(h.dump_boxes());
+  });
+  const std::string tag = std::string("run_amr ") + s.name + " L=" + std::to_string(L) + " x " +
+                          std::to_string(n) + " steps" + (o.time_refine ? " AMRLT" : " AMR") +
+                          (rk2 ? " RK2" : "");
+  report(tag + ": samples and box lists per cycle", ref_samples == dev_samples && ref_boxes == dev_boxes);
+  report(tag + ": final dump_boxes", r.hierarchy->dump_boxes() == g.hierarchy->dump_boxes());
+  bool same = r.hierarchy->n_levels() == g.hierarchy->n_levels();
+  long patches = 0;
+  for (int l = 0; same && l < r.hierarchy->n_levels(); ++l) {
+    const std::vector<double> blocks = g.hierarchy->patch_data(l, 2);
+    size_t c = 0;
+    for (const Patch& p : r.hierarchy->level(l).patches) {
+      ++patches;
+      const BlockData& b = p.data;
+      const int gz = b.ghost_along(2);
+      for (int k = -gz; k < b.n(2) + gz && same; ++k)
+        for (int j = -2; j < b.n(1) + 2 && same; ++j)
+          for (int i = -2; i < b.n(0) + 2; ++i, ++c) {
+            const ConservedState& q = b.at(i, j, k);
+            const double v[5] = {q.rho, q.mom[0], q.mom[1], q.mom[2], q.rhoE};
+            if (5 * c + 4 >= blocks.size() || std::memcmp(v, &blocks[5 * c], sizeof v) != 0) {
+              same = false;
+              break;
+            }
+          }
+    }
+    same = same && 5 * c == blocks.size();
+  }
+  report(tag + ": every patch block with ghosts (" + std::to_string(patches) + " patches)", same);
+  report(tag + ": cells_per_step", r.report.cells_per_step == g.report.cells_per_step);
+  report(tag + ": leaves_per_step", r.report.leaves_per_step == g.report.leaves_per_step);
+  report(tag + ": max_cfl", r.report.max_cfl == g.report.max_cfl);
+  report(tag + ": fallbacks", r.report.fallbacks == g.report.fallbacks);
+  report(tag + ": levels above the base", g.hierarchy->n_levels() >= 2);
+  std::printf("     reference %.2f s, device %.3f s\n", r.report.wall_seconds, g.report.wall_seconds);
+}
+
+int main(int argc, char** argv) {
   std::setvbuf(stdout, nullptr, _IONBF, 0);
+  if (argc > 1 && std::string(argv[1]) == "amr-full") {
+    // the paper's configuration sizes (base 64^2 / 8^3) with the cases' own
+    // step schedules: lax_liu_6 up to 1024^2, ellipsoid3d up to 128^3
+    amr_case("lax_liu_6", 9, true, false);
+    amr_case("lax_liu_6", 10, true, false);
+    amr_case("ellipsoid3d", 6, true, false);
+    amr_case("ellipsoid3d", 7, true, false);
+    std::printf("%s (%d failures)\n", failures ? "SHIM PARITY FAILED" : "SHIM PARITY OK", failures);
+    return failures ? 1 : 0;
+  }
   // Uniform FV: lax_liu_6 (MR preset AUSM+/van Albada/RK2), ellipsoid3d.
   {
     const CaseSpec& s = find_case("lax_liu_6");
@@ -235,60 +302,9 @@ int main() {
     report(tag + " leaves", tree.leaves() == dev.leaves());
     report(tag + " to_uniform", same_grid(tree.to_uniform(L), dev.to_uniform(L)));
   }
-  // run_amr (amr_solver.hpp:34-35) on the reference's built-in cases: the box
-  // lists, every patch block with its ghost layers, the report
-  for (int variant = 0; variant < 4; ++variant) {
-    const bool three_d = variant == 3;
-    const CaseSpec& s = find_case(three_d ? "ellipsoid3d" : "lax_liu_6");
-    SchemeConfig sc = SchemeConfig::amr_preset();
-    if (variant == 2) sc = SchemeConfig::mr_preset();  // the RK2 update_level branch
-    const int L = three_d ? 5 : 8;
-    const long n = s.steps_for_level(L);
-    AmrRunOptions o;
-    o.time_refine = variant != 1;
-    std::vector<long> ref_samples, dev_samples;
-    std::vector<std::string> ref_boxes, dev_boxes;
-    AmrRunOptions oref = o;
-    oref.on_sample = [&](long steps, const PatchHierarchy& h) {
-      ref_samples.push_back(steps);
-      ref_boxes.push_back(h.dump_boxes());
-    };
-    AmrRunResult r = run_amr(s, L, n, sc, oref);
-    gpu::AmrDeviceResult g = gpu::run_amr(s, L, n, sc, o, [&](long steps, gpu::AmrDevice& h) {
-      dev_samples.push_back(steps);
-      dev_boxes.push_back(h.dump_boxes());
-    });
-    const std::string tag = std::string("run_amr ") + s.name + " L=" + std::to_string(L) +
-                            (o.time_refine ? " AMRLT" : " AMR") + (variant == 2 ? " RK2" : "");
-    report(tag + ": samples and box lists per cycle", ref_samples == dev_samples && ref_boxes == dev_boxes);
-    report(tag + ": final dump_boxes", r.hierarchy->dump_boxes() == g.hierarchy->dump_boxes());
-    bool same = r.hierarchy->n_levels() == g.hierarchy->n_levels();
-    for (int l = 0; same && l < r.hierarchy->n_levels(); ++l) {
-      const std::vector<double> blocks = g.hierarchy->patch_data(l, 2);
-      size_t c = 0;
-      for (const Patch& p : r.hierarchy->level(l).patches) {
-        const BlockData& b = p.data;
-        const int gz = b.ghost_along(2);
-        for (int k = -gz; k < b.n(2) + gz && same; ++k)
-          for (int j = -2; j < b.n(1) + 2 && same; ++j)
-            for (int i = -2; i < b.n(0) + 2; ++i, ++c) {
-              const ConservedState& q = b.at(i, j, k);
-              const double v[5] = {q.rho, q.mom[0], q.mom[1], q.mom[2], q.rhoE};
-              if (5 * c + 4 >= blocks.size() || std::memcmp(v, &blocks[5 * c], sizeof v) != 0) {
-                same = false;
-                break;
-              }
-            }
-      }
-      same = same && 5 * c == blocks.size();
-    }
-    report(tag + ": every patch block with ghosts", same);
-    report(tag + ": cells_per_step", r.report.cells_per_step == g.report.cells_per_step);
-    report(tag + ": leaves_per_step", r.report.leaves_per_step == g.report.leaves_per_step);
-    report(tag + ": max_cfl", r.report.max_cfl == g.report.max_cfl);
-    report(tag + ": fallbacks", r.report.fallbacks == g.report.fallbacks);
-    report(tag + ": levels above the base", g.hierarchy->n_levels() >= 2);
-  }
+  for (int variant = 0; variant < 4; ++variant)
+    amr_case(variant == 3 ? "ellipsoid3d" : "lax_liu_6", variant == 3 ? 5 : 8, variant != 1,
+             variant == 2);
   std::printf("%s (%d failures)\n", failures ? "SHIM PARITY FAILED" : "SHIM PARITY OK", failures);
   return failures ? 1 : 0;
 }
