@@ -65,6 +65,11 @@ CASES = [
     ("2d_reflective", 2, 4, 6, 16, 1.0e-3, 0, {"bc": [REFL, REFL, OUT, REFL, OUT, OUT], "seed": 5}),
     ("2d_no_reflux", 2, 4, 6, 16, 1.0e-3, 0, {"flux_correction": False}),
     ("2d_three_levels", 2, 4, 7, 32, 5.0e-4, 0, {"seed": 7, "eff": 0.7}),
+    ("2d_tiny_base", 2, 2, 6, 16, 1.0e-3, 0, {"seed": 4}),
+    ("2d_single_level", 2, 5, 5, 8, 2.0e-3, 0, {}),
+    ("2d_tiny_base_reflective_rk2", 2, 2, 5, 8, 2.0e-3, 0,
+     {"seed": 6, "bc": [REFL] * 6, "flux": 0, "integrator": 0}),
+    ("3d_tiny_base_periodic", 3, 2, 4, 4, 4.0e-3, 2, {"bc": [PER] * 6}),
     ("3d_hancock_lt", 3, 3, 5, 8, 2.0e-3, 2, {}),
     ("3d_rk2_periodic", 3, 3, 5, 8, 1.0e-3, 2, {"bc": [PER] * 6, "flux": 0, "integrator": 0, "seed": 4}),
     ("3d_reflective_global", 3, 3, 5, 4, 2.0e-3, 3, {"bc": [REFL] * 6, "time_refine": False}),
@@ -269,3 +274,16 @@ def test_l1_error_amr_matches_reference():
     assert np.allclose(mine, want, rtol=1e-12, atol=1e-15) and want[0] > 0
     with pytest.raises(LevelMismatch):
         h.l1_error(oracle.case_fill(0, 7, 5), 5)
+
+
+def test_run_amr_helper():
+    """amr.run_amr builds the hierarchy for a resolution level as run_amr does
+    (amr_base_exp, max_levels = level - base) and steps to t_end"""
+    assert amr.amr_base_exp(2, 10) == 6 and amr.amr_base_exp(3, 8) == 3 and amr.amr_base_exp(2, 4) == 3
+    h, rep = amr.run_amr(2, 7, 32, 32 * 5.0e-4, case=(0, 7), scheme=SchemeConfig(1, 1, 1),
+                         options=amr.AmrOptions(cluster_efficiency=0.7))
+    ref = oracle.ref_amr_run(2, 7, 6, 32, 5.0e-4, case_kind=0, seed=7, flux=1, integrator=1,
+                             efficiency=0.7)
+    _compare(h, rep, ref)
+    with pytest.raises(ConfigError):
+        amr.run_amr(2, 0, 8, 0.1, case=(0, 1))
