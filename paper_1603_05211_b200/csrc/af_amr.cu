@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <tuple>
 
@@ -132,7 +133,7 @@ std::vector<ABox> amr_cluster(const uint8_t* flags, const uint8_t* allowed, int 
 // ------------------------------------------------------- device clustering --
 namespace {
 constexpr int kClusterLevels = 4000;  // frontier counters (the bisection depth bound)
-constexpr int kClusterChunk = 16;     // levels launched between two looks at the frontier
+constexpr int kClusterChunk = 12;     // levels launched between two looks at the frontier
 }  // namespace
 
 DeviceCluster::~DeviceCluster() {
@@ -142,6 +143,7 @@ DeviceCluster::~DeviceCluster() {
   cudaFree(qb_);
   cudaFree(out_);
   cudaFree(hdr_);
+  cudaFreeHost(h_pin_);
 }
 
 std::vector<ABox> DeviceCluster::run(int dim, const uint8_t* d_flags, const uint8_t* d_allowed, int n,
@@ -198,7 +200,12 @@ std::vector<ABox> DeviceCluster::run(int dim, const uint8_t* d_flags, const uint
     AF_CUDA(cudaFuncSetAttribute(amr_cluster_level_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     AF_CUDA(cudaFuncSetAttribute(amr_cluster_level_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  std::vector<int> hdr((size_t)kClusterLevels + 2);
+  // pinned landing zone: the counters and the first boxes in one round trip
+  constexpr int kBoxPrefix = 2048;
+  if (!h_pin_)
+    AF_CUDA(cudaMallocHost(&h_pin_, sizeof(int) * (kClusterLevels + 2) + sizeof(CBox) * kBoxPrefix));
+  int* hdr = static_cast<int*>(h_pin_);
+  CBox* hbox = reinterpret_cast<CBox*>(hdr + kClusterLevels + 2);
   int level = 0;
   for (;;) {
     for (int k = 0; k < kClusterChunk && level < kClusterLevels - 1; ++k, ++level) {
@@ -215,14 +222,18 @@ std::vector<ABox> DeviceCluster::run(int dim, const uint8_t* d_flags, const uint
       ++*launches;
     }
     AF_CUDA(cudaGetLastError());
-    AF_CUDA(cudaMemcpyAsync(hdr.data(), hdr_, sizeof(int) * (size_t)(3 + level), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaMemcpyAsync(hdr, hdr_, sizeof(int) * (size_t)(3 + level), cudaMemcpyDeviceToHost, stream_));
+    AF_CUDA(cudaMemcpyAsync(hbox, out_, sizeof(CBox) * (size_t)std::min(cap_, kBoxPrefix), cudaMemcpyDeviceToHost,
+                            stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
     if (hdr[1]) throw Error(AF_E_INTERNAL, "cluster: box queue overflow");
     if (hdr[(size_t)2 + level] == 0) break;
     if (level >= kClusterLevels - 1) throw Error(AF_E_INTERNAL, "cluster: bisection deeper than its bound");
   }
   std::vector<CBox> got((size_t)hdr[0]);
-  if (!got.empty()) {
+  if ((int)got.size() <= kBoxPrefix) {
+    std::copy(hbox, hbox + got.size(), got.begin());
+  } else {
     AF_CUDA(cudaMemcpyAsync(got.data(), out_, sizeof(CBox) * got.size(), cudaMemcpyDeviceToHost, stream_));
     AF_CUDA(cudaStreamSynchronize(stream_));
   }
@@ -305,6 +316,10 @@ Amr::Amr(const af_config& cfg, const af_amr_options& opt) : cfg_(cfg), opt_(opt)
 
 Amr::~Amr() {
   cudaStreamSynchronize(stream_);
+  if (std::getenv("AF_AMR_TRACE"))
+    std::fprintf(stderr, "AF_AMR_TRACE: remesh %.4f s in %ld calls, of which clustering (tables, bisection, "
+                 "box list round trip) %.4f s; %ld launches\n", remesh_seconds_, remesh_calls_, cluster_seconds_,
+                 launches_);
   for (Level& L : lv_) free_level(L);
   for (Level& L : spare_) free_level(L);
   delete clusterer_;
@@ -590,7 +605,10 @@ void Amr::remesh_t(int l) {
     amr_dilate_kernel<D><<<g, 256, 0, stream_>>>(m_tmp_, S.n, b, 1, nest, m_flags_);
     amr_allowed_kernel<D><<<g, 256, 0, stream_>>>(S.pid, S.n, b, m_flags_, m_allowed_, m_masked_, d_flag_);
     launch_count(3);
-    for (const ABox& cbx : cluster_device<D>(m_masked_, m_allowed_, S.n, opt_.cluster_efficiency)) {
+    const auto tc0 = std::chrono::steady_clock::now();
+    const std::vector<ABox> clustered = cluster_device<D>(m_masked_, m_allowed_, S.n, opt_.cluster_efficiency);
+    cluster_seconds_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count();
+    for (const ABox& cbx : clustered) {
       ABox r;  // Box::refined (amr.hpp:49-64)
       for (int a = 0; a < D; ++a) {
         r.lo[a] = 2 * cbx.lo[a];

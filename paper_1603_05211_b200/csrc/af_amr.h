@@ -50,6 +50,7 @@ class DeviceCluster {
   long sat_cap_ = 0;
   int *Sf_ = nullptr, *Sa_ = nullptr;
   void *qa_ = nullptr, *qb_ = nullptr, *out_ = nullptr;
+  void* h_pin_ = nullptr;  // pinned readback buffer
   int* hdr_ = nullptr;  // [0] accepted boxes, [1] overflow, [2 + level] frontier sizes
   int cap_ = 0;
 };
@@ -183,7 +184,7 @@ class Amr {
   long cb_cap_ = 0;
   long launches_ = 0;
   long cell_updates_ = 0;
-  double remesh_seconds_ = 0.0;
+  double remesh_seconds_ = 0.0, cluster_seconds_ = 0.0;
   long remesh_calls_ = 0;
   bool profile_ = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events_;

@@ -1082,8 +1082,12 @@ __host__ __device__ inline int propose_cut_t(const T* sig, int n, int* score) {
 
 // S has (n+1)^D entries: S[k][j][i] = set cells of the mask in [0,i)x[0,j)x[0,k).
 // Pass x writes the row prefixes, passes y and z accumulate along their axis.
+// The scans run along one axis per thread; the loads of a batch of 8 entries
+// are issued before the dependent adds, so a thread waits for memory once per
+// batch instead of once per entry.
 template <int D>
-__global__ void __launch_bounds__(128) amr_sat_x_kernel(const uint8_t* mask, int n, int* S) {
+__global__ void __launch_bounds__(128) amr_sat_x_kernel(const uint8_t* __restrict__ mask, int n,
+                                                        int* __restrict__ S) {
   const long rows = D == 3 ? (long)n * n : n;
   const long r = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (r >= rows) return;
@@ -1093,7 +1097,18 @@ __global__ void __launch_bounds__(128) amr_sat_x_kernel(const uint8_t* mask, int
   int* s = S + ((D == 3 ? (long)(k + 1) * np : 0) + (j + 1)) * np;
   int acc = 0;
   s[0] = 0;
-  for (int i = 0; i < n; ++i) {
+  int i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint8_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = m[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc += v[u] != 0;
+      s[i + u + 1] = acc;
+    }
+  }
+  for (; i < n; ++i) {
     acc += m[i] != 0;
     s[i + 1] = acc;
   }
@@ -1108,9 +1123,20 @@ __global__ void __launch_bounds__(128) amr_sat_y_kernel(int n, int* S) {
   int* s = S + (D == 3 ? (long)(k + 1) * np * np : 0) + i;
   int acc = 0;
   s[0] = 0;
-  for (int j = 1; j <= n; ++j) {
-    acc += s[j * np];
-    s[j * np] = acc;
+  int j = 1;
+  for (; j + 7 <= n; j += 8) {
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = s[(long)(j + u) * np];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc += v[u];
+      s[(long)(j + u) * np] = acc;
+    }
+  }
+  for (; j <= n; ++j) {
+    acc += s[(long)j * np];
+    s[(long)j * np] = acc;
   }
 }
 __global__ void __launch_bounds__(128) amr_sat_z_kernel(int n, int* S) {
@@ -1119,7 +1145,18 @@ __global__ void __launch_bounds__(128) amr_sat_z_kernel(int n, int* S) {
   if (c >= plane) return;
   int acc = 0;
   S[c] = 0;
-  for (int k = 1; k <= n; ++k) {
+  int k = 1;
+  for (; k + 7 <= n; k += 8) {
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = S[(long)(k + u) * plane + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc += v[u];
+      S[(long)(k + u) * plane + c] = acc;
+    }
+  }
+  for (; k <= n; ++k) {
     acc += S[k * plane + c];
     S[k * plane + c] = acc;
   }
