@@ -14,6 +14,9 @@
 //   gpu::run_uniform  unigrid.hpp:24-26 / unigrid.cpp:7-50
 //   gpu::run_mr       mr_solver.hpp:78-79 / mr_solver.cpp:318-400 (returns the
 //                     final to_uniform(L) grid instead of the host MRTree)
+//   gpu::reference_solution  cases.hpp:58-59 / cases.cpp:181-210: the cached uniform
+//                     reference, computed by gpu::run_uniform on a cache miss; same
+//                     cache files, same key text, same CacheCorrupt conditions
 //   gpu::AmrDevice    PatchHierarchy (amr.hpp:123-242) on the device
 //   gpu::run_amr      amr_solver.hpp:34-35 / amr_solver.cpp:62-133 (returns the
 //                     device hierarchy instead of the host PatchHierarchy)
@@ -22,6 +25,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <filesystem>
 #include <functional>
 #include <memory>
 #include <sstream>
@@ -36,6 +40,7 @@
 #include "adaptflow/metrics.hpp"
 #include "adaptflow/mr_solver.hpp"
 #include "adaptflow/scheme.hpp"
+#include "adaptflow/snapshot.hpp"
 #include "adaptflow/step.hpp"
 #include "adaptflow/unigrid.hpp"
 #include "af_gpu.h"
@@ -478,6 +483,43 @@ inline MRDeviceResult run_mr(const CaseSpec& spec, int level, long n_steps,
   out.grid = tree.to_uniform(level);
   out.leaves = tree.leaves();
   return out;
+}
+
+// reference_solution (cases.cpp:181-210): the uniform reference solution of a
+// case at ref_level, from the cache directory when a valid snapshot is there,
+// otherwise computed on the device and cached. The key text (the FNV-1a hash
+// of reference_config_string and the string itself) and the file names are the
+// reference's, so either implementation accepts the other's cache.
+inline UniformGrid reference_solution(const CaseSpec& spec, int ref_level,
+                                      const SchemeConfig& scheme, const std::string& cache_dir) {
+  const std::string config = reference_config_string(spec, ref_level, scheme);
+  unsigned long long h = 1469598103934665603ull;  // FNV-1a, 64 bit
+  for (unsigned char c : config) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  const std::string key = "hash=" + std::to_string(h) + "\n" + config + "\n";
+  std::string path, meta_path;
+  if (!cache_dir.empty()) {
+    std::filesystem::create_directories(cache_dir);
+    path = reference_cache_path(spec, ref_level, scheme, cache_dir);
+    meta_path = path + ".meta";
+    if (std::filesystem::exists(path)) {
+      if (!std::filesystem::exists(meta_path) || read_text_file(meta_path) != key)
+        throw CacheCorrupt("cached reference " + path +
+                           " does not match the requested configuration");
+      Snapshot snap = read_snapshot(path);
+      if (snap.grid.level() != ref_level || snap.grid.dim() != spec.dim)
+        throw CacheCorrupt("cached reference " + path + " has wrong geometry");
+      return std::move(snap.grid);
+    }
+  }
+  UniformRunResult res = gpu::run_uniform(spec, ref_level, spec.steps_for_level(ref_level), scheme);
+  if (!cache_dir.empty()) {
+    write_snapshot(path, res.grid, spec.gas.gamma, spec.t_end);
+    write_text_file(meta_path, key);
+  }
+  return std::move(res.grid);
 }
 
 // ---------------------------------------------------------------- AMR ----

@@ -7,11 +7,13 @@
 // bit-identical.
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <sstream>
 #include <utility>
 #include <string>
 #include <vector>
 
+#include "adaptflow/snapshot.hpp"
 #include "adaptflow_gpu.hpp"
 
 using namespace adaptflow;
@@ -301,6 +303,39 @@ int main(int argc, char** argv) {
     const std::string tag = "MRTree::refine(eps, buffer) variant " + std::to_string(variant);
     report(tag + " leaves", tree.leaves() == dev.leaves());
     report(tag + " to_uniform", same_grid(tree.to_uniform(L), dev.to_uniform(L)));
+  }
+  // reference_solution (cases.hpp:58-59): computed on the device on a miss,
+  // the cache interchangeable with the reference's, CacheCorrupt on a mismatch
+  {
+    const CaseSpec& s = find_case("lax_liu_6");
+    const SchemeConfig sc = SchemeConfig::mr_preset();
+    const int L = 7;
+    const std::string dref = "/tmp/af_shim_cache_ref", ddev = "/tmp/af_shim_cache_dev";
+    std::filesystem::remove_all(dref);
+    std::filesystem::remove_all(ddev);
+    const UniformGrid a = reference_solution(s, L, sc, dref);
+    const UniformGrid b = gpu::reference_solution(s, L, sc, ddev);
+    report("reference_solution lax_liu_6 L=7 (device miss path)", same_grid(a, b));
+    const std::string pa = reference_cache_path(s, L, sc, dref), pb = reference_cache_path(s, L, sc, ddev);
+    report("reference_solution: meta key text identical",
+           read_text_file(pa + ".meta") == read_text_file(pb + ".meta"));
+    // each side reads the other's cache
+    report("reference_solution: the reference accepts the device cache",
+           same_grid(reference_solution(s, L, sc, ddev), a));
+    report("reference_solution: the device shim accepts the reference cache",
+           same_grid(gpu::reference_solution(s, L, sc, dref), a));
+    bool corrupt = false;
+    try {
+      gpu::reference_solution(s, L, SchemeConfig::amr_preset(), dref + "/../af_shim_cache_ref");
+      // same directory, another scheme with another flux name: a fresh file, no throw
+      write_text_file(pa + ".meta", "hash=0\nstale\n");
+      gpu::reference_solution(s, L, sc, dref);
+    } catch (const CacheCorrupt&) {
+      corrupt = true;
+    }
+    report("reference_solution: CacheCorrupt on a stale key", corrupt);
+    std::filesystem::remove_all(dref);
+    std::filesystem::remove_all(ddev);
   }
   for (int variant = 0; variant < 4; ++variant)
     amr_case(variant == 3 ? "ellipsoid3d" : "lax_liu_6", variant == 3 ? 5 : 8, variant != 1,
