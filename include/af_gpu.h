@@ -145,6 +145,10 @@ af_status af_uniform_set_stream(af_uniform* u, void* cuda_stream);
 enum { AF_NUMERICS_EXACT = 0, AF_NUMERICS_TOLERANCE = 1 };
 af_status af_uniform_set_numerics(af_uniform* u, int numerics);
 af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz);
+/* The same split without a solver (host arithmetic, no CUDA call): rank `rank`
+ * of n_ranks owns [z0, z0+nz) of the slab axis of a 2^level mesh; the loop it
+ * shards is unigrid.cpp:33-47. AF_E_CONFIG when a rank would be empty. */
+af_status af_slab_extent(int dim, int level, int n_ranks, int rank, int* z0, int* nz);
 
 /* AoS state transfer of the rank's slab (host or device pointer). */
 af_status af_uniform_upload(af_uniform* u, const double* aos);

@@ -100,6 +100,8 @@ SIGNATURES = {
     "af_uniform_set_stream": (C.c_int, [_vp, _vp]),
     "af_uniform_set_numerics": (C.c_int, [_vp, C.c_int]),
     "af_uniform_local_extent": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "af_slab_extent": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                 C.POINTER(C.c_int)]),
     "af_uniform_upload": (C.c_int, [_vp, _vp]),
     "af_uniform_download": (C.c_int, [_vp, _vp]),
     "af_uniform_step": (C.c_int, [_vp, C.c_double, C.POINTER(StepDiag)]),

@@ -204,6 +204,13 @@ af_status af_uniform_local_extent(const af_uniform* u, int* z0, int* nz) {
   return AF_OK;
 }
 
+af_status af_slab_extent(int dim, int level, int n_ranks, int rank, int* z0, int* nz) {
+  if (!z0 || !nz) return record(nullptr, AF_E_ARGUMENT, "null argument");
+  if (!af::slab_extent(dim, level, n_ranks, rank, z0, nz))
+    return record(nullptr, AF_E_CONFIG, "too many ranks for this mesh");
+  return AF_OK;
+}
+
 af_status af_uniform_upload(af_uniform* u, const double* aos) { AF_U_GUARD(u->impl->upload(aos)); }
 
 af_status af_uniform_download(af_uniform* u, double* aos) { AF_U_GUARD(u->impl->download(aos)); }

@@ -106,6 +106,23 @@ bool is_device_ptr(const void* p) {
 
 }  // namespace
 
+// Contiguous slabs of the slab axis (z in 3D, y in 2D); 2D slabs stay multiples
+// of the tile height. Pure host arithmetic: false when a rank would be empty.
+bool slab_extent(int dim, int level, int n_ranks, int rank, int* z0, int* nz) {
+  if (dim < 2 || dim > 3 || level < 0 || level > 30 || n_ranks < 1 || rank < 0 ||
+      rank >= n_ranks)
+    return false;
+  const int n = 1 << level;
+  const int quantum = dim == 2 ? kTY : 2;
+  const int units = n / quantum;
+  if (units < n_ranks) return false;
+  const int lo_u = (int)((long)units * rank / n_ranks);
+  const int hi_u = (int)((long)units * (rank + 1) / n_ranks);
+  *z0 = lo_u * quantum;
+  *nz = (hi_u - lo_u) * quantum;
+  return true;
+}
+
 Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   if (c.dim != 2 && c.dim != 3) throw Error(AF_E_CONFIG, "dim must be 2 or 3");
   if (c.level < 3 || c.level > 15)
@@ -125,14 +142,8 @@ Uniform::Uniform(const af_config& c, Comm* comm) : cfg_(c), comm_(comm) {
   g_.n = n;
   g_.nranks = comm ? comm->n : 1;
   const int rank = comm ? comm->rank : 0;
-  // Contiguous slabs; 2D slabs stay multiples of the tile height.
-  const int quantum = c.dim == 2 ? kTY : 2;
-  const int units = n / quantum;
-  if (units < g_.nranks) throw Error(AF_E_CONFIG, "too many ranks for this mesh");
-  const int lo_u = (int)((long)units * rank / g_.nranks);
-  const int hi_u = (int)((long)units * (rank + 1) / g_.nranks);
-  g_.zlo = lo_u * quantum;
-  g_.nzl = (hi_u - lo_u) * quantum;
+  if (!slab_extent(c.dim, c.level, g_.nranks, rank, &g_.zlo, &g_.nzl))
+    throw Error(AF_E_CONFIG, "too many ranks for this mesh");
   for (int f = 0; f < 6; ++f) g_.bc[f] = c.bc[f];
   g_.ncomp = c.dim == 3 ? 5 : 4;
   g_.plane = c.dim == 3 ? (long)n * n : (long)n;

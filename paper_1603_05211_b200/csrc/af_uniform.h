@@ -19,6 +19,9 @@ void fv3d_tol_setup();
 void fv3d_tol_launch(int scheme, dim3 grid, cudaStream_t stream, const StageArgs& a,
                      const UGrid& g, const CUtensorMap& tm, const CUtensorMap& tb);
 
+// the slab [z0, z0+nz) of rank `rank` among n_ranks (af_uniform.cu); host arithmetic only
+bool slab_extent(int dim, int level, int n_ranks, int rank, int* z0, int* nz);
+
 class Uniform {
  public:
   Uniform(const af_config& cfg, Comm* comm);

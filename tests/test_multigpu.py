@@ -45,25 +45,27 @@ def test_group_equals_single(gpu_lib, dim, level, ranks, bc, cfl, lim, integ):
     assert r1.max_cfl == r2.max_cfl
 
 
-def _partition(n, units, P, quantum):
-    # restatement of Uniform::Uniform's slab split (af_uniform.cu)
-    out = []
-    for r in range(P):
-        lo, hi = units * r // P, units * (r + 1) // P
-        out.append((lo * quantum, (hi - lo) * quantum))
-    return out
-
-
-@pytest.mark.parametrize("dim,level,P", [(2, 8, 8), (2, 6, 3), (3, 9, 8), (3, 5, 5)])
-def test_slab_partition_tiles_the_mesh(dim, level, P):
+@pytest.mark.parametrize("dim,level,P", [(2, 8, 8), (2, 6, 3), (3, 9, 8), (3, 5, 5), (3, 9, 7),
+                                         (2, 13, 8)])
+def test_slab_partition_tiles_the_mesh(gpu_lib_cpu, dim, level, P):
+    """The library's own slab split (af_slab_extent = what Uniform::Uniform
+    uses, af_uniform.cu): contiguous, non-empty slabs of whole tile rows
+    that tile the slab axis; a rank count that would leave a rank empty is a
+    ConfigError."""
+    import ctypes as C
+    lib = gpu_lib_cpu
     n = 1 << level
     quantum = 8 if dim == 2 else 2
-    parts = _partition(n, n // quantum, P, quantum)
     z = 0
-    for z0, nz in parts:
-        assert z0 == z and nz >= quantum and nz % quantum == 0
-        z += nz
+    for r in range(P):
+        z0, nz = C.c_int(), C.c_int()
+        assert lib.af_slab_extent(dim, level, P, r, C.byref(z0), C.byref(nz)) == 0
+        assert z0.value == z and nz.value >= quantum and nz.value % quantum == 0
+        z += nz.value
     assert z == n
+    z0, nz = C.c_int(), C.c_int()
+    assert lib.af_slab_extent(dim, level, n // quantum + 1, 0, C.byref(z0), C.byref(nz)) != 0
+    assert lib.af_slab_extent(dim, level, P, P, C.byref(z0), C.byref(nz)) != 0
 
 
 def _gloo_worker(rank, world, port, q):
