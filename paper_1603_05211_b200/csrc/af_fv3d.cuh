@@ -191,8 +191,11 @@ __global__ void __launch_bounds__(NW * 32, 2)
   auto convert = [&](int gz, int dslot) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
-    bool fz;
-    const int zl = slab_map(gz, g, 2, fz);
+    // planes inside the domain (all but the chunk ends at the boundary) skip
+    // the boundary mapping: a CTA-uniform branch
+    bool fz = false;
+    int zl = gz - g.zlo + 2;
+    if ((unsigned)gz >= (unsigned)n) zl = slab_map(gz, g, 2, fz);
     double* dst = ring + dslot;
     const bool own_plane = gz >= zc0 && gz < zc1;
 #pragma unroll
