@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(NW * 32, 2)
   }
   const double* ev = a.eval;
   const long cs = g.cs, zs = g.zs;
+  bool reflective = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) reflective |= g.bc[f] == AF_BC_REFLECTIVE;
   double wave = 0.0, ssum = 0.0;
   int bad = 0, nfb = 0;
 
@@ -234,13 +237,15 @@ __global__ void __launch_bounds__(NW * 32, 2)
           if (!cell_ok(q, w)) bad = 1;
           double s, m;
           wave_speeds_tol(w, ir, gamma, s, m);
-          wave = fmax(wave, m);
+          wave = wave > m ? wave : m;
         }
       }
-      const unsigned fl = hflip >> (2 * t);
-      if (fl & 1u) w.v[0] = -w.v[0];
-      if (fl & 2u) w.v[1] = -w.v[1];
-      if (fz) w.v[2] = -w.v[2];
+      if (reflective) {  // CTA-uniform: no face of the mesh reflects otherwise
+        const unsigned fl = hflip >> (2 * t);
+        if (fl & 1u) w.v[0] = -w.v[0];
+        if (fl & 2u) w.v[1] = -w.v[1];
+        if (fz) w.v[2] = -w.v[2];
+      }
       dst[idx] = w.rho;
       dst[K::HP + idx] = w.v[0];
       dst[2 * K::HP + idx] = w.v[1];
