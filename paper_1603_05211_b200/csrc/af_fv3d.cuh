@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
     zd[m] = w2 - w1;
     cell_face_states<S, MODE>(w1, w1 - w0, zd[m], unused, zl[m]);
   }
+  __syncthreads();  // plane zc0-2's slot is read above and refilled with plane zc0+1 next
   const int ixl = ty * TX + tx, ixh = tx + 1 < TX ? ixl + 1 : TX * TY + ty,
             iyl = K::YS + ty * TX + tx;
   double zlo[5];
@@ -460,15 +461,33 @@ __global__ void __launch_bounds__(NW * 32, 2)
   // cell's offset in the slab arrays
   int sk = slot(zc0 - 1), sk1 = slot(zc0), sk2 = slot(zc0 + 1);
   long own = (long)(zc0 - 1 - g.zlo + 2) * zs + (long)(y0 + ty) * n + (x0 + tx);
-  for (int k = zc0 - 1; k < zc1; ++k, own += zs) {
-    const bool first = k < zc0;
+  // Peeled iteration k = zc0-1: only the chunk's first z face, kept as the
+  // first plane's lower face.
+  {
+    convert(zc0 + 1, sk2);
+    __syncthreads();
+    if (zc0 + 2 < zc1 + 2) issue(zc0 + 2);
+    if (zc0 < zc1) issue_base(zc0);
+    const Cons<D> Fz = zface(zc0 - 1, true, sk1, sk2);
+    const int t = sk;
+    sk = sk1;
+    sk1 = sk2;
+    sk2 = t;
+    zlo[0] = Fz.rho;
+    zlo[1] = Fz.m[0];
+    zlo[2] = Fz.m[1];
+    zlo[3] = Fz.m[2];
+    zlo[4] = Fz.E;
+    own += zs;
+  }
+  for (int k = zc0; k < zc1; ++k, own += zs) {
     convert(k + 2, sk2);
     __syncthreads();  // ring slot k+2 complete, staging free, flux free
     if (k + 3 < zc1 + 2) issue(k + 3);
     // its buffer was last read by the update of plane k-1 (before the barrier)
     if (k + 1 < zc1) issue_base(k + 1);
-    if (!first) faces(k, sk);
-    const Cons<D> Fz = zface(k, first, sk1, sk2);
+    faces(k, sk);
+    const Cons<D> Fz = zface(k, false, sk1, sk2);
     {
       const int t = sk;
       sk = sk1;
@@ -476,11 +495,6 @@ __global__ void __launch_bounds__(NW * 32, 2)
       sk2 = t;
     }
     const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
-    if (first) {
-#pragma unroll
-      for (int m = 0; m < 5; ++m) zlo[m] = zh[m];
-      continue;
-    }
     __syncthreads();  // x/y fluxes of plane k complete
     mbar_wait(&bbar[k & 1], (bphase >> (k & 1)) & 1u);
     bphase ^= 1u << (k & 1);
