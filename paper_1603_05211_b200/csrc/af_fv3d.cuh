@@ -93,6 +93,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// the same with the barrier's shared-window address already in a register (the
+// conversion reads SR_CgaCtaId, which costs a long-latency S2R per call)
+__device__ __forceinline__ void mbar_wait_a(unsigned bar_addr, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITA_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITA_%=;\n"
+      "}\n" ::"r"(bar_addr),
+      "r"(parity)
+      : "memory");
+}
 // 4D tiled TMA load (x, y, component, plane) -> shared, completion on `bar`
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, int c3, unsigned long long* bar) {
@@ -121,6 +134,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tid % TX, ty = tid / TX;
+  const unsigned bar_a = smem_u32(&bar), bbar_a = smem_u32(&bbar[0]);
   const int n = g.n;
   const int tiles_x = n / TX;
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
@@ -192,7 +206,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
   };
   unsigned bphase = 0;  // bit j: parity of buffer j's next completion
   auto convert = [&](int gz, int dslot) {
-    mbar_wait(&bar, phase);
+    mbar_wait_a(bar_a, phase);
     phase ^= 1u;
     // planes inside the domain (all but the chunk ends at the boundary) skip
     // the boundary mapping: a CTA-uniform branch
@@ -496,7 +510,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
     }
     const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
     __syncthreads();  // x/y fluxes of plane k complete
-    mbar_wait(&bbar[k & 1], (bphase >> (k & 1)) & 1u);
+    mbar_wait_a(bbar_a + 8u * (k & 1), (bphase >> (k & 1)) & 1u);
     bphase ^= 1u << (k & 1);
     if (owner) {
       double b[5];
