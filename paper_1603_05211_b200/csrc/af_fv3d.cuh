@@ -334,19 +334,25 @@ __global__ void __launch_bounds__(NW * 32, 2)
     constexpr int st = AX == 0 ? 1 : K::HX;
     const int fx = fl.fx, fy = fl.fy;
     const int o = sk + fl.o;
-    Prim<D> l, r;
     bool fb;
-    if constexpr (MODE == 0)
-      fb = muscl_recon<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
-                             prim_at(o + 3 * st), l, r);
-    else
-      fb = muscl_recon_tol<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
-                                 prim_at(o + 3 * st), l, r);
     Cons<D> F;
-    if constexpr (MODE == 0)
-      F = recon_flux_fast_warp<D, AX, S>(l, r, gamma, gm1, rgm1);
-    else
-      F = recon_flux_tol<D, S>(l, r, AX, gamma, gm1, rgm1, rgm1);
+    if constexpr (MODE == 1 && S == 1) {
+      // minmod + AUSM+ in tolerance mode: transverse velocities of the
+      // upwind side only
+      F = face_flux_lazy_tol<AX>(ring + o, st, K::HP, gamma, rgm1, fb);
+    } else {
+      Prim<D> l, r;
+      if constexpr (MODE == 0)
+        fb = muscl_recon<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
+                               prim_at(o + 3 * st), l, r);
+      else
+        fb = muscl_recon_tol<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
+                                   prim_at(o + 3 * st), l, r);
+      if constexpr (MODE == 0)
+        F = recon_flux_fast_warp<D, AX, S>(l, r, gamma, gm1, rgm1);
+      else
+        F = recon_flux_tol<D, S>(l, r, AX, gamma, gm1, rgm1, rgm1);
+    }
     if (__any_sync(0xffffffffu, fb)) {  // rare: first-order fallback (scheme.cpp:160-162)
       if (fb) {
         // the inner cells' conserved states from global memory; their
