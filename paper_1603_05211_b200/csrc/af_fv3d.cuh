@@ -340,6 +340,39 @@ __global__ void __launch_bounds__(NW * 32, 2)
       // minmod + AUSM+ in tolerance mode: transverse velocities of the
       // upwind side only
       F = face_flux_lazy_tol<AX>(ring + o, st, K::HP, gamma, rgm1, fb);
+    } else if constexpr (MODE == 0 && (S >> 1) == 0) {
+      // AUSM+ in exact mode: rho, v_AX and p on both sides (muscl_recon's
+      // operations), the transverse velocities on the upwind side only
+      constexpr int LIM = S & 1;
+      Prim<D> l, r;
+      auto both = [&](int blk, double& lv, double& rv) {
+        const double* q = ring + o + blk * K::HP;
+        const double c0 = q[0], c1 = q[st], c2 = q[2 * st], c3 = q[3 * st];
+        lv = c1 + 0.5 * limiter<LIM>(c1 - c0, c2 - c1);
+        rv = c2 - 0.5 * limiter<LIM>(c2 - c1, c3 - c2);
+      };
+      both(0, l.rho, r.rho);
+      both(4, l.p, r.p);
+      both(1 + AX, l.v[AX], r.v[AX]);
+      fb = !physical(l) || !physical(r);
+      bool ok = true;
+      F = ausm_plus_lazy<D, AX, FastOps>(
+          l, r, gamma, gm1, rgm1,
+          [&](bool up_l, int a) {
+            const double* q = ring + o + (1 + a) * K::HP + (up_l ? 0 : st);
+            const double c0 = q[0], c1 = q[st], c2 = q[2 * st];
+            const double h = 0.5 * limiter<LIM>(c1 - c0, c2 - c1);
+            return up_l ? c1 + h : c1 - h;
+          },
+          ok);
+      if (!__all_sync(0xffffffffu, ok)) {  // rare: an operand left the fast path's range
+        if (!ok) {
+          Prim<D> lf, rf;
+          muscl_recon<D, S>(prim_at(o), prim_at(o + st), prim_at(o + 2 * st),
+                            prim_at(o + 3 * st), lf, rf);
+          F = recon_flux<D, S>(lf, rf, AX, gamma, gm1, rgm1);
+        }
+      }
     } else {
       Prim<D> l, r;
       if constexpr (MODE == 0)
