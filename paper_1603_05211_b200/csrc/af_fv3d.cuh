@@ -106,6 +106,17 @@ __device__ __forceinline__ void mbar_wait_a(unsigned bar_addr, unsigned parity) 
       "r"(parity)
       : "memory");
 }
+// One arrival per warp on a CTA barrier initialised with the warp count: the
+// warp's earlier shared-memory accesses are ordered before it (__syncwarp,
+// then the elected lane's release), so a thread that has seen the phase
+// complete (mbar_wait_a) may read what every warp wrote and overwrite what
+// every warp read. Arrive and wait are separate instructions, so a warp keeps
+// working between them on whatever does not depend on the other warps.
+__device__ __forceinline__ void warp_arrive(unsigned bar_addr, int lane) {
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_addr) : "memory");
+}
 // 4D tiled TMA load (x, y, component, plane) -> shared, completion on `bar`
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, int c3, unsigned long long* bar) {
@@ -129,12 +140,13 @@ __global__ void __launch_bounds__(NW * 32, 2)
   double* flux = sm + K::FLUX;    // [5][NF]
   double* bown = sm + K::OWN;     // [2][5][NCELL] base values of the owned cells (TMA)
   double* red = sm + K::RED;      // [NW]
-  __shared__ unsigned long long bar, bbar[2];
+  __shared__ unsigned long long bar, bbar[2], xb[3];
   __shared__ int s_fb, s_bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tid % TX, ty = tid / TX;
   const unsigned bar_a = smem_u32(&bar), bbar_a = smem_u32(&bbar[0]);
+  const unsigned x1_a = smem_u32(&xb[0]), x2_a = smem_u32(&xb[1]), y_a = smem_u32(&xb[2]);
   const int n = g.n;
   const int tiles_x = n / TX;
   const int x0 = (blockIdx.x % tiles_x) * TX, y0 = (blockIdx.x / tiles_x) * TY;
@@ -150,6 +162,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
     mbar_init(&bar, 1);
     mbar_init(&bbar[0], 1);
     mbar_init(&bbar[1], 1);
+    for (int i = 0; i < 3; ++i) mbar_init(&xb[i], NW);
     if (a.stage == 1 && blockIdx.x == 0 && blockIdx.y == 0) a.r.dt[a.step] = stage_dt_of(a);
   }
   const double* ev = a.eval;
@@ -532,14 +545,30 @@ __global__ void __launch_bounds__(NW * 32, 2)
     zlo[3] = Fz.m[2];
     zlo[4] = Fz.E;
     own += zs;
+    warp_arrive(x1_a, lane);
   }
+  // Per plane, three split barriers (arrive ... wait, one arrival per warp)
+  // instead of two __syncthreads, so the uneven conversion passes and the
+  // warps' face units overlap:
+  //   X1: update(k-1) done    -> flux and base buffers free   (waited before the faces)
+  //   X2: convert(k+2) done   -> ring slot k+2 complete, staging free
+  //                                                (waited before the z face; warp 0
+  //                                                 before it issues the next TMA)
+  //   Y:  x/y faces of k done -> fluxes complete              (waited before the update)
   for (int k = zc0; k < zc1; ++k, own += zs) {
+    const unsigned par = (unsigned)(k - zc0) & 1u;
     convert(k + 2, sk2);
-    __syncthreads();  // ring slot k+2 complete, staging free, flux free
-    if (k + 3 < zc1 + 2) issue(k + 3);
-    // its buffer was last read by the update of plane k-1 (before the barrier)
-    if (k + 1 < zc1) issue_base(k + 1);
+    warp_arrive(x2_a, lane);
+    mbar_wait_a(x1_a, par);
+    if (warp == 0) {
+      mbar_wait_a(x2_a, par);
+      if (k + 3 < zc1 + 2) issue(k + 3);
+      // its buffer was last read by the update of plane k-1
+      if (k + 1 < zc1) issue_base(k + 1);
+    }
     faces(k, sk);
+    warp_arrive(y_a, lane);
+    if (warp != 0) mbar_wait_a(x2_a, par);
     const Cons<D> Fz = zface(k, false, sk1, sk2);
     {
       const int t = sk;
@@ -548,7 +577,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
       sk2 = t;
     }
     const double zh[5] = {Fz.rho, Fz.m[0], Fz.m[1], Fz.m[2], Fz.E};
-    __syncthreads();  // x/y fluxes of plane k complete
+    mbar_wait_a(y_a, par);  // x/y fluxes of plane k complete
     mbar_wait_a(bbar_a + 8u * (k & 1), (bphase >> (k & 1)) & 1u);
     bphase ^= 1u << (k & 1);
     if (owner) {
@@ -595,6 +624,7 @@ __global__ void __launch_bounds__(NW * 32, 2)
         ssum = fmax(ssum, s);
       }
     }
+    warp_arrive(x1_a, lane);  // this warp's reads of the fluxes and base values are done
   }
 
   // Stage diagnostics: positivity, StepDiag wave max, fallbacks.
