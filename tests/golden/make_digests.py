@@ -35,8 +35,9 @@ DIGESTS = {
     # cfg1 at its own size: 2D uniform 256^2, 200 steps
     "cfg1": dict(kind=0, seed=1, level=8, steps=200, cfl=0.5, coarse=6),
     # cfg2 at its own size: 2D MR L=10, level thresholds, min leaf 3, 500 cycles.
-    # Not committed: the reference did not finish it in 90 CPU-minutes here (nor
-    # a 50-cycle prefix in 20: its from_uniform + first coarsen of the full
+    # Not committed: the reference did not finish it in 175 CPU-minutes here (a
+    # second attempt, after one of 90; nor a 50-cycle prefix in 20: its
+    # from_uniform + first coarsen of the full
     # 1024^2 tree dominates, value_at recursing through absent levels); cfg2's
     # rules are pinned at L=7 (tests/golden/mr_quad_L7_epsl_min3.npz, the
     # test_mr_gpu cases) and its full-size properties in test_fullsize_gpu.py
