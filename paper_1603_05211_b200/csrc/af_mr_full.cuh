@@ -239,33 +239,68 @@ __global__ void __launch_bounds__(MRFull2::NT, 2)
       // (fx, fy): the face's high-side cell in tile coordinates
       const int fx = AX == 0 ? (j < TX * TY ? j % TX : TX) : j % TX;
       const int fy = AX == 0 ? (j < TX * TY ? j / TX : j - TX * TY) : j / TX;
-      Prim<D> wm1, w0, wp1, wp2;
-      if constexpr (AX == 0) {
-        wm1 = P(fx, fy + 2);
-        w0 = P(fx + 1, fy + 2);
-        wp1 = P(fx + 2, fy + 2);
-        wp2 = P(fx + 3, fy + 2);
-      } else {
-        wm1 = P(fx + 2, fy);
-        w0 = P(fx + 2, fy + 1);
-        wp1 = P(fx + 2, fy + 2);
-        wp2 = P(fx + 2, fy + 3);
-      }
-      Prim<D> lft, rgt;
+      // the face's first stencil cell in the primitive box and the stencil stride
+      constexpr int st = AX == 0 ? 1 : K::HX;
+      const int o = AX == 0 ? (fy + 2) * K::HX + fx : fy * K::HX + fx + 2;
+      auto Pc = [&](int c) {  // stencil cell c = 0..3
+        const int idx = o + c * st;
+        Prim<D> w;
+        w.rho = pr[idx];
+        w.v[0] = pr[K::HP + idx];
+        w.v[1] = pr[2 * K::HP + idx];
+        w.p = pr[3 * K::HP + idx];
+        return w;
+      };
       bool fb;
       Cons<D> F;
-      if constexpr (MODE == 0) {
-        fb = muscl_recon<D, S>(wm1, w0, wp1, wp2, lft, rgt);
-        F = recon_flux_fast_warp<D, AX, S>(lft, rgt, gamma, gm1, rgm1);
+      if constexpr (MODE == 0 && (S >> 1) == 0) {
+        // AUSM+ in exact mode: rho, v_AX and p on both sides (muscl_recon's
+        // operations), the transverse velocity on the upwind side only
+        // (ausm_plus_lazy, bit-identical to the eager form)
+        constexpr int LIM = S & 1;
+        Prim<D> lft, rgt;
+        auto both = [&](int blk, double& lv, double& rv) {
+          const double* q = pr + blk * K::HP + o;
+          const double c0 = q[0], c1 = q[st], c2 = q[2 * st], c3 = q[3 * st];
+          lv = c1 + 0.5 * limiter<LIM>(c1 - c0, c2 - c1);
+          rv = c2 - 0.5 * limiter<LIM>(c2 - c1, c3 - c2);
+        };
+        both(0, lft.rho, rgt.rho);
+        both(3, lft.p, rgt.p);
+        both(1 + AX, lft.v[AX], rgt.v[AX]);
+        fb = !physical(lft) || !physical(rgt);
+        bool ok = true;
+        F = ausm_plus_lazy<D, AX, FastOps>(
+            lft, rgt, gamma, gm1, rgm1,
+            [&](bool up_l, int a) {
+              const double* q = pr + (1 + a) * K::HP + o + (up_l ? 0 : st);
+              const double c0 = q[0], c1 = q[st], c2 = q[2 * st];
+              const double h = 0.5 * limiter<LIM>(c1 - c0, c2 - c1);
+              return up_l ? c1 + h : c1 - h;
+            },
+            ok);
+        if (!__all_sync(0xffffffffu, ok)) {  // rare: an operand left the fast path's range
+          if (!ok) {
+            Prim<D> lf, rf;
+            muscl_recon<D, S>(Pc(0), Pc(1), Pc(2), Pc(3), lf, rf);
+            F = recon_flux<D, S>(lf, rf, AX, gamma, gm1, rgm1);
+          }
+        }
       } else {
-        fb = muscl_recon_tol<D, S>(wm1, w0, wp1, wp2, lft, rgt);
-        F = recon_flux_tol<D, S>(lft, rgt, AX, gamma, gm1, rgm1, rgm1);
+        Prim<D> lft, rgt;
+        if constexpr (MODE == 0) {
+          fb = muscl_recon<D, S>(Pc(0), Pc(1), Pc(2), Pc(3), lft, rgt);
+          F = recon_flux_fast_warp<D, AX, S>(lft, rgt, gamma, gm1, rgm1);
+        } else {
+          fb = muscl_recon_tol<D, S>(Pc(0), Pc(1), Pc(2), Pc(3), lft, rgt);
+          F = recon_flux_tol<D, S>(lft, rgt, AX, gamma, gm1, rgm1, rgm1);
+        }
       }
       if (__any_sync(0xffffffffu, fb)) {
         if (fb) {
           const int gx = cx0 + fx, gy = cy0 + fy;
-          F = num_flux<D, AX, S>(cons_at(gx - (AX == 0), gy - (AX == 1)), w0, cons_at(gx, gy), wp1,
-                                 gamma);
+          F = num_flux<D, AX, S>(cons_at(gx - (AX == 0), gy - (AX == 1)), Pc(1), cons_at(gx, gy),
+                                 Pc(2), gamma);
         }
       }
       if (real) {
